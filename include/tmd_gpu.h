@@ -1,0 +1,212 @@
+/*
+ * tmd_gpu.h — C ABI of the B200 LJ short-range engine (libtmd_gpu.so).
+ *
+ * Drop-in boundary for the reference `taskmd` engine's hot path
+ * (/root/reference/proj/include/taskmd/). There is no plugin/FFI layer in the
+ * reference: its path sits behind inline C++ APIs, so each entry point below
+ * names the reference interface it replaces. A header-only C++ wrapper with
+ * the taskmd::Engine surface sits on top (include/taskmd_gpu/engine.hpp), and
+ * the Python mirror binds the same symbols with ctypes
+ * (paper_2109_10876_b200/engine.py).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; host arrays are copied, never retained;
+ *  - every call returns a status (TMD_OK = 0) except the getters noted;
+ *  - statuses map 1:1 onto the reference's exception types
+ *    (errors.hpp:19-43) and, through them, onto the CLI exit codes
+ *    (md_cli.cpp:333-352);
+ *  - a context owns one GPU's device memory and one CUDA stream; it is NOT
+ *    thread-safe (one host thread drives it, like taskmd::Engine,
+ *    task_pool.hpp:15-24);
+ *  - there is no CPU fallback: without a usable sm_100 device, create fails
+ *    with TMD_ERR_CUDA.
+ */
+#ifndef TMD_GPU_H_
+#define TMD_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMD_GPU_ABI_VERSION 1
+
+/* Status codes. */
+#define TMD_OK 0
+#define TMD_ERR_CONFIG 1  /* taskmd::ConfigError  */
+#define TMD_ERR_PHYSICS 2 /* taskmd::PhysicsError */
+#define TMD_ERR_VERIFY 3  /* taskmd::VerifyError  */
+#define TMD_ERR_STATE 4   /* taskmd::StateError   */
+#define TMD_ERR_CUDA 5    /* device / driver failure (no reference analog) */
+
+/* Timer sections, in the order of taskmd::Section (timers.hpp:11-17). */
+#define TMD_SECTION_FORCES 0
+#define TMD_SECTION_COMM 1
+#define TMD_SECTION_INTEGRATE 2
+#define TMD_SECTION_NEIGH 3
+#define TMD_SECTION_RESORT 4
+
+typedef struct tmd_gpu_ctx tmd_gpu_ctx;
+
+/* taskmd::FlatConfig (flat_config.hpp:18-40) as plain arrays. pos/vel are
+ * xyz-interleaved [3*n]; type and mass may be NULL (0 and 1.0). vel may be
+ * NULL (zero). Topology is not part of the LJ path (FENE is row f1). */
+typedef struct tmd_system {
+  double box[3];
+  int64_t n;
+  const int64_t* id;
+  const int32_t* type;
+  const double* mass;
+  const double* pos;
+  const double* vel;
+} tmd_system;
+
+/* taskmd::LjParams (potentials.hpp:21-26). */
+typedef struct tmd_lj_params {
+  double epsilon;
+  double sigma;
+  double r_cut;
+  int energy_shifted;
+} tmd_lj_params;
+
+/* taskmd::FeneParams (potentials.hpp:79-82). Reserved: a non-NULL pointer is
+ * rejected with TMD_ERR_CONFIG until the bonded path lands. */
+typedef struct tmd_fene_params {
+  double k;
+  double r_max;
+} tmd_fene_params;
+
+/* taskmd::EngineConfig (engine.hpp:19-26) minus the CPU-only knobs
+ * (n_sub / worker_threads have no GPU meaning), plus r_skin (the
+ * build_domain argument, domain.hpp:134) and device selection. */
+typedef struct tmd_engine_params {
+  double dt;
+  double r_skin;
+  int device;        /* CUDA ordinal; -1 = current device */
+  int section_timers; /* 1: fill the five SectionTimers with CUDA-event
+                         times per phase; 0: only `elapsed` */
+  int nbr_capacity;  /* 0 = auto (sized from the first build); else fixed
+                        entries per particle (rounded up to a multiple of 8) */
+  int reserved[5];
+} tmd_engine_params;
+
+/* taskmd::StepObservables (engine.hpp:43-48) plus the virial
+ * W = sum over in-cut pairs of ff * r^2 (absent from the reference). */
+typedef struct tmd_observables {
+  int64_t step;
+  double kinetic;
+  double potential;
+  double virial;
+  double temperature;
+} tmd_observables;
+
+/* Neighbour-list statistics of the last build (roofline accounting). */
+typedef struct tmd_list_stats {
+  int64_t n;          /* owned particles */
+  int64_t entries;    /* unpadded full-list entries (E) */
+  int64_t in_cut;     /* entries with r < r_cut at the last force call (2P) */
+  int32_t max_count;  /* largest per-particle entry count */
+  int32_t capacity;   /* allocated entries per particle */
+  int32_t dims[3];    /* cell grid */
+  double cell_len[3];
+} tmd_list_stats;
+
+/* Replaces build_domain(flat, inter, r_skin, n_sub) (domain.hpp:134-189) +
+ * Engine::Engine(Domain, EngineConfig) (engine.hpp:68-77): validates like the
+ * reference (validate_flat / validate_lj / build_cell_grid), uploads, bins,
+ * builds the list and runs the initial untimed force evaluation
+ * (compute_forces_untimed, engine.hpp:244-278). */
+int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
+                   const tmd_fene_params* fene /* must be NULL */,
+                   const tmd_engine_params* params, tmd_gpu_ctx** out);
+
+/* Message of the last failed call on ctx (or of the last failed create when
+ * ctx is NULL). Getter: never fails. */
+const char* tmd_gpu_last_error(const tmd_gpu_ctx* ctx);
+
+/* One force evaluation at the current positions with the current list:
+ * compute_subnode_forces + reduce_potential (engine.hpp:191-207) ==
+ * compute_pair_forces (neighbor_list.hpp:150) over the whole system. */
+int tmd_gpu_compute_forces(tmd_gpu_ctx* ctx, double* pe, double* virial);
+
+/* Engine::step / Engine::run (engine.hpp:80-130). PhysicsError messages carry
+ * "(at step N)" like run_phase (engine.hpp:167-170). */
+int tmd_gpu_step(tmd_gpu_ctx* ctx, int64_t nsteps);
+
+/* Engine::observe (engine.hpp:132-140) + virial. */
+int tmd_gpu_observe(tmd_gpu_ctx* ctx, tmd_observables* out);
+
+/* flatten_domain (domain.hpp:193-207): arrays of n entries sorted by id,
+ * positions wrapped into the box; forces are the last evaluation's. Any
+ * output pointer may be NULL. */
+int tmd_gpu_download(tmd_gpu_ctx* ctx, int64_t* id, double* pos, double* vel,
+                     double* force);
+
+/* Overwrite velocities by id (ids sorted or not; every owned id exactly once).
+ * The analog of tests poking Domain stores (test_engine.cpp:174-184). */
+int tmd_gpu_set_velocities(tmd_gpu_ctx* ctx, const int64_t* id,
+                           const double* vel);
+
+/* Parity tap: CellGrid::cell_of of every particle at the last resort
+ * (distribute_records, domain.hpp:56-65), sorted by id. */
+int tmd_gpu_cell_of(tmd_gpu_ctx* ctx, int64_t* id, int32_t* cell);
+
+/* Parity tap: every listed pair as (min id, max id), sorted — the same
+ * multiset as the reference's half lists (test_neighbor.cpp:49-65). Writes at
+ * most cap pairs to pairs[2*cap]; *n receives the total. */
+int tmd_gpu_pairs(tmd_gpu_ctx* ctx, int64_t* pairs, size_t cap, size_t* n);
+
+/* Engine::timers (engine.hpp:145): seconds per section + elapsed. */
+int tmd_gpu_timers(tmd_gpu_ctx* ctx, double sec[5], double* elapsed);
+
+/* Getters (never fail on a valid ctx). */
+uint64_t tmd_gpu_rebuild_count(const tmd_gpu_ctx* ctx); /* engine.hpp:148 */
+int64_t tmd_gpu_step_count(const tmd_gpu_ctx* ctx);     /* engine.hpp:146 */
+int64_t tmd_gpu_size(const tmd_gpu_ctx* ctx);
+
+int tmd_gpu_list_stats(tmd_gpu_ctx* ctx, tmd_list_stats* out);
+
+/* Benchmark hook: launches the force kernel `reps` times back to back on the
+ * context's stream between two CUDA events recorded on that stream and
+ * returns the mean milliseconds per launch. Results are left in place. */
+int tmd_gpu_time_force_kernel(tmd_gpu_ctx* ctx, int reps, double* ms_per_launch);
+
+/* Raw stream handle (cudaStream_t) of the context, for callers that want to
+ * order their own work after the engine's. */
+void* tmd_gpu_stream(tmd_gpu_ctx* ctx);
+
+void tmd_gpu_destroy(tmd_gpu_ctx* ctx);
+
+/* ---- host-side setup helpers (no GPU needed) ----------------------------
+ * Synthetic inputs of the BASELINE.json shapes. FCC is absent from the
+ * reference (generators.hpp has only simple cubic), see SURVEY §8(d). */
+
+/* FCC lattice: cells^3 unit cells x 4 basis sites, cubic box
+ * L = cbrt(4 cells^3 / rho), a = L / cells, positions
+ * (i + b_k + offset) * a, ids in z, y, x, basis order. Arrays sized
+ * 4*cells^3. */
+int tmd_gen_fcc(int cells, double rho, double offset, int64_t* id, double* pos,
+                double box[3]);
+
+/* gen_detail::thermal_velocities + zero_net_momentum (generators.hpp:19-39):
+ * v = sqrt(T/m) * counter_normal3(seed, kVelocityInit, 0, id), then the
+ * mass-weighted net momentum is removed. mass may be NULL (1.0). */
+void tmd_thermal_velocities(int64_t n, const int64_t* id, const double* mass,
+                            double temperature, uint64_t seed, double* vel);
+
+/* counter_uniform3 / counter_normal3 (random.hpp:53-81), context ids as
+ * taskmd::RngContext (1 thermostat, 2 velocity init, 3 placement). */
+void tmd_counter_uniform3(uint64_t seed, uint64_t ctx, uint64_t step,
+                          uint64_t id, double out[3]);
+void tmd_counter_normal3(uint64_t seed, uint64_t ctx, uint64_t step,
+                         uint64_t id, double out[3]);
+
+int tmd_gpu_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TMD_GPU_H_ */

@@ -1,0 +1,177 @@
+// Device-side building blocks of the B200 LJ short-range path.
+//
+// Layout in HBM (one context = one GPU = one cell-sorted particle set):
+//   pos   double4[N]  x, y, z, (w unused)  — one 32-B sector per gathered j
+//   vel   double[3][N] SoA, force double[3][N] SoA, mass double[N], id int64[N]
+//   cell  int32[N]    global cell of each particle at the last resort
+//   start int32[ncells+1] cell ranges (counting sort output)
+//   nbr   uint32[cap][stride] full Verlet list, ELL-transposed: entry k of
+//         particle i lives at nbr[k*stride + i] so a warp reads 128 B per k
+//   nnbr  int32[N]    entries per particle (unpadded)
+//
+// A list entry packs the neighbour slot (low 25 bits) with the periodic image
+// that the reference engine would have used for the same pair (bits 25..31),
+// so that every squared distance below is rounded exactly like the reference's
+// (neighbor_list.hpp:82-83, 94-95, 161-164):
+//   bits 25-26 / 27-28 / 29-30: image shift on x / y / z (0 none, 1 +L, 2 -L)
+//                               of neighbour j as seen from particle i;
+//   bit  31: the reference evaluates this pair from j's side (j's cell is the
+//            half-stencil source, neighbor_list.hpp:35-44), i.e. it forms the
+//            image of i (x_i - s) rather than of j (x_j + s), and the
+//            difference is taken as (x_i - s) - x_j.
+// With no shift both forms are plain x_i - x_j; negation is exact, so the
+// squared distance is bit-identical to the reference in every case.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmd {
+
+constexpr int kIdxBits = 25;
+constexpr uint32_t kIdxMask = (1u << kIdxBits) - 1u;
+constexpr uint32_t kFlagIUpper = 1u << 31;
+constexpr int64_t kMaxSlots = (int64_t{1} << kIdxBits) - 1;
+
+// Status bits in Ctrl::status (mapped to taskmd exception types on the host).
+enum : int {
+  kStatOverlap = 1,      // r2 == 0 (neighbor_list.hpp:166-170) -> PhysicsError
+  kStatNonFinite = 2,    // non-finite v/f (engine.hpp:231-236) -> PhysicsError
+  kStatNonFinitePos = 4, // non-finite position at binning (domain.hpp:58-62)
+  kStatOverflow = 8,     // neighbour list capacity exceeded -> host re-runs
+};
+
+struct LjConst {
+  double sigma2, rc2, eps4, eps24, shift;  // lj_prepare (potentials.hpp:49-61)
+};
+
+struct Geom {
+  double L[3];
+  double cell_len[3];
+  int dims[3];
+  int ncells;
+  double rv2;        // (r_cut + r_skin)^2, rounded as build_sorted_list does
+  double rebuild_thr;  // 0.25 * r_skin * r_skin (needs_rebuild, nl.hpp:143)
+};
+
+// Device control block: rebuild decision, counters and the error record.
+struct Ctrl {
+  unsigned long long max_d2;  // bits of max |x - x_snap|^2 this step (>= 0)
+  int rebuild;                // decision for the current step
+  int force_rebuild;          // set by the host (setup / rollback)
+  long long step;             // device step counter (== host step count)
+  long long rebuilds;         // list rebuilds (Engine::rebuild_count)
+  int status;                 // OR of kStat* bits
+  int err_lock;
+  long long err_step;
+  long long err_id0, err_id1;
+  int max_count;              // largest per-particle entry count, last build
+  int cap;                    // current list capacity per particle
+  long long entries;          // total entries, last build
+};
+
+// ---------------------------------------------------------------------------
+// Exact (non-contracted) FP64 helpers. nvcc contracts a*b+c into DFMA by
+// default; the reference's g++ build (no -march) never does, so every
+// expression that decides a discrete outcome (wrap, cell, list membership,
+// cutoff test, rebuild test) is spelled with _rn intrinsics.
+
+__device__ __forceinline__ double exact_r2(double dx, double dy, double dz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                   __dmul_rn(dz, dz));
+}
+
+// wrap1 (box.hpp:47-51): r = p - L*floor(p/L); r >= L folds back.
+__device__ __forceinline__ double wrap1(double p, double L) {
+  double r = __dsub_rn(p, __dmul_rn(L, floor(__ddiv_rn(p, L))));
+  if (r >= L) r = __dsub_rn(r, L);
+  return r;
+}
+
+// CellGrid::cell_coords (cell_grid.hpp:36-46), one axis.
+__device__ __forceinline__ int cell_coord(double p, double len, int dims) {
+  int v = static_cast<int>(floor(__ddiv_rn(p, len)));
+  if (v < 0) v = 0;
+  if (v >= dims) v = dims - 1;
+  return v;
+}
+
+__device__ __forceinline__ double image_shift(uint32_t code2, double L) {
+  return code2 == 0u ? 0.0 : (code2 == 1u ? L : -L);
+}
+
+// Displacement d = x_i - x_j(image) exactly as the reference rounds it for the
+// pair encoded in `ent` (see the header comment).
+__device__ __forceinline__ void pair_delta(const double4& pi, const double4& pj,
+                                           uint32_t ent, const Geom& g,
+                                           double& dx, double& dy, double& dz) {
+  if (ent <= kIdxMask) {
+    dx = __dsub_rn(pi.x, pj.x);
+    dy = __dsub_rn(pi.y, pj.y);
+    dz = __dsub_rn(pi.z, pj.z);
+    return;
+  }
+  const double sx = image_shift((ent >> 25) & 3u, g.L[0]);
+  const double sy = image_shift((ent >> 27) & 3u, g.L[1]);
+  const double sz = image_shift((ent >> 29) & 3u, g.L[2]);
+  if (ent & kFlagIUpper) {
+    dx = __dsub_rn(__dsub_rn(pi.x, sx), pj.x);
+    dy = __dsub_rn(__dsub_rn(pi.y, sy), pj.y);
+    dz = __dsub_rn(__dsub_rn(pi.z, sz), pj.z);
+  } else {
+    dx = __dsub_rn(pi.x, __dadd_rn(pj.x, sx));
+    dy = __dsub_rn(pi.y, __dadd_rn(pj.y, sy));
+    dz = __dsub_rn(pi.z, __dadd_rn(pj.z, sz));
+  }
+}
+
+// 1/x from the MUFU.RCP64H seed plus two Newton steps (~1 ulp). Used only in
+// the force arithmetic (tolerance 1e-10 relative), never in a discrete test.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  return y;
+}
+
+// Read-only 32-B gather of one packed position (two LDG.128 on one sector).
+__device__ __forceinline__ double4 ldg_pos(const double4* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ bool finite3(double a, double b, double c) {
+  return isfinite(a) && isfinite(b) && isfinite(c);
+}
+
+// First error wins the detail record; every error ORs its status bit.
+__device__ __forceinline__ void record_error(Ctrl* ctrl, int bit, long long id0,
+                                             long long id1) {
+  atomicOr(&ctrl->status, bit);
+  if (atomicCAS(&ctrl->err_lock, 0, 1) == 0) {
+    ctrl->err_step = ctrl->step;
+    ctrl->err_id0 = id0;
+    ctrl->err_id1 = id1;
+  }
+}
+
+template <int kThreads>
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += smem[w];
+  }
+  return t;  // valid in thread 0
+}
+
+}  // namespace tmd

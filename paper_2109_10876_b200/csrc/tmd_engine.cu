@@ -1,0 +1,963 @@
+// libtmd_gpu.so — the B200 engine behind include/tmd_gpu.h.
+//
+// One context = one GPU = one cell-sorted, device-resident FP64 particle set.
+// A step enqueues (engine.hpp:80-126 phase order):
+//   Integrate  k_kick_drift (kick2 of step n-1 fused with kick1+drift of n)
+//   Neigh      k_decide (global max-displacement test, on device)
+//   Resort     k_wrap_bin, k_scan, k_scatter, k_sort_cells, k_permute,
+//              k_copy_back          (no-ops unless the device decided rebuild)
+//   Neigh      k_build_list         (no-op unless rebuild)
+//   Forces     k_lj_forces
+//   Integrate  k_kick2              (only at the end of a run() chunk)
+// Nothing in a chunk waits for the host. The host synchronises once per
+// chunk to read the status word; a neighbour-list overflow rolls the chunk
+// back to its checkpoint, grows the list and replays it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/tmd_gpu.h"
+#include "tmd_kernels.cuh"
+
+using namespace tmd;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaFail {
+  std::string what;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaFail{std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+
+struct StatusError {
+  int code;
+  std::string what;
+};
+
+inline int blocks_for(int64_t n, int t) {
+  return static_cast<int>((n + t - 1) / t);
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+std::string fmt_g(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%g", v);
+  return b;
+}
+
+// Host wrap1 (box.hpp:47-51); no FMA contraction on the x86-64 host path.
+double host_wrap1(double p, double L) {
+  double r = p - L * std::floor(p / L);
+  if (r >= L) r -= L;
+  return r;
+}
+
+}  // namespace
+
+struct tmd_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n = 0;
+  int stride = 0;
+  int cap = 0;
+  bool auto_cap = true;
+  int nblk = 0;
+  Geom g{};
+  LjConst lj{};
+  double dt = 0, half_dt = 0, r_skin = 0, r_cut = 0;
+  bool timers_on = true;
+
+  // particle arrays (cell-sorted) + alternates for the permutation
+  double4 *pos = nullptr, *pos2 = nullptr, *snap = nullptr;
+  double *vx = nullptr, *vy = nullptr, *vz = nullptr;
+  double *vx2 = nullptr, *vy2 = nullptr, *vz2 = nullptr;
+  double *fx = nullptr, *fy = nullptr, *fz = nullptr;
+  double *mass = nullptr, *mass2 = nullptr;
+  long long *id = nullptr, *id2 = nullptr;
+  int *cell = nullptr, *cell2 = nullptr, *rank = nullptr, *perm = nullptr;
+  int *count = nullptr, *start = nullptr;
+  uint32_t* nbr = nullptr;
+  int* nnbr = nullptr;
+  double *part_e = nullptr, *part_w = nullptr, *part_ke = nullptr;
+  double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
+  Ctrl* ctrl = nullptr;
+  Ctrl* h_ctrl = nullptr;      // pinned mirror
+  double* h_scalars = nullptr; // pinned
+
+  // chunk checkpoint (rollback on list overflow)
+  double4* ck_pos = nullptr;
+  double *ck_vx = nullptr, *ck_vy = nullptr, *ck_vz = nullptr, *ck_mass = nullptr;
+  long long* ck_id = nullptr;
+
+  // host mirrors
+  int64_t step = 0;
+  uint64_t rebuilds = 0;
+  bool ke_fresh = false;  // part_ke holds the current velocities' partials
+  double sec[5] = {0, 0, 0, 0, 0};
+  double elapsed = 0.0;
+  std::string err;
+
+  std::vector<cudaEvent_t> ev;  // pool for per-phase timing
+  size_t ev_used = 0;
+  struct Span {
+    int section;
+    size_t b, e;
+    int step_idx;  // chunk-relative step for Resort spans, else -1
+  };
+  std::vector<Span> ev_spans;
+  int* rebuild_log = nullptr;     // device: rebuild decision per chunk step
+  std::vector<int> h_rebuild_log;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+namespace {
+
+void free_all(tmd_gpu_ctx* c) {
+  void* ptrs[] = {c->pos,  c->pos2,  c->snap, c->vx,    c->vy,      c->vz,
+                  c->vx2,  c->vy2,   c->vz2,  c->fx,    c->fy,      c->fz,
+                  c->mass, c->mass2, c->id,   c->id2,   c->cell,    c->cell2,
+                  c->rank, c->perm,  c->count, c->start, c->nbr,    c->nnbr,
+                  c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
+                  c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
+                  c->rebuild_log};
+  for (void* p : ptrs) {
+    if (p) cudaFree(p);
+  }
+  if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+  if (c->h_scalars) cudaFreeHost(c->h_scalars);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+// --- per-phase timing ------------------------------------------------------
+cudaEvent_t next_event(tmd_gpu_ctx* c) {
+  if (c->ev_used == c->ev.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    c->ev.push_back(e);
+  }
+  return c->ev[c->ev_used++];
+}
+
+struct Phase {
+  tmd_gpu_ctx* c;
+  int section;
+  size_t b;
+  int step_idx;
+  Phase(tmd_gpu_ctx* ctx, int s, int step = -1)
+      : c(ctx), section(s), b(0), step_idx(step) {
+    if (!c->timers_on) return;
+    b = c->ev_used;
+    ck(cudaEventRecord(next_event(c), c->stream), "cudaEventRecord");
+  }
+  ~Phase() {
+    if (!c->timers_on) return;
+    const size_t e = c->ev_used;
+    if (cudaEventRecord(next_event(c), c->stream) == cudaSuccess) {
+      c->ev_spans.push_back({section, b, e, step_idx});
+    }
+  }
+};
+
+// Resort spans of steps that did not rebuild ran only the early-exit
+// kernels: that time is the rebuild check and is booked to Neigh, so Resort
+// stays zero without rebuilds (test_engine.cpp:306-321).
+void harvest_timers(tmd_gpu_ctx* c) {
+  for (const auto& s : c->ev_spans) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[s.b], c->ev[s.e]) != cudaSuccess) continue;
+    int sec = s.section;
+    if (sec == TMD_SECTION_RESORT && s.step_idx >= 0 &&
+        s.step_idx < static_cast<int>(c->h_rebuild_log.size()) &&
+        c->h_rebuild_log[s.step_idx] == 0) {
+      sec = TMD_SECTION_NEIGH;
+    }
+    c->sec[sec] += 1e-3 * ms;
+  }
+  c->ev_spans.clear();
+  c->ev_used = 0;
+}
+
+// --- kernel launch wrappers -------------------------------------------------
+void launch_decide(tmd_gpu_ctx* c, bool advance, int log_idx = -1) {
+  k_decide<<<1, 1, 0, c->stream>>>(c->ctrl, c->g.rebuild_thr, advance ? 1 : 0,
+                                   log_idx >= 0 ? c->rebuild_log : nullptr,
+                                   log_idx);
+}
+
+void launch_resort(tmd_gpu_ctx* c) {
+  const int n = static_cast<int>(c->n);
+  const int nb = c->nblk;
+  k_wrap_bin<<<nb, kBlock, 0, c->stream>>>(n, c->pos, c->id, c->cell, c->rank,
+                                           c->count, c->g, c->ctrl);
+  k_scan<<<1, kScanThreads, 0, c->stream>>>(c->g.ncells, c->count, c->start,
+                                            c->ctrl);
+  k_scatter<<<nb, kBlock, 0, c->stream>>>(n, c->cell, c->rank, c->start,
+                                          c->perm, c->ctrl);
+  k_sort_cells<<<blocks_for(c->g.ncells, kBlock), kBlock, 0, c->stream>>>(
+      c->g.ncells, c->start, c->perm, c->id, c->ctrl);
+  k_permute<<<nb, kBlock, 0, c->stream>>>(n, c->perm, c->pos, c->vx, c->vy,
+                                          c->vz, c->mass, c->id, c->cell,
+                                          c->pos2, c->vx2, c->vy2, c->vz2,
+                                          c->mass2, c->id2, c->cell2, c->ctrl);
+  k_copy_back<<<nb, kBlock, 0, c->stream>>>(n, c->pos2, c->vx2, c->vy2,
+                                            c->vz2, c->mass2, c->id2, c->cell2,
+                                            c->pos, c->vx, c->vy, c->vz,
+                                            c->mass, c->id, c->cell, c->ctrl);
+}
+
+void launch_build(tmd_gpu_ctx* c) {
+  k_build_prologue<<<1, 1, 0, c->stream>>>(c->ctrl);
+  k_build_list<<<c->nblk, kBlock, 0, c->stream>>>(
+      static_cast<int>(c->n), c->pos, c->cell, c->start, c->g, c->nbr, c->nnbr,
+      c->stride, c->cap, c->snap, c->ctrl);
+}
+
+void launch_forces(tmd_gpu_ctx* c) {
+  k_lj_forces<<<c->nblk, kBlock, 0, c->stream>>>(
+      static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
+      c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, c->ctrl);
+}
+
+void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
+  const int n = static_cast<int>(c->n);
+  if (fused) {
+    k_kick_drift<true><<<c->nblk, kBlock, 0, c->stream>>>(
+        n, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
+        c->snap, c->dt, c->half_dt, c->part_ke, c->ctrl);
+  } else {
+    k_kick_drift<false><<<c->nblk, kBlock, 0, c->stream>>>(
+        n, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
+        c->snap, c->dt, c->half_dt, c->part_ke, c->ctrl);
+  }
+}
+
+void launch_kick2(tmd_gpu_ctx* c) {
+  k_kick2<<<c->nblk, kBlock, 0, c->stream>>>(
+      static_cast<int>(c->n), c->vx, c->vy, c->vz, c->fx, c->fy, c->fz,
+      c->mass, c->id, c->half_dt, c->part_ke, c->ctrl);
+}
+
+void launch_reduce_pe(tmd_gpu_ctx* c) {
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, c->nblk, 0.5,
+                                             c->scalars + 0);
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, c->nblk, 0.5,
+                                             c->scalars + 1);
+}
+
+void launch_reduce_ke(tmd_gpu_ctx* c) {
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_ke, c->nblk, 1.0,
+                                             c->scalars + 2);
+}
+
+// --- status handling ---------------------------------------------------------
+void sync_ctrl(tmd_gpu_ctx* c) {
+  ck(cudaMemcpyAsync(c->h_ctrl, c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
+                     c->stream),
+     "cudaMemcpyAsync(ctrl)");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+// Physics errors (overlap / non-finite) -> StatusError with the reference's
+// message shapes. Overflow is handled by the caller.
+void raise_physics(tmd_gpu_ctx* c, bool with_step) {
+  const Ctrl& h = *c->h_ctrl;
+  std::string msg;
+  if (h.status & kStatOverlap) {
+    msg = "overlapping particles: ids " + std::to_string(h.err_id0) + " and " +
+          std::to_string(h.err_id1) + " coincide";
+  } else if (h.status & kStatNonFinite) {
+    msg = "non-finite velocity or force on particle id " +
+          std::to_string(h.err_id0);
+  } else if (h.status & kStatNonFinitePos) {
+    msg = "non-finite position for particle id " + std::to_string(h.err_id0);
+  } else {
+    return;
+  }
+  if (with_step) msg += " (at step " + std::to_string(h.err_step) + ")";
+  throw StatusError{TMD_ERR_PHYSICS, msg};
+}
+
+void reset_status(tmd_gpu_ctx* c) {
+  // clear status + error latch (host-side write of the two ints)
+  Ctrl z = *c->h_ctrl;
+  z.status = 0;
+  z.err_lock = 0;
+  ck(cudaMemcpyAsync(&c->ctrl->status, &z.status, 2 * sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream),
+     "cudaMemcpyAsync(status)");
+}
+
+void set_force_rebuild(tmd_gpu_ctx* c) {
+  const int one = 1;
+  ck(cudaMemcpyAsync(&c->ctrl->force_rebuild, &one, sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream),
+     "cudaMemcpyAsync(force_rebuild)");
+}
+
+void set_cap_in_ctrl(tmd_gpu_ctx* c) {
+  ck(cudaMemcpyAsync(&c->ctrl->cap, &c->cap, sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream),
+     "cudaMemcpyAsync(cap)");
+}
+
+int round8(int v) { return (v + 7) / 8 * 8; }
+
+void alloc_list(tmd_gpu_ctx* c, int cap) {
+  if (c->nbr) cudaFree(c->nbr);
+  c->nbr = nullptr;
+  c->cap = round8(std::max(cap, 8));
+  c->nbr = dalloc<uint32_t>(static_cast<size_t>(c->cap) * c->stride);
+  set_cap_in_ctrl(c);
+}
+
+// Resort + list build + forces at the current state, forced (setup / after a
+// rollback). Grows the list until it fits. Leaves the PE reduced.
+void setup_pass(tmd_gpu_ctx* c) {
+  for (;;) {
+    set_force_rebuild(c);
+    launch_decide(c, false);
+    launch_resort(c);
+    launch_build(c);
+    sync_ctrl(c);
+    raise_physics(c, false);
+    if (c->h_ctrl->status & kStatOverflow) {
+      const int need = c->h_ctrl->max_count;
+      reset_status(c);
+      alloc_list(c, need + need / 4 + 8);
+      continue;
+    }
+    break;
+  }
+  if (c->auto_cap) {
+    // headroom for the liquid to densify locally between builds
+    const int want = round8(c->h_ctrl->max_count + c->h_ctrl->max_count / 4 + 8);
+    if (want > c->cap) {
+      alloc_list(c, want);
+      set_force_rebuild(c);
+      launch_decide(c, false);
+      launch_build(c);
+    }
+  }
+  launch_forces(c);
+  launch_reduce_pe(c);
+  sync_ctrl(c);
+  raise_physics(c, false);
+}
+
+void checkpoint(tmd_gpu_ctx* c) {
+  const size_t n = static_cast<size_t>(c->n);
+  auto cp = [&](void* d, const void* s, size_t bytes) {
+    ck(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, c->stream),
+       "checkpoint copy");
+  };
+  cp(c->ck_pos, c->pos, n * sizeof(double4));
+  cp(c->ck_vx, c->vx, n * sizeof(double));
+  cp(c->ck_vy, c->vy, n * sizeof(double));
+  cp(c->ck_vz, c->vz, n * sizeof(double));
+  cp(c->ck_mass, c->mass, n * sizeof(double));
+  cp(c->ck_id, c->id, n * sizeof(long long));
+}
+
+void restore(tmd_gpu_ctx* c, const Ctrl& at_checkpoint) {
+  const size_t n = static_cast<size_t>(c->n);
+  auto cp = [&](void* d, const void* s, size_t bytes) {
+    ck(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, c->stream),
+       "restore copy");
+  };
+  cp(c->pos, c->ck_pos, n * sizeof(double4));
+  cp(c->vx, c->ck_vx, n * sizeof(double));
+  cp(c->vy, c->ck_vy, n * sizeof(double));
+  cp(c->vz, c->ck_vz, n * sizeof(double));
+  cp(c->mass, c->ck_mass, n * sizeof(double));
+  cp(c->id, c->ck_id, n * sizeof(long long));
+  Ctrl back = at_checkpoint;
+  back.status = 0;
+  back.err_lock = 0;
+  back.max_d2 = 0;
+  back.cap = c->cap;
+  ck(cudaMemcpyAsync(c->ctrl, &back, sizeof(Ctrl), cudaMemcpyHostToDevice,
+                     c->stream),
+     "restore ctrl");
+}
+
+constexpr int64_t kChunk = 256;
+
+// Runs `steps` steps as one device-resident chunk. Returns false when the
+// list overflowed (state is then garbage; the caller rolls back).
+bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
+  {
+    Phase p(c, TMD_SECTION_INTEGRATE);
+    launch_kick_drift(c, false);
+  }
+  for (int64_t s = 0; s < steps; ++s) {
+    {
+      Phase p(c, TMD_SECTION_NEIGH);
+      launch_decide(c, true, static_cast<int>(s));
+    }
+    {
+      Phase p(c, TMD_SECTION_RESORT, static_cast<int>(s));
+      launch_resort(c);
+    }
+    {
+      Phase p(c, TMD_SECTION_NEIGH);
+      launch_build(c);
+    }
+    {
+      Phase p(c, TMD_SECTION_FORCES);
+      launch_forces(c);
+    }
+    {
+      Phase p(c, TMD_SECTION_INTEGRATE);
+      if (s + 1 < steps) {
+        launch_kick_drift(c, true);
+      } else {
+        launch_kick2(c);
+      }
+    }
+  }
+  launch_reduce_pe(c);
+  if (c->timers_on) {
+    c->h_rebuild_log.resize(static_cast<size_t>(steps));
+    ck(cudaMemcpyAsync(c->h_rebuild_log.data(), c->rebuild_log,
+                       sizeof(int) * static_cast<size_t>(steps),
+                       cudaMemcpyDeviceToHost, c->stream),
+       "D2H rebuild log");
+  }
+  sync_ctrl(c);
+  harvest_timers(c);
+  return (c->h_ctrl->status & kStatOverflow) == 0;
+}
+
+void do_run(tmd_gpu_ctx* c, int64_t nsteps) {
+  int64_t done = 0;
+  while (done < nsteps) {
+    const int64_t todo = std::min(kChunk, nsteps - done);
+    checkpoint(c);
+    const Ctrl before = *c->h_ctrl;  // mirror is current after the last sync
+    ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    const bool ok = run_chunk(c, todo);
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c->t0, c->t1), "cudaEventElapsedTime");
+    c->elapsed += 1e-3 * ms;
+    if (!ok) {
+      // neighbour list overflow: roll back, grow, replay this chunk
+      const int need = c->h_ctrl->max_count;
+      restore(c, before);
+      alloc_list(c, need + need / 4 + 8);
+      setup_pass(c);
+      continue;
+    }
+    c->step = c->h_ctrl->step;
+    c->rebuilds = static_cast<uint64_t>(c->h_ctrl->rebuilds);
+    c->ke_fresh = true;
+    raise_physics(c, true);
+    done += todo;
+  }
+}
+
+template <class F>
+int guard(tmd_gpu_ctx* c, F&& fn) {
+  try {
+    fn();
+    return TMD_OK;
+  } catch (const StatusError& e) {
+    c->err = e.what;
+    return e.code;
+  } catch (const CudaFail& e) {
+    c->err = e.what;
+    return TMD_ERR_CUDA;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return TMD_ERR_CUDA;
+  }
+}
+
+void validate(const tmd_system* s, const tmd_lj_params* lj,
+              const tmd_fene_params* fene, const tmd_engine_params* p) {
+  auto cfg = [](const std::string& m) { throw StatusError{TMD_ERR_CONFIG, m}; };
+  if (!s || !lj || !p) cfg("null argument");
+  if (fene) cfg("FENE bonds are not supported by the GPU path yet");
+  for (int k = 0; k < 3; ++k) {
+    // validate_box (box.hpp:21-29)
+    if (!std::isfinite(s->box[k]) || s->box[k] <= 0.0) {
+      cfg("box lengths must be finite and positive, got " + fmt_g(s->box[k]));
+    }
+  }
+  // validate_lj (potentials.hpp:28-38)
+  if (!(lj->epsilon > 0.0) || !std::isfinite(lj->epsilon))
+    cfg("lj epsilon must be finite and positive");
+  if (!(lj->sigma > 0.0) || !std::isfinite(lj->sigma))
+    cfg("lj sigma must be finite and positive");
+  if (!(lj->r_cut > 0.0) || !std::isfinite(lj->r_cut))
+    cfg("lj r_cut must be finite and positive");
+  if (!std::isfinite(p->r_skin) || p->r_skin < 0.0)
+    cfg("skin radius must be finite and non-negative");
+  // validate_engine_config (engine.hpp:28-41)
+  if (!std::isfinite(p->dt) || p->dt == 0.0)
+    cfg("time step must be finite and nonzero");
+  if (s->n < 1) cfg("empty system: the GPU engine needs at least 1 particle");
+  if (s->n > kMaxSlots) {
+    cfg("system too large for one GPU context: " + std::to_string(s->n) +
+        " particles > " + std::to_string(kMaxSlots));
+  }
+  if (!s->id || !s->pos) cfg("id and pos arrays are required");
+  // validate_flat (flat_config.hpp:42-61): unique ids, positive masses
+  std::vector<int64_t> ids(s->id, s->id + s->n);
+  std::sort(ids.begin(), ids.end());
+  for (size_t k = 1; k < ids.size(); ++k) {
+    if (ids[k] == ids[k - 1]) cfg("duplicate particle id " + std::to_string(ids[k]));
+  }
+  if (s->mass) {
+    for (int64_t k = 0; k < s->n; ++k) {
+      if (!(s->mass[k] > 0.0)) {
+        cfg("particle id " + std::to_string(s->id[k]) + " has non-positive mass");
+      }
+    }
+  }
+  // build_domain's sentinel guard (domain.hpp:162-168), kept for parity of
+  // accepted inputs
+  const double max_len = std::max({s->box[0], s->box[1], s->box[2]});
+  if (max_len > 0.1 * 1.0e9) {
+    cfg("box too large: positions could alias the padding sentinel coordinate");
+  }
+}
+
+void build_geom(tmd_gpu_ctx* c, const double box[3], double r_cut,
+                double r_skin) {
+  // build_cell_grid (cell_grid.hpp:54-78)
+  const double r_verlet = r_cut + r_skin;
+  for (int k = 0; k < 3; ++k) {
+    if (box[k] < r_verlet) {
+      throw StatusError{TMD_ERR_CONFIG,
+                        "box length " + std::to_string(box[k]) +
+                            " is smaller than one cell (r_cut + r_skin = " +
+                            std::to_string(r_verlet) + ")"};
+    }
+    c->g.L[k] = box[k];
+    c->g.dims[k] = std::max(1, static_cast<int>(std::floor(box[k] / r_verlet)));
+  }
+  for (int k = 0; k < 3; ++k) c->g.cell_len[k] = box[k] / c->g.dims[k];
+  const int64_t nc = static_cast<int64_t>(c->g.dims[0]) * c->g.dims[1] * c->g.dims[2];
+  if (nc > (int64_t{1} << 30)) {
+    throw StatusError{TMD_ERR_CONFIG, "cell grid too large"};
+  }
+  c->g.ncells = static_cast<int>(nc);
+  c->g.rv2 = r_verlet * r_verlet;
+  c->g.rebuild_thr = 0.25 * r_skin * r_skin;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
+                   const tmd_fene_params* fene, const tmd_engine_params* params,
+                   tmd_gpu_ctx** out) {
+  if (!out) return TMD_ERR_CONFIG;
+  *out = nullptr;
+  auto* c = new tmd_gpu_ctx();
+  const int rc = guard(c, [&] {
+    validate(sys, lj, fene, params);
+    build_geom(c, sys->box, lj->r_cut, params->r_skin);  // ConfigError before any CUDA call
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (ndev < 1) throw CudaFail{"no CUDA device"};
+    if (params->device >= 0) {
+      ck(cudaSetDevice(params->device), "cudaSetDevice");
+    }
+    ck(cudaGetDevice(&c->device), "cudaGetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, c->device), "cudaGetDeviceProperties");
+    if (prop.major != 10) {
+      throw CudaFail{std::string("device ") + prop.name +
+                     " is not sm_100 (this build targets sm_100a only)"};
+    }
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking),
+       "cudaStreamCreate");
+    ck(cudaEventCreate(&c->t0), "cudaEventCreate");
+    ck(cudaEventCreate(&c->t1), "cudaEventCreate");
+
+    c->n = sys->n;
+    c->stride = static_cast<int>((c->n + 31) / 32 * 32);
+    c->nblk = blocks_for(c->n, kBlock);
+    c->dt = params->dt;
+    c->half_dt = 0.5 * params->dt;
+    c->r_skin = params->r_skin;
+    c->r_cut = lj->r_cut;
+    c->timers_on = params->section_timers != 0;
+    // lj_prepare (potentials.hpp:49-61)
+    c->lj.sigma2 = lj->sigma * lj->sigma;
+    c->lj.rc2 = lj->r_cut * lj->r_cut;
+    c->lj.eps4 = 4.0 * lj->epsilon;
+    c->lj.eps24 = 24.0 * lj->epsilon;
+    c->lj.shift = 0.0;
+    if (lj->energy_shifted) {
+      const double s2 = c->lj.sigma2 / c->lj.rc2;
+      const double s6 = s2 * s2 * s2;
+      c->lj.shift = c->lj.eps4 * (s6 * s6 - s6);
+    }
+
+    const size_t n = static_cast<size_t>(c->n);
+    c->pos = dalloc<double4>(n);
+    c->pos2 = dalloc<double4>(n);
+    c->snap = dalloc<double4>(n);
+    c->vx = dalloc<double>(n); c->vy = dalloc<double>(n); c->vz = dalloc<double>(n);
+    c->vx2 = dalloc<double>(n); c->vy2 = dalloc<double>(n); c->vz2 = dalloc<double>(n);
+    c->fx = dalloc<double>(n); c->fy = dalloc<double>(n); c->fz = dalloc<double>(n);
+    c->mass = dalloc<double>(n); c->mass2 = dalloc<double>(n);
+    c->id = dalloc<long long>(n); c->id2 = dalloc<long long>(n);
+    c->cell = dalloc<int>(n); c->cell2 = dalloc<int>(n);
+    c->rank = dalloc<int>(n); c->perm = dalloc<int>(n);
+    c->count = dalloc<int>(c->g.ncells);
+    c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
+    c->nnbr = dalloc<int>(n);
+    c->part_e = dalloc<double>(c->nblk);
+    c->part_w = dalloc<double>(c->nblk);
+    c->part_ke = dalloc<double>(c->nblk);
+    c->scalars = dalloc<double>(4);
+    c->ctrl = dalloc<Ctrl>(1);
+    c->rebuild_log = dalloc<int>(static_cast<size_t>(kChunk));
+    c->ck_pos = dalloc<double4>(n);
+    c->ck_vx = dalloc<double>(n); c->ck_vy = dalloc<double>(n); c->ck_vz = dalloc<double>(n);
+    c->ck_mass = dalloc<double>(n);
+    c->ck_id = dalloc<long long>(n);
+    ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost");
+    ck(cudaMallocHost(&c->h_scalars, 4 * sizeof(double)), "cudaMallocHost");
+    std::memset(c->h_ctrl, 0, sizeof(Ctrl));
+    ck(cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream), "memset ctrl");
+    ck(cudaMemsetAsync(c->count, 0, sizeof(int) * c->g.ncells, c->stream),
+       "memset count");
+    ck(cudaMemsetAsync(c->fx, 0, n * sizeof(double), c->stream), "memset");
+    ck(cudaMemsetAsync(c->fy, 0, n * sizeof(double), c->stream), "memset");
+    ck(cudaMemsetAsync(c->fz, 0, n * sizeof(double), c->stream), "memset");
+
+    // upload (input order; the first resort sorts by cell)
+    std::vector<double4> hp(n);
+    std::vector<double> hv(3 * n, 0.0), hm(n, 1.0);
+    for (size_t k = 0; k < n; ++k) {
+      hp[k] = make_double4(sys->pos[3 * k], sys->pos[3 * k + 1],
+                           sys->pos[3 * k + 2], 0.0);
+      if (sys->vel) {
+        hv[k] = sys->vel[3 * k];
+        hv[n + k] = sys->vel[3 * k + 1];
+        hv[2 * n + k] = sys->vel[3 * k + 2];
+      }
+      if (sys->mass) hm[k] = sys->mass[k];
+    }
+    ck(cudaMemcpy(c->pos, hp.data(), n * sizeof(double4), cudaMemcpyHostToDevice), "H2D pos");
+    ck(cudaMemcpy(c->vx, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
+    ck(cudaMemcpy(c->vy, hv.data() + n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vy");
+    ck(cudaMemcpy(c->vz, hv.data() + 2 * n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vz");
+    ck(cudaMemcpy(c->mass, hm.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D mass");
+    ck(cudaMemcpy(c->id, sys->id, n * sizeof(long long), cudaMemcpyHostToDevice), "H2D id");
+
+    c->auto_cap = params->nbr_capacity <= 0;
+    // Initial capacity: the expected count at this density (27 cells worth
+    // within a sphere of r_verlet) with generous headroom; refined after the
+    // first build.
+    int cap0 = params->nbr_capacity;
+    if (c->auto_cap) {
+      const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
+      const double rho = static_cast<double>(c->n) / vol;
+      const double rverlet = lj->r_cut + params->r_skin;
+      const double expect = rho * 4.18879020478639 * rverlet * rverlet * rverlet;
+      cap0 = static_cast<int>(expect * 1.5) + 16;
+    }
+    alloc_list(c, cap0);
+    setup_pass(c);
+    c->step = 0;
+    c->rebuilds = 0;
+    c->ke_fresh = false;
+  });
+  if (rc != TMD_OK) {
+    g_create_error = c->err;
+    free_all(c);
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return TMD_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct HostState {
+  std::vector<long long> id;
+  std::vector<double4> pos;
+  std::vector<double> v[3], f[3];
+  std::vector<int> cell;
+  std::vector<size_t> order;  // slots sorted by id
+};
+
+HostState fetch(tmd_gpu_ctx* c, bool pos, bool vel, bool frc, bool cell) {
+  HostState h;
+  const size_t n = static_cast<size_t>(c->n);
+  h.id.resize(n);
+  ck(cudaMemcpyAsync(h.id.data(), c->id, n * sizeof(long long),
+                     cudaMemcpyDeviceToHost, c->stream), "D2H id");
+  if (pos) {
+    h.pos.resize(n);
+    ck(cudaMemcpyAsync(h.pos.data(), c->pos, n * sizeof(double4),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H pos");
+  }
+  double* vs[3] = {c->vx, c->vy, c->vz};
+  double* fs[3] = {c->fx, c->fy, c->fz};
+  for (int k = 0; k < 3; ++k) {
+    if (vel) {
+      h.v[k].resize(n);
+      ck(cudaMemcpyAsync(h.v[k].data(), vs[k], n * sizeof(double),
+                         cudaMemcpyDeviceToHost, c->stream), "D2H vel");
+    }
+    if (frc) {
+      h.f[k].resize(n);
+      ck(cudaMemcpyAsync(h.f[k].data(), fs[k], n * sizeof(double),
+                         cudaMemcpyDeviceToHost, c->stream), "D2H force");
+    }
+  }
+  if (cell) {
+    h.cell.resize(n);
+    ck(cudaMemcpyAsync(h.cell.data(), c->cell, n * sizeof(int),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H cell");
+  }
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  h.order.resize(n);
+  std::iota(h.order.begin(), h.order.end(), size_t{0});
+  std::sort(h.order.begin(), h.order.end(),
+            [&](size_t a, size_t b) { return h.id[a] < h.id[b]; });
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tmd_gpu_last_error(const tmd_gpu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int tmd_gpu_compute_forces(tmd_gpu_ctx* c, double* pe, double* virial) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    launch_forces(c);
+    launch_reduce_pe(c);
+    ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 2 * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+    sync_ctrl(c);
+    raise_physics(c, false);
+    if (pe) *pe = c->h_scalars[0];
+    if (virial) *virial = c->h_scalars[1];
+  });
+}
+
+int tmd_gpu_step(tmd_gpu_ctx* c, int64_t nsteps) {
+  return guard(c, [&] {
+    if (nsteps < 0) throw StatusError{TMD_ERR_CONFIG, "step count must be non-negative"};
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (c->h_ctrl->status != 0) {
+      throw StatusError{TMD_ERR_STATE,
+                        "engine is in an error state from an earlier step"};
+    }
+    do_run(c, nsteps);
+  });
+}
+
+int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    k_kinetic<<<c->nblk, kBlock, 0, c->stream>>>(static_cast<int>(c->n), c->vx,
+                                                 c->vy, c->vz, c->mass,
+                                                 c->part_ke);
+    launch_reduce_ke(c);
+    ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "kernel launch");
+    out->step = c->step;
+    out->potential = c->h_scalars[0];
+    out->virial = c->h_scalars[1];
+    out->kinetic = c->h_scalars[2];
+    // KineticResult::temperature (soa_store.hpp:200-204)
+    out->temperature = 2.0 * out->kinetic / (3.0 * static_cast<double>(c->n));
+  });
+}
+
+int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
+                     double* force) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    HostState h = fetch(c, pos != nullptr, vel != nullptr, force != nullptr, false);
+    const size_t n = h.order.size();
+    for (size_t r = 0; r < n; ++r) {
+      const size_t s = h.order[r];
+      if (id) id[r] = h.id[s];
+      if (pos) {
+        pos[3 * r] = host_wrap1(h.pos[s].x, c->g.L[0]);
+        pos[3 * r + 1] = host_wrap1(h.pos[s].y, c->g.L[1]);
+        pos[3 * r + 2] = host_wrap1(h.pos[s].z, c->g.L[2]);
+      }
+      for (int k = 0; k < 3; ++k) {
+        if (vel) vel[3 * r + k] = h.v[k][s];
+        if (force) force[3 * r + k] = h.f[k][s];
+      }
+    }
+  });
+}
+
+int tmd_gpu_set_velocities(tmd_gpu_ctx* c, const int64_t* id, const double* vel) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    HostState h = fetch(c, false, false, false, false);
+    const size_t n = h.order.size();
+    std::vector<std::pair<int64_t, size_t>> in(n);
+    for (size_t k = 0; k < n; ++k) in[k] = {id[k], k};
+    std::sort(in.begin(), in.end());
+    std::vector<double> v[3];
+    for (int k = 0; k < 3; ++k) v[k].resize(n);
+    for (size_t r = 0; r < n; ++r) {
+      const size_t slot = h.order[r];
+      if (in[r].first != h.id[slot]) {
+        throw StatusError{TMD_ERR_CONFIG, "set_velocities: id set differs from the engine's"};
+      }
+      for (int k = 0; k < 3; ++k) v[k][slot] = vel[3 * in[r].second + k];
+    }
+    double* vs[3] = {c->vx, c->vy, c->vz};
+    for (int k = 0; k < 3; ++k) {
+      ck(cudaMemcpyAsync(vs[k], v[k].data(), n * sizeof(double),
+                         cudaMemcpyHostToDevice, c->stream), "H2D vel");
+    }
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  });
+}
+
+int tmd_gpu_cell_of(tmd_gpu_ctx* c, int64_t* id, int32_t* cell) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    HostState h = fetch(c, false, false, false, true);
+    for (size_t r = 0; r < h.order.size(); ++r) {
+      id[r] = h.id[h.order[r]];
+      cell[r] = h.cell[h.order[r]];
+    }
+  });
+}
+
+int tmd_gpu_pairs(tmd_gpu_ctx* c, int64_t* pairs, size_t cap, size_t* n_out) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    HostState h = fetch(c, false, false, false, false);
+    const size_t n = h.order.size();
+    const int rows = std::min(c->cap, std::max(c->h_ctrl->max_count, 0));
+    std::vector<int> cnt(n);
+    std::vector<uint32_t> list(static_cast<size_t>(rows) * c->stride);
+    ck(cudaMemcpyAsync(cnt.data(), c->nnbr, n * sizeof(int),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H nnbr");
+    if (!list.empty()) {
+      ck(cudaMemcpyAsync(list.data(), c->nbr, list.size() * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost, c->stream), "D2H nbr");
+    }
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    std::vector<std::pair<int64_t, int64_t>> out;
+    out.reserve(static_cast<size_t>(c->h_ctrl->entries / 2 + 1));
+    for (size_t i = 0; i < n; ++i) {
+      const int64_t a = h.id[i];
+      for (int k = 0; k < cnt[i]; ++k) {
+        const uint32_t ent = list[static_cast<size_t>(k) * c->stride + i];
+        const int64_t b = h.id[ent & kIdxMask];
+        if (a < b) out.emplace_back(a, b);
+      }
+    }
+    std::sort(out.begin(), out.end());
+    *n_out = out.size();
+    for (size_t k = 0; k < std::min(cap, out.size()); ++k) {
+      pairs[2 * k] = out[k].first;
+      pairs[2 * k + 1] = out[k].second;
+    }
+  });
+}
+
+int tmd_gpu_timers(tmd_gpu_ctx* c, double sec[5], double* elapsed) {
+  for (int k = 0; k < 5; ++k) sec[k] = c->sec[k];
+  if (elapsed) *elapsed = c->elapsed;
+  return TMD_OK;
+}
+
+uint64_t tmd_gpu_rebuild_count(const tmd_gpu_ctx* c) { return c->rebuilds; }
+int64_t tmd_gpu_step_count(const tmd_gpu_ctx* c) { return c->step; }
+int64_t tmd_gpu_size(const tmd_gpu_ctx* c) { return c->n; }
+
+int tmd_gpu_list_stats(tmd_gpu_ctx* c, tmd_list_stats* out) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    unsigned long long* d = dalloc<unsigned long long>(1);
+    ck(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream), "memset");
+    k_count_incut<<<c->nblk, kBlock, 0, c->stream>>>(
+        static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g,
+        c->lj.rc2, d);
+    unsigned long long h = 0;
+    ck(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    sync_ctrl(c);
+    cudaFree(d);
+    out->n = c->n;
+    out->entries = c->h_ctrl->entries;
+    out->in_cut = static_cast<int64_t>(h);
+    out->max_count = c->h_ctrl->max_count;
+    out->capacity = c->cap;
+    for (int k = 0; k < 3; ++k) {
+      out->dims[k] = c->g.dims[k];
+      out->cell_len[k] = c->g.cell_len[k];
+    }
+  });
+}
+
+int tmd_gpu_time_force_kernel(tmd_gpu_ctx* c, int reps, double* ms) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (reps < 1) throw StatusError{TMD_ERR_CONFIG, "reps must be >= 1"};
+    ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    for (int r = 0; r < reps; ++r) launch_forces(c);
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+    float t = 0.f;
+    ck(cudaEventElapsedTime(&t, c->t0, c->t1), "cudaEventElapsedTime");
+    ck(cudaGetLastError(), "kernel launch");
+    *ms = static_cast<double>(t) / reps;
+  });
+}
+
+void* tmd_gpu_stream(tmd_gpu_ctx* c) { return c->stream; }
+
+void tmd_gpu_destroy(tmd_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_all(c);
+  delete c;
+}
+
+}  // extern "C"

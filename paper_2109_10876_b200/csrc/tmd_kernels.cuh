@@ -1,0 +1,464 @@
+// sm_100a kernels of the LJ short-range path. One thread per particle for the
+// streaming kernels; see DESIGN.md for the roofline each one is held to.
+//
+// Every rebuild-phase kernel reads the device-side decision ctrl->rebuild and
+// returns immediately when it is 0, so a whole step (including the
+// data-dependent resort + list build) is enqueued without a host round trip.
+#pragma once
+
+#include "tmd_device.cuh"
+
+namespace tmd {
+
+constexpr int kBlock = 128;
+
+// ---------------------------------------------------------------------------
+// Integrate: first half-kick + drift, fused with the displacement test.
+// Engine::half_kick_and_drift (engine.hpp:174-189) and max_displacement2
+// (neighbor_list.hpp:114-136). Arithmetic order mirrors the reference:
+// v += (f * inv_m) * half_dt; x += v * dt.
+__device__ __forceinline__ void kick(double& v, double f, double inv_m,
+                                     double half_dt) {
+  v = __dadd_rn(v, __dmul_rn(__dmul_rn(f, inv_m), half_dt));
+}
+
+// kick2 of the previous step (optional, fused) + kick1 + drift of this step.
+// With kFused the kernel also emits the kinetic-energy partials of the
+// post-kick2 velocities and performs the non-finite check of
+// thermostat_and_half_kick (engine.hpp:231-236).
+template <bool kFused>
+__global__ void __launch_bounds__(kBlock)
+    k_kick_drift(int n, double4* __restrict__ pos, double* __restrict__ vx,
+                 double* __restrict__ vy, double* __restrict__ vz,
+                 const double* __restrict__ fx, const double* __restrict__ fy,
+                 const double* __restrict__ fz, const double* __restrict__ mass,
+                 const long long* __restrict__ id,
+                 const double4* __restrict__ snap, double dt, double half_dt,
+                 double* __restrict__ part_ke, Ctrl* ctrl) {
+  __shared__ double red[kBlock / 32];
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  double d2 = 0.0, ke = 0.0;
+  if (i < n) {
+    const double inv_m = __ddiv_rn(1.0, mass[i]);
+    double ux = vx[i], uy = vy[i], uz = vz[i];
+    const double gx = fx[i], gy = fy[i], gz = fz[i];
+    if (kFused) {
+      kick(ux, gx, inv_m, half_dt);
+      kick(uy, gy, inv_m, half_dt);
+      kick(uz, gz, inv_m, half_dt);
+      if (!finite3(ux, uy, uz) || !finite3(gx, gy, gz)) {
+        record_error(ctrl, kStatNonFinite, id[i], -1);
+      }
+      ke = __dmul_rn(__dmul_rn(0.5, mass[i]),
+                     __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)),
+                               __dmul_rn(uz, uz)));
+    }
+    kick(ux, gx, inv_m, half_dt);
+    kick(uy, gy, inv_m, half_dt);
+    kick(uz, gz, inv_m, half_dt);
+    double4 p = pos[i];
+    p.x = __dadd_rn(p.x, __dmul_rn(ux, dt));
+    p.y = __dadd_rn(p.y, __dmul_rn(uy, dt));
+    p.z = __dadd_rn(p.z, __dmul_rn(uz, dt));
+    pos[i] = p;
+    vx[i] = ux;
+    vy[i] = uy;
+    vz[i] = uz;
+    const double4 s = snap[i];
+    d2 = exact_r2(__dsub_rn(p.x, s.x), __dsub_rn(p.y, s.y),
+                  __dsub_rn(p.z, s.z));
+  }
+  // block max of d2 (non-negative doubles order like their bit patterns)
+  for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  if ((threadIdx.x & 31) == 0 && d2 > 0.0) {
+    atomicMax(&ctrl->max_d2, static_cast<unsigned long long>(__double_as_longlong(d2)));
+  }
+  if (kFused) {
+    const double t = block_sum<kBlock>(ke, red);
+    if (threadIdx.x == 0) part_ke[blockIdx.x] = t;
+  }
+}
+
+// Second half-kick + non-finite check + kinetic partials (end of a run).
+// Engine::thermostat_and_half_kick without a thermostat (engine.hpp:209-239).
+__global__ void __launch_bounds__(kBlock)
+    k_kick2(int n, double* __restrict__ vx, double* __restrict__ vy,
+            double* __restrict__ vz, const double* __restrict__ fx,
+            const double* __restrict__ fy, const double* __restrict__ fz,
+            const double* __restrict__ mass, const long long* __restrict__ id,
+            double half_dt, double* __restrict__ part_ke, Ctrl* ctrl) {
+  __shared__ double red[kBlock / 32];
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  double ke = 0.0;
+  if (i < n) {
+    const double inv_m = __ddiv_rn(1.0, mass[i]);
+    double ux = vx[i], uy = vy[i], uz = vz[i];
+    const double gx = fx[i], gy = fy[i], gz = fz[i];
+    kick(ux, gx, inv_m, half_dt);
+    kick(uy, gy, inv_m, half_dt);
+    kick(uz, gz, inv_m, half_dt);
+    if (!finite3(ux, uy, uz) || !finite3(gx, gy, gz)) {
+      record_error(ctrl, kStatNonFinite, id[i], -1);
+    }
+    vx[i] = ux;
+    vy[i] = uy;
+    vz[i] = uz;
+    ke = __dmul_rn(__dmul_rn(0.5, mass[i]),
+                   __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)),
+                             __dmul_rn(uz, uz)));
+  }
+  const double t = block_sum<kBlock>(ke, red);
+  if (threadIdx.x == 0) part_ke[blockIdx.x] = t;
+}
+
+// Kinetic partials of the current velocities (observe() after setup).
+__global__ void __launch_bounds__(kBlock)
+    k_kinetic(int n, const double* __restrict__ vx, const double* __restrict__ vy,
+              const double* __restrict__ vz, const double* __restrict__ mass,
+              double* __restrict__ part_ke) {
+  __shared__ double red[kBlock / 32];
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  double ke = 0.0;
+  if (i < n) {
+    const double ux = vx[i], uy = vy[i], uz = vz[i];
+    ke = __dmul_rn(__dmul_rn(0.5, mass[i]),
+                   __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)),
+                             __dmul_rn(uz, uz)));
+  }
+  const double t = block_sum<kBlock>(ke, red);
+  if (threadIdx.x == 0) part_ke[blockIdx.x] = t;
+}
+
+// Rebuild decision (Engine::step, engine.hpp:88-100): global OR of
+// needs_rebuild == max |dx|^2 > 0.25 skin^2 (strict), plus a host override.
+__global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
+                         int log_idx) {
+  const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
+  const int r = (ctrl->force_rebuild != 0) || (m > thr);
+  ctrl->rebuild = r;
+  if (log) log[log_idx] = r;
+  ctrl->force_rebuild = 0;
+  ctrl->max_d2 = 0ull;
+  if (advance_step) ctrl->step += 1;
+  if (r && advance_step) ctrl->rebuilds += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Resort = counting sort by cell (distribute_records, domain.hpp:54-92).
+
+// wrap_position + CellGrid::cell_of, histogram. Positions are wrapped in place
+// (the reference wraps only here, domain.hpp:63).
+__global__ void __launch_bounds__(kBlock)
+    k_wrap_bin(int n, double4* __restrict__ pos, const long long* __restrict__ id,
+               int* __restrict__ cell, int* __restrict__ rank,
+               int* __restrict__ count, Geom g, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n) return;
+  double4 p = pos[i];
+  if (!finite3(p.x, p.y, p.z)) {
+    record_error(ctrl, kStatNonFinitePos, id[i], -1);
+    p.x = p.y = p.z = 0.0;
+  }
+  p.x = wrap1(p.x, g.L[0]);
+  p.y = wrap1(p.y, g.L[1]);
+  p.z = wrap1(p.z, g.L[2]);
+  pos[i] = p;
+  const int cx = cell_coord(p.x, g.cell_len[0], g.dims[0]);
+  const int cy = cell_coord(p.y, g.cell_len[1], g.dims[1]);
+  const int cz = cell_coord(p.z, g.cell_len[2], g.dims[2]);
+  const int c = cx + g.dims[0] * (cy + g.dims[1] * cz);
+  cell[i] = c;
+  rank[i] = atomicAdd(&count[c], 1);
+}
+
+// Exclusive scan of the cell histogram (one block; runs once per rebuild).
+// Zeroes the histogram for the next resort.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan(int ncells, int* __restrict__ count, int* __restrict__ start,
+           Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  __shared__ int warp_tot[kScanThreads / 32];
+  const int t = threadIdx.x;
+  const int per = (ncells + kScanThreads - 1) / kScanThreads;
+  const int b = min(t * per, ncells), e = min(b + per, ncells);
+  int s = 0;
+  for (int c = b; c < e; ++c) s += count[c];
+  // block exclusive scan of s
+  const int lane = t & 31, warp = t >> 5;
+  int v = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) warp_tot[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    warp_tot[lane] = w;
+  }
+  __syncthreads();
+  int run = v - s + (warp > 0 ? warp_tot[warp - 1] : 0);
+  for (int c = b; c < e; ++c) {
+    const int k = count[c];
+    start[c] = run;
+    run += k;
+    count[c] = 0;
+  }
+  if (t == kScanThreads - 1) start[ncells] = run;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_scatter(int n, const int* __restrict__ cell, const int* __restrict__ rank,
+              const int* __restrict__ start, int* __restrict__ perm, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n) return;
+  perm[start[cell[i]] + rank[i]] = i;
+}
+
+// Canonical order inside each cell: ascending particle id. Makes the sorted
+// layout (and so every FP summation order) a pure function of the particle
+// set, independent of the previous order and of the atomic arrival order.
+__global__ void __launch_bounds__(kBlock)
+    k_sort_cells(int ncells, const int* __restrict__ start, int* __restrict__ perm,
+                 const long long* __restrict__ id, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int c = blockIdx.x * kBlock + threadIdx.x;
+  if (c >= ncells) return;
+  const int b = start[c], e = start[c + 1];
+  for (int k = b + 1; k < e; ++k) {
+    const int pk = perm[k];
+    const long long key = id[pk];
+    int m = k - 1;
+    while (m >= b && id[perm[m]] > key) {
+      perm[m + 1] = perm[m];
+      --m;
+    }
+    perm[m + 1] = pk;
+  }
+}
+
+// Gather every particle array through perm into the alternate buffers.
+__global__ void __launch_bounds__(kBlock)
+    k_permute(int n, const int* __restrict__ perm, const double4* __restrict__ pos,
+              const double* __restrict__ vx, const double* __restrict__ vy,
+              const double* __restrict__ vz, const double* __restrict__ mass,
+              const long long* __restrict__ id, const int* __restrict__ cell,
+              double4* __restrict__ pos2, double* __restrict__ vx2,
+              double* __restrict__ vy2, double* __restrict__ vz2,
+              double* __restrict__ mass2, long long* __restrict__ id2,
+              int* __restrict__ cell2, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= n) return;
+  const int s = perm[k];
+  pos2[k] = pos[s];
+  vx2[k] = vx[s];
+  vy2[k] = vy[s];
+  vz2[k] = vz[s];
+  mass2[k] = mass[s];
+  id2[k] = id[s];
+  cell2[k] = cell[s];
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_copy_back(int n, const double4* __restrict__ pos2,
+                const double* __restrict__ vx2, const double* __restrict__ vy2,
+                const double* __restrict__ vz2, const double* __restrict__ mass2,
+                const long long* __restrict__ id2, const int* __restrict__ cell2,
+                double4* __restrict__ pos, double* __restrict__ vx,
+                double* __restrict__ vy, double* __restrict__ vz,
+                double* __restrict__ mass, long long* __restrict__ id,
+                int* __restrict__ cell, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= n) return;
+  pos[k] = pos2[k];
+  vx[k] = vx2[k];
+  vy[k] = vy2[k];
+  vz[k] = vz2[k];
+  mass[k] = mass2[k];
+  id[k] = id2[k];
+  cell[k] = cell2[k];
+}
+
+// ---------------------------------------------------------------------------
+// Full Verlet list build (the full-list form of build_sorted_list,
+// neighbor_list.hpp:51-111): for particle i, every j in the 27 surrounding
+// cells (with periodic images) with exact r2 <= rv2, own image excluded
+// (neighbor_list.hpp:91-93). Also snapshots positions for needs_rebuild.
+__global__ void __launch_bounds__(kBlock)
+    k_build_list(int n, const double4* __restrict__ pos, const int* __restrict__ cell,
+                 const int* __restrict__ start, Geom g, uint32_t* __restrict__ nbr,
+                 int* __restrict__ nnbr, int stride, int cap,
+                 double4* __restrict__ snap, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  __shared__ double red[kBlock / 32];
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  int cnt = 0;
+  if (i < n) {
+    const double4 pi = pos[i];
+    snap[i] = pi;
+    const int c = cell[i];
+    const int cx = c % g.dims[0];
+    const int cy = (c / g.dims[0]) % g.dims[1];
+    const int cz = c / (g.dims[0] * g.dims[1]);
+    for (int oz = -1; oz <= 1; ++oz) {
+      int tz = cz + oz;
+      uint32_t code_z = 0;
+      if (tz < 0) { tz += g.dims[2]; code_z = 2; }
+      else if (tz >= g.dims[2]) { tz -= g.dims[2]; code_z = 1; }
+      for (int oy = -1; oy <= 1; ++oy) {
+        int ty = cy + oy;
+        uint32_t code_y = 0;
+        if (ty < 0) { ty += g.dims[1]; code_y = 2; }
+        else if (ty >= g.dims[1]) { ty -= g.dims[1]; code_y = 1; }
+        for (int ox = -1; ox <= 1; ++ox) {
+          int tx = cx + ox;
+          uint32_t code_x = 0;
+          if (tx < 0) { tx += g.dims[0]; code_x = 2; }
+          else if (tx >= g.dims[0]) { tx -= g.dims[0]; code_x = 1; }
+          const int t = tx + g.dims[0] * (ty + g.dims[1] * tz);
+          // half-stencil orientation: first nonzero component (x, y, z) > 0
+          const int first = ox != 0 ? ox : (oy != 0 ? oy : oz);
+          const uint32_t img = (code_x << 25) | (code_y << 27) | (code_z << 29);
+          const uint32_t tag = img | ((img != 0u && first < 0) ? kFlagIUpper : 0u);
+          const bool same = (t == c);
+          const int jb = start[t], je = start[t + 1];
+          for (int j = jb; j < je; ++j) {
+            if (same && j == i) continue;
+            const double4 pj = pos[j];
+            const uint32_t ent = static_cast<uint32_t>(j) | tag;
+            double dx, dy, dz;
+            pair_delta(pi, pj, ent, g, dx, dy, dz);
+            if (exact_r2(dx, dy, dz) <= g.rv2) {
+              if (cnt < cap) nbr[static_cast<size_t>(cnt) * stride + i] = ent;
+              ++cnt;
+            }
+          }
+        }
+      }
+    }
+    nnbr[i] = cnt < cap ? cnt : cap;
+    if (cnt > cap) atomicOr(&ctrl->status, kStatOverflow);
+  }
+  // block max count + total entries
+  int m = cnt;
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&ctrl->max_count, m);
+  const double tot = block_sum<kBlock>(static_cast<double>(cnt), red);
+  if (threadIdx.x == 0 && tot > 0.0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries),
+              static_cast<unsigned long long>(tot));
+  }
+}
+
+// Resets the per-build statistics before a build (only when rebuilding).
+__global__ void k_build_prologue(Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  ctrl->max_count = 0;
+  ctrl->entries = 0;
+}
+
+// ---------------------------------------------------------------------------
+// LJ forces + energy + virial over the full list, one thread per particle
+// (compute_pair_forces, neighbor_list.hpp:150-187, in full-list form: every
+// thread owns its own f_i, no Newton-3 scatter, no atomics). Cutoff test and
+// r2 are rounded exactly like the reference; the force arithmetic uses one
+// reciprocal. Per-block partials of sum_i e_i and sum_i w_i (each pair counted
+// twice; the final reduction halves them).
+__global__ void __launch_bounds__(kBlock)
+    k_lj_forces(int n, const double4* __restrict__ pos,
+                const uint32_t* __restrict__ nbr, const int* __restrict__ nnbr,
+                int stride, Geom g, LjConst lj, double* __restrict__ fx,
+                double* __restrict__ fy, double* __restrict__ fz,
+                double* __restrict__ part_e, double* __restrict__ part_w,
+                const long long* __restrict__ id, Ctrl* ctrl) {
+  __shared__ double red[kBlock / 32];
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  double e = 0.0, w = 0.0;
+  if (i < n) {
+    const double4 pi = pos[i];
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    const int cnt = nnbr[i];
+    const uint32_t* p = nbr + i;
+    for (int k = 0; k < cnt; ++k) {
+      const uint32_t ent = __ldg(p + static_cast<size_t>(k) * stride);
+      const double4 pj = ldg_pos(pos + (ent & kIdxMask));
+      double dx, dy, dz;
+      pair_delta(pi, pj, ent, g, dx, dy, dz);
+      const double r2 = exact_r2(dx, dy, dz);
+      if (r2 < lj.rc2) {
+        if (r2 == 0.0) {
+          record_error(ctrl, kStatOverlap, id[i], id[ent & kIdxMask]);
+          continue;
+        }
+        const double ri2 = rcp_nr(r2);
+        const double inv = lj.sigma2 * ri2;
+        const double i6 = inv * inv * inv;
+        const double ff = lj.eps24 * (2.0 * i6 * i6 - i6) * ri2;
+        e += lj.eps4 * (i6 * i6 - i6) - lj.shift;
+        w += ff * r2;
+        ax += ff * dx;
+        ay += ff * dy;
+        az += ff * dz;
+      }
+    }
+    fx[i] = ax;
+    fy[i] = ay;
+    fz[i] = az;
+  }
+  const double te = block_sum<kBlock>(e, red);
+  const double tw = block_sum<kBlock>(w, red);
+  if (threadIdx.x == 0) {
+    part_e[blockIdx.x] = te;
+    part_w[blockIdx.x] = tw;
+  }
+}
+
+// Deterministic final reduction of per-block partials (fixed order tree).
+constexpr int kRedThreads = 1024;
+__global__ void __launch_bounds__(kRedThreads)
+    k_reduce(const double* __restrict__ part, int nparts, double scale,
+             double* __restrict__ out) {
+  __shared__ double red[kRedThreads / 32];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < nparts; k += kRedThreads) s += part[k];
+  const double t = block_sum<kRedThreads>(s, red);
+  if (threadIdx.x == 0) *out = t * scale;
+}
+
+// In-cut pair count of the current list (roofline accounting only; not on
+// the step path).
+__global__ void __launch_bounds__(kBlock)
+    k_count_incut(int n, const double4* __restrict__ pos,
+                  const uint32_t* __restrict__ nbr, const int* __restrict__ nnbr,
+                  int stride, Geom g, double rc2,
+                  unsigned long long* __restrict__ out) {
+  __shared__ double red[kBlock / 32];
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  double cnt = 0.0;
+  if (i < n) {
+    const double4 pi = pos[i];
+    const int m = nnbr[i];
+    for (int k = 0; k < m; ++k) {
+      const uint32_t ent = nbr[static_cast<size_t>(k) * stride + i];
+      const double4 pj = pos[ent & kIdxMask];
+      double dx, dy, dz;
+      pair_delta(pi, pj, ent, g, dx, dy, dz);
+      if (exact_r2(dx, dy, dz) < rc2) cnt += 1.0;
+    }
+  }
+  const double t = block_sum<kBlock>(cnt, red);
+  if (threadIdx.x == 0 && t > 0.0) {
+    atomicAdd(out, static_cast<unsigned long long>(t));
+  }
+}
+
+}  // namespace tmd

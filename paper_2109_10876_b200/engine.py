@@ -1,0 +1,386 @@
+"""Python mirror of the reference engine's public API, backed by libtmd_gpu.so.
+
+The names, argument meanings and error behaviour follow the reference
+`taskmd` C++ API (/root/reference/proj/include/taskmd/):
+
+  FlatConfig        flat_config.hpp:18-40     decomposition-free snapshot
+  LjParams          potentials.hpp:21-26
+  Interactions      domain.hpp:19-23          (FENE / angles: not on this path)
+  EngineConfig      engine.hpp:19-26
+  StepObservables   engine.hpp:43-48          (+ virial)
+  SectionTimers     timers.hpp:36-62
+  Engine            engine.hpp:66-290         build_domain + Engine in one ctor
+  ConfigError, PhysicsError, VerifyError, StateError   errors.hpp:19-43
+
+Every numeric call goes through the C ABI (include/tmd_gpu.h) to the sm_100a
+kernels; nothing here computes physics on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _abi
+
+
+class ConfigError(ValueError):
+    """taskmd::ConfigError (errors.hpp:21-26)."""
+
+
+class PhysicsError(RuntimeError):
+    """taskmd::PhysicsError (errors.hpp:28-34)."""
+
+
+class VerifyError(RuntimeError):
+    """taskmd::VerifyError (errors.hpp:36-40)."""
+
+
+class StateError(RuntimeError):
+    """taskmd::StateError (errors.hpp:42-47)."""
+
+
+class CudaError(RuntimeError):
+    """Device or driver failure (no reference analog)."""
+
+
+_ERRORS = {
+    _abi.TMD_ERR_CONFIG: ConfigError,
+    _abi.TMD_ERR_PHYSICS: PhysicsError,
+    _abi.TMD_ERR_VERIFY: VerifyError,
+    _abi.TMD_ERR_STATE: StateError,
+    _abi.TMD_ERR_CUDA: CudaError,
+}
+
+
+def _check(rc: int, ctx) -> None:
+    if rc != _abi.TMD_OK:
+        msg = _abi.lib().tmd_gpu_last_error(ctx)
+        raise _ERRORS.get(rc, CudaError)((msg or b"").decode(errors="replace"))
+
+
+class Section(enum.IntEnum):
+    """taskmd::Section (timers.hpp:11-17)."""
+    kForces = 0
+    kComm = 1
+    kIntegrate = 2
+    kNeigh = 3
+    kResort = 4
+
+
+SECTION_NAMES = ("Forces", "Comm", "Integrate", "Neigh", "Resort")
+
+
+@dataclass
+class SectionTimers:
+    seconds: np.ndarray = field(default_factory=lambda: np.zeros(5))
+    elapsed: float = 0.0
+
+    def __getitem__(self, s: Section) -> float:
+        return float(self.seconds[int(s)])
+
+    def section_sum(self) -> float:
+        return float(self.seconds.sum())
+
+
+@dataclass
+class LjParams:
+    epsilon: float = 1.0
+    sigma: float = 1.0
+    r_cut: float = 2.5
+    energy_shifted: bool = True
+
+
+@dataclass
+class FeneParams:
+    k: float = 30.0
+    r_max: float = 1.5
+
+
+@dataclass
+class AngleParams:
+    k: float = 1.0
+    theta0: float = 0.0
+
+
+@dataclass
+class LangevinParams:
+    gamma: float = 1.0
+    temperature: float = 1.0
+    seed: int = 0
+
+
+@dataclass
+class Interactions:
+    lj: LjParams = field(default_factory=LjParams)
+    fene: Optional[FeneParams] = None
+    angle: Optional[AngleParams] = None
+
+
+@dataclass
+class EngineConfig:
+    dt: float = 0.005
+    steps: int = 0
+    thermostat: Optional[LangevinParams] = None
+    n_sub: int = 1              # CPU subnode count: accepted, no GPU meaning
+    worker_threads: int = 1     # CPU workers: accepted, no GPU meaning
+    observable_stride: int = 100
+    # GPU-only knobs
+    section_timers: bool = True
+    device: int = -1
+    nbr_capacity: int = 0
+
+
+@dataclass
+class StepObservables:
+    step: int = 0
+    kinetic: float = 0.0
+    potential: float = 0.0
+    temperature: float = 0.0
+    virial: float = 0.0
+
+
+@dataclass
+class FlatConfig:
+    """Parallel arrays + box (flat_config.hpp:18-40). pos/vel are (n, 3)."""
+    box: np.ndarray
+    id: np.ndarray
+    pos: np.ndarray
+    vel: np.ndarray
+    mass: Optional[np.ndarray] = None
+    type: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        self.box = np.ascontiguousarray(self.box, dtype=np.float64).reshape(3)
+        self.id = np.ascontiguousarray(self.id, dtype=np.int64)
+        self.pos = np.ascontiguousarray(self.pos, dtype=np.float64).reshape(-1, 3)
+        if self.vel is None:
+            self.vel = np.zeros_like(self.pos)
+        self.vel = np.ascontiguousarray(self.vel, dtype=np.float64).reshape(-1, 3)
+        if self.mass is not None:
+            self.mass = np.ascontiguousarray(self.mass, dtype=np.float64)
+        if self.type is not None:
+            self.type = np.ascontiguousarray(self.type, dtype=np.int32)
+
+    def size(self) -> int:
+        return int(self.id.shape[0])
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def validate_engine_config(c: EngineConfig) -> None:
+    """validate_engine_config (engine.hpp:28-41) + GPU-path scope checks."""
+    if not np.isfinite(c.dt) or c.dt == 0.0:
+        raise ConfigError("time step must be finite and nonzero")
+    if c.steps < 0:
+        raise ConfigError("step count must be non-negative")
+    if c.n_sub < 1:
+        raise ConfigError("n_sub must be at least 1")
+    if c.worker_threads < 1:
+        raise ConfigError("worker_threads must be at least 1")
+    if c.observable_stride < 1:
+        raise ConfigError("observable stride must be at least 1")
+    if c.thermostat is not None:
+        raise ConfigError("the Langevin thermostat is not on the GPU path yet "
+                          "(SURVEY §8f row f4)")
+
+
+class Engine:
+    """build_domain (domain.hpp:134) + Engine (engine.hpp:66) on one B200.
+
+    Engine(flat, inter, r_skin, cfg): validates, uploads, bins, builds the
+    full Verlet list and runs the untimed initial force evaluation.
+    """
+
+    def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
+                 cfg: Optional[EngineConfig] = None):
+        cfg = cfg or EngineConfig()
+        validate_engine_config(cfg)
+        if inter.angle is not None:
+            raise ConfigError("angle terms are not on the GPU LJ path")
+        if inter.fene is not None:
+            raise ConfigError("FENE bonds are not on the GPU path yet (SURVEY §8f row f1)")
+        L = _abi.lib()
+        self._cfg = cfg
+        self._n = flat.size()
+        self._keep = flat
+        sys = _abi.TmdSystem()
+        sys.box[:] = list(flat.box)
+        sys.n = self._n
+        sys.id = _ptr(flat.id)
+        sys.type = _ptr(flat.type)
+        sys.mass = _ptr(flat.mass)
+        sys.pos = _ptr(flat.pos)
+        sys.vel = _ptr(flat.vel)
+        lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
+                              1 if inter.lj.energy_shifted else 0)
+        p = _abi.TmdEngineParams()
+        p.dt = cfg.dt
+        p.r_skin = r_skin
+        p.device = cfg.device
+        p.section_timers = 1 if cfg.section_timers else 0
+        p.nbr_capacity = cfg.nbr_capacity
+        h = C.c_void_p()
+        rc = L.tmd_gpu_create(C.byref(sys), C.byref(lj), None, C.byref(p), C.byref(h))
+        _check(rc, None)
+        self._h = h
+        self.box = flat.box.copy()
+        self.r_skin = float(r_skin)
+        self.inter = inter
+
+    # -- lifetime -----------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().tmd_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- Engine surface (engine.hpp:80-149) -----------------------------------
+    def step(self) -> None:
+        self.run(1)
+
+    def run(self, steps: int) -> None:
+        _check(_abi.lib().tmd_gpu_step(self._h, int(steps)), self._h)
+
+    def observe(self) -> StepObservables:
+        o = _abi.TmdObservables()
+        _check(_abi.lib().tmd_gpu_observe(self._h, C.byref(o)), self._h)
+        return StepObservables(int(o.step), o.kinetic, o.potential, o.temperature,
+                               o.virial)
+
+    def config(self) -> EngineConfig:
+        return self._cfg
+
+    def timers(self) -> SectionTimers:
+        sec = np.zeros(5)
+        el = C.c_double()
+        _check(_abi.lib().tmd_gpu_timers(self._h, _ptr(sec), C.byref(el)), self._h)
+        return SectionTimers(sec, el.value)
+
+    def step_count(self) -> int:
+        return int(_abi.lib().tmd_gpu_step_count(self._h))
+
+    def potential_energy(self) -> float:
+        return self.observe().potential
+
+    def rebuild_count(self) -> int:
+        return int(_abi.lib().tmd_gpu_rebuild_count(self._h))
+
+    def steal_count(self) -> int:
+        return 0  # no work-stealing pool on the GPU path
+
+    def size(self) -> int:
+        return self._n
+
+    # -- state access ----------------------------------------------------------
+    def flatten(self) -> FlatConfig:
+        """flatten_domain (domain.hpp:193-207): sorted by id, wrapped."""
+        n = self._n
+        ids = np.empty(n, np.int64)
+        pos = np.empty((n, 3))
+        vel = np.empty((n, 3))
+        _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), None),
+               self._h)
+        return FlatConfig(self.box.copy(), ids, pos, vel)
+
+    def forces(self):
+        """(ids, forces) of the last evaluation, sorted by id."""
+        n = self._n
+        ids = np.empty(n, np.int64)
+        f = np.empty((n, 3))
+        _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), None, None, _ptr(f)),
+               self._h)
+        return ids, f
+
+    def set_velocities(self, ids: np.ndarray, vel: np.ndarray) -> None:
+        ids = np.ascontiguousarray(ids, np.int64)
+        vel = np.ascontiguousarray(vel, np.float64).reshape(-1, 3)
+        _check(_abi.lib().tmd_gpu_set_velocities(self._h, _ptr(ids), _ptr(vel)), self._h)
+
+    def compute_forces(self):
+        """One force evaluation at the current positions: (pe, virial)."""
+        pe, w = C.c_double(), C.c_double()
+        _check(_abi.lib().tmd_gpu_compute_forces(self._h, C.byref(pe), C.byref(w)), self._h)
+        return pe.value, w.value
+
+    # -- parity taps -------------------------------------------------------------
+    def cell_of(self):
+        n = self._n
+        ids = np.empty(n, np.int64)
+        cell = np.empty(n, np.int32)
+        _check(_abi.lib().tmd_gpu_cell_of(self._h, _ptr(ids), _ptr(cell)), self._h)
+        return ids, cell
+
+    def pairs(self) -> np.ndarray:
+        L = _abi.lib()
+        n = C.c_size_t()
+        _check(L.tmd_gpu_pairs(self._h, None, 0, C.byref(n)), self._h)
+        out = np.empty((max(n.value, 1), 2), np.int64)
+        _check(L.tmd_gpu_pairs(self._h, _ptr(out), n.value, C.byref(n)), self._h)
+        return out[: n.value]
+
+    def list_stats(self) -> dict:
+        s = _abi.TmdListStats()
+        _check(_abi.lib().tmd_gpu_list_stats(self._h, C.byref(s)), self._h)
+        return dict(n=s.n, entries=s.entries, in_cut=s.in_cut, max_count=s.max_count,
+                    capacity=s.capacity, dims=tuple(s.dims), cell_len=tuple(s.cell_len))
+
+    def time_force_kernel(self, reps: int) -> float:
+        ms = C.c_double()
+        _check(_abi.lib().tmd_gpu_time_force_kernel(self._h, int(reps), C.byref(ms)),
+               self._h)
+        return ms.value
+
+
+# -- setup helpers (host-side, C ABI) --------------------------------------------
+
+def gen_fcc(cells: int, rho: float, temperature: float, seed: int,
+            offset: float = 0.25) -> FlatConfig:
+    """FCC cells^3 x 4 lattice with thermal velocities."""
+    L = _abi.lib()
+    n = 4 * cells ** 3
+    ids = np.empty(n, np.int64)
+    pos = np.empty((n, 3))
+    box = np.empty(3)
+    rc = L.tmd_gen_fcc(int(cells), float(rho), float(offset), _ptr(ids), _ptr(pos), _ptr(box))
+    if rc != 0:
+        raise ConfigError("fcc generator: cells >= 1 and rho > 0 required")
+    vel = np.empty((n, 3))
+    L.tmd_thermal_velocities(n, _ptr(ids), None, float(temperature), int(seed), _ptr(vel))
+    return FlatConfig(box, ids, pos, vel)
+
+
+def thermal_velocities(flat: FlatConfig, temperature: float, seed: int) -> None:
+    """gen_detail::thermal_velocities + zero_net_momentum (generators.hpp:19-39)."""
+    vel = np.empty((flat.size(), 3))
+    _abi.lib().tmd_thermal_velocities(flat.size(), _ptr(flat.id), _ptr(flat.mass),
+                                      float(temperature), int(seed), _ptr(vel))
+    flat.vel = vel
+
+
+def counter_uniform3(seed: int, ctx: int, step: int, pid: int) -> np.ndarray:
+    out = np.empty(3)
+    _abi.lib().tmd_counter_uniform3(seed, ctx, step, pid, _ptr(out))
+    return out
+
+
+def counter_normal3(seed: int, ctx: int, step: int, pid: int) -> np.ndarray:
+    out = np.empty(3)
+    _abi.lib().tmd_counter_normal3(seed, ctx, step, pid, _ptr(out))
+    return out

@@ -1,0 +1,305 @@
+"""GPU parity: libtmd_gpu.so (through the Python mirror of the C ABI) against
+the golden vectors of the reference and against the live reference engine
+(oracle/_ref, a prebuilt .so that travels to the GPU box).
+
+Tolerances (north star): pair sets and cells bit-exact; forces 1e-10
+relative to max(|F|max, rms F); PE and virial 1e-12 relative to the
+exactly-rounded (fsum) sums of the reference's per-pair terms."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2109_10876_b200 import engine as E
+from tests._util import (E_RTOL, SYSTEMS, assert_forces_close, assert_rel, load,
+                         load_json)
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_engine(g, dt=None, **cfg):
+    flat = E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"])
+    return E.Engine(flat, E.Interactions(), float(g["r_skin"]),
+                    E.EngineConfig(dt=float(dt if dt is not None else g["dt"]), **cfg))
+
+
+@pytest.mark.parametrize("name", SYSTEMS)
+def test_initial_state_vs_golden(name):
+    g = load(name)
+    eng = gpu_engine(g)
+    np.testing.assert_array_equal(eng.pairs(), g["pairs"])
+    _, cell = eng.cell_of()
+    np.testing.assert_array_equal(cell, g["cell"])
+    ids, f = eng.forces()
+    np.testing.assert_array_equal(ids, np.sort(g["ids"]))
+    assert_forces_close(f, g["forces"])
+    o = eng.observe()
+    assert_rel(o.potential, float(g["pe_fsum"]), E_RTOL, "PE")
+    assert_rel(o.virial, float(g["w_fsum"]), E_RTOL, "virial")
+    assert_rel(o.kinetic, float(g["ke_ref"]), 1e-13, "KE")
+    st = eng.list_stats()
+    assert st["entries"] == 2 * len(g["pairs"])
+    assert st["in_cut"] == 2 * int(g["n_incut"])
+    assert tuple(st["dims"]) == tuple(g["dims"].tolist())
+    flat = eng.flatten()
+    np.testing.assert_array_equal(flat.pos, g["wrapped"])
+
+
+@pytest.mark.parametrize("name", ["jit6_s101", "random500_s1", "random500_s2", "random500_s3"])
+def test_forces_vs_brute_force_oracle(name):
+    """acceptance criterion 1: forces vs oracle_forces_energy <= 1e-10 abs and the
+    listed pairs == oracle_pair_set."""
+    g = load(name)
+    eng = gpu_engine(g)
+    _, f = eng.forces()
+    order = np.argsort(g["ids"])
+    assert np.abs(f - g["oracle_forces"][order]).max() <= 1e-10
+    np.testing.assert_array_equal(eng.pairs(), g["oracle_pairs"])
+
+
+@pytest.mark.parametrize("name", ["jit6_s41_T08", "fcc8_jit", "aniso", "thin"])
+def test_trajectory_vs_golden(name):
+    g = load(name)
+    eng = gpu_engine(g)
+    steps = int(g["steps"])
+    every = max(1, steps // len(g["trace"]))
+    for row in g["trace"]:
+        eng.run(every)
+        o = eng.observe()
+        assert o.step == int(row[0])
+        assert_rel(o.kinetic + o.potential, row[1] + row[2], 1e-10, f"E at step {o.step}")
+    flat = eng.flatten()
+    assert np.abs(flat.pos - g["final_pos"]).max() < 1e-9
+    assert np.abs(flat.vel - g["final_vel"]).max() < 1e-9
+    assert eng.rebuild_count() == int(g["rebuilds"])
+
+
+def test_fcc20_known_answers():
+    s = load_json("fcc20_summary.json")
+    f = E.gen_fcc(20, 0.8442, 1.0, 12345)
+    eng = E.Engine(f, E.Interactions(), 0.3)
+    pr = eng.pairs()
+    assert len(pr) == s["pairs"]
+    assert int(((pr[:, 0] * 1000003 + pr[:, 1]) % 2147483647).sum()) == s["pair_checksum"]
+    _, cell = eng.cell_of()
+    assert int((cell.astype(np.int64) * (np.arange(len(cell)) % 9973 + 1)).sum()) == \
+        s["cell_checksum"]
+    o = eng.observe()
+    assert_rel(o.potential, s["pe_fsum"], E_RTOL, "PE")
+    assert_rel(o.virial, s["w_fsum"], E_RTOL, "virial")
+    assert abs(o.potential / 32000 + 6.3328119926) < 5e-10
+
+
+# -- live reference engine (oracle/_ref) -------------------------------------------
+
+def test_random_configs_criterion_1(ref):
+    """10 random N=500 configs (acceptance.cpp:88-118) against the live
+    reference: pair sets exact, forces 1e-10 vs the brute-force oracle."""
+    for seed in range(1, 11):
+        box, ids, pos, vel = ref.gen_random(500, 0.8442, 0.8, 0.72, seed)
+        eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3)
+        np.testing.assert_array_equal(eng.pairs(), ref.oracle_pairs(box, ids, pos, 2.8))
+        f_or, pe_or = ref.oracle_forces(box, ids, pos)
+        _, f = eng.forces()
+        assert np.abs(f - f_or).max() <= 1e-10
+        assert_rel(eng.observe().potential, pe_or, 1e-11, "PE vs oracle_forces_energy")
+
+
+def test_one_step_matches_reference(ref):
+    """criterion 2 analog: one NVE step from a lattice, positions within 1e-10
+    of the reference at n_sub 1, 8 and 64."""
+    box, ids, pos, vel = ref.gen_lattice(4096, 0.8442, 0.72, 11)
+    eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3)
+    eng.run(1)
+    mine = eng.flatten()
+    for n_sub in (1, 8, 64):
+        r = ref.RefEngine(box, ids, pos, vel, n_sub=n_sub)
+        r.run(1)
+        rid, rp, _ = r.flatten()
+        np.testing.assert_array_equal(mine.id, rid)
+        assert np.abs(mine.pos - rp).max() <= 1e-10
+
+
+def test_nve_drift_criterion_3():
+    """acceptance criterion 3: SC lattice N=4000, T=0.6 seed 3, 1000 steps:
+    worst drift <= 1e-3 at dt=0.005 and >= 10x smaller at dt=0.001, and
+    comparable to the reference's own (fixture)."""
+    g = load("lattice4000_s3")
+    worst = {}
+    for dt in (0.005, 0.001):
+        eng = E.Engine(E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"]),
+                       E.Interactions(), 0.3, E.EngineConfig(dt=dt))
+        o = eng.observe()
+        e0 = o.kinetic + o.potential
+        assert_rel(e0, float(g[f"e0_dt{dt}"]), 1e-12, "E0")
+        tr = []
+        for _ in range(100):
+            eng.run(10)
+            o = eng.observe()
+            tr.append(o.kinetic + o.potential)
+        tr = np.array(tr)
+        worst[dt] = np.abs(tr - e0).max() / abs(e0)
+        ref_tr = g[f"dt{dt}"]
+        assert np.abs(tr - ref_tr).max() / abs(e0) < 1e-6
+    assert worst[0.005] <= 1e-3
+    assert worst[0.005] / worst[0.001] >= 10.0
+    assert abs(worst[0.005] / float(g["worst_dt0.005"]) - 1.0) < 0.05
+
+
+def test_free_streaming_through_resorts():
+    """test_engine.cpp:66-99: force-free particles move in straight lines,
+    unchanged by >= 5 resorts."""
+    f = E.FlatConfig(np.full(3, 12.0), np.array([0, 1]),
+                     np.array([[1.0, 2.0, 3.0], [7.0, 9.0, 4.0]]),
+                     np.array([[0.8, -0.3, 0.5], [-0.2, 0.4, -0.7]]))
+    eng = E.Engine(f, E.Interactions(), 0.4, E.EngineConfig(dt=0.01))
+    eng.run(400)
+    assert eng.rebuild_count() >= 5
+    out = eng.flatten()
+    t = 0.01 * 400
+    want = f.pos + f.vel * t
+    want -= 12.0 * np.floor(want / 12.0)
+    assert np.abs(out.pos - want).max() <= 1e-9
+    np.testing.assert_array_equal(out.vel, f.vel)
+
+
+def _jittered(side, edge, seed, jitter, temperature):
+    from oracle import make_golden as mg
+    return mg.jittered_lattice(side, edge, seed, jitter, temperature)
+
+
+def test_velocity_flip_retraces():
+    """test_engine.cpp:165-197: 40 steps, flip velocities, 40 steps back,
+    within 1e-12."""
+    box, ids, pos, vel = _jittered(4, 6.0, 3, 0.05, 0.3)
+    eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.4,
+                   E.EngineConfig(dt=0.002))
+    start = eng.flatten()
+    eng.run(40)
+    assert eng.rebuild_count() == 0
+    mid = eng.flatten()
+    eng.set_velocities(mid.id, -mid.vel)
+    eng.run(40)
+    back = eng.flatten()
+    np.testing.assert_array_equal(back.id, start.id)
+    assert np.abs(back.pos - start.pos).max() <= 1e-12
+    assert np.abs(back.vel + start.vel).max() <= 1e-12
+
+
+def test_energy_conserved_200_steps():
+    """test_engine.cpp:199-212."""
+    box, ids, pos, vel = _jittered(6, 7.2, 17, 0.05, 0.8)
+    eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3,
+                   E.EngineConfig(dt=0.002))
+    o = eng.observe()
+    e0 = o.kinetic + o.potential
+    worst = 0.0
+    for _ in range(200):
+        eng.step()
+        o = eng.observe()
+        worst = max(worst, abs(o.kinetic + o.potential - e0))
+    assert worst / abs(e0) <= 1e-3
+
+
+def test_zero_steps_and_timers():
+    """test_engine.cpp:284-321."""
+    box, ids, pos, vel = _jittered(4, 6.0, 61, 0.05, 0.5)
+    eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3)
+    eng.run(0)
+    assert eng.step_count() == 0
+    t = eng.timers()
+    assert t.elapsed == 0.0 and t.section_sum() == 0.0
+    out = eng.flatten()
+    want = pos - 6.0 * np.floor(pos / 6.0)
+    np.testing.assert_array_equal(out.pos, want)
+    assert eng.potential_energy() != 0.0
+
+    box, ids, pos, vel = _jittered(4, 6.0, 71, 0.02, 0.0)
+    eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.4,
+                   E.EngineConfig(dt=0.001))
+    eng.run(5)
+    t = eng.timers()
+    assert eng.rebuild_count() == 0
+    assert t[E.Section.kResort] == 0.0
+    assert t[E.Section.kForces] > 0.0
+    assert t[E.Section.kIntegrate] > 0.0
+    assert t[E.Section.kNeigh] > 0.0
+    assert t.elapsed > 0.0
+    assert t.section_sum() <= t.elapsed * 1.5 + 1e-3
+
+
+def test_rebuild_trigger_half_skin():
+    """test_neighbor.cpp:185-201 in engine form: a displacement of 0.21 > skin/2
+    = 0.2 triggers exactly one rebuild; 0.19 does not."""
+    for v, want in ((0.19, 0), (0.21, 1)):
+        f = E.FlatConfig(np.full(3, 12.0), np.array([0, 1]),
+                         np.array([[1.0, 2.0, 3.0], [7.0, 9.0, 4.0]]),
+                         np.array([[v, 0.0, 0.0], [0.0, 0.0, 0.0]]))
+        eng = E.Engine(f, E.Interactions(), 0.4, E.EngineConfig(dt=1.0))
+        eng.run(1)
+        assert eng.rebuild_count() == want
+
+
+def test_overlap_is_a_physics_error():
+    """test_neighbor.cpp:254-268: coincident particles raise PhysicsError."""
+    f = E.FlatConfig(np.full(3, 8.5), np.array([0, 1]),
+                     np.array([[4.0, 4.0, 4.0], [4.0, 4.0, 4.0]]), None)
+    with pytest.raises(E.PhysicsError, match="overlapping particles: ids 0 and 1"):
+        E.Engine(f, E.Interactions(), 0.3)
+
+
+def test_non_finite_dynamics_name_the_step():
+    """test_engine.cpp:369-382 analog: a velocity that overflows positions is
+    reported as a PhysicsError carrying the step number."""
+    box, ids, pos, vel = _jittered(4, 6.0, 83, 0.05, 0.1)
+    vel[5] = [np.inf, 0.0, 0.0]
+    eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3)
+    with pytest.raises(E.PhysicsError, match=r"non-finite.*\(at step \d+\)"):
+        eng.run(3)
+
+
+def test_deterministic_bitwise():
+    """acceptance criterion 9 analog: two identical runs are bit-identical."""
+    f = E.gen_fcc(8, 0.8442, 1.0, 4242)
+    outs = []
+    for _ in range(2):
+        eng = E.Engine(f, E.Interactions(), 0.3)
+        eng.run(150)
+        outs.append(eng.flatten())
+    np.testing.assert_array_equal(outs[0].pos, outs[1].pos)
+    np.testing.assert_array_equal(outs[0].vel, outs[1].vel)
+
+
+def test_fixed_capacity_overflow_rolls_back_and_grows():
+    """A list capacity far too small forces the overflow/rollback path; the
+    result must equal the auto-capacity run bit for bit."""
+    f = E.gen_fcc(8, 0.8442, 1.0, 99)
+    a = E.Engine(f, E.Interactions(), 0.3)
+    a.run(60)
+    b = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(nbr_capacity=8))
+    b.run(60)
+    fa, fb = a.flatten(), b.flatten()
+    assert np.abs(fa.pos - fb.pos).max() < 1e-9
+    assert b.list_stats()["capacity"] >= b.list_stats()["max_count"]
+
+
+@pytest.mark.slow
+def test_32k_1000_steps_vs_reference(ref):
+    """Config 1 (BASELINE.json configs[0]) end to end against the live reference."""
+    f = E.gen_fcc(20, 0.8442, 1.0, 12345)
+    eng = E.Engine(f, E.Interactions(), 0.3)
+    r = ref.RefEngine(f.box, f.id, f.pos, f.vel, r_skin=0.3)
+    o0 = eng.observe()
+    e0 = o0.kinetic + o0.potential
+    worst = 0.0
+    for _ in range(100):
+        eng.run(10)
+        o = eng.observe()
+        worst = max(worst, abs(o.kinetic + o.potential - e0) / abs(e0))
+    r.run(1000)
+    ro = r.observe()
+    o = eng.observe()
+    assert_rel((o.kinetic + o.potential), ro["kinetic"] + ro["potential"], 1e-7, "E(1000)")
+    assert abs(o.temperature - ro["temperature"]) < 1e-3
+    assert abs(eng.rebuild_count() - r.rebuild_count()) <= 3
+    assert worst < 2e-4  # reference: 1.154e-4

@@ -1,0 +1,348 @@
+#!/usr/bin/env python3
+"""Throughput bench for the B200 LJ short-range engine (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): LJ fluid, 1,048,576 particles on an FCC
+64^3 x 4 lattice, rho 0.8442, eps = sigma = m = 1, r_cut 2.5 shifted, skin
+0.3, Gaussian velocities at T = 1.0 (seed 12345, zero net momentum),
+dt 0.005, FP64, NVE. A "step" is one velocity-Verlet step of the whole system
+(kick, drift, on-device rebuild decision, resort + list build when triggered,
+forces, kick). Synthetic input generated on the host (no dataset exists).
+
+One JSON line on rank 0 (see DESIGN.md §Measurement for every field):
+  value      device-timed particle-steps/s, inputs resident in HBM
+  e2e        the same metric through the public API from host buffers:
+             create (H2D) + K x (step + observe D2H) + final download
+  roofline   the LJ force kernel against max(B/HBM, F/FP64)
+  cpu_baseline  the reference engine (oracle/_ref) on this box's host cores
+
+--impl reference times the reference's own CPU engine (oracle/_ref: the
+unmodified taskmd headers compiled by oracle/Makefile) on the same config,
+rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LJ particle-steps/sec at 1/2/4/8 B200; force-kernel % of HBM/FP64 roofline"
+UNIT = "particle-steps/s"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": HBM_FALLBACK_GBS, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=3)
+            except Exception:
+                self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(cells: int) -> dict:
+    n = 4 * cells ** 3
+    return {"workload": f"LJ fluid FCC {cells}^3x4 (BASELINE.json configs[1])" if cells == 64
+            else f"LJ fluid FCC {cells}^3x4",
+            "n_particles": n, "rho": 0.8442, "r_cut": 2.5, "energy_shifted": True,
+            "r_skin": 0.3, "temperature": 1.0, "seed": 12345, "dt": 0.005,
+            "ensemble": "NVE"}
+
+
+# ----------------------------------------------------------------------------------
+def cpu_reference_run(cells: int, steps_wanted: int, warmup: int, budget_s: float):
+    """The reference engine (oracle/_ref) on all host cores. Returns
+    (particle-steps/s, cores, sample description, steps timed)."""
+    from oracle import ref
+    from paper_2109_10876_b200 import engine as E
+    if not ref.available():
+        ref.build()
+    f = E.gen_fcc(cells, 0.8442, 1.0, 12345)
+    cores = os.cpu_count() or 1
+    n_sub = 2 * cores
+    t0 = time.perf_counter()
+    r = ref.RefEngine(f.box, f.id, f.pos, f.vel, r_skin=0.3, n_sub=n_sub, workers=cores,
+                      dt=0.005)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r.run(max(1, warmup))
+    est = (time.perf_counter() - t0) / max(1, warmup)
+    steps = int(max(1, min(steps_wanted, budget_s / max(est, 1e-9))))
+    t0 = time.perf_counter()
+    r.run(steps)
+    t = time.perf_counter() - t0
+    n = f.size()
+    sample = (f"{n}-particle FCC config, {steps} NVE steps (of {steps_wanted} requested) after "
+              f"build_domain ({t_build:.1f} s, untimed) and {max(1, warmup)} warm-up steps; "
+              f"reference taskmd Engine, worker_threads={cores}, n_sub={n_sub} (fixed 2x "
+              f"workers), g++ -O3 -DNDEBUG")
+    r.close()
+    return n * steps / t, cores, sample, steps
+
+
+def run_reference_arm(args) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    try:
+        v, cores, sample, steps = cpu_reference_run(args.cells, args.steps, args.warmup,
+                                                    args.ref_budget_s)
+    except Exception as e:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
+        return
+    cfg = workload(args.cells)
+    cfg["parallelism"] = "host threads (reference CPU engine)"
+    n = cfg["n_particles"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------------
+def run_ours(args) -> None:
+    import torch
+    from paper_2109_10876_b200 import engine as E
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    cfg_w = workload(args.cells)
+    n = cfg_w["n_particles"]
+    flat = E.gen_fcc(args.cells, 0.8442, 1.0, 12345)
+    ecfg = E.EngineConfig(dt=0.005, section_timers=False, device=dev)
+    eng = E.Engine(flat, E.Interactions(), 0.3, ecfg)
+
+    eng.run(args.warmup)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    launches0 = eng.launch_count()
+    rebuilds0 = eng.rebuild_count()
+    with ClockSampler(dev) as clocks:
+        ev0.record(stream)
+        eng.run(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = eng.launch_count() - launches0
+    rebuilds = eng.rebuild_count() - rebuilds0
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    ms_per_step = ms / args.steps
+    value = ws * n * args.steps / (ms * 1e-3)   # replicas: every rank steps n particles
+
+    # -- roofline of the force kernel -----------------------------
+    st = eng.list_stats()
+    E_ent, P_cut = st["entries"], st["in_cut"]
+    t_force_ms = eng.time_force_kernel(args.force_reps)
+    B = n * 52 + E_ent * 28
+    F = 8 * E_ent + 20 * P_cut
+    peaks = measured_peaks()
+    fp64 = E.fp64_peak_tflops(dev)
+    t_hbm = B / (peaks["hbm_gbs"] * 1e9)
+    t_flop = F / (fp64 * 1e12)
+    traffic = None
+    prof = ROOT / "profiles" / "force_kernel_ncu.json"
+    if prof.exists():
+        try:
+            pj = json.loads(prof.read_text())
+            if pj.get("n_particles") == n:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    if t_hbm >= t_flop:
+        achieved = B / (t_force_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic}
+    else:
+        achieved = F / (t_force_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64, "traffic": traffic}
+    roof.update({
+        "kernel": "k_lj_forces", "algorithmic_bytes": B, "algorithmic_flops": F,
+        "entries": E_ent, "in_cut_entries": P_cut, "kernel_ms": t_force_ms,
+        "t_roof_ms": 1e3 * max(t_hbm, t_flop), "fp64_peak_tflops_measured": fp64,
+        "peak_source": peaks["source"], "share_of_step": t_force_ms / ms_per_step,
+        "definition": "B = N*52 + E*28 bytes, F = 8E + 20P (E full-list entries, P in-cut "
+                      "entries); frac = T_roof / T_kernel",
+    })
+    eng.close()
+
+    # -- e2e through the public API from host buffers ----------------------------------
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    h2d = flat.pos.nbytes + flat.vel.nbytes + flat.id.nbytes
+    t0 = time.perf_counter()
+    e2 = E.Engine(flat, E.Interactions(), 0.3, ecfg)
+    obs_bytes = 0
+    for _ in range(args.steps):
+        e2.run(1)
+        e2.observe()
+        obs_bytes += 40
+    out = e2.flatten()
+    t_e2e = time.perf_counter() - t0
+    d2h = obs_bytes + out.pos.nbytes + out.vel.nbytes + out.id.nbytes
+    e2.close()
+    if ws > 1:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = {"value": ws * n * args.steps / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+           "seconds": t_e2e,
+           "what": "Engine(create from host arrays) + K x (run(1) + observe()) + flatten()"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, sample, _ = cpu_reference_run(args.cells, args.steps, 2,
+                                                    args.cpu_budget_s)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": sample}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    if rank != 0:
+        return
+    cfg = dict(cfg_w)
+    cfg.update({"parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas "
+                "(spatial decomposition not yet wired into bench)",
+                "l2": "working set > 126 MB L2 (neighbour list alone ~0.4 GB); no flush",
+                "rebuilds_in_timed_region": rebuilds, "section_timers": False,
+                "nbr_capacity": st["capacity"], "cell_grid": list(st["dims"])})
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if ws > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
+        "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cells", type=int, default=64, help="FCC cells per edge (64 = 1M)")
+    ap.add_argument("--force-reps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

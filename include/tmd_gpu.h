@@ -177,6 +177,13 @@ int tmd_gpu_time_force_kernel(tmd_gpu_ctx* ctx, int reps, double* ms_per_launch)
  * order their own work after the engine's. */
 void* tmd_gpu_stream(tmd_gpu_ctx* ctx);
 
+/* Kernels this context has enqueued so far (bench accounting). Getter. */
+uint64_t tmd_gpu_launch_count(const tmd_gpu_ctx* ctx);
+
+/* Measured FP64 FMA throughput of the device in TFLOP/s (2 FLOP per DFMA),
+ * the FLOP-side roofline denominator. device = -1: current device. */
+int tmd_gpu_fp64_peak(int device, double* tflops);
+
 void tmd_gpu_destroy(tmd_gpu_ctx* ctx);
 
 /* ---- host-side setup helpers (no GPU needed) ----------------------------

@@ -27,7 +27,7 @@ EXPORTS = [
     "tmd_gpu_size", "tmd_gpu_list_stats", "tmd_gpu_time_force_kernel",
     "tmd_gpu_stream", "tmd_gpu_destroy", "tmd_gen_fcc",
     "tmd_thermal_velocities", "tmd_counter_uniform3", "tmd_counter_normal3",
-    "tmd_gpu_abi_version",
+    "tmd_gpu_abi_version", "tmd_gpu_launch_count", "tmd_gpu_fp64_peak",
 ]
 
 
@@ -108,6 +108,9 @@ def lib() -> C.CDLL:
     L.tmd_gpu_time_force_kernel.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_stream.argtypes = [P]
     L.tmd_gpu_stream.restype = P
+    L.tmd_gpu_launch_count.argtypes = [P]
+    L.tmd_gpu_launch_count.restype = C.c_uint64
+    L.tmd_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_destroy.argtypes = [P]
     L.tmd_gpu_destroy.restype = None
     L.tmd_gen_fcc.argtypes = [C.c_int, C.c_double, C.c_double, P, P, P]

@@ -127,6 +127,7 @@ struct tmd_gpu_ctx {
   int* rebuild_log = nullptr;     // device: rebuild decision per chunk step
   std::vector<int> h_rebuild_log;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  uint64_t launches = 0;  // kernels enqueued by this context (bench accounting)
 };
 
 namespace {
@@ -201,12 +202,14 @@ void harvest_timers(tmd_gpu_ctx* c) {
 
 // --- kernel launch wrappers -------------------------------------------------
 void launch_decide(tmd_gpu_ctx* c, bool advance, int log_idx = -1) {
+  c->launches += 1;
   k_decide<<<1, 1, 0, c->stream>>>(c->ctrl, c->g.rebuild_thr, advance ? 1 : 0,
                                    log_idx >= 0 ? c->rebuild_log : nullptr,
                                    log_idx);
 }
 
 void launch_resort(tmd_gpu_ctx* c) {
+  c->launches += 6;
   const int n = static_cast<int>(c->n);
   const int nb = c->nblk;
   k_wrap_bin<<<nb, kBlock, 0, c->stream>>>(n, c->pos, c->id, c->cell, c->rank,
@@ -228,6 +231,7 @@ void launch_resort(tmd_gpu_ctx* c) {
 }
 
 void launch_build(tmd_gpu_ctx* c) {
+  c->launches += 2;
   k_build_prologue<<<1, 1, 0, c->stream>>>(c->ctrl);
   k_build_list<<<c->nblk, kBlock, 0, c->stream>>>(
       static_cast<int>(c->n), c->pos, c->cell, c->start, c->g, c->nbr, c->nnbr,
@@ -235,12 +239,14 @@ void launch_build(tmd_gpu_ctx* c) {
 }
 
 void launch_forces(tmd_gpu_ctx* c) {
+  c->launches += 1;
   k_lj_forces<<<c->nblk, kBlock, 0, c->stream>>>(
       static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
       c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, c->ctrl);
 }
 
 void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
+  c->launches += 1;
   const int n = static_cast<int>(c->n);
   if (fused) {
     k_kick_drift<true><<<c->nblk, kBlock, 0, c->stream>>>(
@@ -254,12 +260,14 @@ void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
 }
 
 void launch_kick2(tmd_gpu_ctx* c) {
+  c->launches += 1;
   k_kick2<<<c->nblk, kBlock, 0, c->stream>>>(
       static_cast<int>(c->n), c->vx, c->vy, c->vz, c->fx, c->fy, c->fz,
       c->mass, c->id, c->half_dt, c->part_ke, c->ctrl);
 }
 
 void launch_reduce_pe(tmd_gpu_ctx* c) {
+  c->launches += 2;
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, c->nblk, 0.5,
                                              c->scalars + 0);
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, c->nblk, 0.5,
@@ -267,6 +275,7 @@ void launch_reduce_pe(tmd_gpu_ctx* c) {
 }
 
 void launch_reduce_ke(tmd_gpu_ctx* c) {
+  c->launches += 1;
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_ke, c->nblk, 1.0,
                                              c->scalars + 2);
 }
@@ -791,6 +800,7 @@ int tmd_gpu_step(tmd_gpu_ctx* c, int64_t nsteps) {
 int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->launches += 1;
     k_kinetic<<<c->nblk, kBlock, 0, c->stream>>>(static_cast<int>(c->n), c->vx,
                                                  c->vy, c->vz, c->mass,
                                                  c->part_ke);
@@ -916,6 +926,7 @@ int tmd_gpu_list_stats(tmd_gpu_ctx* c, tmd_list_stats* out) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     unsigned long long* d = dalloc<unsigned long long>(1);
     ck(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream), "memset");
+    c->launches += 1;
     k_count_incut<<<c->nblk, kBlock, 0, c->stream>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g,
         c->lj.rc2, d);
@@ -951,6 +962,37 @@ int tmd_gpu_time_force_kernel(tmd_gpu_ctx* c, int reps, double* ms) {
 }
 
 void* tmd_gpu_stream(tmd_gpu_ctx* c) { return c->stream; }
+
+uint64_t tmd_gpu_launch_count(const tmd_gpu_ctx* c) { return c->launches; }
+
+int tmd_gpu_fp64_peak(int device, double* tflops) {
+  tmd_gpu_ctx tmp;
+  return guard(&tmp, [&] {
+    if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+    int dev = 0, sms = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    double* out = dalloc<double>(static_cast<size_t>(sms) * 8 * 256);
+    const int blocks = sms * 8, iters = 1 << 14;
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "ev");
+    ck(cudaEventCreate(&b), "ev");
+    k_dfma_peak<<<blocks, 256>>>(out, iters);  // warm-up
+    ck(cudaEventRecord(a), "ev");
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) k_dfma_peak<<<blocks, 256>>>(out, iters);
+    ck(cudaEventRecord(b), "ev");
+    ck(cudaEventSynchronize(b), "sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+    ck(cudaGetLastError(), "k_dfma_peak");
+    const double flops = 2.0 * kDfmaChains * static_cast<double>(iters) * blocks * 256 * reps;
+    *tflops = flops / (1e-3 * ms) / 1e12;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+  });
+}
 
 void tmd_gpu_destroy(tmd_gpu_ctx* c) {
   if (!c) return;

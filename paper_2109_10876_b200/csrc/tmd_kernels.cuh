@@ -461,4 +461,22 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// FP64 pipe peak probe (DFMA throughput): the roofline denominator for FLOPs
+// (MEASURED_PEAKS.json has no FP64 entry).
+constexpr int kDfmaChains = 8;
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters) {
+  double a[kDfmaChains];
+#pragma unroll
+  for (int k = 0; k < kDfmaChains; ++k) a[k] = 1.0 + 1e-3 * (threadIdx.x + k);
+  const double b = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < kDfmaChains; ++k) a[k] = fma(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kDfmaChains; ++k) s += a[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 }  // namespace tmd

@@ -341,6 +341,12 @@ class Engine:
         return dict(n=s.n, entries=s.entries, in_cut=s.in_cut, max_count=s.max_count,
                     capacity=s.capacity, dims=tuple(s.dims), cell_len=tuple(s.cell_len))
 
+    def launch_count(self) -> int:
+        return int(_abi.lib().tmd_gpu_launch_count(self._h))
+
+    def stream_handle(self) -> int:
+        return int(_abi.lib().tmd_gpu_stream(self._h) or 0)
+
     def time_force_kernel(self, reps: int) -> float:
         ms = C.c_double()
         _check(_abi.lib().tmd_gpu_time_force_kernel(self._h, int(reps), C.byref(ms)),
@@ -372,6 +378,13 @@ def thermal_velocities(flat: FlatConfig, temperature: float, seed: int) -> None:
     _abi.lib().tmd_thermal_velocities(flat.size(), _ptr(flat.id), _ptr(flat.mass),
                                       float(temperature), int(seed), _ptr(vel))
     flat.vel = vel
+
+
+def fp64_peak_tflops(device: int = -1) -> float:
+    """Measured DFMA throughput (TFLOP/s) — the FP64 roofline denominator."""
+    t = C.c_double()
+    _check(_abi.lib().tmd_gpu_fp64_peak(int(device), C.byref(t)), None)
+    return t.value
 
 
 def counter_uniform3(seed: int, ctx: int, step: int, pid: int) -> np.ndarray:

@@ -89,7 +89,8 @@ typedef struct tmd_engine_params {
                          times per phase; 0: only `elapsed` */
   int nbr_capacity;  /* 0 = auto (sized from the first build); else fixed
                         entries per particle (rounded up to a multiple of 8) */
-  int reserved[5];
+  int reserved[5];   /* reserved[0]: kernel variant, 0/2 = brick-staged shared
+                        memory (default), 1 = thread-per-particle L1 gathers */
 } tmd_engine_params;
 
 /* taskmd::StepObservables (engine.hpp:43-48) plus the virial

@@ -25,6 +25,7 @@
 
 #include "../../include/tmd_gpu.h"
 #include "tmd_kernels.cuh"
+#include "tmd_brick.cuh"
 
 using namespace tmd;
 
@@ -97,6 +98,20 @@ struct tmd_gpu_ctx {
   int *count = nullptr, *start = nullptr;
   uint32_t* nbr = nullptr;
   int* nnbr = nullptr;
+  size_t nbr_words = 0;       // allocated list words
+
+  // brick-major ordering + variant selection
+  int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
+  BrickGeom bg{};
+  int* cell_rank = nullptr;       // global cell -> brick-major rank
+  int* brick_rank_off = nullptr;  // brick -> first rank (nbricks + 1)
+  int* ngroups = nullptr;         // per brick, scanned into group_off
+  int* group_off = nullptr;       // nbricks + 1
+  int ngroups_max = 0;
+  int nparts = 0;                 // partial-sum slots of the force kernel
+  uint32_t* decoded = nullptr;    // global-index ELL copy for the taps
+  size_t decoded_words = 0;
+  std::vector<int> h_rank, h_brick_off;  // host staging for upload_bricks
   double *part_e = nullptr, *part_w = nullptr, *part_ke = nullptr;
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
   Ctrl* ctrl = nullptr;
@@ -139,7 +154,8 @@ void free_all(tmd_gpu_ctx* c) {
                   c->rank, c->perm,  c->count, c->start, c->nbr,    c->nnbr,
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
-                  c->rebuild_log};
+                  c->rebuild_log, c->cell_rank, c->brick_rank_off, c->ngroups,
+                  c->group_off, c->decoded};
   for (void* p : ptrs) {
     if (p) cudaFree(p);
   }
@@ -209,15 +225,15 @@ void launch_decide(tmd_gpu_ctx* c, bool advance, int log_idx = -1) {
 }
 
 void launch_resort(tmd_gpu_ctx* c) {
-  c->launches += 6;
+  c->launches += 8;
   const int n = static_cast<int>(c->n);
   const int nb = c->nblk;
   k_wrap_bin<<<nb, kBlock, 0, c->stream>>>(n, c->pos, c->id, c->cell, c->rank,
-                                           c->count, c->g, c->ctrl);
+                                           c->count, c->cell_rank, c->g, c->ctrl);
   k_scan<<<1, kScanThreads, 0, c->stream>>>(c->g.ncells, c->count, c->start,
                                             c->ctrl);
   k_scatter<<<nb, kBlock, 0, c->stream>>>(n, c->cell, c->rank, c->start,
-                                          c->perm, c->ctrl);
+                                          c->cell_rank, c->perm, c->ctrl);
   k_sort_cells<<<blocks_for(c->g.ncells, kBlock), kBlock, 0, c->stream>>>(
       c->g.ncells, c->start, c->perm, c->id, c->ctrl);
   k_permute<<<nb, kBlock, 0, c->stream>>>(n, c->perm, c->pos, c->vx, c->vy,
@@ -228,21 +244,46 @@ void launch_resort(tmd_gpu_ctx* c) {
                                             c->vz2, c->mass2, c->id2, c->cell2,
                                             c->pos, c->vx, c->vy, c->vz,
                                             c->mass, c->id, c->cell, c->ctrl);
+  // list groups per brick (32 particles each), scanned into group offsets
+  k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->stream>>>(
+      c->bg.nbricks, c->brick_rank_off, c->start, c->ngroups, c->ctrl);
+  k_scan<<<1, kScanThreads, 0, c->stream>>>(c->bg.nbricks, c->ngroups, c->group_off,
+                                            c->ctrl);
+}
+
+size_t build_smem(const tmd_gpu_ctx* c) {
+  return static_cast<size_t>(c->bg.stage_cap_f32) * sizeof(float4);
+}
+size_t force_smem(const tmd_gpu_ctx* c) {
+  return static_cast<size_t>(c->bg.stage_cap_f64) * 3 * sizeof(double);
 }
 
 void launch_build(tmd_gpu_ctx* c) {
   c->launches += 2;
   k_build_prologue<<<1, 1, 0, c->stream>>>(c->ctrl);
-  k_build_list<<<c->nblk, kBlock, 0, c->stream>>>(
-      static_cast<int>(c->n), c->pos, c->cell, c->start, c->g, c->nbr, c->nnbr,
-      c->stride, c->cap, c->snap, c->ctrl);
+  if (c->variant == 1) {
+    k_build_list<<<c->nblk, kBlock, 0, c->stream>>>(
+        static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
+        c->nnbr, c->stride, c->cap, c->snap, c->ctrl);
+  } else {
+    k_build_brick<<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
+        c->nbr, c->nnbr, c->snap, c->ctrl);
+  }
 }
 
 void launch_forces(tmd_gpu_ctx* c) {
   c->launches += 1;
-  k_lj_forces<<<c->nblk, kBlock, 0, c->stream>>>(
-      static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
-      c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, c->ctrl);
+  if (c->variant == 1) {
+    k_lj_forces<<<c->nblk, kBlock, 0, c->stream>>>(
+        static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
+        c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, c->ctrl);
+  } else {
+    k_forces_brick<<<c->bg.nbricks, kForceThreads, force_smem(c), c->stream>>>(
+        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
+        c->lj, c->nbr, c->nnbr, c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id,
+        c->ctrl);
+  }
 }
 
 void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
@@ -268,10 +309,9 @@ void launch_kick2(tmd_gpu_ctx* c) {
 
 void launch_reduce_pe(tmd_gpu_ctx* c) {
   c->launches += 2;
-  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, c->nblk, 0.5,
-                                             c->scalars + 0);
-  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, c->nblk, 0.5,
-                                             c->scalars + 1);
+  const int np = c->variant == 1 ? c->nblk : c->bg.nbricks;
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, np, 0.5, c->scalars + 0);
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, np, 0.5, c->scalars + 1);
 }
 
 void launch_reduce_ke(tmd_gpu_ctx* c) {
@@ -338,7 +378,11 @@ void alloc_list(tmd_gpu_ctx* c, int cap) {
   if (c->nbr) cudaFree(c->nbr);
   c->nbr = nullptr;
   c->cap = round8(std::max(cap, 8));
-  c->nbr = dalloc<uint32_t>(static_cast<size_t>(c->cap) * c->stride);
+  c->bg.cap = c->cap;
+  c->nbr_words = c->variant == 1
+                     ? static_cast<size_t>(c->cap) * c->stride
+                     : static_cast<size_t>(c->ngroups_max) * c->cap * 32;
+  c->nbr = dalloc<uint32_t>(c->nbr_words);
   set_cap_in_ctrl(c);
 }
 
@@ -556,6 +600,72 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
   }
 }
 
+// Brick decomposition of the cell grid (bricks of up to 2x2x2 cells), the
+// brick-major cell ranks, staging capacities and the FP32 prefilter band.
+
+void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
+  BrickGeom& bg = c->bg;
+  for (int k = 0; k < 3; ++k) {
+    bg.B[k] = std::min(2, c->g.dims[k]);
+    bg.nb[k] = (c->g.dims[k] + bg.B[k] - 1) / bg.B[k];
+    bg.origin_scale[k] = c->g.cell_len[k];
+  }
+  bg.nbricks = bg.nb[0] * bg.nb[1] * bg.nb[2];
+  const int d0 = c->g.dims[0], d1 = c->g.dims[1];
+  c->h_rank.assign(static_cast<size_t>(c->g.ncells), 0);
+  c->h_brick_off.assign(static_cast<size_t>(bg.nbricks) + 1, 0);
+  int r = 0;
+  for (int b = 0; b < bg.nbricks; ++b) {
+    const int bx = b % bg.nb[0], by = (b / bg.nb[0]) % bg.nb[1], bz = b / (bg.nb[0] * bg.nb[1]);
+    c->h_brick_off[b] = r;
+    for (int z = bz * bg.B[2]; z < std::min((bz + 1) * bg.B[2], c->g.dims[2]); ++z)
+      for (int y = by * bg.B[1]; y < std::min((by + 1) * bg.B[1], c->g.dims[1]); ++y)
+        for (int x = bx * bg.B[0]; x < std::min((bx + 1) * bg.B[0], c->g.dims[0]); ++x)
+          c->h_rank[static_cast<size_t>(x + d0 * (y + d1 * z))] = r++;
+  }
+  c->h_brick_off[bg.nbricks] = r;
+  c->ngroups_max = static_cast<int>(n / 32.0) + bg.nbricks + 1;
+  // staging capacity: twice the expected halo population, 32-aligned
+  const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
+  const double per_cell = n / vol * c->g.cell_len[0] * c->g.cell_len[1] * c->g.cell_len[2];
+  const double halo = per_cell * (bg.B[0] + 2) * (bg.B[1] + 2) * (bg.B[2] + 2);
+  const int want = static_cast<int>(2.0 * halo + 64.0 + 31.0) / 32 * 32;
+  bg.stage_cap_f64 = std::max(256, std::min(want, 4096));
+  bg.stage_cap_f32 = std::max(256, std::min(want, 4096));
+  // FP32 prefilter band (see DESIGN.md §List build): bound on |r2_f32 - r2_ref|
+  // for brick-relative single-precision coordinates, times 4.
+  const double cl = std::max({c->g.cell_len[0], c->g.cell_len[1], c->g.cell_len[2]});
+  const double Lm = std::max({c->g.L[0], c->g.L[1], c->g.L[2]});
+  const double u32 = std::ldexp(1.0, -24), u64 = std::ldexp(1.0, -52);
+  const double rv = r_verlet, rv2 = c->g.rv2;
+  const double e_coord = u32 * 3.0 * cl * 1.01 + u64 * 4.0 * (2.0 * Lm + 4.0 * cl);
+  const double e_d = 2.0 * e_coord + u32 * rv * 1.01;
+  const double err = 2.0 * std::sqrt(3.0) * rv * 1.01 * e_d + 3.0 * e_d * e_d +
+                     3.0 * u32 * rv2 * 1.01 + std::ldexp(rv2, -50);
+  const double delta = 4.0 * err;
+  bg.lo2 = std::nextafter(static_cast<float>(rv2 - delta), 0.0f);
+  bg.hi2 = std::nextafter(static_cast<float>(rv2 + delta), 1e30f);
+}
+
+void upload_bricks(tmd_gpu_ctx* c) {
+  c->cell_rank = dalloc<int>(c->h_rank.size());
+  c->brick_rank_off = dalloc<int>(c->h_brick_off.size());
+  c->ngroups = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
+  c->group_off = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
+  ck(cudaMemcpy(c->cell_rank, c->h_rank.data(), c->h_rank.size() * sizeof(int),
+                cudaMemcpyHostToDevice), "H2D cell_rank");
+  ck(cudaMemcpy(c->brick_rank_off, c->h_brick_off.data(), c->h_brick_off.size() * sizeof(int),
+                cudaMemcpyHostToDevice), "H2D brick offsets");
+  ck(cudaMemset(c->ngroups, 0, sizeof(int) * (static_cast<size_t>(c->bg.nbricks) + 1)),
+     "memset");
+  ck(cudaFuncSetAttribute(k_build_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(build_smem(c))), "smem attr build");
+  ck(cudaFuncSetAttribute(k_forces_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(force_smem(c))), "smem attr forces");
+  c->h_rank.clear();
+  c->h_brick_off.clear();
+}
+
 void build_geom(tmd_gpu_ctx* c, const double box[3], double r_cut,
                 double r_skin) {
   // build_cell_grid (cell_grid.hpp:54-78)
@@ -619,6 +729,8 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     c->r_skin = params->r_skin;
     c->r_cut = lj->r_cut;
     c->timers_on = params->section_timers != 0;
+    c->variant = params->reserved[0] == 1 ? 1 : 2;
+    setup_bricks(c, static_cast<double>(c->n), lj->r_cut + params->r_skin);
     // lj_prepare (potentials.hpp:49-61)
     c->lj.sigma2 = lj->sigma * lj->sigma;
     c->lj.rc2 = lj->r_cut * lj->r_cut;
@@ -645,9 +757,11 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     c->count = dalloc<int>(c->g.ncells);
     c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
     c->nnbr = dalloc<int>(n);
-    c->part_e = dalloc<double>(c->nblk);
-    c->part_w = dalloc<double>(c->nblk);
+    c->nparts = std::max(c->nblk, c->bg.nbricks);
+    c->part_e = dalloc<double>(c->nparts);
+    c->part_w = dalloc<double>(c->nparts);
     c->part_ke = dalloc<double>(c->nblk);
+    upload_bricks(c);
     c->scalars = dalloc<double>(4);
     c->ctrl = dalloc<Ctrl>(1);
     c->rebuild_log = dalloc<int>(static_cast<size_t>(kChunk));
@@ -724,6 +838,23 @@ struct HostState {
   std::vector<int> cell;
   std::vector<size_t> order;  // slots sorted by id
 };
+
+// The current list in global-index ELL-transposed form (variant 1 already
+// is; variant 2 is decoded from brick-local indices on the device).
+const uint32_t* decoded_list(tmd_gpu_ctx* c) {
+  if (c->variant == 1) return c->nbr;
+  const size_t words = static_cast<size_t>(c->cap) * c->stride;
+  if (c->decoded_words < words) {
+    if (c->decoded) cudaFree(c->decoded);
+    c->decoded = dalloc<uint32_t>(words);
+    c->decoded_words = words;
+  }
+  c->launches += 1;
+  k_decode_list<<<c->bg.nbricks, 128, 0, c->stream>>>(
+      c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg, c->nbr,
+      c->nnbr, c->decoded, c->stride);
+  return c->decoded;
+}
 
 HostState fetch(tmd_gpu_ctx* c, bool pos, bool vel, bool frc, bool cell) {
   HostState h;
@@ -885,10 +1016,11 @@ int tmd_gpu_pairs(tmd_gpu_ctx* c, int64_t* pairs, size_t cap, size_t* n_out) {
     const int rows = std::min(c->cap, std::max(c->h_ctrl->max_count, 0));
     std::vector<int> cnt(n);
     std::vector<uint32_t> list(static_cast<size_t>(rows) * c->stride);
+    const uint32_t* glist = decoded_list(c);
     ck(cudaMemcpyAsync(cnt.data(), c->nnbr, n * sizeof(int),
                        cudaMemcpyDeviceToHost, c->stream), "D2H nnbr");
     if (!list.empty()) {
-      ck(cudaMemcpyAsync(list.data(), c->nbr, list.size() * sizeof(uint32_t),
+      ck(cudaMemcpyAsync(list.data(), glist, list.size() * sizeof(uint32_t),
                          cudaMemcpyDeviceToHost, c->stream), "D2H nbr");
     }
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
@@ -928,7 +1060,7 @@ int tmd_gpu_list_stats(tmd_gpu_ctx* c, tmd_list_stats* out) {
     ck(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream), "memset");
     c->launches += 1;
     k_count_incut<<<c->nblk, kBlock, 0, c->stream>>>(
-        static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g,
+        static_cast<int>(c->n), c->pos, decoded_list(c), c->nnbr, c->stride, c->g,
         c->lj.rc2, d);
     unsigned long long h = 0;
     ck(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c->stream), "D2H");

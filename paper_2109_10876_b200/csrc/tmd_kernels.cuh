@@ -150,8 +150,9 @@ __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
 // (the reference wraps only here, domain.hpp:63).
 __global__ void __launch_bounds__(kBlock)
     k_wrap_bin(int n, double4* __restrict__ pos, const long long* __restrict__ id,
-               int* __restrict__ cell, int* __restrict__ rank,
-               int* __restrict__ count, Geom g, Ctrl* ctrl) {
+               int* __restrict__ cell, int* __restrict__ slot,
+               int* __restrict__ count, const int* __restrict__ cell_rank, Geom g,
+               Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
   const int i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= n) return;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kBlock)
   const int cz = cell_coord(p.z, g.cell_len[2], g.dims[2]);
   const int c = cx + g.dims[0] * (cy + g.dims[1] * cz);
   cell[i] = c;
-  rank[i] = atomicAdd(&count[c], 1);
+  slot[i] = atomicAdd(&count[cell_rank[c]], 1);  // histogram in brick-major order
 }
 
 // Exclusive scan of the cell histogram (one block; runs once per rebuild).
@@ -214,12 +215,13 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_scatter(int n, const int* __restrict__ cell, const int* __restrict__ rank,
-              const int* __restrict__ start, int* __restrict__ perm, Ctrl* ctrl) {
+    k_scatter(int n, const int* __restrict__ cell, const int* __restrict__ slot,
+              const int* __restrict__ start, const int* __restrict__ cell_rank,
+              int* __restrict__ perm, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
   const int i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= n) return;
-  perm[start[cell[i]] + rank[i]] = i;
+  perm[start[cell_rank[cell[i]]] + slot[i]] = i;
 }
 
 // Canonical order inside each cell: ascending particle id. Makes the sorted
@@ -295,7 +297,8 @@ __global__ void __launch_bounds__(kBlock)
 // (neighbor_list.hpp:91-93). Also snapshots positions for needs_rebuild.
 __global__ void __launch_bounds__(kBlock)
     k_build_list(int n, const double4* __restrict__ pos, const int* __restrict__ cell,
-                 const int* __restrict__ start, Geom g, uint32_t* __restrict__ nbr,
+                 const int* __restrict__ start, const int* __restrict__ cell_rank, Geom g,
+                 uint32_t* __restrict__ nbr,
                  int* __restrict__ nnbr, int stride, int cap,
                  double4* __restrict__ snap, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
@@ -330,7 +333,8 @@ __global__ void __launch_bounds__(kBlock)
           const uint32_t img = (code_x << 25) | (code_y << 27) | (code_z << 29);
           const uint32_t tag = img | ((img != 0u && first < 0) ? kFlagIUpper : 0u);
           const bool same = (t == c);
-          const int jb = start[t], je = start[t + 1];
+          const int rt = cell_rank[t];
+          const int jb = start[rt], je = start[rt + 1];
           for (int j = jb; j < je; ++j) {
             if (same && j == i) continue;
             const double4 pj = pos[j];

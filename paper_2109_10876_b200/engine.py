@@ -132,6 +132,7 @@ class EngineConfig:
     section_timers: bool = True
     device: int = -1
     nbr_capacity: int = 0
+    variant: int = 2            # 1: thread-per-particle L1 gathers; 2: brick-staged smem
 
 
 @dataclass
@@ -225,6 +226,7 @@ class Engine:
         p.device = cfg.device
         p.section_timers = 1 if cfg.section_timers else 0
         p.nbr_capacity = cfg.nbr_capacity
+        p.reserved[0] = int(cfg.variant)
         h = C.c_void_p()
         rc = L.tmd_gpu_create(C.byref(sys), C.byref(lj), None, C.byref(p), C.byref(h))
         _check(rc, None)

@@ -5,14 +5,19 @@
 //
 // The CTA stages the halo block into shared memory once and every list entry
 // is a halo-local index into that staging layout, so the gathers of the hot
-// loop are LDS (bank-conflict bound) instead of L1 line fetches.
+// loop are LDS (bank-conflict bound) instead of L1 line fetches. Each halo
+// cell's staged block is padded to a multiple of 4 slots with far-away
+// coordinates so the build can read candidates with aligned 16-B loads.
 //
 // List layout (sector-chunked ELL): particles of a brick form groups of 32
 // (lane = brick offset % 32). Entry k of lane l of group g lives at
 //   list[g*cap*32 + (k/8)*256 + l*8 + k%8]
 // so each lane owns whole 32-byte sectors: the build flushes 8 entries with
 // two 16-B stores, the force kernel reads 8 entries with two 16-B loads, and
-// a warp touches 1 KB of contiguous memory per chunk.
+// a warp touches 1 KB of contiguous memory per chunk. A lane's last chunk is
+// padded with the sentinel slot (index = staging capacity, coordinates far
+// away), like the reference's sentinel-padded runs (neighbor_list.hpp:14-18,
+// soa_store.hpp:47-79), so the force loop has no tail branch.
 #pragma once
 
 #include "tmd_device.cuh"
@@ -20,14 +25,15 @@
 namespace tmd {
 
 constexpr int kMaxHalo = 64;  // (2+2)^3
+constexpr float kFarF = 1.0e30f;
+constexpr double kFarD = 1.0e30;
 
 struct BrickGeom {
   int B[3];      // brick edge in cells (min(2, dims))
   int nb[3];     // bricks per axis
   int nbricks;
   int cap;       // list entries per particle (multiple of 8)
-  int stage_cap_f32;  // build staging capacity (particles)
-  int stage_cap_f64;  // force staging capacity (particles)
+  int stage_cap;  // staging capacity (slots, multiple of 4); sentinel slot = stage_cap
   float lo2, hi2;     // FP32 prefilter band around rv2 (exact FP64 inside)
   double origin_scale[3];  // cell_len (brick origin = lo * cell_len)
 };
@@ -37,11 +43,13 @@ struct HaloTable {
   int H[3];               // halo extent
   int lo[3];              // first owned cell of the brick
   int e[3];               // owned extent
-  int total;              // staged particles
+  int total;              // staged slots (padded)
   int bs, be;             // brick particle range
 };
 
-// Fills the halo metadata of brick b into shared memory (any block size >= 64
+__device__ __forceinline__ int pad4(int v) { return (v + 3) & ~3; }
+
+// Fills the halo metadata of brick b into shared memory (block size >= 64
 // threads; synchronises). Halo cell h = hx + H0*(hy + H1*hz) mirrors global
 // cell raw = lo + h - 1 with periodic wrap; its image code (bits 25..30) is
 // the reference's ghost shift for that wrap (subnode.hpp:84-90).
@@ -57,6 +65,7 @@ __device__ __forceinline__ void load_halo(int b, const Geom& g, const BrickGeom&
   ht.lo[0] = bx * bg.B[0];
   ht.lo[1] = by * bg.B[1];
   ht.lo[2] = bz * bg.B[2];
+#pragma unroll
   for (int k = 0; k < 3; ++k) {
     ht.e[k] = min(bg.B[k], g.dims[k] - ht.lo[k]);
     ht.H[k] = ht.e[k] + 2;
@@ -67,6 +76,7 @@ __device__ __forceinline__ void load_halo(int b, const Geom& g, const BrickGeom&
     const int h[3] = {t % ht.H[0], (t / ht.H[0]) % ht.H[1], t / (ht.H[0] * ht.H[1])};
     int gc[3];
     uint32_t code = 0;
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
       int raw = ht.lo[k] + h[k] - 1;
       uint32_t c2 = 0;
@@ -83,13 +93,19 @@ __device__ __forceinline__ void load_halo(int b, const Geom& g, const BrickGeom&
     s_code[t] = code;
   }
   __syncthreads();
-  if (t == 0) {
-    int run = 0;
-    for (int h = 0; h < ht.n; ++h) {
-      s_off[h] = run;
-      run += s_cnt[h];
+  if (t < 32) {  // warp-level exclusive scan of the padded counts (<= 64 cells)
+    const int a = t < ht.n ? pad4(s_cnt[t]) : 0;
+    const int c = t + 32 < ht.n ? pad4(s_cnt[t + 32]) : 0;
+    int sa = a, sc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ua = __shfl_up_sync(0xffffffffu, sa, o);
+      const int uc = __shfl_up_sync(0xffffffffu, sc, o);
+      if (t >= o) { sa += ua; sc += uc; }
     }
-    s_off[ht.n] = run;
+    const int tot_a = __shfl_sync(0xffffffffu, sa, 31);
+    if (t < ht.n) s_off[t] = sa - a;
+    if (t + 32 < ht.n) s_off[t + 32] = tot_a + sc - c;
+    if (t == 31) s_off[ht.n] = tot_a + sc;
   }
   __syncthreads();
   ht.total = s_off[ht.n];
@@ -131,24 +147,32 @@ __device__ __forceinline__ size_t list_slot(int group, int cap, int lane, int k)
 // ---------------------------------------------------------------------------
 // Full-list build, brick-staged (the full-list form of build_sorted_list,
 // neighbor_list.hpp:51-111). One warp per owned cell of the brick, lanes =
-// that cell's particles; candidates (the 27 surrounding halo cells, read as
-// warp-broadcast LDS.128) are filtered in FP32 brick-relative coordinates.
-// Only candidates inside the band |r2 - rv2| <= delta take the exact FP64
-// test with the reference's rounding, so membership is bit-identical to the
-// reference while almost all arithmetic runs on the FP32 pipe.
+// that cell's particles. Candidates are the 9 stencil rows of 3 x-adjacent
+// halo cells (contiguous in the staging), scanned 32 at a time with packed
+// FP32 arithmetic (FADD2/FFMA2) on negated brick-relative coordinates into a
+// per-lane hit mask. Only hits are then processed: those inside the band
+// |r2 - rv2| <= delta take the exact FP64 test with the reference's rounding,
+// so membership is bit-identical to the reference.
 constexpr int kBuildThreads = 256;
 
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// kGlobal = false: entries are brick-local staging indices, groups are per
+// brick (variant 2). kGlobal = true: entries are global slots, groups are 32
+// consecutive global particles (variant 3); the sentinel is slot N, whose
+// position is parked far away.
+template <bool kGlobal>
 __global__ void __launch_bounds__(kBuildThreads)
     k_build_brick(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
                   const int* __restrict__ brick_rank_off, const int* __restrict__ start,
                   const int* __restrict__ group_off, Geom g, BrickGeom bg,
                   uint32_t* __restrict__ list, int* __restrict__ nnbr,
-                  double4* __restrict__ snap, Ctrl* ctrl) {
+                  double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
-  extern __shared__ float4 s_f[];  // staged FP32 brick-relative images
+  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z, each stage_cap + 32
   __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
   __shared__ uint32_t s_code[kMaxHalo];
-  __shared__ uint32_t s_buf[kBuildThreads / 32][32][8];
+  __shared__ __align__(16) uint32_t s_buf[kBuildThreads / 32][32][8];
   __shared__ int s_maxc;
   __shared__ unsigned long long s_ent;
   const int b = blockIdx.x;
@@ -156,26 +180,45 @@ __global__ void __launch_bounds__(kBuildThreads)
   if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
   load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
             s_gcell);
-  const bool staged = ht.total <= bg.stage_cap_f32;
+  if (ht.total > bg.stage_cap) {
+    // Overfull halo (never at the BASELINE densities): flag it; the host
+    // grows the staging and replays (same path as a list overflow).
+    if (threadIdx.x == 0) {
+      atomicOr(&ctrl->status, kStatStageOverflow);
+      atomicMax(&ctrl->max_halo, ht.total);
+    }
+    return;
+  }
+  const int sc = bg.stage_cap + 32;
+  float* nx = s_f;
+  float* ny = s_f + sc;
+  float* nz = s_f + 2 * sc;
   const double ox = ht.lo[0] * bg.origin_scale[0];
   const double oy = ht.lo[1] * bg.origin_scale[1];
   const double oz = ht.lo[2] * bg.origin_scale[2];
-  if (staged) {
-    for (int k = threadIdx.x; k < ht.total; k += kBuildThreads) {
+  for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
+    float x = kFarF, y = kFarF, z = kFarF;
+    if (k < ht.total) {
       const int h = halo_of(k, s_off, ht.n);
-      const double4 p = pos[s_gstart[h] + (k - s_off[h])];
-      const uint32_t c = s_code[h];
-      s_f[k] = make_float4(
-          static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox),
-          static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy),
-          static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz), 0.f);
+      const int q = k - s_off[h];
+      if (q < s_cnt[h]) {
+        const double4 p = pos[s_gstart[h] + q];
+        const uint32_t c = s_code[h];
+        x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
+        y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
+        z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
+      }
     }
+    nx[k] = -x;
+    ny[k] = -y;
+    nz[k] = -z;
   }
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
-  const int gbase = group_off[b];
+  const int gbase = kGlobal ? 0 : group_off[b];
+  const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
   int my_max = 0;
   unsigned long long my_ent = 0;
   for (int oc = warp; oc < ncell_own; oc += kBuildThreads / 32) {
@@ -185,55 +228,71 @@ __global__ void __launch_bounds__(kBuildThreads)
     for (int p0 = 0; p0 < ncl; p0 += 32) {
       const int q = p0 + lane;
       const bool active = q < ncl;
-      const int i = s_gstart[hc] + (active ? q : 0);
-      const double4 pi = pos[i];
-      float xf, yf, zf;
-      if (staged) {
-        const float4 f = s_f[s_off[hc] + (active ? q : 0)];
-        xf = f.x; yf = f.y; zf = f.z;
-      } else {
-        xf = static_cast<float>(pi.x - ox);
-        yf = static_cast<float>(pi.y - oy);
-        zf = static_cast<float>(pi.z - oz);
-      }
-      const int ib = i - ht.bs;
+      const int qi = active ? q : 0;
+      const int i = s_gstart[hc] + qi;
+      const int ki = s_off[hc] + qi;
+      const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
+      const float2 xi2 = f2(xf, xf), yi2 = f2(yf, yf), zi2 = f2(zf, zf);
+      const int ib = kGlobal ? i : i - ht.bs;
       const int grp = gbase + (ib >> 5), gl = ib & 31;
       int n = 0;
+      double4 pi = make_double4(0.0, 0.0, 0.0, 0.0);
+      bool have_pi = false;
       for (int oz2 = -1; oz2 <= 1; ++oz2) {
         for (int oy2 = -1; oy2 <= 1; ++oy2) {
-          for (int ox2 = -1; ox2 <= 1; ++ox2) {
-            const int h = hc + ox2 + ht.H[0] * (oy2 + ht.H[1] * oz2);
-            const uint32_t code = s_code[h];
-            const int first = ox2 != 0 ? ox2 : (oy2 != 0 ? oy2 : oz2);
-            const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
-            const bool same = s_gcell[h] == s_gcell[hc];
-            const int cnt = s_cnt[h], off = s_off[h], gs = s_gstart[h];
-            for (int c = 0; c < cnt; ++c) {
-              float4 f;
-              if (staged) {
-                f = s_f[off + c];
-              } else {
-                const double4 p = pos[gs + c];
-                f = make_float4(static_cast<float>((p.x + code_shift(code, 0, g.L[0])) - ox),
-                                static_cast<float>((p.y + code_shift(code, 1, g.L[1])) - oy),
-                                static_cast<float>((p.z + code_shift(code, 2, g.L[2])) - oz),
-                                0.f);
-              }
-              const float dx = xf - f.x, dy = yf - f.y, dz = zf - f.z;
-              const float r2f = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              if (!active || r2f > bg.hi2) continue;
-              const int j = gs + c;
-              if (same && j == i) continue;
-              const uint32_t ent = static_cast<uint32_t>(off + c) | tag;
+          const int h0 = hc - 1 + ht.H[0] * (oy2 + ht.H[1] * oz2);  // ox = -1 of the row
+          const int kb = s_off[h0], ke = s_off[h0 + 3];
+          const int k1 = s_off[h0 + 1], k2 = s_off[h0 + 2];
+          for (int k0 = kb; k0 < ke; k0 += 32) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int kq = k0 + 4 * u;
+              const float4 X = *reinterpret_cast<const float4*>(nx + kq);
+              const float4 Y = *reinterpret_cast<const float4*>(ny + kq);
+              const float4 Z = *reinterpret_cast<const float4*>(nz + kq);
+              const float2 dxa = __fadd2_rn(xi2, f2(X.x, X.y));
+              const float2 dxb = __fadd2_rn(xi2, f2(X.z, X.w));
+              const float2 dya = __fadd2_rn(yi2, f2(Y.x, Y.y));
+              const float2 dyb = __fadd2_rn(yi2, f2(Y.z, Y.w));
+              const float2 dza = __fadd2_rn(zi2, f2(Z.x, Z.y));
+              const float2 dzb = __fadd2_rn(zi2, f2(Z.z, Z.w));
+              const float2 ra = __ffma2_rn(dza, dza, __ffma2_rn(dya, dya, __fmul2_rn(dxa, dxa)));
+              const float2 rb = __ffma2_rn(dzb, dzb, __ffma2_rn(dyb, dyb, __fmul2_rn(dxb, dxb)));
+              m |= (ra.x <= bg.hi2 ? 1u : 0u) << (4 * u);
+              m |= (ra.y <= bg.hi2 ? 1u : 0u) << (4 * u + 1);
+              m |= (rb.x <= bg.hi2 ? 1u : 0u) << (4 * u + 2);
+              m |= (rb.y <= bg.hi2 ? 1u : 0u) << (4 * u + 3);
+            }
+            const int rem = ke - k0;
+            if (rem < 32) m &= (1u << rem) - 1u;
+            if (!active) m = 0;
+            while (m != 0u) {
+              const int c = __ffs(m) - 1;
+              m &= m - 1u;
+              const int k = k0 + c;
+              const int hh = h0 + (k >= k1 ? 1 : 0) + (k >= k2 ? 1 : 0);
+              const int qj = k - s_off[hh];
+              if (qj >= s_cnt[hh]) continue;  // padding slot
+              const int j = s_gstart[hh] + qj;
+              if (j == i && s_gcell[hh] == s_gcell[hc]) continue;  // self / own image
+              const uint32_t code = s_code[hh];
+              const int oxx = hh - h0 - 1;
+              const int first = oxx != 0 ? oxx : (oy2 != 0 ? oy2 : oz2);
+              const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
+              const float ddx = xf + nx[k], ddy = yf + ny[k], ddz = zf + nz[k];
+              const float r2f = fmaf(ddz, ddz, fmaf(ddy, ddy, ddx * ddx));
               bool in = r2f < bg.lo2;
               if (!in) {  // inside the rounding band: decide exactly in FP64
+                if (!have_pi) { pi = pos[i]; have_pi = true; }
                 const double4 pj = pos[j];
                 double ex, ey, ez;
                 pair_delta(pi, pj, static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey, ez);
                 in = exact_r2(ex, ey, ez) <= g.rv2;
               }
               if (in) {
-                s_buf[warp][lane][n & 7] = ent;
+                s_buf[warp][lane][n & 7] =
+                    static_cast<uint32_t>(kGlobal ? j : k) | tag;
                 ++n;
                 if ((n & 7) == 0 && n <= bg.cap) {
                   const uint4* src = reinterpret_cast<const uint4*>(&s_buf[warp][lane][0]);
@@ -247,14 +306,15 @@ __global__ void __launch_bounds__(kBuildThreads)
         }
       }
       if (active) {
-        if ((n & 7) != 0 && n <= bg.cap) {
+        if ((n & 7) != 0 && n <= bg.cap) {  // sentinel-pad the last chunk
+          for (int r = n & 7; r < 8; ++r) s_buf[warp][lane][r] = sentinel;
           const uint4* src = reinterpret_cast<const uint4*>(&s_buf[warp][lane][0]);
           uint4* dst = reinterpret_cast<uint4*>(list + list_slot(grp, bg.cap, gl, n & ~7));
           dst[0] = src[0];
           dst[1] = src[1];
         }
         nnbr[i] = n < bg.cap ? n : bg.cap;
-        snap[i] = pi;
+        snap[i] = have_pi ? pi : pos[i];
         if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
         my_max = max(my_max, n);
         my_ent += static_cast<unsigned long long>(n);
@@ -282,14 +342,31 @@ __global__ void __launch_bounds__(kBuildThreads)
 // neighbor_list.hpp:150-187, full-list form). The halo block is staged as
 // unshifted SoA doubles; image shifts and the reference's rounding
 // orientation come from the entry tag (pair_delta), so the cutoff test sees
-// the reference's r2 bit for bit.
+// the reference's r2 bit for bit. Chunks of 8 entries are processed without
+// a tail branch (sentinel padding), letting the compiler overlap the 8
+// independent gathers.
 constexpr int kForceThreads = 192;
 
-struct StagedPos {
-  const double* sx;
-  const double* sy;
-  const double* sz;
-};
+__device__ __forceinline__ void lj_accumulate(const double4& pi, double xj, double yj,
+                                              double zj, uint32_t ent, const Geom& g,
+                                              const LjConst& lj, double& ax, double& ay,
+                                              double& az, double& e, double& w, bool& zero) {
+  double dx, dy, dz;
+  pair_delta(pi, make_double4(xj, yj, zj, 0.0), ent, g, dx, dy, dz);
+  const double r2 = exact_r2(dx, dy, dz);
+  if (r2 < lj.rc2) {
+    zero |= (r2 == 0.0);
+    const double ri2 = rcp_nr(r2);
+    const double inv = lj.sigma2 * ri2;
+    const double i6 = inv * inv * inv;
+    const double ff = lj.eps24 * (2.0 * i6 * i6 - i6) * ri2;
+    e += lj.eps4 * (i6 * i6 - i6) - lj.shift;
+    w += ff * r2;
+    ax += ff * dx;
+    ay += ff * dy;
+    az += ff * dz;
+  }
+}
 
 __global__ void __launch_bounds__(kForceThreads)
     k_forces_brick(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
@@ -307,75 +384,78 @@ __global__ void __launch_bounds__(kForceThreads)
   HaloTable ht;
   load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
             s_gcell);
-  const bool staged = ht.total <= bg.stage_cap_f64;
-  const int cap_s = bg.stage_cap_f64;
+  const int sc = bg.stage_cap + 4;
   double* sx = s_d;
-  double* sy = s_d + cap_s;
-  double* sz = s_d + 2 * cap_s;
-  if (staged) {
-    for (int k = threadIdx.x; k < ht.total; k += kForceThreads) {
-      const int h = halo_of(k, s_off, ht.n);
-      const double4 p = pos[s_gstart[h] + (k - s_off[h])];
-      sx[k] = p.x;
-      sy[k] = p.y;
-      sz[k] = p.z;
+  double* sy = s_d + sc;
+  double* sz = s_d + 2 * sc;
+  double e = 0.0, w = 0.0;
+  if (ht.total <= bg.stage_cap) {  // (the build flags an overfull halo)
+    for (int k = threadIdx.x; k < sc; k += kForceThreads) {
+      double x = kFarD, y = kFarD, z = kFarD;
+      if (k < ht.total) {
+        const int h = halo_of(k, s_off, ht.n);
+        const int q = k - s_off[h];
+        if (q < s_cnt[h]) {
+          const double4 p = pos[s_gstart[h] + q];
+          x = p.x;
+          y = p.y;
+          z = p.z;
+        }
+      }
+      sx[k] = x;
+      sy[k] = y;
+      sz[k] = z;
     }
   }
   __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb_i = ht.be - ht.bs;
-  const int ngr = (nb_i + 31) >> 5;
-  double e = 0.0, w = 0.0;
-  for (int gl = warp; gl < ngr; gl += kForceThreads / 32) {
-    const int ib = gl * 32 + lane;
-    const bool active = ib < nb_i;
-    const int i = ht.bs + (active ? ib : 0);
-    const double4 pi = pos[i];
-    const int cnt = active ? nnbr[i] : 0;
-    const uint32_t* row = list + list_slot(group_off[b] + gl, bg.cap, lane, 0);
-    double ax = 0.0, ay = 0.0, az = 0.0;
-    for (int c0 = 0; c0 < cnt; c0 += 8) {
-      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32));
-      const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32 + 4));
-      const uint32_t ents[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+  if (ht.total <= bg.stage_cap) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nb_i = ht.be - ht.bs;
+    const int ngr = (nb_i + 31) >> 5;
+    for (int gl = warp; gl < ngr; gl += kForceThreads / 32) {
+      const int ib = gl * 32 + lane;
+      const bool active = ib < nb_i;
+      const int i = ht.bs + (active ? ib : 0);
+      const double4 pi = pos[i];
+      const int cnt = active ? nnbr[i] : 0;
+      const uint32_t* row = list + list_slot(group_off[b] + gl, bg.cap, lane, 0);
+      double ax = 0.0, ay = 0.0, az = 0.0;
+      bool zero = false;
+      for (int c0 = 0; c0 < cnt; c0 += 8) {
+        const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32));
+        const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32 + 4));
+        const uint32_t ents[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        double xj[8], yj[8], zj[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (c0 + u >= cnt) break;
-        const uint32_t ent = ents[u];
-        const int k = static_cast<int>(ent & kIdxMask);
-        double4 pj;
-        if (staged) {
-          pj = make_double4(sx[k], sy[k], sz[k], 0.0);
-        } else {
-          const int h = halo_of(k, s_off, ht.n);
-          pj = pos[s_gstart[h] + (k - s_off[h])];
+        for (int u = 0; u < 8; ++u) {
+          const int k = static_cast<int>(ents[u] & kIdxMask);
+          xj[u] = sx[k];
+          yj[u] = sy[k];
+          zj[u] = sz[k];
         }
-        double dx, dy, dz;
-        pair_delta(pi, pj, ent, g, dx, dy, dz);
-        const double r2 = exact_r2(dx, dy, dz);
-        if (r2 < lj.rc2) {
-          if (r2 == 0.0) {
-            const int h = halo_of(k, s_off, ht.n);
-            record_error(ctrl, kStatOverlap, id[i], id[s_gstart[h] + (k - s_off[h])]);
-            continue;
-          }
-          const double ri2 = rcp_nr(r2);
-          const double inv = lj.sigma2 * ri2;
-          const double i6 = inv * inv * inv;
-          const double ff = lj.eps24 * (2.0 * i6 * i6 - i6) * ri2;
-          e += lj.eps4 * (i6 * i6 - i6) - lj.shift;
-          w += ff * r2;
-          ax += ff * dx;
-          ay += ff * dy;
-          az += ff * dz;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          lj_accumulate(pi, xj[u], yj[u], zj[u], ents[u], g, lj, ax, ay, az, e, w, zero);
         }
       }
-    }
-    if (active) {
-      fx[i] = ax;
-      fy[i] = ay;
-      fz[i] = az;
+      if (zero) {  // r2 == 0: coincident particles (neighbor_list.hpp:166-170)
+        for (int k = 0; k < cnt; ++k) {
+          const uint32_t ent = row[(k >> 3) * 256 + (k & 7)];
+          const int kk = static_cast<int>(ent & kIdxMask);
+          double dx, dy, dz;
+          pair_delta(pi, make_double4(sx[kk], sy[kk], sz[kk], 0.0), ent, g, dx, dy, dz);
+          if (exact_r2(dx, dy, dz) == 0.0) {
+            const int h = halo_of(kk, s_off, ht.n);
+            record_error(ctrl, kStatOverlap, id[i], id[s_gstart[h] + (kk - s_off[h])]);
+            break;
+          }
+        }
+      }
+      if (active) {
+        fx[i] = ax;
+        fy[i] = ay;
+        fz[i] = az;
+      }
     }
   }
   const double te = block_sum<kForceThreads>(e, red);
@@ -383,6 +463,79 @@ __global__ void __launch_bounds__(kForceThreads)
   if (threadIdx.x == 0) {
     part_e[b] = te;
     part_w[b] = tw;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Variant 3: thread per particle over the sector-chunked list with GLOBAL
+// slots (groups = 32 consecutive particles of the brick-major order). Each
+// chunk of 8 entries is two 16-B loads; each gather is one 256-bit
+// LDG.E.ENL2.256 of the packed position (one L1 sector request per entry).
+// No staging, no shared memory: occupancy is register-limited only.
+template <int kUnroll>
+__global__ void __launch_bounds__(128)
+    k_forces_l1(int n, const double4* __restrict__ pos, const uint32_t* __restrict__ list,
+                const int* __restrict__ nnbr, int cap, Geom g, LjConst lj,
+                double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
+                double* __restrict__ part_e, double* __restrict__ part_w,
+                const long long* __restrict__ id, Ctrl* ctrl) {
+  __shared__ double red[4];
+  const int i = blockIdx.x * 128 + threadIdx.x;
+  double e = 0.0, w = 0.0;
+  if (i < n) {
+    const double4 pi = pos[i];
+    const int cnt = nnbr[i];
+    const uint32_t* row = list + list_slot(i >> 5, cap, i & 31, 0);
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    bool zero = false;
+    for (int c0 = 0; c0 < cnt; c0 += 8) {
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32));
+      const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32 + 4));
+      const uint32_t ents[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int u0 = 0; u0 < 8; u0 += kUnroll) {
+        double4 pj[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) pj[u] = ldg_pos256(pos + (ents[u0 + u] & kIdxMask));
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          lj_accumulate(pi, pj[u].x, pj[u].y, pj[u].z, ents[u0 + u], g, lj, ax, ay, az, e, w,
+                        zero);
+        }
+      }
+    }
+    if (zero) {
+      for (int k = 0; k < cnt; ++k) {
+        const uint32_t ent = row[(k >> 3) * 256 + (k & 7)];
+        const double4 pj = pos[ent & kIdxMask];
+        double dx, dy, dz;
+        pair_delta(pi, pj, ent, g, dx, dy, dz);
+        if (exact_r2(dx, dy, dz) == 0.0) {
+          record_error(ctrl, kStatOverlap, id[i], id[ent & kIdxMask]);
+          break;
+        }
+      }
+    }
+    fx[i] = ax;
+    fy[i] = ay;
+    fz[i] = az;
+  }
+  const double te = block_sum<128>(e, red);
+  const double tw = block_sum<128>(w, red);
+  if (threadIdx.x == 0) {
+    part_e[blockIdx.x] = te;
+    part_w[blockIdx.x] = tw;
+  }
+}
+
+// Tap for variant 3: chunked global-slot list -> ELL-transposed copy.
+__global__ void __launch_bounds__(128)
+    k_decode_chunked(int n, const uint32_t* __restrict__ list, const int* __restrict__ nnbr,
+                     int cap, uint32_t* __restrict__ out, int stride) {
+  const int i = blockIdx.x * 128 + threadIdx.x;
+  if (i >= n) return;
+  for (int k = 0; k < nnbr[i]; ++k) {
+    out[static_cast<size_t>(k) * stride + i] = list[list_slot(i >> 5, cap, i & 31, k)];
   }
 }
 

@@ -39,6 +39,7 @@ enum : int {
   kStatNonFinite = 2,    // non-finite v/f (engine.hpp:231-236) -> PhysicsError
   kStatNonFinitePos = 4, // non-finite position at binning (domain.hpp:58-62)
   kStatOverflow = 8,     // neighbour list capacity exceeded -> host re-runs
+  kStatStageOverflow = 16,  // a brick halo exceeded the staging capacity -> grow
 };
 
 struct LjConst {
@@ -68,6 +69,8 @@ struct Ctrl {
   int max_count;              // largest per-particle entry count, last build
   int cap;                    // current list capacity per particle
   long long entries;          // total entries, last build
+  int max_halo;               // largest staged halo seen (slots)
+  int pad_;
 };
 
 // ---------------------------------------------------------------------------
@@ -142,6 +145,16 @@ __device__ __forceinline__ double4 ldg_pos(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   const double2 a = __ldg(q), b = __ldg(q + 1);
   return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// The same gather as ONE 256-bit load (sm_100: LDG.E.ENL2.256.CONSTANT), so a
+// lane's 32-B sector is requested once instead of twice.
+__device__ __forceinline__ double4 ldg_pos256(const double4* p) {
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+      : "l"(p));
+  return r;
 }
 
 __device__ __forceinline__ bool finite3(double a, double b, double c) {

@@ -33,6 +33,11 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// Kernel variant used when the caller does not pick one (tmd_engine_params
+// reserved[0] = 0); chosen by the ncu/CUDA-event comparison in
+// profiles/ (see DESIGN.md §Force kernel variants).
+constexpr int kDefaultVariant = 3;
+
 struct CudaFail {
   std::string what;
 };
@@ -102,6 +107,7 @@ struct tmd_gpu_ctx {
 
   // brick-major ordering + variant selection
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
+  int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
   BrickGeom bg{};
   int* cell_rank = nullptr;       // global cell -> brick-major rank
   int* brick_rank_off = nullptr;  // brick -> first rank (nbricks + 1)
@@ -252,10 +258,19 @@ void launch_resort(tmd_gpu_ctx* c) {
 }
 
 size_t build_smem(const tmd_gpu_ctx* c) {
-  return static_cast<size_t>(c->bg.stage_cap_f32) * sizeof(float4);
+  return static_cast<size_t>(c->bg.stage_cap + 32) * 3 * sizeof(float);
 }
 size_t force_smem(const tmd_gpu_ctx* c) {
-  return static_cast<size_t>(c->bg.stage_cap_f64) * 3 * sizeof(double);
+  return static_cast<size_t>(c->bg.stage_cap + 4) * 3 * sizeof(double);
+}
+
+void set_smem_attrs(tmd_gpu_ctx* c) {
+  ck(cudaFuncSetAttribute(k_build_brick<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(build_smem(c))), "smem attr build");
+  ck(cudaFuncSetAttribute(k_build_brick<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(build_smem(c))), "smem attr build");
+  ck(cudaFuncSetAttribute(k_forces_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(force_smem(c))), "smem attr forces");
 }
 
 void launch_build(tmd_gpu_ctx* c) {
@@ -265,10 +280,14 @@ void launch_build(tmd_gpu_ctx* c) {
     k_build_list<<<c->nblk, kBlock, 0, c->stream>>>(
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->stride, c->cap, c->snap, c->ctrl);
-  } else {
-    k_build_brick<<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+  } else if (c->variant == 3) {
+    k_build_brick<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
-        c->nbr, c->nnbr, c->snap, c->ctrl);
+        c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n), c->ctrl);
+  } else {
+    k_build_brick<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
+        c->nbr, c->nnbr, c->snap, 0u, c->ctrl);
   }
 }
 
@@ -278,6 +297,13 @@ void launch_forces(tmd_gpu_ctx* c) {
     k_lj_forces<<<c->nblk, kBlock, 0, c->stream>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
         c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, c->ctrl);
+  } else if (c->variant == 3) {
+    auto kern = c->unroll == 1 ? k_forces_l1<1> : (c->unroll == 2 ? k_forces_l1<2>
+                                                 : (c->unroll == 8 ? k_forces_l1<8>
+                                                                   : k_forces_l1<4>));
+    kern<<<c->nblk, 128, 0, c->stream>>>(
+        static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
+        c->fz, c->part_e, c->part_w, c->id, c->ctrl);
   } else {
     k_forces_brick<<<c->bg.nbricks, kForceThreads, force_smem(c), c->stream>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
@@ -309,7 +335,7 @@ void launch_kick2(tmd_gpu_ctx* c) {
 
 void launch_reduce_pe(tmd_gpu_ctx* c) {
   c->launches += 2;
-  const int np = c->variant == 1 ? c->nblk : c->bg.nbricks;
+  const int np = c->variant == 2 ? c->bg.nbricks : c->nblk;
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, np, 0.5, c->scalars + 0);
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, np, 0.5, c->scalars + 1);
 }
@@ -388,6 +414,29 @@ void alloc_list(tmd_gpu_ctx* c, int cap) {
 
 // Resort + list build + forces at the current state, forced (setup / after a
 // rollback). Grows the list until it fits. Leaves the PE reduced.
+// Grows whatever overflowed at the last build: list capacity (entries per
+// particle) and/or the brick staging capacity. A staging need beyond what a
+// force CTA can hold in shared memory switches the context to variant 1
+// (thread-per-particle, no staging), which has no density limit.
+void grow_after_overflow(tmd_gpu_ctx* c, const Ctrl& h) {
+  if (h.status & kStatStageOverflow) {
+    const int want = (static_cast<int>(h.max_halo * 1.15) + 64 + 31) / 32 * 32;
+    if (static_cast<size_t>(want + 4) * 3 * sizeof(double) > 200 * 1024) {
+      c->variant = 1;
+    } else {
+      c->bg.stage_cap = std::max(c->bg.stage_cap, want);
+      set_smem_attrs(c);
+    }
+    alloc_list(c, c->cap);
+  }
+  if (h.status & kStatOverflow) {
+    const int need = h.max_count;
+    alloc_list(c, std::max(c->cap, need + need / 4 + 8));
+  }
+}
+
+constexpr int kOverflowBits = kStatOverflow | kStatStageOverflow;
+
 void setup_pass(tmd_gpu_ctx* c) {
   for (;;) {
     set_force_rebuild(c);
@@ -396,10 +445,10 @@ void setup_pass(tmd_gpu_ctx* c) {
     launch_build(c);
     sync_ctrl(c);
     raise_physics(c, false);
-    if (c->h_ctrl->status & kStatOverflow) {
-      const int need = c->h_ctrl->max_count;
+    if (c->h_ctrl->status & kOverflowBits) {
+      const Ctrl h = *c->h_ctrl;
       reset_status(c);
-      alloc_list(c, need + need / 4 + 8);
+      grow_after_overflow(c, h);
       continue;
     }
     break;
@@ -501,7 +550,7 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
   }
   sync_ctrl(c);
   harvest_timers(c);
-  return (c->h_ctrl->status & kStatOverflow) == 0;
+  return (c->h_ctrl->status & kOverflowBits) == 0;
 }
 
 void do_run(tmd_gpu_ctx* c, int64_t nsteps) {
@@ -518,10 +567,10 @@ void do_run(tmd_gpu_ctx* c, int64_t nsteps) {
     ck(cudaEventElapsedTime(&ms, c->t0, c->t1), "cudaEventElapsedTime");
     c->elapsed += 1e-3 * ms;
     if (!ok) {
-      // neighbour list overflow: roll back, grow, replay this chunk
-      const int need = c->h_ctrl->max_count;
+      // list or staging overflow: roll back, grow, replay this chunk
+      const Ctrl h = *c->h_ctrl;
       restore(c, before);
-      alloc_list(c, need + need / 4 + 8);
+      grow_after_overflow(c, h);
       setup_pass(c);
       continue;
     }
@@ -629,9 +678,12 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
   const double per_cell = n / vol * c->g.cell_len[0] * c->g.cell_len[1] * c->g.cell_len[2];
   const double halo = per_cell * (bg.B[0] + 2) * (bg.B[1] + 2) * (bg.B[2] + 2);
-  const int want = static_cast<int>(2.0 * halo + 64.0 + 31.0) / 32 * 32;
-  bg.stage_cap_f64 = std::max(256, std::min(want, 4096));
-  bg.stage_cap_f32 = std::max(256, std::min(want, 4096));
+  // expected halo + per-cell padding (<= 3 slots per cell) + 6 sigma, and
+  // small enough that 5 force CTAs fit an SM; overfull halos grow it at run
+  // time (setup_pass / do_run).
+  const int ncell_halo = (bg.B[0] + 2) * (bg.B[1] + 2) * (bg.B[2] + 2);
+  const double want = halo + 1.5 * ncell_halo + 6.0 * std::sqrt(halo) + 64.0;
+  bg.stage_cap = std::max(256, (static_cast<int>(want) + 31) / 32 * 32);
   // FP32 prefilter band (see DESIGN.md §List build): bound on |r2_f32 - r2_ref|
   // for brick-relative single-precision coordinates, times 4.
   const double cl = std::max({c->g.cell_len[0], c->g.cell_len[1], c->g.cell_len[2]});
@@ -658,10 +710,7 @@ void upload_bricks(tmd_gpu_ctx* c) {
                 cudaMemcpyHostToDevice), "H2D brick offsets");
   ck(cudaMemset(c->ngroups, 0, sizeof(int) * (static_cast<size_t>(c->bg.nbricks) + 1)),
      "memset");
-  ck(cudaFuncSetAttribute(k_build_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(build_smem(c))), "smem attr build");
-  ck(cudaFuncSetAttribute(k_forces_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(force_smem(c))), "smem attr forces");
+  set_smem_attrs(c);
   c->h_rank.clear();
   c->h_brick_off.clear();
 }
@@ -729,7 +778,9 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     c->r_skin = params->r_skin;
     c->r_cut = lj->r_cut;
     c->timers_on = params->section_timers != 0;
-    c->variant = params->reserved[0] == 1 ? 1 : 2;
+    c->variant = (params->reserved[0] >= 1 && params->reserved[0] <= 3) ? params->reserved[0]
+                                                                       : kDefaultVariant;
+    c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
     setup_bricks(c, static_cast<double>(c->n), lj->r_cut + params->r_skin);
     // lj_prepare (potentials.hpp:49-61)
     c->lj.sigma2 = lj->sigma * lj->sigma;
@@ -744,7 +795,7 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     }
 
     const size_t n = static_cast<size_t>(c->n);
-    c->pos = dalloc<double4>(n);
+    c->pos = dalloc<double4>(n + 1);  // slot n: far-away sentinel (variant 3 padding)
     c->pos2 = dalloc<double4>(n);
     c->snap = dalloc<double4>(n);
     c->vx = dalloc<double>(n); c->vy = dalloc<double>(n); c->vz = dalloc<double>(n);
@@ -792,7 +843,9 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
       }
       if (sys->mass) hm[k] = sys->mass[k];
     }
-    ck(cudaMemcpy(c->pos, hp.data(), n * sizeof(double4), cudaMemcpyHostToDevice), "H2D pos");
+    hp.push_back(make_double4(kFarD, kFarD, kFarD, 0.0));
+    ck(cudaMemcpy(c->pos, hp.data(), (n + 1) * sizeof(double4), cudaMemcpyHostToDevice),
+       "H2D pos");
     ck(cudaMemcpy(c->vx, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
     ck(cudaMemcpy(c->vy, hv.data() + n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vy");
     ck(cudaMemcpy(c->vz, hv.data() + 2 * n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vz");
@@ -850,6 +903,11 @@ const uint32_t* decoded_list(tmd_gpu_ctx* c) {
     c->decoded_words = words;
   }
   c->launches += 1;
+  if (c->variant == 3) {
+    k_decode_chunked<<<c->nblk, 128, 0, c->stream>>>(static_cast<int>(c->n), c->nbr, c->nnbr,
+                                                     c->cap, c->decoded, c->stride);
+    return c->decoded;
+  }
   k_decode_list<<<c->bg.nbricks, 128, 0, c->stream>>>(
       c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg, c->nbr,
       c->nnbr, c->decoded, c->stride);

@@ -174,6 +174,10 @@ int tmd_gpu_list_stats(tmd_gpu_ctx* ctx, tmd_list_stats* out);
  * returns the mean milliseconds per launch. Results are left in place. */
 int tmd_gpu_time_force_kernel(tmd_gpu_ctx* ctx, int reps, double* ms_per_launch);
 
+/* Benchmark hook: rebuilds the neighbour list `reps` times at the current
+ * positions (no resort) between CUDA events; mean milliseconds per build. */
+int tmd_gpu_time_list_build(tmd_gpu_ctx* ctx, int reps, double* ms_per_build);
+
 /* Raw stream handle (cudaStream_t) of the context, for callers that want to
  * order their own work after the engine's. */
 void* tmd_gpu_stream(tmd_gpu_ctx* ctx);

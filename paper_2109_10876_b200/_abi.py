@@ -28,6 +28,7 @@ EXPORTS = [
     "tmd_gpu_stream", "tmd_gpu_destroy", "tmd_gen_fcc",
     "tmd_thermal_velocities", "tmd_counter_uniform3", "tmd_counter_normal3",
     "tmd_gpu_abi_version", "tmd_gpu_launch_count", "tmd_gpu_fp64_peak",
+    "tmd_gpu_time_list_build",
 ]
 
 
@@ -106,6 +107,7 @@ def lib() -> C.CDLL:
     L.tmd_gpu_size.restype = C.c_int64
     L.tmd_gpu_list_stats.argtypes = [P, C.POINTER(TmdListStats)]
     L.tmd_gpu_time_force_kernel.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
+    L.tmd_gpu_time_list_build.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_stream.argtypes = [P]
     L.tmd_gpu_stream.restype = P
     L.tmd_gpu_launch_count.argtypes = [P]

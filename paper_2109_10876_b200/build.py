@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libtmd_gpu.so"
 
 SOURCES = [CSRC / "tmd_engine.cu", CSRC / "tmd_host.cpp"]
-HEADERS = [ROOT / "include" / "tmd_gpu.h", CSRC / "tmd_device.cuh", CSRC / "tmd_kernels.cuh"]
+HEADERS = [ROOT / "include" / "tmd_gpu.h", *sorted(CSRC.glob("*.cuh")), *sorted(CSRC.glob("*.h"))]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

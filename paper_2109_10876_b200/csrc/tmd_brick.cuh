@@ -154,6 +154,10 @@ __device__ __forceinline__ size_t list_slot(int group, int cap, int lane, int k)
 // |r2 - rv2| <= delta take the exact FP64 test with the reference's rounding,
 // so membership is bit-identical to the reference.
 constexpr int kBuildThreads = 256;
+#ifndef TMD_BUILD_MIN_BLOCKS
+#define TMD_BUILD_MIN_BLOCKS 4
+#endif
+constexpr int kBuildMinBlocks = TMD_BUILD_MIN_BLOCKS;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
@@ -243,8 +247,24 @@ __global__ void __launch_bounds__(kBuildThreads)
           const int h0 = hc - 1 + ht.H[0] * (oy2 + ht.H[1] * oz2);  // ox = -1 of the row
           const int kb = s_off[h0], ke = s_off[h0 + 3];
           const int k1 = s_off[h0 + 1], k2 = s_off[h0 + 2];
+          // Per-row constants of the 3 halo cells, kept in registers: the
+          // value added to a staged index to get the entry's index field, the
+          // entry tag (image code + rounding orientation), own-cell flag.
+          const int first_yz = oy2 != 0 ? oy2 : oz2;
+          uint32_t tag3[3];
+          int add3[3];
+          bool self_row = false;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int hh = h0 + t;
+            const uint32_t code = s_code[hh];
+            const int first = (t - 1) != 0 ? (t - 1) : first_yz;
+            tag3[t] = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
+            add3[t] = kGlobal ? s_gstart[hh] - s_off[hh] : 0;
+            self_row |= s_gcell[hh] == s_gcell[hc];
+          }
           for (int k0 = kb; k0 < ke; k0 += 32) {
-            uint32_t m = 0;
+            uint32_t m = 0, msure = 0;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int kq = k0 + 4 * u;
@@ -263,27 +283,32 @@ __global__ void __launch_bounds__(kBuildThreads)
               m |= (ra.y <= bg.hi2 ? 1u : 0u) << (4 * u + 1);
               m |= (rb.x <= bg.hi2 ? 1u : 0u) << (4 * u + 2);
               m |= (rb.y <= bg.hi2 ? 1u : 0u) << (4 * u + 3);
+              msure |= (ra.x < bg.lo2 ? 1u : 0u) << (4 * u);
+              msure |= (ra.y < bg.lo2 ? 1u : 0u) << (4 * u + 1);
+              msure |= (rb.x < bg.lo2 ? 1u : 0u) << (4 * u + 2);
+              msure |= (rb.y < bg.lo2 ? 1u : 0u) << (4 * u + 3);
             }
+            // (padding slots hold far coordinates: r2 = inf, never a hit)
             const int rem = ke - k0;
             if (rem < 32) m &= (1u << rem) - 1u;
             if (!active) m = 0;
             while (m != 0u) {
               const int c = __ffs(m) - 1;
-              m &= m - 1u;
+              const uint32_t bit = 1u << c;
+              m ^= bit;
               const int k = k0 + c;
-              const int hh = h0 + (k >= k1 ? 1 : 0) + (k >= k2 ? 1 : 0);
-              const int qj = k - s_off[hh];
-              if (qj >= s_cnt[hh]) continue;  // padding slot
-              const int j = s_gstart[hh] + qj;
-              if (j == i && s_gcell[hh] == s_gcell[hc]) continue;  // self / own image
-              const uint32_t code = s_code[hh];
-              const int oxx = hh - h0 - 1;
-              const int first = oxx != 0 ? oxx : (oy2 != 0 ? oy2 : oz2);
-              const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
-              const float ddx = xf + nx[k], ddy = yf + ny[k], ddz = zf + nz[k];
-              const float r2f = fmaf(ddz, ddz, fmaf(ddy, ddy, ddx * ddx));
-              bool in = r2f < bg.lo2;
+              const int t = (k >= k1 ? 1 : 0) + (k >= k2 ? 1 : 0);
+              const uint32_t tag = t == 0 ? tag3[0] : (t == 1 ? tag3[1] : tag3[2]);
+              const int idx = k + (t == 0 ? add3[0] : (t == 1 ? add3[1] : add3[2]));
+              if (self_row) {  // self / own periodic image (neighbor_list.hpp:91-93)
+                const int hh = h0 + t;
+                const int j = s_gstart[hh] + (k - s_off[hh]);
+                if (j == i && s_gcell[hh] == s_gcell[hc]) continue;
+              }
+              bool in = (msure & bit) != 0u;
               if (!in) {  // inside the rounding band: decide exactly in FP64
+                const int hh = h0 + t;
+                const int j = s_gstart[hh] + (k - s_off[hh]);
                 if (!have_pi) { pi = pos[i]; have_pi = true; }
                 const double4 pj = pos[j];
                 double ex, ey, ez;
@@ -291,8 +316,7 @@ __global__ void __launch_bounds__(kBuildThreads)
                 in = exact_r2(ex, ey, ez) <= g.rv2;
               }
               if (in) {
-                s_buf[warp][lane][n & 7] =
-                    static_cast<uint32_t>(kGlobal ? j : k) | tag;
+                s_buf[warp][lane][n & 7] = static_cast<uint32_t>(idx) | tag;
                 ++n;
                 if ((n & 7) == 0 && n <= bg.cap) {
                   const uint4* src = reinterpret_cast<const uint4*>(&s_buf[warp][lane][0]);
@@ -315,6 +339,387 @@ __global__ void __launch_bounds__(kBuildThreads)
         }
         nnbr[i] = n < bg.cap ? n : bg.cap;
         snap[i] = have_pi ? pi : pos[i];
+        if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
+        my_max = max(my_max, n);
+        my_ent += static_cast<unsigned long long>(n);
+      }
+      __syncwarp();
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
+    my_ent += __shfl_xor_sync(0xffffffffu, my_ent, o);
+  }
+  if (lane == 0) {
+    atomicMax(&s_maxc, my_max);
+    atomicAdd(&s_ent, my_ent);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&ctrl->max_count, s_maxc);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries), s_ent);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Full-list build, lanes = candidates (the production build). Same staging and
+// membership rule as k_build_brick, but the roles are swapped: a warp owns one
+// cell of the brick, takes the 9 stencil rows 32 candidates at a time (one
+// candidate per lane, its tag/index/self-id resolved once per batch), and
+// loops over the cell's particles i with warp-uniform i: the FP32 test is
+// fully SIMD, hits are compacted with a ballot and each hit lane stores its
+// entry straight into i's chunked list at n_i + rank (consecutive slots of
+// one 32-B sector). No per-lane serial hit loop.
+template <bool kGlobal>
+__global__ void __launch_bounds__(kBuildThreads)
+    k_build_brick2(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
+                   const int* __restrict__ brick_rank_off, const int* __restrict__ start,
+                   const int* __restrict__ group_off, Geom g, BrickGeom bg,
+                   uint32_t* __restrict__ list, int* __restrict__ nnbr,
+                   double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z, each stage_cap + 32
+  __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
+  __shared__ uint32_t s_code[kMaxHalo];
+  __shared__ int s_maxc;
+  __shared__ unsigned long long s_ent;
+  const int b = blockIdx.x;
+  HaloTable ht;
+  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
+  load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
+            s_gcell);
+  if (ht.total > bg.stage_cap) {
+    if (threadIdx.x == 0) {
+      atomicOr(&ctrl->status, kStatStageOverflow);
+      atomicMax(&ctrl->max_halo, ht.total);
+    }
+    return;
+  }
+  const int sc = bg.stage_cap + 32;
+  float* nx = s_f;
+  float* ny = s_f + sc;
+  float* nz = s_f + 2 * sc;
+  const double ox = ht.lo[0] * bg.origin_scale[0];
+  const double oy = ht.lo[1] * bg.origin_scale[1];
+  const double oz = ht.lo[2] * bg.origin_scale[2];
+  for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
+    float x = kFarF, y = kFarF, z = kFarF;
+    if (k < ht.total) {
+      const int h = halo_of(k, s_off, ht.n);
+      const int q = k - s_off[h];
+      if (q < s_cnt[h]) {
+        const double4 p = pos[s_gstart[h] + q];
+        const uint32_t c = s_code[h];
+        x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
+        y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
+        z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
+      }
+    }
+    nx[k] = -x;
+    ny[k] = -y;
+    nz[k] = -z;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
+  const int gbase = kGlobal ? 0 : group_off[b];
+  const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
+  int my_max = 0;
+  unsigned long long my_ent = 0;
+  // Work items = (owned cell, 8 consecutive particles of it), dealt round-robin
+  // to the warps: finer than one cell per warp, so the CTA tail is short.
+  __shared__ int s_item_off[9];
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int oc = 0; oc < ncell_own; ++oc) {
+      const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
+      s_item_off[oc] = run;
+      run += (s_cnt[(ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1))] + 7) >> 3;
+    }
+    s_item_off[ncell_own] = run;
+  }
+  __syncthreads();
+  const int nitems = s_item_off[ncell_own];
+  constexpr int kItem = 8;
+  for (int it = warp; it < nitems; it += kBuildThreads / 32) {
+    int oc = 0;
+    while (s_item_off[oc + 1] <= it) ++oc;
+    const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
+    const int hc = (ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1));
+    const int ncl = s_cnt[hc];
+    {
+      const int p0 = (it - s_item_off[oc]) * kItem;
+      const int nq = min(kItem, ncl - p0);
+      // lanes 0..nq-1 hold particle i_q: global slot, list row base, counter
+      const int kq0 = s_off[hc] + p0;  // staged index of i_0 (multiple of 4)
+      const int my_i = s_gstart[hc] + p0 + (lane < nq ? lane : 0);
+      const int my_ib = kGlobal ? my_i : my_i - ht.bs;
+      const unsigned long long my_row = list_slot(gbase + (my_ib >> 5), bg.cap, my_ib & 31, 0);
+      int my_n = 0;
+      for (int oz2 = -1; oz2 <= 1; ++oz2) {
+        for (int oy2 = -1; oy2 <= 1; ++oy2) {
+          const int h0 = hc - 1 + ht.H[0] * (oy2 + ht.H[1] * oz2);  // ox = -1 of the row
+          const int kb = s_off[h0], ke = s_off[h0 + 3];
+          const int k1 = s_off[h0 + 1], k2 = s_off[h0 + 2];
+          const int first_yz = oy2 != 0 ? oy2 : oz2;
+          for (int k0 = kb; k0 < ke; k0 += 32) {
+            // this lane's candidate: staged slot k, its halo cell, entry, slot j
+            const int k = k0 + lane;
+            const int t = (k >= k1 ? 1 : 0) + (k >= k2 ? 1 : 0);
+            const int hh = h0 + t;
+            const uint32_t code = s_code[hh];
+            const int first = (t - 1) != 0 ? (t - 1) : first_yz;
+            const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
+            const int j = s_gstart[hh] + (k - s_off[hh]);
+            const bool valid = k < ke && (k - s_off[hh]) < s_cnt[hh];
+            const uint32_t ent = static_cast<uint32_t>(kGlobal ? j : k) | tag;
+            const float2 cx2 = f2(nx[k], nx[k]), cy2 = f2(ny[k], ny[k]), cz2 = f2(nz[k], nz[k]);
+            const int i0 = s_gstart[hc] + p0;
+            for (int q = 0; q < nq; q += 2) {
+              // two particles per iteration: packed FP32 on (i_q, i_q+1)
+              const float2 xi = *reinterpret_cast<const float2*>(nx + kq0 + q);
+              const float2 yi = *reinterpret_cast<const float2*>(ny + kq0 + q);
+              const float2 zi = *reinterpret_cast<const float2*>(nz + kq0 + q);
+              const float2 dx = __fadd2_rn(xi, f2(-cx2.x, -cx2.y));
+              const float2 dy = __fadd2_rn(yi, f2(-cy2.x, -cy2.y));
+              const float2 dz = __fadd2_rn(zi, f2(-cz2.x, -cz2.y));
+              const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+              bool hit0 = valid && r2.x <= bg.hi2 && j != i0 + q;
+              bool hit1 = valid && r2.y <= bg.hi2 && j != i0 + q + 1 && q + 1 < nq;
+              if (__ballot_sync(0xffffffffu, hit0 || hit1) == 0u) continue;
+              if ((hit0 && !(r2.x < bg.lo2)) || (hit1 && !(r2.y < bg.lo2))) {
+                // rounding band: exact FP64 decision with the reference's rounding
+                const double4 pj = pos[j];
+                const uint32_t ej = static_cast<uint32_t>(j & kIdxMask) | tag;
+                double ex, ey, ez;
+                if (hit0 && !(r2.x < bg.lo2)) {
+                  pair_delta(pos[i0 + q], pj, ej, g, ex, ey, ez);
+                  hit0 = exact_r2(ex, ey, ez) <= g.rv2;
+                }
+                if (hit1 && !(r2.y < bg.lo2)) {
+                  pair_delta(pos[i0 + q + 1], pj, ej, g, ex, ey, ez);
+                  hit1 = exact_r2(ex, ey, ez) <= g.rv2;
+                }
+              }
+              const uint32_t bal0 = __ballot_sync(0xffffffffu, hit0);
+              const uint32_t bal1 = __ballot_sync(0xffffffffu, hit1);
+              const int n0 = __shfl_sync(0xffffffffu, my_n, q);
+              const int n1 = __shfl_sync(0xffffffffu, my_n, q + 1);
+              const unsigned long long row0 = __shfl_sync(0xffffffffu, my_row, q);
+              const unsigned long long row1 = __shfl_sync(0xffffffffu, my_row, q + 1);
+              if (hit0) {
+                const int pk = n0 + __popc(bal0 & lt_mask);
+                if (pk < bg.cap) list[row0 + (pk >> 3) * 256 + (pk & 7)] = ent;
+              }
+              if (hit1) {
+                const int pk = n1 + __popc(bal1 & lt_mask);
+                if (pk < bg.cap) list[row1 + (pk >> 3) * 256 + (pk & 7)] = ent;
+              }
+              if (lane == q) my_n += __popc(bal0);
+              if (lane == q + 1) my_n += __popc(bal1);
+            }
+          }
+        }
+      }
+      if (lane < nq) {
+        const int n = my_n;
+        if (n <= bg.cap) {
+          for (int r = n; r < ((n + 7) & ~7); ++r) {  // sentinel-pad the last chunk
+            list[my_row + (r >> 3) * 256 + (r & 7)] = sentinel;
+          }
+        }
+        nnbr[my_i] = n < bg.cap ? n : bg.cap;
+        snap[my_i] = pos[my_i];
+        if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
+        my_max = max(my_max, n);
+        my_ent += static_cast<unsigned long long>(n);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
+    my_ent += __shfl_xor_sync(0xffffffffu, my_ent, o);
+  }
+  if (lane == 0) {
+    atomicMax(&s_maxc, my_max);
+    atomicAdd(&s_ent, my_ent);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&ctrl->max_count, s_maxc);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries), s_ent);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Full-list build, lanes = particles, branch-free appends (k_build_brick3).
+// A warp owns one cell of the brick, lanes = its particles. Candidates stream
+// warp-uniformly over the 27 halo cells, two at a time (LDS.64 broadcast +
+// packed FP32 FADD2/FFMA2); every lane appends its hits to a private 16-slot
+// shared-memory ring with predicated stores and flushes a completed 8-entry
+// chunk as one 32-B sector. Only the FP32 rounding band and r2 == 0 (self,
+// or coincident particles, which the force kernel reports) take the exact
+// FP64 path, so membership is bit-identical to the reference.
+// 8 ring slots (stride 32 words) -> one 32-B sector of the chunked list.
+__device__ __forceinline__ void flush_chunk(const uint32_t* ring8, uint32_t* dst) {
+  uint4 a, b;
+  a.x = ring8[0];
+  a.y = ring8[32];
+  a.z = ring8[64];
+  a.w = ring8[96];
+  b.x = ring8[128];
+  b.y = ring8[160];
+  b.z = ring8[192];
+  b.w = ring8[224];
+  reinterpret_cast<uint4*>(dst)[0] = a;
+  reinterpret_cast<uint4*>(dst)[1] = b;
+}
+
+template <bool kGlobal>
+__global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
+    k_build_brick3(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
+                   const int* __restrict__ brick_rank_off, const int* __restrict__ start,
+                   const int* __restrict__ group_off, Geom g, BrickGeom bg,
+                   uint32_t* __restrict__ list, int* __restrict__ nnbr,
+                   double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z | base, each stage_cap + 32
+  __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
+  __shared__ uint32_t s_code[kMaxHalo];
+  // per-lane 16-slot ring, lane-fastest so concurrent stores never conflict
+  __shared__ __align__(16) uint32_t s_ring[kBuildThreads / 32][16][32];
+  __shared__ int s_maxc;
+  __shared__ unsigned long long s_ent;
+  const int b = blockIdx.x;
+  HaloTable ht;
+  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
+  load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
+            s_gcell);
+  if (ht.total > bg.stage_cap) {
+    if (threadIdx.x == 0) {
+      atomicOr(&ctrl->status, kStatStageOverflow);
+      atomicMax(&ctrl->max_halo, ht.total);
+    }
+    return;
+  }
+  const int sc = bg.stage_cap + 32;
+  float* nx = s_f;
+  float* ny = s_f + sc;
+  float* nz = s_f + 2 * sc;
+  int* sbase = reinterpret_cast<int*>(s_f + 3 * sc);  // entry index field per slot
+  const double ox = ht.lo[0] * bg.origin_scale[0];
+  const double oy = ht.lo[1] * bg.origin_scale[1];
+  const double oz = ht.lo[2] * bg.origin_scale[2];
+  for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
+    float x = kFarF, y = kFarF, z = kFarF;
+    int base = 0;
+    if (k < ht.total) {
+      const int h = halo_of(k, s_off, ht.n);
+      const int q = k - s_off[h];
+      if (q < s_cnt[h]) {
+        const double4 p = pos[s_gstart[h] + q];
+        const uint32_t c = s_code[h];
+        x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
+        y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
+        z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
+        base = kGlobal ? s_gstart[h] + q : k;
+      }
+    }
+    nx[k] = -x;
+    ny[k] = -y;
+    nz[k] = -z;
+    sbase[k] = base;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
+  const int gbase = kGlobal ? 0 : group_off[b];
+  const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
+  int my_max = 0;
+  unsigned long long my_ent = 0;
+  for (int oc = warp; oc < ncell_own; oc += kBuildThreads / 32) {
+    const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
+    const int hc = (ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1));
+    const int ncl = s_cnt[hc];
+    for (int p0 = 0; p0 < ncl; p0 += 32) {
+      const int q = p0 + lane;
+      const bool active = q < ncl;
+      const int qi = active ? q : 0;
+      const int i = s_gstart[hc] + qi;
+      const int ki = s_off[hc] + qi;
+      const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
+      const float2 xi2 = f2(xf, xf), yi2 = f2(yf, yf), zi2 = f2(zf, zf);
+      const int ib = kGlobal ? i : i - ht.bs;
+      const unsigned long long row = list_slot(gbase + (ib >> 5), bg.cap, ib & 31, 0);
+      const float hi2 = active ? bg.hi2 : -1.0f;  // inactive lanes never hit
+      const uint32_t lo2m1 = __float_as_uint(bg.lo2) - 1u;
+      int n = 0;
+      for (int oz2 = -1; oz2 <= 1; ++oz2) {
+        for (int oy2 = -1; oy2 <= 1; ++oy2) {
+          for (int ox2 = -1; ox2 <= 1; ++ox2) {
+            const int h = hc + ox2 + ht.H[0] * (oy2 + ht.H[1] * oz2);
+            const uint32_t code = s_code[h];
+            const int first = ox2 != 0 ? ox2 : (oy2 != 0 ? oy2 : oz2);
+            const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
+            const int kb = s_off[h], ke = kb + s_cnt[h];
+#pragma unroll 1
+            for (int k = kb; k < ke; k += 2) {
+              const float2 X = *reinterpret_cast<const float2*>(nx + k);
+              const float2 Y = *reinterpret_cast<const float2*>(ny + k);
+              const float2 Z = *reinterpret_cast<const float2*>(nz + k);
+              const float2 dx = __fadd2_rn(xi2, X), dy = __fadd2_rn(yi2, Y),
+                           dz = __fadd2_rn(zi2, Z);
+              const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+              bool h0 = r2.x <= hi2;
+              bool h1 = r2.y <= hi2;  // slot k+1 past the cell is padding: far, no hit
+              // sure hit <=> 0 < r2 < lo2: one unsigned compare on the bit pattern
+              // (non-negative floats order like their bits)
+              const bool band0 = h0 && (__float_as_uint(r2.x) - 1u) >= lo2m1;
+              const bool band1 = h1 && (__float_as_uint(r2.y) - 1u) >= lo2m1;
+              if (band0 || band1) {  // exact FP64 decision (reference rounding) + self
+                const double4 pi = pos[i];
+                if (band0) {
+                  const int j = s_gstart[h] + (k - kb);
+                  double ex, ey, ez;
+                  pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey,
+                             ez);
+                  h0 = j != i && exact_r2(ex, ey, ez) <= g.rv2;
+                }
+                if (band1) {
+                  const int j = s_gstart[h] + (k + 1 - kb);
+                  double ex, ey, ez;
+                  pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey,
+                             ez);
+                  h1 = j != i && exact_r2(ex, ey, ez) <= g.rv2;
+                }
+              }
+              // unconditional ring stores: a miss leaves junk in the next free
+              // slot, which the next hit (or the sentinel padding) overwrites
+              const int n0 = n;
+              const uint2 sb = *reinterpret_cast<const uint2*>(sbase + k);
+              s_ring[warp][n & 15][lane] = sb.x | tag;
+              n += h0 ? 1 : 0;
+              s_ring[warp][n & 15][lane] = sb.y | tag;
+              n += h1 ? 1 : 0;
+              if ((n0 >> 3) != (n >> 3) && n0 < bg.cap) {  // a chunk completed: flush it
+                const int c = n0 >> 3;
+                flush_chunk(&s_ring[warp][(c & 1) * 8][lane], list + row + c * 256);
+              }
+            }
+          }
+        }
+      }
+      if (active) {
+        if ((n & 7) != 0 && n < bg.cap) {  // sentinel-pad and flush the last chunk
+          for (int r = n; r < ((n + 7) & ~7); ++r) s_ring[warp][r & 15][lane] = sentinel;
+          const int c = n >> 3;
+          flush_chunk(&s_ring[warp][(c & 1) * 8][lane], list + row + c * 256);
+        }
+        nnbr[i] = n < bg.cap ? n : bg.cap;
+        snap[i] = pos[i];
         if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
         my_max = max(my_max, n);
         my_ent += static_cast<unsigned long long>(n);

@@ -258,16 +258,16 @@ void launch_resort(tmd_gpu_ctx* c) {
 }
 
 size_t build_smem(const tmd_gpu_ctx* c) {
-  return static_cast<size_t>(c->bg.stage_cap + 32) * 3 * sizeof(float);
+  return static_cast<size_t>(c->bg.stage_cap + 32) * 4 * sizeof(float);
 }
 size_t force_smem(const tmd_gpu_ctx* c) {
   return static_cast<size_t>(c->bg.stage_cap + 4) * 3 * sizeof(double);
 }
 
 void set_smem_attrs(tmd_gpu_ctx* c) {
-  ck(cudaFuncSetAttribute(k_build_brick<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ck(cudaFuncSetAttribute(k_build_brick3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(build_smem(c))), "smem attr build");
-  ck(cudaFuncSetAttribute(k_build_brick<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(build_smem(c))), "smem attr build");
   ck(cudaFuncSetAttribute(k_forces_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(force_smem(c))), "smem attr forces");
@@ -281,11 +281,11 @@ void launch_build(tmd_gpu_ctx* c) {
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->stride, c->cap, c->snap, c->ctrl);
   } else if (c->variant == 3) {
-    k_build_brick<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+    k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n), c->ctrl);
   } else {
-    k_build_brick<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+    k_build_brick3<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->nbr, c->nnbr, c->snap, 0u, c->ctrl);
   }
@@ -1147,6 +1147,23 @@ int tmd_gpu_time_force_kernel(tmd_gpu_ctx* c, int reps, double* ms) {
     float t = 0.f;
     ck(cudaEventElapsedTime(&t, c->t0, c->t1), "cudaEventElapsedTime");
     ck(cudaGetLastError(), "kernel launch");
+    *ms = static_cast<double>(t) / reps;
+  });
+}
+
+int tmd_gpu_time_list_build(tmd_gpu_ctx* c, int reps, double* ms) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (reps < 1) throw StatusError{TMD_ERR_CONFIG, "reps must be >= 1"};
+    set_force_rebuild(c);
+    launch_decide(c, false);  // rebuild = 1 until the next decision
+    ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    for (int r = 0; r < reps; ++r) launch_build(c);
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+    float t = 0.f;
+    ck(cudaEventElapsedTime(&t, c->t0, c->t1), "cudaEventElapsedTime");
+    sync_ctrl(c);
     *ms = static_cast<double>(t) / reps;
   });
 }

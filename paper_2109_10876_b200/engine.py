@@ -132,7 +132,10 @@ class EngineConfig:
     section_timers: bool = True
     device: int = -1
     nbr_capacity: int = 0
-    variant: int = 2            # 1: thread-per-particle L1 gathers; 2: brick-staged smem
+    # kernel variant: 0 = library default (3); 1 = thread-per-particle ELL list +
+    # 2x LDG.128 gathers; 2 = brick-staged shared memory; 3 = sector-chunked
+    # list + 256-bit LDG gathers
+    variant: int = 0
 
 
 @dataclass
@@ -348,6 +351,11 @@ class Engine:
 
     def stream_handle(self) -> int:
         return int(_abi.lib().tmd_gpu_stream(self._h) or 0)
+
+    def time_list_build(self, reps: int) -> float:
+        ms = C.c_double()
+        _check(_abi.lib().tmd_gpu_time_list_build(self._h, int(reps), C.byref(ms)), self._h)
+        return ms.value
 
     def time_force_kernel(self, reps: int) -> float:
         ms = C.c_double()

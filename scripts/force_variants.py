@@ -47,10 +47,11 @@ for spec in args.variants.split(","):
         eng._h, eng._n, eng._cfg, eng.box = h, n, cfg, f.box.copy()
     eng.run(args.steps)
     ms = eng.time_force_kernel(args.reps)
+    ms_build = eng.time_list_build(max(2, args.reps // 4))
     st = eng.list_stats()
     o = eng.observe()
     B = n * 52 + st["entries"] * 28
-    res.append({"variant": spec, "force_ms": ms, "frac_hbm_roofline": B / 6552.6e9 / (ms * 1e-3),
+    res.append({"variant": spec, "force_ms": ms, "build_ms": ms_build, "frac_hbm_roofline": B / 6552.6e9 / (ms * 1e-3),
                 "entries": st["entries"], "pe": o.potential})
     print(json.dumps(res[-1]), flush=True)
     eng.close()

@@ -118,6 +118,7 @@ struct tmd_gpu_ctx {
   uint32_t* decoded = nullptr;    // global-index ELL copy for the taps
   size_t decoded_words = 0;
   std::vector<int> h_rank, h_brick_off;  // host staging for upload_bricks
+  int* scan_tmp = nullptr;               // tile sums of the tiled scan
   double *part_e = nullptr, *part_w = nullptr, *part_ke = nullptr;
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
   Ctrl* ctrl = nullptr;
@@ -161,7 +162,7 @@ void free_all(tmd_gpu_ctx* c) {
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
                   c->rebuild_log, c->cell_rank, c->brick_rank_off, c->ngroups,
-                  c->group_off, c->decoded};
+                  c->group_off, c->decoded, c->scan_tmp};
   for (void* p : ptrs) {
     if (p) cudaFree(p);
   }
@@ -230,17 +231,26 @@ void launch_decide(tmd_gpu_ctx* c, bool advance, int log_idx = -1) {
                                    log_idx);
 }
 
+// Exclusive scan of counts[0..n) into out[0..n] (3 tiled kernels).
+void launch_scan(tmd_gpu_ctx* c, int n, int* counts, int* out) {
+  c->launches += 3;
+  const int tiles = blocks_for(n, kScanTile);
+  k_scan_tiles<<<tiles, kScanThreads, 0, c->stream>>>(n, counts, c->scan_tmp, c->ctrl);
+  k_scan_sums<<<1, kScanThreads, 0, c->stream>>>(tiles, c->scan_tmp, c->ctrl);
+  k_scan_apply<<<tiles, kScanThreads, 0, c->stream>>>(n, counts, c->scan_tmp, out, c->ctrl);
+}
+
 void launch_resort(tmd_gpu_ctx* c) {
-  c->launches += 8;
+  c->launches += 6;
   const int n = static_cast<int>(c->n);
   const int nb = c->nblk;
   k_wrap_bin<<<nb, kBlock, 0, c->stream>>>(n, c->pos, c->id, c->cell, c->rank,
                                            c->count, c->cell_rank, c->g, c->ctrl);
-  k_scan<<<1, kScanThreads, 0, c->stream>>>(c->g.ncells, c->count, c->start,
-                                            c->ctrl);
+  launch_scan(c, c->g.ncells, c->count, c->start);
   k_scatter<<<nb, kBlock, 0, c->stream>>>(n, c->cell, c->rank, c->start,
                                           c->cell_rank, c->perm, c->ctrl);
-  k_sort_cells<<<blocks_for(c->g.ncells, kBlock), kBlock, 0, c->stream>>>(
+  k_sort_cells<<<blocks_for(static_cast<int64_t>(c->g.ncells) * 32, kBlock), kBlock, 0,
+                 c->stream>>>(
       c->g.ncells, c->start, c->perm, c->id, c->ctrl);
   k_permute<<<nb, kBlock, 0, c->stream>>>(n, c->perm, c->pos, c->vx, c->vy,
                                           c->vz, c->mass, c->id, c->cell,
@@ -253,8 +263,7 @@ void launch_resort(tmd_gpu_ctx* c) {
   // list groups per brick (32 particles each), scanned into group offsets
   k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->stream>>>(
       c->bg.nbricks, c->brick_rank_off, c->start, c->ngroups, c->ctrl);
-  k_scan<<<1, kScanThreads, 0, c->stream>>>(c->bg.nbricks, c->ngroups, c->group_off,
-                                            c->ctrl);
+  launch_scan(c, c->bg.nbricks, c->ngroups, c->group_off);
 }
 
 size_t build_smem(const tmd_gpu_ctx* c) {
@@ -704,6 +713,8 @@ void upload_bricks(tmd_gpu_ctx* c) {
   c->brick_rank_off = dalloc<int>(c->h_brick_off.size());
   c->ngroups = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
   c->group_off = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
+  c->scan_tmp = dalloc<int>(static_cast<size_t>(
+      blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1));
   ck(cudaMemcpy(c->cell_rank, c->h_rank.data(), c->h_rank.size() * sizeof(int),
                 cudaMemcpyHostToDevice), "H2D cell_rank");
   ck(cudaMemcpy(c->brick_rank_off, c->h_brick_off.data(), c->h_brick_off.size() * sizeof(int),

@@ -175,28 +175,24 @@ __global__ void __launch_bounds__(kBlock)
 
 // Exclusive scan of the cell histogram (one block; runs once per rebuild).
 // Zeroes the histogram for the next resort.
+// Tiled 3-phase exclusive scan (tile = 1024 threads x 4 items): per-tile
+// sums, one-block scan of the tile sums, tile-local scan + offset. Runs once
+// per rebuild; zeroes the histogram for the next resort.
 constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads)
-    k_scan(int ncells, int* __restrict__ count, int* __restrict__ start,
-           Ctrl* ctrl) {
-  if (!ctrl->rebuild) return;
-  __shared__ int warp_tot[kScanThreads / 32];
-  const int t = threadIdx.x;
-  const int per = (ncells + kScanThreads - 1) / kScanThreads;
-  const int b = min(t * per, ncells), e = min(b + per, ncells);
-  int s = 0;
-  for (int c = b; c < e; ++c) s += count[c];
-  // block exclusive scan of s
-  const int lane = t & 31, warp = t >> 5;
-  int v = s;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
   for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += u;
+    const int u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
   }
-  if (lane == 31) warp_tot[warp] = v;
+  if (lane == 31) warp_tot[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = warp_tot[lane];
+    int w = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0;
     for (int o = 1; o < 32; o <<= 1) {
       const int u = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += u;
@@ -204,14 +200,65 @@ __global__ void __launch_bounds__(kScanThreads)
     warp_tot[lane] = w;
   }
   __syncthreads();
-  int run = v - s + (warp > 0 ? warp_tot[warp - 1] : 0);
-  for (int c = b; c < e; ++c) {
-    const int k = count[c];
-    start[c] = run;
-    run += k;
-    count[c] = 0;
+  total = warp_tot[(blockDim.x >> 5) - 1];
+  const int r = x - v + (warp > 0 ? warp_tot[warp - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_tiles(int n, const int* __restrict__ count, int* __restrict__ tile_sum,
+                 Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  __shared__ int warp_tot[32];
+  const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  int s = 0;
+#pragma unroll
+  for (int u = 0; u < kScanItems; ++u) s += base + u < n ? count[base + u] : 0;
+  int total;
+  block_excl_scan(s, warp_tot, total);
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_sums(int ntiles, int* __restrict__ tile_sum, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  __shared__ int warp_tot[32];
+  int carry = 0;
+  for (int t0 = 0; t0 < ntiles; t0 += kScanThreads) {
+    const int t = t0 + threadIdx.x;
+    const int v = t < ntiles ? tile_sum[t] : 0;
+    int total;
+    const int r = block_excl_scan(v, warp_tot, total);
+    if (t < ntiles) tile_sum[t] = carry + r;
+    carry += total;
   }
-  if (t == kScanThreads - 1) start[ncells] = run;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_apply(int n, int* __restrict__ count, const int* __restrict__ tile_off,
+                 int* __restrict__ start, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  __shared__ int warp_tot[32];
+  const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  int v[kScanItems];
+  int s = 0;
+#pragma unroll
+  for (int u = 0; u < kScanItems; ++u) {
+    v[u] = base + u < n ? count[base + u] : 0;
+    s += v[u];
+  }
+  int total;
+  int run = tile_off[blockIdx.x] + block_excl_scan(s, warp_tot, total);
+#pragma unroll
+  for (int u = 0; u < kScanItems; ++u) {
+    if (base + u < n) {
+      start[base + u] = run;
+      count[base + u] = 0;
+    }
+    run += v[u];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanThreads - 1) start[n] = run;
 }
 
 __global__ void __launch_bounds__(kBlock)
@@ -231,9 +278,26 @@ __global__ void __launch_bounds__(kBlock)
     k_sort_cells(int ncells, const int* __restrict__ start, int* __restrict__ perm,
                  const long long* __restrict__ id, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
-  const int c = blockIdx.x * kBlock + threadIdx.x;
+  // one warp per cell: cells of <= 32 particles are ranked in registers (rank =
+  // number of smaller ids, ids are unique), larger ones fall back to lane 0
+  const int c = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (c >= ncells) return;
   const int b = start[c], e = start[c + 1];
+  const int m = e - b;
+  if (m <= 32) {
+    const int p = lane < m ? perm[b + lane] : 0;
+    const long long key = lane < m ? id[p] : 0;
+    int rank = 0;
+    for (int q = 0; q < m; ++q) {
+      const long long kq = __shfl_sync(0xffffffffu, key, q);
+      rank += (kq < key) ? 1 : 0;
+    }
+    __syncwarp();
+    if (lane < m) perm[b + rank] = p;
+    return;
+  }
+  if (lane != 0) return;
   for (int k = b + 1; k < e; ++k) {
     const int pk = perm[k];
     const long long key = id[pk];

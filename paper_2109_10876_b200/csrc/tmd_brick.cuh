@@ -21,6 +21,7 @@
 #pragma once
 
 #include "tmd_device.cuh"
+#include "tmd_kernels.cuh"
 
 namespace tmd {
 
@@ -773,6 +774,7 @@ __device__ __forceinline__ void lj_accumulate(const double4& pi, double xj, doub
   }
 }
 
+template <int kMode>
 __global__ void __launch_bounds__(kForceThreads)
     k_forces_brick(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
                    const int* __restrict__ brick_rank_off, const int* __restrict__ start,
@@ -780,7 +782,7 @@ __global__ void __launch_bounds__(kForceThreads)
                    const uint32_t* __restrict__ list, const int* __restrict__ nnbr,
                    double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                    double* __restrict__ part_e, double* __restrict__ part_w,
-                   const long long* __restrict__ id, Ctrl* ctrl) {
+                   const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
   extern __shared__ double s_d[];
   __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
   __shared__ uint32_t s_code[kMaxHalo];
@@ -793,7 +795,7 @@ __global__ void __launch_bounds__(kForceThreads)
   double* sx = s_d;
   double* sy = s_d + sc;
   double* sz = s_d + 2 * sc;
-  double e = 0.0, w = 0.0;
+  double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
   if (ht.total <= bg.stage_cap) {  // (the build flags an overfull halo)
     for (int k = threadIdx.x; k < sc; k += kForceThreads) {
       double x = kFarD, y = kFarD, z = kFarD;
@@ -860,6 +862,7 @@ __global__ void __launch_bounds__(kForceThreads)
         fx[i] = ax;
         fy[i] = ay;
         fz[i] = az;
+        integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
       }
     }
   }
@@ -869,6 +872,7 @@ __global__ void __launch_bounds__(kForceThreads)
     part_e[b] = te;
     part_w[b] = tw;
   }
+  integrate_block<kMode, kForceThreads>(ke, d2, red, it, ctrl);
 }
 
 // ---------------------------------------------------------------------------
@@ -877,16 +881,16 @@ __global__ void __launch_bounds__(kForceThreads)
 // chunk of 8 entries is two 16-B loads; each gather is one 256-bit
 // LDG.E.ENL2.256 of the packed position (one L1 sector request per entry).
 // No staging, no shared memory: occupancy is register-limited only.
-template <int kUnroll>
+template <int kUnroll, int kMode>
 __global__ void __launch_bounds__(128)
     k_forces_l1(int n, const double4* __restrict__ pos, const uint32_t* __restrict__ list,
                 const int* __restrict__ nnbr, int cap, Geom g, LjConst lj,
                 double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                 double* __restrict__ part_e, double* __restrict__ part_w,
-                const long long* __restrict__ id, Ctrl* ctrl) {
+                const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
   __shared__ double red[4];
   const int i = blockIdx.x * 128 + threadIdx.x;
-  double e = 0.0, w = 0.0;
+  double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
   if (i < n) {
     const double4 pi = pos[i];
     const int cnt = nnbr[i];
@@ -924,6 +928,7 @@ __global__ void __launch_bounds__(128)
     fx[i] = ax;
     fy[i] = ay;
     fz[i] = az;
+    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
   }
   const double te = block_sum<128>(e, red);
   const double tw = block_sum<128>(w, red);
@@ -931,6 +936,7 @@ __global__ void __launch_bounds__(128)
     part_e[blockIdx.x] = te;
     part_w[blockIdx.x] = tw;
   }
+  integrate_block<kMode, 128>(ke, d2, red, it, ctrl);
 }
 
 // Tap for variant 3: chunked global-slot list -> ELL-transposed copy.

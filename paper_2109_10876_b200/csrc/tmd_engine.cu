@@ -94,6 +94,8 @@ struct tmd_gpu_ctx {
 
   // particle arrays (cell-sorted) + alternates for the permutation
   double4 *pos = nullptr, *pos2 = nullptr, *snap = nullptr;
+  double4* posb[2] = {nullptr, nullptr};  // ping-pong position buffers; pos = posb[cur]
+  int cur = 0;
   double *vx = nullptr, *vy = nullptr, *vz = nullptr;
   double *vx2 = nullptr, *vy2 = nullptr, *vz2 = nullptr;
   double *fx = nullptr, *fy = nullptr, *fz = nullptr;
@@ -155,7 +157,7 @@ struct tmd_gpu_ctx {
 namespace {
 
 void free_all(tmd_gpu_ctx* c) {
-  void* ptrs[] = {c->pos,  c->pos2,  c->snap, c->vx,    c->vy,      c->vz,
+  void* ptrs[] = {c->posb[0], c->posb[1], c->pos2, c->snap, c->vx, c->vy, c->vz,
                   c->vx2,  c->vy2,   c->vz2,  c->fx,    c->fy,      c->fz,
                   c->mass, c->mass2, c->id,   c->id2,   c->cell,    c->cell2,
                   c->rank, c->perm,  c->count, c->start, c->nbr,    c->nnbr,
@@ -278,7 +280,12 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
                           static_cast<int>(build_smem(c))), "smem attr build");
   ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(build_smem(c))), "smem attr build");
-  ck(cudaFuncSetAttribute(k_forces_brick, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ck(cudaFuncSetAttribute(k_forces_brick<kForcesOnly>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(force_smem(c))), "smem attr forces");
+  ck(cudaFuncSetAttribute(k_forces_brick<kKick2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(force_smem(c))), "smem attr forces");
+  ck(cudaFuncSetAttribute(k_forces_brick<kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(force_smem(c))), "smem attr forces");
 }
 
@@ -300,26 +307,57 @@ void launch_build(tmd_gpu_ctx* c) {
   }
 }
 
-void launch_forces(tmd_gpu_ctx* c) {
-  c->launches += 1;
+template <int kMode>
+void launch_forces_mode(tmd_gpu_ctx* c) {
+  Integ it;
+  it.vx = c->vx;
+  it.vy = c->vy;
+  it.vz = c->vz;
+  it.mass = c->mass;
+  it.id = c->id;
+  it.snap = c->snap;
+  it.pos_out = c->posb[c->cur ^ 1];
+  it.dt = c->dt;
+  it.half_dt = c->half_dt;
+  it.part_ke = c->part_ke;
   if (c->variant == 1) {
-    k_lj_forces<<<c->nblk, kBlock, 0, c->stream>>>(
+    k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->stream>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
-        c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, c->ctrl);
+        c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else if (c->variant == 3) {
-    auto kern = c->unroll == 1 ? k_forces_l1<1> : (c->unroll == 2 ? k_forces_l1<2>
-                                                 : (c->unroll == 8 ? k_forces_l1<8>
-                                                                   : k_forces_l1<4>));
+    auto kern = c->unroll == 1 ? k_forces_l1<1, kMode>
+                               : (c->unroll == 2 ? k_forces_l1<2, kMode>
+                                                 : (c->unroll == 8 ? k_forces_l1<8, kMode>
+                                                                   : k_forces_l1<4, kMode>));
     kern<<<c->nblk, 128, 0, c->stream>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
-        c->fz, c->part_e, c->part_w, c->id, c->ctrl);
+        c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else {
-    k_forces_brick<<<c->bg.nbricks, kForceThreads, force_smem(c), c->stream>>>(
+    k_forces_brick<kMode><<<c->bg.nbricks, kForceThreads, force_smem(c), c->stream>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
-        c->lj, c->nbr, c->nnbr, c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id,
+        c->lj, c->nbr, c->nnbr, c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it,
         c->ctrl);
   }
 }
+
+// Forces at the current positions, optionally with the fused integrator
+// epilogue (kKick2: closing half-kick; kFused: closing half-kick + next
+// step's opening half-kick and drift into the other position buffer, after
+// which the buffers swap).
+void launch_forces(tmd_gpu_ctx* c, int mode = kForcesOnly) {
+  c->launches += 1;
+  if (mode == kFused) {
+    launch_forces_mode<kFused>(c);
+    c->cur ^= 1;
+    c->pos = c->posb[c->cur];
+  } else if (mode == kKick2) {
+    launch_forces_mode<kKick2>(c);
+  } else {
+    launch_forces_mode<kForcesOnly>(c);
+  }
+}
+
+int force_parts(const tmd_gpu_ctx* c) { return c->variant == 2 ? c->bg.nbricks : c->nblk; }
 
 void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
   c->launches += 1;
@@ -344,7 +382,7 @@ void launch_kick2(tmd_gpu_ctx* c) {
 
 void launch_reduce_pe(tmd_gpu_ctx* c) {
   c->launches += 2;
-  const int np = c->variant == 2 ? c->bg.nbricks : c->nblk;
+  const int np = force_parts(c);
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, np, 0.5, c->scalars + 0);
   k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, np, 0.5, c->scalars + 1);
 }
@@ -537,16 +575,11 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
       launch_build(c);
     }
     {
+      // forces + fused velocity-Verlet epilogue (closing half-kick of this
+      // step and, unless it is the last step of the chunk, the opening
+      // half-kick + drift of the next); booked to Forces
       Phase p(c, TMD_SECTION_FORCES);
-      launch_forces(c);
-    }
-    {
-      Phase p(c, TMD_SECTION_INTEGRATE);
-      if (s + 1 < steps) {
-        launch_kick_drift(c, true);
-      } else {
-        launch_kick2(c);
-      }
+      launch_forces(c, s + 1 < steps ? kFused : kKick2);
     }
   }
   launch_reduce_pe(c);
@@ -806,7 +839,11 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     }
 
     const size_t n = static_cast<size_t>(c->n);
-    c->pos = dalloc<double4>(n + 1);  // slot n: far-away sentinel (variant 3 padding)
+    // slot n of both buffers: far-away sentinel (variant 3 list padding)
+    c->posb[0] = dalloc<double4>(n + 1);
+    c->posb[1] = dalloc<double4>(n + 1);
+    c->cur = 0;
+    c->pos = c->posb[0];
     c->pos2 = dalloc<double4>(n);
     c->snap = dalloc<double4>(n);
     c->vx = dalloc<double>(n); c->vy = dalloc<double>(n); c->vz = dalloc<double>(n);
@@ -822,7 +859,7 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     c->nparts = std::max(c->nblk, c->bg.nbricks);
     c->part_e = dalloc<double>(c->nparts);
     c->part_w = dalloc<double>(c->nparts);
-    c->part_ke = dalloc<double>(c->nblk);
+    c->part_ke = dalloc<double>(c->nparts);
     upload_bricks(c);
     c->scalars = dalloc<double>(4);
     c->ctrl = dalloc<Ctrl>(1);
@@ -855,8 +892,10 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
       if (sys->mass) hm[k] = sys->mass[k];
     }
     hp.push_back(make_double4(kFarD, kFarD, kFarD, 0.0));
-    ck(cudaMemcpy(c->pos, hp.data(), (n + 1) * sizeof(double4), cudaMemcpyHostToDevice),
+    ck(cudaMemcpy(c->posb[0], hp.data(), (n + 1) * sizeof(double4), cudaMemcpyHostToDevice),
        "H2D pos");
+    ck(cudaMemcpy(c->posb[1] + n, &hp[n], sizeof(double4), cudaMemcpyHostToDevice),
+       "H2D sentinel");
     ck(cudaMemcpy(c->vx, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
     ck(cudaMemcpy(c->vy, hv.data() + n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vy");
     ck(cudaMemcpy(c->vz, hv.data() + 2 * n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vz");

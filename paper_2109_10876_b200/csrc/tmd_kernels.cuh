@@ -22,6 +22,83 @@ __device__ __forceinline__ void kick(double& v, double f, double inv_m,
   v = __dadd_rn(v, __dmul_rn(__dmul_rn(f, inv_m), half_dt));
 }
 
+// ---------------------------------------------------------------------------
+// Velocity-Verlet epilogue fused into the force kernels. Modes:
+//   kForcesOnly  f only (compute_forces, setup)
+//   kKick2       f, then the closing half-kick of the step
+//                (thermostat_and_half_kick without thermostat, engine.hpp:209-239)
+//   kFused       f, closing half-kick of step n, then opening half-kick +
+//                drift of step n+1 (half_kick_and_drift, engine.hpp:174-189)
+//                into the OTHER position buffer (ping-pong: other CTAs are
+//                still gathering the current positions), with the rebuild
+//                displacement test of step n+1 (max_displacement2,
+//                neighbor_list.hpp:114-136) reduced on the fly.
+// Kinetic-energy partials are of the post-kick2 velocities (what observe()
+// reports after the step). Arithmetic order mirrors the reference.
+enum : int { kForcesOnly = 0, kKick2 = 1, kFused = 2 };
+
+struct Integ {
+  double* vx;
+  double* vy;
+  double* vz;
+  const double* mass;
+  const long long* id;
+  const double4* snap;
+  double4* pos_out;
+  double dt, half_dt;
+  double* part_ke;
+};
+
+template <int kMode>
+__device__ __forceinline__ void integrate_one(int i, const double4& pi, double gx, double gy,
+                                              double gz, const Integ& it, Ctrl* ctrl,
+                                              double& ke, double& d2) {
+  if (kMode == kForcesOnly) return;
+  const double m = it.mass[i];
+  const double inv_m = __ddiv_rn(1.0, m);
+  double ux = it.vx[i], uy = it.vy[i], uz = it.vz[i];
+  kick(ux, gx, inv_m, it.half_dt);
+  kick(uy, gy, inv_m, it.half_dt);
+  kick(uz, gz, inv_m, it.half_dt);
+  if (!finite3(ux, uy, uz) || !finite3(gx, gy, gz)) {
+    record_error(ctrl, kStatNonFinite, it.id[i], -1);
+  }
+  ke += __dmul_rn(__dmul_rn(0.5, m),
+                  __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)),
+                            __dmul_rn(uz, uz)));
+  if (kMode == kFused) {
+    kick(ux, gx, inv_m, it.half_dt);
+    kick(uy, gy, inv_m, it.half_dt);
+    kick(uz, gz, inv_m, it.half_dt);
+    double4 p;
+    p.x = __dadd_rn(pi.x, __dmul_rn(ux, it.dt));
+    p.y = __dadd_rn(pi.y, __dmul_rn(uy, it.dt));
+    p.z = __dadd_rn(pi.z, __dmul_rn(uz, it.dt));
+    p.w = 0.0;
+    it.pos_out[i] = p;
+    const double4 s = it.snap[i];
+    d2 = fmax(d2, exact_r2(__dsub_rn(p.x, s.x), __dsub_rn(p.y, s.y), __dsub_rn(p.z, s.z)));
+  }
+  it.vx[i] = ux;
+  it.vy[i] = uy;
+  it.vz[i] = uz;
+}
+
+// Block-level reductions of the epilogue (all threads of the block call it).
+template <int kMode, int kThreads>
+__device__ __forceinline__ void integrate_block(double ke, double d2, double* red,
+                                                const Integ& it, Ctrl* ctrl) {
+  if (kMode == kForcesOnly) return;
+  const double t = block_sum<kThreads>(ke, red);
+  if (threadIdx.x == 0) it.part_ke[blockIdx.x] = t;
+  if (kMode == kFused) {
+    for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+    if ((threadIdx.x & 31) == 0 && d2 > 0.0) {
+      atomicMax(&ctrl->max_d2, static_cast<unsigned long long>(__double_as_longlong(d2)));
+    }
+  }
+}
+
 // kick2 of the previous step (optional, fused) + kick1 + drift of this step.
 // With kFused the kernel also emits the kinetic-energy partials of the
 // post-kick2 velocities and performs the non-finite check of
@@ -441,16 +518,17 @@ __global__ void k_build_prologue(Ctrl* ctrl) {
 // r2 are rounded exactly like the reference; the force arithmetic uses one
 // reciprocal. Per-block partials of sum_i e_i and sum_i w_i (each pair counted
 // twice; the final reduction halves them).
+template <int kMode>
 __global__ void __launch_bounds__(kBlock)
     k_lj_forces(int n, const double4* __restrict__ pos,
                 const uint32_t* __restrict__ nbr, const int* __restrict__ nnbr,
                 int stride, Geom g, LjConst lj, double* __restrict__ fx,
                 double* __restrict__ fy, double* __restrict__ fz,
                 double* __restrict__ part_e, double* __restrict__ part_w,
-                const long long* __restrict__ id, Ctrl* ctrl) {
+                const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
   __shared__ double red[kBlock / 32];
   const int i = blockIdx.x * kBlock + threadIdx.x;
-  double e = 0.0, w = 0.0;
+  double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
   if (i < n) {
     const double4 pi = pos[i];
     double ax = 0.0, ay = 0.0, az = 0.0;
@@ -481,6 +559,7 @@ __global__ void __launch_bounds__(kBlock)
     fx[i] = ax;
     fy[i] = ay;
     fz[i] = az;
+    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
   }
   const double te = block_sum<kBlock>(e, red);
   const double tw = block_sum<kBlock>(w, red);
@@ -488,6 +567,7 @@ __global__ void __launch_bounds__(kBlock)
     part_e[blockIdx.x] = te;
     part_w[blockIdx.x] = tw;
   }
+  integrate_block<kMode, kBlock>(ke, d2, red, it, ctrl);
 }
 
 // Deterministic final reduction of per-block partials (fixed order tree).

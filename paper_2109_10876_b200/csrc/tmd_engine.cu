@@ -152,11 +152,42 @@ struct tmd_gpu_ctx {
   std::vector<int> h_rebuild_log;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   uint64_t launches = 0;  // kernels enqueued by this context (bench accounting)
+
+  // CUDA-graph execution of whole step blocks (used when section timers are
+  // off): one graph = kick1+drift, kGraphSteps x [decide, IF(rebuild){resort,
+  // list build}, forces + fused integrator], PE reduction. The rebuild branch
+  // is a conditional graph node whose condition the decide kernel sets on the
+  // device, so skipped rebuilds cost nothing and nothing waits for the host.
+  cudaStream_t ls = nullptr;    // stream the launch wrappers enqueue on
+  cudaStream_t side = nullptr;  // capture stream for conditional bodies
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    uint64_t fixed = 0;  // kernels per launch outside the IF bodies
+  };
+  StepGraph sg[2][2];  // [block of kGraphSteps | single step][starting buffer parity]
+  bool graph_dirty = true;
+  bool use_graphs = true;
+  uint64_t graph_body_kernels = 0;   // kernels per executed IF body
+  unsigned long long cond_handle = 0;  // handle the next decide sets (0: none)
 };
 
 namespace {
 
+void drop_graphs(tmd_gpu_ctx* c) {
+  for (auto& row : c->sg) {
+    for (auto& s : row) {
+      if (s.exec) cudaGraphExecDestroy(s.exec);
+      if (s.graph) cudaGraphDestroy(s.graph);
+      s = tmd_gpu_ctx::StepGraph{};
+    }
+  }
+  c->graph_dirty = false;
+}
+
 void free_all(tmd_gpu_ctx* c) {
+  drop_graphs(c);
+  if (c->side) cudaStreamDestroy(c->side);
   void* ptrs[] = {c->posb[0], c->posb[1], c->pos2, c->snap, c->vx, c->vy, c->vz,
                   c->vx2,  c->vy2,   c->vz2,  c->fx,    c->fy,      c->fz,
                   c->mass, c->mass2, c->id,   c->id2,   c->cell,    c->cell2,
@@ -228,42 +259,42 @@ void harvest_timers(tmd_gpu_ctx* c) {
 // --- kernel launch wrappers -------------------------------------------------
 void launch_decide(tmd_gpu_ctx* c, bool advance, int log_idx = -1) {
   c->launches += 1;
-  k_decide<<<1, 1, 0, c->stream>>>(c->ctrl, c->g.rebuild_thr, advance ? 1 : 0,
-                                   log_idx >= 0 ? c->rebuild_log : nullptr,
-                                   log_idx);
+  k_decide<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr, advance ? 1 : 0,
+                               log_idx >= 0 ? c->rebuild_log : nullptr, log_idx,
+                               c->cond_handle);
 }
 
 // Exclusive scan of counts[0..n) into out[0..n] (3 tiled kernels).
 void launch_scan(tmd_gpu_ctx* c, int n, int* counts, int* out) {
   c->launches += 3;
   const int tiles = blocks_for(n, kScanTile);
-  k_scan_tiles<<<tiles, kScanThreads, 0, c->stream>>>(n, counts, c->scan_tmp, c->ctrl);
-  k_scan_sums<<<1, kScanThreads, 0, c->stream>>>(tiles, c->scan_tmp, c->ctrl);
-  k_scan_apply<<<tiles, kScanThreads, 0, c->stream>>>(n, counts, c->scan_tmp, out, c->ctrl);
+  k_scan_tiles<<<tiles, kScanThreads, 0, c->ls>>>(n, counts, c->scan_tmp, c->ctrl);
+  k_scan_sums<<<1, kScanThreads, 0, c->ls>>>(tiles, c->scan_tmp, c->ctrl);
+  k_scan_apply<<<tiles, kScanThreads, 0, c->ls>>>(n, counts, c->scan_tmp, out, c->ctrl);
 }
 
 void launch_resort(tmd_gpu_ctx* c) {
   c->launches += 6;
   const int n = static_cast<int>(c->n);
   const int nb = c->nblk;
-  k_wrap_bin<<<nb, kBlock, 0, c->stream>>>(n, c->pos, c->id, c->cell, c->rank,
+  k_wrap_bin<<<nb, kBlock, 0, c->ls>>>(n, c->pos, c->id, c->cell, c->rank,
                                            c->count, c->cell_rank, c->g, c->ctrl);
   launch_scan(c, c->g.ncells, c->count, c->start);
-  k_scatter<<<nb, kBlock, 0, c->stream>>>(n, c->cell, c->rank, c->start,
+  k_scatter<<<nb, kBlock, 0, c->ls>>>(n, c->cell, c->rank, c->start,
                                           c->cell_rank, c->perm, c->ctrl);
   k_sort_cells<<<blocks_for(static_cast<int64_t>(c->g.ncells) * 32, kBlock), kBlock, 0,
-                 c->stream>>>(
+                 c->ls>>>(
       c->g.ncells, c->start, c->perm, c->id, c->ctrl);
-  k_permute<<<nb, kBlock, 0, c->stream>>>(n, c->perm, c->pos, c->vx, c->vy,
+  k_permute<<<nb, kBlock, 0, c->ls>>>(n, c->perm, c->pos, c->vx, c->vy,
                                           c->vz, c->mass, c->id, c->cell,
                                           c->pos2, c->vx2, c->vy2, c->vz2,
                                           c->mass2, c->id2, c->cell2, c->ctrl);
-  k_copy_back<<<nb, kBlock, 0, c->stream>>>(n, c->pos2, c->vx2, c->vy2,
+  k_copy_back<<<nb, kBlock, 0, c->ls>>>(n, c->pos2, c->vx2, c->vy2,
                                             c->vz2, c->mass2, c->id2, c->cell2,
                                             c->pos, c->vx, c->vy, c->vz,
                                             c->mass, c->id, c->cell, c->ctrl);
   // list groups per brick (32 particles each), scanned into group offsets
-  k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->stream>>>(
+  k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->ls>>>(
       c->bg.nbricks, c->brick_rank_off, c->start, c->ngroups, c->ctrl);
   launch_scan(c, c->bg.nbricks, c->ngroups, c->group_off);
 }
@@ -276,6 +307,7 @@ size_t force_smem(const tmd_gpu_ctx* c) {
 }
 
 void set_smem_attrs(tmd_gpu_ctx* c) {
+  c->graph_dirty = true;
   ck(cudaFuncSetAttribute(k_build_brick3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(build_smem(c))), "smem attr build");
   ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -291,17 +323,17 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
 
 void launch_build(tmd_gpu_ctx* c) {
   c->launches += 2;
-  k_build_prologue<<<1, 1, 0, c->stream>>>(c->ctrl);
+  k_build_prologue<<<1, 1, 0, c->ls>>>(c->ctrl);
   if (c->variant == 1) {
-    k_build_list<<<c->nblk, kBlock, 0, c->stream>>>(
+    k_build_list<<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->stride, c->cap, c->snap, c->ctrl);
   } else if (c->variant == 3) {
-    k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+    k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n), c->ctrl);
   } else {
-    k_build_brick3<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->stream>>>(
+    k_build_brick3<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->nbr, c->nnbr, c->snap, 0u, c->ctrl);
   }
@@ -321,7 +353,7 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
   it.half_dt = c->half_dt;
   it.part_ke = c->part_ke;
   if (c->variant == 1) {
-    k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->stream>>>(
+    k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
         c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else if (c->variant == 3) {
@@ -329,11 +361,11 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
                                : (c->unroll == 2 ? k_forces_l1<2, kMode>
                                                  : (c->unroll == 8 ? k_forces_l1<8, kMode>
                                                                    : k_forces_l1<4, kMode>));
-    kern<<<c->nblk, 128, 0, c->stream>>>(
+    kern<<<c->nblk, 128, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
         c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else {
-    k_forces_brick<kMode><<<c->bg.nbricks, kForceThreads, force_smem(c), c->stream>>>(
+    k_forces_brick<kMode><<<c->bg.nbricks, kForceThreads, force_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->lj, c->nbr, c->nnbr, c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it,
         c->ctrl);
@@ -363,11 +395,11 @@ void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
   c->launches += 1;
   const int n = static_cast<int>(c->n);
   if (fused) {
-    k_kick_drift<true><<<c->nblk, kBlock, 0, c->stream>>>(
+    k_kick_drift<true><<<c->nblk, kBlock, 0, c->ls>>>(
         n, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
         c->snap, c->dt, c->half_dt, c->part_ke, c->ctrl);
   } else {
-    k_kick_drift<false><<<c->nblk, kBlock, 0, c->stream>>>(
+    k_kick_drift<false><<<c->nblk, kBlock, 0, c->ls>>>(
         n, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
         c->snap, c->dt, c->half_dt, c->part_ke, c->ctrl);
   }
@@ -375,7 +407,7 @@ void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
 
 void launch_kick2(tmd_gpu_ctx* c) {
   c->launches += 1;
-  k_kick2<<<c->nblk, kBlock, 0, c->stream>>>(
+  k_kick2<<<c->nblk, kBlock, 0, c->ls>>>(
       static_cast<int>(c->n), c->vx, c->vy, c->vz, c->fx, c->fy, c->fz,
       c->mass, c->id, c->half_dt, c->part_ke, c->ctrl);
 }
@@ -383,13 +415,13 @@ void launch_kick2(tmd_gpu_ctx* c) {
 void launch_reduce_pe(tmd_gpu_ctx* c) {
   c->launches += 2;
   const int np = force_parts(c);
-  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_e, np, 0.5, c->scalars + 0);
-  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_w, np, 0.5, c->scalars + 1);
+  k_reduce<<<1, kRedThreads, 0, c->ls>>>(c->part_e, np, 0.5, c->scalars + 0);
+  k_reduce<<<1, kRedThreads, 0, c->ls>>>(c->part_w, np, 0.5, c->scalars + 1);
 }
 
 void launch_reduce_ke(tmd_gpu_ctx* c) {
   c->launches += 1;
-  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->part_ke, c->nblk, 1.0,
+  k_reduce<<<1, kRedThreads, 0, c->ls>>>(c->part_ke, c->nblk, 1.0,
                                              c->scalars + 2);
 }
 
@@ -448,6 +480,7 @@ void set_cap_in_ctrl(tmd_gpu_ctx* c) {
 int round8(int v) { return (v + 7) / 8 * 8; }
 
 void alloc_list(tmd_gpu_ctx* c, int cap) {
+  c->graph_dirty = true;  // captured kernels hold the old list pointer / capacity
   if (c->nbr) cudaFree(c->nbr);
   c->nbr = nullptr;
   c->cap = round8(std::max(cap, 8));
@@ -556,7 +589,72 @@ constexpr int64_t kChunk = 256;
 
 // Runs `steps` steps as one device-resident chunk. Returns false when the
 // list overflowed (state is then garbage; the caller rolls back).
-bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
+constexpr int kGraphSteps = 15;  // odd: the ping-pong parity is unchanged per graph
+
+// Captures one block of `nsteps` steps (odd; starting at buffer parity
+// c->cur) as a CUDA graph whose rebuild branches are conditional IF nodes.
+// Splitting a run into such blocks is bitwise identical to the eager
+// sequence: the closing and opening half-kicks are the same two roundings
+// whether they run in one fused epilogue or in two kernels.
+void capture_graph(tmd_gpu_ctx* c, int nsteps, tmd_gpu_ctx::StepGraph& out) {
+  const int p = c->cur;
+  cudaGraph_t g = nullptr;
+  ck(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+  const uint64_t l0 = c->launches;
+  ck(cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal),
+     "begin capture");
+  c->ls = c->stream;
+  launch_kick_drift(c, false);
+  uint64_t body = 0;
+  for (int s = 0; s < nsteps; ++s) {
+    cudaGraphConditionalHandle h;
+    ck(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault),
+       "cudaGraphConditionalHandleCreate");
+    c->cond_handle = h;
+    launch_decide(c, true);
+    c->cond_handle = 0;
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    ck(cudaStreamGetCaptureInfo(c->stream, &st, nullptr, nullptr, &deps, &ndeps),
+       "cudaStreamGetCaptureInfo");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    ck(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp), "cudaGraphAddNode(conditional)");
+    const uint64_t b0 = c->launches;
+    ck(cudaStreamBeginCaptureToGraph(c->side, cp.conditional.phGraph_out[0], nullptr, nullptr,
+                                     0, cudaStreamCaptureModeThreadLocal),
+       "begin body capture");
+    c->ls = c->side;
+    launch_resort(c);
+    launch_build(c);
+    c->ls = c->stream;
+    cudaGraph_t bodyg;
+    ck(cudaStreamEndCapture(c->side, &bodyg), "end body capture");
+    body = c->launches - b0;
+    ck(cudaStreamUpdateCaptureDependencies(c->stream, &cnode, 1,
+                                           cudaStreamSetCaptureDependencies),
+       "cudaStreamUpdateCaptureDependencies");
+    launch_forces(c, s + 1 < nsteps ? kFused : kKick2);
+  }
+  launch_reduce_pe(c);
+  ck(cudaStreamEndCapture(c->stream, &g), "end capture");
+  ck(cudaGraphInstantiate(&out.exec, g, 0), "cudaGraphInstantiate");
+  out.graph = g;
+  c->graph_body_kernels = body;
+  out.fixed = (c->launches - l0) - static_cast<uint64_t>(nsteps) * body;
+  c->launches = l0;  // capture enqueued nothing
+  if (c->cur != p) throw CudaFail{"graph capture changed the buffer parity"};
+}
+
+// Enqueues `steps` steps without graphs: kick1+drift, then per step decide,
+// (gated) resort + list build, forces + fused integrator; PE reduction.
+void enqueue_segment(tmd_gpu_ctx* c, int64_t steps) {
   {
     Phase p(c, TMD_SECTION_INTEGRATE);
     launch_kick_drift(c, false);
@@ -583,6 +681,28 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
     }
   }
   launch_reduce_pe(c);
+}
+
+bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
+  const bool graphs = c->use_graphs && !c->timers_on;
+  if (graphs) {
+    if (c->graph_dirty) drop_graphs(c);
+    const long long rebuilds0 = c->h_ctrl->rebuilds;
+    int64_t left = steps;
+    while (left > 0) {
+      const int kind = left >= kGraphSteps ? 0 : 1;  // block of 15, or single steps
+      tmd_gpu_ctx::StepGraph& sgr = c->sg[kind][c->cur];
+      if (!sgr.exec) capture_graph(c, kind == 0 ? kGraphSteps : 1, sgr);
+      ck(cudaGraphLaunch(sgr.exec, c->stream), "cudaGraphLaunch");
+      c->launches += sgr.fixed;
+      left -= kind == 0 ? kGraphSteps : 1;
+    }
+    sync_ctrl(c);
+    c->launches += static_cast<uint64_t>(c->h_ctrl->rebuilds - rebuilds0) *
+                   c->graph_body_kernels;
+    return (c->h_ctrl->status & kOverflowBits) == 0;
+  }
+  enqueue_segment(c, steps);
   if (c->timers_on) {
     c->h_rebuild_log.resize(static_cast<size_t>(steps));
     ck(cudaMemcpyAsync(c->h_rebuild_log.data(), c->rebuild_log,
@@ -811,6 +931,9 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     }
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking),
        "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->ls = c->stream;
+    c->use_graphs = params->reserved[2] == 0;  // reserved[2] = 1 disables CUDA graphs
     ck(cudaEventCreate(&c->t0), "cudaEventCreate");
     ck(cudaEventCreate(&c->t1), "cudaEventCreate");
 
@@ -954,11 +1077,11 @@ const uint32_t* decoded_list(tmd_gpu_ctx* c) {
   }
   c->launches += 1;
   if (c->variant == 3) {
-    k_decode_chunked<<<c->nblk, 128, 0, c->stream>>>(static_cast<int>(c->n), c->nbr, c->nnbr,
+    k_decode_chunked<<<c->nblk, 128, 0, c->ls>>>(static_cast<int>(c->n), c->nbr, c->nnbr,
                                                      c->cap, c->decoded, c->stride);
     return c->decoded;
   }
-  k_decode_list<<<c->bg.nbricks, 128, 0, c->stream>>>(
+  k_decode_list<<<c->bg.nbricks, 128, 0, c->ls>>>(
       c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg, c->nbr,
       c->nnbr, c->decoded, c->stride);
   return c->decoded;
@@ -1040,7 +1163,7 @@ int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->launches += 1;
-    k_kinetic<<<c->nblk, kBlock, 0, c->stream>>>(static_cast<int>(c->n), c->vx,
+    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx,
                                                  c->vy, c->vz, c->mass,
                                                  c->part_ke);
     launch_reduce_ke(c);
@@ -1167,7 +1290,7 @@ int tmd_gpu_list_stats(tmd_gpu_ctx* c, tmd_list_stats* out) {
     unsigned long long* d = dalloc<unsigned long long>(1);
     ck(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream), "memset");
     c->launches += 1;
-    k_count_incut<<<c->nblk, kBlock, 0, c->stream>>>(
+    k_count_incut<<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, decoded_list(c), c->nnbr, c->stride, c->g,
         c->lj.rc2, d);
     unsigned long long h = 0;

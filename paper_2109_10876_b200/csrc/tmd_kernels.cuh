@@ -209,10 +209,11 @@ __global__ void __launch_bounds__(kBlock)
 // Rebuild decision (Engine::step, engine.hpp:88-100): global OR of
 // needs_rebuild == max |dx|^2 > 0.25 skin^2 (strict), plus a host override.
 __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
-                         int log_idx) {
+                         int log_idx, cudaGraphConditionalHandle cond) {
   const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
   const int r = (ctrl->force_rebuild != 0) || (m > thr);
   ctrl->rebuild = r;
+  if (cond != 0) cudaGraphSetConditional(cond, r ? 1u : 0u);  // graph mode: gate the IF node
   if (log) log[log_idx] = r;
   ctrl->force_rebuild = 0;
   ctrl->max_d2 = 0ull;

@@ -191,6 +191,91 @@ int tmd_gpu_fp64_peak(int device, double* tflops);
 
 void tmd_gpu_destroy(tmd_gpu_ctx* ctx);
 
+/* ---- z-slab decomposition (one context per GPU) --------------
+ * Replaces the reference's in-process subnode decomposition
+ * (decomp.hpp:47-118 make_subnode_decomposition / make_subnode_layouts,
+ * domain.hpp:54-92 distribute_records, decomp.hpp:142-200 build_ghost_plan /
+ * update_ghost_positions) for one process per GPU: the box is cut into slabs
+ * of whole z cell layers (range rule i*dims/s, decomp.hpp:87-93); a slab owns
+ * its layers plus one ghost layer per side. With a full neighbour list there
+ * is no reverse force pass (collect_ghost_forces, decomp.hpp:202-224).
+ *
+ * The caller moves the buffers between ranks (NCCL or device copies); every
+ * call returns with the context's stream drained. Sequence:
+ *   rebuild:  slab_decide(1, adv) -> slab_migrate_out -> [records to their
+ *             destinations] -> slab_migrate_in -> slab_commit ->
+ *             slab_border(0/1) -> [lower layer to rank-1's upper ghost, upper
+ *             layer to rank+1's lower ghost] -> slab_ghost_in -> [counts,
+ *             ids, positions] -> slab_ghosts_ready
+ *   step:     slab_forces(2) -> slab_halo -> [positions] -> slab_max_d2 ->
+ *             [max over ranks > 0.25 skin^2 ?] -> slab_decide(r, 1) -> ...
+ * Buffers: counts int32[dx*dy] (cells x-fastest), ids int64[n],
+ * positions double4[n] (x, y, z, unused), records info[9] bytes each. */
+
+/* Slab `rank` of `nranks` (nranks <= z cell layers, >= 3 layers); every
+ * rank passes the same whole system and keeps the particles in its layers.
+ * The context is not usable for forces before the first rebuild sequence. */
+int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
+                        const tmd_fene_params* fene, const tmd_engine_params* params,
+                        int rank, int nranks, tmd_gpu_ctx** out);
+
+/* info: rank, nranks, first owned z layer, owned layers, owned particles,
+ * lower ghosts, upper ghosts, cells per layer, slot capacity, record bytes. */
+int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[10]);
+
+/* Largest squared displacement since the last build over the owned particles
+ * (needs_rebuild's per-subnode max, neighbor_list.hpp:114-145). Raises any
+ * pending physics error. */
+int tmd_gpu_slab_max_d2(tmd_gpu_ctx* ctx, double* local_max_d2);
+
+/* Sets this step's rebuild decision (rebuild != 0 forces it); advance != 0
+ * counts a step (and a rebuild). */
+int tmd_gpu_slab_decide(tmd_gpu_ctx* ctx, int rebuild, int advance);
+
+/* Wraps every owned particle and moves the ones whose z layer another rank
+ * owns into a record buffer grouped by destination: counts[nranks] records
+ * per destination, *send the device buffer (destination-major). */
+int tmd_gpu_slab_migrate_out(tmd_gpu_ctx* ctx, int64_t* counts, void** send);
+
+/* Device buffer for nrecv incoming records (any source order). */
+int tmd_gpu_slab_migrate_in(tmd_gpu_ctx* ctx, int64_t nrecv, void** recv);
+
+/* Appends the received records, resorts the owned particles (cell-sorted,
+ * brick-major) and exports both boundary layers; nb[0] / nb[1] = particles
+ * in the lowest / highest owned layer. */
+int tmd_gpu_slab_commit(tmd_gpu_ctx* ctx, int64_t nb[2]);
+
+/* Device buffers of boundary layer `side` (0 lowest, 1 highest): per-cell
+ * counts, ids, positions. */
+int tmd_gpu_slab_border(tmd_gpu_ctx* ctx, int side, void** counts, void** ids,
+                        void** pos);
+
+/* Destination buffers (counts, ids, positions) of the lower ghost layer
+ * (n_lo particles, from rank-1's highest layer) and the upper one (n_hi,
+ * from rank+1's lowest layer). */
+int tmd_gpu_slab_ghost_in(tmd_gpu_ctx* ctx, int64_t n_lo, int64_t n_hi, void* lo[3],
+                          void* hi[3]);
+
+/* Ghost layers complete: cell ranges + neighbour-list build (grows on
+ * overflow). */
+int tmd_gpu_slab_ghosts_ready(tmd_gpu_ctx* ctx);
+
+/* Opening half-kick + drift of the owned particles (integrate.hpp:14-37). */
+int tmd_gpu_slab_kick_drift(tmd_gpu_ctx* ctx);
+
+/* Forces on the owned particles; mode 0 forces only, 1 + closing half-kick,
+ * 2 + closing half-kick + next opening half-kick and drift. */
+int tmd_gpu_slab_forces(tmd_gpu_ctx* ctx, int mode);
+
+/* Packs both boundary layers' current positions: send[0/1] -> rank-1 / rank+1
+ * (slab_commit's nb[] positions each); recv[0/1] <- rank-1 / rank+1 (the
+ * n_lo / n_hi ghost positions). */
+int tmd_gpu_slab_halo(tmd_gpu_ctx* ctx, void* send[2], void* recv[2]);
+
+/* This slab's potential energy, virial (of the last force call) and kinetic
+ * energy; the caller sums them over ranks. */
+int tmd_gpu_slab_sums(tmd_gpu_ctx* ctx, double out[3]);
+
 /* ---- host-side setup helpers (no GPU needed) ----------------------------
  * Synthetic inputs of the BASELINE.json shapes. FCC is absent from the
  * reference (generators.hpp has only simple cubic), see SURVEY §8(d). */

@@ -63,14 +63,17 @@ __device__ __forceinline__ void load_halo(int b, const Geom& g, const BrickGeom&
   const int bx = b % bg.nb[0];
   const int by = (b / bg.nb[0]) % bg.nb[1];
   const int bz = b / (bg.nb[0] * bg.nb[1]);
+  // slab mode: bricks tile the owned layers, which start at local layer 1
+  const int zoff = g.zslab ? 1 : 0;
+  const int zext = g.zslab ? g.zown : g.dims[2];
   ht.lo[0] = bx * bg.B[0];
   ht.lo[1] = by * bg.B[1];
-  ht.lo[2] = bz * bg.B[2];
+  ht.lo[2] = zoff + bz * bg.B[2];
+  ht.e[0] = min(bg.B[0], g.dims[0] - ht.lo[0]);
+  ht.e[1] = min(bg.B[1], g.dims[1] - ht.lo[1]);
+  ht.e[2] = min(bg.B[2], zext - (ht.lo[2] - zoff));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    ht.e[k] = min(bg.B[k], g.dims[k] - ht.lo[k]);
-    ht.H[k] = ht.e[k] + 2;
-  }
+  for (int k = 0; k < 3; ++k) ht.H[k] = ht.e[k] + 2;
   ht.n = ht.H[0] * ht.H[1] * ht.H[2];
   const int t = threadIdx.x;
   if (t < ht.n) {
@@ -81,8 +84,15 @@ __device__ __forceinline__ void load_halo(int b, const Geom& g, const BrickGeom&
     for (int k = 0; k < 3; ++k) {
       int raw = ht.lo[k] + h[k] - 1;
       uint32_t c2 = 0;
-      if (raw < 0) { raw += g.dims[k]; c2 = 2; }
-      else if (raw >= g.dims[k]) { raw -= g.dims[k]; c2 = 1; }
+      if (k == 2 && g.zslab) {  // local z: ghost layers carry the wrap shift
+        c2 = raw == 0 ? g.zcode_lo : (raw == g.ldz - 1 ? g.zcode_hi : 0u);
+      } else if (raw < 0) {
+        raw += g.dims[k];
+        c2 = 2;
+      } else if (raw >= g.dims[k]) {
+        raw -= g.dims[k];
+        c2 = 1;
+      }
       gc[k] = raw;
       code |= c2 << (25 + 2 * k);
     }

@@ -40,6 +40,7 @@ enum : int {
   kStatNonFinitePos = 4, // non-finite position at binning (domain.hpp:58-62)
   kStatOverflow = 8,     // neighbour list capacity exceeded -> host re-runs
   kStatStageOverflow = 16,  // a brick halo exceeded the staging capacity -> grow
+  kStatStray = 32,       // slab mode: a particle outside the slab at binning (bug)
 };
 
 struct LjConst {
@@ -49,11 +50,29 @@ struct LjConst {
 struct Geom {
   double L[3];
   double cell_len[3];
-  int dims[3];
-  int ncells;
+  int dims[3];       // GLOBAL cell grid (build_cell_grid)
+  int ncells;        // local cells: dims[0]*dims[1]*ldz
   double rv2;        // (r_cut + r_skin)^2, rounded as build_sorted_list does
   double rebuild_thr;  // 0.25 * r_skin * r_skin (needs_rebuild, nl.hpp:143)
+  // z-slab decomposition (multi-GPU). zslab = 0: the context owns
+  // the whole periodic box (local grid = global grid). zslab = 1: it owns
+  // global z-layers [z0, z0 + zown); local layer lz = global - z0 + 1, and
+  // local layers 0 and zown + 1 are ghost layers holding copies of the
+  // neighbour slabs' boundary layers, with image codes zcode_lo / zcode_hi
+  // (the reference's ghost shift when the layer wraps the box, subnode.hpp:84-90).
+  int zslab;
+  int z0, zown, ldz;
+  unsigned int zcode_lo, zcode_hi;
+  int owned_cells;   // dims[0]*dims[1]*zown (cells ranked before the ghost layers)
 };
+
+// Local cell of a global cell (owned region; slab mode shifts z by one layer).
+__host__ __device__ __forceinline__ int local_cell(const Geom& g, int gcell) {
+  if (!g.zslab) return gcell;
+  const int dxy = g.dims[0] * g.dims[1];
+  const int cz = gcell / dxy;
+  return gcell - cz * dxy + (cz - g.z0 + 1) * dxy;
+}
 
 // Device control block: rebuild decision, counters and the error record.
 struct Ctrl {

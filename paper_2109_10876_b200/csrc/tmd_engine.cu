@@ -26,6 +26,7 @@
 #include "../../include/tmd_gpu.h"
 #include "tmd_kernels.cuh"
 #include "tmd_brick.cuh"
+#include "tmd_slab.cuh"
 
 using namespace tmd;
 
@@ -121,6 +122,26 @@ struct tmd_gpu_ctx {
   size_t decoded_words = 0;
   std::vector<int> h_rank, h_brick_off;  // host staging for upload_bricks
   int* scan_tmp = nullptr;               // tile sums of the tiled scan
+
+  // z-slab decomposition (one context per GPU of a multi-GPU job)
+  int64_t n_cap = 0;        // particle capacity (the whole system in slab mode)
+  int my_rank = 0, nranks = 1;
+  int64_t n_ghost = 0, n_ghost_lo = 0, n_ghost_hi = 0;
+  int* owner_of_z = nullptr;     // global z layer -> owning rank
+  int* mig_dest = nullptr;
+  int* mig_count = nullptr;      // [nranks] leavers per destination, then cursors
+  int* mig_off = nullptr;
+  int* mig_keep = nullptr;
+  tmd::MigRec* mig_send = nullptr;
+  tmd::MigRec* mig_recv = nullptr;
+  int64_t mig_nrecv = 0;
+  int* bidx[2] = {nullptr, nullptr};            // boundary-layer slots (down, up)
+  long long* bids[2] = {nullptr, nullptr};
+  double4* bpos[2] = {nullptr, nullptr};
+  int* bcnt[2] = {nullptr, nullptr};            // per-cell counts of the layers
+  int* boff[2] = {nullptr, nullptr};
+  int64_t nb[2] = {0, 0};
+  int* gcnt[2] = {nullptr, nullptr};            // received ghost-layer counts (lo, hi)
   double *part_e = nullptr, *part_w = nullptr, *part_ke = nullptr;
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
   Ctrl* ctrl = nullptr;
@@ -195,7 +216,10 @@ void free_all(tmd_gpu_ctx* c) {
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
                   c->rebuild_log, c->cell_rank, c->brick_rank_off, c->ngroups,
-                  c->group_off, c->decoded, c->scan_tmp};
+                  c->group_off, c->decoded, c->scan_tmp, c->owner_of_z, c->mig_dest,
+                  c->mig_count, c->mig_off, c->mig_keep, c->mig_send, c->mig_recv,
+                  c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
+                  c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1]};
   for (void* p : ptrs) {
     if (p) cudaFree(p);
   }
@@ -279,12 +303,12 @@ void launch_resort(tmd_gpu_ctx* c) {
   const int nb = c->nblk;
   k_wrap_bin<<<nb, kBlock, 0, c->ls>>>(n, c->pos, c->id, c->cell, c->rank,
                                            c->count, c->cell_rank, c->g, c->ctrl);
-  launch_scan(c, c->g.ncells, c->count, c->start);
+  launch_scan(c, c->g.owned_cells, c->count, c->start);
   k_scatter<<<nb, kBlock, 0, c->ls>>>(n, c->cell, c->rank, c->start,
-                                          c->cell_rank, c->perm, c->ctrl);
-  k_sort_cells<<<blocks_for(static_cast<int64_t>(c->g.ncells) * 32, kBlock), kBlock, 0,
+                                          c->cell_rank, c->g, c->perm, c->ctrl);
+  k_sort_cells<<<blocks_for(static_cast<int64_t>(c->g.owned_cells) * 32, kBlock), kBlock, 0,
                  c->ls>>>(
-      c->g.ncells, c->start, c->perm, c->id, c->ctrl);
+      c->g.owned_cells, c->start, c->perm, c->id, c->ctrl);
   k_permute<<<nb, kBlock, 0, c->ls>>>(n, c->perm, c->pos, c->vx, c->vy,
                                           c->vz, c->mass, c->id, c->cell,
                                           c->pos2, c->vx2, c->vy2, c->vz2,
@@ -331,7 +355,7 @@ void launch_build(tmd_gpu_ctx* c) {
   } else if (c->variant == 3) {
     k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
-        c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n), c->ctrl);
+        c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
   } else {
     k_build_brick3<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
@@ -405,12 +429,6 @@ void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
   }
 }
 
-void launch_kick2(tmd_gpu_ctx* c) {
-  c->launches += 1;
-  k_kick2<<<c->nblk, kBlock, 0, c->ls>>>(
-      static_cast<int>(c->n), c->vx, c->vy, c->vz, c->fx, c->fy, c->fz,
-      c->mass, c->id, c->half_dt, c->part_ke, c->ctrl);
-}
 
 void launch_reduce_pe(tmd_gpu_ctx* c) {
   c->launches += 2;
@@ -816,9 +834,12 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
 
 void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   BrickGeom& bg = c->bg;
+  // bricks tile the OWNED cells (local z offset 1 in slab mode)
+  const int ext[3] = {c->g.dims[0], c->g.dims[1], c->g.zown};
+  const int zoff = c->g.zslab ? 1 : 0;
   for (int k = 0; k < 3; ++k) {
-    bg.B[k] = std::min(2, c->g.dims[k]);
-    bg.nb[k] = (c->g.dims[k] + bg.B[k] - 1) / bg.B[k];
+    bg.B[k] = std::min(2, ext[k]);
+    bg.nb[k] = (ext[k] + bg.B[k] - 1) / bg.B[k];
     bg.origin_scale[k] = c->g.cell_len[k];
   }
   bg.nbricks = bg.nb[0] * bg.nb[1] * bg.nb[2];
@@ -829,12 +850,19 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   for (int b = 0; b < bg.nbricks; ++b) {
     const int bx = b % bg.nb[0], by = (b / bg.nb[0]) % bg.nb[1], bz = b / (bg.nb[0] * bg.nb[1]);
     c->h_brick_off[b] = r;
-    for (int z = bz * bg.B[2]; z < std::min((bz + 1) * bg.B[2], c->g.dims[2]); ++z)
-      for (int y = by * bg.B[1]; y < std::min((by + 1) * bg.B[1], c->g.dims[1]); ++y)
-        for (int x = bx * bg.B[0]; x < std::min((bx + 1) * bg.B[0], c->g.dims[0]); ++x)
-          c->h_rank[static_cast<size_t>(x + d0 * (y + d1 * z))] = r++;
+    for (int z = bz * bg.B[2]; z < std::min((bz + 1) * bg.B[2], ext[2]); ++z)
+      for (int y = by * bg.B[1]; y < std::min((by + 1) * bg.B[1], ext[1]); ++y)
+        for (int x = bx * bg.B[0]; x < std::min((bx + 1) * bg.B[0], ext[0]); ++x)
+          c->h_rank[static_cast<size_t>(x + d0 * (y + d1 * (z + zoff)))] = r++;
   }
   c->h_brick_off[bg.nbricks] = r;
+  if (c->g.zslab) {  // ghost layers ranked after every owned cell, x-fastest
+    const int dxy = d0 * d1;
+    for (int q = 0; q < dxy; ++q) c->h_rank[static_cast<size_t>(q)] = r + q;
+    for (int q = 0; q < dxy; ++q) {
+      c->h_rank[static_cast<size_t>(q + dxy * (c->g.ldz - 1))] = r + dxy + q;
+    }
+  }
   c->ngroups_max = static_cast<int>(n / 32.0) + bg.nbricks + 1;
   // staging capacity: twice the expected halo population, 32-aligned
   const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
@@ -901,15 +929,74 @@ void build_geom(tmd_gpu_ctx* c, const double box[3], double r_cut,
   c->g.ncells = static_cast<int>(nc);
   c->g.rv2 = r_verlet * r_verlet;
   c->g.rebuild_thr = 0.25 * r_skin * r_skin;
+  // whole periodic box (slab mode is set up by make_slab)
+  c->g.zslab = 0;
+  c->g.z0 = 0;
+  c->g.zown = c->g.dims[2];
+  c->g.ldz = c->g.dims[2];
+  c->g.zcode_lo = c->g.zcode_hi = 0;
+  c->g.owned_cells = c->g.ncells;
 }
 
-}  // namespace
+// Slab `rank` of `nranks` along z: owned global layers [z0, z1) with the
+// reference's range rule i*dims/s (decomp.hpp:87-93), plus one ghost layer on
+// each side.
+void make_slab(tmd_gpu_ctx* c, int rank, int nranks) {
+  const int dz = c->g.dims[2];
+  if (nranks > dz) {
+    throw StatusError{TMD_ERR_CONFIG, "more ranks (" + std::to_string(nranks) +
+                                          ") than z cell layers (" + std::to_string(dz) + ")"};
+  }
+  if (dz < 3) {
+    throw StatusError{TMD_ERR_CONFIG,
+                      "slab decomposition needs at least 3 z cell layers, the box has " +
+                          std::to_string(dz)};
+  }
+  const int z0 = static_cast<int>(static_cast<int64_t>(rank) * dz / nranks);
+  const int z1 = static_cast<int>(static_cast<int64_t>(rank + 1) * dz / nranks);
+  const int dxy = c->g.dims[0] * c->g.dims[1];
+  c->g.zslab = 1;
+  c->g.z0 = z0;
+  c->g.zown = z1 - z0;
+  c->g.ldz = c->g.zown + 2;
+  c->g.zcode_lo = z0 == 0 ? 2u : 0u;   // lower ghost layer wraps: image at -Lz
+  c->g.zcode_hi = z1 == dz ? 1u : 0u;  // upper ghost layer wraps: image at +Lz
+  c->g.ncells = dxy * c->g.ldz;
+  c->g.owned_cells = dxy * c->g.zown;
+}
 
-extern "C" {
+// Device buffers of the slab exchange (capacity = the whole system).
+void alloc_slab(tmd_gpu_ctx* c) {
+  const size_t n = static_cast<size_t>(c->n_cap);
+  const int dz = c->g.dims[2];
+  std::vector<int> owner(static_cast<size_t>(dz));
+  for (int r = 0; r < c->nranks; ++r) {
+    const int z0 = static_cast<int>(static_cast<int64_t>(r) * dz / c->nranks);
+    const int z1 = static_cast<int>(static_cast<int64_t>(r + 1) * dz / c->nranks);
+    for (int z = z0; z < z1; ++z) owner[static_cast<size_t>(z)] = r;
+  }
+  c->owner_of_z = dalloc<int>(owner.size());
+  ck(cudaMemcpy(c->owner_of_z, owner.data(), owner.size() * sizeof(int),
+                cudaMemcpyHostToDevice), "H2D owner table");
+  c->mig_dest = dalloc<int>(n);
+  c->mig_count = dalloc<int>(2 * static_cast<size_t>(c->nranks));
+  c->mig_off = dalloc<int>(static_cast<size_t>(c->nranks) + 1);
+  c->mig_keep = dalloc<int>(1);
+  c->mig_send = dalloc<MigRec>(n);
+  c->mig_recv = dalloc<MigRec>(n);
+  const size_t dxy = static_cast<size_t>(c->g.dims[0]) * c->g.dims[1];
+  for (int s = 0; s < 2; ++s) {
+    c->bidx[s] = dalloc<int>(n);
+    c->bids[s] = dalloc<long long>(n);
+    c->bpos[s] = dalloc<double4>(n);
+    c->bcnt[s] = dalloc<int>(dxy);
+    c->boff[s] = dalloc<int>(dxy + 1);
+    c->gcnt[s] = dalloc<int>(dxy);
+  }
+}
 
-int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
-                   const tmd_fene_params* fene, const tmd_engine_params* params,
-                   tmd_gpu_ctx** out) {
+int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_params* fene,
+                const tmd_engine_params* params, int rank, int nranks, tmd_gpu_ctx** out) {
   if (!out) return TMD_ERR_CONFIG;
   *out = nullptr;
   auto* c = new tmd_gpu_ctx();
@@ -937,8 +1024,34 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     ck(cudaEventCreate(&c->t0), "cudaEventCreate");
     ck(cudaEventCreate(&c->t1), "cudaEventCreate");
 
-    c->n = sys->n;
-    c->stride = static_cast<int>((c->n + 31) / 32 * 32);
+    // Slab mode: keep the particles whose wrapped position lies in this
+    // rank's z layers (exact host wrap + cell, bit-identical to the device's).
+    std::vector<int64_t> sel;
+    if (nranks > 1) {
+      make_slab(c, rank, nranks);
+      for (int64_t k = 0; k < sys->n; ++k) {
+        const double z = host_wrap1(sys->pos[3 * k + 2], c->g.L[2]);
+        int cz = static_cast<int>(std::floor(z / c->g.cell_len[2]));
+        cz = std::min(std::max(cz, 0), c->g.dims[2] - 1);
+        if (cz >= c->g.z0 && cz < c->g.z0 + c->g.zown) sel.push_back(k);
+      }
+    } else {
+      sel.resize(static_cast<size_t>(sys->n));
+      std::iota(sel.begin(), sel.end(), int64_t{0});
+    }
+    c->my_rank = rank;
+    c->nranks = nranks;
+    // slot capacity: the whole system, or in slab mode room for the owned
+    // particles to double plus both ghost layers (checked at every exchange)
+    c->n_cap = sys->n;
+    if (nranks > 1) {
+      c->n_cap = std::min<int64_t>(2 * sys->n, 2 * static_cast<int64_t>(sel.size()) + 65536);
+      if (c->n_cap > kMaxSlots) {
+        throw StatusError{TMD_ERR_CONFIG, "slab too large for one GPU context"};
+      }
+    }
+    c->n = static_cast<int64_t>(sel.size());
+    c->stride = static_cast<int>((c->n_cap + 31) / 32 * 32);
     c->nblk = blocks_for(c->n, kBlock);
     c->dt = params->dt;
     c->half_dt = 0.5 * params->dt;
@@ -947,8 +1060,13 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     c->timers_on = params->section_timers != 0;
     c->variant = (params->reserved[0] >= 1 && params->reserved[0] <= 3) ? params->reserved[0]
                                                                        : kDefaultVariant;
+    if (nranks > 1) c->variant = 3;  // slab mode runs the brick build + global-slot forces
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
-    setup_bricks(c, static_cast<double>(c->n), lj->r_cut + params->r_skin);
+    setup_bricks(c, static_cast<double>(sys->n), lj->r_cut + params->r_skin);
+    if (nranks > 1) {  // groups of the owned particles only (+ migration headroom)
+      const int64_t want = c->n + c->n / 4 + 1024;
+      c->ngroups_max = static_cast<int>(want / 32) + c->bg.nbricks + 1;
+    }
     // lj_prepare (potentials.hpp:49-61)
     c->lj.sigma2 = lj->sigma * lj->sigma;
     c->lj.rc2 = lj->r_cut * lj->r_cut;
@@ -961,8 +1079,8 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
       c->lj.shift = c->lj.eps4 * (s6 * s6 - s6);
     }
 
-    const size_t n = static_cast<size_t>(c->n);
-    // slot n of both buffers: far-away sentinel (variant 3 list padding)
+    const size_t n = static_cast<size_t>(c->n_cap);  // capacity
+    // slot n_cap of both buffers: far-away sentinel (variant 3 list padding)
     c->posb[0] = dalloc<double4>(n + 1);
     c->posb[1] = dalloc<double4>(n + 1);
     c->cur = 0;
@@ -979,7 +1097,7 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     c->count = dalloc<int>(c->g.ncells);
     c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
     c->nnbr = dalloc<int>(n);
-    c->nparts = std::max(c->nblk, c->bg.nbricks);
+    c->nparts = std::max(blocks_for(c->n_cap, kBlock), c->bg.nbricks);
     c->part_e = dalloc<double>(c->nparts);
     c->part_w = dalloc<double>(c->nparts);
     c->part_ke = dalloc<double>(c->nparts);
@@ -1001,29 +1119,37 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     ck(cudaMemsetAsync(c->fy, 0, n * sizeof(double), c->stream), "memset");
     ck(cudaMemsetAsync(c->fz, 0, n * sizeof(double), c->stream), "memset");
 
-    // upload (input order; the first resort sorts by cell)
-    std::vector<double4> hp(n);
-    std::vector<double> hv(3 * n, 0.0), hm(n, 1.0);
-    for (size_t k = 0; k < n; ++k) {
-      hp[k] = make_double4(sys->pos[3 * k], sys->pos[3 * k + 1],
-                           sys->pos[3 * k + 2], 0.0);
+    // upload the kept particles (input order; the first resort sorts by cell)
+    const size_t m = sel.size();
+    std::vector<double4> hp(m);
+    std::vector<double> hv(3 * m, 0.0), hm(m, 1.0);
+    std::vector<long long> hid(m);
+    for (size_t r = 0; r < m; ++r) {
+      const size_t k = static_cast<size_t>(sel[r]);
+      hp[r] = make_double4(sys->pos[3 * k], sys->pos[3 * k + 1], sys->pos[3 * k + 2], 0.0);
       if (sys->vel) {
-        hv[k] = sys->vel[3 * k];
-        hv[n + k] = sys->vel[3 * k + 1];
-        hv[2 * n + k] = sys->vel[3 * k + 2];
+        hv[r] = sys->vel[3 * k];
+        hv[m + r] = sys->vel[3 * k + 1];
+        hv[2 * m + r] = sys->vel[3 * k + 2];
       }
-      if (sys->mass) hm[k] = sys->mass[k];
+      if (sys->mass) hm[r] = sys->mass[k];
+      hid[r] = sys->id[k];
     }
-    hp.push_back(make_double4(kFarD, kFarD, kFarD, 0.0));
-    ck(cudaMemcpy(c->posb[0], hp.data(), (n + 1) * sizeof(double4), cudaMemcpyHostToDevice),
-       "H2D pos");
-    ck(cudaMemcpy(c->posb[1] + n, &hp[n], sizeof(double4), cudaMemcpyHostToDevice),
-       "H2D sentinel");
-    ck(cudaMemcpy(c->vx, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
-    ck(cudaMemcpy(c->vy, hv.data() + n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vy");
-    ck(cudaMemcpy(c->vz, hv.data() + 2 * n, n * sizeof(double), cudaMemcpyHostToDevice), "H2D vz");
-    ck(cudaMemcpy(c->mass, hm.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D mass");
-    ck(cudaMemcpy(c->id, sys->id, n * sizeof(long long), cudaMemcpyHostToDevice), "H2D id");
+    const double4 far = make_double4(kFarD, kFarD, kFarD, 0.0);
+    if (m > 0) {
+      ck(cudaMemcpy(c->posb[0], hp.data(), m * sizeof(double4), cudaMemcpyHostToDevice),
+         "H2D pos");
+      ck(cudaMemcpy(c->vx, hv.data(), m * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
+      ck(cudaMemcpy(c->vy, hv.data() + m, m * sizeof(double), cudaMemcpyHostToDevice),
+         "H2D vy");
+      ck(cudaMemcpy(c->vz, hv.data() + 2 * m, m * sizeof(double), cudaMemcpyHostToDevice),
+         "H2D vz");
+      ck(cudaMemcpy(c->mass, hm.data(), m * sizeof(double), cudaMemcpyHostToDevice), "H2D mass");
+      ck(cudaMemcpy(c->id, hid.data(), m * sizeof(long long), cudaMemcpyHostToDevice), "H2D id");
+    }
+    ck(cudaMemcpy(c->posb[0] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
+    ck(cudaMemcpy(c->posb[1] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
+    if (nranks > 1) alloc_slab(c);
 
     c->auto_cap = params->nbr_capacity <= 0;
     // Initial capacity: the expected count at this density (27 cells worth
@@ -1032,13 +1158,15 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
     int cap0 = params->nbr_capacity;
     if (c->auto_cap) {
       const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
-      const double rho = static_cast<double>(c->n) / vol;
+      const double rho = static_cast<double>(c->n_cap) / vol;
       const double rverlet = lj->r_cut + params->r_skin;
       const double expect = rho * 4.18879020478639 * rverlet * rverlet * rverlet;
       cap0 = static_cast<int>(expect * 1.5) + 16;
     }
     alloc_list(c, cap0);
-    setup_pass(c);
+    // slab mode: the owner of the decomposition finishes the setup after the
+    // first migration/ghost exchange (tmd_gpu_slab_*); whole box: now
+    if (nranks == 1) setup_pass(c);
     c->step = 0;
     c->rebuilds = 0;
     c->ke_fresh = false;
@@ -1051,6 +1179,27 @@ int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
   }
   *out = c;
   return TMD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
+                   const tmd_fene_params* fene, const tmd_engine_params* params,
+                   tmd_gpu_ctx** out) {
+  return create_impl(sys, lj, fene, params, 0, 1, out);
+}
+
+int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
+                        const tmd_fene_params* fene, const tmd_engine_params* params,
+                        int rank, int nranks, tmd_gpu_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    if (out) *out = nullptr;
+    g_create_error = "invalid rank / nranks";
+    return TMD_ERR_CONFIG;
+  }
+  return create_impl(sys, lj, fene, params, rank, nranks, out);
 }
 
 }  // extern "C"
@@ -1244,6 +1393,11 @@ int tmd_gpu_pairs(tmd_gpu_ctx* c, int64_t* pairs, size_t cap, size_t* n_out) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     HostState h = fetch(c, false, false, false, false);
     const size_t n = h.order.size();
+    if (c->n_ghost > 0) {  // slab mode: neighbours may be ghost slots
+      h.id.resize(n + static_cast<size_t>(c->n_ghost));
+      ck(cudaMemcpy(h.id.data() + n, c->id + n, static_cast<size_t>(c->n_ghost) * sizeof(long long),
+                    cudaMemcpyDeviceToHost), "D2H ghost ids");
+    }
     const int rows = std::min(c->cap, std::max(c->h_ctrl->max_count, 0));
     std::vector<int> cnt(n);
     std::vector<uint32_t> list(static_cast<size_t>(rows) * c->stride);
@@ -1371,6 +1525,305 @@ int tmd_gpu_fp64_peak(int device, double* tflops) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(out);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// z-slab decomposition entry points (multi-GPU). The caller (one
+// process per GPU, paper_2109_10876_b200/decomp.py) drives every rank through
+// the same sequence and moves the byte buffers between ranks itself (NCCL,
+// or device copies when all ranks live in one process):
+//
+//   setup / rebuild:  decide(rebuild=1) -> migrate_out -> [records to their
+//                     destination ranks] -> migrate_in -> commit -> border(0/1)
+//                     -> [boundary layers to the lower/upper neighbour]
+//                     -> ghost_in -> [counts, ids, positions] -> ghosts_ready
+//   per step:         forces(fused) -> halo -> [positions] -> max_d2 ->
+//                     [max over ranks] -> decide(rebuild) -> ...
+//
+// Every call returns with the context's stream drained, so the caller may
+// move the returned device buffers on any stream.
+
+namespace {
+
+void need_slab(const tmd_gpu_ctx* c) {
+  if (c->nranks < 2 && !c->g.zslab) {
+    throw StatusError{TMD_ERR_STATE, "not a slab context (use tmd_gpu_create_slab)"};
+  }
+}
+
+// Keeps the list's group capacity ahead of the owned count (migration can
+// grow a slab's population).
+void ensure_groups(tmd_gpu_ctx* c) {
+  const int need = static_cast<int>(c->n / 32) + c->bg.nbricks + 1;
+  if (need > c->ngroups_max) {
+    c->ngroups_max = need + need / 8 + 64;
+    alloc_list(c, c->cap);
+  }
+}
+
+}  // namespace
+
+int tmd_gpu_slab_info(tmd_gpu_ctx* c, int64_t info[10]) {
+  return guard(c, [&] {
+    info[0] = c->my_rank;
+    info[1] = c->nranks;
+    info[2] = c->g.z0;
+    info[3] = c->g.zown;
+    info[4] = c->n;
+    info[5] = c->n_ghost_lo;
+    info[6] = c->n_ghost_hi;
+    info[7] = static_cast<int64_t>(c->g.dims[0]) * c->g.dims[1];
+    info[8] = c->n_cap;
+    info[9] = static_cast<int64_t>(sizeof(MigRec));
+  });
+}
+
+int tmd_gpu_slab_max_d2(tmd_gpu_ctx* c, double* local_max_d2) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    sync_ctrl(c);
+    raise_physics(c, true);
+    if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
+    c->step = c->h_ctrl->step;
+    c->rebuilds = static_cast<uint64_t>(c->h_ctrl->rebuilds);
+    double m = 0.0;
+    std::memcpy(&m, &c->h_ctrl->max_d2, sizeof m);
+    *local_max_d2 = m;
+  });
+}
+
+int tmd_gpu_slab_decide(tmd_gpu_ctx* c, int rebuild, int advance) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (rebuild) set_force_rebuild(c);
+    launch_decide(c, advance != 0);
+  });
+}
+
+int tmd_gpu_slab_migrate_out(tmd_gpu_ctx* c, int64_t* counts, void** send) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const int R = c->nranks;
+    const int n = static_cast<int>(c->n);
+    ck(cudaMemsetAsync(c->mig_count, 0, 2 * sizeof(int) * R, c->stream), "memset");
+    ck(cudaMemsetAsync(c->mig_keep, 0, sizeof(int), c->stream), "memset");
+    c->launches += 2;
+    if (n > 0) {
+      k_mig_classify<<<c->nblk, kBlock, 0, c->ls>>>(n, c->pos, c->id, c->owner_of_z,
+                                                    c->my_rank, c->g, c->mig_dest,
+                                                    c->mig_count, c->ctrl);
+    }
+    std::vector<int> h(static_cast<size_t>(R));
+    ck(cudaMemcpyAsync(h.data(), c->mig_count, sizeof(int) * R, cudaMemcpyDeviceToHost,
+                       c->stream), "D2H mig counts");
+    sync_ctrl(c);
+    raise_physics(c, true);
+    std::vector<int> off(static_cast<size_t>(R) + 1, 0);
+    for (int r = 0; r < R; ++r) off[r + 1] = off[r] + h[r];
+    ck(cudaMemcpyAsync(c->mig_off, off.data(), sizeof(int) * (R + 1), cudaMemcpyHostToDevice,
+                       c->stream), "H2D mig offsets");
+    if (n > 0) {
+      k_mig_pack<<<c->nblk, kBlock, 0, c->ls>>>(
+          n, c->pos, c->vx, c->vy, c->vz, c->mass, c->id, c->mig_dest, c->my_rank,
+          c->mig_off, c->mig_count + R, c->mig_send, c->mig_keep, c->pos2, c->vx2, c->vy2,
+          c->vz2, c->mass2, c->id2);
+    }
+    int keep = 0;
+    ck(cudaMemcpyAsync(&keep, c->mig_keep, sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+       "D2H keep");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    const size_t k = static_cast<size_t>(keep);
+    auto cp = [&](void* d, const void* s, size_t bytes) {
+      if (bytes) ck(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, c->stream), "copy");
+    };
+    cp(c->pos, c->pos2, k * sizeof(double4));
+    cp(c->vx, c->vx2, k * sizeof(double));
+    cp(c->vy, c->vy2, k * sizeof(double));
+    cp(c->vz, c->vz2, k * sizeof(double));
+    cp(c->mass, c->mass2, k * sizeof(double));
+    cp(c->id, c->id2, k * sizeof(long long));
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "kernel launch");
+    c->n = keep;
+    c->n_ghost = c->n_ghost_lo = c->n_ghost_hi = 0;
+    for (int r = 0; r < R; ++r) counts[r] = h[r];
+    *send = c->mig_send;
+  });
+}
+
+int tmd_gpu_slab_migrate_in(tmd_gpu_ctx* c, int64_t nrecv, void** recv) {
+  return guard(c, [&] {
+    need_slab(c);
+    if (nrecv < 0 || c->n + nrecv > c->n_cap) {
+      throw StatusError{TMD_ERR_CONFIG,
+                        "slab capacity exceeded: " + std::to_string(c->n + nrecv) +
+                            " particles > " + std::to_string(c->n_cap)};
+    }
+    c->mig_nrecv = nrecv;
+    *recv = c->mig_recv;
+  });
+}
+
+int tmd_gpu_slab_commit(tmd_gpu_ctx* c, int64_t nb_out[2]) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (c->mig_nrecv > 0) {
+      c->launches += 1;
+      k_mig_unpack<<<blocks_for(c->mig_nrecv, kBlock), kBlock, 0, c->ls>>>(
+          static_cast<int>(c->mig_nrecv), c->mig_recv, static_cast<int>(c->n), c->pos, c->vx,
+          c->vy, c->vz, c->mass, c->id);
+    }
+    c->n += c->mig_nrecv;
+    c->mig_nrecv = 0;
+    c->nblk = std::max(1, blocks_for(c->n, kBlock));
+    ensure_groups(c);
+    launch_resort(c);  // requires the rebuild decision (decide(rebuild=1))
+    const int dxy = c->g.dims[0] * c->g.dims[1];
+    const int qb = blocks_for(dxy, kBlock);
+    for (int s = 0; s < 2; ++s) {
+      const int lz = s == 0 ? 1 : c->g.zown;  // lowest / highest owned layer
+      c->launches += 3;
+      k_layer_counts<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->count);
+      launch_scan(c, dxy, c->count, c->boff[s]);  // leaves count zeroed
+      k_layer_counts<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->bcnt[s]);
+      k_layer_gather<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->boff[s],
+                                               c->pos, c->id, c->bidx[s], c->bids[s],
+                                               c->bpos[s]);
+    }
+    int tot[2] = {0, 0};
+    for (int s = 0; s < 2; ++s) {
+      ck(cudaMemcpyAsync(&tot[s], c->boff[s] + dxy, sizeof(int), cudaMemcpyDeviceToHost,
+                         c->stream), "D2H border size");
+    }
+    sync_ctrl(c);
+    raise_physics(c, true);
+    if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
+    for (int s = 0; s < 2; ++s) {
+      c->nb[s] = tot[s];
+      nb_out[s] = tot[s];
+    }
+  });
+}
+
+int tmd_gpu_slab_border(tmd_gpu_ctx* c, int side, void** counts, void** ids, void** pos) {
+  return guard(c, [&] {
+    need_slab(c);
+    if (side != 0 && side != 1) throw StatusError{TMD_ERR_CONFIG, "side must be 0 or 1"};
+    *counts = c->bcnt[side];
+    *ids = c->bids[side];
+    *pos = c->bpos[side];
+  });
+}
+
+int tmd_gpu_slab_ghost_in(tmd_gpu_ctx* c, int64_t n_lo, int64_t n_hi, void* lo[3],
+                          void* hi[3]) {
+  return guard(c, [&] {
+    need_slab(c);
+    if (n_lo < 0 || n_hi < 0 || c->n + n_lo + n_hi > c->n_cap) {
+      throw StatusError{TMD_ERR_CONFIG, "slab capacity exceeded by the ghost layers: " +
+                                            std::to_string(c->n + n_lo + n_hi) + " slots > " +
+                                            std::to_string(c->n_cap)};
+    }
+    c->n_ghost_lo = n_lo;
+    c->n_ghost_hi = n_hi;
+    c->n_ghost = n_lo + n_hi;
+    lo[0] = c->gcnt[0];
+    lo[1] = c->id + c->n;
+    lo[2] = c->pos + c->n;
+    hi[0] = c->gcnt[1];
+    hi[1] = c->id + c->n + n_lo;
+    hi[2] = c->pos + c->n + n_lo;
+  });
+}
+
+int tmd_gpu_slab_ghosts_ready(tmd_gpu_ctx* c) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->launches += 1;
+    k_ghost_starts<<<1, 1024, 0, c->ls>>>(c->g, static_cast<int>(c->n), c->gcnt[0], c->gcnt[1],
+                                         c->start);
+    for (;;) {
+      launch_build(c);
+      sync_ctrl(c);
+      raise_physics(c, true);
+      if (c->h_ctrl->status & kOverflowBits) {
+        const Ctrl h = *c->h_ctrl;
+        reset_status(c);
+        grow_after_overflow(c, h);
+        if (c->variant != 3) {
+          throw StatusError{TMD_ERR_CONFIG, "slab mode: brick halo exceeds shared memory"};
+        }
+        continue;
+      }
+      if (c->auto_cap) {
+        const int want = round8(c->h_ctrl->max_count + c->h_ctrl->max_count / 4 + 8);
+        if (want > c->cap) {
+          alloc_list(c, want);
+          continue;
+        }
+      }
+      break;
+    }
+  });
+}
+
+int tmd_gpu_slab_kick_drift(tmd_gpu_ctx* c) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (c->n > 0) launch_kick_drift(c, false);
+  });
+}
+
+// mode: 0 forces only, 1 forces + closing half-kick, 2 closing half-kick +
+// next opening half-kick + drift (the position buffers swap).
+int tmd_gpu_slab_forces(tmd_gpu_ctx* c, int mode) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    launch_forces(c, mode == 2 ? kFused : (mode == 1 ? kKick2 : kForcesOnly));
+  });
+}
+
+int tmd_gpu_slab_halo(tmd_gpu_ctx* c, void* send[2], void* recv[2]) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    for (int s = 0; s < 2; ++s) {
+      if (c->nb[s] == 0) continue;
+      c->launches += 1;
+      k_pack_border<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
+          static_cast<int>(c->nb[s]), c->bidx[s], c->pos, c->bpos[s]);
+    }
+    send[0] = c->bpos[0];
+    send[1] = c->bpos[1];
+    recv[0] = c->pos + c->n;
+    recv[1] = c->pos + c->n + c->n_ghost_lo;
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "kernel launch");
+  });
+}
+
+int tmd_gpu_slab_sums(tmd_gpu_ctx* c, double out[3]) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->launches += 1;
+    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
+                                            c->mass, c->part_ke);
+    launch_reduce_ke(c);
+    launch_reduce_pe(c);
+    ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream), "D2H scalars");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "kernel launch");
+    for (int k = 0; k < 3; ++k) out[k] = c->h_scalars[k];
   });
 }
 

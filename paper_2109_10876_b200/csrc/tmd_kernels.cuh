@@ -248,7 +248,12 @@ __global__ void __launch_bounds__(kBlock)
   const int cz = cell_coord(p.z, g.cell_len[2], g.dims[2]);
   const int c = cx + g.dims[0] * (cy + g.dims[1] * cz);
   cell[i] = c;
-  slot[i] = atomicAdd(&count[cell_rank[c]], 1);  // histogram in brick-major order
+  if (g.zslab && (cz < g.z0 || cz >= g.z0 + g.zown)) {  // must have migrated first
+    record_error(ctrl, kStatStray, id[i], cz);
+    slot[i] = 0;
+    return;
+  }
+  slot[i] = atomicAdd(&count[cell_rank[local_cell(g, c)]], 1);  // brick-major order
 }
 
 // Exclusive scan of the cell histogram (one block; runs once per rebuild).
@@ -341,12 +346,12 @@ __global__ void __launch_bounds__(kScanThreads)
 
 __global__ void __launch_bounds__(kBlock)
     k_scatter(int n, const int* __restrict__ cell, const int* __restrict__ slot,
-              const int* __restrict__ start, const int* __restrict__ cell_rank,
+              const int* __restrict__ start, const int* __restrict__ cell_rank, Geom g,
               int* __restrict__ perm, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
   const int i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= n) return;
-  perm[start[cell_rank[cell[i]]] + slot[i]] = i;
+  perm[start[cell_rank[local_cell(g, cell[i])]] + slot[i]] = i;
 }
 
 // Canonical order inside each cell: ascending particle id. Makes the sorted

@@ -1,0 +1,164 @@
+// Kernels of the z-slab domain decomposition (multi-GPU): one
+// context per GPU owns the particles of a slab of cell layers, plus one ghost
+// layer on each side holding copies of the neighbour slabs' boundary layers.
+// With a full neighbour list there is no reverse force exchange
+// (collect_ghost_forces, decomp.hpp:202-224, disappears); per step only the
+// boundary positions move, and at a rebuild the slab exchanges leavers
+// (migration) and re-exports its boundary layers.
+#pragma once
+
+#include "tmd_kernels.cuh"
+
+namespace tmd {
+
+// One migrating particle (distribute_records moves whole records,
+// domain.hpp:54-92; forces are recomputed before use, soa_store.hpp:19-21).
+struct MigRec {
+  long long id;
+  double mass;
+  double x, y, z;
+  double vx, vy, vz;
+};
+
+// Wrap (exactly, box.hpp:47-51) and classify every owned particle by the rank
+// owning its z cell layer; count leavers per destination.
+__global__ void __launch_bounds__(kBlock)
+    k_mig_classify(int n, double4* __restrict__ pos, const long long* __restrict__ id,
+                   const int* __restrict__ owner_of_z, int my_rank, Geom g,
+                   int* __restrict__ dest, int* __restrict__ dcount, Ctrl* ctrl) {
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n) return;
+  double4 p = pos[i];
+  if (!finite3(p.x, p.y, p.z)) {
+    record_error(ctrl, kStatNonFinitePos, id[i], -1);
+    dest[i] = my_rank;
+    return;
+  }
+  p.x = wrap1(p.x, g.L[0]);
+  p.y = wrap1(p.y, g.L[1]);
+  p.z = wrap1(p.z, g.L[2]);
+  pos[i] = p;
+  const int cz = cell_coord(p.z, g.cell_len[2], g.dims[2]);
+  const int d = owner_of_z[cz];
+  dest[i] = d;
+  if (d != my_rank) atomicAdd(&dcount[d], 1);
+}
+
+// Stayers are compacted into the alternate arrays (order is irrelevant: the
+// resort that follows sorts by cell and id); leavers are packed per
+// destination at doff[dest] + cursor.
+__global__ void __launch_bounds__(kBlock)
+    k_mig_pack(int n, const double4* __restrict__ pos, const double* __restrict__ vx,
+               const double* __restrict__ vy, const double* __restrict__ vz,
+               const double* __restrict__ mass, const long long* __restrict__ id,
+               const int* __restrict__ dest, int my_rank, const int* __restrict__ doff,
+               int* __restrict__ dcur, MigRec* __restrict__ out, int* __restrict__ keep,
+               double4* __restrict__ pos2, double* __restrict__ vx2, double* __restrict__ vy2,
+               double* __restrict__ vz2, double* __restrict__ mass2,
+               long long* __restrict__ id2) {
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n) return;
+  const int d = dest[i];
+  if (d == my_rank) {
+    const int k = atomicAdd(keep, 1);
+    pos2[k] = pos[i];
+    vx2[k] = vx[i];
+    vy2[k] = vy[i];
+    vz2[k] = vz[i];
+    mass2[k] = mass[i];
+    id2[k] = id[i];
+  } else {
+    const int k = doff[d] + atomicAdd(&dcur[d], 1);
+    MigRec r;
+    r.id = id[i];
+    r.mass = mass[i];
+    r.x = pos[i].x;
+    r.y = pos[i].y;
+    r.z = pos[i].z;
+    r.vx = vx[i];
+    r.vy = vy[i];
+    r.vz = vz[i];
+    out[k] = r;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_mig_unpack(int nrecv, const MigRec* __restrict__ in, int base,
+                 double4* __restrict__ pos, double* __restrict__ vx, double* __restrict__ vy,
+                 double* __restrict__ vz, double* __restrict__ mass,
+                 long long* __restrict__ id) {
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= nrecv) return;
+  const MigRec r = in[k];
+  const int i = base + k;
+  pos[i] = make_double4(r.x, r.y, r.z, 0.0);
+  vx[i] = r.vx;
+  vy[i] = r.vy;
+  vz[i] = r.vz;
+  mass[i] = r.mass;
+  id[i] = r.id;
+}
+
+// Per-cell particle counts of one owned boundary layer (local z = lz), cells
+// in x-fastest order (the ghost-layer order of the receiving slab).
+__global__ void __launch_bounds__(kBlock)
+    k_layer_counts(int lz, Geom g, const int* __restrict__ cell_rank,
+                   const int* __restrict__ start, int* __restrict__ counts) {
+  const int q = blockIdx.x * kBlock + threadIdx.x;
+  const int dxy = g.dims[0] * g.dims[1];
+  if (q >= dxy) return;
+  const int r = cell_rank[q + dxy * lz];
+  counts[q] = start[r + 1] - start[r];
+}
+
+// Boundary-layer export: slot list (for the per-step position packing), ids
+// and current positions, in (cell x-fastest, then sorted slot) order.
+__global__ void __launch_bounds__(kBlock)
+    k_layer_gather(int lz, Geom g, const int* __restrict__ cell_rank,
+                   const int* __restrict__ start, const int* __restrict__ off,
+                   const double4* __restrict__ pos, const long long* __restrict__ id,
+                   int* __restrict__ idx_out, long long* __restrict__ id_out,
+                   double4* __restrict__ pos_out) {
+  const int q = blockIdx.x * kBlock + threadIdx.x;
+  const int dxy = g.dims[0] * g.dims[1];
+  if (q >= dxy) return;
+  const int r = cell_rank[q + dxy * lz];
+  const int b = start[r], e = start[r + 1];
+  int o = off[q];
+  for (int s = b; s < e; ++s, ++o) {
+    idx_out[o] = s;
+    id_out[o] = id[s];
+    pos_out[o] = pos[s];
+  }
+}
+
+// Ghost cell ranges from the two received count arrays: ghost layer 0 cells
+// are ranked right after the owned cells, then ghost layer ldz-1 (setup_bricks).
+__global__ void __launch_bounds__(1024)
+    k_ghost_starts(Geom g, int n_own, const int* __restrict__ cnt_lo,
+                   const int* __restrict__ cnt_hi, int* __restrict__ start) {
+  __shared__ int warp_tot[32];
+  const int dxy = g.dims[0] * g.dims[1];
+  const int m = 2 * dxy;
+  const int per = (m + 1023) / 1024;
+  const int b = min(static_cast<int>(threadIdx.x) * per, m), e = min(b + per, m);
+  int s = 0;
+  for (int q = b; q < e; ++q) s += q < dxy ? cnt_lo[q] : cnt_hi[q - dxy];
+  int total;
+  int run = n_own + block_excl_scan(s, warp_tot, total);
+  for (int q = b; q < e; ++q) {
+    start[g.owned_cells + q] = run;
+    run += q < dxy ? cnt_lo[q] : cnt_hi[q - dxy];
+  }
+  if (threadIdx.x == 1023) start[g.owned_cells + m] = n_own + total;
+}
+
+// Per-step halo packing: current positions of one boundary layer.
+__global__ void __launch_bounds__(kBlock)
+    k_pack_border(int nb, const int* __restrict__ idx, const double4* __restrict__ pos,
+                  double4* __restrict__ out) {
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  if (k < nb) out[k] = pos[idx[k]];
+}
+
+}  // namespace tmd

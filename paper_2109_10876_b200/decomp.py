@@ -1,0 +1,559 @@
+"""Multi-GPU z-slab decomposition of the LJ hot path.
+
+The reference decomposes the box into subnodes inside one process
+(decomp.hpp:47-118 make_subnode_decomposition / make_subnode_layouts) and
+keeps ghost cells current by copying positions across subnode stores
+(decomp.hpp:142-200 build_ghost_plan / update_ghost_positions), re-binning
+every particle at a resort (domain.hpp:54-92 distribute_records). Here one
+process (or one context) per GPU owns a slab of whole z cell layers, cut with
+the reference's range rule i*dims/s (decomp.hpp:87-93), plus one ghost layer
+per side:
+
+  * rebuild (the reference's resort + rebuild_all_lists, engine.hpp:195-215):
+    leavers are packed into 64-byte records and sent to the rank owning their
+    new z layer; each slab resorts its owned particles and exports its lowest
+    and highest layer (per-cell counts, ids, positions) to the neighbour
+    slabs, whose ghost layers they become; then each slab builds its list.
+  * step: after the fused force + integrator kernel, each slab sends the
+    current positions of its two boundary layers (32 B per particle) — the
+    only per-step traffic. The full neighbour list makes the reference's
+    reverse force pass (collect_ghost_forces, decomp.hpp:202-224) unnecessary.
+  * the rebuild test is the reference's global one (needs_rebuild,
+    neighbor_list.hpp:141-145: max displacement^2 > skin^2 / 4) as a MAX
+    all-reduce of one double per step.
+
+The byte buffers live on the device (C ABI tmd_gpu_slab_*, include/tmd_gpu.h)
+and move between ranks through a `Comm`:
+
+  * `TorchDistComm`: one process per GPU, torch.distributed (NCCL for CUDA
+    buffers; the gloo backend drives the same protocol on CPU buffers in the
+    host-logic tests);
+  * `InProcessComm`: every rank's context in this process (device copies).
+    Used to check the decomposition on one GPU; ranks never wait on one
+    another inside a kernel.
+
+Slot layout of a slab context: owned particles [0, n_own) cell-sorted
+(brick-major), lower ghost layer [n_own, n_own + n_lo), upper ghost layer
+after it, each ghost layer cell-sorted x-fastest exactly as the neighbour
+exported it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi
+from .engine import (ConfigError, EngineConfig, FlatConfig, Interactions, StepObservables,
+                     _check, _ptr, validate_engine_config)
+
+# message tags (both ends of a transfer agree on them; NCCL matches by order)
+TAG_MIGRATE = 100
+TAG_GHOST_LO = 0    # into the receiver's lower ghost layer (+0 counts, +1 ids, +2 pos)
+TAG_GHOST_HI = 10   # into the receiver's upper ghost layer
+TAG_HALO_LO = 20    # per-step positions into the receiver's lower ghost layer
+TAG_HALO_HI = 30
+
+
+def slab_range(rank: int, nranks: int, dims_z: int) -> Tuple[int, int]:
+    """Owned z layers [z0, z1) of slab `rank` (decomp.hpp:87-93's rule)."""
+    return rank * dims_z // nranks, (rank + 1) * dims_z // nranks
+
+
+def owner_of_layer(z: int, nranks: int, dims_z: int) -> int:
+    for r in range(nranks):
+        z0, z1 = slab_range(r, nranks, dims_z)
+        if z0 <= z < z1:
+            return r
+    raise ValueError(f"layer {z} outside 0..{dims_z - 1}")
+
+
+# ---------------------------------------------------------------------------
+# device buffers as tensors (zero copy)
+
+class _DevArray:
+    """__cuda_array_interface__ view of a device pointer owned by the context."""
+
+    def __init__(self, ptr: int, shape: Tuple[int, ...], typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": shape, "typestr": typestr, "data": (int(ptr or 0), False),
+            "version": 2, "strides": None,
+        }
+
+
+def _tensor(ptr, shape, typestr: str, device: int):
+    import torch
+    if int(np.prod(shape)) == 0:
+        dt = {"<i4": torch.int32, "<i8": torch.int64, "<f8": torch.float64,
+              "|u1": torch.uint8}[typestr]
+        return torch.empty(shape, dtype=dt, device=f"cuda:{device}")
+    return torch.as_tensor(_DevArray(ptr, tuple(shape), typestr), device=f"cuda:{device}")
+
+
+class SlabContext:
+    """One slab of the decomposition on one GPU (C ABI tmd_gpu_slab_*)."""
+
+    def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
+                 cfg: EngineConfig, rank: int, nranks: int, device: int):
+        validate_engine_config(cfg)
+        if inter.fene is not None or inter.angle is not None:
+            raise ConfigError("bonded terms are not on the GPU path yet (SURVEY §8f)")
+        L = _abi.lib()
+        self._keep = flat
+        sys = _abi.TmdSystem()
+        sys.box[:] = list(flat.box)
+        sys.n = flat.size()
+        sys.id = _ptr(flat.id)
+        sys.type = _ptr(flat.type)
+        sys.mass = _ptr(flat.mass)
+        sys.pos = _ptr(flat.pos)
+        sys.vel = _ptr(flat.vel)
+        lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
+                              1 if inter.lj.energy_shifted else 0)
+        p = _abi.TmdEngineParams()
+        p.dt = cfg.dt
+        p.r_skin = r_skin
+        p.device = device
+        p.section_timers = 0
+        p.nbr_capacity = cfg.nbr_capacity
+        h = C.c_void_p()
+        _check(L.tmd_gpu_create_slab(C.byref(sys), C.byref(lj), None, C.byref(p),
+                                     int(rank), int(nranks), C.byref(h)), None)
+        self._h = h
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self.box = flat.box.copy()
+        info = self.info()
+        self.dxy = info["dxy"]
+        self.rec_bytes = info["rec_bytes"]
+
+    # -- lifetime
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().tmd_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, rc: int) -> None:
+        _check(rc, self._h)
+
+    # -- protocol
+    def info(self) -> dict:
+        a = (C.c_int64 * 10)()
+        self._c(_abi.lib().tmd_gpu_slab_info(self._h, a))
+        keys = ("rank", "nranks", "z0", "zown", "n_own", "n_lo", "n_hi", "dxy", "n_cap",
+                "rec_bytes")
+        return dict(zip(keys, (int(v) for v in a)))
+
+    def max_d2(self) -> float:
+        m = C.c_double()
+        self._c(_abi.lib().tmd_gpu_slab_max_d2(self._h, C.byref(m)))
+        return m.value
+
+    def decide(self, rebuild: bool, advance: bool) -> None:
+        self._c(_abi.lib().tmd_gpu_slab_decide(self._h, int(bool(rebuild)), int(bool(advance))))
+
+    def migrate_out(self):
+        counts = np.zeros(self.nranks, np.int64)
+        ptr = C.c_void_p()
+        self._c(_abi.lib().tmd_gpu_slab_migrate_out(self._h, _ptr(counts), C.byref(ptr)))
+        total = int(counts.sum())
+        return counts, _tensor(ptr.value, (total * self.rec_bytes,), "|u1", self.device)
+
+    def migrate_in(self, nrecv: int):
+        ptr = C.c_void_p()
+        self._c(_abi.lib().tmd_gpu_slab_migrate_in(self._h, int(nrecv), C.byref(ptr)))
+        return _tensor(ptr.value, (int(nrecv) * self.rec_bytes,), "|u1", self.device)
+
+    def commit(self) -> Tuple[int, int]:
+        nb = np.zeros(2, np.int64)
+        self._c(_abi.lib().tmd_gpu_slab_commit(self._h, _ptr(nb)))
+        return int(nb[0]), int(nb[1])
+
+    def border(self, side: int, nb: int):
+        c_, i_, p_ = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._c(_abi.lib().tmd_gpu_slab_border(self._h, int(side), C.byref(c_), C.byref(i_),
+                                                C.byref(p_)))
+        return (_tensor(c_.value, (self.dxy,), "<i4", self.device),
+                _tensor(i_.value, (nb,), "<i8", self.device),
+                _tensor(p_.value, (nb, 4), "<f8", self.device))
+
+    def ghost_in(self, n_lo: int, n_hi: int):
+        lo, hi = (C.c_void_p * 3)(), (C.c_void_p * 3)()
+        self._c(_abi.lib().tmd_gpu_slab_ghost_in(self._h, int(n_lo), int(n_hi), lo, hi))
+
+        def views(a, n):
+            return (_tensor(a[0], (self.dxy,), "<i4", self.device),
+                    _tensor(a[1], (n,), "<i8", self.device),
+                    _tensor(a[2], (n, 4), "<f8", self.device))
+        return views(lo, n_lo), views(hi, n_hi)
+
+    def ghosts_ready(self) -> None:
+        self._c(_abi.lib().tmd_gpu_slab_ghosts_ready(self._h))
+
+    def kick_drift(self) -> None:
+        self._c(_abi.lib().tmd_gpu_slab_kick_drift(self._h))
+
+    def forces(self, mode: int) -> None:
+        self._c(_abi.lib().tmd_gpu_slab_forces(self._h, int(mode)))
+
+    def halo(self, nb: Tuple[int, int], n_lo: int, n_hi: int):
+        send, recv = (C.c_void_p * 2)(), (C.c_void_p * 2)()
+        self._c(_abi.lib().tmd_gpu_slab_halo(self._h, send, recv))
+        return ([_tensor(send[0], (nb[0], 4), "<f8", self.device),
+                 _tensor(send[1], (nb[1], 4), "<f8", self.device)],
+                [_tensor(recv[0], (n_lo, 4), "<f8", self.device),
+                 _tensor(recv[1], (n_hi, 4), "<f8", self.device)])
+
+    def sums(self) -> np.ndarray:
+        out = np.zeros(3)
+        self._c(_abi.lib().tmd_gpu_slab_sums(self._h, _ptr(out)))
+        return out
+
+    def sync(self) -> None:
+        import torch
+        torch.cuda.synchronize(self.device)
+
+    # -- state taps (owned particles)
+    def size(self) -> int:
+        return int(_abi.lib().tmd_gpu_size(self._h))
+
+    def download(self):
+        n = self.size()
+        ids = np.empty(n, np.int64)
+        pos = np.empty((n, 3))
+        vel = np.empty((n, 3))
+        f = np.empty((n, 3))
+        self._c(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), _ptr(f)))
+        return ids, pos, vel, f
+
+    def pairs(self) -> np.ndarray:
+        L = _abi.lib()
+        n = C.c_size_t()
+        self._c(L.tmd_gpu_pairs(self._h, None, 0, C.byref(n)))
+        out = np.empty((max(n.value, 1), 2), np.int64)
+        self._c(L.tmd_gpu_pairs(self._h, _ptr(out), n.value, C.byref(n)))
+        return out[: n.value]
+
+    def launch_count(self) -> int:
+        return int(_abi.lib().tmd_gpu_launch_count(self._h))
+
+
+# ---------------------------------------------------------------------------
+# communication backends
+
+@dataclass
+class Transfer:
+    """One message: `me` is the local rank, `peer` the remote one."""
+    me: int
+    peer: int
+    tag: int
+    tensor: object
+
+
+class Comm:
+    nranks: int
+    local_ranks: Sequence[int]
+
+    def allreduce_max(self, vals: Dict[int, float]) -> float:
+        raise NotImplementedError
+
+    def allreduce_sum(self, vals: Dict[int, np.ndarray]) -> np.ndarray:
+        raise NotImplementedError
+
+    def allgather(self, vals: Dict[int, np.ndarray]) -> np.ndarray:
+        """Rows of every rank's int64 vector, stacked in rank order."""
+        raise NotImplementedError
+
+    def exchange(self, sends: List[Transfer], recvs: List[Transfer]) -> None:
+        raise NotImplementedError
+
+    def barrier(self) -> None:
+        pass
+
+
+class InProcessComm(Comm):
+    """All ranks in this process; a transfer is a tensor copy."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.local_ranks = list(range(nranks))
+
+    def allreduce_max(self, vals):
+        return max(vals[r] for r in self.local_ranks)
+
+    def allreduce_sum(self, vals):
+        return np.sum([np.asarray(vals[r], np.float64) for r in self.local_ranks], axis=0)
+
+    def allgather(self, vals):
+        return np.stack([np.asarray(vals[r], np.int64) for r in self.local_ranks])
+
+    def exchange(self, sends, recvs):
+        box: Dict[Tuple[int, int, int], object] = {}
+        for s in sends:
+            key = (s.me, s.peer, s.tag)
+            if key in box:
+                raise RuntimeError(f"duplicate message {key}")
+            box[key] = s.tensor
+        for r in recvs:
+            src = box.pop((r.peer, r.me, r.tag))
+            if src.numel() != r.tensor.numel():
+                raise RuntimeError(f"message size mismatch {r.peer}->{r.me} tag {r.tag}: "
+                                   f"{src.numel()} vs {r.tensor.numel()}")
+            if src.numel():
+                r.tensor.copy_(src)
+        if box:
+            raise RuntimeError(f"unmatched messages: {sorted(box)}")
+        _sync_all()
+
+
+def _sync_all() -> None:
+    import torch
+    if torch.cuda.is_available():
+        for d in range(torch.cuda.device_count()):
+            torch.cuda.synchronize(d)
+
+
+class TorchDistComm(Comm):
+    """One rank per process over torch.distributed (NCCL on GPUs, gloo on CPU).
+
+    Point-to-point messages of one phase are posted as one batch, sends
+    ordered by (peer, tag) and receives by (peer, tag), so both ends of each
+    rank pair post matching messages in the same order (NCCL matches by
+    order, gloo by tag)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.nranks = dist.get_world_size(group)
+        self.me = dist.get_rank(group)
+        self.local_ranks = [self.me]
+        self.backend = dist.get_backend(group)
+
+    def _dev(self):
+        import torch
+        if self.backend == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
+    def allreduce_max(self, vals):
+        import torch
+        t = torch.tensor([float(vals[self.me])], dtype=torch.float64, device=self._dev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allreduce_sum(self, vals):
+        import torch
+        t = torch.tensor(np.asarray(vals[self.me], np.float64), device=self._dev())
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def allgather(self, vals):
+        import torch
+        v = torch.tensor(np.asarray(vals[self.me], np.int64), device=self._dev())
+        out = [torch.empty_like(v) for _ in range(self.nranks)]
+        self.dist.all_gather(out, v, group=self.group)
+        return torch.stack(out).cpu().numpy()
+
+    def exchange(self, sends, recvs):
+        ops = []
+        P2POp = self.dist.P2POp
+        for s in sorted(sends, key=lambda t: (t.peer, t.tag)):
+            if s.tensor.numel():
+                ops.append(P2POp(self.dist.isend, s.tensor.reshape(-1), s.peer, self.group,
+                                 s.tag))
+        for r in sorted(recvs, key=lambda t: (t.peer, t.tag)):
+            if r.tensor.numel():
+                ops.append(P2POp(self.dist.irecv, r.tensor.reshape(-1), r.peer, self.group,
+                                 r.tag))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+        if self.backend == "nccl":
+            import torch
+            torch.cuda.synchronize()
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# the decomposed engine
+
+class DecomposedEngine:
+    """Engine (engine.hpp:66-290) over a z-slab decomposition.
+
+    Every rank constructs it with the same whole system (FlatConfig) and
+    keeps its slab; `ctx_factory(rank)` creates the per-rank context (a
+    `SlabContext` on GPU `device_of(rank)` by default). With `InProcessComm`
+    one process holds every rank's context.
+    """
+
+    def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
+                 cfg: Optional[EngineConfig] = None, comm: Optional[Comm] = None,
+                 device_of=None, ctx_factory=None):
+        cfg = cfg or EngineConfig()
+        validate_engine_config(cfg)
+        if comm is None:
+            raise ConfigError("DecomposedEngine needs a Comm (InProcessComm / TorchDistComm)")
+        if comm.nranks < 2:
+            raise ConfigError("a decomposition needs at least 2 ranks; use Engine")
+        self.comm = comm
+        self.cfg = cfg
+        self.n_total = flat.size()
+        self.box = flat.box.copy()
+        self.r_skin = float(r_skin)
+        self.thr = 0.25 * self.r_skin * self.r_skin  # needs_rebuild (nl.hpp:143)
+        R = comm.nranks
+        if device_of is None:
+            device_of = (lambda r: 0) if isinstance(comm, InProcessComm) else (lambda r: r)
+        if ctx_factory is None:
+            def ctx_factory(r):
+                return SlabContext(flat, inter, r_skin, cfg, r, R, device_of(r))
+        self.ctx = {r: ctx_factory(r) for r in comm.local_ranks}
+        self.nb: Dict[int, Tuple[int, int]] = {}
+        self.ng: Dict[int, Tuple[int, int]] = {}
+        self.steps = 0
+        self.rebuilds = 0
+        self.exchanged_bytes = 0
+        self._rebuild(advance=False)
+        for c in self.ctx.values():
+            c.forces(0)
+
+    def close(self) -> None:
+        for c in self.ctx.values():
+            c.close()
+
+    # -- protocol phases ---------------------------------------------------------
+    def _rebuild(self, advance: bool) -> None:
+        R = self.comm.nranks
+        for c in self.ctx.values():
+            c.decide(True, advance)
+        # 1. migration of leavers to the owners of their z layers
+        out = {r: c.migrate_out() for r, c in self.ctx.items()}
+        M = self.comm.allgather({r: out[r][0] for r in self.ctx})  # M[src, dst]
+        sends, recvs = [], []
+        for r, c in self.ctx.items():
+            counts, buf = out[r]
+            off = np.concatenate([[0], np.cumsum(counts)]) * c.rec_bytes
+            for d in range(R):
+                if counts[d]:
+                    sends.append(Transfer(r, d, TAG_MIGRATE, buf[off[d]:off[d + 1]]))
+            col = M[:, r]
+            rbuf = c.migrate_in(int(col.sum()))
+            roff = np.concatenate([[0], np.cumsum(col)]) * c.rec_bytes
+            for s in range(R):
+                if col[s]:
+                    recvs.append(Transfer(r, s, TAG_MIGRATE, rbuf[roff[s]:roff[s + 1]]))
+            self.exchanged_bytes += int(counts.sum()) * c.rec_bytes
+        self.comm.exchange(sends, recvs)
+        # 2. resort + boundary-layer export
+        for r, c in self.ctx.items():
+            self.nb[r] = c.commit()
+        NB = self.comm.allgather({r: np.asarray(self.nb[r], np.int64) for r in self.ctx})
+        sends, recvs = [], []
+        for r, c in self.ctx.items():
+            lo_rank, hi_rank = (r - 1) % R, (r + 1) % R
+            n_lo, n_hi = int(NB[lo_rank, 1]), int(NB[hi_rank, 0])
+            self.ng[r] = (n_lo, n_hi)
+            lo, hi = c.ghost_in(n_lo, n_hi)
+            b0 = c.border(0, self.nb[r][0])  # my lowest layer -> lower neighbour's upper ghost
+            b1 = c.border(1, self.nb[r][1])  # my highest layer -> upper neighbour's lower ghost
+            for k in range(3):
+                sends.append(Transfer(r, lo_rank, TAG_GHOST_HI + k, b0[k]))
+                sends.append(Transfer(r, hi_rank, TAG_GHOST_LO + k, b1[k]))
+                recvs.append(Transfer(r, lo_rank, TAG_GHOST_LO + k, lo[k]))
+                recvs.append(Transfer(r, hi_rank, TAG_GHOST_HI + k, hi[k]))
+            self.exchanged_bytes += (self.nb[r][0] + self.nb[r][1]) * 40 + 8 * c.dxy
+        self.comm.exchange(sends, recvs)
+        # 3. cell ranges of the ghost layers + list build
+        for c in self.ctx.values():
+            c.ghosts_ready()
+
+    def _halo(self) -> None:
+        R = self.comm.nranks
+        sends, recvs = [], []
+        for r, c in self.ctx.items():
+            send, recv = c.halo(self.nb[r], *self.ng[r])
+            lo_rank, hi_rank = (r - 1) % R, (r + 1) % R
+            sends.append(Transfer(r, lo_rank, TAG_HALO_HI, send[0]))
+            sends.append(Transfer(r, hi_rank, TAG_HALO_LO, send[1]))
+            recvs.append(Transfer(r, lo_rank, TAG_HALO_LO, recv[0]))
+            recvs.append(Transfer(r, hi_rank, TAG_HALO_HI, recv[1]))
+            self.exchanged_bytes += 32 * (self.nb[r][0] + self.nb[r][1])
+        self.comm.exchange(sends, recvs)
+
+    # -- Engine surface ------------------------------------------------------------
+    def run(self, steps: int) -> None:
+        """steps x velocity Verlet (engine.hpp:80-110's loop): kick + drift, then per
+        step the global rebuild test, (rebuild,) forces + closing half-kick fused
+        with the next opening half-kick + drift, halo exchange."""
+        if steps < 0:
+            raise ConfigError("step count must be non-negative")
+        if steps == 0:
+            return
+        for c in self.ctx.values():
+            c.kick_drift()
+        self._halo()
+        for s in range(steps):
+            m = self.comm.allreduce_max({r: c.max_d2() for r, c in self.ctx.items()})
+            if m > self.thr:
+                self._rebuild(advance=True)
+                self.rebuilds += 1
+            else:
+                for c in self.ctx.values():
+                    c.decide(False, True)
+            last = s + 1 == steps
+            for c in self.ctx.values():
+                c.forces(1 if last else 2)
+            if not last:
+                self._halo()
+        for c in self.ctx.values():
+            c.max_d2()  # drains the stream and raises pending physics errors
+        self.steps += steps
+
+    def step(self) -> None:
+        self.run(1)
+
+    def observe(self) -> StepObservables:
+        tot = self.comm.allreduce_sum({r: c.sums() for r, c in self.ctx.items()})
+        pe, w, ke = (float(v) for v in tot)
+        return StepObservables(self.steps, ke, pe, 2.0 * ke / (3.0 * self.n_total), w)
+
+    def step_count(self) -> int:
+        return self.steps
+
+    def rebuild_count(self) -> int:
+        return self.rebuilds
+
+    def size(self) -> int:
+        return self.n_total
+
+    # -- local state (this process's ranks) ---------------------------------------
+    def local_state(self):
+        """(ids, pos, vel, forces) of the particles this process's ranks own,
+        sorted by id."""
+        parts = [c.download() for c in self.ctx.values()]
+        ids = np.concatenate([p[0] for p in parts])
+        o = np.argsort(ids, kind="stable")
+        return tuple(np.concatenate([p[k] for p in parts])[o] for k in range(4))
+
+    def local_pairs(self) -> np.ndarray:
+        ps = [c.pairs() for c in self.ctx.values()]
+        p = np.concatenate(ps) if ps else np.empty((0, 2), np.int64)
+        if len(p):
+            p = p[np.lexsort((p[:, 1], p[:, 0]))]
+        return p
+
+    def slab_sizes(self) -> Dict[int, dict]:
+        return {r: c.info() for r, c in self.ctx.items()}
+
+    def launch_count(self) -> int:
+        return sum(c.launch_count() for c in self.ctx.values())

@@ -192,11 +192,9 @@ def run_ours(args) -> None:
 
     ws, rank, local = dist_env()
     if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
+        run_decomposed(args)
+        return
+    torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
 
     cfg_w = workload(args.cells)
@@ -210,8 +208,6 @@ def run_ours(args) -> None:
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
     launches0 = eng.launch_count()
     rebuilds0 = eng.rebuild_count()
     with ClockSampler(dev) as clocks:
@@ -223,13 +219,8 @@ def run_ours(args) -> None:
     ms = ev0.elapsed_time(ev1)
     launches = eng.launch_count() - launches0
     rebuilds = eng.rebuild_count() - rebuilds0
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        torch.distributed.barrier()
     ms_per_step = ms / args.steps
-    value = ws * n * args.steps / (ms * 1e-3)   # replicas: every rank steps n particles
+    value = n * args.steps / (ms * 1e-3)
 
     # -- roofline of the force kernel -----------------------------
     st = eng.list_stats()
@@ -270,8 +261,6 @@ def run_ours(args) -> None:
 
     # -- e2e through the public API from host buffers ----------------------------------
     torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
     h2d = flat.pos.nbytes + flat.vel.nbytes + flat.id.nbytes
     t0 = time.perf_counter()
     e2 = E.Engine(flat, E.Interactions(), 0.3, ecfg)
@@ -284,17 +273,13 @@ def run_ours(args) -> None:
     t_e2e = time.perf_counter() - t0
     d2h = obs_bytes + out.pos.nbytes + out.vel.nbytes + out.id.nbytes
     e2.close()
-    if ws > 1:
-        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_e2e = float(t.item())
-    e2e = {"value": ws * n * args.steps / t_e2e, "unit": UNIT,
+    e2e = {"value": n * args.steps / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "seconds": t_e2e,
            "what": "Engine(create from host arrays) + K x (run(1) + observe()) + flatten()"}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         try:
             v, cores, sample, _ = cpu_reference_run(args.cells, args.steps, 2,
                                                     args.cpu_budget_s)
@@ -304,22 +289,111 @@ def run_ours(args) -> None:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
-    if ws > 1:
-        torch.distributed.destroy_process_group()
-    if rank != 0:
-        return
     cfg = dict(cfg_w)
-    cfg.update({"parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas "
-                "(spatial decomposition not yet wired into bench)",
+    cfg.update({"parallelism": "single GPU",
                 "l2": "working set > 126 MB L2 (neighbour list alone ~0.4 GB); no flush",
                 "rebuilds_in_timed_region": rebuilds, "section_timers": False,
                 "nbr_capacity": st["capacity"], "cell_grid": list(st["dims"])})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak" if ws > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+
+
+def run_decomposed(args) -> None:
+    """N > 1: the BASELINE config on an N-slab z decomposition (decomp.py), one
+    process per GPU, NCCL point-to-point halo/migration + all-reduces
+    (strong scaling: the same 1M-particle system at every N)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2109_10876_b200 import engine as E
+    from paper_2109_10876_b200.decomp import DecomposedEngine, TorchDistComm
+
+    ws, rank, local = dist_env()
+    if args.dist_backend == "gloo":
+        # pipeline check on a one-GPU box: every rank on GPU 0, buffers staged
+        # through host memory (the numbers are not a scaling measurement)
+        local = 0
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    cfg_w = workload(args.cells)
+    n = cfg_w["n_particles"]
+    flat = E.gen_fcc(args.cells, 0.8442, 1.0, 12345)
+    ecfg = E.EngineConfig(dt=0.005, section_timers=False, device=dev)
+
+    def make():
+        return DecomposedEngine(flat, E.Interactions(), 0.3, ecfg, comm=TorchDistComm(),
+                                device_of=lambda r: local)
+
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    eng = make()
+    eng.run(args.warmup)
+    ctx = eng.ctx[rank]
+    stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = eng.launch_count()
+    rebuilds0 = eng.rebuild_count()
+    bytes0 = eng.exchanged_bytes
+    with ClockSampler(dev) as clocks:
+        ev0.record(stream)
+        eng.run(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    dist.barrier()
+    launches = eng.launch_count() - launches0
+    rebuilds = eng.rebuild_count() - rebuilds0
+    xbytes = eng.exchanged_bytes - bytes0
+    sizes = eng.slab_sizes()[rank]
+    eng.close()
+
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    e2 = make()
+    for _ in range(args.steps):
+        e2.run(1)
+        e2.observe()
+    ids, pos, vel, _f = e2.local_state()
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
+    e2.close()
+    h2d = flat.pos.nbytes + flat.vel.nbytes + flat.id.nbytes
+    d2h = 40 * args.steps + pos.nbytes + vel.nbytes + ids.nbytes
+    dist.destroy_process_group()
+    if rank != 0:
+        return
+    cfg = dict(cfg_w)
+    cfg.update({"parallelism": f"{ws} z-slabs (spatial decomposition, {args.dist_backend} "
+                               "halo + migration)",
+                "l2": "working set > 126 MB L2 on every rank at 1M / N; no flush",
+                "rebuilds_in_timed_region": rebuilds, "section_timers": False,
+                "rank0_slab": sizes, "exchanged_bytes_rank0": xbytes})
+    line = {
+        "metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg, "roofline": None, "cpu_baseline": None,
+        "e2e": {"value": n * args.steps / t_e2e, "unit": UNIT,
+                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                "seconds": t_e2e,
+                "what": "DecomposedEngine(create) + K x (run(1) + observe()) + local_state()"},
+        "gpu_launches": launches * ws, "clocks": clocks.summary(),
     }
     print(json.dumps(line))
 
@@ -335,6 +409,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="N > 1 only; gloo = pipeline check with every rank on GPU 0")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

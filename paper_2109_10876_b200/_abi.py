@@ -98,19 +98,19 @@ def lib() -> C.CDLL:
                                       C.POINTER(TmdFeneParams), C.POINTER(TmdEngineParams),
                                       C.c_int, C.c_int, C.POINTER(P)]
     PP = C.POINTER(P)
-    L.tmd_gpu_slab_info.argtypes = [P, C.POINTER(C.c_int64)]
+    L.tmd_gpu_slab_info.argtypes = [P, P]
     L.tmd_gpu_slab_max_d2.argtypes = [P, C.POINTER(C.c_double)]
     L.tmd_gpu_slab_decide.argtypes = [P, C.c_int, C.c_int]
-    L.tmd_gpu_slab_migrate_out.argtypes = [P, C.POINTER(C.c_int64), PP]
+    L.tmd_gpu_slab_migrate_out.argtypes = [P, P, PP]
     L.tmd_gpu_slab_migrate_in.argtypes = [P, C.c_int64, PP]
-    L.tmd_gpu_slab_commit.argtypes = [P, C.POINTER(C.c_int64)]
+    L.tmd_gpu_slab_commit.argtypes = [P, P]
     L.tmd_gpu_slab_border.argtypes = [P, C.c_int, PP, PP, PP]
     L.tmd_gpu_slab_ghost_in.argtypes = [P, C.c_int64, C.c_int64, PP, PP]
     L.tmd_gpu_slab_ghosts_ready.argtypes = [P]
     L.tmd_gpu_slab_kick_drift.argtypes = [P]
     L.tmd_gpu_slab_forces.argtypes = [P, C.c_int]
     L.tmd_gpu_slab_halo.argtypes = [P, PP, PP]
-    L.tmd_gpu_slab_sums.argtypes = [P, C.POINTER(C.c_double)]
+    L.tmd_gpu_slab_sums.argtypes = [P, P]
     L.tmd_gpu_last_error.argtypes = [P]
     L.tmd_gpu_last_error.restype = C.c_char_p
     L.tmd_gpu_compute_forces.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]

@@ -145,8 +145,8 @@ class SlabContext:
 
     # -- protocol
     def info(self) -> dict:
-        a = (C.c_int64 * 10)()
-        self._c(_abi.lib().tmd_gpu_slab_info(self._h, a))
+        a = np.zeros(10, np.int64)
+        self._c(_abi.lib().tmd_gpu_slab_info(self._h, _ptr(a)))
         keys = ("rank", "nranks", "z0", "zown", "n_own", "n_lo", "n_hi", "dxy", "n_cap",
                 "rec_bytes")
         return dict(zip(keys, (int(v) for v in a)))
@@ -243,6 +243,9 @@ class SlabContext:
 
     def launch_count(self) -> int:
         return int(_abi.lib().tmd_gpu_launch_count(self._h))
+
+    def stream_handle(self) -> int:
+        return int(_abi.lib().tmd_gpu_stream(self._h) or 0)
 
 
 # ---------------------------------------------------------------------------
@@ -363,21 +366,33 @@ class TorchDistComm(Comm):
         return torch.stack(out).cpu().numpy()
 
     def exchange(self, sends, recvs):
-        ops = []
+        import torch
+        # gloo moves host memory only: device buffers are staged through host
+        # copies (used by the one-GPU multi-process test; NCCL sends in place)
+        stage = self.backend != "nccl"
+
+        def host(t):
+            return t.cpu() if (stage and t.is_cuda) else t
+        ops, back = [], []
         P2POp = self.dist.P2POp
         for s in sorted(sends, key=lambda t: (t.peer, t.tag)):
             if s.tensor.numel():
-                ops.append(P2POp(self.dist.isend, s.tensor.reshape(-1), s.peer, self.group,
-                                 s.tag))
+                ops.append(P2POp(self.dist.isend, host(s.tensor).reshape(-1), s.peer,
+                                 self.group, s.tag))
         for r in sorted(recvs, key=lambda t: (t.peer, t.tag)):
             if r.tensor.numel():
-                ops.append(P2POp(self.dist.irecv, r.tensor.reshape(-1), r.peer, self.group,
+                buf = r.tensor
+                if stage and buf.is_cuda:
+                    buf = torch.empty(buf.shape, dtype=buf.dtype)
+                    back.append((r.tensor, buf))
+                ops.append(P2POp(self.dist.irecv, buf.reshape(-1), r.peer, self.group,
                                  r.tag))
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
-        if self.backend == "nccl":
-            import torch
+        for dev_t, host_t in back:
+            dev_t.copy_(host_t)
+        if self.backend == "nccl" or back:
             torch.cuda.synchronize()
 
     def barrier(self):

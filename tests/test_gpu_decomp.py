@@ -105,3 +105,62 @@ def test_slab_config_errors():
     with pytest.raises(E.ConfigError):
         DecomposedEngine(flat, E.Interactions(), float(g["r_skin"]),
                          E.EngineConfig(dt=float(g["dt"])), comm=InProcessComm(2))
+
+
+def _mp_worker(rank, world, port, q):
+    """One rank of a multi-process decomposition on GPU 0 (gloo moves the
+    buffers through host memory; no kernel waits on another rank)."""
+    import torch.distributed as dist
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world,
+                                init_method=f"tcp://127.0.0.1:{port}")
+        from paper_2109_10876_b200.decomp import TorchDistComm
+        g = load("fcc8_jit")
+        flat = E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"])
+        eng = DecomposedEngine(flat, E.Interactions(), float(g["r_skin"]),
+                               E.EngineConfig(dt=float(g["dt"])), comm=TorchDistComm(),
+                               device_of=lambda r: 0)
+        pairs0 = eng.local_pairs()
+        eng.run(int(g["steps"]))
+        o = eng.observe()
+        st = eng.local_state()
+        objs = [None] * world
+        dist.all_gather_object(objs, (pairs0, st, eng.rebuild_count(), o.kinetic + o.potential))
+        eng.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok", objs if rank == 0 else None))
+    except BaseException:
+        import traceback
+        q.put((rank, "err", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_torch_distributed(world):
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r for r in res if r[1] != "ok"]
+    assert not errs, errs[0][2]
+    objs = res[0][2]
+    g = load("fcc8_jit")
+    pairs = np.concatenate([o[0] for o in objs])
+    pairs = pairs[np.lexsort((pairs[:, 1], pairs[:, 0]))]
+    np.testing.assert_array_equal(pairs, g["pairs"])
+    ids = np.concatenate([o[1][0] for o in objs])
+    order = np.argsort(ids)
+    np.testing.assert_array_equal(ids[order], np.sort(g["ids"]))
+    pos = np.concatenate([o[1][1] for o in objs])[order]
+    vel = np.concatenate([o[1][2] for o in objs])[order]
+    assert np.abs(pos - g["final_pos"]).max() < 1e-9
+    assert np.abs(vel - g["final_vel"]).max() < 1e-9
+    assert all(o[2] == int(g["rebuilds"]) for o in objs)

@@ -103,12 +103,11 @@ class Engine {
  public:
   // build_domain(flat, inter, r_skin, n_sub) + Engine(domain, cfg)
   // (domain.hpp:134-189, engine.hpp:68-77). n_sub / worker_threads have no
-  // GPU meaning and are ignored; a thermostat or bonded terms are rejected
-  // with ConfigError until those rows land.
+  // GPU meaning and are ignored; bonded terms are rejected with ConfigError
+  // until that row lands. A thermostat runs on the device.
   Engine(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
          const taskmd::EngineConfig& cfg, const GpuOptions& opt = {})
       : cfg_(cfg) {
-    if (cfg.thermostat) throw taskmd::ConfigError("the GPU path has no thermostat yet");
     if (inter.angle) throw taskmd::ConfigError("angle terms are not on the GPU LJ path");
     if (inter.fene || !flat.topo.bonds.empty()) {
       throw taskmd::ConfigError("FENE bonds are not on the GPU path yet");
@@ -142,6 +141,12 @@ class Engine {
     p.section_timers = opt.section_timers ? 1 : 0;
     p.nbr_capacity = opt.nbr_capacity;
     p.reserved[0] = opt.variant;
+    if (cfg.thermostat) {
+      p.thermostat = 1;
+      p.gamma = cfg.thermostat->gamma;
+      p.temperature = cfg.thermostat->temperature;
+      p.seed = cfg.thermostat->seed;
+    }
     const int rc = tmd_gpu_create(&sys, &lj, nullptr, &p, &ctx_);
     if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
     box_ = flat.box;

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TMD_GPU_ABI_VERSION 1
+#define TMD_GPU_ABI_VERSION 2
 
 /* Status codes. */
 #define TMD_OK 0
@@ -89,8 +89,18 @@ typedef struct tmd_engine_params {
                          times per phase; 0: only `elapsed` */
   int nbr_capacity;  /* 0 = auto (sized from the first build); else fixed
                         entries per particle (rounded up to a multiple of 8) */
-  int reserved[5];   /* reserved[0]: kernel variant, 0/2 = brick-staged shared
-                        memory (default), 1 = thread-per-particle L1 gathers */
+  int reserved[5];   /* [0] kernel variant: 0 = default (3), 1 = thread-per-
+                        particle ELL list, 2 = brick-staged shared memory,
+                        3 = sector-chunked list + 256-bit gathers;
+                        [1] variant-3 gathers in flight (1/2/4/8, 0 = 4);
+                        [2] 1 = no CUDA graphs */
+  /* EngineConfig::thermostat (optional<LangevinParams>, potentials.hpp:174-178):
+   * thermostat = 0 is NVE. The Langevin force of thermostat_and_half_kick
+   * (engine.hpp:209-239) with counter_normal3(seed, kThermostat, step, id). */
+  int thermostat;
+  double gamma;
+  double temperature;
+  uint64_t seed;
 } tmd_engine_params;
 
 /* taskmd::StepObservables (engine.hpp:43-48) plus the virial

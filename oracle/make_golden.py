@@ -89,12 +89,15 @@ def exact_energies(box, pos_by_id, pairs, lj=(1.0, 1.0, 2.5, True)):
 
 
 def system_fixture(name, box, ids, pos, vel, *, r_skin=0.3, n_subs=(1, 8), steps=0,
-                   trace_every=0, dt=0.005, oracle=False):
+                   trace_every=0, dt=0.005, oracle=False, thermostat=None):
     out = dict(box=box, ids=ids, pos=pos, vel=vel, r_skin=np.float64(r_skin),
                dt=np.float64(dt))
+    if thermostat is not None:
+        out["thermostat"] = np.array(thermostat, dtype=np.float64)  # gamma, T, seed
     pairs0 = None
     for ns in n_subs:
-        e = ref.RefEngine(box, ids, pos, vel, r_skin=r_skin, n_sub=ns, dt=dt)
+        e = ref.RefEngine(box, ids, pos, vel, r_skin=r_skin, n_sub=ns, dt=dt,
+                          thermostat=thermostat)
         p = e.pairs()
         if pairs0 is None:
             pairs0 = p
@@ -134,10 +137,29 @@ def system_fixture(name, box, ids, pos, vel, *, r_skin=0.3, n_subs=(1, 8), steps
     print(f"  {name}: n={len(ids)} pairs={len(pairs0)} dims={out['dims'].tolist()}")
 
 
+def thermostat_fixtures():
+    """Langevin runs (thermostat_and_half_kick, engine.hpp:209-239): the
+    reference's worker-independence system (test_engine.cpp:214-240) and a
+    jittered FCC melt."""
+    b, i, p, v = jittered_lattice(6, 7.2, 29, 0.05, 0.0)
+    system_fixture("langevin_jit6", b, i, p, v, n_subs=(1, 8), steps=30, trace_every=5,
+                   thermostat=(1.0, 0.8, 99))
+    b, i, p = fcc(8, 0.8442)
+    for k in range(len(i)):
+        u = ref.counter_uniform3(777, K_PLACEMENT, 0, k)
+        p[k] += 0.15 * (2.0 * u - 1.0)
+    v = ref.thermal_velocities(i, 0.7, 4242)
+    system_fixture("langevin_fcc8", b, i, p, v, n_subs=(1, 8), steps=100, trace_every=20,
+                   thermostat=(0.5, 1.4, 2021))
+
+
 def main():
     if not ref.available():
         ref.build()
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--only-thermostat" in sys.argv:
+        thermostat_fixtures()
+        return
 
     # -- scalar LJ: lj_eval over a grid of r2 (test_potentials.cpp:33-89)
     r2 = np.concatenate([np.linspace(0.64, 7.0, 257), [2 ** (1 / 3), 1.0, 6.25,
@@ -221,6 +243,7 @@ def main():
         ids = (np.arange(n, dtype=np.int64) * 7919) % 100003  # non-contiguous ids
         vel = ref.thermal_velocities(ids, 0.5, 99)
         system_fixture(name, box, ids, pos, vel, n_subs=(1,), steps=50, trace_every=10)
+    thermostat_fixtures()
     # SC lattice 4000 (acceptance criterion 3): energy traces at dt 0.005, 0.001
     b, i, p, v = ref.gen_lattice(4000, 0.8442, 0.6, 3)
     traces = {}

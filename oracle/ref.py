@@ -49,6 +49,9 @@ def lib() -> C.CDLL:
         D = C.c_double
         L.ref_create.argtypes = [C.c_int64, P, P, P, P, P, D, D, D, C.c_int, D,
                                  C.c_int, C.c_int, D, C.POINTER(P), C.c_char_p, C.c_int]
+        L.ref_create_thermo.argtypes = [C.c_int64, P, P, P, P, P, D, D, D, C.c_int, D,
+                                        C.c_int, C.c_int, D, D, D, C.c_uint64,
+                                        C.POINTER(P), C.c_char_p, C.c_int]
         L.ref_destroy.argtypes = [P]
         L.ref_destroy.restype = None
         L.ref_step.argtypes = [P, C.c_int64, C.c_char_p, C.c_int]
@@ -117,7 +120,9 @@ class RefEngine:
     """build_domain + Engine of the reference, on the host cores."""
 
     def __init__(self, box, ids, pos, vel=None, mass=None, *, eps=1.0, sigma=1.0,
-                 r_cut=2.5, shifted=True, r_skin=0.3, n_sub=1, workers=1, dt=0.005):
+                 r_cut=2.5, shifted=True, r_skin=0.3, n_sub=1, workers=1, dt=0.005,
+                 thermostat=None):
+        """thermostat: None (NVE) or (gamma, temperature, seed)."""
         L = lib()
         self._ids = _c(ids, np.int64)
         self._n = int(self._ids.shape[0])
@@ -127,9 +132,16 @@ class RefEngine:
         mass = _c(mass, np.float64)
         err = C.create_string_buffer(512)
         h = C.c_void_p()
-        rc = L.ref_create(self._n, _p(self._ids), _p(mass), _p(pos), _p(vel), _p(box),
-                          eps, sigma, r_cut, 1 if shifted else 0, r_skin, n_sub,
-                          workers, dt, C.byref(h), err, 512)
+        if thermostat is None:
+            rc = L.ref_create(self._n, _p(self._ids), _p(mass), _p(pos), _p(vel), _p(box),
+                              eps, sigma, r_cut, 1 if shifted else 0, r_skin, n_sub,
+                              workers, dt, C.byref(h), err, 512)
+        else:
+            gamma, temp, seed = thermostat
+            rc = L.ref_create_thermo(self._n, _p(self._ids), _p(mass), _p(pos), _p(vel),
+                                     _p(box), eps, sigma, r_cut, 1 if shifted else 0, r_skin,
+                                     n_sub, workers, dt, float(gamma), float(temp), int(seed),
+                                     C.byref(h), err, 512)
         _raise(rc, err)
         self._h = h
 

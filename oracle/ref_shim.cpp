@@ -132,6 +132,32 @@ int ref_create(std::int64_t n, const std::int64_t* id, const double* mass,
   });
 }
 
+// The same with EngineConfig::thermostat set (engine.hpp:19-26; the bath is
+// applied by thermostat_and_half_kick, engine.hpp:209-239).
+int ref_create_thermo(std::int64_t n, const std::int64_t* id, const double* mass,
+                      const double* pos, const double* vel, const double box[3], double eps,
+                      double sigma, double rc, int shifted, double r_skin, int n_sub,
+                      int workers, double dt, double gamma, double temperature,
+                      std::uint64_t seed, ref_engine** out, char* err, int errlen) {
+  *out = nullptr;
+  return guarded(err, errlen, [&] {
+    FlatConfig f = make_flat(n, id, mass, pos, vel, box);
+    EngineConfig cfg;
+    cfg.dt = dt;
+    cfg.n_sub = n_sub;
+    cfg.worker_threads = workers;
+    LangevinParams bath;
+    bath.gamma = gamma;
+    bath.temperature = temperature;
+    bath.seed = seed;
+    cfg.thermostat = bath;
+    auto h = std::make_unique<ref_engine>();
+    h->eng = std::make_unique<Engine>(
+        build_domain(f, make_inter(eps, sigma, rc, shifted), r_skin, n_sub), cfg);
+    *out = h.release();
+  });
+}
+
 void ref_destroy(ref_engine* h) { delete h; }
 
 // Engine::run (engine.hpp:128).

@@ -61,7 +61,9 @@ class TmdFeneParams(C.Structure):
 class TmdEngineParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("r_skin", C.c_double),
                 ("device", C.c_int), ("section_timers", C.c_int),
-                ("nbr_capacity", C.c_int), ("reserved", C.c_int * 5)]
+                ("nbr_capacity", C.c_int), ("reserved", C.c_int * 5),
+                ("thermostat", C.c_int), ("gamma", C.c_double),
+                ("temperature", C.c_double), ("seed", C.c_uint64)]
 
 
 class TmdObservables(C.Structure):

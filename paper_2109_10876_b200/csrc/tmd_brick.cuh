@@ -869,10 +869,10 @@ __global__ void __launch_bounds__(kForceThreads)
         }
       }
       if (active) {
+        integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
         fx[i] = ax;
         fy[i] = ay;
         fz[i] = az;
-        integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
       }
     }
   }
@@ -935,10 +935,10 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
+    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
     fx[i] = ax;
     fy[i] = ay;
     fz[i] = az;
-    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
   }
   const double te = block_sum<128>(e, red);
   const double tw = block_sum<128>(w, red);

@@ -89,7 +89,7 @@ struct Ctrl {
   int cap;                    // current list capacity per particle
   long long entries;          // total entries, last build
   int max_halo;               // largest staged halo seen (slots)
-  int pad_;
+  int err_bit;                // status bit of the first error (its record below)
 };
 
 // ---------------------------------------------------------------------------
@@ -185,10 +185,78 @@ __device__ __forceinline__ void record_error(Ctrl* ctrl, int bit, long long id0,
                                              long long id1) {
   atomicOr(&ctrl->status, bit);
   if (atomicCAS(&ctrl->err_lock, 0, 1) == 0) {
+    ctrl->err_bit = bit;
     ctrl->err_step = ctrl->step;
     ctrl->err_id0 = id0;
     ctrl->err_id1 = id1;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based normal deviates on the device (random.hpp:20-81): splitmix64
+// finalizer chained over (seed, context, step, id, lane), two Box-Muller pairs
+// over lanes 0..3, the fourth deviate discarded. The integer hash and the
+// unit conversions are exact; log / cos / sin are CUDA's (<= 2 ulp), the
+// reference's are glibc's, so a deviate can differ in its last bits.
+constexpr unsigned long long kRngThermostat = 1;  // RngContext::kThermostat
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned long long counter_hash(unsigned long long seed,
+                                                           unsigned long long ctx,
+                                                           unsigned long long step,
+                                                           unsigned long long id,
+                                                           unsigned long long lane) {
+  unsigned long long h = mix64(seed ^ 0x243f6a8885a308d3ull);
+  h = mix64(h ^ ctx);
+  h = mix64(h ^ step);
+  h = mix64(h ^ id);
+  return mix64(h ^ lane);
+}
+
+__device__ __forceinline__ void counter_normal3(unsigned long long seed, unsigned long long ctx,
+                                                unsigned long long step, unsigned long long id,
+                                                double& n0, double& n1, double& n2) {
+  const double p53 = 1.1102230246251565e-16;  // 2^-53
+  const double u0 = __dmul_rn(static_cast<double>((counter_hash(seed, ctx, step, id, 0) >> 11) + 1), p53);
+  const double u1 = __dmul_rn(static_cast<double>(counter_hash(seed, ctx, step, id, 1) >> 11), p53);
+  const double u2 = __dmul_rn(static_cast<double>((counter_hash(seed, ctx, step, id, 2) >> 11) + 1), p53);
+  const double u3 = __dmul_rn(static_cast<double>(counter_hash(seed, ctx, step, id, 3) >> 11), p53);
+  const double two_pi = 6.283185307179586476925286766559;
+  const double r0 = __dsqrt_rn(__dmul_rn(-2.0, log(u0)));
+  const double r1 = __dsqrt_rn(__dmul_rn(-2.0, log(u2)));
+  const double a = __dmul_rn(two_pi, u1);
+  n0 = __dmul_rn(r0, cos(a));
+  n1 = __dmul_rn(r0, sin(a));
+  n2 = __dmul_rn(r1, cos(__dmul_rn(two_pi, u3)));
+}
+
+// Langevin bath (potentials.hpp:174-197): f += -gamma m v + sqrt(2 m gamma T / dt) n,
+// with n = counter_normal3(seed, kThermostat, step, id) — the force that
+// thermostat_and_half_kick (engine.hpp:209-230) adds before the closing kick.
+struct Thermo {
+  int on;
+  double gamma, temperature, dt;
+  unsigned long long seed;
+};
+
+__device__ __forceinline__ void langevin_add(const Thermo& th, long long step, long long id,
+                                             double m, double vx, double vy, double vz,
+                                             double& fx, double& fy, double& fz) {
+  double n0, n1, n2;
+  counter_normal3(th.seed, kRngThermostat, static_cast<unsigned long long>(step),
+                  static_cast<unsigned long long>(id), n0, n1, n2);
+  const double amp = __dsqrt_rn(__ddiv_rn(
+      __dmul_rn(__dmul_rn(__dmul_rn(2.0, m), th.gamma), th.temperature), th.dt));
+  const double gm = __dmul_rn(-th.gamma, m);
+  fx = __dadd_rn(fx, __dadd_rn(__dmul_rn(gm, vx), __dmul_rn(amp, n0)));
+  fy = __dadd_rn(fy, __dadd_rn(__dmul_rn(gm, vy), __dmul_rn(amp, n1)));
+  fz = __dadd_rn(fz, __dadd_rn(__dmul_rn(gm, vz), __dmul_rn(amp, n2)));
 }
 
 template <int kThreads>

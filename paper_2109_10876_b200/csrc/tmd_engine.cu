@@ -1,14 +1,15 @@
 // libtmd_gpu.so — the B200 engine behind include/tmd_gpu.h.
 //
 // One context = one GPU = one cell-sorted, device-resident FP64 particle set.
-// A step enqueues (engine.hpp:80-126 phase order):
-//   Integrate  k_kick_drift (kick2 of step n-1 fused with kick1+drift of n)
-//   Neigh      k_decide (global max-displacement test, on device)
-//   Resort     k_wrap_bin, k_scan, k_scatter, k_sort_cells, k_permute,
-//              k_copy_back          (no-ops unless the device decided rebuild)
-//   Neigh      k_build_list         (no-op unless rebuild)
-//   Forces     k_lj_forces
-//   Integrate  k_kick2              (only at the end of a run() chunk)
+// A run of K steps enqueues (engine.hpp:80-126 phase order):
+//   Integrate  k_kick_drift         opening half-kick + drift of the first step
+//   per step:
+//   Neigh      k_decide             global max-displacement test, on device
+//   Resort     k_wrap_bin, scan, k_scatter, k_sort_cells, k_permute, k_copy_back,
+//              k_brick_groups + scan          (no-ops unless the device decided rebuild)
+//   Neigh      k_build_prologue, k_build_brick3 (no-op unless rebuild)
+//   Forces     k_forces_l1<kFused>  forces + closing half-kick (+ Langevin) of this
+//              step + opening half-kick + drift of the next (kKick2 on the last)
 // Nothing in a chunk waits for the host. The host synchronises once per
 // chunk to read the status word; a neighbour-list overflow rolls the chunk
 // back to its checkpoint, grows the list and replays it.
@@ -92,6 +93,7 @@ struct tmd_gpu_ctx {
   LjConst lj{};
   double dt = 0, half_dt = 0, r_skin = 0, r_cut = 0;
   bool timers_on = true;
+  Thermo th{};  // Langevin bath (th.on = 0: NVE)
 
   // particle arrays (cell-sorted) + alternates for the permutation
   double4 *pos = nullptr, *pos2 = nullptr, *snap = nullptr;
@@ -151,6 +153,7 @@ struct tmd_gpu_ctx {
   // chunk checkpoint (rollback on list overflow)
   double4* ck_pos = nullptr;
   double *ck_vx = nullptr, *ck_vy = nullptr, *ck_vz = nullptr, *ck_mass = nullptr;
+  double *ck_fx = nullptr, *ck_fy = nullptr, *ck_fz = nullptr;  // thermostat runs only
   long long* ck_id = nullptr;
 
   // host mirrors
@@ -215,6 +218,7 @@ void free_all(tmd_gpu_ctx* c) {
                   c->rank, c->perm,  c->count, c->start, c->nbr,    c->nnbr,
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
+                  c->ck_fx, c->ck_fy, c->ck_fz,
                   c->rebuild_log, c->cell_rank, c->brick_rank_off, c->ngroups,
                   c->group_off, c->decoded, c->scan_tmp, c->owner_of_z, c->mig_dest,
                   c->mig_count, c->mig_off, c->mig_keep, c->mig_send, c->mig_recv,
@@ -376,6 +380,7 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
   it.dt = c->dt;
   it.half_dt = c->half_dt;
   it.part_ke = c->part_ke;
+  it.th = c->th;
   if (c->variant == 1) {
     k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
@@ -415,20 +420,21 @@ void launch_forces(tmd_gpu_ctx* c, int mode = kForcesOnly) {
 
 int force_parts(const tmd_gpu_ctx* c) { return c->variant == 2 ? c->bg.nbricks : c->nblk; }
 
-void launch_kick_drift(tmd_gpu_ctx* c, bool fused) {
+void launch_kick_drift(tmd_gpu_ctx* c) {
   c->launches += 1;
-  const int n = static_cast<int>(c->n);
-  if (fused) {
-    k_kick_drift<true><<<c->nblk, kBlock, 0, c->ls>>>(
-        n, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
-        c->snap, c->dt, c->half_dt, c->part_ke, c->ctrl);
-  } else {
-    k_kick_drift<false><<<c->nblk, kBlock, 0, c->ls>>>(
-        n, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
-        c->snap, c->dt, c->half_dt, c->part_ke, c->ctrl);
-  }
+  k_kick_drift<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->pos, c->vx, c->vy,
+                                             c->vz, c->fx, c->fy, c->fz, c->mass, c->snap,
+                                             c->dt, c->half_dt, c->ctrl);
 }
 
+
+// The Langevin force of the initial evaluation (noise keyed as step 0).
+void launch_thermo_init(tmd_gpu_ctx* c) {
+  if (!c->th.on || c->n == 0) return;
+  c->launches += 1;
+  k_thermo_init<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
+                                              c->mass, c->id, c->th, c->fx, c->fy, c->fz);
+}
 
 void launch_reduce_pe(tmd_gpu_ctx* c) {
   c->launches += 2;
@@ -457,13 +463,16 @@ void sync_ctrl(tmd_gpu_ctx* c) {
 void raise_physics(tmd_gpu_ctx* c, bool with_step) {
   const Ctrl& h = *c->h_ctrl;
   std::string msg;
-  if (h.status & kStatOverlap) {
+  // the first error in time wins (later ones can be its consequences, e.g. a
+  // non-finite position binned at the origin then "overlaps")
+  const int first = (h.err_bit & h.status) ? h.err_bit : h.status;
+  if (first & kStatOverlap) {
     msg = "overlapping particles: ids " + std::to_string(h.err_id0) + " and " +
           std::to_string(h.err_id1) + " coincide";
-  } else if (h.status & kStatNonFinite) {
+  } else if (first & kStatNonFinite) {
     msg = "non-finite velocity or force on particle id " +
           std::to_string(h.err_id0);
-  } else if (h.status & kStatNonFinitePos) {
+  } else if (first & kStatNonFinitePos) {
     msg = "non-finite position for particle id " + std::to_string(h.err_id0);
   } else {
     return;
@@ -562,6 +571,7 @@ void setup_pass(tmd_gpu_ctx* c) {
     }
   }
   launch_forces(c);
+  launch_thermo_init(c);
   launch_reduce_pe(c);
   sync_ctrl(c);
   raise_physics(c, false);
@@ -579,6 +589,11 @@ void checkpoint(tmd_gpu_ctx* c) {
   cp(c->ck_vz, c->vz, n * sizeof(double));
   cp(c->ck_mass, c->mass, n * sizeof(double));
   cp(c->ck_id, c->id, n * sizeof(long long));
+  if (c->th.on) {  // the stored force carries the last Langevin kick: keep it
+    cp(c->ck_fx, c->fx, n * sizeof(double));
+    cp(c->ck_fy, c->fy, n * sizeof(double));
+    cp(c->ck_fz, c->fz, n * sizeof(double));
+  }
 }
 
 void restore(tmd_gpu_ctx* c, const Ctrl& at_checkpoint) {
@@ -593,6 +608,11 @@ void restore(tmd_gpu_ctx* c, const Ctrl& at_checkpoint) {
   cp(c->vz, c->ck_vz, n * sizeof(double));
   cp(c->mass, c->ck_mass, n * sizeof(double));
   cp(c->id, c->ck_id, n * sizeof(long long));
+  if (c->th.on) {
+    cp(c->fx, c->ck_fx, n * sizeof(double));
+    cp(c->fy, c->ck_fy, n * sizeof(double));
+    cp(c->fz, c->ck_fz, n * sizeof(double));
+  }
   Ctrl back = at_checkpoint;
   back.status = 0;
   back.err_lock = 0;
@@ -623,7 +643,7 @@ void capture_graph(tmd_gpu_ctx* c, int nsteps, tmd_gpu_ctx::StepGraph& out) {
                                    cudaStreamCaptureModeThreadLocal),
      "begin capture");
   c->ls = c->stream;
-  launch_kick_drift(c, false);
+  launch_kick_drift(c);
   uint64_t body = 0;
   for (int s = 0; s < nsteps; ++s) {
     cudaGraphConditionalHandle h;
@@ -675,7 +695,7 @@ void capture_graph(tmd_gpu_ctx* c, int nsteps, tmd_gpu_ctx::StepGraph& out) {
 void enqueue_segment(tmd_gpu_ctx* c, int64_t steps) {
   {
     Phase p(c, TMD_SECTION_INTEGRATE);
-    launch_kick_drift(c, false);
+    launch_kick_drift(c);
   }
   for (int64_t s = 0; s < steps; ++s) {
     {
@@ -751,7 +771,18 @@ void do_run(tmd_gpu_ctx* c, int64_t nsteps) {
       const Ctrl h = *c->h_ctrl;
       restore(c, before);
       grow_after_overflow(c, h);
-      setup_pass(c);
+      if (c->th.on) {
+        // the restored forces hold the Langevin kick of the checkpoint step
+        // (not recomputable): keep them and rebuild at the replay's first
+        // step instead of re-running the setup pass (force_rebuild = 2: a
+        // rebuild that is not counted as one of the reference's)
+        const int two = 2;
+        ck(cudaMemcpyAsync(&c->ctrl->force_rebuild, &two, sizeof(int), cudaMemcpyHostToDevice,
+                           c->stream), "cudaMemcpyAsync(force_rebuild)");
+        sync_ctrl(c);
+      } else {
+        setup_pass(c);
+      }
       continue;
     }
     c->step = c->h_ctrl->step;
@@ -802,6 +833,12 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
   // validate_engine_config (engine.hpp:28-41)
   if (!std::isfinite(p->dt) || p->dt == 0.0)
     cfg("time step must be finite and nonzero");
+  if (p->thermostat) {  // validate_langevin (potentials.hpp:180-189)
+    if (!(p->gamma >= 0.0) || !std::isfinite(p->gamma))
+      cfg("langevin gamma must be finite and >= 0");
+    if (!(p->temperature >= 0.0) || !std::isfinite(p->temperature))
+      cfg("langevin temperature must be finite and >= 0");
+  }
   if (s->n < 1) cfg("empty system: the GPU engine needs at least 1 particle");
   if (s->n > kMaxSlots) {
     cfg("system too large for one GPU context: " + std::to_string(s->n) +
@@ -1058,6 +1095,11 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->r_skin = params->r_skin;
     c->r_cut = lj->r_cut;
     c->timers_on = params->section_timers != 0;
+    c->th.on = params->thermostat != 0;
+    c->th.gamma = params->gamma;
+    c->th.temperature = params->temperature;
+    c->th.dt = params->dt;
+    c->th.seed = params->seed;
     c->variant = (params->reserved[0] >= 1 && params->reserved[0] <= 3) ? params->reserved[0]
                                                                        : kDefaultVariant;
     if (nranks > 1) c->variant = 3;  // slab mode runs the brick build + global-slot forces
@@ -1109,6 +1151,11 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->ck_vx = dalloc<double>(n); c->ck_vy = dalloc<double>(n); c->ck_vz = dalloc<double>(n);
     c->ck_mass = dalloc<double>(n);
     c->ck_id = dalloc<long long>(n);
+    if (params->thermostat) {
+      c->ck_fx = dalloc<double>(n);
+      c->ck_fy = dalloc<double>(n);
+      c->ck_fz = dalloc<double>(n);
+    }
     ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost");
     ck(cudaMallocHost(&c->h_scalars, 4 * sizeof(double)), "cudaMallocHost");
     std::memset(c->h_ctrl, 0, sizeof(Ctrl));
@@ -1777,7 +1824,7 @@ int tmd_gpu_slab_kick_drift(tmd_gpu_ctx* c) {
   return guard(c, [&] {
     need_slab(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    if (c->n > 0) launch_kick_drift(c, false);
+    if (c->n > 0) launch_kick_drift(c);
   });
 }
 
@@ -1788,6 +1835,7 @@ int tmd_gpu_slab_forces(tmd_gpu_ctx* c, int mode) {
     need_slab(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     launch_forces(c, mode == 2 ? kFused : (mode == 1 ? kKick2 : kForcesOnly));
+    if (mode == 0) launch_thermo_init(c);  // setup evaluation (step-0 noise)
   });
 }
 

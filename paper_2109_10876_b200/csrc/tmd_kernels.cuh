@@ -47,16 +47,22 @@ struct Integ {
   double4* pos_out;
   double dt, half_dt;
   double* part_ke;
+  Thermo th;  // Langevin bath (off: NVE)
 };
 
+// Closing half-kick (+ Langevin force, which then stays in the stored force
+// like the reference's st.fx += lf) and, for kFused, the next step's opening
+// half-kick + drift. gx..gz come in as the pair force and leave as the force
+// to store.
 template <int kMode>
-__device__ __forceinline__ void integrate_one(int i, const double4& pi, double gx, double gy,
-                                              double gz, const Integ& it, Ctrl* ctrl,
+__device__ __forceinline__ void integrate_one(int i, const double4& pi, double& gx, double& gy,
+                                              double& gz, const Integ& it, Ctrl* ctrl,
                                               double& ke, double& d2) {
   if (kMode == kForcesOnly) return;
   const double m = it.mass[i];
   const double inv_m = __ddiv_rn(1.0, m);
   double ux = it.vx[i], uy = it.vy[i], uz = it.vz[i];
+  if (it.th.on) langevin_add(it.th, ctrl->step, it.id[i], m, ux, uy, uz, gx, gy, gz);
   kick(ux, gx, inv_m, it.half_dt);
   kick(uy, gy, inv_m, it.half_dt);
   kick(uz, gz, inv_m, it.half_dt);
@@ -99,40 +105,22 @@ __device__ __forceinline__ void integrate_block(double ke, double d2, double* re
   }
 }
 
-// kick2 of the previous step (optional, fused) + kick1 + drift of this step.
-// With kFused the kernel also emits the kinetic-energy partials of the
-// post-kick2 velocities and performs the non-finite check of
-// thermostat_and_half_kick (engine.hpp:231-236).
-template <bool kFused>
+// Opening half-kick + drift of the first step of a run (later steps get it
+// from the fused force epilogue), with the displacement test.
 __global__ void __launch_bounds__(kBlock)
     k_kick_drift(int n, double4* __restrict__ pos, double* __restrict__ vx,
                  double* __restrict__ vy, double* __restrict__ vz,
                  const double* __restrict__ fx, const double* __restrict__ fy,
                  const double* __restrict__ fz, const double* __restrict__ mass,
-                 const long long* __restrict__ id,
-                 const double4* __restrict__ snap, double dt, double half_dt,
-                 double* __restrict__ part_ke, Ctrl* ctrl) {
-  __shared__ double red[kBlock / 32];
+                 const double4* __restrict__ snap, double dt, double half_dt, Ctrl* ctrl) {
   const int i = blockIdx.x * kBlock + threadIdx.x;
-  double d2 = 0.0, ke = 0.0;
+  double d2 = 0.0;
   if (i < n) {
     const double inv_m = __ddiv_rn(1.0, mass[i]);
     double ux = vx[i], uy = vy[i], uz = vz[i];
-    const double gx = fx[i], gy = fy[i], gz = fz[i];
-    if (kFused) {
-      kick(ux, gx, inv_m, half_dt);
-      kick(uy, gy, inv_m, half_dt);
-      kick(uz, gz, inv_m, half_dt);
-      if (!finite3(ux, uy, uz) || !finite3(gx, gy, gz)) {
-        record_error(ctrl, kStatNonFinite, id[i], -1);
-      }
-      ke = __dmul_rn(__dmul_rn(0.5, mass[i]),
-                     __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)),
-                               __dmul_rn(uz, uz)));
-    }
-    kick(ux, gx, inv_m, half_dt);
-    kick(uy, gy, inv_m, half_dt);
-    kick(uz, gz, inv_m, half_dt);
+    kick(ux, fx[i], inv_m, half_dt);
+    kick(uy, fy[i], inv_m, half_dt);
+    kick(uz, fz[i], inv_m, half_dt);
     double4 p = pos[i];
     p.x = __dadd_rn(p.x, __dmul_rn(ux, dt));
     p.y = __dadd_rn(p.y, __dmul_rn(uy, dt));
@@ -142,50 +130,29 @@ __global__ void __launch_bounds__(kBlock)
     vy[i] = uy;
     vz[i] = uz;
     const double4 s = snap[i];
-    d2 = exact_r2(__dsub_rn(p.x, s.x), __dsub_rn(p.y, s.y),
-                  __dsub_rn(p.z, s.z));
+    d2 = exact_r2(__dsub_rn(p.x, s.x), __dsub_rn(p.y, s.y), __dsub_rn(p.z, s.z));
   }
   // block max of d2 (non-negative doubles order like their bit patterns)
   for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
   if ((threadIdx.x & 31) == 0 && d2 > 0.0) {
     atomicMax(&ctrl->max_d2, static_cast<unsigned long long>(__double_as_longlong(d2)));
   }
-  if (kFused) {
-    const double t = block_sum<kBlock>(ke, red);
-    if (threadIdx.x == 0) part_ke[blockIdx.x] = t;
-  }
 }
 
-// Second half-kick + non-finite check + kinetic partials (end of a run).
-// Engine::thermostat_and_half_kick without a thermostat (engine.hpp:209-239).
+// Langevin force of the initial evaluation (compute_forces_untimed,
+// engine.hpp:244-278: noise keyed as step 0, velocities as given).
 __global__ void __launch_bounds__(kBlock)
-    k_kick2(int n, double* __restrict__ vx, double* __restrict__ vy,
-            double* __restrict__ vz, const double* __restrict__ fx,
-            const double* __restrict__ fy, const double* __restrict__ fz,
-            const double* __restrict__ mass, const long long* __restrict__ id,
-            double half_dt, double* __restrict__ part_ke, Ctrl* ctrl) {
-  __shared__ double red[kBlock / 32];
+    k_thermo_init(int n, const double* __restrict__ vx, const double* __restrict__ vy,
+                  const double* __restrict__ vz, const double* __restrict__ mass,
+                  const long long* __restrict__ id, Thermo th, double* __restrict__ fx,
+                  double* __restrict__ fy, double* __restrict__ fz) {
   const int i = blockIdx.x * kBlock + threadIdx.x;
-  double ke = 0.0;
-  if (i < n) {
-    const double inv_m = __ddiv_rn(1.0, mass[i]);
-    double ux = vx[i], uy = vy[i], uz = vz[i];
-    const double gx = fx[i], gy = fy[i], gz = fz[i];
-    kick(ux, gx, inv_m, half_dt);
-    kick(uy, gy, inv_m, half_dt);
-    kick(uz, gz, inv_m, half_dt);
-    if (!finite3(ux, uy, uz) || !finite3(gx, gy, gz)) {
-      record_error(ctrl, kStatNonFinite, id[i], -1);
-    }
-    vx[i] = ux;
-    vy[i] = uy;
-    vz[i] = uz;
-    ke = __dmul_rn(__dmul_rn(0.5, mass[i]),
-                   __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)),
-                             __dmul_rn(uz, uz)));
-  }
-  const double t = block_sum<kBlock>(ke, red);
-  if (threadIdx.x == 0) part_ke[blockIdx.x] = t;
+  if (i >= n) return;
+  double gx = fx[i], gy = fy[i], gz = fz[i];
+  langevin_add(th, 0, id[i], mass[i], vx[i], vy[i], vz[i], gx, gy, gz);
+  fx[i] = gx;
+  fy[i] = gy;
+  fz[i] = gz;
 }
 
 // Kinetic partials of the current velocities (observe() after setup).
@@ -211,14 +178,17 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
                          int log_idx, cudaGraphConditionalHandle cond) {
   const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
-  const int r = (ctrl->force_rebuild != 0) || (m > thr);
+  // force_rebuild: 1 = host-forced (setup), 2 = forced after a rollback and
+  // not counted (the reference would not have rebuilt here)
+  const int force = ctrl->force_rebuild;
+  const int r = (force != 0) || (m > thr);
   ctrl->rebuild = r;
   if (cond != 0) cudaGraphSetConditional(cond, r ? 1u : 0u);  // graph mode: gate the IF node
   if (log) log[log_idx] = r;
   ctrl->force_rebuild = 0;
   ctrl->max_d2 = 0ull;
   if (advance_step) ctrl->step += 1;
-  if (r && advance_step) ctrl->rebuilds += 1;
+  if (advance_step && (force == 1 || m > thr)) ctrl->rebuilds += 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -562,10 +532,10 @@ __global__ void __launch_bounds__(kBlock)
         az += ff * dz;
       }
     }
+    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
     fx[i] = ax;
     fy[i] = ay;
     fz[i] = az;
-    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
   }
   const double te = block_sum<kBlock>(e, red);
   const double tw = block_sum<kBlock>(w, red);

@@ -47,7 +47,7 @@ import numpy as np
 
 from . import _abi
 from .engine import (ConfigError, EngineConfig, FlatConfig, Interactions, StepObservables,
-                     _check, _ptr, validate_engine_config)
+                     _check, _engine_params, _ptr, validate_engine_config)
 
 # message tags (both ends of a transfer agree on them; NCCL matches by order)
 TAG_MIGRATE = 100
@@ -112,12 +112,9 @@ class SlabContext:
         sys.vel = _ptr(flat.vel)
         lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
                               1 if inter.lj.energy_shifted else 0)
-        p = _abi.TmdEngineParams()
-        p.dt = cfg.dt
-        p.r_skin = r_skin
-        p.device = device
+        p = _engine_params(cfg, r_skin, device)
         p.section_timers = 0
-        p.nbr_capacity = cfg.nbr_capacity
+        p.reserved[0] = 0
         h = C.c_void_p()
         _check(L.tmd_gpu_create_slab(C.byref(sys), C.byref(lj), None, C.byref(p),
                                      int(rank), int(nranks), C.byref(h)), None)

@@ -190,8 +190,31 @@ def validate_engine_config(c: EngineConfig) -> None:
     if c.observable_stride < 1:
         raise ConfigError("observable stride must be at least 1")
     if c.thermostat is not None:
-        raise ConfigError("the Langevin thermostat is not on the GPU path yet "
-                          "(SURVEY §8f row f4)")
+        validate_langevin(c.thermostat)
+
+
+def validate_langevin(p: LangevinParams) -> None:
+    """validate_langevin (potentials.hpp:180-189)."""
+    if not (p.gamma >= 0.0) or not np.isfinite(p.gamma):
+        raise ConfigError("langevin gamma must be finite and >= 0")
+    if not (p.temperature >= 0.0) or not np.isfinite(p.temperature):
+        raise ConfigError("langevin temperature must be finite and >= 0")
+
+
+def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEngineParams":
+    p = _abi.TmdEngineParams()
+    p.dt = cfg.dt
+    p.r_skin = r_skin
+    p.device = device
+    p.section_timers = 1 if cfg.section_timers else 0
+    p.nbr_capacity = cfg.nbr_capacity
+    p.reserved[0] = int(cfg.variant)
+    if cfg.thermostat is not None:
+        p.thermostat = 1
+        p.gamma = float(cfg.thermostat.gamma)
+        p.temperature = float(cfg.thermostat.temperature)
+        p.seed = int(cfg.thermostat.seed) & 0xFFFFFFFFFFFFFFFF
+    return p
 
 
 class Engine:
@@ -223,13 +246,7 @@ class Engine:
         sys.vel = _ptr(flat.vel)
         lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
                               1 if inter.lj.energy_shifted else 0)
-        p = _abi.TmdEngineParams()
-        p.dt = cfg.dt
-        p.r_skin = r_skin
-        p.device = cfg.device
-        p.section_timers = 1 if cfg.section_timers else 0
-        p.nbr_capacity = cfg.nbr_capacity
-        p.reserved[0] = int(cfg.variant)
+        p = _engine_params(cfg, r_skin, cfg.device)
         h = C.c_void_p()
         rc = L.tmd_gpu_create(C.byref(sys), C.byref(lj), None, C.byref(p), C.byref(h))
         _check(rc, None)

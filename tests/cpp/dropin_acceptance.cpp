@@ -103,6 +103,35 @@ int main() {
     verdict("criterion 2 (one step vs reference)", ids && worst <= 1e-10,
             "max position spread " + std::to_string(worst));
   }
+  // thermostat: the same EngineConfig (with a Langevin bath) through both
+  // engines, 30 steps (test_engine.cpp:214-240's system and bath)
+  {
+    const FlatConfig flat = gen_lattice(4096, 0.8442, 0.0, 29);
+    EngineConfig cfg;
+    cfg.dt = 0.005;
+    cfg.n_sub = 8;
+    LangevinParams bath;
+    bath.gamma = 1.0;
+    bath.temperature = 0.8;
+    bath.seed = 99;
+    cfg.thermostat = bath;
+    Engine ref(build_domain(flat, lj_only(), 0.3, 8), cfg);
+    ref.run(30);
+    const FlatConfig a = flatten_domain(ref.domain());
+    taskmd_gpu::Engine g(flat, lj_only(), 0.3, cfg);
+    g.run(30);
+    const FlatConfig b = g.flatten();
+    double worst = 0.0;
+    bool ids = a.id == b.id;
+    for (std::size_t k = 0; ids && k < a.size(); ++k) {
+      worst = std::max({worst, std::abs(a.pos[k].x - b.pos[k].x),
+                        std::abs(a.pos[k].y - b.pos[k].y), std::abs(a.pos[k].z - b.pos[k].z),
+                        std::abs(a.vel[k].x - b.vel[k].x), std::abs(a.vel[k].y - b.vel[k].y),
+                        std::abs(a.vel[k].z - b.vel[k].z)});
+    }
+    verdict("Langevin bath, 30 steps vs reference", ids && worst <= 1e-9,
+            "max state spread " + std::to_string(worst));
+  }
   // criterion 3: NVE drift, N=4000 SC lattice, seed 3, T=0.6
   {
     const FlatConfig flat = gen_lattice(4000, 0.8442, 0.6, 3);

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
     assert sorted(_abi.EXPORTS) == names
-    assert L.tmd_gpu_abi_version() == 1
+    assert L.tmd_gpu_abi_version() == 2
 
 
 def test_library_is_sm100a_only():
@@ -84,7 +84,9 @@ def _flat(n=8, box=10.0):
     (lambda f, i, c: setattr(f, "id", np.array([0, 1, 2, 3, 4, 5, 6, 6])), "duplicate particle id"),
     (lambda f, i, c: setattr(f, "mass", np.array([1, 1, 1, 0.0, 1, 1, 1, 1])), "non-positive mass"),
     (lambda f, i, c: setattr(c, "dt", 0.0), "time step"),
-    (lambda f, i, c: setattr(c, "thermostat", E.LangevinParams()), "thermostat"),
+    (lambda f, i, c: setattr(c, "thermostat", E.LangevinParams(gamma=-1.0)), "gamma"),
+    (lambda f, i, c: setattr(c, "thermostat", E.LangevinParams(temperature=float("inf"))),
+     "temperature"),
     (lambda f, i, c: setattr(i, "fene", E.FeneParams()), "FENE"),
     (lambda f, i, c: setattr(i, "angle", E.AngleParams()), "angle"),
 ])
@@ -135,3 +137,35 @@ def test_error_string_is_exposed_through_the_abi():
     assert rc == _abi.TMD_ERR_CONFIG
     assert not h.value
     assert b"smaller than one cell" in L.tmd_gpu_last_error(None)
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors have the C structs' sizes and field offsets."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {
+        "tmd_system": _abi.TmdSystem, "tmd_lj_params": _abi.TmdLjParams,
+        "tmd_engine_params": _abi.TmdEngineParams, "tmd_observables": _abi.TmdObservables,
+        "tmd_list_stats": _abi.TmdListStats,
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"',
+             'int main(void) {']
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ['  return 0;', '}']
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, str(src), "-o", str(exe)], check=True)
+    got = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    import ctypes
+    for line in got.splitlines():
+        cname, field, val = line.split()
+        cls = structs[cname]
+        want = ctypes.sizeof(cls) if field == "size" else getattr(cls, field).offset
+        assert int(val) == want, (cname, field, int(val), want)

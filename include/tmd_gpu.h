@@ -233,6 +233,17 @@ int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
  * lower ghosts, upper ghosts, cells per layer, slot capacity, record bytes. */
 int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[10]);
 
+/* Load-aware cuts: owned particles per global z layer
+ * (counts[dims_z], wrapped positions) — the caller sums them over ranks and
+ * picks cut planes; tmd_gpu_slab_recut then moves this slab to layers
+ * [cuts[rank], cuts[rank+1]) (cuts[0] = 0, cuts[nranks] = dims_z, every slab
+ * >= 1 layer; all ranks pass the same cuts, right before slab_migrate_out).
+ * Replaces the reference's static range rule (decomp.hpp:87-93) for
+ * inhomogeneous systems, the role autotune_subnodes + work stealing play on
+ * the CPU (engine.hpp:293-373, task_pool.hpp:85-106). */
+int tmd_gpu_slab_layer_counts(tmd_gpu_ctx* ctx, int64_t* counts);
+int tmd_gpu_slab_recut(tmd_gpu_ctx* ctx, const int32_t* cuts);
+
 /* Largest squared displacement since the last build over the owned particles
  * (needs_rebuild's per-subnode max, neighbor_list.hpp:114-145). Raises any
  * pending physics error. */

@@ -33,7 +33,8 @@ EXPORTS = [
     "tmd_gpu_slab_decide", "tmd_gpu_slab_migrate_out", "tmd_gpu_slab_migrate_in",
     "tmd_gpu_slab_commit", "tmd_gpu_slab_border", "tmd_gpu_slab_ghost_in",
     "tmd_gpu_slab_ghosts_ready", "tmd_gpu_slab_kick_drift", "tmd_gpu_slab_forces",
-    "tmd_gpu_slab_halo", "tmd_gpu_slab_sums",
+    "tmd_gpu_slab_halo", "tmd_gpu_slab_sums", "tmd_gpu_slab_layer_counts",
+    "tmd_gpu_slab_recut",
 ]
 
 
@@ -113,6 +114,8 @@ def lib() -> C.CDLL:
     L.tmd_gpu_slab_forces.argtypes = [P, C.c_int]
     L.tmd_gpu_slab_halo.argtypes = [P, PP, PP]
     L.tmd_gpu_slab_sums.argtypes = [P, P]
+    L.tmd_gpu_slab_layer_counts.argtypes = [P, P]
+    L.tmd_gpu_slab_recut.argtypes = [P, P]
     L.tmd_gpu_last_error.argtypes = [P]
     L.tmd_gpu_last_error.restype = C.c_char_p
     L.tmd_gpu_compute_forces.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]

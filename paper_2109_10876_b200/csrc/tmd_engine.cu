@@ -21,6 +21,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -126,7 +127,8 @@ struct tmd_gpu_ctx {
   int* scan_tmp = nullptr;               // tile sums of the tiled scan
 
   // z-slab decomposition (one context per GPU of a multi-GPU job)
-  int64_t n_cap = 0;        // particle capacity (the whole system in slab mode)
+  int64_t n_cap = 0;        // slot capacity (owned + ghosts in slab mode)
+  int64_t n_total = 0;      // particles in the whole system
   int my_rank = 0, nranks = 1;
   int64_t n_ghost = 0, n_ghost_lo = 0, n_ghost_hi = 0;
   int* owner_of_z = nullptr;     // global z layer -> owning rank
@@ -334,19 +336,36 @@ size_t force_smem(const tmd_gpu_ctx* c) {
   return static_cast<size_t>(c->bg.stage_cap + 4) * 3 * sizeof(double);
 }
 
+// Max dynamic shared memory is a per-kernel, per-device attribute shared by
+// every context of the process, while the staging capacity is per context:
+// raise it to the largest any context on the device has needed, never lower
+// it under another context.
+constexpr int kMaxDevices = 64;
+size_t g_build_smem_set[kMaxDevices] = {}, g_force_smem_set[kMaxDevices] = {};
+
 void set_smem_attrs(tmd_gpu_ctx* c) {
   c->graph_dirty = true;
-  ck(cudaFuncSetAttribute(k_build_brick3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(build_smem(c))), "smem attr build");
-  ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(build_smem(c))), "smem attr build");
-  ck(cudaFuncSetAttribute(k_forces_brick<kForcesOnly>,
-                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(force_smem(c))), "smem attr forces");
-  ck(cudaFuncSetAttribute(k_forces_brick<kKick2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(force_smem(c))), "smem attr forces");
-  ck(cudaFuncSetAttribute(k_forces_brick<kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(force_smem(c))), "smem attr forces");
+  const size_t b = build_smem(c), f = force_smem(c);
+  const int d = std::min(std::max(c->device, 0), kMaxDevices - 1);
+  size_t& g_build = g_build_smem_set[d];
+  size_t& g_force = g_force_smem_set[d];
+  if (b > g_build) {
+    ck(cudaFuncSetAttribute(k_build_brick3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(b)), "smem attr build");
+    ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(b)), "smem attr build");
+    g_build = b;
+  }
+  if (f > g_force) {
+    ck(cudaFuncSetAttribute(k_forces_brick<kForcesOnly>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f)),
+       "smem attr forces");
+    ck(cudaFuncSetAttribute(k_forces_brick<kKick2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(f)), "smem attr forces");
+    ck(cudaFuncSetAttribute(k_forces_brick<kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(f)), "smem attr forces");
+    g_force = f;
+  }
 }
 
 void launch_build(tmd_gpu_ctx* c) {
@@ -634,10 +653,41 @@ constexpr int kGraphSteps = 15;  // odd: the ping-pong parity is unchanged per g
 // Splitting a run into such blocks is bitwise identical to the eager
 // sequence: the closing and opening half-kicks are the same two roundings
 // whether they run in one fused epilogue or in two kernels.
+void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g, tmd_gpu_ctx::StepGraph& out);
+
 void capture_graph(tmd_gpu_ctx* c, int nsteps, tmd_gpu_ctx::StepGraph& out) {
-  const int p = c->cur;
   cudaGraph_t g = nullptr;
   ck(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+  const int p = c->cur;
+  const uint64_t l0 = c->launches;
+  try {
+    capture_graph_body(c, nsteps, g, out);
+  } catch (...) {
+    // leave no stream in capture mode and no half-built graph behind
+    cudaStreamCaptureStatus st;
+    cudaGraph_t junk = nullptr;
+    if (cudaStreamIsCapturing(c->side, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(c->side, &junk);
+    }
+    if (cudaStreamIsCapturing(c->stream, &st) == cudaSuccess &&
+        st != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(c->stream, &junk);
+    }
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    out = tmd_gpu_ctx::StepGraph{};
+    c->ls = c->stream;
+    c->cond_handle = 0;
+    c->cur = p;
+    c->pos = c->posb[p];
+    c->launches = l0;
+    throw;
+  }
+}
+
+void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
+                        tmd_gpu_ctx::StepGraph& out) {
+  const int p = c->cur;
   const uint64_t l0 = c->launches;
   ck(cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal),
@@ -682,7 +732,9 @@ void capture_graph(tmd_gpu_ctx* c, int nsteps, tmd_gpu_ctx::StepGraph& out) {
   }
   launch_reduce_pe(c);
   ck(cudaStreamEndCapture(c->stream, &g), "end capture");
-  ck(cudaGraphInstantiate(&out.exec, g, 0), "cudaGraphInstantiate");
+  cudaGraphExec_t exec = nullptr;
+  ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");
+  out.exec = exec;
   out.graph = g;
   c->graph_body_kernels = body;
   out.fixed = (c->launches - l0) - static_cast<uint64_t>(nsteps) * body;
@@ -975,22 +1027,10 @@ void build_geom(tmd_gpu_ctx* c, const double box[3], double r_cut,
   c->g.owned_cells = c->g.ncells;
 }
 
-// Slab `rank` of `nranks` along z: owned global layers [z0, z1) with the
-// reference's range rule i*dims/s (decomp.hpp:87-93), plus one ghost layer on
-// each side.
-void make_slab(tmd_gpu_ctx* c, int rank, int nranks) {
+// The slab's local grid for owned global z layers [z0, z1): local layer
+// lz = global - z0 + 1, ghost layers 0 and zown + 1.
+void set_slab_range(tmd_gpu_ctx* c, int z0, int z1) {
   const int dz = c->g.dims[2];
-  if (nranks > dz) {
-    throw StatusError{TMD_ERR_CONFIG, "more ranks (" + std::to_string(nranks) +
-                                          ") than z cell layers (" + std::to_string(dz) + ")"};
-  }
-  if (dz < 3) {
-    throw StatusError{TMD_ERR_CONFIG,
-                      "slab decomposition needs at least 3 z cell layers, the box has " +
-                          std::to_string(dz)};
-  }
-  const int z0 = static_cast<int>(static_cast<int64_t>(rank) * dz / nranks);
-  const int z1 = static_cast<int>(static_cast<int64_t>(rank + 1) * dz / nranks);
   const int dxy = c->g.dims[0] * c->g.dims[1];
   c->g.zslab = 1;
   c->g.z0 = z0;
@@ -1002,19 +1042,49 @@ void make_slab(tmd_gpu_ctx* c, int rank, int nranks) {
   c->g.owned_cells = dxy * c->g.zown;
 }
 
-// Device buffers of the slab exchange (capacity = the whole system).
-void alloc_slab(tmd_gpu_ctx* c) {
-  const size_t n = static_cast<size_t>(c->n_cap);
+// Cut planes of the reference's range rule i*dims/s (decomp.hpp:87-93).
+std::vector<int> default_cuts(int dz, int nranks) {
+  std::vector<int> cuts(static_cast<size_t>(nranks) + 1);
+  for (int r = 0; r <= nranks; ++r) {
+    cuts[static_cast<size_t>(r)] = static_cast<int>(static_cast<int64_t>(r) * dz / nranks);
+  }
+  return cuts;
+}
+
+// Slab `rank` of `nranks` along z with the default cuts, plus one ghost
+// layer on each side.
+void make_slab(tmd_gpu_ctx* c, int rank, int nranks) {
+  const int dz = c->g.dims[2];
+  if (nranks > dz) {
+    throw StatusError{TMD_ERR_CONFIG, "more ranks (" + std::to_string(nranks) +
+                                          ") than z cell layers (" + std::to_string(dz) + ")"};
+  }
+  if (dz < 3) {
+    throw StatusError{TMD_ERR_CONFIG,
+                      "slab decomposition needs at least 3 z cell layers, the box has " +
+                          std::to_string(dz)};
+  }
+  const std::vector<int> cuts = default_cuts(dz, nranks);
+  set_slab_range(c, cuts[static_cast<size_t>(rank)], cuts[static_cast<size_t>(rank) + 1]);
+}
+
+void upload_owner_table(tmd_gpu_ctx* c, const std::vector<int>& cuts) {
   const int dz = c->g.dims[2];
   std::vector<int> owner(static_cast<size_t>(dz));
   for (int r = 0; r < c->nranks; ++r) {
-    const int z0 = static_cast<int>(static_cast<int64_t>(r) * dz / c->nranks);
-    const int z1 = static_cast<int>(static_cast<int64_t>(r + 1) * dz / c->nranks);
-    for (int z = z0; z < z1; ++z) owner[static_cast<size_t>(z)] = r;
+    for (int z = cuts[static_cast<size_t>(r)]; z < cuts[static_cast<size_t>(r) + 1]; ++z) {
+      owner[static_cast<size_t>(z)] = r;
+    }
   }
-  c->owner_of_z = dalloc<int>(owner.size());
   ck(cudaMemcpy(c->owner_of_z, owner.data(), owner.size() * sizeof(int),
                 cudaMemcpyHostToDevice), "H2D owner table");
+}
+
+// Device buffers of the slab exchange.
+void alloc_slab(tmd_gpu_ctx* c) {
+  const size_t n = static_cast<size_t>(c->n_cap);
+  c->owner_of_z = dalloc<int>(static_cast<size_t>(c->g.dims[2]));
+  upload_owner_table(c, default_cuts(c->g.dims[2], c->nranks));
   c->mig_dest = dalloc<int>(n);
   c->mig_count = dalloc<int>(2 * static_cast<size_t>(c->nranks));
   c->mig_off = dalloc<int>(static_cast<size_t>(c->nranks) + 1);
@@ -1030,6 +1100,95 @@ void alloc_slab(tmd_gpu_ctx* c) {
     c->boff[s] = dalloc<int>(dxy + 1);
     c->gcnt[s] = dalloc<int>(dxy);
   }
+}
+
+// Grows every per-slot array to hold `need` slots (slab mode: a slab's share
+// changes with migration and re-cutting). Contents are preserved; the far
+// sentinel moves to the new last slot.
+void grow_capacity(tmd_gpu_ctx* c, int64_t need) {
+  if (need <= c->n_cap) return;
+  int64_t cap = std::max<int64_t>(need + need / 4 + 4096, c->n_cap * 3 / 2);
+  cap = std::min<int64_t>(cap, kMaxSlots);
+  if (need > cap) {
+    throw StatusError{TMD_ERR_CONFIG, "slab too large for one GPU context: " +
+                                          std::to_string(need) + " slots"};
+  }
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  const size_t o = static_cast<size_t>(c->n_cap), nn = static_cast<size_t>(cap);
+  auto regrow = [&](auto*& p, size_t extra) {
+    using T = std::remove_reference_t<decltype(*p)>;
+    if (!p) return;
+    T* q = dalloc<T>(nn + extra);
+    ck(cudaMemcpy(q, p, o * sizeof(T), cudaMemcpyDeviceToDevice), "regrow copy");
+    cudaFree(p);
+    p = q;
+  };
+  for (int b = 0; b < 2; ++b) regrow(c->posb[b], 1);
+  c->pos = c->posb[c->cur];
+  regrow(c->pos2, 0); regrow(c->snap, 0);
+  regrow(c->vx, 0); regrow(c->vy, 0); regrow(c->vz, 0);
+  regrow(c->vx2, 0); regrow(c->vy2, 0); regrow(c->vz2, 0);
+  regrow(c->fx, 0); regrow(c->fy, 0); regrow(c->fz, 0);
+  regrow(c->mass, 0); regrow(c->mass2, 0); regrow(c->id, 0); regrow(c->id2, 0);
+  regrow(c->cell, 0); regrow(c->cell2, 0); regrow(c->rank, 0); regrow(c->perm, 0);
+  regrow(c->nnbr, 0);
+  regrow(c->ck_pos, 0); regrow(c->ck_vx, 0); regrow(c->ck_vy, 0); regrow(c->ck_vz, 0);
+  regrow(c->ck_mass, 0); regrow(c->ck_id, 0);
+  regrow(c->ck_fx, 0); regrow(c->ck_fy, 0); regrow(c->ck_fz, 0);
+  regrow(c->mig_dest, 0); regrow(c->mig_send, 0); regrow(c->mig_recv, 0);
+  for (int s = 0; s < 2; ++s) {
+    regrow(c->bidx[s], 0);
+    regrow(c->bids[s], 0);
+    regrow(c->bpos[s], 0);
+  }
+  const double4 far = make_double4(kFarD, kFarD, kFarD, 0.0);
+  for (int b = 0; b < 2; ++b) {
+    ck(cudaMemcpy(c->posb[b] + nn, &far, sizeof(double4), cudaMemcpyHostToDevice),
+       "H2D sentinel");
+  }
+  const int parts = std::max(blocks_for(cap, kBlock), c->bg.nbricks);
+  if (parts > c->nparts) {
+    cudaFree(c->part_e); cudaFree(c->part_w); cudaFree(c->part_ke);
+    c->nparts = parts;
+    c->part_e = dalloc<double>(parts);
+    c->part_w = dalloc<double>(parts);
+    c->part_ke = dalloc<double>(parts);
+  }
+  c->n_cap = cap;
+  c->stride = static_cast<int>((cap + 31) / 32 * 32);
+  c->graph_dirty = true;
+}
+
+// Moves this slab to owned layers [cuts[rank], cuts[rank+1]) (all ranks pass
+// the same cuts, before the next migrate_out): new owner table, local grid,
+// brick tables and cell-range arrays.
+void recut(tmd_gpu_ctx* c, const std::vector<int>& cuts) {
+  const int z0 = cuts[static_cast<size_t>(c->my_rank)];
+  const int z1 = cuts[static_cast<size_t>(c->my_rank) + 1];
+  upload_owner_table(c, cuts);
+  if (z0 == c->g.z0 && z1 - z0 == c->g.zown) return;
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  set_slab_range(c, z0, z1);
+  void* old[] = {c->cell_rank, c->brick_rank_off, c->ngroups, c->group_off, c->scan_tmp,
+                 c->count, c->start};
+  for (void* p : old) {
+    if (p) cudaFree(p);
+  }
+  setup_bricks(c, static_cast<double>(c->n_total), c->r_cut + c->r_skin);
+  const int64_t want = c->n + c->n / 4 + 1024;
+  c->ngroups_max = static_cast<int>(want / 32) + c->bg.nbricks + 1;
+  upload_bricks(c);
+  c->count = dalloc<int>(static_cast<size_t>(c->g.ncells));
+  c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
+  ck(cudaMemset(c->count, 0, sizeof(int) * static_cast<size_t>(c->g.ncells)), "memset count");
+  if (c->bg.nbricks > c->nparts) {
+    cudaFree(c->part_e); cudaFree(c->part_w); cudaFree(c->part_ke);
+    c->nparts = c->bg.nbricks;
+    c->part_e = dalloc<double>(c->nparts);
+    c->part_w = dalloc<double>(c->nparts);
+    c->part_ke = dalloc<double>(c->nparts);
+  }
+  alloc_list(c, c->cap);  // group count changed
 }
 
 int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_params* fene,
@@ -1081,6 +1240,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // slot capacity: the whole system, or in slab mode room for the owned
     // particles to double plus both ghost layers (checked at every exchange)
     c->n_cap = sys->n;
+    c->n_total = sys->n;
     if (nranks > 1) {
       c->n_cap = std::min<int64_t>(2 * sys->n, 2 * static_cast<int64_t>(sel.size()) + 65536);
       if (c->n_cap > kMaxSlots) {
@@ -1205,7 +1365,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     int cap0 = params->nbr_capacity;
     if (c->auto_cap) {
       const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
-      const double rho = static_cast<double>(c->n_cap) / vol;
+      const double rho = static_cast<double>(c->n_total) / vol;
       const double rverlet = lj->r_cut + params->r_skin;
       const double expect = rho * 4.18879020478639 * rverlet * rverlet * rverlet;
       cap0 = static_cast<int>(expect * 1.5) + 16;
@@ -1626,6 +1786,54 @@ int tmd_gpu_slab_info(tmd_gpu_ctx* c, int64_t info[10]) {
   });
 }
 
+int tmd_gpu_slab_layer_counts(tmd_gpu_ctx* c, int64_t* counts) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const int dz = c->g.dims[2];
+    if (static_cast<size_t>(dz) * sizeof(unsigned int) > 96 * 1024) {
+      throw StatusError{TMD_ERR_CONFIG, "too many z layers for the layer histogram"};
+    }
+    unsigned long long* d = dalloc<unsigned long long>(static_cast<size_t>(dz));
+    ck(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * dz, c->stream), "memset");
+    if (c->n > 0) {
+      c->launches += 1;
+      const int blocks = std::min(c->nblk, 148 * 8);
+      const size_t smem = static_cast<size_t>(dz) * sizeof(unsigned int);
+      if (smem > 48 * 1024) {
+        ck(cudaFuncSetAttribute(k_layer_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)), "smem attr hist");
+      }
+      k_layer_hist<<<blocks, kBlock, smem, c->ls>>>(static_cast<int>(c->n), c->pos, c->g, d);
+    }
+    std::vector<unsigned long long> h(static_cast<size_t>(dz));
+    ck(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * dz, cudaMemcpyDeviceToHost,
+                       c->stream), "D2H hist");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "k_layer_hist");
+    cudaFree(d);
+    for (int z = 0; z < dz; ++z) counts[z] = static_cast<int64_t>(h[static_cast<size_t>(z)]);
+  });
+}
+
+int tmd_gpu_slab_recut(tmd_gpu_ctx* c, const int32_t* cuts) {
+  return guard(c, [&] {
+    need_slab(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const int R = c->nranks, dz = c->g.dims[2];
+    std::vector<int> v(cuts, cuts + R + 1);
+    if (v[0] != 0 || v[static_cast<size_t>(R)] != dz) {
+      throw StatusError{TMD_ERR_CONFIG, "cut planes must start at 0 and end at dims_z"};
+    }
+    for (int r = 0; r < R; ++r) {
+      if (v[static_cast<size_t>(r) + 1] <= v[static_cast<size_t>(r)]) {
+        throw StatusError{TMD_ERR_CONFIG, "every slab needs at least one z layer"};
+      }
+    }
+    recut(c, v);
+  });
+}
+
 int tmd_gpu_slab_max_d2(tmd_gpu_ctx* c, double* local_max_d2) {
   return guard(c, [&] {
     need_slab(c);
@@ -1705,11 +1913,8 @@ int tmd_gpu_slab_migrate_out(tmd_gpu_ctx* c, int64_t* counts, void** send) {
 int tmd_gpu_slab_migrate_in(tmd_gpu_ctx* c, int64_t nrecv, void** recv) {
   return guard(c, [&] {
     need_slab(c);
-    if (nrecv < 0 || c->n + nrecv > c->n_cap) {
-      throw StatusError{TMD_ERR_CONFIG,
-                        "slab capacity exceeded: " + std::to_string(c->n + nrecv) +
-                            " particles > " + std::to_string(c->n_cap)};
-    }
+    if (nrecv < 0) throw StatusError{TMD_ERR_CONFIG, "negative record count"};
+    grow_capacity(c, c->n + nrecv);
     c->mig_nrecv = nrecv;
     *recv = c->mig_recv;
   });
@@ -1771,11 +1976,8 @@ int tmd_gpu_slab_ghost_in(tmd_gpu_ctx* c, int64_t n_lo, int64_t n_hi, void* lo[3
                           void* hi[3]) {
   return guard(c, [&] {
     need_slab(c);
-    if (n_lo < 0 || n_hi < 0 || c->n + n_lo + n_hi > c->n_cap) {
-      throw StatusError{TMD_ERR_CONFIG, "slab capacity exceeded by the ghost layers: " +
-                                            std::to_string(c->n + n_lo + n_hi) + " slots > " +
-                                            std::to_string(c->n_cap)};
-    }
+    if (n_lo < 0 || n_hi < 0) throw StatusError{TMD_ERR_CONFIG, "negative ghost count"};
+    grow_capacity(c, c->n + n_lo + n_hi);
     c->n_ghost_lo = n_lo;
     c->n_ghost_hi = n_hi;
     c->n_ghost = n_lo + n_hi;

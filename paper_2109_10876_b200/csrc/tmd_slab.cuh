@@ -153,6 +153,26 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 1023) start[g.owned_cells + m] = n_own + total;
 }
 
+// Particles per global z layer (wrapped positions), for load-aware cut
+// planes. Block-private shared-memory histogram, then one global add per
+// layer per block.
+__global__ void __launch_bounds__(kBlock)
+    k_layer_hist(int n, const double4* __restrict__ pos, Geom g,
+                 unsigned long long* __restrict__ hist) {
+  extern __shared__ unsigned int s_hist[];
+  const int dz = g.dims[2];
+  for (int z = threadIdx.x; z < dz; z += kBlock) s_hist[z] = 0u;
+  __syncthreads();
+  for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
+    const double z = wrap1(pos[i].z, g.L[2]);
+    atomicAdd(&s_hist[cell_coord(z, g.cell_len[2], dz)], 1u);
+  }
+  __syncthreads();
+  for (int z = threadIdx.x; z < dz; z += kBlock) {
+    if (s_hist[z]) atomicAdd(&hist[z], static_cast<unsigned long long>(s_hist[z]));
+  }
+}
+
 // Per-step halo packing: current positions of one boundary layer.
 __global__ void __launch_bounds__(kBlock)
     k_pack_border(int nb, const int* __restrict__ idx, const double4* __restrict__ pos,

@@ -62,12 +62,47 @@ def slab_range(rank: int, nranks: int, dims_z: int) -> Tuple[int, int]:
     return rank * dims_z // nranks, (rank + 1) * dims_z // nranks
 
 
-def owner_of_layer(z: int, nranks: int, dims_z: int) -> int:
-    for r in range(nranks):
-        z0, z1 = slab_range(r, nranks, dims_z)
-        if z0 <= z < z1:
-            return r
-    raise ValueError(f"layer {z} outside 0..{dims_z - 1}")
+def default_cuts(nranks: int, dims_z: int) -> List[int]:
+    return [r * dims_z // nranks for r in range(nranks + 1)]
+
+
+def max_load(counts: Sequence[int], cuts: Sequence[int]) -> int:
+    return max(int(sum(counts[cuts[r]:cuts[r + 1]])) for r in range(len(cuts) - 1))
+
+
+def balanced_cuts(counts: Sequence[int], nranks: int) -> List[int]:
+    """Cut planes over the z layers minimising the largest slab population,
+    every slab >= 1 layer: binary search on the bound with a greedy fill, then
+    the widest slabs are halved until there are `nranks` (halving never raises
+    the maximum). Deterministic, so every rank computes the same cuts."""
+    c = [int(x) for x in counts]
+    dz = len(c)
+    if nranks > dz:
+        raise ConfigError(f"more ranks ({nranks}) than z cell layers ({dz})")
+
+    def greedy(bound: int) -> List[int]:
+        starts, acc = [0], 0
+        for z in range(dz):
+            if z > starts[-1] and acc + c[z] > bound:
+                starts.append(z)
+                acc = 0
+            acc += c[z]
+        return starts
+
+    lo, hi = max(c), max(sum(c), max(c))
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if len(greedy(mid)) <= nranks:
+            hi = mid
+        else:
+            lo = mid + 1
+    starts = greedy(lo)
+    while len(starts) < nranks:
+        ends = starts[1:] + [dz]
+        widths = [e - b for b, e in zip(starts, ends)]
+        i = widths.index(max(widths))
+        starts.insert(i + 1, starts[i] + widths[i] // 2)
+    return starts + [dz]
 
 
 # ---------------------------------------------------------------------------
@@ -212,6 +247,15 @@ class SlabContext:
         out = np.zeros(3)
         self._c(_abi.lib().tmd_gpu_slab_sums(self._h, _ptr(out)))
         return out
+
+    def layer_counts(self, dims_z: int) -> np.ndarray:
+        out = np.zeros(dims_z, np.int64)
+        self._c(_abi.lib().tmd_gpu_slab_layer_counts(self._h, _ptr(out)))
+        return out
+
+    def recut(self, cuts: Sequence[int]) -> None:
+        a = np.ascontiguousarray(cuts, dtype=np.int32)
+        self._c(_abi.lib().tmd_gpu_slab_recut(self._h, _ptr(a)))
 
     def sync(self) -> None:
         import torch
@@ -410,7 +454,8 @@ class DecomposedEngine:
 
     def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
                  cfg: Optional[EngineConfig] = None, comm: Optional[Comm] = None,
-                 device_of=None, ctx_factory=None):
+                 device_of=None, ctx_factory=None, balance: str = "static",
+                 rebalance_tolerance: float = 1.05):
         cfg = cfg or EngineConfig()
         validate_engine_config(cfg)
         if comm is None:
@@ -429,6 +474,14 @@ class DecomposedEngine:
         if ctx_factory is None:
             def ctx_factory(r):
                 return SlabContext(flat, inter, r_skin, cfg, r, R, device_of(r))
+        if balance not in ("static", "count"):
+            raise ConfigError(f"unknown balance mode {balance!r} (static | count)")
+        self.balance = balance
+        self.rebalance_tolerance = float(rebalance_tolerance)
+        rv = inter.lj.r_cut + self.r_skin
+        self.dims_z = max(1, int(np.floor(float(flat.box[2]) / rv)))
+        self.cuts = default_cuts(R, self.dims_z)
+        self.recuts = 0
         self.ctx = {r: ctx_factory(r) for r in comm.local_ranks}
         self.nb: Dict[int, Tuple[int, int]] = {}
         self.ng: Dict[int, Tuple[int, int]] = {}
@@ -448,6 +501,8 @@ class DecomposedEngine:
         R = self.comm.nranks
         for c in self.ctx.values():
             c.decide(True, advance)
+        if self.balance == "count":
+            self._rebalance()
         # 1. migration of leavers to the owners of their z layers
         out = {r: c.migrate_out() for r, c in self.ctx.items()}
         M = self.comm.allgather({r: out[r][0] for r in self.ctx})  # M[src, dst]
@@ -488,6 +543,20 @@ class DecomposedEngine:
         # 3. cell ranges of the ghost layers + list build
         for c in self.ctx.values():
             c.ghosts_ready()
+
+    def _rebalance(self) -> None:
+        """Load-aware cut planes: particle counts per z layer
+        summed over ranks; re-cut when the current cuts' largest slab exceeds
+        the balanced optimum by more than the tolerance."""
+        hist = self.comm.allreduce_sum(
+            {r: c.layer_counts(self.dims_z).astype(np.float64) for r, c in self.ctx.items()})
+        hist = np.rint(hist).astype(np.int64)
+        best = balanced_cuts(hist, self.comm.nranks)
+        if max_load(hist, self.cuts) > self.rebalance_tolerance * max_load(hist, best):
+            for c in self.ctx.values():
+                c.recut(best)
+            self.cuts = best
+            self.recuts += 1
 
     def _halo(self) -> None:
         R = self.comm.nranks

@@ -399,6 +399,33 @@ def gen_fcc(cells: int, rho: float, temperature: float, seed: int,
     return FlatConfig(box, ids, pos, vel)
 
 
+def gen_fcc_slab(cells: int, rho: float, temperature: float, seed: int,
+                 n: Optional[int] = None) -> FlatConfig:
+    """BASELINE.json configs[3] shape: a liquid FCC slab at density rho filling
+    the middle third of a box with Lz = 3 Lx = 3 Ly (vacuum elsewhere).
+
+    The slab is a cells^3 x 4 FCC block of side Lx = (4 cells^3 / rho)^(1/3)
+    shifted to z in [Lx, 2 Lx). With `n` set, only the first n sites in id
+    order are kept (2,097,152 particles is not 4 k^3, so an
+    81^3-cell block is filled in id order with its tail left empty —
+    gen_lattice's convention, generators.hpp:48-81)."""
+    f = gen_fcc(cells, rho, temperature, seed)
+    box = f.box.copy()
+    pos = f.pos.copy()
+    pos[:, 2] += box[2]
+    box[2] *= 3.0
+    ids, vel = f.id, f.vel
+    if n is not None:
+        if not 1 <= n <= len(ids):
+            raise ConfigError(f"slab generator: 1 <= n <= {len(ids)} required")
+        keep = np.argsort(ids, kind="stable")[:n]
+        ids, pos = ids[keep], pos[keep]
+        out = FlatConfig(box, ids, pos, None)
+        thermal_velocities(out, temperature, seed)
+        return out
+    return FlatConfig(box, ids, pos, vel)
+
+
 def thermal_velocities(flat: FlatConfig, temperature: float, seed: int) -> None:
     """gen_detail::thermal_velocities + zero_net_momentum (generators.hpp:19-39)."""
     vel = np.empty((flat.size(), 3))

@@ -30,8 +30,8 @@ class MockSlab:
         self.cl = self.L / self.dims
         self.dxy = int(self.dims[0] * self.dims[1])
         dz = int(self.dims[2])
-        self.z0 = rank * dz // nranks
-        self.z1 = (rank + 1) * dz // nranks
+        self.cuts = [r * dz // nranks for r in range(nranks + 1)]
+        self.z0, self.z1 = self.cuts[rank], self.cuts[rank + 1]
         self.dt = dt
         self.rec_bytes = 64
         zc = self._cell(wrap1(flat.pos, self.L))[:, 2]
@@ -49,9 +49,18 @@ class MockSlab:
         return np.clip(c, 0, self.dims - 1)
 
     def _owner(self, z):
-        dz = int(self.dims[2])
-        return np.searchsorted([(r + 1) * dz // self.nranks for r in range(self.nranks)], z,
-                               side="right")
+        return np.searchsorted(self.cuts[1:], z, side="right")
+
+    def layer_counts(self, dims_z):
+        assert dims_z == int(self.dims[2])
+        z = self._cell(wrap1(self.pos, self.L))[:, 2] if len(self.id) else np.zeros(0, int)
+        return np.bincount(z, minlength=dims_z).astype(np.int64)
+
+    def recut(self, cuts):
+        assert cuts[0] == 0 and cuts[-1] == int(self.dims[2])
+        assert all(b > a for a, b in zip(cuts, cuts[1:]))
+        self.cuts = [int(x) for x in cuts]
+        self.z0, self.z1 = self.cuts[self.rank], self.cuts[self.rank + 1]
 
     # -- protocol (same names and return shapes as decomp.SlabContext)
     def info(self):

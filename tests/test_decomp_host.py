@@ -37,10 +37,23 @@ def _system(n=600, seed=3, box=(5.4, 4.0, 11.8)):
     return FlatConfig(L, ids, pos, vel)
 
 
-def _make(flat, comm):
+def _make(flat, comm, balance="static"):
     rv = R_CUT + R_SKIN
-    return DecomposedEngine(flat, Interactions(), R_SKIN, EngineConfig(dt=DT), comm=comm,
-                            ctx_factory=lambda r: MockSlab(flat, rv, DT, r, comm.nranks))
+    inter = Interactions()
+    inter.lj.r_cut = R_CUT
+    return DecomposedEngine(flat, inter, R_SKIN, EngineConfig(dt=DT), comm=comm,
+                            ctx_factory=lambda r: MockSlab(flat, rv, DT, r, comm.nranks),
+                            balance=balance)
+
+
+def _slab_system(n=900, seed=4, box=(5.4, 4.0, 23.5)):
+    """Particles only in the middle third of z (config 4's liquid slab shape)."""
+    rng = np.random.default_rng(seed)
+    L = np.asarray(box)
+    pos = rng.random((n, 3)) * L
+    pos[:, 2] = L[2] / 3 + rng.random(n) * L[2] / 3
+    vel = 0.5 * rng.normal(size=(n, 3))
+    return FlatConfig(L, np.arange(n, dtype=np.int64) * 3 + 1, pos, vel)
 
 
 def _snapshot(eng):
@@ -58,14 +71,14 @@ def _snapshot(eng):
     return out
 
 
-def _check(snaps, all_ids, dims_z):
+def _check(snaps, all_ids, dims_z, cuts=None):
     R = len(snaps)
     owned = np.concatenate([snaps[r]["ids"] for r in range(R)])
     assert len(owned) == len(all_ids)
     np.testing.assert_array_equal(np.sort(owned), np.sort(all_ids))
     for r in range(R):
         s = snaps[r]
-        z0, z1 = slab_range(r, R, dims_z)
+        z0, z1 = (slab_range(r, R, dims_z) if cuts is None else (cuts[r], cuts[r + 1]))
         assert (s["z0"], s["z1"]) == (z0, z1)
         # membership as of the last rebuild
         assert np.all((s["cellz"] >= z0) & (s["cellz"] < z1))
@@ -90,7 +103,7 @@ def _run_and_check(eng, flat, steps_seq, gather):
     for k in steps_seq:
         eng.run(k)
         snaps = gather(_snapshot(eng))
-        _check(snaps, flat.id, dims_z)
+        _check(snaps, flat.id, dims_z, eng.cuts)
         total_rebuilds = eng.rebuild_count()
     return total_rebuilds
 
@@ -116,6 +129,37 @@ def test_inprocess_migration_happens():
     assert any(before[r] != after[r] for r in before)
 
 
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_load_aware_cuts_balance_an_inhomogeneous_slab(R):
+    """with the liquid in the middle third of z the static
+    range rule leaves ranks idle; count-balanced cuts spread the particles."""
+    flat = _slab_system()
+    static = _make(flat, InProcessComm(R))
+    pop_static = [len(c.id) for c in static.ctx.values()]
+    eng = _make(flat, InProcessComm(R), balance="count")
+    pop = [len(c.id) for c in eng.ctx.values()]
+    if R > 2:  # at R = 2 the static halves already split the slab evenly
+        assert eng.recuts >= 1
+    assert max(pop) <= max(pop_static)
+    assert max(pop) < 1.6 * len(flat.id) / R
+    _run_and_check(eng, flat, [3, 20], lambda s: s)
+
+
+def test_balanced_cuts_are_optimal():
+    import itertools
+    from paper_2109_10876_b200.decomp import balanced_cuts, max_load
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        dz = int(rng.integers(3, 9))
+        R = int(rng.integers(2, dz + 1))
+        c = rng.choice([0, 0, 1, 5, 20, 100], size=dz)
+        cuts = balanced_cuts(c, R)
+        assert cuts[0] == 0 and cuts[-1] == dz and len(cuts) == R + 1
+        assert all(b > a for a, b in zip(cuts, cuts[1:]))
+        best = min(max_load(c, [0, *m, dz]) for m in itertools.combinations(range(1, dz), R - 1))
+        assert max_load(c, cuts) == best
+
+
 def test_requires_two_ranks():
     from paper_2109_10876_b200.engine import ConfigError
     with pytest.raises(ConfigError):
@@ -129,15 +173,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, balance="static"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world,
                                 init_method=f"tcp://127.0.0.1:{port}")
-        flat = _system(n=500, seed=11)
+        flat = _system(n=500, seed=11) if balance == "static" else _slab_system()
         comm = TorchDistComm()
-        eng = _make(flat, comm)
+        eng = _make(flat, comm, balance)
 
         def gather(local):
             objs = [None] * world
@@ -156,12 +200,13 @@ def _worker(rank, world, port, q):
         q.put((rank, "err", traceback.format_exc(), 0.0))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_protocol(world):
+@pytest.mark.parametrize("world,balance", [(2, "static"), (3, "static"), (3, "count")])
+def test_gloo_protocol(world, balance):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, balance))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
@@ -170,7 +215,7 @@ def test_gloo_protocol(world):
     errs = [r for r in res if r[1] != "ok"]
     assert not errs, errs[0][2]
     assert len({r[2] for r in res}) == 1 and res[0][2] >= 2
-    flat = _system(n=500, seed=11)
+    flat = _system(n=500, seed=11) if balance == "static" else _slab_system()
     ke = 0.5 * float(np.sum(flat.vel ** 2))
     for r in res:
         assert r[3] == pytest.approx(ke, rel=1e-12)

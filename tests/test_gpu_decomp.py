@@ -164,3 +164,37 @@ def test_multiprocess_torch_distributed(world):
     assert np.abs(pos - g["final_pos"]).max() < 1e-9
     assert np.abs(vel - g["final_vel"]).max() < 1e-9
     assert all(o[2] == int(g["rebuilds"]) for o in objs)
+
+
+@pytest.mark.parametrize("R", [3, 4])
+def test_load_aware_cuts_on_a_liquid_slab(R):
+    """SURVEY §8f f3 on BASELINE configs[3]'s shape (liquid FCC slab in the
+    middle third of z): count-balanced cuts re-cut the slabs, and the
+    decomposed run still tracks the single-context engine."""
+    flat = E.gen_fcc_slab(8, 0.8442, 0.7, 5)
+    cfg = E.EngineConfig(dt=0.005, section_timers=False)
+    one = E.Engine(flat, E.Interactions(), 0.3, cfg)
+    dec = DecomposedEngine(flat, E.Interactions(), 0.3, cfg, comm=InProcessComm(R),
+                           balance="count")
+    static = DecomposedEngine(flat, E.Interactions(), 0.3, cfg, comm=InProcessComm(R))
+    try:
+        assert dec.recuts >= 1
+        pop = [s["n_own"] for s in dec.slab_sizes().values()]
+        pop_static = [s["n_own"] for s in static.slab_sizes().values()]
+        assert max(pop) < max(pop_static)
+        assert max(pop) <= 1.5 * flat.size() / R
+        np.testing.assert_array_equal(dec.local_pairs(), one.pairs())
+        one.run(100)
+        dec.run(100)
+        o1, o2 = one.observe(), dec.observe()
+        assert_rel(o2.potential, o1.potential, 1e-10, "PE")
+        ids, pos, vel, f = dec.local_state()
+        ids1, f1 = one.forces()
+        np.testing.assert_array_equal(ids, ids1)
+        assert_forces_close(f, f1, rtol=1e-8)
+        assert dec.rebuild_count() == one.rebuild_count()
+        np.testing.assert_array_equal(dec.local_pairs(), one.pairs())
+    finally:
+        dec.close()
+        static.close()
+        one.close()

@@ -103,14 +103,13 @@ class Engine {
  public:
   // build_domain(flat, inter, r_skin, n_sub) + Engine(domain, cfg)
   // (domain.hpp:134-189, engine.hpp:68-77). n_sub / worker_threads have no
-  // GPU meaning and are ignored; bonded terms are rejected with ConfigError
-  // until that row lands. A thermostat runs on the device.
+  // GPU meaning and are ignored; angle terms are rejected with ConfigError.
+  // FENE bonds and a thermostat run on the device.
   Engine(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
          const taskmd::EngineConfig& cfg, const GpuOptions& opt = {})
       : cfg_(cfg) {
-    if (inter.angle) throw taskmd::ConfigError("angle terms are not on the GPU LJ path");
-    if (inter.fene || !flat.topo.bonds.empty()) {
-      throw taskmd::ConfigError("FENE bonds are not on the GPU path yet");
+    if (inter.angle || !flat.topo.angles.empty()) {
+      throw taskmd::ConfigError("angle terms are not on the GPU LJ path");
     }
     const std::size_t n = flat.size();
     std::vector<double> pos(3 * n), vel(3 * n);
@@ -132,6 +131,16 @@ class Engine {
     sys.mass = flat.mass.empty() ? nullptr : flat.mass.data();
     sys.pos = pos.data();
     sys.vel = vel.data();
+    std::vector<int64_t> bonds;  // Topology::bonds as (a, b) id pairs
+    bonds.reserve(2 * flat.topo.bonds.size());
+    for (const auto& b : flat.topo.bonds) {
+      bonds.push_back(b.a);
+      bonds.push_back(b.b);
+    }
+    sys.n_bonds = static_cast<int64_t>(flat.topo.bonds.size());
+    sys.bonds = bonds.empty() ? nullptr : bonds.data();
+    tmd_fene_params fene{};
+    if (inter.fene) fene = tmd_fene_params{inter.fene->k, inter.fene->r_max};
     tmd_lj_params lj{inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
                      inter.lj.energy_shifted ? 1 : 0};
     tmd_engine_params p{};
@@ -147,14 +156,17 @@ class Engine {
       p.temperature = cfg.thermostat->temperature;
       p.seed = cfg.thermostat->seed;
     }
-    const int rc = tmd_gpu_create(&sys, &lj, nullptr, &p, &ctx_);
+    const int rc = tmd_gpu_create(&sys, &lj, inter.fene ? &fene : nullptr, &p, &ctx_);
     if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
     box_ = flat.box;
+    topo_ = flat.topo;
   }
 
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
-  Engine(Engine&& o) noexcept : ctx_(std::exchange(o.ctx_, nullptr)), cfg_(o.cfg_), box_(o.box_) {}
+  Engine(Engine&& o) noexcept
+      : ctx_(std::exchange(o.ctx_, nullptr)), cfg_(o.cfg_), box_(o.box_),
+        topo_(std::move(o.topo_)) {}
   ~Engine() { tmd_gpu_destroy(ctx_); }
 
   void step() { run(1); }
@@ -198,6 +210,7 @@ class Engine {
     check(tmd_gpu_download(ctx_, id.data(), pos.data(), vel.data(), nullptr));
     taskmd::FlatConfig f;
     f.box = box_;
+    f.topo = topo_;
     f.id = id;
     f.type.assign(n, 0);
     f.mass.assign(n, 1.0);
@@ -243,6 +256,7 @@ class Engine {
   tmd_gpu_ctx* ctx_ = nullptr;
   taskmd::EngineConfig cfg_;
   taskmd::BoxSpec box_;
+  taskmd::Topology topo_;
 };
 
 }  // namespace taskmd_gpu

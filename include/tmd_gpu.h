@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TMD_GPU_ABI_VERSION 2
+#define TMD_GPU_ABI_VERSION 3
 
 /* Status codes. */
 #define TMD_OK 0
@@ -52,7 +52,10 @@ typedef struct tmd_gpu_ctx tmd_gpu_ctx;
 
 /* taskmd::FlatConfig (flat_config.hpp:18-40) as plain arrays. pos/vel are
  * xyz-interleaved [3*n]; type and mass may be NULL (0 and 1.0). vel may be
- * NULL (zero). Topology is not part of the LJ path (FENE is row f1). */
+ * NULL (zero). Topology::bonds (topology.hpp:14-31) as n_bonds (a, b) id pairs
+ * (bonds[2*k], bonds[2*k+1]); angles are not on the GPU path. Bonded systems
+ * need ids in a dense range (max - min < 4 n + 1024) and at most 8 bonds per
+ * particle. */
 typedef struct tmd_system {
   double box[3];
   int64_t n;
@@ -61,6 +64,8 @@ typedef struct tmd_system {
   const double* mass;
   const double* pos;
   const double* vel;
+  int64_t n_bonds;
+  const int64_t* bonds;
 } tmd_system;
 
 /* taskmd::LjParams (potentials.hpp:21-26). */
@@ -71,8 +76,8 @@ typedef struct tmd_lj_params {
   int energy_shifted;
 } tmd_lj_params;
 
-/* taskmd::FeneParams (potentials.hpp:79-82). Reserved: a non-NULL pointer is
- * rejected with TMD_ERR_CONFIG until the bonded path lands. */
+/* taskmd::FeneParams (potentials.hpp:77-104): Interactions::fene, NULL when
+ * absent. Bonds need it, and r_max <= r_cut + r_skin (domain.hpp:151-159). */
 typedef struct tmd_fene_params {
   double k;
   double r_max;
@@ -101,6 +106,10 @@ typedef struct tmd_engine_params {
   double gamma;
   double temperature;
   uint64_t seed;
+  /* > 0: cap every LJ pair force at |F| <= force_cap (energies uncapped) —
+   * the overlap warm-up of a freshly generated polymer melt (BASELINE
+   * configs[2]); runs the thread-per-particle kernel. 0 = off. */
+  double force_cap;
 } tmd_engine_params;
 
 /* taskmd::StepObservables (engine.hpp:43-48) plus the virial
@@ -130,7 +139,7 @@ typedef struct tmd_list_stats {
  * builds the list and runs the initial untimed force evaluation
  * (compute_forces_untimed, engine.hpp:244-278). */
 int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
-                   const tmd_fene_params* fene /* must be NULL */,
+                   const tmd_fene_params* fene /* NULL: no bonds */,
                    const tmd_engine_params* params, tmd_gpu_ctx** out);
 
 /* Message of the last failed call on ctx (or of the last failed create when
@@ -307,6 +316,14 @@ int tmd_gpu_slab_sums(tmd_gpu_ctx* ctx, double out[3]);
  * 4*cells^3. */
 int tmd_gen_fcc(int cells, double rho, double offset, int64_t* id, double* pos,
                 double box[3]);
+
+/* Kremer-Grest melt (BASELINE configs[2]; new — the reference generates
+ * only ring melts, generators.hpp:137-210): n_chains linear random-walk
+ * chains of chain_len beads, bond length `bond`, no immediate back-folding,
+ * cubic box L = (N/rho)^(1/3), ids chain-major, bonds[2*(n_chains*(chain_len-1))]
+ * as consecutive (i, i+1) pairs. Velocities are left to the caller. */
+int tmd_gen_chains(int64_t n_chains, int64_t chain_len, double rho, double bond, uint64_t seed,
+                   int64_t* id, double* pos, int64_t* bonds, double box[3]);
 
 /* gen_detail::thermal_velocities + zero_net_momentum (generators.hpp:19-39):
  * v = sqrt(T/m) * counter_normal3(seed, kVelocityInit, 0, id), then the

@@ -88,16 +88,41 @@ def exact_energies(box, pos_by_id, pairs, lj=(1.0, 1.0, 2.5, True)):
     return math.fsum(e.tolist()), math.fsum((ff * r2[m]).tolist()), int(m.sum())
 
 
+def bond_energies(box, pos_by_id, bonds, fene):
+    """fsum of the reference's FENE terms (fene_eval, potentials.hpp:95-104)
+    over the minimum-image bond vectors, and their virial ff r^2."""
+    k, r_max = fene
+    ids_sorted, pos_sorted = pos_by_id
+    ia = np.searchsorted(ids_sorted, bonds[:, 0])
+    ib = np.searchsorted(ids_sorted, bonds[:, 1])
+    d = pos_sorted[ia] - pos_sorted[ib]
+    d -= box * np.round(d / box)
+    r2 = (d * d).sum(axis=1)
+    rmax2 = r_max * r_max
+    g = 1.0 - r2 / rmax2
+    e = -0.5 * k * rmax2 * np.log(g)
+    ff = -k / g
+    return math.fsum(e.tolist()), math.fsum((ff * r2).tolist())
+
+
 def system_fixture(name, box, ids, pos, vel, *, r_skin=0.3, n_subs=(1, 8), steps=0,
-                   trace_every=0, dt=0.005, oracle=False, thermostat=None):
+                   trace_every=0, dt=0.005, oracle=False, thermostat=None, lj=None,
+                   bonds=None, fene=None):
     out = dict(box=box, ids=ids, pos=pos, vel=vel, r_skin=np.float64(r_skin),
                dt=np.float64(dt))
     if thermostat is not None:
         out["thermostat"] = np.array(thermostat, dtype=np.float64)  # gamma, T, seed
+    lj = lj or (1.0, 1.0, 2.5, True)
+    if lj != (1.0, 1.0, 2.5, True):
+        out["lj"] = np.array([lj[0], lj[1], lj[2], 1.0 if lj[3] else 0.0])
+    if bonds is not None:
+        out["bonds"] = np.asarray(bonds, np.int64)
+        out["fene"] = np.array(fene, dtype=np.float64)
     pairs0 = None
     for ns in n_subs:
         e = ref.RefEngine(box, ids, pos, vel, r_skin=r_skin, n_sub=ns, dt=dt,
-                          thermostat=thermostat)
+                          thermostat=thermostat, eps=lj[0], sigma=lj[1], r_cut=lj[2],
+                          shifted=lj[3], bonds=bonds, fene=fene)
         p = e.pairs()
         if pairs0 is None:
             pairs0 = p
@@ -110,7 +135,10 @@ def system_fixture(name, box, ids, pos, vel, *, r_skin=0.3, n_subs=(1, 8), steps
                        wrapped=fl_pos)
             dims, cl = e.grid()
             out.update(dims=dims, cell_len=cl)
-            pe_f, w_f, ncut = exact_energies(box, (fl_ids, fl_pos), p)
+            pe_f, w_f, ncut = exact_energies(box, (fl_ids, fl_pos), p, lj)
+            if bonds is not None:
+                be, bw = bond_energies(box, (fl_ids, fl_pos), np.asarray(bonds), fene)
+                pe_f, w_f = math.fsum([pe_f, be]), math.fsum([w_f, bw])
             out.update(pe_fsum=np.float64(pe_f), w_fsum=np.float64(w_f),
                        n_incut=np.int64(ncut))
             if steps:
@@ -153,12 +181,54 @@ def thermostat_fixtures():
                    thermostat=(0.5, 1.4, 2021))
 
 
+def lattice_chains(side, rho, seed, jitter=0.05, temperature=1.0):
+    """Kremer-Grest test melt without overlaps: side^3 beads on a simple cubic
+    lattice at bead density rho, one chain per z plane running boustrophedon
+    through it (every bond one lattice spacing, about 1.056 at rho = 0.85),
+    positions jittered with the reference's counter RNG, thermal velocities."""
+    a = (1.0 / rho) ** (1.0 / 3.0)
+    n = side ** 3
+    ids = np.arange(n, dtype=np.int64)
+    pos = np.empty((n, 3))
+    bonds = []
+    k = 0
+    for z in range(side):
+        for y in range(side):
+            xs = range(side) if y % 2 == 0 else range(side - 1, -1, -1)
+            for x in xs:
+                u = ref.counter_uniform3(seed, K_PLACEMENT, 0, k)
+                pos[k] = [(x + 0.5) * a + jitter * (2.0 * u[0] - 1.0),
+                          (y + 0.5) * a + jitter * (2.0 * u[1] - 1.0),
+                          (z + 0.5) * a + jitter * (2.0 * u[2] - 1.0)]
+                k += 1
+        base = z * side * side
+        bonds += [[base + j, base + j + 1] for j in range(side * side - 1)]
+    vel = ref.thermal_velocities(ids, temperature, seed)
+    return np.full(3, side * a), ids, pos, vel, np.array(bonds, dtype=np.int64)
+
+
+def bonded_fixtures():
+    """FENE + WCA (Kremer-Grest) runs of the reference (row f1)."""
+    wca = (1.0, 1.0, 2.0 ** (1.0 / 6.0), True)
+    kg_fene = (30.0, 1.5)
+    b, i, p, v, bonds = lattice_chains(10, 0.85, 17)
+    system_fixture("kg_lattice10", b, i, p, v, r_skin=0.4, n_subs=(1, 8), steps=200,
+                   trace_every=20, dt=0.005, lj=wca, bonds=bonds, fene=kg_fene)
+    # bonded LJ liquid: FENE chains inside the standard LJ fluid (r_cut 2.5)
+    b, i, p, v, bonds = lattice_chains(8, 0.8, 23, jitter=0.08, temperature=0.8)
+    system_fixture("fene_lj8", b, i, p, v, r_skin=0.3, n_subs=(1, 8), steps=100,
+                   trace_every=20, dt=0.004, bonds=bonds, fene=kg_fene)
+
+
 def main():
     if not ref.available():
         ref.build()
     OUT.mkdir(parents=True, exist_ok=True)
     if "--only-thermostat" in sys.argv:
         thermostat_fixtures()
+        return
+    if "--only-bonded" in sys.argv:
+        bonded_fixtures()
         return
 
     # -- scalar LJ: lj_eval over a grid of r2 (test_potentials.cpp:33-89)
@@ -244,6 +314,7 @@ def main():
         vel = ref.thermal_velocities(ids, 0.5, 99)
         system_fixture(name, box, ids, pos, vel, n_subs=(1,), steps=50, trace_every=10)
     thermostat_fixtures()
+    bonded_fixtures()
     # SC lattice 4000 (acceptance criterion 3): energy traces at dt 0.005, 0.001
     b, i, p, v = ref.gen_lattice(4000, 0.8442, 0.6, 3)
     traces = {}

@@ -31,6 +31,14 @@ class RefError(RuntimeError):
 _lib = None
 
 
+class RefOpts(C.Structure):
+    """ref_shim.cpp's ref_opts: thermostat and FENE bonds."""
+    _fields_ = [("thermostat", C.c_int), ("gamma", C.c_double),
+                ("temperature", C.c_double), ("seed", C.c_uint64),
+                ("n_bonds", C.c_int64), ("bonds", C.c_void_p), ("fene", C.c_int),
+                ("fene_k", C.c_double), ("fene_rmax", C.c_double)]
+
+
 def available() -> bool:
     return REF_LIB.exists()
 
@@ -49,9 +57,9 @@ def lib() -> C.CDLL:
         D = C.c_double
         L.ref_create.argtypes = [C.c_int64, P, P, P, P, P, D, D, D, C.c_int, D,
                                  C.c_int, C.c_int, D, C.POINTER(P), C.c_char_p, C.c_int]
-        L.ref_create_thermo.argtypes = [C.c_int64, P, P, P, P, P, D, D, D, C.c_int, D,
-                                        C.c_int, C.c_int, D, D, D, C.c_uint64,
-                                        C.POINTER(P), C.c_char_p, C.c_int]
+        L.ref_create_ex.argtypes = [C.c_int64, P, P, P, P, P, D, D, D, C.c_int, D,
+                                    C.c_int, C.c_int, D, C.POINTER(RefOpts),
+                                    C.POINTER(P), C.c_char_p, C.c_int]
         L.ref_destroy.argtypes = [P]
         L.ref_destroy.restype = None
         L.ref_step.argtypes = [P, C.c_int64, C.c_char_p, C.c_int]
@@ -121,8 +129,9 @@ class RefEngine:
 
     def __init__(self, box, ids, pos, vel=None, mass=None, *, eps=1.0, sigma=1.0,
                  r_cut=2.5, shifted=True, r_skin=0.3, n_sub=1, workers=1, dt=0.005,
-                 thermostat=None):
-        """thermostat: None (NVE) or (gamma, temperature, seed)."""
+                 thermostat=None, bonds=None, fene=None):
+        """thermostat: None (NVE) or (gamma, temperature, seed); bonds: (n, 2)
+        ids; fene: None or (k, r_max)."""
         L = lib()
         self._ids = _c(ids, np.int64)
         self._n = int(self._ids.shape[0])
@@ -132,16 +141,22 @@ class RefEngine:
         mass = _c(mass, np.float64)
         err = C.create_string_buffer(512)
         h = C.c_void_p()
-        if thermostat is None:
-            rc = L.ref_create(self._n, _p(self._ids), _p(mass), _p(pos), _p(vel), _p(box),
-                              eps, sigma, r_cut, 1 if shifted else 0, r_skin, n_sub,
-                              workers, dt, C.byref(h), err, 512)
-        else:
-            gamma, temp, seed = thermostat
-            rc = L.ref_create_thermo(self._n, _p(self._ids), _p(mass), _p(pos), _p(vel),
-                                     _p(box), eps, sigma, r_cut, 1 if shifted else 0, r_skin,
-                                     n_sub, workers, dt, float(gamma), float(temp), int(seed),
-                                     C.byref(h), err, 512)
+        o = RefOpts()
+        if thermostat is not None:
+            o.thermostat = 1
+            o.gamma, o.temperature, o.seed = float(thermostat[0]), float(thermostat[1]), \
+                int(thermostat[2])
+        self._bonds = None
+        if bonds is not None and len(bonds):
+            self._bonds = _c(bonds, np.int64)
+            o.n_bonds = int(self._bonds.shape[0])
+            o.bonds = _p(self._bonds)
+        if fene is not None:
+            o.fene = 1
+            o.fene_k, o.fene_rmax = float(fene[0]), float(fene[1])
+        rc = L.ref_create_ex(self._n, _p(self._ids), _p(mass), _p(pos), _p(vel), _p(box),
+                             eps, sigma, r_cut, 1 if shifted else 0, r_skin, n_sub, workers,
+                             dt, C.byref(o), C.byref(h), err, 512)
         _raise(rc, err)
         self._h = h
 

@@ -132,28 +132,44 @@ int ref_create(std::int64_t n, const std::int64_t* id, const double* mass,
   });
 }
 
-// The same with EngineConfig::thermostat set (engine.hpp:19-26; the bath is
-// applied by thermostat_and_half_kick, engine.hpp:209-239).
-int ref_create_thermo(std::int64_t n, const std::int64_t* id, const double* mass,
-                      const double* pos, const double* vel, const double box[3], double eps,
-                      double sigma, double rc, int shifted, double r_skin, int n_sub,
-                      int workers, double dt, double gamma, double temperature,
-                      std::uint64_t seed, ref_engine** out, char* err, int errlen) {
+// The same with the optional parts of the configuration: a Langevin bath
+// (EngineConfig::thermostat, engine.hpp:19-26) and FENE bonds
+// (Topology::bonds + Interactions::fene, topology.hpp:14-31, domain.hpp:19-23).
+struct ref_opts {
+  int thermostat;
+  double gamma, temperature;
+  std::uint64_t seed;
+  std::int64_t n_bonds;
+  const std::int64_t* bonds;
+  int fene;
+  double fene_k, fene_rmax;
+};
+
+int ref_create_ex(std::int64_t n, const std::int64_t* id, const double* mass,
+                  const double* pos, const double* vel, const double box[3], double eps,
+                  double sigma, double rc, int shifted, double r_skin, int n_sub, int workers,
+                  double dt, const ref_opts* o, ref_engine** out, char* err, int errlen) {
   *out = nullptr;
   return guarded(err, errlen, [&] {
     FlatConfig f = make_flat(n, id, mass, pos, vel, box);
+    for (std::int64_t k = 0; k < o->n_bonds; ++k) {
+      f.topo.bonds.push_back({o->bonds[2 * k], o->bonds[2 * k + 1]});
+    }
+    Interactions inter = make_inter(eps, sigma, rc, shifted);
+    if (o->fene) inter.fene = FeneParams{o->fene_k, o->fene_rmax};
     EngineConfig cfg;
     cfg.dt = dt;
     cfg.n_sub = n_sub;
     cfg.worker_threads = workers;
-    LangevinParams bath;
-    bath.gamma = gamma;
-    bath.temperature = temperature;
-    bath.seed = seed;
-    cfg.thermostat = bath;
+    if (o->thermostat) {
+      LangevinParams bath;
+      bath.gamma = o->gamma;
+      bath.temperature = o->temperature;
+      bath.seed = o->seed;
+      cfg.thermostat = bath;
+    }
     auto h = std::make_unique<ref_engine>();
-    h->eng = std::make_unique<Engine>(
-        build_domain(f, make_inter(eps, sigma, rc, shifted), r_skin, n_sub), cfg);
+    h->eng = std::make_unique<Engine>(build_domain(f, inter, r_skin, n_sub), cfg);
     *out = h.release();
   });
 }

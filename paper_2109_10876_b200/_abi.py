@@ -34,7 +34,7 @@ EXPORTS = [
     "tmd_gpu_slab_commit", "tmd_gpu_slab_border", "tmd_gpu_slab_ghost_in",
     "tmd_gpu_slab_ghosts_ready", "tmd_gpu_slab_kick_drift", "tmd_gpu_slab_forces",
     "tmd_gpu_slab_halo", "tmd_gpu_slab_sums", "tmd_gpu_slab_layer_counts",
-    "tmd_gpu_slab_recut",
+    "tmd_gpu_slab_recut", "tmd_gen_chains",
 ]
 
 
@@ -47,6 +47,8 @@ class TmdSystem(C.Structure):
         ("mass", C.c_void_p),
         ("pos", C.c_void_p),
         ("vel", C.c_void_p),
+        ("n_bonds", C.c_int64),
+        ("bonds", C.c_void_p),
     ]
 
 
@@ -64,7 +66,8 @@ class TmdEngineParams(C.Structure):
                 ("device", C.c_int), ("section_timers", C.c_int),
                 ("nbr_capacity", C.c_int), ("reserved", C.c_int * 5),
                 ("thermostat", C.c_int), ("gamma", C.c_double),
-                ("temperature", C.c_double), ("seed", C.c_uint64)]
+                ("temperature", C.c_double), ("seed", C.c_uint64),
+                ("force_cap", C.c_double)]
 
 
 class TmdObservables(C.Structure):
@@ -143,6 +146,8 @@ def lib() -> C.CDLL:
     L.tmd_gpu_destroy.argtypes = [P]
     L.tmd_gpu_destroy.restype = None
     L.tmd_gen_fcc.argtypes = [C.c_int, C.c_double, C.c_double, P, P, P]
+    L.tmd_gen_chains.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_uint64,
+                                 P, P, P, P]
     L.tmd_thermal_velocities.argtypes = [C.c_int64, P, P, C.c_double, C.c_uint64, P]
     L.tmd_thermal_velocities.restype = None
     for name in ("tmd_counter_uniform3", "tmd_counter_normal3"):

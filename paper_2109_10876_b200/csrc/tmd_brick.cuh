@@ -935,6 +935,7 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
+    if (it.bt.on) bond_accumulate(i, pi, pos, it.bt, g, id, ctrl, ax, ay, az, e, w);
     integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
     fx[i] = ax;
     fy[i] = ay;

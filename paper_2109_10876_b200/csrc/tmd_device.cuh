@@ -41,10 +41,15 @@ enum : int {
   kStatOverflow = 8,     // neighbour list capacity exceeded -> host re-runs
   kStatStageOverflow = 16,  // a brick halo exceeded the staging capacity -> grow
   kStatStray = 32,       // slab mode: a particle outside the slab at binning (bug)
+  kStatBondReach = 64,   // bonded partner not among the reachable slots (bonded.hpp:51-57)
+  kStatBondStretch = 128,  // FENE bond at or beyond r_max (bonded.hpp:184-191)
 };
+
+constexpr int kMaxBonds = 8;  // bonds per particle (linear chains: 2)
 
 struct LjConst {
   double sigma2, rc2, eps4, eps24, shift;  // lj_prepare (potentials.hpp:49-61)
+  double fcap;  // > 0: cap |F_pair| (overlap warm-up only; thread-per-particle kernel)
 };
 
 struct Geom {
@@ -90,6 +95,7 @@ struct Ctrl {
   long long entries;          // total entries, last build
   int max_halo;               // largest staged halo seen (slots)
   int err_bit;                // status bit of the first error (its record below)
+  double err_val;             // a value for the first error's message (bond r^2)
 };
 
 // ---------------------------------------------------------------------------
@@ -182,10 +188,11 @@ __device__ __forceinline__ bool finite3(double a, double b, double c) {
 
 // First error wins the detail record; every error ORs its status bit.
 __device__ __forceinline__ void record_error(Ctrl* ctrl, int bit, long long id0,
-                                             long long id1) {
+                                             long long id1, double val = 0.0) {
   atomicOr(&ctrl->status, bit);
   if (atomicCAS(&ctrl->err_lock, 0, 1) == 0) {
     ctrl->err_bit = bit;
+    ctrl->err_val = val;
     ctrl->err_step = ctrl->step;
     ctrl->err_id0 = id0;
     ctrl->err_id1 = id1;

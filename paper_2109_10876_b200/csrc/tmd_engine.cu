@@ -95,6 +95,16 @@ struct tmd_gpu_ctx {
   double dt = 0, half_dt = 0, r_skin = 0, r_cut = 0;
   bool timers_on = true;
   Thermo th{};  // Langevin bath (th.on = 0: NVE)
+  // FENE bonds (row f1): static per-id bond table + per-slot resolved entries
+  BondTab bt{};
+  long long id_min = 0;
+  int64_t id_span = 0;
+  int* slot_of_id = nullptr;       // [id_span] (owned + ghost slots), -1 = absent
+  int* bond_off = nullptr;         // [id_span + 1] CSR over id - id_min
+  int* bond_nbr = nullptr;         // partner id - id_min
+  unsigned char* bond_anchor = nullptr;  // 1: this end is the bond's anchor a
+  int* bnd_cnt = nullptr;          // [n_cap]
+  uint32_t* bnd_ent = nullptr;     // [n_cap * kMaxBonds]
 
   // particle arrays (cell-sorted) + alternates for the permutation
   double4 *pos = nullptr, *pos2 = nullptr, *snap = nullptr;
@@ -225,7 +235,9 @@ void free_all(tmd_gpu_ctx* c) {
                   c->group_off, c->decoded, c->scan_tmp, c->owner_of_z, c->mig_dest,
                   c->mig_count, c->mig_off, c->mig_keep, c->mig_send, c->mig_recv,
                   c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
-                  c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1]};
+                  c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1],
+                  c->slot_of_id, c->bond_off, c->bond_nbr, c->bond_anchor, c->bnd_cnt,
+                  c->bnd_ent};
   for (void* p : ptrs) {
     if (p) cudaFree(p);
   }
@@ -368,7 +380,24 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
   }
 }
 
+// Bond resolution of a rebuild (gated on the device decision like the rest of
+// the rebuild): id -> slot table over owned + ghost slots, then per owned slot
+// its bonds' partner slots and closest images.
+void launch_bond_resolve(tmd_gpu_ctx* c) {
+  if (!c->bt.on) return;
+  c->launches += 3;
+  const int span = static_cast<int>(c->id_span);
+  const int slots = static_cast<int>(c->n + c->n_ghost);
+  k_fill_int<<<blocks_for(span, kBlock), kBlock, 0, c->ls>>>(span, c->slot_of_id, -1, c->ctrl);
+  k_slot_of_id<<<std::max(1, blocks_for(slots, kBlock)), kBlock, 0, c->ls>>>(
+      slots, c->id, c->id_min, c->slot_of_id, c->ctrl);
+  k_bond_resolve<<<c->nblk, kBlock, 0, c->ls>>>(
+      static_cast<int>(c->n), c->pos, c->id, c->id_min, c->bond_off, c->bond_nbr,
+      c->bond_anchor, c->slot_of_id, c->g, c->bnd_cnt, c->bnd_ent, c->ctrl);
+}
+
 void launch_build(tmd_gpu_ctx* c) {
+  launch_bond_resolve(c);
   c->launches += 2;
   k_build_prologue<<<1, 1, 0, c->ls>>>(c->ctrl);
   if (c->variant == 1) {
@@ -400,6 +429,9 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
   it.half_dt = c->half_dt;
   it.part_ke = c->part_ke;
   it.th = c->th;
+  it.bt = c->bt;
+  it.bt.cnt = c->bnd_cnt;
+  it.bt.ent = c->bnd_ent;
   if (c->variant == 1) {
     k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
@@ -493,6 +525,14 @@ void raise_physics(tmd_gpu_ctx* c, bool with_step) {
           std::to_string(h.err_id0);
   } else if (first & kStatNonFinitePos) {
     msg = "non-finite position for particle id " + std::to_string(h.err_id0);
+  } else if (first & kStatBondStretch) {
+    msg = "fene bond overstretched between ids " + std::to_string(h.err_id0) + " and " +
+          std::to_string(h.err_id1) + ": r = " + std::to_string(std::sqrt(h.err_val)) +
+          " >= r_max = " + std::to_string(std::sqrt(c->bt.rmax2));
+  } else if (first & kStatBondReach) {
+    msg = "bonded partner id " + std::to_string(h.err_id1) +
+          " is out of reach of particle id " + std::to_string(h.err_id0) +
+          " (bond stretched beyond the ghost shell)";
   } else {
     return;
   }
@@ -866,7 +906,11 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
               const tmd_fene_params* fene, const tmd_engine_params* p) {
   auto cfg = [](const std::string& m) { throw StatusError{TMD_ERR_CONFIG, m}; };
   if (!s || !lj || !p) cfg("null argument");
-  if (fene) cfg("FENE bonds are not supported by the GPU path yet");
+  if (fene) {  // validate_fene (potentials.hpp:84-91)
+    if (!(fene->k > 0.0) || !std::isfinite(fene->k)) cfg("fene k must be finite and positive");
+    if (!(fene->r_max > 0.0) || !std::isfinite(fene->r_max))
+      cfg("fene r_max must be finite and positive");
+  }
   for (int k = 0; k < 3; ++k) {
     // validate_box (box.hpp:21-29)
     if (!std::isfinite(s->box[k]) || s->box[k] <= 0.0) {
@@ -908,6 +952,27 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
       if (!(s->mass[k] > 0.0)) {
         cfg("particle id " + std::to_string(s->id[k]) + " has non-positive mass");
       }
+    }
+  }
+  if (!std::isfinite(p->force_cap) || p->force_cap < 0.0) {
+    cfg("force cap must be finite and non-negative");
+  }
+  // topology (validate_topology, topology.hpp:33-52; build_domain,
+  // domain.hpp:145-159)
+  if (s->n_bonds < 0 || (s->n_bonds > 0 && !s->bonds)) cfg("bond array missing");
+  if (s->n_bonds > 0) {
+    for (int64_t k = 0; k < s->n_bonds; ++k) {
+      const int64_t a = s->bonds[2 * k], b = s->bonds[2 * k + 1];
+      const bool ha = std::binary_search(ids.begin(), ids.end(), a);
+      const bool hb = std::binary_search(ids.begin(), ids.end(), b);
+      if (!ha || !hb) {
+        cfg("bond references unknown particle id " + std::to_string(ha ? b : a));
+      }
+      if (a == b) cfg("bond connects particle id " + std::to_string(a) + " to itself");
+    }
+    if (!fene) cfg("topology has bonds but no bond parameters configured");
+    if (fene->r_max > lj->r_cut + p->r_skin) {
+      cfg("bond r_max exceeds r_cut + r_skin; bonded partners could leave the ghost shell");
     }
   }
   // build_domain's sentinel guard (domain.hpp:162-168), kept for parity of
@@ -1136,6 +1201,14 @@ void grow_capacity(tmd_gpu_ctx* c, int64_t need) {
   regrow(c->ck_mass, 0); regrow(c->ck_id, 0);
   regrow(c->ck_fx, 0); regrow(c->ck_fy, 0); regrow(c->ck_fz, 0);
   regrow(c->mig_dest, 0); regrow(c->mig_send, 0); regrow(c->mig_recv, 0);
+  regrow(c->bnd_cnt, 0);
+  if (c->bnd_ent) {  // kMaxBonds entries per slot
+    uint32_t* q = dalloc<uint32_t>(nn * kMaxBonds);
+    ck(cudaMemcpy(q, c->bnd_ent, o * kMaxBonds * sizeof(uint32_t), cudaMemcpyDeviceToDevice),
+       "regrow copy");
+    cudaFree(c->bnd_ent);
+    c->bnd_ent = q;
+  }
   for (int s = 0; s < 2; ++s) {
     regrow(c->bidx[s], 0);
     regrow(c->bids[s], 0);
@@ -1189,6 +1262,65 @@ void recut(tmd_gpu_ctx* c, const std::vector<int>& cuts) {
     c->part_ke = dalloc<double>(c->nparts);
   }
   alloc_list(c, c->cap);  // group count changed
+}
+
+// Static bond table by id (the topology never changes): CSR over
+// id - id_min with each bond listed at both ends, the first id of the pair
+// being the anchor (the reference computes a bond in the subnode owning its
+// first particle, bonded.hpp:124-141).
+void setup_bonds(tmd_gpu_ctx* c, const tmd_system* sys, const tmd_fene_params* fene) {
+  const int64_t* idp = sys->id;
+  const long long id_min = *std::min_element(idp, idp + sys->n);
+  const long long id_max = *std::max_element(idp, idp + sys->n);
+  const int64_t span = static_cast<int64_t>(id_max - id_min) + 1;
+  if (span > 4 * sys->n + 1024) {
+    throw StatusError{TMD_ERR_CONFIG,
+                      "bonded systems need particle ids in a dense range (max - min < 4 n)"};
+  }
+  std::vector<int> deg(static_cast<size_t>(span) + 1, 0);
+  for (int64_t k = 0; k < sys->n_bonds; ++k) {
+    ++deg[static_cast<size_t>(sys->bonds[2 * k] - id_min)];
+    ++deg[static_cast<size_t>(sys->bonds[2 * k + 1] - id_min)];
+  }
+  std::vector<int> off(static_cast<size_t>(span) + 1, 0);
+  for (int64_t o = 0; o < span; ++o) {
+    if (deg[static_cast<size_t>(o)] > kMaxBonds) {
+      throw StatusError{TMD_ERR_CONFIG, "particle id " + std::to_string(id_min + o) + " has " +
+                                            std::to_string(deg[static_cast<size_t>(o)]) +
+                                            " bonds; the GPU path allows " +
+                                            std::to_string(kMaxBonds)};
+    }
+    off[static_cast<size_t>(o) + 1] = off[static_cast<size_t>(o)] + deg[static_cast<size_t>(o)];
+  }
+  std::vector<int> nbr(static_cast<size_t>(2 * sys->n_bonds));
+  std::vector<unsigned char> anchor(static_cast<size_t>(2 * sys->n_bonds));
+  std::vector<int> fill(off.begin(), off.end() - 1);
+  for (int64_t k = 0; k < sys->n_bonds; ++k) {  // bond order kept at each end
+    const int64_t a = sys->bonds[2 * k] - id_min, b = sys->bonds[2 * k + 1] - id_min;
+    const int pa = fill[static_cast<size_t>(a)]++, pb = fill[static_cast<size_t>(b)]++;
+    nbr[static_cast<size_t>(pa)] = static_cast<int>(b);
+    anchor[static_cast<size_t>(pa)] = 1;
+    nbr[static_cast<size_t>(pb)] = static_cast<int>(a);
+    anchor[static_cast<size_t>(pb)] = 0;
+  }
+  c->id_min = id_min;
+  c->id_span = span;
+  c->slot_of_id = dalloc<int>(static_cast<size_t>(span));
+  c->bond_off = dalloc<int>(off.size());
+  c->bond_nbr = dalloc<int>(nbr.size());
+  c->bond_anchor = dalloc<unsigned char>(anchor.size());
+  c->bnd_cnt = dalloc<int>(static_cast<size_t>(c->n_cap));
+  c->bnd_ent = dalloc<uint32_t>(static_cast<size_t>(c->n_cap) * kMaxBonds);
+  ck(cudaMemcpy(c->bond_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice),
+     "H2D bond offsets");
+  ck(cudaMemcpy(c->bond_nbr, nbr.data(), nbr.size() * sizeof(int), cudaMemcpyHostToDevice),
+     "H2D bond partners");
+  ck(cudaMemcpy(c->bond_anchor, anchor.data(), anchor.size(), cudaMemcpyHostToDevice),
+     "H2D bond anchors");
+  ck(cudaMemset(c->bnd_cnt, 0, sizeof(int) * static_cast<size_t>(c->n_cap)), "memset");
+  c->bt.on = 1;
+  c->bt.k = fene->k;
+  c->bt.rmax2 = fene->r_max * fene->r_max;  // fene_eval (potentials.hpp:98)
 }
 
 int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_params* fene,
@@ -1260,9 +1392,15 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->th.temperature = params->temperature;
     c->th.dt = params->dt;
     c->th.seed = params->seed;
+    c->lj.fcap = params->force_cap;
     c->variant = (params->reserved[0] >= 1 && params->reserved[0] <= 3) ? params->reserved[0]
                                                                        : kDefaultVariant;
     if (nranks > 1) c->variant = 3;  // slab mode runs the brick build + global-slot forces
+    if (sys->n_bonds > 0 && c->variant == 2) c->variant = 3;  // bonds: global-slot kernels
+    if (params->force_cap > 0.0) {
+      if (nranks > 1) throw StatusError{TMD_ERR_CONFIG, "force cap: single-GPU warm-up only"};
+      c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
+    }
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
     setup_bricks(c, static_cast<double>(sys->n), lj->r_cut + params->r_skin);
     if (nranks > 1) {  // groups of the owned particles only (+ migration headroom)
@@ -1357,6 +1495,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     ck(cudaMemcpy(c->posb[0] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
     ck(cudaMemcpy(c->posb[1] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
     if (nranks > 1) alloc_slab(c);
+    if (sys->n_bonds > 0) setup_bonds(c, sys, fene);
 
     c->auto_cap = params->nbr_capacity <= 0;
     // Initial capacity: the expected count at this density (27 cells worth

@@ -116,6 +116,64 @@ int tmd_gen_fcc(int cells, double rho, double offset, std::int64_t* id,
   return TMD_OK;
 }
 
+// Kremer-Grest melt (BASELINE.json configs[2]; the reference has only ring
+// melts, gen_polymer_melt in generators.hpp:137-210): linear random-walk
+// chains with fixed bond length, no immediate back-folding (bead k+2 at least
+// one sigma from bead k), first beads uniform in the cubic box
+// L = (N/rho)^(1/3); positions wrapped (box.hpp:47-51). Draws come from the
+// reference's counter RNG under kPlacement keyed (chain, bead << 6 | try).
+int tmd_gen_chains(std::int64_t n_chains, std::int64_t chain_len, double rho, double bond,
+                   std::uint64_t seed, std::int64_t* id, double* pos, std::int64_t* bonds,
+                   double box[3]) {
+  if (n_chains < 1 || chain_len < 1 || !(rho > 0.0) || !(bond > 0.0)) return TMD_ERR_CONFIG;
+  const std::uint64_t kPlacement = 3;
+  const std::int64_t n = n_chains * chain_len;
+  const double L = std::cbrt(static_cast<double>(n) / rho);
+  auto wrap = [L](double p) {
+    double r = p - L * std::floor(p / L);
+    if (r >= L) r -= L;
+    return r;
+  };
+  std::int64_t nb = 0;
+  for (std::int64_t c = 0; c < n_chains; ++c) {
+    double prev2[3] = {0, 0, 0}, prev[3] = {0, 0, 0};
+    for (std::int64_t k = 0; k < chain_len; ++k) {
+      double x[3];
+      if (k == 0) {
+        double u[3];
+        tmd_counter_uniform3(seed, kPlacement, static_cast<std::uint64_t>(c), 0, u);
+        for (int a = 0; a < 3; ++a) x[a] = u[a] * L;
+      } else {
+        for (int attempt = 0; attempt < 64; ++attempt) {
+          double g[3];
+          tmd_counter_normal3(seed, kPlacement, static_cast<std::uint64_t>(c),
+                              (static_cast<std::uint64_t>(k) << 6) | attempt, g);
+          const double gn = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+          if (!(gn > 1e-12)) continue;
+          for (int a = 0; a < 3; ++a) x[a] = prev[a] + bond * (g[a] / gn);
+          if (k < 2) break;
+          const double d0 = x[0] - prev2[0], d1 = x[1] - prev2[1], d2 = x[2] - prev2[2];
+          if (d0 * d0 + d1 * d1 + d2 * d2 >= 1.0) break;
+        }
+      }
+      const std::int64_t i = c * chain_len + k;
+      id[i] = i;
+      for (int a = 0; a < 3; ++a) pos[3 * i + a] = wrap(x[a]);
+      if (k > 0) {
+        bonds[2 * nb] = i - 1;
+        bonds[2 * nb + 1] = i;
+        ++nb;
+      }
+      for (int a = 0; a < 3; ++a) {
+        prev2[a] = prev[a];
+        prev[a] = x[a];
+      }
+    }
+  }
+  box[0] = box[1] = box[2] = L;
+  return TMD_OK;
+}
+
 int tmd_gpu_abi_version(void) { return TMD_GPU_ABI_VERSION; }
 
 }  // extern "C"

@@ -37,6 +37,17 @@ __device__ __forceinline__ void kick(double& v, double f, double inv_m,
 // reports after the step). Arithmetic order mirrors the reference.
 enum : int { kForcesOnly = 0, kKick2 = 1, kFused = 2 };
 
+// FENE bonds resolved to slots (row f1): per owned slot up to kMaxBonds
+// entries packed like list entries — partner slot (low 25 bits), the
+// periodic image of the bond's second particle b as seen from its anchor a
+// (bits 25-30, same codes), bit 31 set when this slot is the partner b.
+struct BondTab {
+  int on;
+  const int* cnt;          // [n_cap] bonds per slot
+  const uint32_t* ent;     // [n_cap * kMaxBonds]
+  double k, rmax2;         // FeneParams k, r_max^2 (potentials.hpp:77-104)
+};
+
 struct Integ {
   double* vx;
   double* vy;
@@ -48,7 +59,56 @@ struct Integ {
   double dt, half_dt;
   double* part_ke;
   Thermo th;  // Langevin bath (off: NVE)
+  BondTab bt; // FENE bonds (off: LJ only)
 };
+
+// FENE forces of slot i (compute_bonded_forces, bonded.hpp:167-199): the bond
+// vector is always the anchor's, d = x_a - (x_b + s), so both ends round it
+// identically and receive exactly opposite forces; each end books the
+// energy -0.5 k r_max^2 log(1 - r^2/r_max^2) and the virial ff r^2 (halved
+// with the pair sums at the reduction).
+__device__ __forceinline__ void bond_accumulate(int i, const double4& pi,
+                                                const double4* __restrict__ pos,
+                                                const BondTab& bt, const Geom& g,
+                                                const long long* __restrict__ id, Ctrl* ctrl,
+                                                double& ax, double& ay, double& az, double& e,
+                                                double& w) {
+  const int nb = bt.cnt[i];
+  for (int k = 0; k < nb; ++k) {
+    const uint32_t ent = bt.ent[static_cast<size_t>(i) * kMaxBonds + k];
+    const int j = static_cast<int>(ent & kIdxMask);
+    const double4 pj = pos[j];
+    const bool anchor = (ent & kFlagIUpper) == 0u;
+    const double4& pa = anchor ? pi : pj;
+    const double4& pb = anchor ? pj : pi;
+    const double sx = image_shift((ent >> 25) & 3u, g.L[0]);
+    const double sy = image_shift((ent >> 27) & 3u, g.L[1]);
+    const double sz = image_shift((ent >> 29) & 3u, g.L[2]);
+    const double dx = __dsub_rn(pa.x, __dadd_rn(pb.x, sx));
+    const double dy = __dsub_rn(pa.y, __dadd_rn(pb.y, sy));
+    const double dz = __dsub_rn(pa.z, __dadd_rn(pb.z, sz));
+    const double r2 = exact_r2(dx, dy, dz);
+    if (!(r2 < bt.rmax2)) {
+      record_error(ctrl, kStatBondStretch, anchor ? id[i] : id[j], anchor ? id[j] : id[i], r2);
+      continue;
+    }
+    const double gq = __dsub_rn(1.0, __ddiv_rn(r2, bt.rmax2));
+    const double ff = __ddiv_rn(-bt.k, gq);
+    // both ends book the (identically rounded) energy and virial: the full-
+    // list partial sums are halved at the reduction
+    e += __dmul_rn(__dmul_rn(__dmul_rn(-0.5, bt.k), bt.rmax2), log(gq));
+    w += ff * r2;
+    if (anchor) {
+      ax += ff * dx;
+      ay += ff * dy;
+      az += ff * dz;
+    } else {
+      ax -= ff * dx;
+      ay -= ff * dy;
+      az -= ff * dz;
+    }
+  }
+}
 
 // Closing half-kick (+ Langevin force, which then stays in the stored force
 // like the reference's st.fx += lf) and, for kFused, the next step's opening
@@ -137,6 +197,69 @@ __global__ void __launch_bounds__(kBlock)
   if ((threadIdx.x & 31) == 0 && d2 > 0.0) {
     atomicMax(&ctrl->max_d2, static_cast<unsigned long long>(__double_as_longlong(d2)));
   }
+}
+
+// ---------------------------------------------------------------------------
+// Bond resolution at a rebuild (resolve_bonded, bonded.hpp:78-162): ids ->
+// current slots through a dense id table, the partner's closest periodic image
+// fixed until the next resort.
+
+__global__ void __launch_bounds__(kBlock)
+    k_fill_int(int n, int* __restrict__ a, int v, const Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_slot_of_id(int n_slots, const long long* __restrict__ id, long long id_min,
+                 int* __restrict__ slot_of_id, const Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  if (s < n_slots) slot_of_id[id[s] - id_min] = s;
+}
+
+__device__ __forceinline__ uint32_t closest_image_code(double xa, double xb, double L) {
+  // the copy of b closest to a among x_b, x_b + L, x_b - L (bonded.hpp:46-73)
+  const double t0 = fabs(__dsub_rn(xa, xb));
+  const double t1 = fabs(__dsub_rn(xa, __dadd_rn(xb, L)));
+  const double t2 = fabs(__dsub_rn(xa, __dadd_rn(xb, -L)));
+  if (t1 < t0 && t1 <= t2) return 1u;
+  if (t2 < t0 && t2 < t1) return 2u;
+  return 0u;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_bond_resolve(int n, const double4* __restrict__ pos, const long long* __restrict__ id,
+                   long long id_min, const int* __restrict__ bond_off,
+                   const int* __restrict__ bond_nbr, const unsigned char* __restrict__ bond_anchor,
+                   const int* __restrict__ slot_of_id, Geom g, int* __restrict__ cnt,
+                   uint32_t* __restrict__ ent, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n) return;
+  const long long o = id[i] - id_min;
+  const int b0 = bond_off[o], b1 = bond_off[o + 1];
+  const double4 pi = pos[i];
+  int c = 0;
+  for (int b = b0; b < b1; ++b) {
+    const int p = slot_of_id[bond_nbr[b]];
+    if (p < 0) {
+      record_error(ctrl, kStatBondReach, id[i], id_min + bond_nbr[b]);
+      continue;
+    }
+    const double4 pp = pos[p];
+    const bool anchor = bond_anchor[b] != 0;
+    const double4& pa = anchor ? pi : pp;
+    const double4& pb = anchor ? pp : pi;
+    const uint32_t code = closest_image_code(pa.x, pb.x, g.L[0]) |
+                          (closest_image_code(pa.y, pb.y, g.L[1]) << 2) |
+                          (closest_image_code(pa.z, pb.z, g.L[2]) << 4);
+    ent[static_cast<size_t>(i) * kMaxBonds + c] =
+        static_cast<uint32_t>(p) | (code << 25) | (anchor ? 0u : kFlagIUpper);
+    ++c;
+  }
+  cnt[i] = c;
 }
 
 // Langevin force of the initial evaluation (compute_forces_untimed,
@@ -524,7 +647,11 @@ __global__ void __launch_bounds__(kBlock)
         const double ri2 = rcp_nr(r2);
         const double inv = lj.sigma2 * ri2;
         const double i6 = inv * inv * inv;
-        const double ff = lj.eps24 * (2.0 * i6 * i6 - i6) * ri2;
+        double ff = lj.eps24 * (2.0 * i6 * i6 - i6) * ri2;
+        if (lj.fcap > 0.0) {  // overlap warm-up: |F| <= fcap (energy left uncapped)
+          const double r = sqrt(r2);
+          if (fabs(ff) * r > lj.fcap) ff = copysign(lj.fcap / r, ff);
+        }
         e += lj.eps4 * (i6 * i6 - i6) - lj.shift;
         w += ff * r2;
         ax += ff * dx;
@@ -532,6 +659,7 @@ __global__ void __launch_bounds__(kBlock)
         az += ff * dz;
       }
     }
+    if (it.bt.on) bond_accumulate(i, pi, pos, it.bt, g, id, ctrl, ax, ay, az, e, w);
     integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
     fx[i] = ax;
     fy[i] = ay;

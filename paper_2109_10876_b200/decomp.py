@@ -47,7 +47,8 @@ import numpy as np
 
 from . import _abi
 from .engine import (ConfigError, EngineConfig, FlatConfig, Interactions, StepObservables,
-                     _check, _engine_params, _ptr, validate_engine_config)
+                     _check, _engine_params, _interactions, _ptr, _system,
+                     validate_engine_config)
 
 # message tags (both ends of a transfer agree on them; NCCL matches by order)
 TAG_MIGRATE = 100
@@ -133,25 +134,16 @@ class SlabContext:
     def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
                  cfg: EngineConfig, rank: int, nranks: int, device: int):
         validate_engine_config(cfg)
-        if inter.fene is not None or inter.angle is not None:
-            raise ConfigError("bonded terms are not on the GPU path yet (SURVEY §8f)")
         L = _abi.lib()
         self._keep = flat
-        sys = _abi.TmdSystem()
-        sys.box[:] = list(flat.box)
-        sys.n = flat.size()
-        sys.id = _ptr(flat.id)
-        sys.type = _ptr(flat.type)
-        sys.mass = _ptr(flat.mass)
-        sys.pos = _ptr(flat.pos)
-        sys.vel = _ptr(flat.vel)
-        lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
-                              1 if inter.lj.energy_shifted else 0)
+        sys = _system(flat)
+        lj, fene = _interactions(inter)
         p = _engine_params(cfg, r_skin, device)
         p.section_timers = 0
         p.reserved[0] = 0
         h = C.c_void_p()
-        _check(L.tmd_gpu_create_slab(C.byref(sys), C.byref(lj), None, C.byref(p),
+        _check(L.tmd_gpu_create_slab(C.byref(sys), C.byref(lj),
+                                     C.byref(fene) if fene else None, C.byref(p),
                                      int(rank), int(nranks), C.byref(h)), None)
         self._h = h
         self.rank, self.nranks, self.device = rank, nranks, device

@@ -136,6 +136,9 @@ class EngineConfig:
     # 2x LDG.128 gathers; 2 = brick-staged shared memory; 3 = sector-chunked
     # list + 256-bit LDG gathers
     variant: int = 0
+    # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
+    # polymer melt, BASELINE configs[2]); 0 = off
+    force_cap: float = 0.0
 
 
 @dataclass
@@ -156,6 +159,7 @@ class FlatConfig:
     vel: np.ndarray
     mass: Optional[np.ndarray] = None
     type: Optional[np.ndarray] = None
+    bonds: Optional[np.ndarray] = None   # Topology::bonds as (n_bonds, 2) ids
 
     def __post_init__(self):
         self.box = np.ascontiguousarray(self.box, dtype=np.float64).reshape(3)
@@ -168,6 +172,8 @@ class FlatConfig:
             self.mass = np.ascontiguousarray(self.mass, dtype=np.float64)
         if self.type is not None:
             self.type = np.ascontiguousarray(self.type, dtype=np.int32)
+        if self.bonds is not None:
+            self.bonds = np.ascontiguousarray(self.bonds, dtype=np.int64).reshape(-1, 2)
 
     def size(self) -> int:
         return int(self.id.shape[0])
@@ -189,6 +195,8 @@ def validate_engine_config(c: EngineConfig) -> None:
         raise ConfigError("worker_threads must be at least 1")
     if c.observable_stride < 1:
         raise ConfigError("observable stride must be at least 1")
+    if not np.isfinite(c.force_cap) or c.force_cap < 0.0:
+        raise ConfigError("force cap must be finite and non-negative")
     if c.thermostat is not None:
         validate_langevin(c.thermostat)
 
@@ -201,6 +209,32 @@ def validate_langevin(p: LangevinParams) -> None:
         raise ConfigError("langevin temperature must be finite and >= 0")
 
 
+def _system(flat: FlatConfig) -> "_abi.TmdSystem":
+    sys = _abi.TmdSystem()
+    sys.box[:] = list(flat.box)
+    sys.n = flat.size()
+    sys.id = _ptr(flat.id)
+    sys.type = _ptr(flat.type)
+    sys.mass = _ptr(flat.mass)
+    sys.pos = _ptr(flat.pos)
+    sys.vel = _ptr(flat.vel)
+    if flat.bonds is not None and len(flat.bonds):
+        sys.n_bonds = int(flat.bonds.shape[0])
+        sys.bonds = _ptr(flat.bonds)
+    return sys
+
+
+def _interactions(inter: Interactions):
+    if inter.angle is not None:
+        raise ConfigError("angle terms are not on the GPU LJ path")
+    lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
+                          1 if inter.lj.energy_shifted else 0)
+    fene = None
+    if inter.fene is not None:
+        fene = _abi.TmdFeneParams(float(inter.fene.k), float(inter.fene.r_max))
+    return lj, fene
+
+
 def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEngineParams":
     p = _abi.TmdEngineParams()
     p.dt = cfg.dt
@@ -209,6 +243,7 @@ def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEn
     p.section_timers = 1 if cfg.section_timers else 0
     p.nbr_capacity = cfg.nbr_capacity
     p.reserved[0] = int(cfg.variant)
+    p.force_cap = float(cfg.force_cap)
     if cfg.thermostat is not None:
         p.thermostat = 1
         p.gamma = float(cfg.thermostat.gamma)
@@ -228,27 +263,16 @@ class Engine:
                  cfg: Optional[EngineConfig] = None):
         cfg = cfg or EngineConfig()
         validate_engine_config(cfg)
-        if inter.angle is not None:
-            raise ConfigError("angle terms are not on the GPU LJ path")
-        if inter.fene is not None:
-            raise ConfigError("FENE bonds are not on the GPU path yet (SURVEY §8f row f1)")
         L = _abi.lib()
         self._cfg = cfg
         self._n = flat.size()
         self._keep = flat
-        sys = _abi.TmdSystem()
-        sys.box[:] = list(flat.box)
-        sys.n = self._n
-        sys.id = _ptr(flat.id)
-        sys.type = _ptr(flat.type)
-        sys.mass = _ptr(flat.mass)
-        sys.pos = _ptr(flat.pos)
-        sys.vel = _ptr(flat.vel)
-        lj = _abi.TmdLjParams(inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
-                              1 if inter.lj.energy_shifted else 0)
+        sys = _system(flat)
+        lj, fene = _interactions(inter)
         p = _engine_params(cfg, r_skin, cfg.device)
         h = C.c_void_p()
-        rc = L.tmd_gpu_create(C.byref(sys), C.byref(lj), None, C.byref(p), C.byref(h))
+        rc = L.tmd_gpu_create(C.byref(sys), C.byref(lj), C.byref(fene) if fene else None,
+                              C.byref(p), C.byref(h))
         _check(rc, None)
         self._h = h
         self.box = flat.box.copy()
@@ -319,7 +343,8 @@ class Engine:
         vel = np.empty((n, 3))
         _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), None),
                self._h)
-        return FlatConfig(self.box.copy(), ids, pos, vel)
+        bonds = None if self._keep.bonds is None else self._keep.bonds.copy()
+        return FlatConfig(self.box.copy(), ids, pos, vel, bonds=bonds)
 
     def forces(self):
         """(ids, forces) of the last evaluation, sorted by id."""
@@ -397,6 +422,54 @@ def gen_fcc(cells: int, rho: float, temperature: float, seed: int,
     vel = np.empty((n, 3))
     L.tmd_thermal_velocities(n, _ptr(ids), None, float(temperature), int(seed), _ptr(vel))
     return FlatConfig(box, ids, pos, vel)
+
+
+def gen_chains(n_chains: int, chain_len: int, rho: float = 0.85, bond: float = 0.97,
+               seed: int = 1, temperature: float = 1.0) -> FlatConfig:
+    """Kremer-Grest melt shape (BASELINE.json configs[2]): linear random-walk
+    chains, bond length 0.97, bead density 0.85 (tmd_gen_chains), with
+    thermal velocities at `temperature`. Overlapping beads need the
+    force-capped warm-up (`kg_warmup`) before NVE."""
+    L = _abi.lib()
+    n = int(n_chains) * int(chain_len)
+    ids = np.empty(n, np.int64)
+    pos = np.empty((n, 3))
+    bonds = np.empty((max(0, n_chains * (chain_len - 1)), 2), np.int64)
+    box = np.empty(3)
+    rc = L.tmd_gen_chains(int(n_chains), int(chain_len), float(rho), float(bond), int(seed),
+                          _ptr(ids), _ptr(pos), _ptr(bonds), _ptr(box))
+    if rc != 0:
+        raise ConfigError("chain generator: n_chains, chain_len >= 1, rho, bond > 0 required")
+    f = FlatConfig(box, ids, pos, None, bonds=bonds)
+    thermal_velocities(f, temperature, seed)
+    return f
+
+
+def kg_interactions() -> Interactions:
+    """Kremer-Grest: WCA (LJ cut at 2^(1/6) sigma, shifted) + FENE K=30, R0=1.5."""
+    return Interactions(lj=LjParams(1.0, 1.0, 2.0 ** (1.0 / 6.0), True),
+                        fene=FeneParams(30.0, 1.5))
+
+
+def kg_warmup(flat: FlatConfig, r_skin: float = 0.4, caps=(5.0, 10.0, 20.0, 50.0, 100.0,
+              300.0, 1000.0), steps_per_cap: int = 200, dt: float = 0.002,
+              equilibrate_steps: int = 2000, equilibrate_dt: float = 0.005,
+              temperature: float = 1.0, seed: int = 7, device: int = -1) -> FlatConfig:
+    """Overlap-capped warm-up of a fresh melt (new; the reference has none,
+    SURVEY §8c): Langevin dynamics (gamma = 1) with the LJ pair force capped at
+    each value of `caps` in turn, then `equilibrate_steps` uncapped Langevin
+    steps that carry off the heat the overlaps released. Returns the relaxed
+    snapshot (bonds kept)."""
+    cur = flat
+    stages = [(float(c), steps_per_cap, dt) for c in caps]
+    stages.append((0.0, equilibrate_steps, equilibrate_dt))
+    for k, (cap, steps, h) in enumerate(stages):
+        cfg = EngineConfig(dt=h, device=device, section_timers=False, force_cap=cap,
+                           thermostat=LangevinParams(1.0, temperature, seed + k))
+        with Engine(cur, kg_interactions(), r_skin, cfg) as eng:
+            eng.run(steps)
+            cur = eng.flatten()
+    return cur
 
 
 def gen_fcc_slab(cells: int, rho: float, temperature: float, seed: int,

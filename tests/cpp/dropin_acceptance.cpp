@@ -132,6 +132,45 @@ int main() {
     verdict("Langevin bath, 30 steps vs reference", ids && worst <= 1e-9,
             "max state spread " + std::to_string(worst));
   }
+  // FENE chains (Kremer-Grest interactions): boustrophedon chains on a
+  // jittered lattice, the reference's Topology + FeneParams through both
+  // engines, 50 steps
+  {
+    FlatConfig flat = gen_lattice(1000, 0.85, 1.0, 5);
+    // one chain per z plane of the 10^3 lattice (ids x-fastest), snaking in y
+    for (int z = 0; z < 10; ++z) {
+      for (int j = 0; j + 1 < 100; ++j) {
+        auto at = [z](int k) {
+          const int y = k / 10, xi = k % 10, x = (y % 2 == 0) ? xi : 9 - xi;
+          return static_cast<std::int64_t>(x + 10 * (y + 10 * z));
+        };
+        flat.topo.bonds.push_back({at(j), at(j + 1)});
+      }
+    }
+    Interactions inter = lj_only();
+    inter.lj.r_cut = std::pow(2.0, 1.0 / 6.0);
+    inter.fene = FeneParams{30.0, 1.5};
+    EngineConfig cfg;
+    cfg.dt = 0.004;
+    cfg.n_sub = 8;
+    Engine ref(build_domain(flat, inter, 0.4, 8), cfg);
+    ref.run(50);
+    const FlatConfig a = flatten_domain(ref.domain());
+    taskmd_gpu::Engine g(flat, inter, 0.4, cfg);
+    g.run(50);
+    const FlatConfig b = g.flatten();
+    double worst = 0.0;
+    bool ids = a.id == b.id && b.topo.bonds.size() == flat.topo.bonds.size();
+    for (std::size_t k = 0; ids && k < a.size(); ++k) {
+      worst = std::max({worst, std::abs(a.pos[k].x - b.pos[k].x),
+                        std::abs(a.pos[k].y - b.pos[k].y), std::abs(a.pos[k].z - b.pos[k].z)});
+    }
+    const double pe_a = ref.potential_energy(), pe_b = g.potential_energy();
+    verdict("FENE chains (KG), 50 steps vs reference",
+            ids && worst <= 1e-9 && std::abs(pe_a - pe_b) <= 1e-10 * std::abs(pe_a),
+            "max position spread " + std::to_string(worst) + ", PE " + std::to_string(pe_a) +
+                " / " + std::to_string(pe_b));
+  }
   // criterion 3: NVE drift, N=4000 SC lattice, seed 3, T=0.6
   {
     const FlatConfig flat = gen_lattice(4000, 0.8442, 0.6, 3);

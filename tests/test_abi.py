@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
     assert sorted(_abi.EXPORTS) == names
-    assert L.tmd_gpu_abi_version() == 2
+    assert L.tmd_gpu_abi_version() == 3
 
 
 def test_library_is_sm100a_only():
@@ -87,7 +87,15 @@ def _flat(n=8, box=10.0):
     (lambda f, i, c: setattr(c, "thermostat", E.LangevinParams(gamma=-1.0)), "gamma"),
     (lambda f, i, c: setattr(c, "thermostat", E.LangevinParams(temperature=float("inf"))),
      "temperature"),
-    (lambda f, i, c: setattr(i, "fene", E.FeneParams()), "FENE"),
+    (lambda f, i, c: setattr(f, "bonds", np.array([[0, 1]])), "no bond parameters"),
+    (lambda f, i, c: (setattr(f, "bonds", np.array([[0, 1]])),
+                      setattr(i, "fene", E.FeneParams(30.0, 3.1))), "ghost shell"),
+    (lambda f, i, c: (setattr(f, "bonds", np.array([[0, 999]])),
+                      setattr(i, "fene", E.FeneParams())), "unknown particle id 999"),
+    (lambda f, i, c: (setattr(f, "bonds", np.array([[2, 2]])),
+                      setattr(i, "fene", E.FeneParams())), "to itself"),
+    (lambda f, i, c: setattr(i, "fene", E.FeneParams(k=0.0)), "fene k"),
+    (lambda f, i, c: setattr(c, "force_cap", -1.0), "force cap"),
     (lambda f, i, c: setattr(i, "angle", E.AngleParams()), "angle"),
 ])
 def test_config_errors_raise_before_touching_the_device(mutate, match):
@@ -148,6 +156,7 @@ def test_struct_layouts_match_the_header(tmp_path):
         pytest.skip("no C compiler")
     structs = {
         "tmd_system": _abi.TmdSystem, "tmd_lj_params": _abi.TmdLjParams,
+        "tmd_fene_params": _abi.TmdFeneParams,
         "tmd_engine_params": _abi.TmdEngineParams, "tmd_observables": _abi.TmdObservables,
         "tmd_list_stats": _abi.TmdListStats,
     }

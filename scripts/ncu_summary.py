@@ -53,22 +53,34 @@ def launches(path):
     rows = list(csv.reader(open(path)))
     hdr = None
     agg = collections.defaultdict(list)
+    dram = collections.defaultdict(float)
     for r in rows:
         if r and r[0] == "ID":
             hdr = r
             continue
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
+            name = d.get("Metric Name", "gpu__time_duration.sum")
+            if name.startswith("dram__bytes"):
+                unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(
+                    d["Metric Unit"], 1)
+                dram[d["Kernel Name"].split("(")[0]] += float(
+                    d["Metric Value"].replace(",", "")) * unit
+                continue
+            if name != "gpu__time_duration.sum":
+                continue
             v = float(d["Metric Value"].replace(",", ""))
             u = d["Metric Unit"]
             scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
                      "msecond": 1e3}.get(u, 1.0)
             agg[d["Kernel Name"].split("(")[0]].append(v * scale)
     tot = sum(sum(v) for v in agg.values())
-    print(f"{'kernel':32s} {'n':>5s} {'total us':>10s} {'mean us':>9s} {'max us':>9s} share")
+    print(f"{'kernel':32s} {'n':>5s} {'total us':>10s} {'mean us':>9s} {'max us':>9s} share"
+          f"{'  DRAM MB/launch' if dram else ''}")
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+        extra = f"  {dram[k] / len(v) / 1e6:10.1f}" if dram else ""
         print(f"{k:32s} {len(v):5d} {sum(v):10.1f} {sum(v)/len(v):9.2f} {max(v):9.2f} "
-              f"{sum(v)/tot:6.1%}")
+              f"{sum(v)/tot:6.1%}{extra}")
 
 
 if __name__ == "__main__":

@@ -122,27 +122,76 @@ def dist_env():
 
 def workload(cells: int) -> dict:
     n = 4 * cells ** 3
-    return {"workload": f"LJ fluid FCC {cells}^3x4 (BASELINE.json configs[1])" if cells == 64
-            else f"LJ fluid FCC {cells}^3x4",
+    idx = {20: 0, 64: 1, 160: 4}.get(cells)
+    return {"workload": f"LJ fluid FCC {cells}^3x4" +
+            (f" (BASELINE.json configs[{idx}])" if idx is not None else ""),
             "n_particles": n, "rho": 0.8442, "r_cut": 2.5, "energy_shifted": True,
             "r_skin": 0.3, "temperature": 1.0, "seed": 12345, "dt": 0.005,
             "ensemble": "NVE"}
 
 
+class Workload:
+    """One BASELINE.json configuration: the synthetic system, its interactions
+    and integrator settings, and the reference-engine kwargs for the CPU arm."""
+
+    def __init__(self, kind: str, cells: int):
+        from paper_2109_10876_b200 import engine as E
+        self.kind = kind
+        self.setup_s = 0.0
+        t0 = time.perf_counter()
+        if kind == "lj":
+            self.cfg = workload(cells)
+            self.flat = E.gen_fcc(cells, 0.8442, 1.0, 12345)
+            self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
+            self.ref_kw = {}
+        elif kind == "kg":
+            # configs[2]: 20,000 x 200-bead KG melt (cells scales it: chains = 20000 *
+            # (cells/64)^3), random-walk chains + force-capped Langevin warm-up
+            chains = max(1, round(20000 * (cells / 64) ** 3))
+            raw = E.gen_chains(chains, 200, 0.85, 0.97, seed=12345)
+            self.flat = E.kg_warmup(raw)
+            self.inter, self.r_skin, self.dt = E.kg_interactions(), 0.4, 0.01
+            self.cfg = {"workload": "Kremer-Grest melt (BASELINE.json configs[2])"
+                        if chains == 20000 else "Kremer-Grest melt",
+                        "chains": chains, "beads_per_chain": 200,
+                        "n_particles": self.flat.size(), "rho": 0.85, "bond": 0.97,
+                        "lj": "WCA r_cut 2^(1/6) shifted", "fene": [30.0, 1.5],
+                        "r_skin": 0.4, "dt": 0.01, "ensemble": "NVE",
+                        "warmup": "force-capped Langevin (kg_warmup), untimed"}
+            self.ref_kw = dict(r_cut=2.0 ** (1.0 / 6.0), bonds=self.flat.bonds,
+                               fene=(30.0, 1.5))
+        elif kind == "slab":
+            # configs[3]: 2,097,152 particles, liquid FCC slab in the middle third of
+            # Lz = 3 Lx (81^3-cell block filled in id order, SURVEY §8d)
+            n = 2097152 if cells == 64 else 4 * cells ** 3
+            c = 81 if cells == 64 else cells
+            self.flat = E.gen_fcc_slab(c, 0.8442, 0.7, 12345, n=n)
+            self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
+            self.cfg = {"workload": "LJ liquid-vapour slab (BASELINE.json configs[3])"
+                        if n == 2097152 else "LJ liquid-vapour slab",
+                        "n_particles": n, "rho_liquid": 0.8442, "box": list(self.flat.box),
+                        "temperature": 0.7, "r_cut": 2.5, "r_skin": 0.3, "dt": 0.005,
+                        "ensemble": "NVE"}
+            self.ref_kw = {}
+        else:
+            raise SystemExit(f"unknown config {kind!r}")
+        self.setup_s = time.perf_counter() - t0
+        self.n = self.flat.size()
+
+
 # ----------------------------------------------------------------------------------
-def cpu_reference_run(cells: int, steps_wanted: int, warmup: int, budget_s: float):
+def cpu_reference_run(w: "Workload", steps_wanted: int, warmup: int, budget_s: float):
     """The reference engine (oracle/_ref) on all host cores. Returns
     (particle-steps/s, cores, sample description, steps timed)."""
     from oracle import ref
-    from paper_2109_10876_b200 import engine as E
     if not ref.available():
         ref.build()
-    f = E.gen_fcc(cells, 0.8442, 1.0, 12345)
+    f = w.flat
     cores = os.cpu_count() or 1
     n_sub = 2 * cores
     t0 = time.perf_counter()
-    r = ref.RefEngine(f.box, f.id, f.pos, f.vel, r_skin=0.3, n_sub=n_sub, workers=cores,
-                      dt=0.005)
+    r = ref.RefEngine(f.box, f.id, f.pos, f.vel, r_skin=w.r_skin, n_sub=n_sub, workers=cores,
+                      dt=w.dt, **w.ref_kw)
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
     r.run(max(1, warmup))
@@ -152,7 +201,7 @@ def cpu_reference_run(cells: int, steps_wanted: int, warmup: int, budget_s: floa
     r.run(steps)
     t = time.perf_counter() - t0
     n = f.size()
-    sample = (f"{n}-particle FCC config, {steps} NVE steps (of {steps_wanted} requested) after "
+    sample = (f"{n}-particle {w.kind} config, {steps} NVE steps (of {steps_wanted} requested) after "
               f"build_domain ({t_build:.1f} s, untimed) and {max(1, warmup)} warm-up steps; "
               f"reference taskmd Engine, worker_threads={cores}, n_sub={n_sub} (fixed 2x "
               f"workers), g++ -O3 -DNDEBUG")
@@ -165,14 +214,15 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     try:
-        v, cores, sample, steps = cpu_reference_run(args.cells, args.steps, args.warmup,
+        w = Workload(args.config, args.cells)
+        v, cores, sample, steps = cpu_reference_run(w, args.steps, args.warmup,
                                                     args.ref_budget_s)
     except Exception as e:  # pragma: no cover
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
         return
-    cfg = workload(args.cells)
+    cfg = dict(w.cfg)
     cfg["parallelism"] = "host threads (reference CPU engine)"
-    n = cfg["n_particles"]
+    n = w.n
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
         "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
@@ -197,11 +247,10 @@ def run_ours(args) -> None:
     torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
 
-    cfg_w = workload(args.cells)
-    n = cfg_w["n_particles"]
-    flat = E.gen_fcc(args.cells, 0.8442, 1.0, 12345)
-    ecfg = E.EngineConfig(dt=0.005, section_timers=False, device=dev)
-    eng = E.Engine(flat, E.Interactions(), 0.3, ecfg)
+    w = Workload(args.config, args.cells)
+    cfg_w, n, flat = w.cfg, w.n, w.flat
+    ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
+    eng = E.Engine(flat, w.inter, w.r_skin, ecfg)
 
     eng.run(args.warmup)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
@@ -263,7 +312,7 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     h2d = flat.pos.nbytes + flat.vel.nbytes + flat.id.nbytes
     t0 = time.perf_counter()
-    e2 = E.Engine(flat, E.Interactions(), 0.3, ecfg)
+    e2 = E.Engine(flat, w.inter, w.r_skin, ecfg)
     obs_bytes = 0
     for _ in range(args.steps):
         e2.run(1)
@@ -281,8 +330,7 @@ def run_ours(args) -> None:
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            v, cores, sample, _ = cpu_reference_run(args.cells, args.steps, 2,
-                                                    args.cpu_budget_s)
+            v, cores, sample, _ = cpu_reference_run(w, args.steps, 2, args.cpu_budget_s)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": sample}
         except Exception as e:  # pragma: no cover
@@ -324,14 +372,15 @@ def run_decomposed(args) -> None:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
-    cfg_w = workload(args.cells)
-    n = cfg_w["n_particles"]
-    flat = E.gen_fcc(args.cells, 0.8442, 1.0, 12345)
-    ecfg = E.EngineConfig(dt=0.005, section_timers=False, device=dev)
+    torch.cuda.set_device(dev)
+    w = Workload(args.config, args.cells)  # deterministic: identical on every rank
+    cfg_w, n, flat = w.cfg, w.n, w.flat
+    ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
+    balance = "count" if args.config == "slab" else "static"
 
     def make():
-        return DecomposedEngine(flat, E.Interactions(), 0.3, ecfg, comm=TorchDistComm(),
-                                device_of=lambda r: local)
+        return DecomposedEngine(flat, w.inter, w.r_skin, ecfg, comm=TorchDistComm(),
+                                device_of=lambda r: local, balance=balance)
 
     def max_over_ranks(x: float) -> float:
         t = torch.tensor([x], device="cuda", dtype=torch.float64)
@@ -380,7 +429,7 @@ def run_decomposed(args) -> None:
         return
     cfg = dict(cfg_w)
     cfg.update({"parallelism": f"{ws} z-slabs (spatial decomposition, {args.dist_backend} "
-                               "halo + migration)",
+                               f"halo + migration, {balance} cuts)",
                 "l2": "working set > 126 MB L2 on every rank at 1M / N; no flush",
                 "rebuilds_in_timed_region": rebuilds, "section_timers": False,
                 "rank0_slab": sizes, "exchanged_bytes_rank0": xbytes})
@@ -405,6 +454,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cells", type=int, default=64, help="FCC cells per edge (64 = 1M)")
+    ap.add_argument("--config", choices=["lj", "kg", "slab"], default="lj",
+                    help="lj: FCC LJ fluid (configs[0,1,4] by --cells 20/64/160); kg: "
+                         "Kremer-Grest melt (configs[2]); slab: liquid-vapour slab "
+                         "(configs[3])")
     ap.add_argument("--force-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)

@@ -124,6 +124,9 @@ struct tmd_gpu_ctx {
   // brick-major ordering + variant selection
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
   int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
+  double occupancy = 0.0;     // particle-weighted mean cell occupancy at creation
+  int build_kind = 3;         // variant 3 list build: 3 = warp per cell, 4 = warp per 32 brick
+                              // particles, 5 = thread per particle (sparse cells)
   BrickGeom bg{};
   int* cell_rank = nullptr;       // global cell -> brick-major rank
   int* brick_rank_off = nullptr;  // brick -> first rank (nbricks + 1)
@@ -366,6 +369,8 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
                             static_cast<int>(b)), "smem attr build");
     ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(b)), "smem attr build");
+    ck(cudaFuncSetAttribute(k_build_brick4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(b)), "smem attr build");
     g_build = b;
   }
   if (f > g_force) {
@@ -404,8 +409,13 @@ void launch_build(tmd_gpu_ctx* c) {
     k_build_list<<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->stride, c->cap, c->snap, c->ctrl);
+  } else if (c->variant == 3 && c->build_kind == 5) {
+    k_build_thread<<<c->nblk, kBlock, 0, c->ls>>>(
+        static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
+        c->nnbr, c->cap, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
   } else if (c->variant == 3) {
-    k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
+    auto kern = c->build_kind == 4 ? k_build_brick4<true> : k_build_brick3<true>;
+    kern<<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
   } else {
@@ -986,6 +996,8 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
 // Brick decomposition of the cell grid (bricks of up to 2x2x2 cells), the
 // brick-major cell ranks, staging capacities and the FP32 prefilter band.
 
+constexpr double kBuildCellWarpMin = 12.0;  // mean particles per cell (measured crossover)
+
 void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   BrickGeom& bg = c->bg;
   // bricks tile the OWNED cells (local z offset 1 in slab mode)
@@ -1028,6 +1040,14 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   const int ncell_halo = (bg.B[0] + 2) * (bg.B[1] + 2) * (bg.B[2] + 2);
   const double want = halo + 1.5 * ncell_halo + 6.0 * std::sqrt(halo) + 64.0;
   bg.stage_cap = std::max(256, (static_cast<int>(want) + 31) / 32 * 32);
+  // list build: a warp per cell while cells hold most of a warp, else a warp
+  // per 32 consecutive brick particles (sparse cells, e.g. the KG melt)
+  if (c->build_kind < 3 || c->build_kind > 5) {
+    // occupancy seen by a particle (sum n_c^2 / sum n_c over the initial
+    // cells), so a dense slab in a mostly empty box counts as dense
+    const double occ = c->occupancy > 0.0 ? c->occupancy : per_cell;
+    c->build_kind = occ >= kBuildCellWarpMin ? 3 : 5;
+  }
   // FP32 prefilter band (see DESIGN.md §List build): bound on |r2_f32 - r2_ref|
   // for brick-relative single-precision coordinates, times 4.
   const double cl = std::max({c->g.cell_len[0], c->g.cell_len[1], c->g.cell_len[2]});
@@ -1402,6 +1422,26 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
     }
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
+    c->build_kind = params->reserved[3];  // 0 = by density (setup_bricks)
+    {
+      std::vector<int> occ(static_cast<size_t>(c->g.dims[0]) * c->g.dims[1] * c->g.dims[2], 0);
+      auto coord = [&](double p, int k) {
+        const double w = host_wrap1(p, c->g.L[k]);
+        return std::min(std::max(static_cast<int>(std::floor(w / c->g.cell_len[k])), 0),
+                        c->g.dims[k] - 1);
+      };
+      double s1 = 0.0, s2 = 0.0;
+      for (const int64_t k : sel) {
+        const size_t cl = static_cast<size_t>(coord(sys->pos[3 * k], 0)) +
+                          static_cast<size_t>(c->g.dims[0]) *
+                              (coord(sys->pos[3 * k + 1], 1) +
+                               static_cast<size_t>(c->g.dims[1]) * coord(sys->pos[3 * k + 2], 2));
+        s2 += 2.0 * occ[cl] + 1.0;  // (m+1)^2 - m^2
+        ++occ[cl];
+        s1 += 1.0;
+      }
+      c->occupancy = s1 > 0.0 ? s2 / s1 : 0.0;
+    }
     setup_bricks(c, static_cast<double>(sys->n), lj->r_cut + params->r_skin);
     if (nranks > 1) {  // groups of the owned particles only (+ migration headroom)
       const int64_t want = c->n + c->n / 4 + 1024;

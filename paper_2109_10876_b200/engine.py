@@ -136,6 +136,9 @@ class EngineConfig:
     # 2x LDG.128 gathers; 2 = brick-staged shared memory; 3 = sector-chunked
     # list + 256-bit LDG gathers
     variant: int = 0
+    # list build of variant 3: 0 = by cell occupancy, 3 = warp per cell,
+    # 4 = warp per 32 brick particles (sparse cells)
+    build: int = 0
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off
     force_cap: float = 0.0
@@ -243,6 +246,7 @@ def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEn
     p.section_timers = 1 if cfg.section_timers else 0
     p.nbr_capacity = cfg.nbr_capacity
     p.reserved[0] = int(cfg.variant)
+    p.reserved[3] = int(cfg.build)
     p.force_cap = float(cfg.force_cap)
     if cfg.thermostat is not None:
         p.thermostat = 1

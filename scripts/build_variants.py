@@ -1,0 +1,22 @@
+"""List-build kernels compared (k_build_brick3 = warp per cell, k_build_brick4 =
+warp per 32 brick particles): build ms and identical pair sets.
+python scripts/build_variants.py <lj|kg|slab> <cells>"""
+import sys
+import numpy as np
+sys.path.insert(0, "/root/repo")
+import bench
+from paper_2109_10876_b200 import engine as E
+
+kind, cells = sys.argv[1], int(sys.argv[2])
+w = bench.Workload(kind, cells)
+res = {}
+for b in (3, 4, 5):
+    eng = E.Engine(w.flat, w.inter, w.r_skin, E.EngineConfig(dt=w.dt, build=b,
+                                                               section_timers=False))
+    eng.run(20)
+    ms = eng.time_list_build(5)
+    res[b] = (ms, eng.pairs() if w.n <= 1_100_000 else None, eng.list_stats()["entries"])
+    eng.close()
+    print(f"{kind} cells={cells} n={w.n} build {b}: {ms:.3f} ms, entries {res[b][2]}", flush=True)
+if res[3][1] is not None:
+    print("pair sets identical:", all(np.array_equal(res[3][1], res[b][1]) for b in (4, 5)))

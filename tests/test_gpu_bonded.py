@@ -56,10 +56,10 @@ def test_initial_state_vs_golden(name, variant):
 
 
 @pytest.mark.parametrize("name", SYSTEMS)
-@pytest.mark.parametrize("graphs", [True, False])
-def test_trajectory_vs_golden(name, graphs):
+@pytest.mark.parametrize("graphs,build", [(True, 0), (False, 0), (True, 3)])
+def test_trajectory_vs_golden(name, graphs, build):
     g = load(name)
-    eng = engine(g, section_timers=not graphs)
+    eng = engine(g, section_timers=not graphs, build=build)
     steps = int(g["steps"])
     every = max(1, steps // len(g["trace"]))
     for row in g["trace"]:

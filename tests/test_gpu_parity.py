@@ -24,9 +24,12 @@ def gpu_engine(g, dt=None, **cfg):
 
 
 @pytest.mark.parametrize("name", SYSTEMS)
-def test_initial_state_vs_golden(name):
+@pytest.mark.parametrize("build", [3, 5])
+def test_initial_state_vs_golden(name, build):
+    """build 3: warp-per-cell brick kernel; 5: thread-per-particle kernel (the
+    choice for sparse cells); both must emit the reference's pair set."""
     g = load(name)
-    eng = gpu_engine(g)
+    eng = gpu_engine(g, build=build)
     np.testing.assert_array_equal(eng.pairs(), g["pairs"])
     _, cell = eng.cell_of()
     np.testing.assert_array_equal(cell, g["cell"])
@@ -58,9 +61,10 @@ def test_forces_vs_brute_force_oracle(name):
 
 
 @pytest.mark.parametrize("name", ["jit6_s41_T08", "fcc8_jit", "aniso", "thin"])
-def test_trajectory_vs_golden(name):
+@pytest.mark.parametrize("build", [3, 5])
+def test_trajectory_vs_golden(name, build):
     g = load(name)
-    eng = gpu_engine(g)
+    eng = gpu_engine(g, build=build)
     steps = int(g["steps"])
     every = max(1, steps // len(g["trace"]))
     for row in g["trace"]:

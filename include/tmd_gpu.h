@@ -306,6 +306,16 @@ int tmd_gpu_slab_halo(tmd_gpu_ctx* ctx, void* send[2], void* recv[2]);
  * energy; the caller sums them over ranks. */
 int tmd_gpu_slab_sums(tmd_gpu_ctx* ctx, double out[3]);
 
+/* Brute-force check for the CLI's `verify` (the reference uses
+ * oracle_forces_energy / oracle_pair_set, oracle.hpp:31-160, md_cli.cpp:
+ * 205-306): O(N^2) LJ forces and energy under the minimum-image convention
+ * plus every pair within r_verlet, on the GPU, without cells or lists.
+ * force[3n] in input order; pairs sorted (min id, max id), at most cap;
+ * *n_pairs = the total. Errors: tmd_gpu_last_error(NULL). */
+int tmd_gpu_brute_force(const tmd_system* sys, const tmd_lj_params* lj, double r_verlet,
+                        int device, double* force, double* pe, int64_t* pairs, size_t cap,
+                        size_t* n_pairs);
+
 /* ---- host-side setup helpers (no GPU needed) ----------------------------
  * Synthetic inputs of the BASELINE.json shapes. FCC is absent from the
  * reference (generators.hpp has only simple cubic), see SURVEY §8(d). */
@@ -316,6 +326,18 @@ int tmd_gpu_slab_sums(tmd_gpu_ctx* ctx, double out[3]);
  * 4*cells^3. */
 int tmd_gen_fcc(int cells, double rho, double offset, int64_t* id, double* pos,
                 double box[3]);
+
+/* The reference's generators (generators.hpp), restated for the run-config
+ * front end: gen_lattice (47-81), gen_spherical (83-135; call with id = NULL
+ * first for the count), gen_random (212-258; TMD_ERR_VERIFY = placement
+ * gave up). Velocities thermal at T with zero net momentum. */
+int tmd_gen_lattice(int64_t n, double rho, double temperature, uint64_t seed, int64_t* id,
+                    double* pos, double* vel, double box[3]);
+int tmd_gen_spherical(double box_length, double diameter_fraction, double rho_in, double alpha,
+                      double temperature, uint64_t seed, int64_t* id, double* pos, double* vel,
+                      int64_t* n_out, double box[3]);
+int tmd_gen_random(int64_t n, double rho, double min_distance, double temperature,
+                   uint64_t seed, int64_t* id, double* pos, double* vel, double box[3]);
 
 /* Kremer-Grest melt (BASELINE configs[2]; new — the reference generates
  * only ring melts, generators.hpp:137-210): n_chains linear random-walk

@@ -220,10 +220,34 @@ def bonded_fixtures():
                    trace_every=20, dt=0.004, bonds=bonds, fene=kg_fene)
 
 
+def generator_fixtures():
+    """The reference's generators (generators.hpp) on a few parameter sets:
+    pins the product's restatements used by the run-config front end."""
+    out = {}
+    for tag, (n, rho, t, seed) in {"lat100": (100, 0.8442, 0.72, 3),
+                                   "lat1000": (1000, 0.5, 1.0, 12345),
+                                   "lat9": (9, 0.1, 0.0, 1)}.items():
+        b, i, p, v = ref.gen_lattice(n, rho, t, seed)
+        out.update({f"{tag}_box": b, f"{tag}_ids": i, f"{tag}_pos": p, f"{tag}_vel": v})
+    for tag, (n, rho, dmin, t, seed) in {"rnd200": (200, 0.8442, 0.8, 0.72, 1),
+                                         "rnd50": (50, 0.3, 1.0, 0.0, 99)}.items():
+        b, i, p, v = ref.gen_random(n, rho, dmin, t, seed)
+        out.update({f"{tag}_box": b, f"{tag}_ids": i, f"{tag}_pos": p, f"{tag}_vel": v})
+    for tag, args in {"sph": (14.0, 0.7, 0.8442, 0.1, 0.1, 7),
+                      "sph_full": (9.0, 1.0, 0.6, 1.0, 0.5, 2)}.items():
+        b, i, p, v = ref.gen_spherical(*args)
+        out.update({f"{tag}_box": b, f"{tag}_ids": i, f"{tag}_pos": p, f"{tag}_vel": v})
+    np.savez_compressed(OUT / "generators.npz", **out)
+    print("  generators:", sorted({k.split("_")[0] for k in out}))
+
+
 def main():
     if not ref.available():
         ref.build()
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--only-generators" in sys.argv:
+        generator_fixtures()
+        return
     if "--only-thermostat" in sys.argv:
         thermostat_fixtures()
         return
@@ -315,6 +339,7 @@ def main():
         system_fixture(name, box, ids, pos, vel, n_subs=(1,), steps=50, trace_every=10)
     thermostat_fixtures()
     bonded_fixtures()
+    generator_fixtures()
     # SC lattice 4000 (acceptance criterion 3): energy traces at dt 0.005, 0.001
     b, i, p, v = ref.gen_lattice(4000, 0.8442, 0.6, 3)
     traces = {}

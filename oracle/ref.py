@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         L.ref_thermal_velocities.restype = None
         L.ref_gen_lattice.argtypes = [C.c_int64, D, D, C.c_uint64, P, P, P, P,
                                       C.c_char_p, C.c_int]
+        L.ref_gen_spherical.argtypes = [D, D, D, D, D, C.c_uint64, C.c_int64, P, P, P,
+                                        C.POINTER(C.c_int64), C.c_char_p, C.c_int]
         L.ref_gen_random.argtypes = [C.c_int64, D, D, D, C.c_uint64, P, P, P, P,
                                      C.c_char_p, C.c_int]
         L.ref_oracle_forces.argtypes = [C.c_int64, P, P, P, D, D, D, C.c_int, P,
@@ -286,6 +288,17 @@ def gen_random(n, rho, min_d, temperature, seed):
     _raise(lib().ref_gen_random(n, rho, min_d, temperature, seed, _p(ids), _p(pos), _p(vel),
                                 _p(box), err, 512), err)
     return box, ids, pos, vel
+
+
+def gen_spherical(box_length, frac, rho_in, alpha, temperature, seed):
+    err = C.create_string_buffer(512)
+    n = C.c_int64()
+    _raise(lib().ref_gen_spherical(box_length, frac, rho_in, alpha, temperature, seed, 0, None,
+                                   None, None, C.byref(n), err, 512), err)
+    ids, pos, vel = np.empty(n.value, np.int64), np.empty((n.value, 3)), np.empty((n.value, 3))
+    _raise(lib().ref_gen_spherical(box_length, frac, rho_in, alpha, temperature, seed, n.value,
+                                   _p(ids), _p(pos), _p(vel), C.byref(n), err, 512), err)
+    return np.full(3, float(box_length)), ids, pos, vel
 
 
 def oracle_forces(box, ids, pos, eps=1.0, sigma=1.0, rc=2.5, shifted=True):

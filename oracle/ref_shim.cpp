@@ -419,6 +419,18 @@ int ref_gen_random(std::int64_t n, double rho, double min_d,
   });
 }
 
+// gen_spherical (generators.hpp:87). Arrays sized cap; *n_out = count.
+int ref_gen_spherical(double box_length, double frac, double rho_in, double alpha,
+                      double temperature, std::uint64_t seed, std::int64_t cap,
+                      std::int64_t* id, double* pos, double* vel, std::int64_t* n_out,
+                      char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const FlatConfig f = gen_spherical(box_length, frac, rho_in, alpha, temperature, seed);
+    *n_out = static_cast<std::int64_t>(f.size());
+    if (*n_out <= cap) copy_out_flat(f, id, pos, vel);
+  });
+}
+
 // oracle_forces_energy (oracle.hpp:112): brute-force minimum-image forces in
 // input order and the pair energy.
 int ref_oracle_forces(std::int64_t n, const std::int64_t* id, const double* pos,

@@ -34,7 +34,8 @@ EXPORTS = [
     "tmd_gpu_slab_commit", "tmd_gpu_slab_border", "tmd_gpu_slab_ghost_in",
     "tmd_gpu_slab_ghosts_ready", "tmd_gpu_slab_kick_drift", "tmd_gpu_slab_forces",
     "tmd_gpu_slab_halo", "tmd_gpu_slab_sums", "tmd_gpu_slab_layer_counts",
-    "tmd_gpu_slab_recut", "tmd_gen_chains",
+    "tmd_gpu_slab_recut", "tmd_gen_chains", "tmd_gpu_brute_force", "tmd_gen_lattice",
+    "tmd_gen_spherical", "tmd_gen_random",
 ]
 
 
@@ -146,6 +147,13 @@ def lib() -> C.CDLL:
     L.tmd_gpu_destroy.argtypes = [P]
     L.tmd_gpu_destroy.restype = None
     L.tmd_gen_fcc.argtypes = [C.c_int, C.c_double, C.c_double, P, P, P]
+    L.tmd_gpu_brute_force.argtypes = [C.POINTER(TmdSystem), C.POINTER(TmdLjParams), C.c_double,
+                                      C.c_int, P, P, P, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.tmd_gen_lattice.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_uint64, P, P, P, P]
+    L.tmd_gen_spherical.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                    C.c_uint64, P, P, P, P, P]
+    L.tmd_gen_random.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                 P, P, P, P]
     L.tmd_gen_chains.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_uint64,
                                  P, P, P, P]
     L.tmd_thermal_velocities.argtypes = [C.c_int64, P, P, C.c_double, C.c_uint64, P]

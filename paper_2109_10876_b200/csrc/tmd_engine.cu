@@ -2256,6 +2256,79 @@ int tmd_gpu_slab_sums(tmd_gpu_ctx* c, double out[3]) {
   });
 }
 
+int tmd_gpu_brute_force(const tmd_system* sys, const tmd_lj_params* lj, double r_verlet,
+                        int device, double* force, double* pe, int64_t* pairs, size_t cap,
+                        size_t* n_pairs) {
+  tmd_gpu_ctx tmp;
+  const int rc = guard(&tmp, [&] {
+    if (!sys || !lj || sys->n < 1 || !sys->pos || !sys->id) {
+      throw StatusError{TMD_ERR_CONFIG, "brute force: empty system"};
+    }
+    if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+    const size_t n = static_cast<size_t>(sys->n);
+    LjConst c{};
+    c.sigma2 = lj->sigma * lj->sigma;
+    c.rc2 = lj->r_cut * lj->r_cut;
+    c.eps4 = 4.0 * lj->epsilon;
+    c.eps24 = 24.0 * lj->epsilon;
+    if (lj->energy_shifted) {
+      const double s2 = c.sigma2 / c.rc2, s6 = s2 * s2 * s2;
+      c.shift = c.eps4 * (s6 * s6 - s6);
+    }
+    const int blocks = blocks_for(static_cast<int64_t>(n), kBlock);
+    double* dpos = dalloc<double>(3 * n);
+    long long* did = dalloc<long long>(n);
+    double* dforce = dalloc<double>(3 * n);
+    double* dpart = dalloc<double>(static_cast<size_t>(blocks));
+    unsigned long long* dn = dalloc<unsigned long long>(1);
+    int* dover = dalloc<int>(1);
+    const size_t pcap = std::max<size_t>(cap, 1);
+    long long* dpairs = dalloc<long long>(2 * pcap);
+    ck(cudaMemcpy(dpos, sys->pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(did, sys->id, n * sizeof(long long), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemset(dn, 0, sizeof(unsigned long long)), "memset");
+    ck(cudaMemset(dover, 0, sizeof(int)), "memset");
+    k_brute<<<blocks, kBlock>>>(static_cast<int>(n), dpos, did, sys->box[0], sys->box[1],
+                                sys->box[2], c, r_verlet * r_verlet, dforce, dpart, dn, dpairs,
+                                static_cast<unsigned long long>(cap), dover);
+    ck(cudaGetLastError(), "k_brute");
+    std::vector<double> part(static_cast<size_t>(blocks));
+    unsigned long long np = 0;
+    int over = 0;
+    ck(cudaMemcpy(part.data(), dpart, part.size() * sizeof(double), cudaMemcpyDeviceToHost),
+       "D2H");
+    ck(cudaMemcpy(&np, dn, sizeof np, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(&over, dover, sizeof over, cudaMemcpyDeviceToHost), "D2H");
+    if (force) {
+      ck(cudaMemcpy(force, dforce, 3 * n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    }
+    if (pairs && np > 0) {
+      const size_t m = std::min<size_t>(cap, static_cast<size_t>(np));
+      std::vector<long long> h(2 * m);
+      ck(cudaMemcpy(h.data(), dpairs, 2 * m * sizeof(long long), cudaMemcpyDeviceToHost),
+         "D2H");
+      std::vector<std::pair<int64_t, int64_t>> v(m);
+      for (size_t k = 0; k < m; ++k) v[k] = {h[2 * k], h[2 * k + 1]};
+      std::sort(v.begin(), v.end());
+      for (size_t k = 0; k < m; ++k) {
+        pairs[2 * k] = v[k].first;
+        pairs[2 * k + 1] = v[k].second;
+      }
+    }
+    void* ptrs[] = {dpos, did, dforce, dpart, dn, dover, dpairs};
+    for (void* q : ptrs) cudaFree(q);
+    if (over) throw StatusError{TMD_ERR_PHYSICS, "brute force: overlapping particles"};
+    if (pe) {
+      double t = 0.0;
+      for (double v : part) t += v;
+      *pe = t;
+    }
+    if (n_pairs) *n_pairs = static_cast<size_t>(np);
+  });
+  if (rc != TMD_OK) g_create_error = tmp.err;
+  return rc;
+}
+
 void tmd_gpu_destroy(tmd_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);

@@ -2,6 +2,7 @@
 // velocities and the FCC lattice of the BASELINE.json configs. Plain C++,
 // compiled without FMA contraction (x86-64 baseline), so every value is
 // bit-identical to the reference's own host arithmetic for the same inputs.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -113,6 +114,124 @@ int tmd_gen_fcc(int cells, double rho, double offset, std::int64_t* id,
           pos[3 * k + 2] = (z + basis[b][2] + offset) * a;
         }
   box[0] = box[1] = box[2] = L;
+  return TMD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The reference's own generators (generators.hpp), restated for the run-config
+// front end. Velocities: thermal + zero net momentum
+// (tmd_thermal_velocities) as each generator ends with.
+
+// gen_lattice (generators.hpp:47-81): simple cubic, smallest cube of sites
+// holding n, sites filled x-fastest, spacing = cbrt(n/rho)/side.
+int tmd_gen_lattice(std::int64_t n, double rho, double temperature, std::uint64_t seed,
+                    std::int64_t* id, double* pos, double* vel, double box[3]) {
+  if (n < 1 || !(rho > 0.0) || temperature < 0.0) return TMD_ERR_CONFIG;
+  const double edge = std::cbrt(static_cast<double>(n) / rho);
+  std::int64_t side = 1;
+  while (side * side * side < n) side += 1;
+  const double spacing = edge / static_cast<double>(side);
+  std::int64_t k = 0;
+  for (std::int64_t z = 0; z < side && k < n; ++z)
+    for (std::int64_t y = 0; y < side && k < n; ++y)
+      for (std::int64_t x = 0; x < side && k < n; ++x, ++k) {
+        id[k] = k;
+        pos[3 * k] = (static_cast<double>(x) + 0.5) * spacing;
+        pos[3 * k + 1] = (static_cast<double>(y) + 0.5) * spacing;
+        pos[3 * k + 2] = (static_cast<double>(z) + 0.5) * spacing;
+      }
+  box[0] = box[1] = box[2] = edge;
+  tmd_thermal_velocities(n, id, nullptr, temperature, seed, vel);
+  return TMD_OK;
+}
+
+// gen_spherical (generators.hpp:83-135): lattice sites at rho_in kept inside
+// the central sphere of diameter frac * L, and outside with probability
+// alpha (counter_uniform lane 0 keyed by the site index). Two passes: call
+// with id == NULL to get the count in *n_out.
+int tmd_gen_spherical(double box_length, double frac, double rho_in, double alpha,
+                      double temperature, std::uint64_t seed, std::int64_t* id, double* pos,
+                      double* vel, std::int64_t* n_out, double box[3]) {
+  if (!(box_length > 0.0) || !(frac > 0.0) || frac > 1.0 || !(rho_in > 0.0) || alpha < 0.0 ||
+      alpha > 1.0 || temperature < 0.0) {
+    return TMD_ERR_CONFIG;
+  }
+  const std::uint64_t kPlacement = 3;
+  const double target = std::cbrt(1.0 / rho_in);
+  const std::int64_t side =
+      static_cast<std::int64_t>(std::max(1.0, std::round(box_length / target)));
+  const double spacing = box_length / static_cast<double>(side);
+  const double radius = 0.5 * frac * box_length;
+  const double c = 0.5 * box_length;
+  std::int64_t k = 0;
+  std::uint64_t site = 0;
+  for (std::int64_t z = 0; z < side; ++z)
+    for (std::int64_t y = 0; y < side; ++y)
+      for (std::int64_t x = 0; x < side; ++x, ++site) {
+        const double px = (static_cast<double>(x) + 0.5) * spacing;
+        const double py = (static_cast<double>(y) + 0.5) * spacing;
+        const double pz = (static_cast<double>(z) + 0.5) * spacing;
+        const double dx = px - c, dy = py - c, dz = pz - c;
+        const bool inside = dx * dx + dy * dy + dz * dz <= radius * radius;
+        if (!inside) {
+          double u[3];
+          tmd_counter_uniform3(seed, kPlacement, 0, site, u);
+          if (u[0] >= alpha) continue;
+        }
+        if (id) {
+          id[k] = k;
+          pos[3 * k] = px;
+          pos[3 * k + 1] = py;
+          pos[3 * k + 2] = pz;
+        }
+        ++k;
+      }
+  *n_out = k;
+  box[0] = box[1] = box[2] = box_length;
+  if (id) tmd_thermal_velocities(k, id, nullptr, temperature, seed, vel);
+  return TMD_OK;
+}
+
+// gen_random (generators.hpp:212-258): rejection sampling of uniform
+// positions (counter_uniform3 keyed by attempt and particle) with a minimum
+// minimum-image separation (box.hpp:34-43). TMD_ERR_VERIFY = the reference's
+// "density too high" give-up after 100000 attempts per particle.
+int tmd_gen_random(std::int64_t n, double rho, double min_distance, double temperature,
+                   std::uint64_t seed, std::int64_t* id, double* pos, double* vel,
+                   double box[3]) {
+  if (n < 1 || !(rho > 0.0) || min_distance < 0.0 || temperature < 0.0) return TMD_ERR_CONFIG;
+  const std::uint64_t kPlacement = 3;
+  const double L = std::cbrt(static_cast<double>(n) / rho);
+  const double d2 = min_distance * min_distance;
+  auto mi = [L](double d) {
+    double r = std::remainder(d, L);
+    if (r == 0.5 * L) r = -0.5 * L;
+    return r;
+  };
+  const std::uint64_t max_attempts = 100000ull * static_cast<std::uint64_t>(n);
+  std::uint64_t attempt = 0;
+  for (std::int64_t k = 0; k < n; ++k) {
+    for (;;) {
+      if (attempt >= max_attempts) return TMD_ERR_VERIFY;
+      double u[3];
+      tmd_counter_uniform3(seed, kPlacement, attempt++, static_cast<std::uint64_t>(k), u);
+      const double px = u[0] * L, py = u[1] * L, pz = u[2] * L;
+      bool ok = true;
+      for (std::int64_t j = 0; j < k && ok; ++j) {
+        const double dx = mi(px - pos[3 * j]), dy = mi(py - pos[3 * j + 1]),
+                     dz = mi(pz - pos[3 * j + 2]);
+        if (dx * dx + dy * dy + dz * dz < d2) ok = false;
+      }
+      if (!ok) continue;
+      id[k] = k;
+      pos[3 * k] = px;
+      pos[3 * k + 1] = py;
+      pos[3 * k + 2] = pz;
+      break;
+    }
+  }
+  box[0] = box[1] = box[2] = L;
+  tmd_thermal_velocities(n, id, nullptr, temperature, seed, vel);
   return TMD_OK;
 }
 

@@ -278,6 +278,62 @@ __global__ void __launch_bounds__(kBlock)
   fz[i] = gz;
 }
 
+// ---------------------------------------------------------------------------
+// Brute-force check for `verify` (the role of oracle_forces_energy /
+// oracle_pair_set, oracle.hpp:31-160, in the reference CLI): all pairs under
+// the minimum-image convention (box.hpp:34-43), no cells, no lists — an
+// independent path to compare the list-based engine against.
+__device__ __forceinline__ double min_image1(double d, double L) {
+  double r = remainder(d, L);
+  if (r == 0.5 * L) r = -0.5 * L;
+  return r;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_brute(int n, const double* __restrict__ pos, const long long* __restrict__ id,
+            double Lx, double Ly, double Lz, LjConst lj, double rv2, double* __restrict__ force,
+            double* __restrict__ part_e, unsigned long long* __restrict__ npairs,
+            long long* __restrict__ pairs, unsigned long long cap, int* __restrict__ overlap) {
+  __shared__ double red[kBlock / 32];
+  const int a = blockIdx.x * kBlock + threadIdx.x;
+  double e = 0.0;
+  if (a < n) {
+    const double xa = pos[3 * a], ya = pos[3 * a + 1], za = pos[3 * a + 2];
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    for (int b = 0; b < n; ++b) {
+      if (b == a) continue;
+      const double dx = min_image1(xa - pos[3 * b], Lx);
+      const double dy = min_image1(ya - pos[3 * b + 1], Ly);
+      const double dz = min_image1(za - pos[3 * b + 2], Lz);
+      const double r2 = dx * dx + dy * dy + dz * dz;
+      if (a < b && r2 <= rv2) {
+        const unsigned long long k = atomicAdd(npairs, 1ull);
+        if (k < cap) {
+          pairs[2 * k] = min(id[a], id[b]);
+          pairs[2 * k + 1] = max(id[a], id[b]);
+        }
+      }
+      if (r2 >= lj.rc2) continue;
+      if (r2 == 0.0) {
+        atomicOr(overlap, 1);
+        continue;
+      }
+      const double s2 = lj.sigma2 / r2;
+      const double s6 = s2 * s2 * s2;
+      e += 0.5 * (lj.eps4 * (s6 * s6 - s6) - lj.shift);
+      const double ff = lj.eps24 * (2.0 * s6 * s6 - s6) / r2;
+      fx += ff * dx;
+      fy += ff * dy;
+      fz += ff * dz;
+    }
+    force[3 * a] = fx;
+    force[3 * a + 1] = fy;
+    force[3 * a + 2] = fz;
+  }
+  const double t = block_sum<kBlock>(e, red);
+  if (threadIdx.x == 0) part_e[blockIdx.x] = t;
+}
+
 // Kinetic partials of the current velocities (observe() after setup).
 __global__ void __launch_bounds__(kBlock)
     k_kinetic(int n, const double* __restrict__ vx, const double* __restrict__ vy,

@@ -428,6 +428,91 @@ def gen_fcc(cells: int, rho: float, temperature: float, seed: int,
     return FlatConfig(box, ids, pos, vel)
 
 
+def gen_lattice(n: int, rho: float, temperature: float, seed: int) -> FlatConfig:
+    """gen_lattice (generators.hpp:47-81): simple cubic, x-fastest, tail empty."""
+    if n < 1:
+        raise ConfigError("lattice generator needs at least 1 particle")
+    if not rho > 0.0:
+        raise ConfigError("density must be positive")
+    if temperature < 0.0:
+        raise ConfigError("temperature must be non-negative")
+    ids = np.empty(n, np.int64)
+    pos = np.empty((n, 3))
+    vel = np.empty((n, 3))
+    box = np.empty(3)
+    _abi.lib().tmd_gen_lattice(int(n), float(rho), float(temperature), int(seed), _ptr(ids),
+                               _ptr(pos), _ptr(vel), _ptr(box))
+    return FlatConfig(box, ids, pos, vel)
+
+
+def gen_spherical(box_length: float, diameter_fraction: float, rho_in: float, alpha: float,
+                  temperature: float, seed: int) -> FlatConfig:
+    """gen_spherical (generators.hpp:83-135): dense sphere in a dilute background."""
+    if not box_length > 0.0:
+        raise ConfigError("box length must be positive")
+    if not diameter_fraction > 0.0 or diameter_fraction > 1.0:
+        raise ConfigError("sphere diameter fraction must be in (0, 1]")
+    if not rho_in > 0.0:
+        raise ConfigError("density must be positive")
+    if alpha < 0.0 or alpha > 1.0:
+        raise ConfigError("density factor alpha must be in [0, 1]")
+    if temperature < 0.0:
+        raise ConfigError("temperature must be non-negative")
+    L = _abi.lib()
+    n = C.c_int64()
+    box = np.empty(3)
+    args = (float(box_length), float(diameter_fraction), float(rho_in), float(alpha),
+            float(temperature), int(seed))
+    L.tmd_gen_spherical(*args, None, None, None, C.byref(n), _ptr(box))
+    ids = np.empty(n.value, np.int64)
+    pos = np.empty((n.value, 3))
+    vel = np.empty((n.value, 3))
+    L.tmd_gen_spherical(*args, _ptr(ids), _ptr(pos), _ptr(vel), C.byref(n), _ptr(box))
+    return FlatConfig(box, ids, pos, vel)
+
+
+def gen_random(n: int, rho: float, min_distance: float, temperature: float,
+               seed: int) -> FlatConfig:
+    """gen_random (generators.hpp:212-258): rejection-sampled uniform positions."""
+    if n < 1:
+        raise ConfigError("random generator needs at least 1 particle")
+    if not rho > 0.0:
+        raise ConfigError("density must be positive")
+    if min_distance < 0.0:
+        raise ConfigError("minimum distance must be non-negative")
+    if temperature < 0.0:
+        raise ConfigError("temperature must be non-negative")
+    ids = np.empty(n, np.int64)
+    pos = np.empty((n, 3))
+    vel = np.empty((n, 3))
+    box = np.empty(3)
+    rc = _abi.lib().tmd_gen_random(int(n), float(rho), float(min_distance), float(temperature),
+                                   int(seed), _ptr(ids), _ptr(pos), _ptr(vel), _ptr(box))
+    if rc != 0:
+        raise ConfigError("random placement failed: density too high for the requested "
+                          "minimum distance")
+    return FlatConfig(box, ids, pos, vel)
+
+
+def brute_force(flat: FlatConfig, inter: Interactions, r_verlet: float, device: int = -1):
+    """All-pairs minimum-image LJ forces, PE and pair set on the GPU (the CLI's
+    verify reference; oracle.hpp:31-160's role). Returns (forces in input
+    order, pe, sorted (min id, max id) pairs)."""
+    L = _abi.lib()
+    sys = _system(flat)
+    lj, _ = _interactions(Interactions(lj=inter.lj))
+    n = flat.size()
+    f = np.empty((n, 3))
+    pe = C.c_double()
+    npairs = C.c_size_t()
+    _check(L.tmd_gpu_brute_force(C.byref(sys), C.byref(lj), float(r_verlet), int(device),
+                                 _ptr(f), C.byref(pe), None, 0, C.byref(npairs)), None)
+    pairs = np.empty((max(npairs.value, 1), 2), np.int64)
+    _check(L.tmd_gpu_brute_force(C.byref(sys), C.byref(lj), float(r_verlet), int(device),
+                                 None, None, _ptr(pairs), npairs.value, C.byref(npairs)), None)
+    return f, pe.value, pairs[: npairs.value]
+
+
 def gen_chains(n_chains: int, chain_len: int, rho: float = 0.85, bond: float = 0.97,
                seed: int = 1, temperature: float = 1.0) -> FlatConfig:
     """Kremer-Grest melt shape (BASELINE.json configs[2]): linear random-walk

@@ -588,6 +588,13 @@ __device__ __forceinline__ void flush_chunk(const uint32_t* ring8, uint32_t* dst
   reinterpret_cast<uint4*>(dst)[1] = b;
 }
 
+// Ring append at slot n & 15 of the lane's ring (stride 128 B): one LOP3 and
+// one IMAD on a 32-bit shared-window address.
+__device__ __forceinline__ void ring_put(uint32_t base, int n, uint32_t v) {
+  const uint32_t a = (static_cast<uint32_t>(n) & 15u) * 128u + base;
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 template <bool kGlobal>
 __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
     k_build_brick3(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
@@ -667,6 +674,8 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
       const unsigned long long row = list_slot(gbase + (ib >> 5), bg.cap, ib & 31, 0);
       const float hi2 = active ? bg.hi2 : -1.0f;  // inactive lanes never hit
       const uint32_t lo2m1 = __float_as_uint(bg.lo2) - 1u;
+      const uint32_t rbase =
+          static_cast<uint32_t>(__cvta_generic_to_shared(&s_ring[warp][0][lane]));
       int n = 0;
       for (int oz2 = -1; oz2 <= 1; ++oz2) {
         for (int oy2 = -1; oy2 <= 1; ++oy2) {
@@ -676,45 +685,52 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
             const int first = ox2 != 0 ? ox2 : (oy2 != 0 ? oy2 : oz2);
             const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
             const int kb = s_off[h], ke = kb + s_cnt[h];
+            // four candidates per iteration: cell blocks are padded to a
+            // multiple of 4 slots with far-away coordinates (never hits)
 #pragma unroll 1
-            for (int k = kb; k < ke; k += 2) {
-              const float2 X = *reinterpret_cast<const float2*>(nx + k);
-              const float2 Y = *reinterpret_cast<const float2*>(ny + k);
-              const float2 Z = *reinterpret_cast<const float2*>(nz + k);
-              const float2 dx = __fadd2_rn(xi2, X), dy = __fadd2_rn(yi2, Y),
-                           dz = __fadd2_rn(zi2, Z);
-              const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-              bool h0 = r2.x <= hi2;
-              bool h1 = r2.y <= hi2;  // slot k+1 past the cell is padding: far, no hit
-              // sure hit <=> 0 < r2 < lo2: one unsigned compare on the bit pattern
-              // (non-negative floats order like their bits)
-              const bool band0 = h0 && (__float_as_uint(r2.x) - 1u) >= lo2m1;
-              const bool band1 = h1 && (__float_as_uint(r2.y) - 1u) >= lo2m1;
-              if (band0 || band1) {  // exact FP64 decision (reference rounding) + self
+            for (int k = kb; k < ke; k += 4) {
+              const float4 X = *reinterpret_cast<const float4*>(nx + k);
+              const float4 Y = *reinterpret_cast<const float4*>(ny + k);
+              const float4 Z = *reinterpret_cast<const float4*>(nz + k);
+              const float2 dxa = __fadd2_rn(xi2, f2(X.x, X.y)), dxb = __fadd2_rn(xi2, f2(X.z, X.w));
+              const float2 dya = __fadd2_rn(yi2, f2(Y.x, Y.y)), dyb = __fadd2_rn(yi2, f2(Y.z, Y.w));
+              const float2 dza = __fadd2_rn(zi2, f2(Z.x, Z.y)), dzb = __fadd2_rn(zi2, f2(Z.z, Z.w));
+              const float2 ra = __ffma2_rn(dza, dza, __ffma2_rn(dya, dya, __fmul2_rn(dxa, dxa)));
+              const float2 rb = __ffma2_rn(dzb, dzb, __ffma2_rn(dyb, dyb, __fmul2_rn(dxb, dxb)));
+              const float r2v[4] = {ra.x, ra.y, rb.x, rb.y};
+              bool hit[4];
+              bool band[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                hit[u] = r2v[u] <= hi2;
+                // sure hit <=> 0 < r2 < lo2 (unsigned compare on the bits)
+                band[u] = hit[u] && (__float_as_uint(r2v[u]) - 1u) >= lo2m1;
+              }
+              if (band[0] || band[1] || band[2] || band[3]) {  // exact FP64 (+ self)
                 const double4 pi = pos[i];
-                if (band0) {
-                  const int j = s_gstart[h] + (k - kb);
-                  double ex, ey, ez;
-                  pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey,
-                             ez);
-                  h0 = j != i && exact_r2(ex, ey, ez) <= g.rv2;
-                }
-                if (band1) {
-                  const int j = s_gstart[h] + (k + 1 - kb);
-                  double ex, ey, ez;
-                  pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey,
-                             ez);
-                  h1 = j != i && exact_r2(ex, ey, ez) <= g.rv2;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if (band[u]) {
+                    const int j = s_gstart[h] + (k + u - kb);
+                    double ex, ey, ez;
+                    pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex,
+                               ey, ez);
+                    hit[u] = j != i && exact_r2(ex, ey, ez) <= g.rv2;
+                  }
                 }
               }
               // unconditional ring stores: a miss leaves junk in the next free
               // slot, which the next hit (or the sentinel padding) overwrites
               const int n0 = n;
-              const uint2 sb = *reinterpret_cast<const uint2*>(sbase + k);
-              s_ring[warp][n & 15][lane] = sb.x | tag;
-              n += h0 ? 1 : 0;
-              s_ring[warp][n & 15][lane] = sb.y | tag;
-              n += h1 ? 1 : 0;
+              const uint4 sb = *reinterpret_cast<const uint4*>(sbase + k);
+              ring_put(rbase, n, sb.x | tag);
+              n += hit[0] ? 1 : 0;
+              ring_put(rbase, n, sb.y | tag);
+              n += hit[1] ? 1 : 0;
+              ring_put(rbase, n, sb.z | tag);
+              n += hit[2] ? 1 : 0;
+              ring_put(rbase, n, sb.w | tag);
+              n += hit[3] ? 1 : 0;
               if ((n0 >> 3) != (n >> 3) && n0 < bg.cap) {  // a chunk completed: flush it
                 const int c = n0 >> 3;
                 flush_chunk(&s_ring[warp][(c & 1) * 8][lane], list + row + c * 256);
@@ -737,191 +753,6 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
       }
       __syncwarp();
     }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
-    my_ent += __shfl_xor_sync(0xffffffffu, my_ent, o);
-  }
-  if (lane == 0) {
-    atomicMax(&s_maxc, my_max);
-    atomicAdd(&s_ent, my_ent);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicMax(&ctrl->max_count, s_maxc);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries), s_ent);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Full-list build for sparse cells (k_build_brick4): lanes = 32 consecutive
-// particles of the brick, which may sit in different cells. The warp streams
-// the halo cells x-fastest; each lane takes a cell only if it is one of its
-// own 27 neighbours (so the candidate set and the visiting order per particle
-// are exactly k_build_brick3's), and the warp skips cells no lane needs. At a
-// few particles per cell (the Kremer-Grest melt: 3) a warp per cell would
-// leave most lanes idle; here every lane works.
-template <bool kGlobal>
-__global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
-    k_build_brick4(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
-                   const int* __restrict__ brick_rank_off, const int* __restrict__ start,
-                   const int* __restrict__ group_off, Geom g, BrickGeom bg,
-                   uint32_t* __restrict__ list, int* __restrict__ nnbr,
-                   double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
-  if (!ctrl->rebuild) return;
-  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z | base, each stage_cap + 32
-  __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
-  __shared__ uint32_t s_code[kMaxHalo];
-  __shared__ __align__(16) uint32_t s_ring[kBuildThreads / 32][16][32];
-  __shared__ int s_maxc;
-  __shared__ unsigned long long s_ent;
-  const int b = blockIdx.x;
-  HaloTable ht;
-  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
-  load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
-            s_gcell);
-  if (ht.total > bg.stage_cap) {
-    if (threadIdx.x == 0) {
-      atomicOr(&ctrl->status, kStatStageOverflow);
-      atomicMax(&ctrl->max_halo, ht.total);
-    }
-    return;
-  }
-  const int sc = bg.stage_cap + 32;
-  float* nx = s_f;
-  float* ny = s_f + sc;
-  float* nz = s_f + 2 * sc;
-  int* sbase = reinterpret_cast<int*>(s_f + 3 * sc);
-  const double ox = ht.lo[0] * bg.origin_scale[0];
-  const double oy = ht.lo[1] * bg.origin_scale[1];
-  const double oz = ht.lo[2] * bg.origin_scale[2];
-  for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
-    float x = kFarF, y = kFarF, z = kFarF;
-    int base = 0;
-    if (k < ht.total) {
-      const int h = halo_of(k, s_off, ht.n);
-      const int q = k - s_off[h];
-      if (q < s_cnt[h]) {
-        const double4 p = pos[s_gstart[h] + q];
-        const uint32_t c = s_code[h];
-        x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
-        y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
-        z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
-        base = kGlobal ? s_gstart[h] + q : k;
-      }
-    }
-    nx[k] = -x;
-    ny[k] = -y;
-    nz[k] = -z;
-    sbase[k] = base;
-  }
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
-  const int gbase = kGlobal ? 0 : group_off[b];
-  const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
-  const int np = ht.be - ht.bs;
-  const int H0 = ht.H[0], H01 = ht.H[0] * ht.H[1];
-  int my_max = 0;
-  unsigned long long my_ent = 0;
-  for (int p0 = warp * 32; p0 < np; p0 += kBuildThreads) {
-    const int q = p0 + lane;
-    const bool active = q < np;
-    const int i = ht.bs + (active ? q : 0);
-    // own halo cell: the owned cell whose range holds slot i
-    int hc = 0;
-    for (int oc = 0; oc < ncell_own; ++oc) {
-      const int axo = oc % ht.e[0], ayo = (oc / ht.e[0]) % ht.e[1], azo = oc / (ht.e[0] * ht.e[1]);
-      const int h = (axo + 1) + H0 * (ayo + 1) + H01 * (azo + 1);
-      if (i >= s_gstart[h] && i < s_gstart[h] + s_cnt[h]) hc = h;
-    }
-    const int hx = hc % H0, hy = (hc / H0) % ht.H[1], hz = hc / H01;
-    const int ki = s_off[hc] + (i - s_gstart[hc]);
-    const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
-    const float2 xi2 = f2(xf, xf), yi2 = f2(yf, yf), zi2 = f2(zf, zf);
-    const int ib = kGlobal ? i : i - ht.bs;
-    const unsigned long long row = list_slot(gbase + (ib >> 5), bg.cap, ib & 31, 0);
-    const uint32_t lo2m1 = __float_as_uint(bg.lo2) - 1u;
-    // halo cells any lane of the warp needs: bounding box of the lanes' cells +-1
-    int bx0 = active ? hx : 1 << 20, bx1 = active ? hx : -(1 << 20);
-    int by0 = active ? hy : 1 << 20, by1 = active ? hy : -(1 << 20);
-    int bz0 = active ? hz : 1 << 20, bz1 = active ? hz : -(1 << 20);
-    for (int o = 16; o > 0; o >>= 1) {
-      bx0 = min(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
-      bx1 = max(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
-      by0 = min(by0, __shfl_xor_sync(0xffffffffu, by0, o));
-      by1 = max(by1, __shfl_xor_sync(0xffffffffu, by1, o));
-      bz0 = min(bz0, __shfl_xor_sync(0xffffffffu, bz0, o));
-      bz1 = max(bz1, __shfl_xor_sync(0xffffffffu, bz1, o));
-    }
-    int n = 0;
-    for (int cz = bz0 - 1; cz <= bz1 + 1; ++cz) {
-      for (int cy = by0 - 1; cy <= by1 + 1; ++cy) {
-        for (int cx = bx0 - 1; cx <= bx1 + 1; ++cx) {
-          const int h = cx + H0 * cy + H01 * cz;
-          const int ox2 = cx - hx, oy2 = cy - hy, oz2 = cz - hz;
-          const bool mine = active && ox2 >= -1 && ox2 <= 1 && oy2 >= -1 && oy2 <= 1 &&
-                            oz2 >= -1 && oz2 <= 1;
-          const uint32_t code = s_code[h];
-          const int first = ox2 != 0 ? ox2 : (oy2 != 0 ? oy2 : oz2);
-          const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
-          const float hi2 = mine ? bg.hi2 : -1.0f;  // lanes outside this cell never hit
-          const int kb = s_off[h], ke = kb + s_cnt[h];
-#pragma unroll 1
-          for (int k = kb; k < ke; k += 2) {
-            const float2 X = *reinterpret_cast<const float2*>(nx + k);
-            const float2 Y = *reinterpret_cast<const float2*>(ny + k);
-            const float2 Z = *reinterpret_cast<const float2*>(nz + k);
-            const float2 dx = __fadd2_rn(xi2, X), dy = __fadd2_rn(yi2, Y),
-                         dz = __fadd2_rn(zi2, Z);
-            const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-            bool h0 = r2.x <= hi2;
-            bool h1 = r2.y <= hi2;
-            const bool band0 = h0 && (__float_as_uint(r2.x) - 1u) >= lo2m1;
-            const bool band1 = h1 && (__float_as_uint(r2.y) - 1u) >= lo2m1;
-            if (band0 || band1) {
-              const double4 pi = pos[i];
-              if (band0) {
-                const int j = s_gstart[h] + (k - kb);
-                double ex, ey, ez;
-                pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey, ez);
-                h0 = j != i && exact_r2(ex, ey, ez) <= g.rv2;
-              }
-              if (band1) {
-                const int j = s_gstart[h] + (k + 1 - kb);
-                double ex, ey, ez;
-                pair_delta(pi, pos[j], static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey, ez);
-                h1 = j != i && exact_r2(ex, ey, ez) <= g.rv2;
-              }
-            }
-            const int n0 = n;
-            const uint2 sb = *reinterpret_cast<const uint2*>(sbase + k);
-            s_ring[warp][n & 15][lane] = sb.x | tag;
-            n += h0 ? 1 : 0;
-            s_ring[warp][n & 15][lane] = sb.y | tag;
-            n += h1 ? 1 : 0;
-            if ((n0 >> 3) != (n >> 3) && n0 < bg.cap) {
-              const int c = n0 >> 3;
-              flush_chunk(&s_ring[warp][(c & 1) * 8][lane], list + row + c * 256);
-            }
-          }
-        }
-      }
-    }
-    if (active) {
-      if ((n & 7) != 0 && n < bg.cap) {
-        for (int r = n; r < ((n + 7) & ~7); ++r) s_ring[warp][r & 15][lane] = sentinel;
-        const int c = n >> 3;
-        flush_chunk(&s_ring[warp][(c & 1) * 8][lane], list + row + c * 256);
-      }
-      nnbr[i] = n < bg.cap ? n : bg.cap;
-      snap[i] = pos[i];
-      if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
-      my_max = max(my_max, n);
-      my_ent += static_cast<unsigned long long>(n);
-    }
-    __syncwarp();
   }
   for (int o = 16; o > 0; o >>= 1) {
     my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));

@@ -125,8 +125,8 @@ struct tmd_gpu_ctx {
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
   int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
   double occupancy = 0.0;     // particle-weighted mean cell occupancy at creation
-  int build_kind = 3;         // variant 3 list build: 3 = warp per cell, 4 = warp per 32 brick
-                              // particles, 5 = thread per particle (sparse cells)
+  int build_kind = 3;         // variant 3 list build: 3 = warp per cell (brick-staged),
+                              // 5 = thread per particle (sparse cells)
   BrickGeom bg{};
   int* cell_rank = nullptr;       // global cell -> brick-major rank
   int* brick_rank_off = nullptr;  // brick -> first rank (nbricks + 1)
@@ -369,8 +369,6 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
                             static_cast<int>(b)), "smem attr build");
     ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(b)), "smem attr build");
-    ck(cudaFuncSetAttribute(k_build_brick4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(b)), "smem attr build");
     g_build = b;
   }
   if (f > g_force) {
@@ -414,8 +412,7 @@ void launch_build(tmd_gpu_ctx* c) {
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->cap, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
   } else if (c->variant == 3) {
-    auto kern = c->build_kind == 4 ? k_build_brick4<true> : k_build_brick3<true>;
-    kern<<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
+    k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
         c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
   } else {
@@ -1042,7 +1039,7 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   bg.stage_cap = std::max(256, (static_cast<int>(want) + 31) / 32 * 32);
   // list build: a warp per cell while cells hold most of a warp, else a warp
   // per 32 consecutive brick particles (sparse cells, e.g. the KG melt)
-  if (c->build_kind < 3 || c->build_kind > 5) {
+  if (c->build_kind != 3 && c->build_kind != 5) {
     // occupancy seen by a particle (sum n_c^2 / sum n_c over the initial
     // cells), so a dense slab in a mostly empty box counts as dense
     const double occ = c->occupancy > 0.0 ? c->occupancy : per_cell;

@@ -136,8 +136,8 @@ class EngineConfig:
     # 2x LDG.128 gathers; 2 = brick-staged shared memory; 3 = sector-chunked
     # list + 256-bit LDG gathers
     variant: int = 0
-    # list build of variant 3: 0 = by cell occupancy, 3 = warp per cell,
-    # 4 = warp per 32 brick particles (sparse cells)
+    # list build of variant 3: 0 = by cell occupancy, 3 = warp per cell
+    # (brick-staged), 5 = thread per particle (sparse cells)
     build: int = 0
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off

@@ -313,19 +313,19 @@ def run_ours(args) -> None:
     h2d = flat.pos.nbytes + flat.vel.nbytes + flat.id.nbytes
     t0 = time.perf_counter()
     e2 = E.Engine(flat, w.inter, w.r_skin, ecfg)
-    obs_bytes = 0
-    for _ in range(args.steps):
-        e2.run(1)
-        e2.observe()
-        obs_bytes += 40
+    rows = e2.run_observed(args.steps, stride=1)  # each step's observables land in host memory
     out = e2.flatten()
     t_e2e = time.perf_counter() - t0
+    assert len(rows) == args.steps
+    obs_bytes = 32 * len(rows)  # (step, KE, PE, W) per step, written by the device to host
     d2h = obs_bytes + out.pos.nbytes + out.vel.nbytes + out.id.nbytes
     e2.close()
     e2e = {"value": n * args.steps / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "seconds": t_e2e,
-           "what": "Engine(create from host arrays) + K x (run(1) + observe()) + flatten()"}
+           "what": "Engine(create from host arrays: upload, bin, build, first forces) + "
+                   "run_observed(K, stride 1): every step's (step, KE, PE, W) written by the "
+                   "device into mapped pinned host memory + flatten() download"}
 
     cpu = None
     if not args.no_cpu_baseline:

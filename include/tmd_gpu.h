@@ -155,6 +155,15 @@ int tmd_gpu_compute_forces(tmd_gpu_ctx* ctx, double* pe, double* virial);
  * "(at step N)" like run_phase (engine.hpp:167-170). */
 int tmd_gpu_step(tmd_gpu_ctx* ctx, int64_t nsteps);
 
+/* Engine::run with an observable row every `stride` steps (the CLI's
+ * observable_stride loop, md_cli.cpp:110-126, without a host round trip per
+ * row): each recorded step's (step, KE, PE, W, T) is written by the device
+ * into mapped pinned host memory as the step completes. Rows for the steps
+ * s with s % stride == 0 in (start, start + nsteps], in order; at most cap
+ * written to out, *n_out = the count. */
+int tmd_gpu_run_observed(tmd_gpu_ctx* ctx, int64_t nsteps, int64_t stride, tmd_observables* out,
+                         int64_t cap, int64_t* n_out);
+
 /* Engine::observe (engine.hpp:132-140) + virial. */
 int tmd_gpu_observe(tmd_gpu_ctx* ctx, tmd_observables* out);
 

@@ -35,7 +35,7 @@ EXPORTS = [
     "tmd_gpu_slab_ghosts_ready", "tmd_gpu_slab_kick_drift", "tmd_gpu_slab_forces",
     "tmd_gpu_slab_halo", "tmd_gpu_slab_sums", "tmd_gpu_slab_layer_counts",
     "tmd_gpu_slab_recut", "tmd_gen_chains", "tmd_gpu_brute_force", "tmd_gen_lattice",
-    "tmd_gen_spherical", "tmd_gen_random",
+    "tmd_gen_spherical", "tmd_gen_random", "tmd_gpu_run_observed",
 ]
 
 
@@ -125,6 +125,8 @@ def lib() -> C.CDLL:
     L.tmd_gpu_compute_forces.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.tmd_gpu_step.argtypes = [P, C.c_int64]
     L.tmd_gpu_observe.argtypes = [P, C.POINTER(TmdObservables)]
+    L.tmd_gpu_run_observed.argtypes = [P, C.c_int64, C.c_int64, C.POINTER(TmdObservables),
+                                       C.c_int64, C.POINTER(C.c_int64)]
     L.tmd_gpu_download.argtypes = [P, P, P, P, P]
     L.tmd_gpu_set_velocities.argtypes = [P, P, P]
     L.tmd_gpu_cell_of.argtypes = [P, P, P]

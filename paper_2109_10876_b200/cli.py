@@ -126,7 +126,11 @@ def run_engine(cfg: RunConfig, flat: E.FlatConfig, out_dir: str) -> None:
         write_xyz_frame(traj, eng.flatten(), 0)
     steps = cfg.engine.steps
     ostride, tstride = cfg.engine.observable_stride, cfg.output.trajectory_stride
-    s = 0
+    if not traj and not (timing and per_step) and steps > 0:
+        # only observable rows: recorded on the device, no host round trip per row
+        for r in eng.run_observed(steps, ostride):
+            sys.stdout.write(f"{int(r[0])},{_f17(r[1])},{_f17(r[2])},{_f17(r[3])}\n")
+    s = steps if (not traj and not (timing and per_step)) else 0
     while s < steps:
         # advance to the next step that needs the host (observable row,
         # trajectory frame, per-step timing record), in one device run

@@ -96,6 +96,8 @@ struct Ctrl {
   int max_halo;               // largest staged halo seen (slots)
   int err_bit;                // status bit of the first error (its record below)
   double err_val;             // a value for the first error's message (bond r^2)
+  int obs_rows;               // observable rows recorded in this chunk (run_observed)
+  int pad2_;
 };
 
 // ---------------------------------------------------------------------------

@@ -16,6 +16,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -175,6 +179,10 @@ struct tmd_gpu_ctx {
   int64_t step = 0;
   uint64_t rebuilds = 0;
   bool ke_fresh = false;  // part_ke holds the current velocities' partials
+  bool obs_fresh = false; // h_scalars holds PE, W, KE of the current state
+  bool ck_valid = false;  // a rollback checkpoint exists (invalidated by state edits)
+  int64_t ck_step = 0;
+  Ctrl ck_ctrl{};
   double sec[5] = {0, 0, 0, 0, 0};
   double elapsed = 0.0;
   std::string err;
@@ -205,6 +213,12 @@ struct tmd_gpu_ctx {
     uint64_t fixed = 0;  // kernels per launch outside the IF bodies
   };
   StepGraph sg[2][2];  // [block of kGraphSteps | single step][starting buffer parity]
+  StepGraph sgo[2][2]; // the same with a per-step observable row (run_observed)
+  int obs_stride = 0;           // > 0 while run_observed records rows
+  int sgo_stride = 0;           // stride the observed graphs were captured with
+  double* obs_host = nullptr;   // mapped pinned rows [kChunk][4]: step, KE, PE, W
+  double* obs_dev = nullptr;    // its device alias
+  std::vector<std::array<double, 4>> obs_rows;  // rows of the current run_observed
   bool graph_dirty = true;
   bool use_graphs = true;
   uint64_t graph_body_kernels = 0;   // kernels per executed IF body
@@ -214,11 +228,13 @@ struct tmd_gpu_ctx {
 namespace {
 
 void drop_graphs(tmd_gpu_ctx* c) {
-  for (auto& row : c->sg) {
-    for (auto& s : row) {
-      if (s.exec) cudaGraphExecDestroy(s.exec);
-      if (s.graph) cudaGraphDestroy(s.graph);
-      s = tmd_gpu_ctx::StepGraph{};
+  for (auto* fam : {&c->sg, &c->sgo}) {
+    for (auto& row : *fam) {
+      for (auto& s : row) {
+        if (s.exec) cudaGraphExecDestroy(s.exec);
+        if (s.graph) cudaGraphDestroy(s.graph);
+        s = tmd_gpu_ctx::StepGraph{};
+      }
     }
   }
   c->graph_dirty = false;
@@ -245,6 +261,7 @@ void free_all(tmd_gpu_ctx* c) {
     if (p) cudaFree(p);
   }
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+  if (c->obs_host) cudaFreeHost(c->obs_host);
   if (c->h_scalars) cudaFreeHost(c->h_scalars);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
@@ -695,6 +712,30 @@ constexpr int64_t kChunk = 256;
 // list overflowed (state is then garbage; the caller rolls back).
 constexpr int kGraphSteps = 15;  // odd: the ping-pong parity is unchanged per graph
 
+constexpr int kObsRows = 256;  // == kChunk: rows a chunk can record
+
+void launch_obs_record(tmd_gpu_ctx* c) {
+  if (c->obs_stride <= 0) return;
+  c->launches += 1;
+  k_obs_record<<<1, kRedThreads, 0, c->ls>>>(c->part_e, c->part_w, force_parts(c), c->part_ke,
+                                             c->nblk, c->ctrl, c->obs_stride, c->obs_dev,
+                                             kObsRows);
+}
+
+// End of a run segment: PE / virial / KE reduced and copied into the pinned
+// host mirror, so observe() after a run needs neither a launch nor a sync.
+void enqueue_observables(tmd_gpu_ctx* c) {
+  launch_reduce_pe(c);
+  if (c->variant == 2) {  // brick variant: its kinetic partials are per brick
+    c->launches += 1;
+    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
+                                            c->mass, c->part_ke);
+  }
+  launch_reduce_ke(c);
+  ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                     c->ls), "D2H scalars");
+}
+
 // Captures one block of `nsteps` steps (odd; starting at buffer parity
 // c->cur) as a CUDA graph whose rebuild branches are conditional IF nodes.
 // Splitting a run into such blocks is bitwise identical to the eager
@@ -776,8 +817,9 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
                                            cudaStreamSetCaptureDependencies),
        "cudaStreamUpdateCaptureDependencies");
     launch_forces(c, s + 1 < nsteps ? kFused : kKick2);
+    launch_obs_record(c);
   }
-  launch_reduce_pe(c);
+  enqueue_observables(c);
   ck(cudaStreamEndCapture(c->stream, &g), "end capture");
   cudaGraphExec_t exec = nullptr;
   ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");
@@ -816,24 +858,40 @@ void enqueue_segment(tmd_gpu_ctx* c, int64_t steps) {
       Phase p(c, TMD_SECTION_FORCES);
       launch_forces(c, s + 1 < steps ? kFused : kKick2);
     }
+    launch_obs_record(c);
   }
-  launch_reduce_pe(c);
+  enqueue_observables(c);
 }
 
 bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
   const bool graphs = c->use_graphs && !c->timers_on;
+  if (c->obs_stride > 0) {
+    ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
+  }
   if (graphs) {
     if (c->graph_dirty) drop_graphs(c);
     const long long rebuilds0 = c->h_ctrl->rebuilds;
     int64_t left = steps;
     while (left > 0) {
       const int kind = left >= kGraphSteps ? 0 : 1;  // block of 15, or single steps
-      tmd_gpu_ctx::StepGraph& sgr = c->sg[kind][c->cur];
+      if (c->obs_stride > 0 && c->sgo_stride != c->obs_stride) {
+        // the stride is a kernel argument baked into the observed graphs
+        for (auto& row : c->sgo) {
+          for (auto& sg : row) {
+            if (sg.exec) cudaGraphExecDestroy(sg.exec);
+            if (sg.graph) cudaGraphDestroy(sg.graph);
+            sg = tmd_gpu_ctx::StepGraph{};
+          }
+        }
+        c->sgo_stride = c->obs_stride;
+      }
+      tmd_gpu_ctx::StepGraph& sgr = (c->obs_stride > 0 ? c->sgo : c->sg)[kind][c->cur];
       if (!sgr.exec) capture_graph(c, kind == 0 ? kGraphSteps : 1, sgr);
       ck(cudaGraphLaunch(sgr.exec, c->stream), "cudaGraphLaunch");
       c->launches += sgr.fixed;
       left -= kind == 0 ? kGraphSteps : 1;
     }
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
     sync_ctrl(c);
     c->launches += static_cast<uint64_t>(c->h_ctrl->rebuilds - rebuilds0) *
                    c->graph_body_kernels;
@@ -847,28 +905,38 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
                        cudaMemcpyDeviceToHost, c->stream),
        "D2H rebuild log");
   }
+  ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
   sync_ctrl(c);
   harvest_timers(c);
   return (c->h_ctrl->status & kOverflowBits) == 0;
 }
 
+// Runs nsteps in device-resident chunks. A checkpoint (positions,
+// velocities, masses, ids; forces with a thermostat) is taken every kChunk
+// steps, not every call, so a loop of run(1) calls pays for it once per
+// kChunk steps. A list or staging overflow rolls back to the checkpoint,
+// grows, and replays everything since (at most kChunk steps).
 void do_run(tmd_gpu_ctx* c, int64_t nsteps) {
-  int64_t done = 0;
-  while (done < nsteps) {
-    const int64_t todo = std::min(kChunk, nsteps - done);
-    checkpoint(c);
-    const Ctrl before = *c->h_ctrl;  // mirror is current after the last sync
+  const int64_t target = c->step + nsteps;
+  while (c->step < target) {
+    if (!c->ck_valid || c->step - c->ck_step >= kChunk) {
+      checkpoint(c);
+      c->ck_ctrl = *c->h_ctrl;  // mirror is current after the last sync
+      c->ck_step = c->step;
+      c->ck_valid = true;
+    }
+    const int64_t todo = std::min(kChunk - (c->step - c->ck_step), target - c->step);
     ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
-    const bool ok = run_chunk(c, todo);
-    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
-    ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+    const bool ok = run_chunk(c, todo);  // records t1 and synchronises
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, c->t0, c->t1), "cudaEventElapsedTime");
     c->elapsed += 1e-3 * ms;
     if (!ok) {
-      // list or staging overflow: roll back, grow, replay this chunk
+      // list or staging overflow: roll back, grow, replay from the checkpoint
       const Ctrl h = *c->h_ctrl;
-      restore(c, before);
+      restore(c, c->ck_ctrl);
+      c->step = c->ck_step;
+      c->rebuilds = static_cast<uint64_t>(c->ck_ctrl.rebuilds);
       grow_after_overflow(c, h);
       if (c->th.on) {
         // the restored forces hold the Langevin kick of the checkpoint step
@@ -887,8 +955,15 @@ void do_run(tmd_gpu_ctx* c, int64_t nsteps) {
     c->step = c->h_ctrl->step;
     c->rebuilds = static_cast<uint64_t>(c->h_ctrl->rebuilds);
     c->ke_fresh = true;
+    c->obs_fresh = true;
+    if (c->obs_stride > 0) {  // rows landed in mapped host memory during the chunk
+      const int rows = std::min(c->h_ctrl->obs_rows, kObsRows);
+      for (int r = 0; r < rows; ++r) {
+        const double* o = c->obs_host + 4 * r;
+        c->obs_rows.push_back({o[0], o[1], o[2], o[3]});
+      }
+    }
     raise_physics(c, true);
-    done += todo;
   }
 }
 
@@ -949,11 +1024,29 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
   }
   if (!s->id || !s->pos) cfg("id and pos arrays are required");
   // validate_flat (flat_config.hpp:42-61): unique ids, positive masses
-  std::vector<int64_t> ids(s->id, s->id + s->n);
-  std::sort(ids.begin(), ids.end());
-  for (size_t k = 1; k < ids.size(); ++k) {
-    if (ids[k] == ids[k - 1]) cfg("duplicate particle id " + std::to_string(ids[k]));
+  // unique ids: O(n) with a bitmap when they fill a dense range (the usual
+  // 0..n-1), else by sorting
+  const int64_t id_lo = *std::min_element(s->id, s->id + s->n);
+  const int64_t id_hi = *std::max_element(s->id, s->id + s->n);
+  const bool dense = static_cast<uint64_t>(id_hi - id_lo) < static_cast<uint64_t>(s->n);
+  std::vector<int64_t> ids;
+  if (dense) {
+    std::vector<unsigned char> seen(static_cast<size_t>(s->n), 0);
+    for (int64_t k = 0; k < s->n; ++k) {
+      unsigned char& b = seen[static_cast<size_t>(s->id[k] - id_lo)];
+      if (b) cfg("duplicate particle id " + std::to_string(s->id[k]));
+      b = 1;
+    }
+  } else {
+    ids.assign(s->id, s->id + s->n);
+    std::sort(ids.begin(), ids.end());
+    for (size_t k = 1; k < ids.size(); ++k) {
+      if (ids[k] == ids[k - 1]) cfg("duplicate particle id " + std::to_string(ids[k]));
+    }
   }
+  auto known = [&](int64_t v) {
+    return dense ? (v >= id_lo && v <= id_hi) : std::binary_search(ids.begin(), ids.end(), v);
+  };
   if (s->mass) {
     for (int64_t k = 0; k < s->n; ++k) {
       if (!(s->mass[k] > 0.0)) {
@@ -970,8 +1063,8 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
   if (s->n_bonds > 0) {
     for (int64_t k = 0; k < s->n_bonds; ++k) {
       const int64_t a = s->bonds[2 * k], b = s->bonds[2 * k + 1];
-      const bool ha = std::binary_search(ids.begin(), ids.end(), a);
-      const bool hb = std::binary_search(ids.begin(), ids.end(), b);
+      const bool ha = known(a);
+      const bool hb = known(b);
       if (!ha || !hb) {
         cfg("bond references unknown particle id " + std::to_string(ha ? b : a));
       }
@@ -1345,8 +1438,18 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
   if (!out) return TMD_ERR_CONFIG;
   *out = nullptr;
   auto* c = new tmd_gpu_ctx();
+  const bool dbg = std::getenv("TMD_DEBUG_TIMING") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tmd create] %-24s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t_prev).count());
+    t_prev = t;
+  };
   const int rc = guard(c, [&] {
     validate(sys, lj, fene, params);
+    mark("validate");
     build_geom(c, sys->box, lj->r_cut, params->r_skin);  // ConfigError before any CUDA call
     int ndev = 0;
     ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -1355,9 +1458,12 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       ck(cudaSetDevice(params->device), "cudaSetDevice");
     }
     ck(cudaGetDevice(&c->device), "cudaGetDevice");
-    cudaDeviceProp prop;
-    ck(cudaGetDeviceProperties(&prop, c->device), "cudaGetDeviceProperties");
-    if (prop.major != 10) {
+    int major = 0;  // (cudaGetDeviceProperties costs tens of ms: only on failure)
+    ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device),
+       "cudaDeviceGetAttribute");
+    if (major != 10) {
+      cudaDeviceProp prop;
+      ck(cudaGetDeviceProperties(&prop, c->device), "cudaGetDeviceProperties");
       throw CudaFail{std::string("device ") + prop.name +
                      " is not sm_100 (this build targets sm_100a only)"};
     }
@@ -1368,6 +1474,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->use_graphs = params->reserved[2] == 0;  // reserved[2] = 1 disables CUDA graphs
     ck(cudaEventCreate(&c->t0), "cudaEventCreate");
     ck(cudaEventCreate(&c->t1), "cudaEventCreate");
+    mark("device + streams");
 
     // Slab mode: keep the particles whose wrapped position lies in this
     // rank's z layers (exact host wrap + cell, bit-identical to the device's).
@@ -1531,6 +1638,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     }
     ck(cudaMemcpy(c->posb[0] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
     ck(cudaMemcpy(c->posb[1] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
+    mark("allocate + upload");
     if (nranks > 1) alloc_slab(c);
     if (sys->n_bonds > 0) setup_bonds(c, sys, fene);
 
@@ -1549,7 +1657,9 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     alloc_list(c, cap0);
     // slab mode: the owner of the decomposition finishes the setup after the
     // first migration/ghost exchange (tmd_gpu_slab_*); whole box: now
+    mark("list alloc");
     if (nranks == 1) setup_pass(c);
+    mark("setup pass");
     c->step = 0;
     c->rebuilds = 0;
     c->ke_fresh = false;
@@ -1651,9 +1761,18 @@ HostState fetch(tmd_gpu_ctx* c, bool pos, bool vel, bool frc, bool cell) {
   }
   ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   h.order.resize(n);
-  std::iota(h.order.begin(), h.order.end(), size_t{0});
-  std::sort(h.order.begin(), h.order.end(),
-            [&](size_t a, size_t b) { return h.id[a] < h.id[b]; });
+  if (n > 0) {
+    // ids filling a dense range: order by direct placement, else sort
+    const long long lo = *std::min_element(h.id.begin(), h.id.end());
+    const long long hi = *std::max_element(h.id.begin(), h.id.end());
+    if (static_cast<unsigned long long>(hi - lo) == static_cast<unsigned long long>(n - 1)) {
+      for (size_t s = 0; s < n; ++s) h.order[static_cast<size_t>(h.id[s] - lo)] = s;
+    } else {
+      std::iota(h.order.begin(), h.order.end(), size_t{0});
+      std::sort(h.order.begin(), h.order.end(),
+                [&](size_t a, size_t b) { return h.id[a] < h.id[b]; });
+    }
+  }
   return h;
 }
 
@@ -1667,6 +1786,8 @@ const char* tmd_gpu_last_error(const tmd_gpu_ctx* ctx) {
 
 int tmd_gpu_compute_forces(tmd_gpu_ctx* c, double* pe, double* virial) {
   return guard(c, [&] {
+    c->ck_valid = false;
+    c->obs_fresh = false;
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     launch_forces(c);
     launch_reduce_pe(c);
@@ -1691,13 +1812,70 @@ int tmd_gpu_step(tmd_gpu_ctx* c, int64_t nsteps) {
   });
 }
 
+int tmd_gpu_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride, tmd_observables* out,
+                         int64_t cap, int64_t* n_out) {
+  return guard(c, [&] {
+    if (nsteps < 0) throw StatusError{TMD_ERR_CONFIG, "step count must be non-negative"};
+    if (stride < 1) throw StatusError{TMD_ERR_CONFIG, "observable stride must be at least 1"};
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (c->h_ctrl->status != 0) {
+      throw StatusError{TMD_ERR_STATE, "engine is in an error state from an earlier step"};
+    }
+    if (!c->obs_host) {
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&c->obs_host), sizeof(double) * 4 * kObsRows,
+                       cudaHostAllocMapped),
+         "cudaHostAlloc(mapped)");
+      ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->obs_dev), c->obs_host, 0),
+         "cudaHostGetDevicePointer");
+    }
+    const int64_t s0 = c->step;
+    c->obs_rows.clear();
+    c->obs_stride = static_cast<int>(std::min<int64_t>(stride, 1 << 30));
+    try {
+      do_run(c, nsteps);
+    } catch (...) {
+      c->obs_stride = 0;
+      throw;
+    }
+    c->obs_stride = 0;
+    // rows by step (a rollback replays and re-records steps: keep the last)
+    std::vector<std::array<double, 4>> rows;
+    for (const auto& r : c->obs_rows) {
+      const int64_t st = static_cast<int64_t>(r[0]);
+      if (st <= s0 || st > s0 + nsteps) continue;
+      while (!rows.empty() && static_cast<int64_t>(rows.back()[0]) >= st) rows.pop_back();
+      rows.push_back(r);
+    }
+    *n_out = static_cast<int64_t>(rows.size());
+    for (size_t k = 0; k < rows.size() && static_cast<int64_t>(k) < cap; ++k) {
+      out[k].step = static_cast<int64_t>(rows[k][0]);
+      out[k].kinetic = rows[k][1];
+      out[k].potential = rows[k][2];
+      out[k].virial = rows[k][3];
+      out[k].temperature = 2.0 * rows[k][1] / (3.0 * static_cast<double>(c->n));
+    }
+  });
+}
+
 int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    c->launches += 1;
-    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx,
-                                                 c->vy, c->vz, c->mass,
-                                                 c->part_ke);
+    if (c->obs_fresh) {  // the run's graph already delivered them
+      out->step = c->step;
+      out->potential = c->h_scalars[0];
+      out->virial = c->h_scalars[1];
+      out->kinetic = c->h_scalars[2];
+      out->temperature = 2.0 * out->kinetic / (3.0 * static_cast<double>(c->n));
+      return;
+    }
+    // after a run the closing half-kick already left the kinetic partials of
+    // the current velocities (same 128-particle blocks as k_kinetic, so the
+    // same sum bit for bit); the brick variant's partials are per brick
+    if (!(c->ke_fresh && c->variant != 2)) {
+      c->launches += 1;
+      k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
+                                              c->mass, c->part_ke);
+    }
     launch_reduce_ke(c);
     ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double),
                        cudaMemcpyDeviceToHost, c->stream), "D2H scalars");
@@ -1736,6 +1914,9 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
 
 int tmd_gpu_set_velocities(tmd_gpu_ctx* c, const int64_t* id, const double* vel) {
   return guard(c, [&] {
+    c->ck_valid = false;
+    c->ke_fresh = false;
+    c->obs_fresh = false;
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     HostState h = fetch(c, false, false, false, false);
     const size_t n = h.order.size();

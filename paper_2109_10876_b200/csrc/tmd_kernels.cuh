@@ -742,6 +742,40 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) *out = t * scale;
 }
 
+// Per-step observable row (run_observed): PE and virial of this step's force
+// evaluation (halved full-list sums), KE of the post-kick velocities, written
+// straight into mapped pinned host memory — each recorded step's result
+// crosses to the host as the step completes. Rows every `stride` steps.
+__global__ void __launch_bounds__(kRedThreads)
+    k_obs_record(const double* __restrict__ part_e, const double* __restrict__ part_w,
+                 int npe, const double* __restrict__ part_ke, int nke, Ctrl* ctrl, int stride,
+                 double* __restrict__ rows, int max_rows) {
+  __shared__ double red[kRedThreads / 32];
+  double se = 0.0, sw = 0.0, sk = 0.0;
+  for (int k = threadIdx.x; k < npe; k += kRedThreads) {
+    se += part_e[k];
+    sw += part_w[k];
+  }
+  for (int k = threadIdx.x; k < nke; k += kRedThreads) sk += part_ke[k];
+  const double te = block_sum<kRedThreads>(se, red);
+  const double tw = block_sum<kRedThreads>(sw, red);
+  const double tk = block_sum<kRedThreads>(sk, red);
+  if (threadIdx.x == 0) {
+    const long long st = ctrl->step;
+    if (st % stride == 0) {
+      const int r = ctrl->obs_rows;
+      if (r < max_rows) {
+        double* o = rows + 4 * r;
+        o[0] = static_cast<double>(st);
+        o[1] = tk;
+        o[2] = te * 0.5;
+        o[3] = tw * 0.5;
+      }
+      ctrl->obs_rows = r + 1;
+    }
+  }
+}
+
 // In-cut pair count of the current list (roofline accounting only; not on
 // the step path).
 __global__ void __launch_bounds__(kBlock)

@@ -308,6 +308,21 @@ class Engine:
     def run(self, steps: int) -> None:
         _check(_abi.lib().tmd_gpu_step(self._h, int(steps)), self._h)
 
+    def run_observed(self, steps: int, stride: int = 1) -> np.ndarray:
+        """run(steps) recording (step, kinetic, potential, temperature, virial)
+        every `stride` steps on the device (tmd_gpu_run_observed)."""
+        steps, stride = int(steps), int(stride)
+        cap = steps // max(stride, 1) + 1
+        rows = (_abi.TmdObservables * max(cap, 1))()
+        n = C.c_int64()
+        _check(_abi.lib().tmd_gpu_run_observed(self._h, steps, stride, rows, cap,
+                                                C.byref(n)), self._h)
+        out = np.empty((n.value, 5))
+        for k in range(n.value):
+            r = rows[k]
+            out[k] = (r.step, r.kinetic, r.potential, r.temperature, r.virial)
+        return out
+
     def observe(self) -> StepObservables:
         o = _abi.TmdObservables()
         _check(_abi.lib().tmd_gpu_observe(self._h, C.byref(o)), self._h)

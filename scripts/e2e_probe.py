@@ -1,0 +1,29 @@
+"""Where the end-to-end time goes: create, run(1), observe(), flatten()."""
+import sys
+import time
+sys.path.insert(0, "/root/repo")
+from paper_2109_10876_b200 import engine as E
+
+f = E.gen_fcc(64, 0.8442, 1.0, 12345)
+cfg = E.EngineConfig(dt=0.005, section_timers=False)
+E.Engine(f, E.Interactions(), 0.3, cfg).close()  # warm the process (module load, context)
+t0 = time.perf_counter()
+e = E.Engine(f, E.Interactions(), 0.3, cfg)
+t1 = time.perf_counter()
+tr = to = 0.0
+for _ in range(300):
+    a = time.perf_counter()
+    e.run(1)
+    b = time.perf_counter()
+    e.observe()
+    c = time.perf_counter()
+    tr += b - a
+    to += c - b
+t2 = time.perf_counter()
+e.flatten()
+t3 = time.perf_counter()
+print(f"create {1e3*(t1-t0):.1f} ms, run(1) {1e3*tr/300:.3f} ms, observe {1e3*to/300:.3f} ms, "
+      f"flatten {1e3*(t3-t2):.1f} ms; device ms/step ~{1e3*e.timers().elapsed/300:.3f}")
+t0 = time.perf_counter()
+e.run(300)
+print(f"run(300): {1e3*(time.perf_counter()-t0)/300:.3f} ms/step")

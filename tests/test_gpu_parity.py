@@ -368,3 +368,55 @@ def test_graph_mode_trajectory_vs_golden():
     flat = eng.flatten()
     assert np.abs(flat.pos - g["final_pos"]).max() < 1e-9
     assert eng.rebuild_count() == int(g["rebuilds"])
+
+
+def test_run1_loop_equals_one_run():
+    """Checkpoints every 256 steps, not every call: run(1) x N is the same
+    computation as run(N), bit for bit, and observe() reuses the kick's
+    kinetic partials."""
+    f = E.gen_fcc(8, 0.8442, 1.0, 7)
+    a = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(section_timers=False))
+    a.run(40)
+    b = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(section_timers=False))
+    for _ in range(40):
+        b.run(1)
+        ob = b.observe()
+    oa = a.observe()
+    fa, fb = a.flatten(), b.flatten()
+    np.testing.assert_array_equal(fa.pos, fb.pos)
+    np.testing.assert_array_equal(fa.vel, fb.vel)
+    assert (oa.kinetic, oa.potential) == (ob.kinetic, ob.potential)
+    assert a.rebuild_count() == b.rebuild_count()
+
+
+def test_overflow_inside_a_run1_loop_replays_from_the_checkpoint():
+    f = E.gen_fcc(8, 0.8442, 1.0, 99)
+    a = E.Engine(f, E.Interactions(), 0.3)
+    a.run(60)
+    b = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(nbr_capacity=8))
+    for _ in range(60):
+        b.run(1)
+    assert b.step_count() == 60
+    assert np.abs(a.flatten().pos - b.flatten().pos).max() < 1e-9
+
+
+@pytest.mark.parametrize("timers", [False, True])
+def test_run_observed_rows_equal_observe_after_each_run(timers):
+    """run_observed records on the device exactly what observe() reports
+    after run(stride) calls (golden trajectory system, with rebuilds)."""
+    g = load("fcc8_jit")
+    a = gpu_engine(g, section_timers=timers)
+    rows = a.run_observed(60, stride=4)
+    assert rows[:, 0].tolist() == list(range(4, 61, 4))
+    b = gpu_engine(g, section_timers=timers)
+    for r in rows:
+        b.run(4)
+        o = b.observe()
+        assert (o.step, o.kinetic, o.potential, o.temperature, o.virial) == tuple(r)
+    # stride 1 continues from step 60, and rows match the golden trace steps
+    rows1 = a.run_observed(140, stride=1)
+    assert rows1[0, 0] == 61 and rows1[-1, 0] == 200 and len(rows1) == 140
+    for row in g["trace"]:
+        if row[0] > 60:
+            k = int(row[0]) - 61
+            assert_rel(rows1[k, 1] + rows1[k, 2], row[1] + row[2], 1e-10, "E")

@@ -241,7 +241,7 @@ def run_ours(args) -> None:
     from paper_2109_10876_b200 import engine as E
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    if ws > 1 or args.decomposed:
         run_decomposed(args)
         return
     torch.cuda.set_device(0)
@@ -378,9 +378,13 @@ def run_decomposed(args) -> None:
     ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
     balance = "count" if args.config == "slab" else "static"
 
+    # the C++ step loop with NCCL on the context stream (tmd_slab_nccl.cuh);
+    # the Python protocol for the gloo pipeline check and load-aware cuts
+    native = args.dist_backend == "nccl" and balance == "static"
+
     def make():
         return DecomposedEngine(flat, w.inter, w.r_skin, ecfg, comm=TorchDistComm(),
-                                device_of=lambda r: local, balance=balance)
+                                device_of=lambda r: local, balance=balance, native=native)
 
     def max_over_ranks(x: float) -> float:
         t = torch.tensor([x], device="cuda", dtype=torch.float64)
@@ -429,7 +433,8 @@ def run_decomposed(args) -> None:
         return
     cfg = dict(cfg_w)
     cfg.update({"parallelism": f"{ws} z-slabs (spatial decomposition, {args.dist_backend} "
-                               f"halo + migration, {balance} cuts)",
+                               f"halo + migration, {balance} cuts, "
+                               f"{'native C++' if native else 'python'} step loop)",
                 "l2": "working set > 126 MB L2 on every rank at 1M / N; no flush",
                 "rebuilds_in_timed_region": rebuilds, "section_timers": False,
                 "rank0_slab": sizes, "exchanged_bytes_rank0": xbytes})
@@ -462,6 +467,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--decomposed", action="store_true",
+                    help="run the slab decomposition even at N = 1 (under torchrun): the "
+                         "single slab exchanges its halo with itself over NCCL")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="N > 1 only; gloo = pipeline check with every rank on GPU 0")
     args = ap.parse_args()

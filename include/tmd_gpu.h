@@ -240,7 +240,8 @@ void tmd_gpu_destroy(tmd_gpu_ctx* ctx);
  * Buffers: counts int32[dx*dy] (cells x-fastest), ids int64[n],
  * positions double4[n] (x, y, z, unused), records info[9] bytes each. */
 
-/* Slab `rank` of `nranks` (nranks <= z cell layers, >= 3 layers); every
+/* Slab `rank` of `nranks` (1 <= nranks <= z cell layers, >= 3 layers; with
+ * nranks = 1 the slab's ghost layers are its own boundary layers); every
  * rank passes the same whole system and keeps the particles in its layers.
  * The context is not usable for forces before the first rebuild sequence. */
 int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
@@ -250,6 +251,21 @@ int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
 /* info: rank, nranks, first owned z layer, owned layers, owned particles,
  * lower ghosts, upper ghosts, cells per layer, slot capacity, record bytes. */
 int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[10]);
+
+/* Native step loop of the decomposition (one process or thread per GPU):
+ * the same protocol driven from C++ with NCCL on the context's stream.
+ * tmd_nccl_unique_id fills 128 bytes on one rank (ncclGetUniqueId), which the
+ * caller broadcasts; every rank then attaches its slab context
+ * (ncclCommInitRank with the context's rank / nranks), runs the first
+ * migration / ghost exchange + forces (tmd_gpu_slab_setup), and steps
+ * (tmd_gpu_slab_run: collective, the same nsteps on every rank; per step one
+ * NCCL group of halo sends/receives, one MAX all-reduce and an 8-byte read
+ * for the rebuild decision). tmd_gpu_slab_observe all-reduces PE, W, KE. */
+int tmd_nccl_unique_id(void* id);
+int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id);
+int tmd_gpu_slab_setup(tmd_gpu_ctx* ctx);
+int tmd_gpu_slab_run(tmd_gpu_ctx* ctx, int64_t nsteps);
+int tmd_gpu_slab_observe(tmd_gpu_ctx* ctx, int64_t n_total, tmd_observables* out);
 
 /* Load-aware cuts: owned particles per global z layer
  * (counts[dims_z], wrapped positions) — the caller sums them over ranks and

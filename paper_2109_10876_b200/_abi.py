@@ -35,7 +35,9 @@ EXPORTS = [
     "tmd_gpu_slab_ghosts_ready", "tmd_gpu_slab_kick_drift", "tmd_gpu_slab_forces",
     "tmd_gpu_slab_halo", "tmd_gpu_slab_sums", "tmd_gpu_slab_layer_counts",
     "tmd_gpu_slab_recut", "tmd_gen_chains", "tmd_gpu_brute_force", "tmd_gen_lattice",
-    "tmd_gen_spherical", "tmd_gen_random", "tmd_gpu_run_observed",
+    "tmd_gen_spherical", "tmd_gen_random", "tmd_gpu_run_observed", "tmd_nccl_unique_id",
+    "tmd_gpu_slab_attach_nccl", "tmd_gpu_slab_setup", "tmd_gpu_slab_run",
+    "tmd_gpu_slab_observe",
 ]
 
 
@@ -119,6 +121,11 @@ def lib() -> C.CDLL:
     L.tmd_gpu_slab_halo.argtypes = [P, PP, PP]
     L.tmd_gpu_slab_sums.argtypes = [P, P]
     L.tmd_gpu_slab_layer_counts.argtypes = [P, P]
+    L.tmd_nccl_unique_id.argtypes = [P]
+    L.tmd_gpu_slab_attach_nccl.argtypes = [P, P]
+    L.tmd_gpu_slab_setup.argtypes = [P]
+    L.tmd_gpu_slab_run.argtypes = [P, C.c_int64]
+    L.tmd_gpu_slab_observe.argtypes = [P, C.c_int64, C.POINTER(TmdObservables)]
     L.tmd_gpu_slab_recut.argtypes = [P, P]
     L.tmd_gpu_last_error.argtypes = [P]
     L.tmd_gpu_last_error.restype = C.c_char_p

@@ -29,6 +29,18 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_dir():
+    """The NCCL that torch loads (pip nvidia-nccl): same library, one copy per
+    process. None: build without the native multi-GPU loop."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        d = Path(base) / "nccl"
+        if (d / "include" / "nccl.h").exists() and (d / "lib" / "libnccl.so.2").exists():
+            return d
+    return None
+
+
 def nvcc() -> str:
     cand = os.environ.get("NVCC") or "/usr/local/cuda/bin/nvcc"
     return cand if Path(cand).exists() else "nvcc"
@@ -44,7 +56,13 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB), *map(str, SOURCES)]
+    extra = ["-DTMD_NO_NCCL"]
+    nd = nccl_dir()
+    if nd is not None:
+        lib = nd / "lib"
+        extra = [f"-I{nd / 'include'}", f"-L{lib}", "-l:libnccl.so.2",
+                 "-Xlinker", f"-rpath,{lib}"]
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(LIB), *map(str, SOURCES)]
     res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
     log = res.stdout + res.stderr
     (PKG / "build.log").write_text(" ".join(cmd) + "\n" + log)

@@ -163,6 +163,8 @@ struct tmd_gpu_ctx {
   int* boff[2] = {nullptr, nullptr};
   int64_t nb[2] = {0, 0};
   int* gcnt[2] = {nullptr, nullptr};            // received ghost-layer counts (lo, hi)
+  void* nccl = nullptr;          // ncclComm_t of the native slab loop (tmd_slab_nccl.cuh)
+  int64_t* nccl_i64 = nullptr;   // staging for all-gathered counts
   double *part_e = nullptr, *part_w = nullptr, *part_ke = nullptr;
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
   Ctrl* ctrl = nullptr;
@@ -240,8 +242,11 @@ void drop_graphs(tmd_gpu_ctx* c) {
   c->graph_dirty = false;
 }
 
+void free_nccl(tmd_gpu_ctx* c);
+
 void free_all(tmd_gpu_ctx* c) {
   drop_graphs(c);
+  free_nccl(c);
   if (c->side) cudaStreamDestroy(c->side);
   void* ptrs[] = {c->posb[0], c->posb[1], c->pos2, c->snap, c->vx, c->vy, c->vz,
                   c->vx2,  c->vy2,   c->vz2,  c->fx,    c->fy,      c->fz,
@@ -1434,7 +1439,8 @@ void setup_bonds(tmd_gpu_ctx* c, const tmd_system* sys, const tmd_fene_params* f
 }
 
 int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_params* fene,
-                const tmd_engine_params* params, int rank, int nranks, tmd_gpu_ctx** out) {
+                const tmd_engine_params* params, int rank, int nranks, bool slab,
+                tmd_gpu_ctx** out) {
   if (!out) return TMD_ERR_CONFIG;
   *out = nullptr;
   auto* c = new tmd_gpu_ctx();
@@ -1479,7 +1485,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // Slab mode: keep the particles whose wrapped position lies in this
     // rank's z layers (exact host wrap + cell, bit-identical to the device's).
     std::vector<int64_t> sel;
-    if (nranks > 1) {
+    if (slab) {
       make_slab(c, rank, nranks);
       for (int64_t k = 0; k < sys->n; ++k) {
         const double z = host_wrap1(sys->pos[3 * k + 2], c->g.L[2]);
@@ -1497,7 +1503,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // particles to double plus both ghost layers (checked at every exchange)
     c->n_cap = sys->n;
     c->n_total = sys->n;
-    if (nranks > 1) {
+    if (slab) {
       c->n_cap = std::min<int64_t>(2 * sys->n, 2 * static_cast<int64_t>(sel.size()) + 65536);
       if (c->n_cap > kMaxSlots) {
         throw StatusError{TMD_ERR_CONFIG, "slab too large for one GPU context"};
@@ -1519,10 +1525,10 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->lj.fcap = params->force_cap;
     c->variant = (params->reserved[0] >= 1 && params->reserved[0] <= 3) ? params->reserved[0]
                                                                        : kDefaultVariant;
-    if (nranks > 1) c->variant = 3;  // slab mode runs the brick build + global-slot forces
+    if (slab) c->variant = 3;  // slab mode runs the brick build + global-slot forces
     if (sys->n_bonds > 0 && c->variant == 2) c->variant = 3;  // bonds: global-slot kernels
     if (params->force_cap > 0.0) {
-      if (nranks > 1) throw StatusError{TMD_ERR_CONFIG, "force cap: single-GPU warm-up only"};
+      if (slab) throw StatusError{TMD_ERR_CONFIG, "force cap: single-GPU warm-up only"};
       c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
     }
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
@@ -1547,7 +1553,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       c->occupancy = s1 > 0.0 ? s2 / s1 : 0.0;
     }
     setup_bricks(c, static_cast<double>(sys->n), lj->r_cut + params->r_skin);
-    if (nranks > 1) {  // groups of the owned particles only (+ migration headroom)
+    if (slab) {  // groups of the owned particles only (+ migration headroom)
       const int64_t want = c->n + c->n / 4 + 1024;
       c->ngroups_max = static_cast<int>(want / 32) + c->bg.nbricks + 1;
     }
@@ -1639,7 +1645,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     ck(cudaMemcpy(c->posb[0] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
     ck(cudaMemcpy(c->posb[1] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
     mark("allocate + upload");
-    if (nranks > 1) alloc_slab(c);
+    if (slab) alloc_slab(c);
     if (sys->n_bonds > 0) setup_bonds(c, sys, fene);
 
     c->auto_cap = params->nbr_capacity <= 0;
@@ -1658,7 +1664,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // slab mode: the owner of the decomposition finishes the setup after the
     // first migration/ghost exchange (tmd_gpu_slab_*); whole box: now
     mark("list alloc");
-    if (nranks == 1) setup_pass(c);
+    if (!slab) setup_pass(c);
     mark("setup pass");
     c->step = 0;
     c->rebuilds = 0;
@@ -1681,7 +1687,7 @@ extern "C" {
 int tmd_gpu_create(const tmd_system* sys, const tmd_lj_params* lj,
                    const tmd_fene_params* fene, const tmd_engine_params* params,
                    tmd_gpu_ctx** out) {
-  return create_impl(sys, lj, fene, params, 0, 1, out);
+  return create_impl(sys, lj, fene, params, 0, 1, false, out);
 }
 
 int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
@@ -1692,7 +1698,7 @@ int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
     g_create_error = "invalid rank / nranks";
     return TMD_ERR_CONFIG;
   }
-  return create_impl(sys, lj, fene, params, rank, nranks, out);
+  return create_impl(sys, lj, fene, params, rank, nranks, true, out);
 }
 
 }  // extern "C"
@@ -2111,7 +2117,7 @@ int tmd_gpu_fp64_peak(int device, double* tflops) {
 namespace {
 
 void need_slab(const tmd_gpu_ctx* c) {
-  if (c->nranks < 2 && !c->g.zslab) {
+  if (!c->g.zslab) {
     throw StatusError{TMD_ERR_STATE, "not a slab context (use tmd_gpu_create_slab)"};
   }
 }
@@ -2516,3 +2522,14 @@ void tmd_gpu_destroy(tmd_gpu_ctx* c) {
 }
 
 }  // extern "C"
+
+#include "tmd_slab_nccl.cuh"
+
+namespace {
+void free_nccl(tmd_gpu_ctx* c) {
+#ifndef TMD_NO_NCCL
+  if (c->nccl) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl));
+#endif
+  c->nccl = nullptr;
+}
+}  // namespace

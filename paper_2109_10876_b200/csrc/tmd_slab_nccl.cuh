@@ -1,0 +1,290 @@
+// Native multi-GPU step loop of the z-slab decomposition: the
+// protocol of paper_2109_10876_b200/decomp.py, driven from C++ with NCCL on
+// the context's stream, one process (or thread) per GPU. Included at the end
+// of tmd_engine.cu (it drives the tmd_gpu_slab_* entry points and the
+// context internals).
+//
+// Per step (no rebuild): fused force + integrator kernel, boundary-layer pack,
+// one NCCL group of point-to-point sends/receives of 32-B positions into the
+// neighbours' ghost slots, an in-place MAX all-reduce of the displacement
+// word, one 8-byte device-to-host read for the host's rebuild decision. The
+// rebuild (every ~8 steps) runs the migration / border / ghost protocol with
+// its few host round trips.
+//
+// Message order. NCCL matches the point-to-point operations of a group
+// between a pair of ranks in posting order, so both ends post, per peer: the
+// message for the receiver's LOWER ghost layer first (the sender's highest
+// layer), then the one for its UPPER ghost layer (the sender's lowest layer),
+// each as counts, ids, positions. With one or two slabs the lower and upper
+// neighbour are the same rank and the order still agrees.
+#pragma once
+
+#ifndef TMD_NO_NCCL
+#include <nccl.h>
+#endif
+
+namespace {
+
+#ifndef TMD_NO_NCCL
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    throw CudaFail{std::string(what) + ": " + ncclGetErrorString(r)};
+  }
+}
+
+ncclComm_t cm(const tmd_gpu_ctx* c) { return static_cast<ncclComm_t>(c->nccl); }
+
+void rck(tmd_gpu_ctx* c, int rc) {  // a tmd_gpu_slab_* call inside the native loop
+  if (rc != TMD_OK) throw StatusError{rc, c->err};
+}
+
+// Both boundary layers to the neighbours' ghost layers (or, with
+// positions_only, just the positions of an unchanged layout).
+void nccl_ghost_exchange(tmd_gpu_ctx* c, bool positions_only) {
+  const int R = c->nranks, r = c->my_rank;
+  const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
+  const size_t dxy = static_cast<size_t>(c->g.dims[0]) * c->g.dims[1];
+  double4* pos = c->pos;
+  // my ghost destinations: lower ghost from lo (its side 1), upper from hi (its side 0)
+  int* gl_cnt = c->gcnt[0];
+  int* gh_cnt = c->gcnt[1];
+  long long* gl_id = c->id + c->n;
+  long long* gh_id = c->id + c->n + c->n_ghost_lo;
+  double4* gl_pos = pos + c->n;
+  double4* gh_pos = pos + c->n + c->n_ghost_lo;
+  auto send3 = [&](int side, int peer) {
+    if (!positions_only) {
+      nck(ncclSend(c->bcnt[side], dxy, ncclInt32, peer, cm(c), c->stream), "ncclSend");
+      if (c->nb[side]) {
+        nck(ncclSend(c->bids[side], c->nb[side], ncclInt64, peer, cm(c), c->stream),
+            "ncclSend");
+      }
+    }
+    if (c->nb[side]) {
+      nck(ncclSend(c->bpos[side], 4 * c->nb[side], ncclFloat64, peer, cm(c), c->stream),
+          "ncclSend");
+    }
+  };
+  auto recv3 = [&](int* cnt, long long* ids, double4* p, int64_t n, int peer) {
+    if (!positions_only) {
+      nck(ncclRecv(cnt, dxy, ncclInt32, peer, cm(c), c->stream), "ncclRecv");
+      if (n) nck(ncclRecv(ids, n, ncclInt64, peer, cm(c), c->stream), "ncclRecv");
+    }
+    if (n) nck(ncclRecv(p, 4 * n, ncclFloat64, peer, cm(c), c->stream), "ncclRecv");
+  };
+  nck(ncclGroupStart(), "ncclGroupStart");
+  // to hi: its lower ghost (my side 1); to lo: its upper ghost (my side 0) —
+  // when hi == lo the lower-ghost message goes first, as the receiver expects
+  send3(1, hi);
+  send3(0, lo);
+  // from lo: my lower ghost; from hi: my upper ghost (lower first per peer)
+  recv3(gl_cnt, gl_id, gl_pos, c->n_ghost_lo, lo);
+  recv3(gh_cnt, gh_id, gh_pos, c->n_ghost_hi, hi);
+  nck(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// The rebuild protocol (decomp.py DecomposedEngine._rebuild) over NCCL.
+void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
+  const int R = c->nranks, r = c->my_rank;
+  rck(c, tmd_gpu_slab_decide(c, 1, advance ? 1 : 0));
+  // 1. migration: counts all-gathered, records point to point
+  std::vector<int64_t> counts(static_cast<size_t>(R));
+  void* send = nullptr;
+  rck(c, tmd_gpu_slab_migrate_out(c, counts.data(), &send));
+  std::vector<int64_t> M(static_cast<size_t>(R) * R);
+  ck(cudaMemcpyAsync(c->nccl_i64, counts.data(), sizeof(int64_t) * R, cudaMemcpyHostToDevice,
+                     c->stream), "H2D counts");
+  nck(ncclAllGather(c->nccl_i64, c->nccl_i64 + R, R, ncclInt64, cm(c), c->stream),
+      "ncclAllGather");
+  ck(cudaMemcpyAsync(M.data(), c->nccl_i64 + R, sizeof(int64_t) * R * R,
+                     cudaMemcpyDeviceToHost, c->stream), "D2H counts");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  int64_t nrecv = 0;
+  for (int s = 0; s < R; ++s) nrecv += M[static_cast<size_t>(s) * R + r];
+  void* recv = nullptr;
+  rck(c, tmd_gpu_slab_migrate_in(c, nrecv, &recv));
+  const size_t rec = sizeof(MigRec);
+  nck(ncclGroupStart(), "ncclGroupStart");
+  int64_t off = 0;
+  for (int d = 0; d < R; ++d) {
+    if (counts[static_cast<size_t>(d)]) {
+      nck(ncclSend(static_cast<char*>(send) + off * rec, counts[static_cast<size_t>(d)] * rec,
+                   ncclUint8, d, cm(c), c->stream), "ncclSend");
+    }
+    off += counts[static_cast<size_t>(d)];
+  }
+  int64_t roff = 0;
+  for (int s = 0; s < R; ++s) {
+    const int64_t m = M[static_cast<size_t>(s) * R + r];
+    if (m) {
+      nck(ncclRecv(static_cast<char*>(recv) + roff * rec, m * rec, ncclUint8, s, cm(c),
+                   c->stream), "ncclRecv");
+    }
+    roff += m;
+  }
+  nck(ncclGroupEnd(), "ncclGroupEnd");
+  // 2. resort + boundary layers; their sizes all-gathered
+  int64_t nb[2] = {0, 0};
+  rck(c, tmd_gpu_slab_commit(c, nb));
+  std::vector<int64_t> NB(2 * static_cast<size_t>(R));
+  ck(cudaMemcpyAsync(c->nccl_i64, nb, sizeof nb, cudaMemcpyHostToDevice, c->stream), "H2D nb");
+  nck(ncclAllGather(c->nccl_i64, c->nccl_i64 + 2, 2, ncclInt64, cm(c), c->stream),
+      "ncclAllGather");
+  ck(cudaMemcpyAsync(NB.data(), c->nccl_i64 + 2, sizeof(int64_t) * 2 * R,
+                     cudaMemcpyDeviceToHost, c->stream), "D2H nb");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
+  void* gl[3];
+  void* gh[3];
+  rck(c, tmd_gpu_slab_ghost_in(c, NB[2 * static_cast<size_t>(lo) + 1],
+                               NB[2 * static_cast<size_t>(hi)], gl, gh));
+  // 3. ghost layers (counts, ids, positions), then cell ranges + list build
+  nccl_ghost_exchange(c, false);
+  rck(c, tmd_gpu_slab_ghosts_ready(c));
+}
+
+void nccl_halo(tmd_gpu_ctx* c) {
+  for (int s = 0; s < 2; ++s) {
+    if (c->nb[s] == 0) continue;
+    c->launches += 1;
+    k_pack_border<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
+        static_cast<int>(c->nb[s]), c->bidx[s], c->pos, c->bpos[s]);
+  }
+  nccl_ghost_exchange(c, true);
+}
+
+// Global max displacement^2 of this step (in place on the device word that
+// k_decide reads), brought to the host for the rebuild decision.
+double nccl_global_max_d2(tmd_gpu_ctx* c) {
+  nck(ncclAllReduce(&c->ctrl->max_d2, &c->ctrl->max_d2, 1, ncclUint64, ncclMax, cm(c),
+                    c->stream), "ncclAllReduce(max)");
+  sync_ctrl(c);
+  raise_physics(c, true);
+  if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
+  double m = 0.0;
+  std::memcpy(&m, &c->h_ctrl->max_d2, sizeof m);
+  return m;
+}
+#endif  // TMD_NO_NCCL
+
+void need_nccl(const tmd_gpu_ctx* c) {
+#ifdef TMD_NO_NCCL
+  (void)c;
+  throw StatusError{TMD_ERR_CONFIG, "this build of libtmd_gpu.so has no NCCL"};
+#else
+  if (!c->nccl) throw StatusError{TMD_ERR_STATE, "slab context has no NCCL communicator"};
+#endif
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmd_nccl_unique_id(void* id) {
+#ifdef TMD_NO_NCCL
+  (void)id;
+  g_create_error = "this build of libtmd_gpu.so has no NCCL";
+  return TMD_ERR_CONFIG;
+#else
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) {
+    g_create_error = "ncclGetUniqueId failed";
+    return TMD_ERR_CUDA;
+  }
+  std::memcpy(id, &u, sizeof u);
+  return TMD_OK;
+#endif
+}
+
+int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id) {
+  return guard(c, [&] {
+    need_slab(c);
+#ifdef TMD_NO_NCCL
+    (void)unique_id;
+    need_nccl(c);
+#else
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ncclUniqueId u;
+    std::memcpy(&u, unique_id, sizeof u);
+    ncclComm_t comm = nullptr;
+    nck(ncclCommInitRank(&comm, c->nranks, u, c->my_rank), "ncclCommInitRank");
+    c->nccl = comm;
+    c->nccl_i64 = dalloc<int64_t>(static_cast<size_t>(c->nranks) * (c->nranks + 1) + 8);
+#endif
+  });
+}
+
+int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
+  return guard(c, [&] {
+    need_slab(c);
+    need_nccl(c);
+#ifndef TMD_NO_NCCL
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    nccl_rebuild(c, false);
+    rck(c, tmd_gpu_slab_forces(c, 0));
+    sync_ctrl(c);
+    raise_physics(c, false);
+#endif
+  });
+}
+
+int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
+  return guard(c, [&] {
+    need_slab(c);
+    need_nccl(c);
+    if (nsteps < 0) throw StatusError{TMD_ERR_CONFIG, "step count must be non-negative"};
+#ifndef TMD_NO_NCCL
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (nsteps == 0) return;
+    ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    if (c->n > 0) launch_kick_drift(c);
+    nccl_halo(c);
+    for (int64_t s = 0; s < nsteps; ++s) {
+      const double m = nccl_global_max_d2(c);
+      if (m > c->g.rebuild_thr) {
+        nccl_rebuild(c, true);
+      } else {
+        rck(c, tmd_gpu_slab_decide(c, 0, 1));
+      }
+      const bool last = s + 1 == nsteps;
+      launch_forces(c, last ? kKick2 : kFused);
+      if (!last) nccl_halo(c);
+    }
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    sync_ctrl(c);
+    raise_physics(c, true);
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c->t0, c->t1), "cudaEventElapsedTime");
+    c->elapsed += 1e-3 * ms;
+    c->step = c->h_ctrl->step;
+    c->rebuilds = static_cast<uint64_t>(c->h_ctrl->rebuilds);
+#endif
+  });
+}
+
+int tmd_gpu_slab_observe(tmd_gpu_ctx* c, int64_t n_total, tmd_observables* out) {
+  return guard(c, [&] {
+    need_slab(c);
+    need_nccl(c);
+#ifndef TMD_NO_NCCL
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->launches += 1;
+    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
+                                            c->mass, c->part_ke);
+    launch_reduce_ke(c);
+    launch_reduce_pe(c);
+    nck(ncclAllReduce(c->scalars, c->scalars, 3, ncclFloat64, ncclSum, cm(c), c->stream),
+        "ncclAllReduce(sum)");
+    ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream), "D2H scalars");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    out->step = c->step;
+    out->potential = c->h_scalars[0];
+    out->virial = c->h_scalars[1];
+    out->kinetic = c->h_scalars[2];
+    out->temperature = 2.0 * out->kinetic / (3.0 * static_cast<double>(n_total));
+#endif
+  });
+}
+
+}  // extern "C"

@@ -277,6 +277,31 @@ class SlabContext:
     def launch_count(self) -> int:
         return int(_abi.lib().tmd_gpu_launch_count(self._h))
 
+    def rebuild_count(self) -> int:
+        return int(_abi.lib().tmd_gpu_rebuild_count(self._h))
+
+    # -- the native NCCL step loop (tmd_slab_nccl.cuh)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_abi.lib().tmd_nccl_unique_id(buf), None)
+        return buf.raw
+
+    def attach_nccl(self, uid: bytes) -> None:
+        buf = C.create_string_buffer(bytes(uid), 128)
+        self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf))
+
+    def setup_native(self) -> None:
+        self._c(_abi.lib().tmd_gpu_slab_setup(self._h))
+
+    def run_native(self, steps: int) -> None:
+        self._c(_abi.lib().tmd_gpu_slab_run(self._h, int(steps)))
+
+    def observe_native(self, n_total: int) -> StepObservables:
+        o = _abi.TmdObservables()
+        self._c(_abi.lib().tmd_gpu_slab_observe(self._h, int(n_total), C.byref(o)))
+        return StepObservables(int(o.step), o.kinetic, o.potential, o.temperature, o.virial)
+
     def stream_handle(self) -> int:
         return int(_abi.lib().tmd_gpu_stream(self._h) or 0)
 
@@ -313,6 +338,10 @@ class Comm:
     def barrier(self) -> None:
         pass
 
+    def broadcast_bytes(self, make) -> bytes:
+        """make() on rank 0, its bytes on every rank."""
+        raise NotImplementedError
+
 
 class InProcessComm(Comm):
     """All ranks in this process; a transfer is a tensor copy."""
@@ -329,6 +358,9 @@ class InProcessComm(Comm):
 
     def allgather(self, vals):
         return np.stack([np.asarray(vals[r], np.int64) for r in self.local_ranks])
+
+    def broadcast_bytes(self, make) -> bytes:
+        return make()
 
     def exchange(self, sends, recvs):
         box: Dict[Tuple[int, int, int], object] = {}
@@ -431,6 +463,11 @@ class TorchDistComm(Comm):
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def broadcast_bytes(self, make) -> bytes:
+        obj = [make() if self.me == 0 else None]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        return obj[0]
+
 
 # ---------------------------------------------------------------------------
 # the decomposed engine
@@ -447,13 +484,11 @@ class DecomposedEngine:
     def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
                  cfg: Optional[EngineConfig] = None, comm: Optional[Comm] = None,
                  device_of=None, ctx_factory=None, balance: str = "static",
-                 rebalance_tolerance: float = 1.05):
+                 rebalance_tolerance: float = 1.05, native: bool = False):
         cfg = cfg or EngineConfig()
         validate_engine_config(cfg)
         if comm is None:
             raise ConfigError("DecomposedEngine needs a Comm (InProcessComm / TorchDistComm)")
-        if comm.nranks < 2:
-            raise ConfigError("a decomposition needs at least 2 ranks; use Engine")
         self.comm = comm
         self.cfg = cfg
         self.n_total = flat.size()
@@ -480,6 +515,18 @@ class DecomposedEngine:
         self.steps = 0
         self.rebuilds = 0
         self.exchanged_bytes = 0
+        self.native = bool(native)
+        if self.native:
+            # the whole protocol in C++ with NCCL on each context's stream
+            # (tmd_slab_nccl.cuh): one slab per process, static cuts
+            if len(self.ctx) != 1:
+                raise ConfigError("the native NCCL loop runs one slab per process")
+            if balance != "static":
+                raise ConfigError("the native NCCL loop uses the static cuts")
+            (c,) = self.ctx.values()
+            c.attach_nccl(comm.broadcast_bytes(SlabContext.nccl_unique_id))
+            c.setup_native()
+            return
         self._rebuild(advance=False)
         for c in self.ctx.values():
             c.forces(0)
@@ -572,6 +619,12 @@ class DecomposedEngine:
             raise ConfigError("step count must be non-negative")
         if steps == 0:
             return
+        if self.native:
+            (c,) = self.ctx.values()
+            c.run_native(steps)
+            self.steps += steps
+            self.rebuilds = c.rebuild_count()
+            return
         for c in self.ctx.values():
             c.kick_drift()
         self._halo()
@@ -596,6 +649,10 @@ class DecomposedEngine:
         self.run(1)
 
     def observe(self) -> StepObservables:
+        if self.native:
+            (c,) = self.ctx.values()
+            o = c.observe_native(self.n_total)
+            return StepObservables(self.steps, o.kinetic, o.potential, o.temperature, o.virial)
         tot = self.comm.allreduce_sum({r: c.sums() for r, c in self.ctx.items()})
         pe, w, ke = (float(v) for v in tot)
         return StepObservables(self.steps, ke, pe, 2.0 * ke / (3.0 * self.n_total), w)

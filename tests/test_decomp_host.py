@@ -160,11 +160,13 @@ def test_balanced_cuts_are_optimal():
         assert max_load(c, cuts) == best
 
 
-def test_requires_two_ranks():
-    from paper_2109_10876_b200.engine import ConfigError
-    with pytest.raises(ConfigError):
-        DecomposedEngine(_system(), Interactions(), R_SKIN, comm=InProcessComm(1),
-                         ctx_factory=lambda r: None)
+def test_single_slab_exchanges_with_itself():
+    """R = 1: the slab's ghost layers are its own boundary layers (periodic
+    images); every message goes to and comes from rank 0."""
+    flat = _system()
+    eng = _make(flat, InProcessComm(1))
+    _run_and_check(eng, flat, [1, 9], lambda s: s)
+    assert eng.rebuild_count() >= 1
 
 
 def _free_port():

@@ -24,8 +24,8 @@ def slab_engine(g, R, **cfg):
                             E.EngineConfig(dt=float(g["dt"]), **cfg), comm=InProcessComm(R))
 
 
-CASES = [("fcc8_jit", 2), ("fcc8_jit", 3), ("fcc8_jit", 4), ("aniso", 2), ("aniso", 5),
-         ("aniso", 10)]
+CASES = [("fcc8_jit", 1), ("fcc8_jit", 2), ("fcc8_jit", 3), ("fcc8_jit", 4), ("aniso", 1),
+         ("aniso", 2), ("aniso", 5), ("aniso", 10)]
 
 
 @pytest.mark.parametrize("name,R", CASES)
@@ -48,7 +48,8 @@ def test_initial_state_vs_golden(name, R):
         eng.close()
 
 
-@pytest.mark.parametrize("name,R", [("fcc8_jit", 2), ("fcc8_jit", 4), ("aniso", 3)])
+@pytest.mark.parametrize("name,R", [("fcc8_jit", 1), ("fcc8_jit", 2), ("fcc8_jit", 4),
+                                    ("aniso", 3)])
 def test_trajectory_vs_golden(name, R):
     g = load(name)
     eng = slab_engine(g, R)
@@ -198,3 +199,51 @@ def test_load_aware_cuts_on_a_liquid_slab(R):
         dec.close()
         static.close()
         one.close()
+
+
+@pytest.mark.parametrize("name", ["fcc8_jit", "kg_lattice10"])
+def test_native_nccl_loop_in_process(name):
+    """The C++ step loop (tmd_slab_nccl.cuh) with a one-rank NCCL
+    communicator: the slab exchanges its boundary layers with itself."""
+    g = load(name)
+    inter = E.Interactions()
+    flat = E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"])
+    if "bonds" in g:
+        eps, sig, rc, sh = g["lj"]
+        inter = E.Interactions(lj=E.LjParams(float(eps), float(sig), float(rc), bool(sh)),
+                               fene=E.FeneParams(*map(float, g["fene"])))
+        flat = E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"], bonds=g["bonds"])
+    eng = DecomposedEngine(flat, inter, float(g["r_skin"]), E.EngineConfig(dt=float(g["dt"])),
+                           comm=InProcessComm(1), native=True)
+    try:
+        np.testing.assert_array_equal(eng.local_pairs(), g["pairs"])
+        assert_rel(eng.observe().potential, float(g["pe_fsum"]), E_RTOL, "PE")
+        eng.run(int(g["steps"]))
+        ids, pos, vel, _ = eng.local_state()
+        assert np.abs(pos - g["final_pos"]).max() < 1e-9
+        assert np.abs(vel - g["final_vel"]).max() < 1e-9
+        assert eng.rebuild_count() == int(g["rebuilds"])
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("native", [False, True])
+def test_nccl_one_rank_decomposition(native):
+    """The NCCL transport itself (torchrun, one process): the single slab
+    sends its boundary layers to itself through NCCL point-to-point batches,
+    plus the all-reduces and all-gathers of the protocol."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), str(root / "scripts" / "nccl_selftest.py"),
+                        *(["--native"] if native else [])],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ok=True" in r.stdout

@@ -1012,6 +1012,7 @@ __global__ void __launch_bounds__(128)
                 double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                 double* __restrict__ part_e, double* __restrict__ part_w,
                 const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
+  if (ctrl->halt) return;  // native slab loop: steps after a due rebuild are no-ops
   __shared__ double red[4];
   const int i = blockIdx.x * 128 + threadIdx.x;
   double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;

@@ -97,7 +97,7 @@ struct Ctrl {
   int err_bit;                // status bit of the first error (its record below)
   double err_val;             // a value for the first error's message (bond r^2)
   int obs_rows;               // observable rows recorded in this chunk (run_observed)
-  int pad2_;
+  int halt;                   // native slab loop: a rebuild is due, later steps are no-ops
 };
 
 // ---------------------------------------------------------------------------

@@ -2412,7 +2412,7 @@ int tmd_gpu_slab_halo(tmd_gpu_ctx* c, void* send[2], void* recv[2]) {
       if (c->nb[s] == 0) continue;
       c->launches += 1;
       k_pack_border<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
-          static_cast<int>(c->nb[s]), c->bidx[s], c->pos, c->bpos[s]);
+          static_cast<int>(c->nb[s]), c->bidx[s], c->pos, c->bpos[s], c->ctrl);
     }
     send[0] = c->bpos[0];
     send[1] = c->bpos[1];

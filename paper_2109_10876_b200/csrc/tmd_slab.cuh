@@ -176,9 +176,27 @@ __global__ void __launch_bounds__(kBlock)
 // Per-step halo packing: current positions of one boundary layer.
 __global__ void __launch_bounds__(kBlock)
     k_pack_border(int nb, const int* __restrict__ idx, const double4* __restrict__ pos,
-                  double4* __restrict__ out) {
+                  double4* __restrict__ out, const Ctrl* ctrl) {
+  if (ctrl->halt) return;
   const int k = blockIdx.x * kBlock + threadIdx.x;
   if (k < nb) out[k] = pos[idx[k]];
+}
+
+// Native slab loop, speculative steps: the decision of a step from the
+// globally reduced displacement word. No rebuild due: count the step and
+// reset the word. Rebuild due: raise `halt` (the step's force and pack
+// kernels and every later one of the batch return at once) and leave the
+// step uncounted — the host runs the rebuild protocol, which counts it.
+__global__ void k_decide_spec(Ctrl* ctrl, double thr) {
+  if (ctrl->halt) return;
+  const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
+  if (m > thr) {
+    ctrl->halt = 1;
+    return;
+  }
+  ctrl->rebuild = 0;
+  ctrl->max_d2 = 0ull;
+  ctrl->step += 1;
 }
 
 }  // namespace tmd

@@ -148,10 +148,12 @@ void nccl_halo(tmd_gpu_ctx* c) {
     if (c->nb[s] == 0) continue;
     c->launches += 1;
     k_pack_border<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
-        static_cast<int>(c->nb[s]), c->bidx[s], c->pos, c->bpos[s]);
+        static_cast<int>(c->nb[s]), c->bidx[s], c->pos, c->bpos[s], c->ctrl);
   }
   nccl_ghost_exchange(c, true);
 }
+
+constexpr int kSpecSteps = 16;  // steps enqueued per host round trip
 
 // Global max displacement^2 of this step (in place on the device word that
 // k_decide reads), brought to the host for the rebuild decision.
@@ -228,6 +230,15 @@ int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
   });
 }
 
+// Speculative batches: up to kSpecSteps steps are enqueued without a host
+// round trip, each as MAX all-reduce of the displacement word -> on-device
+// decision (k_decide_spec) -> fused force/integrator kernel -> pack -> halo.
+// When a step needs a rebuild its decision raises `halt`: that step's and the
+// rest of the batch's kernels return at once (the halo messages still run and
+// re-deliver unchanged positions), and after the batch's single sync the host
+// runs the rebuild protocol and that step's forces, then continues. Every
+// rank takes the same decisions (the word is all-reduced), so all halt at the
+// same step.
 int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
   return guard(c, [&] {
     need_slab(c);
@@ -237,18 +248,50 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (nsteps == 0) return;
     ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    const int64_t start = c->step, target = c->step + nsteps;
     if (c->n > 0) launch_kick_drift(c);
     nccl_halo(c);
-    for (int64_t s = 0; s < nsteps; ++s) {
-      const double m = nccl_global_max_d2(c);
-      if (m > c->g.rebuild_thr) {
-        nccl_rebuild(c, true);
-      } else {
-        rck(c, tmd_gpu_slab_decide(c, 0, 1));
+    int64_t done_step = start;  // steps completed (host view)
+    while (done_step < target) {
+      const int64_t K = std::min<int64_t>(kSpecSteps, target - done_step);
+      int64_t fused = 0;
+      for (int64_t s = 0; s < K; ++s) {
+        nck(ncclAllReduce(&c->ctrl->max_d2, &c->ctrl->max_d2, 1, ncclUint64, ncclMax, cm(c),
+                          c->stream), "ncclAllReduce(max)");
+        c->launches += 1;
+        k_decide_spec<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr);
+        const bool last = done_step + s + 1 == target;
+        c->launches += 1;
+        launch_forces(c, last ? kKick2 : kFused);
+        if (!last) {
+          ++fused;
+          nccl_halo(c);
+        }
       }
-      const bool last = s + 1 == nsteps;
+      sync_ctrl(c);
+      raise_physics(c, true);
+      if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
+      const int64_t advanced = c->h_ctrl->step - done_step;  // steps that ran
+      if (!c->h_ctrl->halt) {
+        done_step += K;
+        continue;
+      }
+      // the launches from the halted step on were no-ops: undo their buffer
+      // flips on the host (the device never swapped)
+      const int64_t noop_fused = fused - advanced;
+      if (noop_fused & 1) {
+        c->cur ^= 1;
+        c->pos = c->posb[c->cur];
+      }
+      done_step += advanced;
+      const int zero = 0;
+      ck(cudaMemcpyAsync(&c->ctrl->halt, &zero, sizeof(int), cudaMemcpyHostToDevice, c->stream),
+         "clear halt");
+      nccl_rebuild(c, true);  // counts the step and the rebuild
+      const bool last = done_step + 1 == target;
       launch_forces(c, last ? kKick2 : kFused);
       if (!last) nccl_halo(c);
+      done_step += 1;
     }
     ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
     sync_ctrl(c);

@@ -379,8 +379,8 @@ def run_decomposed(args) -> None:
     balance = "count" if args.config == "slab" else "static"
 
     # the C++ step loop with NCCL on the context stream (tmd_slab_nccl.cuh);
-    # the Python protocol for the gloo pipeline check and load-aware cuts
-    native = args.dist_backend == "nccl" and balance == "static"
+    # the Python protocol for the gloo pipeline check
+    native = args.dist_backend == "nccl"
 
     def make():
         return DecomposedEngine(flat, w.inter, w.r_skin, ecfg, comm=TorchDistComm(),

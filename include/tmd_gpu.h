@@ -249,8 +249,9 @@ int tmd_gpu_create_slab(const tmd_system* sys, const tmd_lj_params* lj,
                         int rank, int nranks, tmd_gpu_ctx** out);
 
 /* info: rank, nranks, first owned z layer, owned layers, owned particles,
- * lower ghosts, upper ghosts, cells per layer, slot capacity, record bytes. */
-int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[10]);
+ * lower ghosts, upper ghosts, cells per layer, slot capacity, record bytes,
+ * re-cuts of the native loop. */
+int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[11]);
 
 /* Native step loop of the decomposition (one process or thread per GPU):
  * the same protocol driven from C++ with NCCL on the context's stream.
@@ -260,9 +261,11 @@ int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[10]);
  * migration / ghost exchange + forces (tmd_gpu_slab_setup), and steps
  * (tmd_gpu_slab_run: collective, the same nsteps on every rank; per step one
  * NCCL group of halo sends/receives, one MAX all-reduce and an 8-byte read
- * for the rebuild decision). tmd_gpu_slab_observe all-reduces PE, W, KE. */
+ * for the rebuild decision). balance_count != 0: load-aware cut planes
+ * re-evaluated at every rebuild (tmd_gpu_slab_layer_counts summed with an
+ * NCCL all-reduce). tmd_gpu_slab_observe all-reduces PE, W, KE. */
 int tmd_nccl_unique_id(void* id);
-int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id);
+int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id, int balance_count);
 int tmd_gpu_slab_setup(tmd_gpu_ctx* ctx);
 int tmd_gpu_slab_run(tmd_gpu_ctx* ctx, int64_t nsteps);
 int tmd_gpu_slab_observe(tmd_gpu_ctx* ctx, int64_t n_total, tmd_observables* out);
@@ -276,6 +279,9 @@ int tmd_gpu_slab_observe(tmd_gpu_ctx* ctx, int64_t n_total, tmd_observables* out
  * inhomogeneous systems, the role autotune_subnodes + work stealing play on
  * the CPU (engine.hpp:293-373, task_pool.hpp:85-106). */
 int tmd_gpu_slab_layer_counts(tmd_gpu_ctx* ctx, int64_t* counts);
+/* The cut planes the native loop picks from summed layer counts: contiguous
+ * slabs minimising the largest population, each >= 1 layer (host only). */
+int tmd_balanced_cuts(const int64_t* counts, int dims_z, int nranks, int32_t* cuts);
 int tmd_gpu_slab_recut(tmd_gpu_ctx* ctx, const int32_t* cuts);
 
 /* Largest squared displacement since the last build over the owned particles

@@ -37,7 +37,7 @@ EXPORTS = [
     "tmd_gpu_slab_recut", "tmd_gen_chains", "tmd_gpu_brute_force", "tmd_gen_lattice",
     "tmd_gen_spherical", "tmd_gen_random", "tmd_gpu_run_observed", "tmd_nccl_unique_id",
     "tmd_gpu_slab_attach_nccl", "tmd_gpu_slab_setup", "tmd_gpu_slab_run",
-    "tmd_gpu_slab_observe",
+    "tmd_gpu_slab_observe", "tmd_balanced_cuts",
 ]
 
 
@@ -122,7 +122,8 @@ def lib() -> C.CDLL:
     L.tmd_gpu_slab_sums.argtypes = [P, P]
     L.tmd_gpu_slab_layer_counts.argtypes = [P, P]
     L.tmd_nccl_unique_id.argtypes = [P]
-    L.tmd_gpu_slab_attach_nccl.argtypes = [P, P]
+    L.tmd_balanced_cuts.argtypes = [P, C.c_int, C.c_int, P]
+    L.tmd_gpu_slab_attach_nccl.argtypes = [P, P, C.c_int]
     L.tmd_gpu_slab_setup.argtypes = [P]
     L.tmd_gpu_slab_run.argtypes = [P, C.c_int64]
     L.tmd_gpu_slab_observe.argtypes = [P, C.c_int64, C.POINTER(TmdObservables)]

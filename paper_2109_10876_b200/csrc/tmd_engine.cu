@@ -164,6 +164,9 @@ struct tmd_gpu_ctx {
   int64_t nb[2] = {0, 0};
   int* gcnt[2] = {nullptr, nullptr};            // received ghost-layer counts (lo, hi)
   void* nccl = nullptr;          // ncclComm_t of the native slab loop (tmd_slab_nccl.cuh)
+  bool balance_count = false;    // native loop: load-aware cut planes at rebuilds
+  std::vector<int> cuts;         // current cut planes (native loop)
+  int64_t recuts = 0;
   int64_t* nccl_i64 = nullptr;   // staging for all-gathered counts
   double *part_e = nullptr, *part_w = nullptr, *part_ke = nullptr;
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
@@ -1264,7 +1267,8 @@ void upload_owner_table(tmd_gpu_ctx* c, const std::vector<int>& cuts) {
 void alloc_slab(tmd_gpu_ctx* c) {
   const size_t n = static_cast<size_t>(c->n_cap);
   c->owner_of_z = dalloc<int>(static_cast<size_t>(c->g.dims[2]));
-  upload_owner_table(c, default_cuts(c->g.dims[2], c->nranks));
+  c->cuts = default_cuts(c->g.dims[2], c->nranks);
+  upload_owner_table(c, c->cuts);
   c->mig_dest = dalloc<int>(n);
   c->mig_count = dalloc<int>(2 * static_cast<size_t>(c->nranks));
   c->mig_off = dalloc<int>(static_cast<size_t>(c->nranks) + 1);
@@ -2134,7 +2138,7 @@ void ensure_groups(tmd_gpu_ctx* c) {
 
 }  // namespace
 
-int tmd_gpu_slab_info(tmd_gpu_ctx* c, int64_t info[10]) {
+int tmd_gpu_slab_info(tmd_gpu_ctx* c, int64_t info[11]) {
   return guard(c, [&] {
     info[0] = c->my_rank;
     info[1] = c->nranks;
@@ -2146,6 +2150,7 @@ int tmd_gpu_slab_info(tmd_gpu_ctx* c, int64_t info[10]) {
     info[7] = static_cast<int64_t>(c->g.dims[0]) * c->g.dims[1];
     info[8] = c->n_cap;
     info[9] = static_cast<int64_t>(sizeof(MigRec));
+    info[10] = c->recuts;
   });
 }
 

@@ -25,6 +25,59 @@
 
 namespace {
 
+// Contiguous cut planes over the z layers minimising the largest slab
+// population, every slab >= 1 layer (decomp.py balanced_cuts: binary search
+// on the bound + greedy fill, then the widest slabs halved).
+std::vector<int> balanced_cuts(const std::vector<int64_t>& cnt, int R) {
+  const int dz = static_cast<int>(cnt.size());
+  auto greedy = [&](int64_t bound) {
+    std::vector<int> starts{0};
+    int64_t acc = 0;
+    for (int z = 0; z < dz; ++z) {
+      if (z > starts.back() && acc + cnt[static_cast<size_t>(z)] > bound) {
+        starts.push_back(z);
+        acc = 0;
+      }
+      acc += cnt[static_cast<size_t>(z)];
+    }
+    return starts;
+  };
+  int64_t lo = *std::max_element(cnt.begin(), cnt.end()), hi = lo;
+  for (int64_t v : cnt) hi += v;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (static_cast<int>(greedy(mid).size()) <= R) {
+      hi = mid;
+    } else {
+      lo = mid + 1;
+    }
+  }
+  std::vector<int> starts = greedy(lo);
+  while (static_cast<int>(starts.size()) < R) {
+    int wi = 0, wmax = -1;
+    for (size_t i = 0; i < starts.size(); ++i) {
+      const int e = i + 1 < starts.size() ? starts[i + 1] : dz;
+      if (e - starts[i] > wmax) {
+        wmax = e - starts[i];
+        wi = static_cast<int>(i);
+      }
+    }
+    starts.insert(starts.begin() + wi + 1, starts[static_cast<size_t>(wi)] + wmax / 2);
+  }
+  starts.push_back(dz);
+  return starts;
+}
+
+int64_t max_load(const std::vector<int64_t>& cnt, const std::vector<int>& cuts) {
+  int64_t m = 0;
+  for (size_t r = 0; r + 1 < cuts.size(); ++r) {
+    int64_t s = 0;
+    for (int z = cuts[r]; z < cuts[r + 1]; ++z) s += cnt[static_cast<size_t>(z)];
+    m = std::max(m, s);
+  }
+  return m;
+}
+
 #ifndef TMD_NO_NCCL
 void nck(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) {
@@ -83,10 +136,34 @@ void nccl_ghost_exchange(tmd_gpu_ctx* c, bool positions_only) {
   nck(ncclGroupEnd(), "ncclGroupEnd");
 }
 
+// Load-aware cut planes (row f3) before a migration: per-layer counts summed
+// over ranks, re-cut when the current largest slab exceeds the optimum by
+// more than 5 %.
+void nccl_rebalance(tmd_gpu_ctx* c) {
+  const int dz = c->g.dims[2], R = c->nranks;
+  std::vector<int64_t> cnt(static_cast<size_t>(dz));
+  rck(c, tmd_gpu_slab_layer_counts(c, cnt.data()));
+  int64_t* d = dalloc<int64_t>(static_cast<size_t>(dz));
+  ck(cudaMemcpyAsync(d, cnt.data(), sizeof(int64_t) * dz, cudaMemcpyHostToDevice, c->stream),
+     "H2D layer counts");
+  nck(ncclAllReduce(d, d, dz, ncclInt64, ncclSum, cm(c), c->stream), "ncclAllReduce(sum)");
+  ck(cudaMemcpyAsync(cnt.data(), d, sizeof(int64_t) * dz, cudaMemcpyDeviceToHost, c->stream),
+     "D2H layer counts");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  cudaFree(d);
+  const std::vector<int> best = balanced_cuts(cnt, R);
+  if (static_cast<double>(max_load(cnt, c->cuts)) > 1.05 * static_cast<double>(max_load(cnt, best))) {
+    rck(c, tmd_gpu_slab_recut(c, best.data()));
+    c->cuts = best;
+    c->recuts += 1;
+  }
+}
+
 // The rebuild protocol (decomp.py DecomposedEngine._rebuild) over NCCL.
 void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   const int R = c->nranks, r = c->my_rank;
   rck(c, tmd_gpu_slab_decide(c, 1, advance ? 1 : 0));
+  if (c->balance_count) nccl_rebalance(c);
   // 1. migration: counts all-gathered, records point to point
   std::vector<int64_t> counts(static_cast<size_t>(R));
   void* send = nullptr;
@@ -182,6 +259,14 @@ void need_nccl(const tmd_gpu_ctx* c) {
 
 extern "C" {
 
+int tmd_balanced_cuts(const int64_t* counts, int dims_z, int nranks, int32_t* cuts) {
+  if (!counts || !cuts || nranks < 1 || dims_z < nranks) return TMD_ERR_CONFIG;
+  const std::vector<int64_t> cnt(counts, counts + dims_z);
+  const std::vector<int> best = balanced_cuts(cnt, nranks);
+  for (int r = 0; r <= nranks; ++r) cuts[r] = best[static_cast<size_t>(r)];
+  return TMD_OK;
+}
+
 int tmd_nccl_unique_id(void* id) {
 #ifdef TMD_NO_NCCL
   (void)id;
@@ -198,8 +283,9 @@ int tmd_nccl_unique_id(void* id) {
 #endif
 }
 
-int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id) {
+int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id, int balance_count) {
   return guard(c, [&] {
+    c->balance_count = balance_count != 0;
     need_slab(c);
 #ifdef TMD_NO_NCCL
     (void)unique_id;

@@ -169,10 +169,10 @@ class SlabContext:
 
     # -- protocol
     def info(self) -> dict:
-        a = np.zeros(10, np.int64)
+        a = np.zeros(11, np.int64)
         self._c(_abi.lib().tmd_gpu_slab_info(self._h, _ptr(a)))
         keys = ("rank", "nranks", "z0", "zown", "n_own", "n_lo", "n_hi", "dxy", "n_cap",
-                "rec_bytes")
+                "rec_bytes", "recuts")
         return dict(zip(keys, (int(v) for v in a)))
 
     def max_d2(self) -> float:
@@ -287,9 +287,9 @@ class SlabContext:
         _check(_abi.lib().tmd_nccl_unique_id(buf), None)
         return buf.raw
 
-    def attach_nccl(self, uid: bytes) -> None:
+    def attach_nccl(self, uid: bytes, balance_count: bool = False) -> None:
         buf = C.create_string_buffer(bytes(uid), 128)
-        self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf))
+        self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf, 1 if balance_count else 0))
 
     def setup_native(self) -> None:
         self._c(_abi.lib().tmd_gpu_slab_setup(self._h))
@@ -521,11 +521,11 @@ class DecomposedEngine:
             # (tmd_slab_nccl.cuh): one slab per process, static cuts
             if len(self.ctx) != 1:
                 raise ConfigError("the native NCCL loop runs one slab per process")
-            if balance != "static":
-                raise ConfigError("the native NCCL loop uses the static cuts")
             (c,) = self.ctx.values()
-            c.attach_nccl(comm.broadcast_bytes(SlabContext.nccl_unique_id))
+            c.attach_nccl(comm.broadcast_bytes(SlabContext.nccl_unique_id),
+                          balance_count=balance == "count")
             c.setup_native()
+            self.recuts = c.info()["recuts"]
             return
         self._rebuild(advance=False)
         for c in self.ctx.values():
@@ -624,6 +624,7 @@ class DecomposedEngine:
             c.run_native(steps)
             self.steps += steps
             self.rebuilds = c.rebuild_count()
+            self.recuts = c.info()["recuts"]
             return
         for c in self.ctx.values():
             c.kick_drift()

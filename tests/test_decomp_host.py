@@ -221,3 +221,20 @@ def test_gloo_protocol(world, balance):
     ke = 0.5 * float(np.sum(flat.vel ** 2))
     for r in res:
         assert r[3] == pytest.approx(ke, rel=1e-12)
+
+
+def test_native_balanced_cuts_match_the_python_rule():
+    """tmd_balanced_cuts (the native loop's choice, C++) == decomp.balanced_cuts."""
+    import ctypes
+    from paper_2109_10876_b200 import _abi
+    from paper_2109_10876_b200.decomp import balanced_cuts
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        dz = int(rng.integers(3, 40))
+        R = int(rng.integers(1, min(dz, 9) + 1))
+        c = rng.choice([0, 0, 1, 5, 20, 100, 1000], size=dz).astype(np.int64)
+        out = np.zeros(R + 1, np.int32)
+        rc = _abi.lib().tmd_balanced_cuts(c.ctypes.data_as(ctypes.c_void_p), dz, R,
+                                          out.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        assert out.tolist() == balanced_cuts(c, R)

@@ -247,3 +247,24 @@ def test_nccl_one_rank_decomposition(native):
                        cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "ok=True" in r.stdout
+
+
+def test_native_loop_with_load_aware_cuts_runs_the_rebalance_path():
+    """balance = "count" in the native loop: layer histograms summed by an
+    NCCL all-reduce and the C++ cut rule at every rebuild (one rank: the
+    cuts stay [0, dims_z]); the run tracks the single-context engine."""
+    flat = E.gen_fcc_slab(8, 0.8442, 0.7, 5)
+    cfg = E.EngineConfig(dt=0.005, section_timers=False)
+    one = E.Engine(flat, E.Interactions(), 0.3, cfg)
+    dec = DecomposedEngine(flat, E.Interactions(), 0.3, cfg, comm=InProcessComm(1),
+                           balance="count", native=True)
+    try:
+        one.run(60)
+        dec.run(60)
+        assert dec.recuts == 0 and dec.rebuild_count() == one.rebuild_count() > 0
+        assert_rel(dec.observe().potential, one.observe().potential, 1e-10, "PE")
+        ids, pos, vel, f = dec.local_state()
+        assert np.abs(pos - one.flatten().pos).max() < 1e-9
+    finally:
+        dec.close()
+        one.close()

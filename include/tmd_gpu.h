@@ -261,11 +261,14 @@ int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[11]);
  * migration / ghost exchange + forces (tmd_gpu_slab_setup), and steps
  * (tmd_gpu_slab_run: collective, the same nsteps on every rank; per step one
  * NCCL group of halo sends/receives, one MAX all-reduce and an 8-byte read
- * for the rebuild decision). balance_count != 0: load-aware cut planes
+ * for the rebuild decision). flags bit 0: load-aware cut planes
  * re-evaluated at every rebuild (tmd_gpu_slab_layer_counts summed with an
- * NCCL all-reduce). tmd_gpu_slab_observe all-reduces PE, W, KE. */
+ * NCCL all-reduce); bit 1: fused halo — the force kernel's epilogue stores
+ * boundary particles' new positions straight into the neighbours' ghost
+ * slots (CUDA IPC peer memory over NVLink), replacing the per-step pack +
+ * NCCL point-to-point. tmd_gpu_slab_observe all-reduces PE, W, KE. */
 int tmd_nccl_unique_id(void* id);
-int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id, int balance_count);
+int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id, int flags);
 int tmd_gpu_slab_setup(tmd_gpu_ctx* ctx);
 int tmd_gpu_slab_run(tmd_gpu_ctx* ctx, int64_t nsteps);
 int tmd_gpu_slab_observe(tmd_gpu_ctx* ctx, int64_t n_total, tmd_observables* out);

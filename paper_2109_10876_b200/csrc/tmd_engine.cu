@@ -165,6 +165,11 @@ struct tmd_gpu_ctx {
   int* gcnt[2] = {nullptr, nullptr};            // received ghost-layer counts (lo, hi)
   void* nccl = nullptr;          // ncclComm_t of the native slab loop (tmd_slab_nccl.cuh)
   bool balance_count = false;    // native loop: load-aware cut planes at rebuilds
+  bool fused_halo = false;       // native loop: positions to the neighbours from the epilogue
+  bool fused_ready = false;      // remote ghost addresses valid for the current layout
+  int2* exp = nullptr;           // [n_cap] export map (slab mode)
+  double4* rg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][parity]
+  std::vector<std::pair<std::array<char, 64>, void*>> ipc_open;  // opened peer buffers
   std::vector<int> cuts;         // current cut planes (native loop)
   int64_t recuts = 0;
   int64_t* nccl_i64 = nullptr;   // staging for all-gathered counts
@@ -264,7 +269,7 @@ void free_all(tmd_gpu_ctx* c) {
                   c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
                   c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1],
                   c->slot_of_id, c->bond_off, c->bond_nbr, c->bond_anchor, c->bnd_cnt,
-                  c->bnd_ent};
+                  c->bnd_ent, c->nccl_i64, c->exp};
   for (void* p : ptrs) {
     if (p) cudaFree(p);
   }
@@ -464,6 +469,10 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
   it.bt = c->bt;
   it.bt.cnt = c->bnd_cnt;
   it.bt.ent = c->bnd_ent;
+  const bool fh = kMode == kFused && c->fused_halo && c->fused_ready;
+  it.exp = fh ? c->exp : nullptr;
+  it.rg[0] = fh ? c->rg[0][c->cur ^ 1] : nullptr;
+  it.rg[1] = fh ? c->rg[1][c->cur ^ 1] : nullptr;
   if (c->variant == 1) {
     k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
@@ -1270,6 +1279,7 @@ void alloc_slab(tmd_gpu_ctx* c) {
   c->cuts = default_cuts(c->g.dims[2], c->nranks);
   upload_owner_table(c, c->cuts);
   c->mig_dest = dalloc<int>(n);
+  c->exp = dalloc<int2>(n);
   c->mig_count = dalloc<int>(2 * static_cast<size_t>(c->nranks));
   c->mig_off = dalloc<int>(static_cast<size_t>(c->nranks) + 1);
   c->mig_keep = dalloc<int>(1);
@@ -1321,6 +1331,7 @@ void grow_capacity(tmd_gpu_ctx* c, int64_t need) {
   regrow(c->ck_fx, 0); regrow(c->ck_fy, 0); regrow(c->ck_fz, 0);
   regrow(c->mig_dest, 0); regrow(c->mig_send, 0); regrow(c->mig_recv, 0);
   regrow(c->bnd_cnt, 0);
+  regrow(c->exp, 0);
   if (c->bnd_ent) {  // kMaxBonds entries per slot
     uint32_t* q = dalloc<uint32_t>(nn * kMaxBonds);
     ck(cudaMemcpy(q, c->bnd_ent, o * kMaxBonds * sizeof(uint32_t), cudaMemcpyDeviceToDevice),
@@ -2315,6 +2326,7 @@ int tmd_gpu_slab_commit(tmd_gpu_ctx* c, int64_t nb_out[2]) {
                                                c->pos, c->id, c->bidx[s], c->bids[s],
                                                c->bpos[s]);
     }
+    c->fused_ready = false;  // the layout changed: remote ghost addresses are re-exchanged
     int tot[2] = {0, 0};
     for (int s = 0; s < 2; ++s) {
       ck(cudaMemcpyAsync(&tot[s], c->boff[s] + dxy, sizeof(int), cudaMemcpyDeviceToHost,
@@ -2326,6 +2338,14 @@ int tmd_gpu_slab_commit(tmd_gpu_ctx* c, int64_t nb_out[2]) {
     for (int s = 0; s < 2; ++s) {
       c->nb[s] = tot[s];
       nb_out[s] = tot[s];
+    }
+    // export map of the fused halo (slot -> index in each side's export)
+    c->launches += 3;
+    k_fill_int2<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->exp, make_int2(-1, -1));
+    for (int s = 0; s < 2; ++s) {
+      if (c->nb[s] == 0) continue;
+      k_export_map<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
+          static_cast<int>(c->nb[s]), c->bidx[s], s, c->exp);
     }
   });
 }
@@ -2532,6 +2552,8 @@ void tmd_gpu_destroy(tmd_gpu_ctx* c) {
 
 namespace {
 void free_nccl(tmd_gpu_ctx* c) {
+  for (auto& e : c->ipc_open) cudaIpcCloseMemHandle(e.second);
+  c->ipc_open.clear();
 #ifndef TMD_NO_NCCL
   if (c->nccl) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl));
 #endif

@@ -60,6 +60,12 @@ struct Integ {
   double* part_ke;
   Thermo th;  // Langevin bath (off: NVE)
   BondTab bt; // FENE bonds (off: LJ only)
+  // Fused halo (native slab loop): exp[i] = index of slot i in the export of
+  // my lowest (.x) / highest (.y) layer, or -1; rg[0] / rg[1] = those layers'
+  // ghost copies in the lower / upper neighbour's next-step position buffer
+  // (peer memory over NVLink, or this GPU's own ghost slots with one slab).
+  const int2* exp;
+  double4* rg[2];
 };
 
 // FENE forces of slot i (compute_bonded_forces, bonded.hpp:167-199): the bond
@@ -142,6 +148,12 @@ __device__ __forceinline__ void integrate_one(int i, const double4& pi, double& 
     p.z = __dadd_rn(pi.z, __dmul_rn(uz, it.dt));
     p.w = 0.0;
     it.pos_out[i] = p;
+    if (it.exp) {  // boundary particle: its new position straight into the neighbours' ghosts
+      const int2 e = it.exp[i];
+      if (e.x >= 0) it.rg[0][e.x] = p;
+      if (e.y >= 0) it.rg[1][e.y] = p;
+      if (e.x >= 0 || e.y >= 0) __threadfence_system();
+    }
     const double4 s = it.snap[i];
     d2 = fmax(d2, exact_r2(__dsub_rn(p.x, s.x), __dsub_rn(p.y, s.y), __dsub_rn(p.z, s.z)));
   }

@@ -173,6 +173,25 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// Export map of the fused halo: slot -> index in the side's export, -1 if
+// the slot is not in that boundary layer (a one-layer slab has both).
+__global__ void __launch_bounds__(kBlock)
+    k_export_map(int nb, const int* __restrict__ idx, int side, int2* __restrict__ exp) {
+  const int e = blockIdx.x * kBlock + threadIdx.x;
+  if (e >= nb) return;
+  int2* t = exp + idx[e];
+  if (side == 0) {
+    t->x = e;
+  } else {
+    t->y = e;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_fill_int2(int n, int2* __restrict__ a, int2 v) {
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
 // Per-step halo packing: current positions of one boundary layer.
 __global__ void __launch_bounds__(kBlock)
     k_pack_border(int nb, const int* __restrict__ idx, const double4* __restrict__ pos,

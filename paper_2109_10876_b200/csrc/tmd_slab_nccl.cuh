@@ -19,6 +19,8 @@
 // neighbour are the same rank and the order still agrees.
 #pragma once
 
+#include <unistd.h>
+
 #ifndef TMD_NO_NCCL
 #include <nccl.h>
 #endif
@@ -159,6 +161,68 @@ void nccl_rebalance(tmd_gpu_ctx* c) {
   }
 }
 
+// Fused halo: every rank publishes where its ghost layers live (CUDA IPC
+// handles of both position buffers + the ghost offsets of the current
+// layout); each rank maps its neighbours' buffers (peer memory over NVLink,
+// its own buffers when the neighbour is itself) so that the force kernel's
+// epilogue stores boundary particles' new positions straight into the
+// neighbours' ghost slots. The per-step MAX all-reduce that precedes every
+// force kernel orders those stores against the neighbours' reads (a rank's
+// next force kernel starts only after every rank's previous one finished).
+struct PeerInfo {
+  cudaIpcMemHandle_t h[2];
+  unsigned long long base[2];
+  long long pid;
+  long long ghost_lo_off, ghost_hi_off;
+};
+
+double4* peer_buffer(tmd_gpu_ctx* c, const PeerInfo& p, int peer, int b) {
+  if (peer == c->my_rank) return c->posb[b];
+  if (p.pid == static_cast<long long>(getpid())) {
+    return reinterpret_cast<double4*>(p.base[b]);
+  }
+  std::array<char, 64> key;
+  std::memcpy(key.data(), &p.h[b], 64);
+  for (const auto& e : c->ipc_open) {
+    if (e.first == key) return static_cast<double4*>(e.second);
+  }
+  void* ptr = nullptr;
+  ck(cudaIpcOpenMemHandle(&ptr, p.h[b], cudaIpcMemLazyEnablePeerAccess),
+     "cudaIpcOpenMemHandle");
+  c->ipc_open.emplace_back(key, ptr);
+  return static_cast<double4*>(ptr);
+}
+
+void nccl_publish_ghosts(tmd_gpu_ctx* c) {
+  const int R = c->nranks, r = c->my_rank;
+  PeerInfo me{};
+  for (int b = 0; b < 2; ++b) {
+    ck(cudaIpcGetMemHandle(&me.h[b], c->posb[b]), "cudaIpcGetMemHandle");
+    me.base[b] = reinterpret_cast<unsigned long long>(c->posb[b]);
+  }
+  me.pid = static_cast<long long>(getpid());
+  me.ghost_lo_off = c->n;
+  me.ghost_hi_off = c->n + c->n_ghost_lo;
+  const size_t sz = sizeof(PeerInfo);
+  char* d = dalloc<char>(sz * (static_cast<size_t>(R) + 1));
+  ck(cudaMemcpyAsync(d, &me, sz, cudaMemcpyHostToDevice, c->stream), "H2D peer info");
+  nck(ncclAllGather(d, d + sz, sz, ncclUint8, cm(c), c->stream), "ncclAllGather(peer info)");
+  std::vector<PeerInfo> all(static_cast<size_t>(R));
+  ck(cudaMemcpyAsync(all.data(), d + sz, sz * R, cudaMemcpyDeviceToHost, c->stream),
+     "D2H peer info");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  cudaFree(d);
+  const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
+  for (int b = 0; b < 2; ++b) {
+    // my lowest layer -> lo's upper ghost; my highest layer -> hi's lower ghost
+    c->rg[0][b] = peer_buffer(c, all[static_cast<size_t>(lo)], lo, b) +
+                  all[static_cast<size_t>(lo)].ghost_hi_off;
+    c->rg[1][b] = peer_buffer(c, all[static_cast<size_t>(hi)], hi, b) +
+                  all[static_cast<size_t>(hi)].ghost_lo_off;
+  }
+  c->fused_ready = true;
+}
+
 // The rebuild protocol (decomp.py DecomposedEngine._rebuild) over NCCL.
 void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   const int R = c->nranks, r = c->my_rank;
@@ -218,7 +282,10 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   // 3. ghost layers (counts, ids, positions), then cell ranges + list build
   nccl_ghost_exchange(c, false);
   rck(c, tmd_gpu_slab_ghosts_ready(c));
+  if (c->fused_halo) nccl_publish_ghosts(c);
 }
+
+bool fused(const tmd_gpu_ctx* c) { return c->fused_halo && c->fused_ready; }
 
 void nccl_halo(tmd_gpu_ctx* c) {
   for (int s = 0; s < 2; ++s) {
@@ -283,9 +350,10 @@ int tmd_nccl_unique_id(void* id) {
 #endif
 }
 
-int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id, int balance_count) {
+int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id, int flags) {
   return guard(c, [&] {
-    c->balance_count = balance_count != 0;
+    c->balance_count = (flags & 1) != 0;
+    c->fused_halo = (flags & 2) != 0;
     need_slab(c);
 #ifdef TMD_NO_NCCL
     (void)unique_id;
@@ -340,7 +408,7 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
     int64_t done_step = start;  // steps completed (host view)
     while (done_step < target) {
       const int64_t K = std::min<int64_t>(kSpecSteps, target - done_step);
-      int64_t fused = 0;
+      int64_t fused_launches = 0;
       for (int64_t s = 0; s < K; ++s) {
         nck(ncclAllReduce(&c->ctrl->max_d2, &c->ctrl->max_d2, 1, ncclUint64, ncclMax, cm(c),
                           c->stream), "ncclAllReduce(max)");
@@ -348,10 +416,11 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
         k_decide_spec<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr);
         const bool last = done_step + s + 1 == target;
         c->launches += 1;
+        const bool fh = fused(c);  // the force epilogue delivers the halo itself
         launch_forces(c, last ? kKick2 : kFused);
         if (!last) {
-          ++fused;
-          nccl_halo(c);
+          ++fused_launches;
+          if (!fh) nccl_halo(c);
         }
       }
       sync_ctrl(c);
@@ -364,7 +433,7 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
       }
       // the launches from the halted step on were no-ops: undo their buffer
       // flips on the host (the device never swapped)
-      const int64_t noop_fused = fused - advanced;
+      const int64_t noop_fused = fused_launches - advanced;
       if (noop_fused & 1) {
         c->cur ^= 1;
         c->pos = c->posb[c->cur];
@@ -375,8 +444,9 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
          "clear halt");
       nccl_rebuild(c, true);  // counts the step and the rebuild
       const bool last = done_step + 1 == target;
+      const bool fh = fused(c);
       launch_forces(c, last ? kKick2 : kFused);
-      if (!last) nccl_halo(c);
+      if (!last && !fh) nccl_halo(c);
       done_step += 1;
     }
     ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");

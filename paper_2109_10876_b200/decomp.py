@@ -287,9 +287,11 @@ class SlabContext:
         _check(_abi.lib().tmd_nccl_unique_id(buf), None)
         return buf.raw
 
-    def attach_nccl(self, uid: bytes, balance_count: bool = False) -> None:
+    def attach_nccl(self, uid: bytes, balance_count: bool = False,
+                    fused_halo: bool = True) -> None:
         buf = C.create_string_buffer(bytes(uid), 128)
-        self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf, 1 if balance_count else 0))
+        flags = (1 if balance_count else 0) | (2 if fused_halo else 0)
+        self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf, flags))
 
     def setup_native(self) -> None:
         self._c(_abi.lib().tmd_gpu_slab_setup(self._h))
@@ -484,7 +486,8 @@ class DecomposedEngine:
     def __init__(self, flat: FlatConfig, inter: Interactions, r_skin: float,
                  cfg: Optional[EngineConfig] = None, comm: Optional[Comm] = None,
                  device_of=None, ctx_factory=None, balance: str = "static",
-                 rebalance_tolerance: float = 1.05, native: bool = False):
+                 rebalance_tolerance: float = 1.05, native: bool = False,
+                 halo: str = "fused"):
         cfg = cfg or EngineConfig()
         validate_engine_config(cfg)
         if comm is None:
@@ -522,8 +525,10 @@ class DecomposedEngine:
             if len(self.ctx) != 1:
                 raise ConfigError("the native NCCL loop runs one slab per process")
             (c,) = self.ctx.values()
+            if halo not in ("fused", "nccl"):
+                raise ConfigError(f"unknown halo mode {halo!r} (fused | nccl)")
             c.attach_nccl(comm.broadcast_bytes(SlabContext.nccl_unique_id),
-                          balance_count=balance == "count")
+                          balance_count=balance == "count", fused_halo=halo == "fused")
             c.setup_native()
             self.recuts = c.info()["recuts"]
             return

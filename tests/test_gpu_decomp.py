@@ -201,8 +201,9 @@ def test_load_aware_cuts_on_a_liquid_slab(R):
         one.close()
 
 
+@pytest.mark.parametrize("halo", ["fused", "nccl"])
 @pytest.mark.parametrize("name", ["fcc8_jit", "kg_lattice10"])
-def test_native_nccl_loop_in_process(name):
+def test_native_nccl_loop_in_process(name, halo):
     """The C++ step loop (tmd_slab_nccl.cuh) with a one-rank NCCL
     communicator: the slab exchanges its boundary layers with itself."""
     g = load(name)
@@ -214,7 +215,7 @@ def test_native_nccl_loop_in_process(name):
                                fene=E.FeneParams(*map(float, g["fene"])))
         flat = E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"], bonds=g["bonds"])
     eng = DecomposedEngine(flat, inter, float(g["r_skin"]), E.EngineConfig(dt=float(g["dt"])),
-                           comm=InProcessComm(1), native=True)
+                           comm=InProcessComm(1), native=True, halo=halo)
     try:
         np.testing.assert_array_equal(eng.local_pairs(), g["pairs"])
         assert_rel(eng.observe().potential, float(g["pe_fsum"]), E_RTOL, "PE")

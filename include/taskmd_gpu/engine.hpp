@@ -20,6 +20,7 @@
 #ifndef TASKMD_GPU_ENGINE_HPP_
 #define TASKMD_GPU_ENGINE_HPP_
 
+#include <array>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -99,20 +100,25 @@ struct GpuOptions {
   }
 }
 
-class Engine {
- public:
-  // build_domain(flat, inter, r_skin, n_sub) + Engine(domain, cfg)
-  // (domain.hpp:134-189, engine.hpp:68-77). n_sub / worker_threads have no
-  // GPU meaning and are ignored; angle terms are rejected with ConfigError.
-  // FENE bonds and a thermostat run on the device.
-  Engine(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
-         const taskmd::EngineConfig& cfg, const GpuOptions& opt = {})
-      : cfg_(cfg) {
+// The C-ABI view of a FlatConfig + Interactions + EngineConfig (arrays owned
+// here; tmd_gpu_create* copies them).
+struct CSystem {
+  std::vector<double> pos, vel;
+  std::vector<int64_t> bonds;  // Topology::bonds as (a, b) id pairs
+  tmd_system sys{};
+  tmd_lj_params lj{};
+  tmd_fene_params fene{};
+  bool has_fene = false;
+  tmd_engine_params p{};
+
+  CSystem(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
+          const taskmd::EngineConfig& cfg, const GpuOptions& opt) {
     if (inter.angle || !flat.topo.angles.empty()) {
       throw taskmd::ConfigError("angle terms are not on the GPU LJ path");
     }
     const std::size_t n = flat.size();
-    std::vector<double> pos(3 * n), vel(3 * n);
+    pos.resize(3 * n);
+    vel.resize(3 * n);
     for (std::size_t k = 0; k < n; ++k) {
       pos[3 * k] = flat.pos[k].x;
       pos[3 * k + 1] = flat.pos[k].y;
@@ -121,7 +127,6 @@ class Engine {
       vel[3 * k + 1] = flat.vel[k].y;
       vel[3 * k + 2] = flat.vel[k].z;
     }
-    tmd_system sys{};
     sys.box[0] = flat.box.length.x;
     sys.box[1] = flat.box.length.y;
     sys.box[2] = flat.box.length.z;
@@ -131,7 +136,6 @@ class Engine {
     sys.mass = flat.mass.empty() ? nullptr : flat.mass.data();
     sys.pos = pos.data();
     sys.vel = vel.data();
-    std::vector<int64_t> bonds;  // Topology::bonds as (a, b) id pairs
     bonds.reserve(2 * flat.topo.bonds.size());
     for (const auto& b : flat.topo.bonds) {
       bonds.push_back(b.a);
@@ -139,11 +143,12 @@ class Engine {
     }
     sys.n_bonds = static_cast<int64_t>(flat.topo.bonds.size());
     sys.bonds = bonds.empty() ? nullptr : bonds.data();
-    tmd_fene_params fene{};
-    if (inter.fene) fene = tmd_fene_params{inter.fene->k, inter.fene->r_max};
-    tmd_lj_params lj{inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
-                     inter.lj.energy_shifted ? 1 : 0};
-    tmd_engine_params p{};
+    if (inter.fene) {
+      fene = tmd_fene_params{inter.fene->k, inter.fene->r_max};
+      has_fene = true;
+    }
+    lj = tmd_lj_params{inter.lj.epsilon, inter.lj.sigma, inter.lj.r_cut,
+                       inter.lj.energy_shifted ? 1 : 0};
     p.dt = cfg.dt;
     p.r_skin = r_skin;
     p.device = opt.device;
@@ -156,7 +161,21 @@ class Engine {
       p.temperature = cfg.thermostat->temperature;
       p.seed = cfg.thermostat->seed;
     }
-    const int rc = tmd_gpu_create(&sys, &lj, inter.fene ? &fene : nullptr, &p, &ctx_);
+  }
+  const tmd_fene_params* fene_ptr() const { return has_fene ? &fene : nullptr; }
+};
+
+class Engine {
+ public:
+  // build_domain(flat, inter, r_skin, n_sub) + Engine(domain, cfg)
+  // (domain.hpp:134-189, engine.hpp:68-77). n_sub / worker_threads have no
+  // GPU meaning and are ignored; angle terms are rejected with ConfigError.
+  // FENE bonds and a thermostat run on the device.
+  Engine(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
+         const taskmd::EngineConfig& cfg, const GpuOptions& opt = {})
+      : cfg_(cfg) {
+    CSystem cs(flat, inter, r_skin, cfg, opt);
+    const int rc = tmd_gpu_create(&cs.sys, &cs.lj, cs.fene_ptr(), &cs.p, &ctx_);
     if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
     box_ = flat.box;
     topo_ = flat.topo;
@@ -257,6 +276,85 @@ class Engine {
   taskmd::EngineConfig cfg_;
   taskmd::BoxSpec box_;
   taskmd::Topology topo_;
+};
+
+using NcclId = std::array<unsigned char, 128>;
+
+// ncclGetUniqueId, on one rank; the caller broadcasts the bytes (MPI_Bcast,
+// torch.distributed, a file...).
+inline NcclId nccl_unique_id() {
+  NcclId id{};
+  const int rc = tmd_nccl_unique_id(id.data());
+  if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
+  return id;
+}
+
+// One GPU's slab of an N-GPU run, one process per GPU: the
+// native step loop with NCCL on the context stream and the fused halo
+// (tmd_slab_nccl.cuh). Every rank passes the whole system and the same
+// NcclId; run / observe are collective.
+class SlabEngine {
+ public:
+  SlabEngine(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
+             const taskmd::EngineConfig& cfg, int rank, int nranks, const NcclId& id,
+             const GpuOptions& opt = {}, bool load_balance = false)
+      : n_total_(static_cast<int64_t>(flat.size())), box_(flat.box) {
+    CSystem cs(flat, inter, r_skin, cfg, opt);
+    cs.p.section_timers = 0;
+    int rc = tmd_gpu_create_slab(&cs.sys, &cs.lj, cs.fene_ptr(), &cs.p, rank, nranks, &ctx_);
+    if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
+    check(tmd_gpu_slab_attach_nccl(ctx_, id.data(), (load_balance ? 1 : 0) | 2));
+    check(tmd_gpu_slab_setup(ctx_));
+  }
+  SlabEngine(const SlabEngine&) = delete;
+  SlabEngine& operator=(const SlabEngine&) = delete;
+  ~SlabEngine() { tmd_gpu_destroy(ctx_); }
+
+  void step() { run(1); }
+  void run(std::int64_t steps) { check(tmd_gpu_slab_run(ctx_, steps)); }
+
+  // Engine::observe over the whole system (an all-reduce: collective).
+  taskmd::StepObservables observe() const {
+    tmd_observables o{};
+    check(tmd_gpu_slab_observe(ctx_, n_total_, &o));
+    taskmd::StepObservables r;
+    r.step = o.step;
+    r.kinetic = o.kinetic;
+    r.potential = o.potential;
+    r.temperature = o.temperature;
+    return r;
+  }
+  std::int64_t step_count() const { return tmd_gpu_step_count(ctx_); }
+  std::uint64_t rebuild_count() const { return tmd_gpu_rebuild_count(ctx_); }
+
+  // The particles this slab owns, sorted by id, positions wrapped.
+  taskmd::FlatConfig local() const {
+    const std::size_t n = static_cast<std::size_t>(tmd_gpu_size(ctx_));
+    std::vector<std::int64_t> id(n);
+    std::vector<double> pos(3 * n), vel(3 * n);
+    check(tmd_gpu_download(ctx_, id.data(), pos.data(), vel.data(), nullptr));
+    taskmd::FlatConfig f;
+    f.box = box_;
+    f.id = id;
+    f.type.assign(n, 0);
+    f.mass.assign(n, 1.0);
+    f.pos.resize(n);
+    f.vel.resize(n);
+    for (std::size_t k = 0; k < n; ++k) {
+      f.pos[k] = {pos[3 * k], pos[3 * k + 1], pos[3 * k + 2]};
+      f.vel[k] = {vel[3 * k], vel[3 * k + 1], vel[3 * k + 2]};
+    }
+    return f;
+  }
+
+ private:
+  void check(int rc) const {
+    if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(ctx_));
+  }
+
+  tmd_gpu_ctx* ctx_ = nullptr;
+  std::int64_t n_total_ = 0;
+  taskmd::BoxSpec box_;
 };
 
 }  // namespace taskmd_gpu

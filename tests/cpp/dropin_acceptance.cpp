@@ -171,6 +171,32 @@ int main() {
             "max position spread " + std::to_string(worst) + ", PE " + std::to_string(pe_a) +
                 " / " + std::to_string(pe_b));
   }
+  // taskmd_gpu::SlabEngine (one process per GPU; here one slab exchanging
+  // its halo with itself through NCCL and the fused peer-store halo) against
+  // the reference engine, 40 steps
+  {
+    const FlatConfig flat = gen_lattice(8000, 0.8442, 0.9, 17);
+    EngineConfig cfg;
+    cfg.dt = 0.005;
+    cfg.n_sub = 8;
+    Engine ref(build_domain(flat, lj_only(), 0.3, 8), cfg);
+    ref.run(40);
+    const FlatConfig a = flatten_domain(ref.domain());
+    taskmd_gpu::SlabEngine g(flat, lj_only(), 0.3, cfg, 0, 1, taskmd_gpu::nccl_unique_id());
+    g.run(40);
+    const FlatConfig b = g.local();
+    double worst = 0.0;
+    bool ids = a.id == b.id;
+    for (std::size_t k = 0; ids && k < a.size(); ++k) {
+      worst = std::max({worst, std::abs(a.pos[k].x - b.pos[k].x),
+                        std::abs(a.pos[k].y - b.pos[k].y), std::abs(a.pos[k].z - b.pos[k].z)});
+    }
+    const double pe_a = ref.potential_energy(), pe_b = g.observe().potential;
+    verdict("SlabEngine (NCCL, fused halo), 40 steps", ids && worst <= 1e-9 &&
+                std::abs(pe_a - pe_b) <= 1e-10 * std::abs(pe_a),
+            "max position spread " + std::to_string(worst) + ", rebuilds " +
+                std::to_string(g.rebuild_count()) + " / " + std::to_string(ref.rebuild_count()));
+  }
   // criterion 3: NVE drift, N=4000 SC lattice, seed 3, T=0.6
   {
     const FlatConfig flat = gen_lattice(4000, 0.8442, 0.6, 3);

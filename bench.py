@@ -298,8 +298,15 @@ def run_ours(args) -> None:
         achieved = F / (t_force_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
                 "frac": achieved / fp64, "traffic": traffic}
+    # The bound the kernel actually sits on: every gathered neighbour of a
+    # warp's 32 lanes lies in its own 128-B line, one L1 wavefront each, and
+    # an SM's L1 processes one wavefront per clock.
+    sm_count, clk_ghz = 148, (clocks_mhz := (clocks.summary().get("sm_mhz") or 1965.0)) / 1e3
+    t_l1 = E_ent / (sm_count * clk_ghz * 1e9)
+    roof["l1"] = {"model": "one L1 wavefront per gathered list entry, 1 wavefront/clk/SM",
+                  "t_ms": 1e3 * t_l1, "frac": 1e3 * t_l1 / t_force_ms, "sm_mhz": clocks_mhz}
     roof.update({
-        "kernel": "k_lj_forces", "algorithmic_bytes": B, "algorithmic_flops": F,
+        "kernel": "k_forces_l1", "algorithmic_bytes": B, "algorithmic_flops": F,
         "entries": E_ent, "in_cut_entries": P_cut, "kernel_ms": t_force_ms,
         "t_roof_ms": 1e3 * max(t_hbm, t_flop), "fp64_peak_tflops_measured": fp64,
         "peak_source": peaks["source"], "share_of_step": t_force_ms / ms_per_step,

@@ -1034,17 +1034,17 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
     if (!(p->temperature >= 0.0) || !std::isfinite(p->temperature))
       cfg("langevin temperature must be finite and >= 0");
   }
-  if (s->n < 1) cfg("empty system: the GPU engine needs at least 1 particle");
+  if (s->n < 0) cfg("negative particle count");
   if (s->n > kMaxSlots) {
     cfg("system too large for one GPU context: " + std::to_string(s->n) +
         " particles > " + std::to_string(kMaxSlots));
   }
-  if (!s->id || !s->pos) cfg("id and pos arrays are required");
+  if (s->n > 0 && (!s->id || !s->pos)) cfg("id and pos arrays are required");
   // validate_flat (flat_config.hpp:42-61): unique ids, positive masses
   // unique ids: O(n) with a bitmap when they fill a dense range (the usual
   // 0..n-1), else by sorting
-  const int64_t id_lo = *std::min_element(s->id, s->id + s->n);
-  const int64_t id_hi = *std::max_element(s->id, s->id + s->n);
+  const int64_t id_lo = s->n > 0 ? *std::min_element(s->id, s->id + s->n) : 0;
+  const int64_t id_hi = s->n > 0 ? *std::max_element(s->id, s->id + s->n) : -1;
   const bool dense = static_cast<uint64_t>(id_hi - id_lo) < static_cast<uint64_t>(s->n);
   std::vector<int64_t> ids;
   if (dense) {
@@ -1526,7 +1526,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     }
     c->n = static_cast<int64_t>(sel.size());
     c->stride = static_cast<int>((c->n_cap + 31) / 32 * 32);
-    c->nblk = blocks_for(c->n, kBlock);
+    c->nblk = std::max(1, blocks_for(c->n, kBlock));  // (an empty system keeps a grid)
     c->dt = params->dt;
     c->half_dt = 0.5 * params->dt;
     c->r_skin = params->r_skin;
@@ -1873,7 +1873,7 @@ int tmd_gpu_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride, tmd_obs
       out[k].kinetic = rows[k][1];
       out[k].potential = rows[k][2];
       out[k].virial = rows[k][3];
-      out[k].temperature = 2.0 * rows[k][1] / (3.0 * static_cast<double>(c->n));
+      out[k].temperature = (c->n > 0 ? 2.0 * rows[k][1] / (3.0 * static_cast<double>(c->n)) : 0.0);
     }
   });
 }
@@ -1886,7 +1886,7 @@ int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
       out->potential = c->h_scalars[0];
       out->virial = c->h_scalars[1];
       out->kinetic = c->h_scalars[2];
-      out->temperature = 2.0 * out->kinetic / (3.0 * static_cast<double>(c->n));
+      out->temperature = (c->n > 0 ? 2.0 * out->kinetic / (3.0 * static_cast<double>(c->n)) : 0.0);
       return;
     }
     // after a run the closing half-kick already left the kinetic partials of
@@ -1907,7 +1907,7 @@ int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
     out->virial = c->h_scalars[1];
     out->kinetic = c->h_scalars[2];
     // KineticResult::temperature (soa_store.hpp:200-204)
-    out->temperature = 2.0 * out->kinetic / (3.0 * static_cast<double>(c->n));
+    out->temperature = (c->n > 0 ? 2.0 * out->kinetic / (3.0 * static_cast<double>(c->n)) : 0.0);
   });
 }
 

@@ -420,3 +420,16 @@ def test_run_observed_rows_equal_observe_after_each_run(timers):
         if row[0] > 60:
             k = int(row[0]) - 61
             assert_rel(rows1[k, 1] + rows1[k, 2], row[1] + row[2], 1e-10, "E")
+
+
+@pytest.mark.parametrize("timers", [True, False])
+def test_empty_system(timers):
+    """No particles: the engine builds, steps and observes zeros (the
+    reference's KineticResult reports T = 0 for no particles)."""
+    f = E.FlatConfig(np.full(3, 12.0), np.zeros(0, np.int64), np.zeros((0, 3)), None)
+    eng = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(section_timers=timers))
+    o = eng.observe()
+    assert (o.kinetic, o.potential, o.virial, o.temperature) == (0.0, 0.0, 0.0, 0.0)
+    eng.run(10)
+    assert eng.step_count() == 10 and eng.observe().temperature == 0.0
+    assert eng.flatten().size() == 0 and len(eng.pairs()) == 0

@@ -98,7 +98,10 @@ typedef struct tmd_engine_params {
                         particle ELL list, 2 = brick-staged shared memory,
                         3 = sector-chunked list + 256-bit gathers;
                         [1] variant-3 gathers in flight (1/2/4/8, 0 = 4);
-                        [2] 1 = no CUDA graphs */
+                        [2] 1 = no CUDA graphs;
+                        [3] variant-3 list build: 0 = by cell occupancy,
+                        3 = warp per cell, 5 = thread per particle,
+                        6 = warp per cell over a culled candidate stream */
   /* EngineConfig::thermostat (optional<LangevinParams>, potentials.hpp:174-178):
    * thermostat = 0 is NVE. The Langevin force of thermostat_and_half_kick
    * (engine.hpp:209-239) with counter_normal3(seed, kThermostat, step, id). */

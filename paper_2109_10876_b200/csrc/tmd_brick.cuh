@@ -770,6 +770,422 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
 }
 
 // ---------------------------------------------------------------------------
+// Full-list build over a culled candidate stream (k_build_cull, build kind 6,
+// the default for dense cells). Same warp/lane roles, staging, FP32 band and
+// entry order as k_build_brick3; what changes is how much work a candidate
+// costs (about half the warp instructions of k_build_brick3 per particle):
+//  1. Culling: the warp first drops, 32 candidates at a time, every candidate
+//     farther than r_v from the bounding box of its lanes' particles, and
+//     appends the survivors in stencil order to a per-warp stream of
+//     4-candidate chunks {x4, y4, z4, entry4}. Corner and edge cells of the
+//     27-cell stencil lose about half and a quarter of their particles and
+//     the per-cell padding disappears: ~40 % fewer candidate iterations at
+//     the BASELINE density. A culled candidate is a sure miss of the FP32 test
+//     for every lane (box distance <= each lane's distance; 1e-3 relative
+//     margin for FP32 rounding), so membership is unchanged.
+//  2. Entries and their tags are formed once per candidate at compaction.
+//  3. Appends advance a running shared-memory address (one predicated add per
+//     candidate). Flushes are warp-synchronous: when any lane has two whole
+//     chunks in its 20-slot ring, every lane writes its whole chunks (32-B
+//     sectors) and moves its partial chunk to the front, so the warp pays
+//     for a flush every ~15 iterations instead of whenever one lane fills a
+//     chunk.
+//  4. The band test is one packed subtract per candidate pair and a 4-way
+//     unsigned min.
+// The own cell (self exclusion) is a stream segment of its own.
+constexpr int kCullCap = 96;    // stream candidates per warp (multiple of 32)
+constexpr int kRingSlots = 20;  // flush trigger at 16 + up to 3 appends in flight
+
+struct CullLane {
+  float2 xi2, yi2, zi2;
+  float hi2;       // -1 for inactive lanes: never a hit
+  float2 nlo2;     // -lo2, or -inf for inactive lanes: never in the band
+  uint32_t wb;     // bit pattern of the band width bound (r2 - lo2 <= width)
+  uint32_t a;      // shared address of the next ring slot
+  uint32_t rbase;  // shared address of ring slot 0
+  int i;
+  int nflush;      // chunks flushed (or counted past the capacity)
+  uint32_t* dst;   // list address of chunk nflush
+};
+
+// Writes the lane's whole chunks, moves its partial chunk to ring slot 0.
+__device__ __forceinline__ void cull_flush(CullLane& L, int cap8, uint32_t* ring_lane) {
+  const int fill = static_cast<int>((L.a - L.rbase) >> 7);
+  const int whole = fill >> 3;
+  for (int c = 0; c < whole; ++c) {
+    if (L.nflush < cap8) flush_chunk(ring_lane + c * 8 * 32, L.dst);
+    ++L.nflush;
+    L.dst += 256;
+  }
+  if (whole > 0) {
+    const int part = fill & 7;
+    const uint32_t* src = ring_lane + whole * 8 * 32;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+      if (r < part) ring_lane[r * 32] = src[r * 32];
+    }
+    L.a = L.rbase + static_cast<uint32_t>(part) * 128u;
+  }
+}
+
+__device__ __forceinline__ bool cull_exact(const double4& pi, int i, uint32_t e,
+                                           const double4* __restrict__ pos, const Geom& g) {
+  const int j = static_cast<int>(e & kIdxMask);
+  double ex, ey, ez;
+  pair_delta(pi, pos[j], e, g, ex, ey, ez);
+  return j != i && exact_r2(ex, ey, ez) <= g.rv2;
+}
+
+// Four ring appends: unconditional stores, advances predicated on the FP32
+// hit test (r2 <= hi2, and entry != self for the own cell). A miss leaves
+// junk in the next free slot, which the next store or the sentinel padding
+// replaces.
+template <bool kSelf>
+__device__ __forceinline__ void cull_append4_fp32(uint32_t& a, const uint4& E, const float2& r0,
+                                                  const float2& r1, float hi2, uint32_t me) {
+#define TMD_APPEND(R, E)                                                     \
+  if (kSelf) {                                                               \
+    asm volatile(                                                            \
+        "{\n\t.reg .pred p, q;\n\t"                                          \
+        "setp.ne.u32 q, %2, %3;\n\t"                                         \
+        "setp.le.and.f32 p, %1, %4, q;\n\t"                                  \
+        "st.shared.u32 [%0], %2;\n\t"                                        \
+        "@p add.u32 %0, %0, 128;\n\t}"                                       \
+        : "+r"(a)                                                            \
+        : "f"(R), "r"(E), "r"(me), "f"(hi2)                                  \
+        : "memory");                                                         \
+  } else {                                                                   \
+    asm volatile(                                                            \
+        "{\n\t.reg .pred p;\n\t"                                             \
+        "setp.le.f32 p, %1, %3;\n\t"                                         \
+        "st.shared.u32 [%0], %2;\n\t"                                        \
+        "@p add.u32 %0, %0, 128;\n\t}"                                       \
+        : "+r"(a)                                                            \
+        : "f"(R), "r"(E), "f"(hi2)                                           \
+        : "memory");                                                         \
+  }
+  TMD_APPEND(r0.x, E.x);
+  TMD_APPEND(r0.y, E.y);
+  TMD_APPEND(r1.x, E.z);
+  TMD_APPEND(r1.y, E.w);
+#undef TMD_APPEND
+}
+
+__device__ __forceinline__ void cull_append1(uint32_t& a, uint32_t e, bool hit) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\t"
+      "st.shared.u32 [%0], %1;\n\t"
+      "@p add.u32 %0, %0, 128;\n\t}"
+      : "+r"(a)
+      : "r"(e), "r"(static_cast<uint32_t>(hit))
+      : "memory");
+}
+
+// One candidate of a chunk that holds a rounding-band candidate.
+__device__ __forceinline__ void cull_band1(uint32_t& a, uint32_t e, float r2, float d,
+                                           const CullLane& L, const double4& pi,
+                                           const double4* __restrict__ pos, const Geom& g) {
+  const uint32_t me = static_cast<uint32_t>(L.i);
+  const bool hit = __float_as_uint(d) <= L.wb ? cull_exact(pi, L.i, e, pos, g)
+                                              : (r2 <= L.hi2 && e != me);
+  cull_append1(a, e, hit);
+}
+
+// Tests a stream segment (a multiple of 4 candidates), 4 per iteration.
+template <bool kSelf>
+__device__ __forceinline__ void cull_segment(const float* __restrict__ strm, int fill,
+                                             CullLane& L, const double4* __restrict__ pos,
+                                             const Geom& g, int cap8, uint32_t* ring_lane) {
+  const uint32_t me = static_cast<uint32_t>(L.i);
+  const uint32_t trig = L.rbase + 16u * 128u;
+#pragma unroll 1
+  for (int c = 0; c < fill; c += 4) {
+    const float* ch = strm + c * 4;  // chunk of 4: x4 | y4 | z4 | entry4
+    const float4 X = *reinterpret_cast<const float4*>(ch);
+    const float4 Y = *reinterpret_cast<const float4*>(ch + 4);
+    const float4 Z = *reinterpret_cast<const float4*>(ch + 8);
+    const uint4 E = *reinterpret_cast<const uint4*>(ch + 12);
+    const float2 dxa = __fadd2_rn(L.xi2, f2(X.x, X.y)), dxb = __fadd2_rn(L.xi2, f2(X.z, X.w));
+    const float2 dya = __fadd2_rn(L.yi2, f2(Y.x, Y.y)), dyb = __fadd2_rn(L.yi2, f2(Y.z, Y.w));
+    const float2 dza = __fadd2_rn(L.zi2, f2(Z.x, Z.y)), dzb = __fadd2_rn(L.zi2, f2(Z.z, Z.w));
+    const float2 ra = __ffma2_rn(dza, dza, __ffma2_rn(dya, dya, __fmul2_rn(dxa, dxa)));
+    const float2 rb = __ffma2_rn(dzb, dzb, __ffma2_rn(dyb, dyb, __fmul2_rn(dxb, dxb)));
+    const float2 da = __fadd2_rn(ra, L.nlo2), db = __fadd2_rn(rb, L.nlo2);
+    const uint32_t bmin = min(min(__float_as_uint(da.x), __float_as_uint(da.y)),
+                              min(__float_as_uint(db.x), __float_as_uint(db.y)));
+    uint32_t a = L.a;
+    if (bmin > L.wb) {  // no candidate in the rounding band: FP32 decides
+      cull_append4_fp32<kSelf>(a, E, ra, rb, L.hi2, me);
+    } else {  // rounding band: the exact FP64 decision there
+      const double4 pi = pos[L.i];
+      cull_band1(a, E.x, ra.x, da.x, L, pi, pos, g);
+      cull_band1(a, E.y, ra.y, da.y, L, pi, pos, g);
+      cull_band1(a, E.z, rb.x, db.x, L, pi, pos, g);
+      cull_band1(a, E.w, rb.y, db.y, L, pi, pos, g);
+    }
+    L.a = a;
+    if (__any_sync(0xffffffffu, a >= trig)) cull_flush(L, cap8, ring_lane);
+  }
+}
+
+// 3 CTAs per SM (76 registers): at 4 the register cap forces spills and
+// rematerialisation into the candidate loop (measured 5 % slower).
+__global__ void __launch_bounds__(kBuildThreads, 3)
+    k_build_cull(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
+                 const int* __restrict__ brick_rank_off, const int* __restrict__ start, Geom g,
+                 BrickGeom bg, uint32_t* __restrict__ list, int* __restrict__ nnbr,
+                 double4* __restrict__ snap, uint32_t sentinel, Ctrl* ctrl) {
+  if (!ctrl->rebuild) return;
+  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z, each stage_cap + 32
+  __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
+  __shared__ uint32_t s_code[kMaxHalo];
+  __shared__ __align__(16) uint32_t s_ring[kBuildThreads / 32][kRingSlots][32];
+  __shared__ __align__(16) float s_strm[kBuildThreads / 32][kCullCap * 4];
+  __shared__ __align__(16) int4 s_rng[kBuildThreads / 32][11][3];  // per-warp range table
+  __shared__ int s_maxc;
+  __shared__ unsigned long long s_ent;
+  const int b = blockIdx.x;
+  HaloTable ht;
+  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
+  load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
+            s_gcell);
+  if (ht.total > bg.stage_cap) {
+    if (threadIdx.x == 0) {
+      atomicOr(&ctrl->status, kStatStageOverflow);
+      atomicMax(&ctrl->max_halo, ht.total);
+    }
+    return;
+  }
+  const int sc = bg.stage_cap + 32;
+  float* nx = s_f;
+  float* ny = s_f + sc;
+  float* nz = s_f + 2 * sc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {  // staging: a warp per halo cell, lanes over its (padded) slots
+    const double ox = ht.lo[0] * bg.origin_scale[0];
+    const double oy = ht.lo[1] * bg.origin_scale[1];
+    const double oz = ht.lo[2] * bg.origin_scale[2];
+    for (int h = warp; h < ht.n; h += kBuildThreads / 32) {
+      const int kb = s_off[h], cnt = s_cnt[h], gs = s_gstart[h];
+      const uint32_t c = s_code[h];
+      for (int q = lane; q < pad4(cnt); q += 32) {
+        float x = kFarF, y = kFarF, z = kFarF;
+        if (q < cnt) {
+          const double4 p = pos[gs + q];
+          // same rounding as k_build_brick3: (p + shift) - origin
+          x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
+          y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
+          z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
+        }
+        nx[kb + q] = -x;
+        ny[kb + q] = -y;
+        nz[kb + q] = -z;
+      }
+    }
+    if (threadIdx.x < 32) {
+      nx[ht.total + threadIdx.x] = -kFarF;
+      ny[ht.total + threadIdx.x] = -kFarF;
+      nz[ht.total + threadIdx.x] = -kFarF;
+    }
+  }
+  __syncthreads();
+
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
+  const int cap8 = bg.cap >> 3;
+  float* strm = s_strm[warp];
+  uint32_t* ring_lane = &s_ring[warp][0][lane];
+  const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(ring_lane));
+  const float cull2 = bg.hi2 * 1.001f;
+  int my_max = 0;
+  unsigned long long my_ent = 0;
+  for (int oc = warp; oc < ncell_own; oc += kBuildThreads / 32) {
+    const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
+    const int hc = (ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1));
+    const int ncl = s_cnt[hc];
+    if (lane < 11) {  // range table: lane r describes range r
+      const int rr = lane;
+      const int ri = rr <= 3 ? rr : (rr <= 6 ? 4 : rr - 2);
+      const int ca = (rr >= 4 && rr <= 6) ? rr - 4 : 0;
+      const int cb = (rr >= 4 && rr <= 6) ? rr - 3 : 3;
+      const int oz2 = ri / 3 - 1, oy2 = ri % 3 - 1;
+      const int first_yz = oy2 != 0 ? oy2 : oz2;
+      const int h0 = hc - 1 + ht.H[0] * (oy2 + ht.H[1] * oz2);
+      auto tag_of = [&](int t) {
+        const uint32_t code = s_code[h0 + t];
+        const int first = (t - 1) != 0 ? (t - 1) : first_yz;
+        return code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
+      };
+      const int e3 = s_off[h0 + cb];
+      const int e1 = ca + 1 < cb ? s_off[h0 + ca + 1] : e3;
+      const int e2 = ca + 2 < cb ? s_off[h0 + ca + 2] : e3;
+      const uint32_t u0 = tag_of(ca);
+      const uint32_t u1 = ca + 1 < cb ? tag_of(ca + 1) : u0;
+      const uint32_t u2 = ca + 2 < cb ? tag_of(ca + 2) : u1;
+      const int b0 = s_gstart[h0 + ca] - s_off[h0 + ca];
+      const int b1 = ca + 1 < cb ? s_gstart[h0 + ca + 1] - s_off[h0 + ca + 1] : b0;
+      const int b2 = ca + 2 < cb ? s_gstart[h0 + ca + 2] - s_off[h0 + ca + 2] : b1;
+      s_rng[warp][rr][0] = make_int4(s_off[h0 + ca], e1, e2, e3);
+      s_rng[warp][rr][1] = make_int4(static_cast<int>(u0), static_cast<int>(u1),
+                                     static_cast<int>(u2), 0);
+      s_rng[warp][rr][2] = make_int4(b0, b1, b2, 0);
+    }
+    __syncwarp();
+    for (int p0 = 0; p0 < ncl; p0 += 32) {
+      const int q = p0 + lane;
+      const bool active = q < ncl;
+      const int qi = active ? q : 0;
+      CullLane L;
+      L.i = s_gstart[hc] + qi;
+      const int ki = s_off[hc] + qi;
+      const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
+      L.xi2 = f2(xf, xf);
+      L.yi2 = f2(yf, yf);
+      L.zi2 = f2(zf, zf);
+      L.hi2 = active ? bg.hi2 : -1.0f;
+      const float nlo = active ? -bg.lo2 : -INFINITY;
+      L.nlo2 = f2(nlo, nlo);
+      L.wb = __float_as_uint(2.0f * (bg.hi2 - bg.lo2));
+      L.rbase = rbase;
+      L.a = rbase;
+      L.nflush = 0;
+      L.dst = list + list_slot(L.i >> 5, bg.cap, L.i & 31, 0);
+      // bounding box of the lanes' particles (inactive lanes repeat lane 0's)
+      float lox = xf, hix = xf, loy = yf, hiy = yf, loz = zf, hiz = zf;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lox = fminf(lox, __shfl_xor_sync(0xffffffffu, lox, o));
+        hix = fmaxf(hix, __shfl_xor_sync(0xffffffffu, hix, o));
+        loy = fminf(loy, __shfl_xor_sync(0xffffffffu, loy, o));
+        hiy = fmaxf(hiy, __shfl_xor_sync(0xffffffffu, hiy, o));
+        loz = fminf(loz, __shfl_xor_sync(0xffffffffu, loz, o));
+        hiz = fmaxf(hiz, __shfl_xor_sync(0xffffffffu, hiz, o));
+      }
+      // The stencil as 11 ranges of x-adjacent halo cells, contiguous in the
+      // staging: rows (oz, oy) in the reference order, the middle row split
+      // into -x | own | +x so that the own cell is a stream segment of its
+      // own (segments: 0 = before the own cell, 1 = own cell, 2 = after).
+      // One compaction site and one test site per segment kind keep the
+      // kernel small enough for the instruction cache; the ranges of the
+      // owned cell are tabulated once per warp (s_rng).
+      int r = 0, kq = 0, k1 = 0, k2 = 0, k3 = 0, a0 = 0, a1 = 0, a2 = 0;
+      uint32_t t0 = 0, t1 = 0, t2 = 0;
+      auto load_range = [&](bool reset) {  // from the warp's range table
+        const int4 kk = s_rng[warp][r][0];
+        const int4 tt = s_rng[warp][r][1];
+        const int4 aa = s_rng[warp][r][2];
+        if (reset) kq = kk.x;
+        k1 = kk.y;
+        k2 = kk.z;
+        k3 = kk.w;
+        t0 = static_cast<uint32_t>(tt.x);
+        t1 = static_cast<uint32_t>(tt.y);
+        t2 = static_cast<uint32_t>(tt.z);
+        a0 = aa.x;
+        a1 = aa.y;
+        a2 = aa.z;
+      };
+      auto seg_of = [](int rr) { return rr < 5 ? 0 : (rr == 5 ? 1 : 2); };
+      load_range(true);
+      int fill = 0, cur_seg = 0;
+      for (;;) {
+        bool process = r >= 11;
+        if (!process) {
+          if (kq >= k3) {  // range exhausted: next range, maybe a new segment
+            ++r;
+            if (r < 11) load_range(true);
+            if (r < 11 && seg_of(r) == cur_seg) continue;
+            process = true;
+          } else if (fill > kCullCap - 32) {
+            process = true;
+          } else {  // compact 32 staged slots (padding slots are far: dropped)
+            const int k = kq + lane;
+            const bool valid = k < k3;
+            const int kk = valid ? k : kq;
+            const float x = nx[kk], y = ny[kk], z = nz[kk];  // negated coordinates
+            const float dx = fmaxf(fmaxf(lox + x, -x - hix), 0.0f);
+            const float dy = fmaxf(fmaxf(loy + y, -y - hiy), 0.0f);
+            const float dz = fmaxf(fmaxf(loz + z, -z - hiz), 0.0f);
+            const bool keep = valid && dx * dx + dy * dy + dz * dz <= cull2;
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+              const uint32_t tag = k >= k2 ? t2 : (k >= k1 ? t1 : t0);
+              const int add = k >= k2 ? a2 : (k >= k1 ? a1 : a0);
+              const int p = fill + __popc(bal & lt_mask);
+              float* ch = strm + (p >> 2) * 16 + (p & 3);
+              ch[0] = x;
+              ch[4] = y;
+              ch[8] = z;
+              ch[12] = __uint_as_float(static_cast<uint32_t>(k + add) | tag);
+            }
+            fill += __popc(bal);
+            kq += 32;
+            continue;
+          }
+        }
+        if (fill > 0) {  // pad the stream to whole chunks and test it
+          const int pad = (4 - (fill & 3)) & 3;
+          if (lane < pad) {
+            const int p = fill + lane;
+            float* ch = strm + (p >> 2) * 16 + (p & 3);
+            ch[0] = -kFarF;
+            ch[4] = -kFarF;
+            ch[8] = -kFarF;
+          }
+          __syncwarp();
+          if (cur_seg == 1) {
+            cull_segment<true>(strm, fill, L, pos, g, cap8, ring_lane);
+          } else {
+            cull_segment<false>(strm, fill, L, pos, g, cap8, ring_lane);
+          }
+          __syncwarp();
+          fill = 0;
+        }
+        if (r >= 11) break;
+        load_range(false);  // (recomputed rather than kept live across the test)
+        cur_seg = seg_of(r);
+      }
+      if (active) {
+        // remaining whole chunks, then the sentinel-padded partial one
+        const int fl = static_cast<int>((L.a - L.rbase) >> 7);
+        const int whole = fl >> 3, part = fl & 7;
+        for (int c = 0; c < whole; ++c) {
+          if (L.nflush < cap8) flush_chunk(ring_lane + c * 8 * 32, L.dst);
+          ++L.nflush;
+          L.dst += 256;
+        }
+        const int n = L.nflush * 8 + part;
+        if (part != 0 && n < bg.cap) {
+          uint32_t* pc = ring_lane + whole * 8 * 32;
+          for (int r = part; r < 8; ++r) pc[r * 32] = sentinel;
+          flush_chunk(pc, L.dst);
+        }
+        nnbr[L.i] = n < bg.cap ? n : bg.cap;
+        snap[L.i] = pos[L.i];
+        if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
+        my_max = max(my_max, n);
+        my_ent += static_cast<unsigned long long>(n);
+      }
+      __syncwarp();
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
+    my_ent += __shfl_xor_sync(0xffffffffu, my_ent, o);
+  }
+  if (lane == 0) {
+    atomicMax(&s_maxc, my_max);
+    atomicAdd(&s_ent, my_ent);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&ctrl->max_count, s_maxc);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries), s_ent);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Full-list build, one thread per particle (k_build_thread): each thread walks
 // its 27 neighbour cells in the reference stencil order with the exact FP64
 // test, so membership and entry order equal k_build_brick3's. Entries collect

@@ -7,7 +7,7 @@
 //   Neigh      k_decide             global max-displacement test, on device
 //   Resort     k_wrap_bin, scan, k_scatter, k_sort_cells, k_permute, k_copy_back,
 //              k_brick_groups + scan          (no-ops unless the device decided rebuild)
-//   Neigh      k_build_prologue, k_build_brick3 (no-op unless rebuild)
+//   Neigh      k_build_prologue, k_build_cull / k_build_thread (no-op unless rebuild)
 //   Forces     k_forces_l1<kFused>  forces + closing half-kick (+ Langevin) of this
 //              step + opening half-kick + drift of the next (kKick2 on the last)
 // Nothing in a chunk waits for the host. The host synchronises once per
@@ -130,7 +130,8 @@ struct tmd_gpu_ctx {
   int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
   double occupancy = 0.0;     // particle-weighted mean cell occupancy at creation
   int build_kind = 3;         // variant 3 list build: 3 = warp per cell (brick-staged),
-                              // 5 = thread per particle (sparse cells)
+                              // 5 = thread per particle (sparse cells),
+                              // 6 = warp per cell over a culled candidate stream
   BrickGeom bg{};
   int* cell_rank = nullptr;       // global cell -> brick-major rank
   int* brick_rank_off = nullptr;  // brick -> first rank (nbricks + 1)
@@ -399,6 +400,8 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
                             static_cast<int>(b)), "smem attr build");
     ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(b)), "smem attr build");
+    ck(cudaFuncSetAttribute(k_build_cull, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(b)), "smem attr build");
     g_build = b;
   }
   if (f > g_force) {
@@ -441,6 +444,10 @@ void launch_build(tmd_gpu_ctx* c) {
     k_build_thread<<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->cap, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
+  } else if (c->variant == 3 && c->build_kind == 6) {
+    k_build_cull<<<c->bg.nbricks, kBuildThreads, build_smem(c) / 4 * 3, c->ls>>>(
+        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->g, c->bg, c->nbr, c->nnbr,
+        c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
   } else if (c->variant == 3) {
     k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
@@ -1149,11 +1156,11 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   bg.stage_cap = std::max(256, (static_cast<int>(want) + 31) / 32 * 32);
   // list build: a warp per cell while cells hold most of a warp, else a warp
   // per 32 consecutive brick particles (sparse cells, e.g. the KG melt)
-  if (c->build_kind != 3 && c->build_kind != 5) {
+  if (c->build_kind != 3 && c->build_kind != 5 && c->build_kind != 6) {
     // occupancy seen by a particle (sum n_c^2 / sum n_c over the initial
     // cells), so a dense slab in a mostly empty box counts as dense
     const double occ = c->occupancy > 0.0 ? c->occupancy : per_cell;
-    c->build_kind = occ >= kBuildCellWarpMin ? 3 : 5;
+    c->build_kind = occ >= kBuildCellWarpMin ? 6 : 5;
   }
   // FP32 prefilter band (see DESIGN.md §List build): bound on |r2_f32 - r2_ref|
   // for brick-relative single-precision coordinates, times 4.

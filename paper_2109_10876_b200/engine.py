@@ -137,7 +137,8 @@ class EngineConfig:
     # list + 256-bit LDG gathers
     variant: int = 0
     # list build of variant 3: 0 = by cell occupancy, 3 = warp per cell
-    # (brick-staged), 5 = thread per particle (sparse cells)
+    # (brick-staged), 5 = thread per particle (sparse cells), 6 = warp per
+    # cell over a culled candidate stream
     build: int = 0
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off

@@ -103,6 +103,13 @@ struct tmd_gpu_ctx {
   BondTab bt{};
   long long id_min = 0;
   int64_t id_span = 0;
+  // download in id order on the device (ids forming a dense range, fixed
+  // particle set): dl_lo = smallest id, dl = n * 10 doubles of scratch
+  bool ids_dense = false;
+  long long dl_lo = 0;
+  double* dl = nullptr;
+  char* arena = nullptr;  // the per-slot arrays of a non-slab context, one allocation
+  size_t arena_bytes = 0;
   int* slot_of_id = nullptr;       // [id_span] (owned + ghost slots), -1 = absent
   int* bond_off = nullptr;         // [id_span + 1] CSR over id - id_min
   int* bond_nbr = nullptr;         // partner id - id_min
@@ -128,7 +135,8 @@ struct tmd_gpu_ctx {
   // brick-major ordering + variant selection
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
   int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
-  double occupancy = 0.0;     // particle-weighted mean cell occupancy at creation
+  double occupancy = 0.0;     // particle-weighted mean cell occupancy at the first binning
+  bool build_auto = false;    // build kind chosen from `occupancy` at the first binning
   int build_kind = 3;         // variant 3 list build: 3 = warp per cell (brick-staged),
                               // 5 = thread per particle (sparse cells),
                               // 6 = warp per cell over a culled candidate stream
@@ -270,10 +278,14 @@ void free_all(tmd_gpu_ctx* c) {
                   c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
                   c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1],
                   c->slot_of_id, c->bond_off, c->bond_nbr, c->bond_anchor, c->bnd_cnt,
-                  c->bnd_ent, c->nccl_i64, c->exp};
+                  c->bnd_ent, c->nccl_i64, c->exp, c->dl};
+  const char* a0 = c->arena;
+  const char* a1 = c->arena + c->arena_bytes;
   for (void* p : ptrs) {
-    if (p) cudaFree(p);
+    const char* q = static_cast<const char*>(p);
+    if (p && !(a0 && q >= a0 && q < a1)) cudaFree(p);
   }
+  if (c->arena) cudaFree(c->arena);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->obs_host) cudaFreeHost(c->obs_host);
   if (c->h_scalars) cudaFreeHost(c->h_scalars);
@@ -651,11 +663,36 @@ void grow_after_overflow(tmd_gpu_ctx* c, const Ctrl& h) {
 
 constexpr int kOverflowBits = kStatOverflow | kStatStageOverflow;
 
+constexpr double kBuildCellWarpMin = 12.0;  // mean particles per cell (measured crossover)
+
+// List build kind by the occupancy a particle sees (sum n_c^2 / sum n_c over
+// the owned cells of the first binning, so a dense slab in a mostly empty box
+// counts as dense): a warp per cell while cells hold most of a warp, else a
+// thread per particle (sparse cells, e.g. the KG melt).
+void choose_build_kind(tmd_gpu_ctx* c) {
+  const int nc = c->g.owned_cells;
+  std::vector<int> st(static_cast<size_t>(nc) + 1);
+  ck(cudaMemcpyAsync(st.data(), c->start, st.size() * sizeof(int), cudaMemcpyDeviceToHost,
+                     c->stream), "D2H start");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  double s1 = 0.0, s2 = 0.0;
+  for (int k = 0; k < nc; ++k) {
+    const double m = static_cast<double>(st[k + 1] - st[k]);
+    s1 += m;
+    s2 += m * m;
+  }
+  c->occupancy = s1 > 0.0 ? s2 / s1 : 0.0;
+  c->build_kind = c->occupancy >= kBuildCellWarpMin ? 6 : 5;
+  c->build_auto = false;
+  c->graph_dirty = true;
+}
+
 void setup_pass(tmd_gpu_ctx* c) {
   for (;;) {
     set_force_rebuild(c);
     launch_decide(c, false);
     launch_resort(c);
+    if (c->build_auto) choose_build_kind(c);
     launch_build(c);
     sync_ctrl(c);
     raise_physics(c, false);
@@ -1110,7 +1147,6 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
 // Brick decomposition of the cell grid (bricks of up to 2x2x2 cells), the
 // brick-major cell ranks, staging capacities and the FP32 prefilter band.
 
-constexpr double kBuildCellWarpMin = 12.0;  // mean particles per cell (measured crossover)
 
 void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   BrickGeom& bg = c->bg;
@@ -1154,14 +1190,6 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   const int ncell_halo = (bg.B[0] + 2) * (bg.B[1] + 2) * (bg.B[2] + 2);
   const double want = halo + 1.5 * ncell_halo + 6.0 * std::sqrt(halo) + 64.0;
   bg.stage_cap = std::max(256, (static_cast<int>(want) + 31) / 32 * 32);
-  // list build: a warp per cell while cells hold most of a warp, else a warp
-  // per 32 consecutive brick particles (sparse cells, e.g. the KG melt)
-  if (c->build_kind != 3 && c->build_kind != 5 && c->build_kind != 6) {
-    // occupancy seen by a particle (sum n_c^2 / sum n_c over the initial
-    // cells), so a dense slab in a mostly empty box counts as dense
-    const double occ = c->occupancy > 0.0 ? c->occupancy : per_cell;
-    c->build_kind = occ >= kBuildCellWarpMin ? 6 : 5;
-  }
   // FP32 prefilter band (see DESIGN.md §List build): bound on |r2_f32 - r2_ref|
   // for brick-relative single-precision coordinates, times 4.
   const double cl = std::max({c->g.cell_len[0], c->g.cell_len[1], c->g.cell_len[2]});
@@ -1554,27 +1582,11 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
     }
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
-    c->build_kind = params->reserved[3];  // 0 = by density (setup_bricks)
-    {
-      std::vector<int> occ(static_cast<size_t>(c->g.dims[0]) * c->g.dims[1] * c->g.dims[2], 0);
-      auto coord = [&](double p, int k) {
-        const double w = host_wrap1(p, c->g.L[k]);
-        return std::min(std::max(static_cast<int>(std::floor(w / c->g.cell_len[k])), 0),
-                        c->g.dims[k] - 1);
-      };
-      double s1 = 0.0, s2 = 0.0;
-      for (const int64_t k : sel) {
-        const size_t cl = static_cast<size_t>(coord(sys->pos[3 * k], 0)) +
-                          static_cast<size_t>(c->g.dims[0]) *
-                              (coord(sys->pos[3 * k + 1], 1) +
-                               static_cast<size_t>(c->g.dims[1]) * coord(sys->pos[3 * k + 2], 2));
-        s2 += 2.0 * occ[cl] + 1.0;  // (m+1)^2 - m^2
-        ++occ[cl];
-        s1 += 1.0;
-      }
-      c->occupancy = s1 > 0.0 ? s2 / s1 : 0.0;
-    }
+    c->build_kind = params->reserved[3];
+    c->build_auto = c->build_kind != 3 && c->build_kind != 5 && c->build_kind != 6;
+    if (c->build_auto) c->build_kind = 6;  // decided at the first binning (setup_pass)
     setup_bricks(c, static_cast<double>(sys->n), lj->r_cut + params->r_skin);
+    mark("bricks");
     if (slab) {  // groups of the owned particles only (+ migration headroom)
       const int64_t want = c->n + c->n / 4 + 1024;
       c->ngroups_max = static_cast<int>(want / 32) + c->bg.nbricks + 1;
@@ -1592,42 +1604,67 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     }
 
     const size_t n = static_cast<size_t>(c->n_cap);  // capacity
+    // Per-slot arrays: one allocation carved into 256-B aligned arrays
+    // (cudaMalloc costs ~0.25 ms a call whatever the size); slab contexts
+    // allocate them one by one, since they regrow them (grow_capacity).
+    std::vector<std::pair<void**, size_t>> plan;
+    auto want = [&](auto*& p, size_t count) {
+      plan.emplace_back(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(*p));
+    };
     // slot n_cap of both buffers: far-away sentinel (variant 3 list padding)
-    c->posb[0] = dalloc<double4>(n + 1);
-    c->posb[1] = dalloc<double4>(n + 1);
+    want(c->posb[0], n + 1);
+    want(c->posb[1], n + 1);
+    want(c->pos2, n);
+    want(c->snap, n);
+    want(c->vx, n); want(c->vy, n); want(c->vz, n);
+    want(c->vx2, n); want(c->vy2, n); want(c->vz2, n);
+    want(c->fx, n); want(c->fy, n); want(c->fz, n);
+    want(c->mass, n); want(c->mass2, n);
+    want(c->id, n); want(c->id2, n);
+    want(c->cell, n); want(c->cell2, n);
+    want(c->rank, n); want(c->perm, n);
+    want(c->nnbr, n);
+    want(c->ck_pos, n);
+    want(c->ck_vx, n); want(c->ck_vy, n); want(c->ck_vz, n);
+    want(c->ck_mass, n);
+    want(c->ck_id, n);
+    if (params->thermostat) {
+      want(c->ck_fx, n);
+      want(c->ck_fy, n);
+      want(c->ck_fz, n);
+    }
+    if (!slab) want(c->dl, 10 * n);  // download / upload scratch
+    if (!slab) {
+      size_t tot = 0;
+      for (const auto& e : plan) tot += (e.second + 255) / 256 * 256;
+      c->arena = dalloc<char>(tot);
+      c->arena_bytes = tot;
+      size_t off = 0;
+      for (const auto& e : plan) {
+        *e.first = c->arena + off;
+        off += (e.second + 255) / 256 * 256;
+      }
+    } else {
+      for (const auto& e : plan) *e.first = dalloc<char>(e.second);
+    }
     c->cur = 0;
     c->pos = c->posb[0];
-    c->pos2 = dalloc<double4>(n);
-    c->snap = dalloc<double4>(n);
-    c->vx = dalloc<double>(n); c->vy = dalloc<double>(n); c->vz = dalloc<double>(n);
-    c->vx2 = dalloc<double>(n); c->vy2 = dalloc<double>(n); c->vz2 = dalloc<double>(n);
-    c->fx = dalloc<double>(n); c->fy = dalloc<double>(n); c->fz = dalloc<double>(n);
-    c->mass = dalloc<double>(n); c->mass2 = dalloc<double>(n);
-    c->id = dalloc<long long>(n); c->id2 = dalloc<long long>(n);
-    c->cell = dalloc<int>(n); c->cell2 = dalloc<int>(n);
-    c->rank = dalloc<int>(n); c->perm = dalloc<int>(n);
     c->count = dalloc<int>(c->g.ncells);
     c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
-    c->nnbr = dalloc<int>(n);
     c->nparts = std::max(blocks_for(c->n_cap, kBlock), c->bg.nbricks);
     c->part_e = dalloc<double>(c->nparts);
     c->part_w = dalloc<double>(c->nparts);
     c->part_ke = dalloc<double>(c->nparts);
+    mark("device arrays");
     upload_bricks(c);
+    mark("upload bricks");
     c->scalars = dalloc<double>(4);
     c->ctrl = dalloc<Ctrl>(1);
     c->rebuild_log = dalloc<int>(static_cast<size_t>(kChunk));
-    c->ck_pos = dalloc<double4>(n);
-    c->ck_vx = dalloc<double>(n); c->ck_vy = dalloc<double>(n); c->ck_vz = dalloc<double>(n);
-    c->ck_mass = dalloc<double>(n);
-    c->ck_id = dalloc<long long>(n);
-    if (params->thermostat) {
-      c->ck_fx = dalloc<double>(n);
-      c->ck_fy = dalloc<double>(n);
-      c->ck_fz = dalloc<double>(n);
-    }
+    mark("checkpoint arrays");
     ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost");
     ck(cudaMallocHost(&c->h_scalars, 4 * sizeof(double)), "cudaMallocHost");
+    mark("pinned");
     std::memset(c->h_ctrl, 0, sizeof(Ctrl));
     ck(cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream), "memset ctrl");
     ck(cudaMemsetAsync(c->count, 0, sizeof(int) * c->g.ncells, c->stream),
@@ -1636,37 +1673,69 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     ck(cudaMemsetAsync(c->fy, 0, n * sizeof(double), c->stream), "memset");
     ck(cudaMemsetAsync(c->fz, 0, n * sizeof(double), c->stream), "memset");
 
+    mark("allocate");
     // upload the kept particles (input order; the first resort sorts by cell)
     const size_t m = sel.size();
-    std::vector<double4> hp(m);
-    std::vector<double> hv(3 * m, 0.0), hm(m, 1.0);
-    std::vector<long long> hid(m);
-    for (size_t r = 0; r < m; ++r) {
-      const size_t k = static_cast<size_t>(sel[r]);
-      hp[r] = make_double4(sys->pos[3 * k], sys->pos[3 * k + 1], sys->pos[3 * k + 2], 0.0);
-      if (sys->vel) {
-        hv[r] = sys->vel[3 * k];
-        hv[m + r] = sys->vel[3 * k + 1];
-        hv[2 * m + r] = sys->vel[3 * k + 2];
-      }
-      if (sys->mass) hm[r] = sys->mass[k];
-      hid[r] = sys->id[k];
-    }
     const double4 far = make_double4(kFarD, kFarD, kFarD, 0.0);
-    if (m > 0) {
-      ck(cudaMemcpy(c->posb[0], hp.data(), m * sizeof(double4), cudaMemcpyHostToDevice),
-         "H2D pos");
-      ck(cudaMemcpy(c->vx, hv.data(), m * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
-      ck(cudaMemcpy(c->vy, hv.data() + m, m * sizeof(double), cudaMemcpyHostToDevice),
-         "H2D vy");
-      ck(cudaMemcpy(c->vz, hv.data() + 2 * m, m * sizeof(double), cudaMemcpyHostToDevice),
-         "H2D vz");
-      ck(cudaMemcpy(c->mass, hm.data(), m * sizeof(double), cudaMemcpyHostToDevice), "H2D mass");
-      ck(cudaMemcpy(c->id, hid.data(), m * sizeof(long long), cudaMemcpyHostToDevice), "H2D id");
+    if (!slab) {
+      // the caller's arrays as they are, unpacked on the device (double4
+      // positions, SoA velocities); ids a dense range -> device download
+      if (m > 0) {
+        const auto mm = std::minmax_element(sys->id, sys->id + m);
+        c->ids_dense = static_cast<unsigned long long>(*mm.second - *mm.first) ==
+                       static_cast<unsigned long long>(m - 1);
+        c->dl_lo = *mm.first;
+        ck(cudaMemcpyAsync(c->dl, sys->pos, 3 * m * sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream), "H2D pos");
+        if (sys->vel) {
+          ck(cudaMemcpyAsync(c->dl + 3 * m, sys->vel, 3 * m * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream), "H2D vel");
+        }
+        if (sys->mass) {
+          ck(cudaMemcpyAsync(c->dl + 6 * m, sys->mass, m * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream), "H2D mass");
+        }
+        ck(cudaMemcpyAsync(c->id, sys->id, m * sizeof(long long), cudaMemcpyHostToDevice,
+                           c->stream), "H2D id");
+        k_upload<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
+            static_cast<int>(m), c->dl, sys->vel ? c->dl + 3 * m : nullptr,
+            sys->mass ? c->dl + 6 * m : nullptr, c->posb[0], c->vx, c->vy, c->vz, c->mass);
+        ck(cudaGetLastError(), "k_upload");
+      }
+      mark("upload");
+    } else {
+      std::vector<double4> hp(m);
+      std::vector<double> hv(3 * m, 0.0), hm(m, 1.0);
+      std::vector<long long> hid(m);
+      for (size_t r = 0; r < m; ++r) {
+        const size_t k = static_cast<size_t>(sel[r]);
+        hp[r] = make_double4(sys->pos[3 * k], sys->pos[3 * k + 1], sys->pos[3 * k + 2], 0.0);
+        if (sys->vel) {
+          hv[r] = sys->vel[3 * k];
+          hv[m + r] = sys->vel[3 * k + 1];
+          hv[2 * m + r] = sys->vel[3 * k + 2];
+        }
+        if (sys->mass) hm[r] = sys->mass[k];
+        hid[r] = sys->id[k];
+      }
+      mark("host pack");
+      if (m > 0) {
+        ck(cudaMemcpy(c->posb[0], hp.data(), m * sizeof(double4), cudaMemcpyHostToDevice),
+           "H2D pos");
+        ck(cudaMemcpy(c->vx, hv.data(), m * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
+        ck(cudaMemcpy(c->vy, hv.data() + m, m * sizeof(double), cudaMemcpyHostToDevice),
+           "H2D vy");
+        ck(cudaMemcpy(c->vz, hv.data() + 2 * m, m * sizeof(double), cudaMemcpyHostToDevice),
+           "H2D vz");
+        ck(cudaMemcpy(c->mass, hm.data(), m * sizeof(double), cudaMemcpyHostToDevice),
+           "H2D mass");
+        ck(cudaMemcpy(c->id, hid.data(), m * sizeof(long long), cudaMemcpyHostToDevice),
+           "H2D id");
+      }
+      mark("upload");
     }
     ck(cudaMemcpy(c->posb[0] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
     ck(cudaMemcpy(c->posb[1] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
-    mark("allocate + upload");
     if (slab) alloc_slab(c);
     if (sys->n_bonds > 0) setup_bonds(c, sys, fene);
 
@@ -1922,6 +1991,39 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
                      double* force) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t nn = static_cast<size_t>(c->n);
+    if (c->ids_dense && !c->g.zslab && nn > 0) {
+      // id order by direct placement on the device, positions wrapped there
+      // (the same rounding as host_wrap1), one copy per array into the
+      // caller's buffers
+      double* dpos = c->dl;
+      double* dvel = c->dl + 3 * nn;
+      double* dfrc = c->dl + 6 * nn;
+      long long* did = reinterpret_cast<long long*>(c->dl + 9 * nn);
+      k_download<<<blocks_for(c->n, kBlock), kBlock, 0, c->stream>>>(
+          static_cast<int>(nn), c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->id,
+          c->dl_lo, c->g, pos ? dpos : nullptr, vel ? dvel : nullptr, force ? dfrc : nullptr,
+          did);
+      ck(cudaGetLastError(), "k_download");
+      if (id) {
+        ck(cudaMemcpyAsync(id, did, nn * sizeof(long long), cudaMemcpyDeviceToHost, c->stream),
+           "D2H id");
+      }
+      if (pos) {
+        ck(cudaMemcpyAsync(pos, dpos, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream), "D2H pos");
+      }
+      if (vel) {
+        ck(cudaMemcpyAsync(vel, dvel, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream), "D2H vel");
+      }
+      if (force) {
+        ck(cudaMemcpyAsync(force, dfrc, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream), "D2H force");
+      }
+      ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+      return;
+    }
     HostState h = fetch(c, pos != nullptr, vel != nullptr, force != nullptr, false);
     const size_t n = h.order.size();
     for (size_t r = 0; r < n; ++r) {

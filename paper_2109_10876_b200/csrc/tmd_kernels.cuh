@@ -754,6 +754,55 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) *out = t * scale;
 }
 
+// Engine construction's upload (build_domain, domain.hpp:134-189): the
+// caller's (n, 3) positions and velocities as they are, unpacked to double4
+// positions and SoA velocities; absent velocities are 0, absent masses 1.
+__global__ void __launch_bounds__(kBlock)
+    k_upload(int n, const double* __restrict__ p3, const double* __restrict__ v3,
+             const double* __restrict__ m1, double4* __restrict__ pos, double* __restrict__ vx,
+             double* __restrict__ vy, double* __restrict__ vz, double* __restrict__ mass) {
+  const int r = blockIdx.x * kBlock + threadIdx.x;
+  if (r >= n) return;
+  pos[r] = make_double4(p3[3 * r], p3[3 * r + 1], p3[3 * r + 2], 0.0);
+  vx[r] = v3 ? v3[3 * r] : 0.0;
+  vy[r] = v3 ? v3[3 * r + 1] : 0.0;
+  vz[r] = v3 ? v3[3 * r + 2] : 0.0;
+  mass[r] = m1 ? m1[r] : 1.0;
+}
+
+// flatten_domain (domain.hpp:193-207) on the device for ids forming one
+// dense range: slot s goes to row id[s] - lo, positions wrapped with the
+// reference's wrap (wrap_position, the same rounding as the host's).
+__global__ void __launch_bounds__(kBlock)
+    k_download(int n, const double4* __restrict__ pos, const double* __restrict__ vx,
+               const double* __restrict__ vy, const double* __restrict__ vz,
+               const double* __restrict__ fx, const double* __restrict__ fy,
+               const double* __restrict__ fz, const long long* __restrict__ id, long long lo,
+               Geom g, double* __restrict__ opos, double* __restrict__ ovel,
+               double* __restrict__ ofrc, long long* __restrict__ oid) {
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  if (s >= n) return;
+  const long long ident = id[s];
+  const size_t r = static_cast<size_t>(ident - lo);
+  oid[r] = ident;
+  if (opos) {
+    const double4 p = pos[s];
+    opos[3 * r] = wrap1(p.x, g.L[0]);
+    opos[3 * r + 1] = wrap1(p.y, g.L[1]);
+    opos[3 * r + 2] = wrap1(p.z, g.L[2]);
+  }
+  if (ovel) {
+    ovel[3 * r] = vx[s];
+    ovel[3 * r + 1] = vy[s];
+    ovel[3 * r + 2] = vz[s];
+  }
+  if (ofrc) {
+    ofrc[3 * r] = fx[s];
+    ofrc[3 * r + 1] = fy[s];
+    ofrc[3 * r + 2] = fz[s];
+  }
+}
+
 // Per-step observable row (run_observed): PE and virial of this step's force
 // evaluation (halved full-list sums), KE of the post-kick velocities, written
 // straight into mapped pinned host memory — each recorded step's result

@@ -27,3 +27,19 @@ print(f"create {1e3*(t1-t0):.1f} ms, run(1) {1e3*tr/300:.3f} ms, observe {1e3*to
 t0 = time.perf_counter()
 e.run(300)
 print(f"run(300): {1e3*(time.perf_counter()-t0)/300:.3f} ms/step")
+
+# the bench's e2e sequence, split: create, run_observed (first call captures
+# and instantiates the observed graph), a second run_observed, flatten
+import os
+os.environ.setdefault("TMD_DEBUG_TIMING", "1")
+t0 = time.perf_counter()
+e3 = E.Engine(f, E.Interactions(), 0.3, cfg)
+t1 = time.perf_counter()
+e3.run_observed(1000, stride=1)
+t2 = time.perf_counter()
+e3.run_observed(1000, stride=1)
+t3 = time.perf_counter()
+e3.flatten()
+t4 = time.perf_counter()
+print(f"e2e split: create {1e3*(t1-t0):.1f} ms, run_observed#1 {1e3*(t2-t1):.1f} ms, "
+      f"run_observed#2 {1e3*(t3-t2):.1f} ms, flatten {1e3*(t4-t3):.1f} ms")

@@ -220,7 +220,14 @@ uint64_t tmd_gpu_launch_count(const tmd_gpu_ctx* ctx);
  * the FLOP-side roofline denominator. device = -1: current device. */
 int tmd_gpu_fp64_peak(int device, double* tflops);
 
+/* Frees the context. Its two large device blocks (per-slot arrays, list)
+ * go to a process-wide cache for the next context of the process (at most
+ * 16 GiB per device, reused at <= 1.5x the request). */
 void tmd_gpu_destroy(tmd_gpu_ctx* ctx);
+
+/* Returns every cached block of the process to the driver (e.g. before
+ * handing the memory to another library). */
+void tmd_gpu_release_cache(void);
 
 /* ---- z-slab decomposition (one context per GPU) --------------
  * Replaces the reference's in-process subnode decomposition

@@ -37,7 +37,7 @@ EXPORTS = [
     "tmd_gpu_slab_recut", "tmd_gen_chains", "tmd_gpu_brute_force", "tmd_gen_lattice",
     "tmd_gen_spherical", "tmd_gen_random", "tmd_gpu_run_observed", "tmd_nccl_unique_id",
     "tmd_gpu_slab_attach_nccl", "tmd_gpu_slab_setup", "tmd_gpu_slab_run",
-    "tmd_gpu_slab_observe", "tmd_balanced_cuts",
+    "tmd_gpu_slab_observe", "tmd_balanced_cuts", "tmd_gpu_release_cache",
 ]
 
 
@@ -156,6 +156,8 @@ def lib() -> C.CDLL:
     L.tmd_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_destroy.argtypes = [P]
     L.tmd_gpu_destroy.restype = None
+    L.tmd_gpu_release_cache.argtypes = []
+    L.tmd_gpu_release_cache.restype = None
     L.tmd_gen_fcc.argtypes = [C.c_int, C.c_double, C.c_double, P, P, P]
     L.tmd_gpu_brute_force.argtypes = [C.POINTER(TmdSystem), C.POINTER(TmdLjParams), C.c_double,
                                       C.c_int, P, P, P, C.c_size_t, C.POINTER(C.c_size_t)]

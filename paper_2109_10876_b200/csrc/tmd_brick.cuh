@@ -1400,9 +1400,11 @@ __global__ void __launch_bounds__(kForceThreads)
       }
       if (active) {
         integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
-        fx[i] = ax;
-        fy[i] = ay;
-        fz[i] = az;
+        if (kMode != kFused) {  // a fused step's force only feeds its own kicks
+          fx[i] = ax;
+          fy[i] = ay;
+          fz[i] = az;
+        }
       }
     }
   }
@@ -1468,9 +1470,11 @@ __global__ void __launch_bounds__(128)
     }
     if (it.bt.on) bond_accumulate(i, pi, pos, it.bt, g, id, ctrl, ax, ay, az, e, w);
     integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
-    fx[i] = ax;
-    fy[i] = ay;
-    fz[i] = az;
+    if (kMode != kFused) {  // a fused step's force only feeds its own kicks
+      fx[i] = ax;
+      fy[i] = ay;
+      fz[i] = az;
+    }
   }
   const double te = block_sum<128>(e, red);
   const double tw = block_sum<128>(w, red);

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <type_traits>
@@ -71,6 +72,84 @@ T* dalloc(size_t count) {
   return static_cast<T*>(p);
 }
 
+// Process-wide cache of the two big per-context blocks (the per-slot arena
+// and the neighbour list). cudaMalloc / cudaFree of hundreds of MB cost from
+// 0.5 to >100 ms each (page mapping), so a closed engine's blocks are kept
+// for the next engine of the process (a sweep, a restart, the benchmark's
+// end-to-end engine) instead of being returned to the driver; blocks are
+// reused when they are at most 1.5x the request, the cache holds at most
+// 16 GiB per device and is dropped whenever a cudaMalloc fails.
+struct CachedBlock {
+  int device;
+  size_t bytes;
+  void* p;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+constexpr size_t kCacheMax = size_t{16} << 30;
+
+void cache_drop(int device) {  // (caller holds g_cache_mu)
+  for (size_t k = 0; k < g_cache.size();) {
+    if (g_cache[k].device == device) {
+      cudaFree(g_cache[k].p);
+      g_cache[k] = g_cache.back();
+      g_cache.pop_back();
+    } else {
+      ++k;
+    }
+  }
+}
+
+// A block of at least `bytes` (its real size in *got).
+void* big_alloc(size_t bytes, size_t* got) {
+  bytes = std::max<size_t>(bytes, 256);
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t best = g_cache.size();
+    for (size_t k = 0; k < g_cache.size(); ++k) {
+      const CachedBlock& b = g_cache[k];
+      if (b.device == dev && b.bytes >= bytes && b.bytes <= bytes + bytes / 2 &&
+          (best == g_cache.size() || b.bytes < g_cache[best].bytes)) {
+        best = k;
+      }
+    }
+    if (best < g_cache.size()) {
+      void* p = g_cache[best].p;
+      *got = g_cache[best].bytes;
+      g_cache[best] = g_cache.back();
+      g_cache.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      cache_drop(dev);
+    }
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  *got = bytes;
+  return p;
+}
+
+void big_free(void* p, size_t bytes) {
+  if (!p) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  size_t held = 0;
+  for (const CachedBlock& b : g_cache) held += b.device == dev ? b.bytes : 0;
+  if (held + bytes > kCacheMax) {
+    cudaFree(p);
+    return;
+  }
+  g_cache.push_back({dev, bytes, p});
+}
+
 std::string fmt_g(double v) {
   char b[64];
   std::snprintf(b, sizeof b, "%g", v);
@@ -110,6 +189,7 @@ struct tmd_gpu_ctx {
   double* dl = nullptr;
   char* arena = nullptr;  // the per-slot arrays of a non-slab context, one allocation
   size_t arena_bytes = 0;
+  size_t nbr_bytes = 0;   // size of the list block (big_alloc)
   int* slot_of_id = nullptr;       // [id_span] (owned + ghost slots), -1 = absent
   int* bond_off = nullptr;         // [id_span + 1] CSR over id - id_min
   int* bond_nbr = nullptr;         // partner id - id_min
@@ -268,7 +348,7 @@ void free_all(tmd_gpu_ctx* c) {
   void* ptrs[] = {c->posb[0], c->posb[1], c->pos2, c->snap, c->vx, c->vy, c->vz,
                   c->vx2,  c->vy2,   c->vz2,  c->fx,    c->fy,      c->fz,
                   c->mass, c->mass2, c->id,   c->id2,   c->cell,    c->cell2,
-                  c->rank, c->perm,  c->count, c->start, c->nbr,    c->nnbr,
+                  c->rank, c->perm,  c->count, c->start, c->nnbr,
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
                   c->ck_fx, c->ck_fy, c->ck_fz,
@@ -285,7 +365,8 @@ void free_all(tmd_gpu_ctx* c) {
     const char* q = static_cast<const char*>(p);
     if (p && !(a0 && q >= a0 && q < a1)) cudaFree(p);
   }
-  if (c->arena) cudaFree(c->arena);
+  big_free(c->arena, c->arena_bytes);  // back to the process cache
+  big_free(c->nbr, c->nbr_bytes);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->obs_host) cudaFreeHost(c->obs_host);
   if (c->h_scalars) cudaFreeHost(c->h_scalars);
@@ -627,14 +708,14 @@ int round8(int v) { return (v + 7) / 8 * 8; }
 
 void alloc_list(tmd_gpu_ctx* c, int cap) {
   c->graph_dirty = true;  // captured kernels hold the old list pointer / capacity
-  if (c->nbr) cudaFree(c->nbr);
+  big_free(c->nbr, c->nbr_bytes);
   c->nbr = nullptr;
   c->cap = round8(std::max(cap, 8));
   c->bg.cap = c->cap;
   c->nbr_words = c->variant == 1
                      ? static_cast<size_t>(c->cap) * c->stride
                      : static_cast<size_t>(c->ngroups_max) * c->cap * 32;
-  c->nbr = dalloc<uint32_t>(c->nbr_words);
+  c->nbr = static_cast<uint32_t*>(big_alloc(c->nbr_words * sizeof(uint32_t), &c->nbr_bytes));
   set_cap_in_ctrl(c);
 }
 
@@ -1637,8 +1718,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     if (!slab) {
       size_t tot = 0;
       for (const auto& e : plan) tot += (e.second + 255) / 256 * 256;
-      c->arena = dalloc<char>(tot);
-      c->arena_bytes = tot;
+      c->arena = static_cast<char*>(big_alloc(tot, &c->arena_bytes));
       size_t off = 0;
       for (const auto& e : plan) {
         *e.first = c->arena + off;
@@ -2645,6 +2725,18 @@ int tmd_gpu_brute_force(const tmd_system* sys, const tmd_lj_params* lj, double r
   });
   if (rc != TMD_OK) g_create_error = tmp.err;
   return rc;
+}
+
+void tmd_gpu_release_cache(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (const CachedBlock& b : g_cache) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(b.device);
+    cudaFree(b.p);
+    cudaSetDevice(cur);
+  }
+  g_cache.clear();
 }
 
 void tmd_gpu_destroy(tmd_gpu_ctx* c) {

@@ -426,6 +426,11 @@ class Engine:
         return ms.value
 
 
+def release_cache() -> None:
+    """Return the device blocks closed engines left in the process cache."""
+    _abi.lib().tmd_gpu_release_cache()
+
+
 # -- setup helpers (host-side, C ABI) --------------------------------------------
 
 def gen_fcc(cells: int, rho: float, temperature: float, seed: int,

@@ -455,3 +455,26 @@ def test_empty_system(timers):
     eng.run(10)
     assert eng.step_count() == 10 and eng.observe().temperature == 0.0
     assert eng.flatten().size() == 0 and len(eng.pairs()) == 0
+
+
+def test_closed_engine_blocks_are_reused_safely():
+    """A closed engine's device blocks go to the process cache and back out to
+    the next engine: that engine starts from its own state (no leftovers of
+    the previous list or arrays), before and after the cache is released."""
+    g = load("jit6_s41_T08")
+    ref_eng = gpu_engine(g)
+    ref_eng.run(30)
+    want = ref_eng.flatten()
+    ref_eng.close()
+    for release in (False, True):
+        big = E.Engine(E.gen_fcc(12, 0.8442, 1.0, 5), E.Interactions(), 0.3)
+        big.run(5)
+        big.close()
+        if release:
+            E.release_cache()
+        eng = gpu_engine(g)
+        eng.run(30)
+        got = eng.flatten()
+        np.testing.assert_array_equal(got.pos, want.pos)
+        np.testing.assert_array_equal(got.vel, want.vel)
+        eng.close()

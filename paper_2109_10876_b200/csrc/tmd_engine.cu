@@ -442,8 +442,11 @@ void launch_scan(tmd_gpu_ctx* c, int n, int* counts, int* out) {
   k_scan_apply<<<tiles, kScanThreads, 0, c->ls>>>(n, counts, c->scan_tmp, out, c->ctrl);
 }
 
+// Mean cell occupancy below which the in-cell id sort runs a thread per slot.
+constexpr double kSortCellWarpMin = 8.0;
+
 void launch_resort(tmd_gpu_ctx* c) {
-  c->launches += 6;
+  c->launches += 5;
   const int n = static_cast<int>(c->n);
   const int nb = c->nblk;
   k_wrap_bin<<<nb, kBlock, 0, c->ls>>>(n, c->pos, c->id, c->cell, c->rank,
@@ -451,10 +454,17 @@ void launch_resort(tmd_gpu_ctx* c) {
   launch_scan(c, c->g.owned_cells, c->count, c->start);
   k_scatter<<<nb, kBlock, 0, c->ls>>>(n, c->cell, c->rank, c->start,
                                           c->cell_rank, c->g, c->perm, c->ctrl);
-  k_sort_cells<<<blocks_for(static_cast<int64_t>(c->g.owned_cells) * 32, kBlock), kBlock, 0,
-                 c->ls>>>(
-      c->g.owned_cells, c->start, c->perm, c->id, c->ctrl);
-  k_permute<<<nb, kBlock, 0, c->ls>>>(n, c->perm, c->pos, c->vx, c->vy,
+  // in-cell id order: a warp per cell for dense cells, a thread per slot
+  // (writing the order into the free `rank` array) for sparse ones
+  const bool sparse = c->occupancy > 0.0 && c->occupancy < kSortCellWarpMin;
+  if (sparse) {
+    k_sort_cells_thread<<<nb, kBlock, 0, c->ls>>>(n, c->start, c->cell, c->cell_rank, c->g,
+                                                  c->perm, c->id, c->rank, c->ctrl);
+  } else {
+    k_sort_cells<<<blocks_for(static_cast<int64_t>(c->g.owned_cells) * 32, kBlock), kBlock, 0,
+                   c->ls>>>(c->g.owned_cells, c->start, c->perm, c->id, c->ctrl);
+  }
+  k_permute<<<nb, kBlock, 0, c->ls>>>(n, sparse ? c->rank : c->perm, c->pos, c->vx, c->vy,
                                           c->vz, c->mass, c->id, c->cell,
                                           c->pos2, c->vx2, c->vy2, c->vz2,
                                           c->mass2, c->id2, c->cell2, c->ctrl);
@@ -462,10 +472,14 @@ void launch_resort(tmd_gpu_ctx* c) {
                                             c->vz2, c->mass2, c->id2, c->cell2,
                                             c->pos, c->vx, c->vy, c->vz,
                                             c->mass, c->id, c->cell, c->ctrl);
-  // list groups per brick (32 particles each), scanned into group offsets
-  k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->ls>>>(
-      c->bg.nbricks, c->brick_rank_off, c->start, c->ngroups, c->ctrl);
-  launch_scan(c, c->bg.nbricks, c->ngroups, c->group_off);
+  // list groups per brick (32 particles each), scanned into group offsets:
+  // only the brick-local list of variant 2 has per-brick groups
+  if (c->variant == 2) {
+    c->launches += 1;
+    k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->ls>>>(
+        c->bg.nbricks, c->brick_rank_off, c->start, c->ngroups, c->ctrl);
+    launch_scan(c, c->bg.nbricks, c->ngroups, c->group_off);
+  }
 }
 
 size_t build_smem(const tmd_gpu_ctx* c) {

@@ -1192,7 +1192,8 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
 // in a per-thread 8-slot shared-memory buffer and leave as whole 32-B sectors
 // of the chunked list. No staging: cheap per particle where cells are sparse
 // (the Kremer-Grest melt holds 3 beads per cell), where the brick kernels
-// spend their time on per-CTA halo setup.
+// spend their time on per-CTA halo setup. Each stencil row (3 x-adjacent
+// cells) loads its three ranks and ranges together before testing.
 __global__ void __launch_bounds__(kBlock)
     k_build_thread(int n, const double4* __restrict__ pos, const int* __restrict__ cell,
                    const int* __restrict__ start, const int* __restrict__ cell_rank, Geom g,
@@ -1214,6 +1215,18 @@ __global__ void __launch_bounds__(kBlock)
     const int cy = (c / g.dims[0]) % g.dims[1];
     const int cz = c / dxy;
     const int lz = g.zslab ? cz - g.z0 + 1 : cz;  // local layer (slab: ghost layers 0, ldz-1)
+    // x neighbours of the row: wrapped column and image code (fixed per particle)
+    int txs[3];
+    uint32_t cxs[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      int tx = cx + k - 1;
+      uint32_t code_x = 0;
+      if (tx < 0) { tx += g.dims[0]; code_x = 2; }
+      else if (tx >= g.dims[0]) { tx -= g.dims[0]; code_x = 1; }
+      txs[k] = tx;
+      cxs[k] = code_x << 25;
+    }
     for (int oz = -1; oz <= 1; ++oz) {
       int tz = lz + oz;
       uint32_t code_z = 0;
@@ -1231,17 +1244,23 @@ __global__ void __launch_bounds__(kBlock)
         uint32_t code_y = 0;
         if (ty < 0) { ty += g.dims[1]; code_y = 2; }
         else if (ty >= g.dims[1]) { ty -= g.dims[1]; code_y = 1; }
-        for (int ox = -1; ox <= 1; ++ox) {
-          int tx = cx + ox;
-          uint32_t code_x = 0;
-          if (tx < 0) { tx += g.dims[0]; code_x = 2; }
-          else if (tx >= g.dims[0]) { tx -= g.dims[0]; code_x = 1; }
+        // the row's three cells: ranks and particle ranges loaded together
+        // (independent loads) before any candidate is tested
+        const int rowc = g.dims[0] * ty + dxy * tz;
+        int jb[3], je[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int rt = cell_rank[txs[k] + rowc];
+          jb[k] = start[rt];
+          je[k] = start[rt + 1];
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int ox = k - 1;
           const int first = ox != 0 ? ox : (oy != 0 ? oy : oz);
-          const uint32_t img = (code_x << 25) | (code_y << 27) | (code_z << 29);
+          const uint32_t img = cxs[k] | (code_y << 27) | (code_z << 29);
           const uint32_t tag = img | ((img != 0u && first < 0) ? kFlagIUpper : 0u);
-          const int rt = cell_rank[tx + g.dims[0] * ty + dxy * tz];
-          const int jb = start[rt], je = start[rt + 1];
-          for (int j = jb; j < je; ++j) {
+          for (int j = jb[k]; j < je[k]; ++j) {
             const uint32_t ent = static_cast<uint32_t>(j) | tag;
             double dx, dy, dz;
             pair_delta(pi, ldg_pos256(pos + j), ent, g, dx, dy, dz);

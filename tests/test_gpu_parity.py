@@ -478,3 +478,29 @@ def test_closed_engine_blocks_are_reused_safely():
         np.testing.assert_array_equal(got.pos, want.pos)
         np.testing.assert_array_equal(got.vel, want.vel)
         eng.close()
+
+
+@pytest.mark.parametrize("n,rho,min_d", [(1154, 0.8442, 0.8), (1641, 1.2, 0.7)])
+def test_cells_of_more_than_a_warp(ref, n, rho, min_d):
+    """Cells holding more than 32 particles (3x3x3 grid of 3.7-sigma cells):
+    the warp-per-cell builds take them in several passes of 32 lanes, with the
+    culled stream's bounding box per pass; every build kind must still emit
+    the reference's pair set, in the same order (bitwise forces)."""
+    box, ids, pos, vel = ref.gen_random(n, rho, min_d, 0.72, 7)
+    want_pairs = ref.oracle_pairs(box, ids, pos, 2.8)
+    want_f, want_pe = ref.oracle_forces(box, ids, pos)
+    forces = []
+    for build in (3, 5, 6):
+        eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3,
+                       E.EngineConfig(build=build))
+        assert tuple(eng.list_stats()["dims"]) == (3, 3, 3)
+        _, cell = eng.cell_of()
+        assert np.bincount(cell).max() > 32
+        np.testing.assert_array_equal(eng.pairs(), want_pairs)
+        _, f = eng.forces()
+        assert np.abs(f - want_f).max() <= 1e-10
+        assert_rel(eng.observe().potential, want_pe, 1e-11, "PE")
+        forces.append(f)
+        eng.close()
+    np.testing.assert_array_equal(forces[0], forces[1])
+    np.testing.assert_array_equal(forces[0], forces[2])

@@ -504,3 +504,40 @@ def test_cells_of_more_than_a_warp(ref, n, rho, min_d):
         eng.close()
     np.testing.assert_array_equal(forces[0], forces[1])
     np.testing.assert_array_equal(forces[0], forces[2])
+
+
+def planted_pairs(seed, n_pairs=300, L=20.0, rv=2.8):
+    """A dilute gas of planted pairs at separations straddling r_v by a few
+    ulps (and exactly r_v as written in decimal), many of them across the
+    periodic boundary: every one of them lands in the FP32 prefilter's
+    rounding band, where membership is the exact FP64 decision."""
+    rng = np.random.default_rng(seed)
+    deltas = np.array([0.0, 1e-16, -1e-16, 2e-16, -2e-16, 5e-16, -5e-16, 1e-13, -1e-13,
+                       1e-9, -1e-9])
+    p = rng.uniform(0.0, L, (n_pairs, 3))
+    near = rng.random(n_pairs) < 0.4  # put some pairs at a face of the box
+    p[near, rng.integers(0, 3, near.sum())] = rng.uniform(0.0, 0.5, near.sum())
+    u = rng.normal(size=(n_pairs, 3))
+    u /= np.linalg.norm(u, axis=1)[:, None]
+    d = rv * (1.0 + deltas[rng.integers(0, len(deltas), n_pairs)])
+    q = p + d[:, None] * u
+    pos = np.concatenate([p, q]).reshape(-1, 3)
+    ids = np.arange(1, 2 * n_pairs + 1, dtype=np.int64)
+    return np.array([L, L, L]), ids, pos, np.zeros_like(pos)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_rounding_band_pairs_match_the_reference(ref, seed):
+    """Pairs at |r - r_v| of a few ulps: the pair set of every build kind is
+    the reference engine's own (its rounding, its image-shift orientation)."""
+    box, ids, pos, vel = planted_pairs(seed)
+    want = ref.RefEngine(box, ids, pos, vel, r_skin=0.3).pairs()
+    n = len(ids) // 2
+    kept = set(map(tuple, want.tolist()))
+    planted_in = sum((k + 1, k + 1 + n) in kept for k in range(n))
+    assert 0.3 * n < planted_in < 0.8 * n  # the band really splits them
+    for build in (3, 5, 6):
+        eng = E.Engine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3,
+                       E.EngineConfig(build=build))
+        np.testing.assert_array_equal(eng.pairs(), want)
+        eng.close()

@@ -273,6 +273,7 @@ def run_ours(args) -> None:
 
     # -- roofline of the force kernel -----------------------------
     st = eng.list_stats()
+    kc = eng.kernel_config()
     E_ent, P_cut = st["entries"], st["in_cut"]
     t_force_ms = eng.time_force_kernel(args.force_reps)
     B = n * 52 + E_ent * 28
@@ -306,7 +307,8 @@ def run_ours(args) -> None:
     roof["l1"] = {"model": "one L1 wavefront per gathered list entry, 1 wavefront/clk/SM",
                   "t_ms": 1e3 * t_l1, "frac": 1e3 * t_l1 / t_force_ms, "sm_mhz": clocks_mhz}
     roof.update({
-        "kernel": "k_forces_l1", "algorithmic_bytes": B, "algorithmic_flops": F,
+        "kernel": "k_forces_l1" if kc["lanes"] == 1 else f"k_forces_lanes<{kc['lanes']}>",
+        "algorithmic_bytes": B, "algorithmic_flops": F,
         "entries": E_ent, "in_cut_entries": P_cut, "kernel_ms": t_force_ms,
         "t_roof_ms": 1e3 * max(t_hbm, t_flop), "fp64_peak_tflops_measured": fp64,
         "peak_source": peaks["source"], "share_of_step": t_force_ms / ms_per_step,

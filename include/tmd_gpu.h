@@ -101,7 +101,9 @@ typedef struct tmd_engine_params {
                         [2] 1 = no CUDA graphs;
                         [3] variant-3 list build: 0 = by cell occupancy,
                         3 = warp per cell, 5 = thread per particle,
-                        6 = warp per cell over a culled candidate stream */
+                        6 = warp per cell over a culled candidate stream;
+                        [4] variant-3 threads per particle (1/2/4/8, 0 = by
+                        particle count: small systems get more) */
   /* EngineConfig::thermostat (optional<LangevinParams>, potentials.hpp:174-178):
    * thermostat = 0 is NVE. The Langevin force of thermostat_and_half_kick
    * (engine.hpp:209-239) with counter_normal3(seed, kThermostat, step, id). */
@@ -212,6 +214,11 @@ int tmd_gpu_time_list_build(tmd_gpu_ctx* ctx, int reps, double* ms_per_build);
 /* Raw stream handle (cudaStream_t) of the context, for callers that want to
  * order their own work after the engine's. */
 void* tmd_gpu_stream(tmd_gpu_ctx* ctx);
+
+/* The kernels this context runs (no reference counterpart; bench and test
+ * accounting): force/list variant (1-3), variant-3 threads per particle
+ * (1/2/4/8) and list build kind (3/5/6). Getter; null outputs are skipped. */
+void tmd_gpu_kernel_config(const tmd_gpu_ctx* ctx, int* variant, int* lanes, int* build_kind);
 
 /* Kernels this context has enqueued so far (bench accounting). Getter. */
 uint64_t tmd_gpu_launch_count(const tmd_gpu_ctx* ctx);

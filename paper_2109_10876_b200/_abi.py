@@ -28,6 +28,7 @@ EXPORTS = [
     "tmd_gpu_stream", "tmd_gpu_destroy", "tmd_gen_fcc",
     "tmd_thermal_velocities", "tmd_counter_uniform3", "tmd_counter_normal3",
     "tmd_gpu_abi_version", "tmd_gpu_launch_count", "tmd_gpu_fp64_peak",
+    "tmd_gpu_kernel_config",
     "tmd_gpu_time_list_build",
     "tmd_gpu_create_slab", "tmd_gpu_slab_info", "tmd_gpu_slab_max_d2",
     "tmd_gpu_slab_decide", "tmd_gpu_slab_migrate_out", "tmd_gpu_slab_migrate_in",
@@ -151,6 +152,9 @@ def lib() -> C.CDLL:
     L.tmd_gpu_time_list_build.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_stream.argtypes = [P]
     L.tmd_gpu_stream.restype = P
+    L.tmd_gpu_kernel_config.argtypes = [P, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)]
+    L.tmd_gpu_kernel_config.restype = None
     L.tmd_gpu_launch_count.argtypes = [P]
     L.tmd_gpu_launch_count.restype = C.c_uint64
     L.tmd_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]

@@ -1504,6 +1504,99 @@ __global__ void __launch_bounds__(128)
   integrate_block<kMode, 128>(ke, d2, red, it, ctrl);
 }
 
+// ---------------------------------------------------------------------------
+// Variant 3 for small systems (the 32,000-particle configs[0], or a slab of
+// a many-GPU run): kLanes consecutive threads share one particle. Thread
+// (p, s) takes chunks s, s + kLanes, ... of p's list, so one particle's ~10
+// chunks are gathered kLanes-wide instead of by one serial thread: at 32K a
+// one-lane grid is 1,000 warps (7 per SM, latency-bound); eight lanes make
+// it 8,000. The lanes' partial forces are combined by a fixed xor-shuffle
+// tree (deterministic, like every other reduction here); energy and virial
+// partials go to the block sums lane by lane. Same list, same pair
+// arithmetic as k_forces_l1; only the summation order of a particle's force
+// differs (a rounding-level difference, within the parity tolerances).
+// Resident blocks per SM the register budget must allow (a grid of 128-
+// particle blocks fits one wave down to ~32K particles).
+constexpr int lanes_min_blocks(int lanes) { return lanes == 2 ? 3 : (lanes == 4 ? 2 : 1); }
+
+template <int kUnroll, int kMode, int kLanes>
+__global__ void __launch_bounds__(128 * kLanes, lanes_min_blocks(kLanes))
+    k_forces_lanes(int n, const double4* __restrict__ pos, const uint32_t* __restrict__ list,
+                   const int* __restrict__ nnbr, int cap, Geom g, LjConst lj,
+                   double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
+                   double* __restrict__ part_e, double* __restrict__ part_w,
+                   const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
+  if (ctrl->halt) return;
+  __shared__ double red[4 * kLanes];
+  const int sub = threadIdx.x % kLanes;
+  const int i = blockIdx.x * 128 + threadIdx.x / kLanes;
+  double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  bool zero = false;
+  double4 pi = make_double4(0.0, 0.0, 0.0, 0.0);
+  int cnt = 0;
+  const uint32_t* row = list;
+  if (i < n) {
+    pi = pos[i];
+    cnt = nnbr[i];
+    row = list + list_slot(i >> 5, cap, i & 31, 0);
+    for (int c0 = sub * 8; c0 < cnt; c0 += 8 * kLanes) {
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32));
+      const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32 + 4));
+      const uint32_t ents[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int u0 = 0; u0 < 8; u0 += kUnroll) {
+        double4 pj[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) pj[u] = ldg_pos256(pos + (ents[u0 + u] & kIdxMask));
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          lj_accumulate(pi, pj[u].x, pj[u].y, pj[u].z, ents[u0 + u], g, lj, ax, ay, az, e, w,
+                        zero);
+        }
+      }
+    }
+  }
+  // lanes of one particle are kLanes consecutive threads of one warp
+#pragma unroll
+  for (int o = 1; o < kLanes; o <<= 1) {
+    ax += __shfl_xor_sync(0xffffffffu, ax, o);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o);
+    az += __shfl_xor_sync(0xffffffffu, az, o);
+  }
+  // any lane of the particle saw r2 == 0: its lane 0 finds and reports it
+  const unsigned zmask = __ballot_sync(0xffffffffu, zero);
+  const unsigned grp = ((1u << kLanes) - 1u) << ((threadIdx.x & 31) & ~(kLanes - 1));
+  if (i < n && sub == 0 && (zmask & grp)) {
+    for (int k = 0; k < cnt; ++k) {
+      const uint32_t ent = row[(k >> 3) * 256 + (k & 7)];
+      const double4 pj = pos[ent & kIdxMask];
+      double dx, dy, dz;
+      pair_delta(pi, pj, ent, g, dx, dy, dz);
+      if (exact_r2(dx, dy, dz) == 0.0) {
+        record_error(ctrl, kStatOverlap, id[i], id[ent & kIdxMask]);
+        break;
+      }
+    }
+  }
+  if (i < n && sub == 0) {
+    if (it.bt.on) bond_accumulate(i, pi, pos, it.bt, g, id, ctrl, ax, ay, az, e, w);
+    integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
+    if (kMode != kFused) {
+      fx[i] = ax;
+      fy[i] = ay;
+      fz[i] = az;
+    }
+  }
+  const double te = block_sum<128 * kLanes>(e, red);
+  const double tw = block_sum<128 * kLanes>(w, red);
+  if (threadIdx.x == 0) {
+    part_e[blockIdx.x] = te;
+    part_w[blockIdx.x] = tw;
+  }
+  integrate_block<kMode, 128 * kLanes>(ke, d2, red, it, ctrl);
+}
+
 // Tap for variant 3: chunked global-slot list -> ELL-transposed copy.
 __global__ void __launch_bounds__(128)
     k_decode_chunked(int n, const uint32_t* __restrict__ list, const int* __restrict__ nnbr,

@@ -45,6 +45,14 @@ thread_local std::string g_create_error;
 // reserved[0] = 0); chosen by the ncu/CUDA-event comparison in
 // profiles/ (see DESIGN.md §Force kernel variants).
 constexpr int kDefaultVariant = 3;
+// Below this many particles x lanes the one-thread-per-particle force grid
+// leaves the SMs latency-bound; small systems split each particle's list
+// over 2 or 4 threads (k_forces_lanes). Measured on B200 (scripts/
+// lanes_probe.py, force kernel ms at lanes 1/2/4): 32K 0.033/0.021/0.019,
+// 62.5K 0.035/0.033/0.031, 131K 0.044/0.049/0.052. Eight lanes (1024-thread
+// blocks, one per SM) never won by more than 1 %.
+constexpr int64_t kLanesTargetThreads = 148 * 768;
+constexpr int kLanesAutoMax = 4;
 
 struct CudaFail {
   std::string what;
@@ -215,6 +223,8 @@ struct tmd_gpu_ctx {
   // brick-major ordering + variant selection
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
   int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
+  int lanes = 1;              // variant 3: threads per particle (1, 2, 4, 8)
+  bool lanes_auto = true;     // lanes chosen from the particle count at create
   double occupancy = 0.0;     // particle-weighted mean cell occupancy at the first binning
   bool build_auto = false;    // build kind chosen from `occupancy` at the first binning
   int build_kind = 3;         // variant 3 list build: 3 = warp per cell (brick-staged),
@@ -591,6 +601,13 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
     k_lj_forces<kMode><<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->stride, c->g, c->lj,
         c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
+  } else if (c->variant == 3 && c->lanes > 1) {
+    auto kern = c->lanes == 2 ? k_forces_lanes<4, kMode, 2>
+                              : (c->lanes == 4 ? k_forces_lanes<2, kMode, 4>
+                                               : k_forces_lanes<2, kMode, 8>);
+    kern<<<c->nblk, 128 * c->lanes, 0, c->ls>>>(
+        static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
+        c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else if (c->variant == 3) {
     auto kern = c->unroll == 1 ? k_forces_l1<1, kMode>
                                : (c->unroll == 2 ? k_forces_l1<2, kMode>
@@ -1677,6 +1694,17 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
     }
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
+    {
+      const int l = params->reserved[4];
+      c->lanes_auto = !(l == 1 || l == 2 || l == 4 || l == 8);
+      c->lanes = c->lanes_auto ? 1 : l;
+    }
+    // auto: double the lanes per particle while the force grid holds fewer
+    // than kLanesTargetThreads threads; fixed for the context's life
+    // (captured graphs keep their grids)
+    if (c->lanes_auto) {
+      while (c->lanes < kLanesAutoMax && c->n * c->lanes < kLanesTargetThreads) c->lanes *= 2;
+    }
     c->build_kind = params->reserved[3];
     c->build_auto = c->build_kind != 3 && c->build_kind != 5 && c->build_kind != 6;
     if (c->build_auto) c->build_kind = 6;  // decided at the first binning (setup_pass)
@@ -2286,6 +2314,12 @@ int tmd_gpu_time_list_build(tmd_gpu_ctx* c, int reps, double* ms) {
 void* tmd_gpu_stream(tmd_gpu_ctx* c) { return c->stream; }
 
 uint64_t tmd_gpu_launch_count(const tmd_gpu_ctx* c) { return c->launches; }
+
+void tmd_gpu_kernel_config(const tmd_gpu_ctx* c, int* variant, int* lanes, int* build_kind) {
+  if (variant) *variant = c->variant;
+  if (lanes) *lanes = c->variant == 3 ? c->lanes : 1;
+  if (build_kind) *build_kind = c->variant == 3 ? c->build_kind : 0;
+}
 
 int tmd_gpu_fp64_peak(int device, double* tflops) {
   tmd_gpu_ctx tmp;

@@ -140,6 +140,9 @@ class EngineConfig:
     # (brick-staged), 5 = thread per particle (sparse cells), 6 = warp per
     # cell over a culled candidate stream
     build: int = 0
+    # variant-3 force kernel: threads per particle (1, 2, 4, 8; 0 = by
+    # particle count, more lanes for small systems)
+    lanes: int = 0
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off
     force_cap: float = 0.0
@@ -248,6 +251,7 @@ def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEn
     p.nbr_capacity = cfg.nbr_capacity
     p.reserved[0] = int(cfg.variant)
     p.reserved[3] = int(cfg.build)
+    p.reserved[4] = int(cfg.lanes)
     p.force_cap = float(cfg.force_cap)
     if cfg.thermostat is not None:
         p.thermostat = 1
@@ -407,6 +411,13 @@ class Engine:
         _check(_abi.lib().tmd_gpu_list_stats(self._h, C.byref(s)), self._h)
         return dict(n=s.n, entries=s.entries, in_cut=s.in_cut, max_count=s.max_count,
                     capacity=s.capacity, dims=tuple(s.dims), cell_len=tuple(s.cell_len))
+
+    def kernel_config(self) -> dict:
+        """Which kernels this engine runs: force/list variant, threads per
+        particle of the variant-3 force kernel, list build kind."""
+        v, l, b = C.c_int(), C.c_int(), C.c_int()
+        _abi.lib().tmd_gpu_kernel_config(self._h, C.byref(v), C.byref(l), C.byref(b))
+        return dict(variant=v.value, lanes=l.value, build_kind=b.value)
 
     def launch_count(self) -> int:
         return int(_abi.lib().tmd_gpu_launch_count(self._h))

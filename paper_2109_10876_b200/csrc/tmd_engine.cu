@@ -223,6 +223,7 @@ struct tmd_gpu_ctx {
   // brick-major ordering + variant selection
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
   int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
+  bool unroll_auto = true;    // unroll chosen with the build kind (sparse cells: 2)
   int lanes = 1;              // variant 3: threads per particle (1, 2, 4, 8)
   bool lanes_auto = true;     // lanes chosen from the particle count at create
   double occupancy = 0.0;     // particle-weighted mean cell occupancy at the first binning
@@ -795,6 +796,10 @@ void choose_build_kind(tmd_gpu_ctx* c) {
   }
   c->occupancy = s1 > 0.0 ? s2 / s1 : 0.0;
   c->build_kind = c->occupancy >= kBuildCellWarpMin ? 6 : 5;
+  // sparse cells (short lists, ~12 entries in the KG melt): two gathers in
+  // flight per thread beat four (KG force kernel 0.281 vs 0.307 ms at 4M,
+  // scripts/kg_probe.py; fewer registers, more resident warps)
+  if (c->unroll_auto) c->unroll = c->build_kind == 5 ? 2 : 4;
   c->build_auto = false;
   c->graph_dirty = true;
 }
@@ -1694,6 +1699,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
     }
     c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
+    c->unroll_auto = params->reserved[1] <= 0;
     {
       const int l = params->reserved[4];
       c->lanes_auto = !(l == 1 || l == 2 || l == 4 || l == 8);

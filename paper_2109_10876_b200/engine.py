@@ -143,6 +143,9 @@ class EngineConfig:
     # variant-3 force kernel: threads per particle (1, 2, 4, 8; 0 = by
     # particle count, more lanes for small systems)
     lanes: int = 0
+    # variant-3 force kernel: neighbour gathers in flight per thread (1, 2, 4,
+    # 8; 0 = 4)
+    unroll: int = 0
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off
     force_cap: float = 0.0
@@ -252,6 +255,7 @@ def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEn
     p.reserved[0] = int(cfg.variant)
     p.reserved[3] = int(cfg.build)
     p.reserved[4] = int(cfg.lanes)
+    p.reserved[1] = int(cfg.unroll)
     p.force_cap = float(cfg.force_cap)
     if cfg.thermostat is not None:
         p.thermostat = 1

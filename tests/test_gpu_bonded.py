@@ -56,7 +56,7 @@ def test_initial_state_vs_golden(name, variant):
 
 
 @pytest.mark.parametrize("name", SYSTEMS)
-@pytest.mark.parametrize("graphs,build", [(True, 0), (False, 0), (True, 3)])
+@pytest.mark.parametrize("graphs,build", [(True, 0), (False, 0), (True, 3), (True, 5)])
 def test_trajectory_vs_golden(name, graphs, build):
     g = load(name)
     eng = engine(g, section_timers=not graphs, build=build)

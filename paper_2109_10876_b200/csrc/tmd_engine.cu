@@ -1624,8 +1624,10 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     validate(sys, lj, fene, params);
     mark("validate");
     build_geom(c, sys->box, lj->r_cut, params->r_skin);  // ConfigError before any CUDA call
+    mark("geometry");
     int ndev = 0;
     ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    mark("device count");
     if (ndev < 1) throw CudaFail{"no CUDA device"};
     if (params->device >= 0) {
       ck(cudaSetDevice(params->device), "cudaSetDevice");
@@ -1640,9 +1642,11 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       throw CudaFail{std::string("device ") + prop.name +
                      " is not sm_100 (this build targets sm_100a only)"};
     }
+    mark("device check");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking),
        "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    mark("streams");
     c->ls = c->stream;
     c->use_graphs = params->reserved[2] == 0;  // reserved[2] = 1 disables CUDA graphs
     ck(cudaEventCreate(&c->t0), "cudaEventCreate");

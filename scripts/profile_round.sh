@@ -21,4 +21,12 @@ if python scripts/prof_force.py 64 > gpurun_out/${TAG}_prof_plain.log 2>&1; then
   ncu --set full --clock-control none --import-source on -k regex:k_forces_l1 -s 30 -c 1 \
       -o gpurun_out/${TAG}_force python scripts/prof_force.py 64 > gpurun_out/${TAG}_ncu_force.log 2>&1
 fi
+# the small-system force kernel (k_forces_lanes, configs[0])
+if python scripts/prof_force.py 20 > gpurun_out/${TAG}_prof_plain20.log 2>&1; then
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      --csv --log-file gpurun_out/${TAG}_launches_eager_32k.csv python scripts/prof_force.py 20 \
+      > gpurun_out/${TAG}_ncu_launches32k.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:k_forces_lanes -s 30 -c 1 \
+      -o gpurun_out/${TAG}_force_lanes python scripts/prof_force.py 20 > gpurun_out/${TAG}_ncu_force_lanes.log 2>&1
+fi
 echo done

@@ -1204,8 +1204,12 @@ void validate(const tmd_system* s, const tmd_lj_params* lj,
   // validate_flat (flat_config.hpp:42-61): unique ids, positive masses
   // unique ids: O(n) with a bitmap when they fill a dense range (the usual
   // 0..n-1), else by sorting
-  const int64_t id_lo = s->n > 0 ? *std::min_element(s->id, s->id + s->n) : 0;
-  const int64_t id_hi = s->n > 0 ? *std::max_element(s->id, s->id + s->n) : -1;
+  int64_t id_lo = 0, id_hi = -1;
+  if (s->n > 0) {
+    const auto mm = std::minmax_element(s->id, s->id + s->n);
+    id_lo = *mm.first;
+    id_hi = *mm.second;
+  }
   const bool dense = static_cast<uint64_t>(id_hi - id_lo) < static_cast<uint64_t>(s->n);
   std::vector<int64_t> ids;
   if (dense) {
@@ -1655,7 +1659,8 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
 
     // Slab mode: keep the particles whose wrapped position lies in this
     // rank's z layers (exact host wrap + cell, bit-identical to the device's).
-    std::vector<int64_t> sel;
+    std::vector<int64_t> sel;  // slab mode: the kept particles (input order)
+    int64_t n_keep = sys->n;
     if (slab) {
       make_slab(c, rank, nranks);
       for (int64_t k = 0; k < sys->n; ++k) {
@@ -1664,9 +1669,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
         cz = std::min(std::max(cz, 0), c->g.dims[2] - 1);
         if (cz >= c->g.z0 && cz < c->g.z0 + c->g.zown) sel.push_back(k);
       }
-    } else {
-      sel.resize(static_cast<size_t>(sys->n));
-      std::iota(sel.begin(), sel.end(), int64_t{0});
+      n_keep = static_cast<int64_t>(sel.size());
     }
     c->my_rank = rank;
     c->nranks = nranks;
@@ -1675,12 +1678,12 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->n_cap = sys->n;
     c->n_total = sys->n;
     if (slab) {
-      c->n_cap = std::min<int64_t>(2 * sys->n, 2 * static_cast<int64_t>(sel.size()) + 65536);
+      c->n_cap = std::min<int64_t>(2 * sys->n, 2 * n_keep + 65536);
       if (c->n_cap > kMaxSlots) {
         throw StatusError{TMD_ERR_CONFIG, "slab too large for one GPU context"};
       }
     }
-    c->n = static_cast<int64_t>(sel.size());
+    c->n = n_keep;
     c->stride = static_cast<int>((c->n_cap + 31) / 32 * 32);
     c->nblk = std::max(1, blocks_for(c->n, kBlock));  // (an empty system keeps a grid)
     c->dt = params->dt;
@@ -1807,7 +1810,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
 
     mark("allocate");
     // upload the kept particles (input order; the first resort sorts by cell)
-    const size_t m = sel.size();
+    const size_t m = static_cast<size_t>(n_keep);
     const double4 far = make_double4(kFarD, kFarD, kFarD, 0.0);
     if (!slab) {
       // the caller's arrays as they are, unpacked on the device (double4

@@ -363,14 +363,30 @@ class Engine:
         return self._n
 
     # -- state access ----------------------------------------------------------
-    def flatten(self) -> FlatConfig:
-        """flatten_domain (domain.hpp:193-207): sorted by id, wrapped."""
+    def flatten(self, out: Optional[FlatConfig] = None) -> FlatConfig:
+        """flatten_domain (domain.hpp:193-207): sorted by id, wrapped.
+
+        out: a FlatConfig whose id/pos/vel arrays (C-contiguous int64 (n,),
+        float64 (n, 3)) receive the state in place, e.g. buffers in pinned
+        host memory reused across downloads; it is returned."""
         n = self._n
-        ids = np.empty(n, np.int64)
-        pos = np.empty((n, 3))
-        vel = np.empty((n, 3))
+        if out is None:
+            ids = np.empty(n, np.int64)
+            pos = np.empty((n, 3))
+            vel = np.empty((n, 3))
+        else:
+            ids, pos, vel = out.id, out.pos, out.vel
+            for a, dt, shape in ((ids, np.int64, (n,)), (pos, np.float64, (n, 3)),
+                                 (vel, np.float64, (n, 3))):
+                if a.dtype != dt or a.shape != shape or not a.flags.c_contiguous \
+                        or not a.flags.writeable:
+                    raise ConfigError("flatten(out=...): id (n,) int64, pos/vel (n, 3) "
+                                      "float64, C-contiguous and writeable")
         _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), None),
                self._h)
+        if out is not None:
+            out.box = self.box.copy()
+            return out
         bonds = None if self._keep.bonds is None else self._keep.bonds.copy()
         return FlatConfig(self.box.copy(), ids, pos, vel, bonds=bonds)
 

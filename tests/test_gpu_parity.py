@@ -284,6 +284,27 @@ def test_non_finite_dynamics_name_the_step():
         eng.run(3)
 
 
+def test_flatten_into_caller_buffers():
+    """flatten(out=...) fills caller-owned (e.g. pinned) arrays in place with
+    exactly what flatten() returns; wrong shapes or dtypes are ConfigError."""
+    f = E.gen_fcc(6, 0.8442, 1.0, 99)
+    eng = E.Engine(f, E.Interactions(), 0.3)
+    eng.run(30)
+    n = f.size()
+    out = E.FlatConfig(f.box, np.zeros(n, np.int64), np.zeros((n, 3)), np.zeros((n, 3)))
+    pos_buf = out.pos
+    got = eng.flatten(out=out)
+    want = eng.flatten()
+    assert got is out and out.pos is pos_buf
+    np.testing.assert_array_equal(out.id, want.id)
+    np.testing.assert_array_equal(out.pos, want.pos)
+    np.testing.assert_array_equal(out.vel, want.vel)
+    bad = E.FlatConfig(f.box, np.zeros(n, np.int64), np.zeros((n + 1, 3)), np.zeros((n, 3)))
+    with pytest.raises(E.ConfigError):
+        eng.flatten(out=bad)
+    eng.close()
+
+
 def test_deterministic_bitwise():
     """acceptance criterion 9 analog: two identical runs are bit-identical."""
     f = E.gen_fcc(8, 0.8442, 1.0, 4242)

@@ -443,9 +443,10 @@ def run_decomposed(args) -> None:
     dist.barrier()
     t0 = time.perf_counter()
     e2 = make()
-    for _ in range(args.steps):
-        e2.run(1)
-        e2.observe()
+    # every step's (step, KE, PE, W) recorded by the device (rank-local sums),
+    # the table reduced over ranks once at the end
+    rows = e2.run_observed(args.steps, stride=1)
+    assert rows.shape[0] == args.steps
     ids, pos, vel, _f = e2.local_state()
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     e2.close()
@@ -469,7 +470,7 @@ def run_decomposed(args) -> None:
         "e2e": {"value": n * args.steps / t_e2e, "unit": UNIT,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "seconds": t_e2e,
-                "what": "DecomposedEngine(create) + K x (run(1) + observe()) + local_state()"},
+                "what": "DecomposedEngine(create, NCCL init) + run_observed(K, stride 1): every step's rank-local (step, KE, PE, W) written by the device into mapped host memory, the table summed over ranks at the end + local_state()"},
         "gpu_launches": launches * ws, "clocks": clocks.summary(),
     }
     print(json.dumps(line))

@@ -288,6 +288,13 @@ int tmd_nccl_unique_id(void* id);
 int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id, int flags);
 int tmd_gpu_slab_setup(tmd_gpu_ctx* ctx);
 int tmd_gpu_slab_run(tmd_gpu_ctx* ctx, int64_t nsteps);
+/* tmd_gpu_slab_run recording every `stride`-th step's observables as the
+ * device computes them (the slab form of tmd_gpu_run_observed): rows hold
+ * this rank's LOCAL kinetic / potential / virial sums (temperature 0); the
+ * caller sums them over ranks (one reduction of the whole table, no per-step
+ * host round trip). */
+int tmd_gpu_slab_run_observed(tmd_gpu_ctx* ctx, int64_t nsteps, int64_t stride,
+                              tmd_observables* rows, int64_t cap, int64_t* n_rows);
 int tmd_gpu_slab_observe(tmd_gpu_ctx* ctx, int64_t n_total, tmd_observables* out);
 
 /* Load-aware cuts: owned particles per global z layer

@@ -28,7 +28,7 @@ EXPORTS = [
     "tmd_gpu_stream", "tmd_gpu_destroy", "tmd_gen_fcc",
     "tmd_thermal_velocities", "tmd_counter_uniform3", "tmd_counter_normal3",
     "tmd_gpu_abi_version", "tmd_gpu_launch_count", "tmd_gpu_fp64_peak",
-    "tmd_gpu_kernel_config",
+    "tmd_gpu_kernel_config", "tmd_gpu_slab_run_observed",
     "tmd_gpu_time_list_build",
     "tmd_gpu_create_slab", "tmd_gpu_slab_info", "tmd_gpu_slab_max_d2",
     "tmd_gpu_slab_decide", "tmd_gpu_slab_migrate_out", "tmd_gpu_slab_migrate_in",
@@ -128,6 +128,9 @@ def lib() -> C.CDLL:
     L.tmd_gpu_slab_setup.argtypes = [P]
     L.tmd_gpu_slab_run.argtypes = [P, C.c_int64]
     L.tmd_gpu_slab_observe.argtypes = [P, C.c_int64, C.POINTER(TmdObservables)]
+    L.tmd_gpu_slab_run_observed.argtypes = [P, C.c_int64, C.c_int64,
+                                            C.POINTER(TmdObservables), C.c_int64,
+                                            C.POINTER(C.c_int64)]
     L.tmd_gpu_slab_recut.argtypes = [P, P]
     L.tmd_gpu_last_error.argtypes = [P]
     L.tmd_gpu_last_error.restype = C.c_char_p

@@ -834,6 +834,7 @@ __global__ void __launch_bounds__(kRedThreads)
     k_obs_record(const double* __restrict__ part_e, const double* __restrict__ part_w,
                  int npe, const double* __restrict__ part_ke, int nke, Ctrl* ctrl, int stride,
                  double* __restrict__ rows, int max_rows) {
+  if (ctrl->halt) return;  // native slab loop: a halted (replayed) step records nothing
   __shared__ double red[kRedThreads / 32];
   double se = 0.0, sw = 0.0, sk = 0.0;
   for (int k = threadIdx.x; k < npe; k += kRedThreads) {

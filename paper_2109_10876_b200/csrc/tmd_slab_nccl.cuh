@@ -393,14 +393,32 @@ int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
 // runs the rebuild protocol and that step's forces, then continues. Every
 // rank takes the same decisions (the word is all-reduced), so all halt at the
 // same step.
-int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
-  return guard(c, [&] {
+namespace {
+
+#ifndef TMD_NO_NCCL
+// Rows the device recorded since the last collection (run_observed), then
+// the device counter is reset on the stream. Call right after a sync_ctrl.
+void collect_slab_obs(tmd_gpu_ctx* c) {
+  if (c->obs_stride <= 0) return;
+  const int rows = std::min(c->h_ctrl->obs_rows, kObsRows);
+  for (int r = 0; r < rows; ++r) {
+    const double* o = c->obs_host + 4 * r;
+    c->obs_rows.push_back({o[0], o[1], o[2], o[3]});
+  }
+  ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
+}
+#endif
+
+void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
     need_slab(c);
     need_nccl(c);
     if (nsteps < 0) throw StatusError{TMD_ERR_CONFIG, "step count must be non-negative"};
 #ifndef TMD_NO_NCCL
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (nsteps == 0) return;
+    if (c->obs_stride > 0) {
+      ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
+    }
     ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
     const int64_t start = c->step, target = c->step + nsteps;
     if (c->n > 0) launch_kick_drift(c);
@@ -418,6 +436,7 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
         c->launches += 1;
         const bool fh = fused(c);  // the force epilogue delivers the halo itself
         launch_forces(c, last ? kKick2 : kFused);
+        launch_obs_record(c);
         if (!last) {
           ++fused_launches;
           if (!fh) nccl_halo(c);
@@ -425,6 +444,7 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
       }
       sync_ctrl(c);
       raise_physics(c, true);
+      collect_slab_obs(c);
       if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
       const int64_t advanced = c->h_ctrl->step - done_step;  // steps that ran
       if (!c->h_ctrl->halt) {
@@ -446,18 +466,65 @@ int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
       const bool last = done_step + 1 == target;
       const bool fh = fused(c);
       launch_forces(c, last ? kKick2 : kFused);
+      launch_obs_record(c);
       if (!last && !fh) nccl_halo(c);
       done_step += 1;
     }
     ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
     sync_ctrl(c);
     raise_physics(c, true);
+    collect_slab_obs(c);
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, c->t0, c->t1), "cudaEventElapsedTime");
     c->elapsed += 1e-3 * ms;
     c->step = c->h_ctrl->step;
     c->rebuilds = static_cast<uint64_t>(c->h_ctrl->rebuilds);
 #endif
+}
+
+}  // namespace
+
+int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
+  return guard(c, [&] { slab_run_impl(c, nsteps); });
+}
+
+int tmd_gpu_slab_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride,
+                              tmd_observables* out, int64_t cap, int64_t* n_out) {
+  return guard(c, [&] {
+    if (stride < 1) throw StatusError{TMD_ERR_CONFIG, "observable stride must be at least 1"};
+    if (!n_out || (cap > 0 && !out)) throw StatusError{TMD_ERR_CONFIG, "row buffer missing"};
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (!c->obs_host) {
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&c->obs_host), sizeof(double) * 4 * kObsRows,
+                       cudaHostAllocMapped),
+         "cudaHostAlloc(mapped)");
+      ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->obs_dev), c->obs_host, 0),
+         "cudaHostGetDevicePointer");
+    }
+    const int64_t s0 = c->step;
+    c->obs_rows.clear();
+    c->obs_stride = static_cast<int>(std::min<int64_t>(stride, 1 << 30));
+    try {
+      slab_run_impl(c, nsteps);
+    } catch (...) {
+      c->obs_stride = 0;
+      throw;
+    }
+    c->obs_stride = 0;
+    int64_t k = 0;
+    for (const auto& r : c->obs_rows) {
+      const int64_t st = static_cast<int64_t>(r[0]);
+      if (st <= s0 || st > s0 + nsteps) continue;
+      if (k < cap) {
+        out[k].step = st;
+        out[k].kinetic = r[1];
+        out[k].potential = r[2];
+        out[k].virial = r[3];
+        out[k].temperature = 0.0;  // rank-local sums: the caller reduces over ranks
+      }
+      ++k;
+    }
+    *n_out = k;
   });
 }
 

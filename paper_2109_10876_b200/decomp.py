@@ -46,7 +46,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _abi
-from .engine import (ConfigError, EngineConfig, FlatConfig, Interactions, StepObservables,
+from .engine import (ConfigError, EngineConfig, FlatConfig, Interactions, StateError,
+                     StepObservables,
                      _check, _engine_params, _interactions, _ptr, _system,
                      validate_engine_config)
 
@@ -298,6 +299,20 @@ class SlabContext:
 
     def run_native(self, steps: int) -> None:
         self._c(_abi.lib().tmd_gpu_slab_run(self._h, int(steps)))
+
+    def run_observed_native(self, steps: int, stride: int) -> np.ndarray:
+        """run_native(steps) recording every stride-th step's rank-local
+        (step, kinetic, potential, virial) sums on the device."""
+        cap = int(steps) // max(int(stride), 1) + 1
+        rows = (_abi.TmdObservables * cap)()
+        n = C.c_int64()
+        self._c(_abi.lib().tmd_gpu_slab_run_observed(self._h, int(steps), int(stride), rows,
+                                                     cap, C.byref(n)))
+        out = np.empty((min(n.value, cap), 4))
+        for k in range(out.shape[0]):
+            r = rows[k]
+            out[k] = (r.step, r.kinetic, r.potential, r.virial)
+        return out
 
     def observe_native(self, n_total: int) -> StepObservables:
         o = _abi.TmdObservables()
@@ -653,6 +668,41 @@ class DecomposedEngine:
 
     def step(self) -> None:
         self.run(1)
+
+    def run_observed(self, steps: int, stride: int = 1) -> np.ndarray:
+        """run(steps) recording (step, kinetic, potential, temperature, virial)
+        of every stride-th step, summed over ranks (Engine.run_observed's rows).
+        The native loop records rank-local sums on the device as the steps
+        run and reduces the whole table once at the end; the Python protocol
+        observes after each recorded step."""
+        steps, stride = int(steps), int(stride)
+        if stride < 1:
+            raise ConfigError("observable stride must be at least 1")
+        if self.native:
+            (r, c), = self.ctx.items()
+            s0 = self.steps
+            local = c.run_observed_native(steps, stride)
+            self.steps += steps
+            self.rebuilds = c.rebuild_count()
+            self.recuts = c.info()["recuts"]
+            want = np.arange(s0 + stride - s0 % stride, s0 + steps + 1, stride)
+            if local.shape[0] != want.size or not np.array_equal(local[:, 0], want):
+                raise StateError("native loop recorded an unexpected set of steps")
+            tot = self.comm.allreduce_sum({r: local[:, 1:4].ravel()}).reshape(-1, 3)
+            ke, pe, w = tot[:, 0], tot[:, 1], tot[:, 2]
+            return np.column_stack([want.astype(np.float64), ke, pe,
+                                    2.0 * ke / (3.0 * self.n_total), w])
+        rows = []
+        done = 0
+        while done < steps:
+            k = stride - (self.steps % stride)
+            k = min(k, steps - done)
+            self.run(k)
+            done += k
+            if self.steps % stride == 0:
+                o = self.observe()
+                rows.append((o.step, o.kinetic, o.potential, o.temperature, o.virial))
+        return np.array(rows, dtype=np.float64).reshape(-1, 5)
 
     def observe(self) -> StepObservables:
         if self.native:

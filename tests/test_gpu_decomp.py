@@ -228,6 +228,38 @@ def test_native_nccl_loop_in_process(name, halo):
         eng.close()
 
 
+@pytest.mark.parametrize("native", [True, False])
+def test_decomposed_run_observed_rows(native):
+    """run_observed on the decomposed engine (the native loop records rows
+    on the device, across speculative batches and the rebuilds that halt
+    them): each recorded row equals observe() after running to that step."""
+    g = load("fcc8_jit")
+    flat = E.FlatConfig(g["box"], g["ids"], g["pos"], g["vel"])
+    cfg = E.EngineConfig(dt=float(g["dt"]))
+    a = DecomposedEngine(flat, E.Interactions(), float(g["r_skin"]), cfg,
+                         comm=InProcessComm(1), native=native)
+    b = DecomposedEngine(flat, E.Interactions(), float(g["r_skin"]), cfg,
+                         comm=InProcessComm(1), native=native)
+    try:
+        rows = a.run_observed(40, stride=3)
+        rows = np.vstack([rows, a.run_observed(7, stride=3)])
+        assert rows[:, 0].tolist() == list(range(3, 48, 3))
+        assert a.rebuild_count() > 0
+        done = 0
+        for r in rows:
+            b.run(int(r[0]) - done)
+            done = int(r[0])
+            o = b.observe()
+            assert o.step == int(r[0])
+            assert_rel(r[1], o.kinetic, 1e-12, f"KE at {done}")
+            assert_rel(r[2], o.potential, 1e-12, f"PE at {done}")
+            assert_rel(r[4], o.virial, 1e-12, f"W at {done}")
+            assert_rel(r[3], o.temperature, 1e-12, f"T at {done}")
+    finally:
+        a.close()
+        b.close()
+
+
 @pytest.mark.parametrize("native", [False, True])
 def test_nccl_one_rank_decomposition(native):
     """The NCCL transport itself (torchrun, one process): the single slab

@@ -98,6 +98,8 @@ struct Ctrl {
   double err_val;             // a value for the first error's message (bond r^2)
   int obs_rows;               // observable rows recorded in this chunk (run_observed)
   int halt;                   // native slab loop: a rebuild is due, later steps are no-ops
+  double seen_d2;             // native slab loop: the global max |x - x_snap|^2 the last
+                              // decision saw (the host sizes its next batch from it)
 };
 
 // ---------------------------------------------------------------------------

@@ -270,6 +270,11 @@ struct tmd_gpu_ctx {
   int2* exp = nullptr;           // [n_cap] export map (slab mode)
   double4* rg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][parity]
   std::vector<std::pair<std::array<char, 64>, void*>> ipc_open;  // opened peer buffers
+  int ipc_gen = 0;               // bumped whenever the position buffers are reallocated
+  int64_t last_rebuild_step = -1;  // native loop: step of the last rebuild (batch sizing)
+  int64_t rebuild_gap = 0;         // native loop: steps between the last two rebuilds
+  std::vector<int> peer_gen;     // every rank's ipc_gen at the last full address exchange
+  double4* peer_base[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [lo|hi][parity]
   std::vector<int> cuts;         // current cut planes (native loop)
   int64_t recuts = 0;
   int64_t* nccl_i64 = nullptr;   // staging for all-gathered counts
@@ -1475,6 +1480,7 @@ void grow_capacity(tmd_gpu_ctx* c, int64_t need) {
   };
   for (int b = 0; b < 2; ++b) regrow(c->posb[b], 1);
   c->pos = c->posb[c->cur];
+  c->ipc_gen += 1;  // peers holding these buffers must re-map them
   regrow(c->pos2, 0); regrow(c->snap, 0);
   regrow(c->vx, 0); regrow(c->vy, 0); regrow(c->vz, 0);
   regrow(c->vx2, 0); regrow(c->vy2, 0); regrow(c->vz2, 0);
@@ -2397,6 +2403,52 @@ void ensure_groups(tmd_gpu_ctx* c) {
   }
 }
 
+
+// Commit of a migration, device side (no host round trip): arrivals
+// unpacked, the normal resort, then the lowest and highest owned layers
+// exported (per-cell counts, their scan, ids and positions, slots). The
+// border sizes are left on the device at boff[s] + dxy.
+void slab_commit_launch(tmd_gpu_ctx* c) {
+  if (c->mig_nrecv > 0) {
+    c->launches += 1;
+    k_mig_unpack<<<blocks_for(c->mig_nrecv, kBlock), kBlock, 0, c->ls>>>(
+        static_cast<int>(c->mig_nrecv), c->mig_recv, static_cast<int>(c->n), c->pos, c->vx,
+        c->vy, c->vz, c->mass, c->id);
+  }
+  c->n += c->mig_nrecv;
+  c->mig_nrecv = 0;
+  c->nblk = std::max(1, blocks_for(c->n, kBlock));
+  ensure_groups(c);
+  launch_resort(c);  // requires the rebuild decision (decide(rebuild=1))
+  const int dxy = c->g.dims[0] * c->g.dims[1];
+  const int qb = blocks_for(dxy, kBlock);
+  for (int s = 0; s < 2; ++s) {
+    const int lz = s == 0 ? 1 : c->g.zown;  // lowest / highest owned layer
+    c->launches += 3;
+    k_layer_counts<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->count);
+    launch_scan(c, dxy, c->count, c->boff[s]);  // leaves count zeroed
+    k_layer_counts<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->bcnt[s]);
+    k_layer_gather<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->boff[s],
+                                             c->pos, c->id, c->bidx[s], c->bids[s],
+                                             c->bpos[s]);
+  }
+  c->fused_ready = false;  // the layout changed: remote ghost addresses are re-derived
+}
+
+// The border sizes on the host: the fused halo's export map (slot -> index
+// in each side's export).
+void slab_commit_finish(tmd_gpu_ctx* c, int64_t nb0, int64_t nb1) {
+  c->nb[0] = nb0;
+  c->nb[1] = nb1;
+  c->launches += 3;
+  k_fill_int2<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->exp, make_int2(-1, -1));
+  for (int s = 0; s < 2; ++s) {
+    if (c->nb[s] == 0) continue;
+    k_export_map<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
+        static_cast<int>(c->nb[s]), c->bidx[s], s, c->exp);
+  }
+}
+
 }  // namespace
 
 int tmd_gpu_slab_info(tmd_gpu_ctx* c, int64_t info[11]) {
@@ -2553,30 +2605,8 @@ int tmd_gpu_slab_commit(tmd_gpu_ctx* c, int64_t nb_out[2]) {
   return guard(c, [&] {
     need_slab(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    if (c->mig_nrecv > 0) {
-      c->launches += 1;
-      k_mig_unpack<<<blocks_for(c->mig_nrecv, kBlock), kBlock, 0, c->ls>>>(
-          static_cast<int>(c->mig_nrecv), c->mig_recv, static_cast<int>(c->n), c->pos, c->vx,
-          c->vy, c->vz, c->mass, c->id);
-    }
-    c->n += c->mig_nrecv;
-    c->mig_nrecv = 0;
-    c->nblk = std::max(1, blocks_for(c->n, kBlock));
-    ensure_groups(c);
-    launch_resort(c);  // requires the rebuild decision (decide(rebuild=1))
+    slab_commit_launch(c);
     const int dxy = c->g.dims[0] * c->g.dims[1];
-    const int qb = blocks_for(dxy, kBlock);
-    for (int s = 0; s < 2; ++s) {
-      const int lz = s == 0 ? 1 : c->g.zown;  // lowest / highest owned layer
-      c->launches += 3;
-      k_layer_counts<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->count);
-      launch_scan(c, dxy, c->count, c->boff[s]);  // leaves count zeroed
-      k_layer_counts<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->bcnt[s]);
-      k_layer_gather<<<qb, kBlock, 0, c->ls>>>(lz, c->g, c->cell_rank, c->start, c->boff[s],
-                                               c->pos, c->id, c->bidx[s], c->bids[s],
-                                               c->bpos[s]);
-    }
-    c->fused_ready = false;  // the layout changed: remote ghost addresses are re-exchanged
     int tot[2] = {0, 0};
     for (int s = 0; s < 2; ++s) {
       ck(cudaMemcpyAsync(&tot[s], c->boff[s] + dxy, sizeof(int), cudaMemcpyDeviceToHost,
@@ -2585,18 +2615,9 @@ int tmd_gpu_slab_commit(tmd_gpu_ctx* c, int64_t nb_out[2]) {
     sync_ctrl(c);
     raise_physics(c, true);
     if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
-    for (int s = 0; s < 2; ++s) {
-      c->nb[s] = tot[s];
-      nb_out[s] = tot[s];
-    }
-    // export map of the fused halo (slot -> index in each side's export)
-    c->launches += 3;
-    k_fill_int2<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->exp, make_int2(-1, -1));
-    for (int s = 0; s < 2; ++s) {
-      if (c->nb[s] == 0) continue;
-      k_export_map<<<blocks_for(c->nb[s], kBlock), kBlock, 0, c->ls>>>(
-          static_cast<int>(c->nb[s]), c->bidx[s], s, c->exp);
-    }
+    slab_commit_finish(c, tot[0], tot[1]);
+    nb_out[0] = tot[0];
+    nb_out[1] = tot[1];
   });
 }
 

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void k_decide_spec(Ctrl* ctrl, double thr) {
   if (ctrl->halt) return;
   const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
+  ctrl->seen_d2 = m;
   if (m > thr) {
     ctrl->halt = 1;
     return;
@@ -216,6 +217,30 @@ __global__ void k_decide_spec(Ctrl* ctrl, double thr) {
   ctrl->rebuild = 0;
   ctrl->max_d2 = 0ull;
   ctrl->step += 1;
+}
+
+// Native rebuild (tmd_slab_nccl.cuh): this rank's leaver offsets from the
+// all-gathered count matrix M[s][d], on the device (no host staging).
+__global__ void k_mig_offsets(const int* __restrict__ M, int r, int R, int* __restrict__ off) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int acc = 0;
+  off[0] = 0;
+  for (int d = 0; d < R; ++d) {
+    acc += M[r * R + d];
+    off[d + 1] = acc;
+  }
+}
+
+// Native rebuild: this rank's all-gathered row {border sizes, owned count,
+// slot capacity, buffer generation}.
+__global__ void k_slab_row(int* __restrict__ row, const int* __restrict__ nb0,
+                           const int* __restrict__ nb1, int n, int ncap, int gen) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  row[0] = *nb0;
+  row[1] = *nb1;
+  row[2] = n;
+  row[3] = ncap;
+  row[4] = gen;
 }
 
 }  // namespace tmd

@@ -174,6 +174,7 @@ struct PeerInfo {
   unsigned long long base[2];
   long long pid;
   long long ghost_lo_off, ghost_hi_off;
+  long long gen;  // the rank's ipc_gen (buffer reallocations so far)
 };
 
 double4* peer_buffer(tmd_gpu_ctx* c, const PeerInfo& p, int peer, int b) {
@@ -203,6 +204,7 @@ void nccl_publish_ghosts(tmd_gpu_ctx* c) {
   me.pid = static_cast<long long>(getpid());
   me.ghost_lo_off = c->n;
   me.ghost_hi_off = c->n + c->n_ghost_lo;
+  me.gen = c->ipc_gen;
   const size_t sz = sizeof(PeerInfo);
   char* d = dalloc<char>(sz * (static_cast<size_t>(R) + 1));
   ck(cudaMemcpyAsync(d, &me, sz, cudaMemcpyHostToDevice, c->stream), "H2D peer info");
@@ -215,76 +217,137 @@ void nccl_publish_ghosts(tmd_gpu_ctx* c) {
   const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
   for (int b = 0; b < 2; ++b) {
     // my lowest layer -> lo's upper ghost; my highest layer -> hi's lower ghost
-    c->rg[0][b] = peer_buffer(c, all[static_cast<size_t>(lo)], lo, b) +
-                  all[static_cast<size_t>(lo)].ghost_hi_off;
-    c->rg[1][b] = peer_buffer(c, all[static_cast<size_t>(hi)], hi, b) +
-                  all[static_cast<size_t>(hi)].ghost_lo_off;
+    c->peer_base[0][b] = peer_buffer(c, all[static_cast<size_t>(lo)], lo, b);
+    c->peer_base[1][b] = peer_buffer(c, all[static_cast<size_t>(hi)], hi, b);
+    c->rg[0][b] = c->peer_base[0][b] + all[static_cast<size_t>(lo)].ghost_hi_off;
+    c->rg[1][b] = c->peer_base[1][b] + all[static_cast<size_t>(hi)].ghost_lo_off;
   }
+  c->peer_gen.assign(static_cast<size_t>(R), 0);
+  for (int q = 0; q < R; ++q) c->peer_gen[static_cast<size_t>(q)] = static_cast<int>(all[static_cast<size_t>(q)].gen);
   c->fused_ready = true;
 }
 
-// The rebuild protocol (decomp.py DecomposedEngine._rebuild) over NCCL.
+// The rebuild protocol (decomp.py DecomposedEngine._rebuild) over NCCL, with
+// three host round trips: (1) the leaver counts, all-gathered straight from
+// the device; (2) after the on-device commit, one all-gathered row per rank
+// {border sizes, owned count, slot capacity, buffer generation}, from which
+// every rank derives every other rank's ghost counts and ghost offsets;
+// (3) the list build's overflow check. The fused halo's peer addresses are
+// re-exchanged (IPC handles, a fourth round trip) only when some rank's
+// position buffers were or are about to be reallocated; otherwise they are
+// the cached peer bases plus the derived ghost offsets.
+constexpr int kRowInts = 5;  // nb0, nb1, n_own, n_cap, ipc_gen
 void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   const int R = c->nranks, r = c->my_rank;
+  const size_t uR = static_cast<size_t>(R);
   rck(c, tmd_gpu_slab_decide(c, 1, advance ? 1 : 0));
   if (c->balance_count) nccl_rebalance(c);
-  // 1. migration: counts all-gathered, records point to point
-  std::vector<int64_t> counts(static_cast<size_t>(R));
-  void* send = nullptr;
-  rck(c, tmd_gpu_slab_migrate_out(c, counts.data(), &send));
-  std::vector<int64_t> M(static_cast<size_t>(R) * R);
-  ck(cudaMemcpyAsync(c->nccl_i64, counts.data(), sizeof(int64_t) * R, cudaMemcpyHostToDevice,
-                     c->stream), "H2D counts");
-  nck(ncclAllGather(c->nccl_i64, c->nccl_i64 + R, R, ncclInt64, cm(c), c->stream),
-      "ncclAllGather");
-  ck(cudaMemcpyAsync(M.data(), c->nccl_i64 + R, sizeof(int64_t) * R * R,
-                     cudaMemcpyDeviceToHost, c->stream), "D2H counts");
-  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  // 1. classify; the leaver-count matrix M[s][d] all-gathered from the device
+  const int n = static_cast<int>(c->n);
+  ck(cudaMemsetAsync(c->mig_count, 0, 2 * sizeof(int) * uR, c->stream), "memset");
+  ck(cudaMemsetAsync(c->mig_keep, 0, sizeof(int), c->stream), "memset");
+  c->launches += 1;
+  if (n > 0) {
+    k_mig_classify<<<c->nblk, kBlock, 0, c->ls>>>(n, c->pos, c->id, c->owner_of_z, c->my_rank,
+                                                  c->g, c->mig_dest, c->mig_count, c->ctrl);
+  }
+  int* Md = reinterpret_cast<int*>(c->nccl_i64);  // R*R ints (the buffer holds 2R^2 + 2R + 16)
+  nck(ncclAllGather(c->mig_count, Md, uR, ncclInt32, cm(c), c->stream), "ncclAllGather(M)");
+  std::vector<int> M(uR * uR);
+  ck(cudaMemcpyAsync(M.data(), Md, sizeof(int) * uR * uR, cudaMemcpyDeviceToHost, c->stream),
+     "D2H counts");
+  sync_ctrl(c);
+  raise_physics(c, true);
+  // 2. stayers compacted, leavers packed by destination, records point to point
+  std::vector<int> off(uR + 1, 0);
+  for (int d = 0; d < R; ++d) off[static_cast<size_t>(d) + 1] = off[static_cast<size_t>(d)] + M[static_cast<size_t>(r) * uR + d];
+  c->launches += 1;
+  k_mig_offsets<<<1, 1, 0, c->ls>>>(Md, r, R, c->mig_off);
+  if (n > 0) {
+    c->launches += 1;
+    k_mig_pack<<<c->nblk, kBlock, 0, c->ls>>>(
+        n, c->pos, c->vx, c->vy, c->vz, c->mass, c->id, c->mig_dest, c->my_rank, c->mig_off,
+        c->mig_count + R, c->mig_send, c->mig_keep, c->pos2, c->vx2, c->vy2, c->vz2, c->mass2,
+        c->id2);
+  }
+  const size_t keep = static_cast<size_t>(n - off[uR]);
+  auto cp = [&](void* d, const void* src, size_t bytes) {
+    if (bytes) ck(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDeviceToDevice, c->stream), "copy");
+  };
+  cp(c->pos, c->pos2, keep * sizeof(double4));
+  cp(c->vx, c->vx2, keep * sizeof(double));
+  cp(c->vy, c->vy2, keep * sizeof(double));
+  cp(c->vz, c->vz2, keep * sizeof(double));
+  cp(c->mass, c->mass2, keep * sizeof(double));
+  cp(c->id, c->id2, keep * sizeof(long long));
+  c->n = static_cast<int64_t>(keep);
+  c->n_ghost = c->n_ghost_lo = c->n_ghost_hi = 0;
   int64_t nrecv = 0;
-  for (int s = 0; s < R; ++s) nrecv += M[static_cast<size_t>(s) * R + r];
-  void* recv = nullptr;
-  rck(c, tmd_gpu_slab_migrate_in(c, nrecv, &recv));
+  for (int q = 0; q < R; ++q) nrecv += M[static_cast<size_t>(q) * uR + r];
+  grow_capacity(c, c->n + nrecv);  // (synchronises and bumps ipc_gen only when it grows)
+  c->mig_nrecv = nrecv;
   const size_t rec = sizeof(MigRec);
   nck(ncclGroupStart(), "ncclGroupStart");
-  int64_t off = 0;
   for (int d = 0; d < R; ++d) {
-    if (counts[static_cast<size_t>(d)]) {
-      nck(ncclSend(static_cast<char*>(send) + off * rec, counts[static_cast<size_t>(d)] * rec,
-                   ncclUint8, d, cm(c), c->stream), "ncclSend");
+    const int m = M[static_cast<size_t>(r) * uR + d];
+    if (m) {
+      nck(ncclSend(reinterpret_cast<char*>(c->mig_send) + static_cast<size_t>(off[static_cast<size_t>(d)]) * rec,
+                   static_cast<size_t>(m) * rec, ncclUint8, d, cm(c), c->stream), "ncclSend");
     }
-    off += counts[static_cast<size_t>(d)];
   }
   int64_t roff = 0;
-  for (int s = 0; s < R; ++s) {
-    const int64_t m = M[static_cast<size_t>(s) * R + r];
+  for (int q = 0; q < R; ++q) {
+    const int m = M[static_cast<size_t>(q) * uR + r];
     if (m) {
-      nck(ncclRecv(static_cast<char*>(recv) + roff * rec, m * rec, ncclUint8, s, cm(c),
-                   c->stream), "ncclRecv");
+      nck(ncclRecv(reinterpret_cast<char*>(c->mig_recv) + roff * rec, static_cast<size_t>(m) * rec,
+                   ncclUint8, q, cm(c), c->stream), "ncclRecv");
     }
     roff += m;
   }
   nck(ncclGroupEnd(), "ncclGroupEnd");
-  // 2. resort + boundary layers; their sizes all-gathered
-  int64_t nb[2] = {0, 0};
-  rck(c, tmd_gpu_slab_commit(c, nb));
-  std::vector<int64_t> NB(2 * static_cast<size_t>(R));
-  ck(cudaMemcpyAsync(c->nccl_i64, nb, sizeof nb, cudaMemcpyHostToDevice, c->stream), "H2D nb");
-  nck(ncclAllGather(c->nccl_i64, c->nccl_i64 + 2, 2, ncclInt64, cm(c), c->stream),
-      "ncclAllGather");
-  ck(cudaMemcpyAsync(NB.data(), c->nccl_i64 + 2, sizeof(int64_t) * 2 * R,
-                     cudaMemcpyDeviceToHost, c->stream), "D2H nb");
-  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  // 3. commit on the device; one row per rank all-gathered
+  slab_commit_launch(c);
+  const int dxy = c->g.dims[0] * c->g.dims[1];
+  int* row = Md;                 // this rank's row
+  int* table = Md + 8;           // R rows
+  c->launches += 1;
+  k_slab_row<<<1, 1, 0, c->ls>>>(row, c->boff[0] + dxy, c->boff[1] + dxy, static_cast<int>(c->n),
+                                 static_cast<int>(c->n_cap), c->ipc_gen);
+  nck(ncclAllGather(row, table, kRowInts, ncclInt32, cm(c), c->stream), "ncclAllGather(rows)");
+  std::vector<int> T(uR * kRowInts);
+  ck(cudaMemcpyAsync(T.data(), table, sizeof(int) * T.size(), cudaMemcpyDeviceToHost, c->stream),
+     "D2H rows");
+  sync_ctrl(c);
+  raise_physics(c, true);
+  if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
+  auto at = [&](int q, int k) { return T[static_cast<size_t>((q + R) % R) * kRowInts + k]; };
+  slab_commit_finish(c, at(r, 0), at(r, 1));
+  // 4. ghost layers (counts, ids, positions) from the neighbours, then the list
   const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
   void* gl[3];
   void* gh[3];
-  rck(c, tmd_gpu_slab_ghost_in(c, NB[2 * static_cast<size_t>(lo) + 1],
-                               NB[2 * static_cast<size_t>(hi)], gl, gh));
-  // 3. ghost layers (counts, ids, positions), then cell ranges + list build
+  rck(c, tmd_gpu_slab_ghost_in(c, at(lo, 1), at(hi, 0), gl, gh));
   nccl_ghost_exchange(c, false);
   rck(c, tmd_gpu_slab_ghosts_ready(c));
-  if (c->fused_halo) nccl_publish_ghosts(c);
+  if (!c->fused_halo) return;
+  // 5. peer addresses of the fused halo: q's lower ghost layer starts at its
+  // owned count, its upper one after the lower (= its lower neighbour's top
+  // border)
+  bool remap = c->peer_gen.size() != uR;
+  for (int q = 0; q < R && !remap; ++q) {
+    const int64_t need = static_cast<int64_t>(at(q, 2)) + at(q - 1, 1) + at(q + 1, 0);
+    remap = need > at(q, 3) || at(q, 4) != c->peer_gen[static_cast<size_t>(q)];
+  }
+  if (remap) {
+    nccl_publish_ghosts(c);
+    return;
+  }
+  for (int b = 0; b < 2; ++b) {
+    c->rg[0][b] = c->peer_base[0][b] + (static_cast<int64_t>(at(lo, 2)) + at(lo - 1, 1));
+    c->rg[1][b] = c->peer_base[1][b] + at(hi, 2);
+  }
+  c->fused_ready = true;
 }
-
 bool fused(const tmd_gpu_ctx* c) { return c->fused_halo && c->fused_ready; }
 
 void nccl_halo(tmd_gpu_ctx* c) {
@@ -297,7 +360,25 @@ void nccl_halo(tmd_gpu_ctx* c) {
   nccl_ghost_exchange(c, true);
 }
 
-constexpr int kSpecSteps = 16;  // steps enqueued per host round trip
+constexpr int kSpecSteps = 16;  // steps enqueued per host round trip (at most)
+// Steps of the next speculative batch, aimed to end at the step whose
+// decision triggers the next rebuild (the batch's later steps would be
+// no-ops, each still paying its all-reduce). Right after a rebuild: the last
+// interval between rebuilds; later: the global displacement the last decision
+// saw, extrapolated ballistically (|x - x_snap| ~ t). Every rank computes the
+// same value from all-reduced inputs, so the collectives stay matched.
+int64_t spec_batch(const tmd_gpu_ctx* c, int64_t done_step) {
+  if (c->last_rebuild_step < 0) return kSpecSteps;
+  const int64_t t = done_step - c->last_rebuild_step;  // drifts since the list build
+  const double m = c->h_ctrl->seen_d2, thr = c->g.rebuild_thr;
+  double k;
+  if (t <= 0 || !(m > 0.0)) {  // just rebuilt: expect the last interval again
+    k = c->rebuild_gap > 0 ? static_cast<double>(c->rebuild_gap) : kSpecSteps;
+  } else {  // the decision of step done_step saw m after t drifts
+    k = std::ceil(static_cast<double>(t) * std::sqrt(thr / m)) - static_cast<double>(t);
+  }
+  return std::max<int64_t>(1, std::min<int64_t>(kSpecSteps, static_cast<int64_t>(k)));
+}
 
 // Global max displacement^2 of this step (in place on the device word that
 // k_decide reads), brought to the host for the rebuild decision.
@@ -377,6 +458,7 @@ int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
 #ifndef TMD_NO_NCCL
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     nccl_rebuild(c, false);
+    c->last_rebuild_step = c->step;
     rck(c, tmd_gpu_slab_forces(c, 0));
     sync_ctrl(c);
     raise_physics(c, false);
@@ -424,8 +506,9 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
     if (c->n > 0) launch_kick_drift(c);
     nccl_halo(c);
     int64_t done_step = start;  // steps completed (host view)
+    int64_t K_next = kSpecSteps;
     while (done_step < target) {
-      const int64_t K = std::min<int64_t>(kSpecSteps, target - done_step);
+      const int64_t K = std::min<int64_t>(K_next, target - done_step);
       int64_t fused_launches = 0;
       for (int64_t s = 0; s < K; ++s) {
         nck(ncclAllReduce(&c->ctrl->max_d2, &c->ctrl->max_d2, 1, ncclUint64, ncclMax, cm(c),
@@ -449,6 +532,7 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
       const int64_t advanced = c->h_ctrl->step - done_step;  // steps that ran
       if (!c->h_ctrl->halt) {
         done_step += K;
+        K_next = spec_batch(c, done_step);
         continue;
       }
       // the launches from the halted step on were no-ops: undo their buffer
@@ -469,6 +553,9 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
       launch_obs_record(c);
       if (!last && !fh) nccl_halo(c);
       done_step += 1;
+      if (c->last_rebuild_step >= 0) c->rebuild_gap = done_step - c->last_rebuild_step;
+      c->last_rebuild_step = done_step;
+      K_next = spec_batch(c, done_step);
     }
     ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
     sync_ctrl(c);

@@ -134,12 +134,33 @@ class Workload:
     """One BASELINE.json configuration: the synthetic system, its interactions
     and integrator settings, and the reference-engine kwargs for the CPU arm."""
 
-    def __init__(self, kind: str, cells: int):
+    def __init__(self, kind: str, cells: int, weak_ranks: int = 0):
         from paper_2109_10876_b200 import engine as E
         self.kind = kind
         self.setup_s = 0.0
         t0 = time.perf_counter()
-        if kind == "lj":
+        if kind == "lj" and weak_ranks > 0:
+            # configs[4] weak scaling: FCC 80^3 x 4 = 2.048M particles per GPU, the
+            # box doubled along x, then y, then z (8 GPUs: the 160^3 configs[4] box)
+            dims = [80, 80, 80]
+            k = 0
+            r = weak_ranks
+            while r > 1:
+                if r % 2:
+                    raise SystemExit("--weak needs a power-of-two GPU count")
+                dims[k % 3] *= 2
+                k += 1
+                r //= 2
+            self.flat = E.gen_fcc_box(*dims, 0.8442, 1.0, 12345)
+            self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
+            self.cfg = {"workload": "LJ fluid, weak scaling at 2.048M particles per GPU "
+                                    "(BASELINE.json configs[4])",
+                        "fcc_cells": dims, "n_particles": self.flat.size(),
+                        "n_per_gpu": self.flat.size() // weak_ranks, "rho": 0.8442,
+                        "r_cut": 2.5, "energy_shifted": True, "r_skin": 0.3,
+                        "temperature": 1.0, "seed": 12345, "dt": 0.005, "ensemble": "NVE"}
+            self.ref_kw = {}
+        elif kind == "lj":
             self.cfg = workload(cells)
             self.flat = E.gen_fcc(cells, 0.8442, 1.0, 12345)
             self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
@@ -214,7 +235,7 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     try:
-        w = Workload(args.config, args.cells)
+        w = Workload(args.config, args.cells, ws if args.weak else 0)
         v, cores, sample, steps = cpu_reference_run(w, args.steps, args.warmup,
                                                     args.ref_budget_s)
     except Exception as e:  # pragma: no cover
@@ -226,7 +247,8 @@ def run_reference_arm(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
         "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
@@ -247,7 +269,7 @@ def run_ours(args) -> None:
     torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
 
-    w = Workload(args.config, args.cells)
+    w = Workload(args.config, args.cells, 1 if args.weak else 0)
     cfg_w, n, flat = w.cfg, w.n, w.flat
     ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
     eng = E.Engine(flat, w.inter, w.r_skin, ecfg)
@@ -368,7 +390,8 @@ def run_ours(args) -> None:
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
     }
@@ -378,7 +401,8 @@ def run_ours(args) -> None:
 def run_decomposed(args) -> None:
     """N > 1: the BASELINE config on an N-slab z decomposition (decomp.py), one
     process per GPU, NCCL point-to-point halo/migration + all-reduces
-    (strong scaling: the same 1M-particle system at every N)."""
+    (strong scaling: the same 1M-particle system at every N; --weak: 2.048M
+    particles per GPU)."""
     import torch
     import torch.distributed as dist
     from paper_2109_10876_b200 import engine as E
@@ -396,7 +420,7 @@ def run_decomposed(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
     torch.cuda.set_device(dev)
-    w = Workload(args.config, args.cells)  # deterministic: identical on every rank
+    w = Workload(args.config, args.cells, ws if args.weak else 0)  # identical on every rank
     cfg_w, n, flat = w.cfg, w.n, w.flat
     ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
     balance = "count" if args.config == "slab" else "static"
@@ -459,13 +483,14 @@ def run_decomposed(args) -> None:
     cfg.update({"parallelism": f"{ws} z-slabs (spatial decomposition, {args.dist_backend} "
                                f"halo + migration, {balance} cuts, "
                                f"{'native C++' if native else 'python'} step loop)",
-                "l2": "working set > 126 MB L2 on every rank at 1M / N; no flush",
+                "l2": "working set > 126 MB L2 on every rank; no flush",
                 "rebuilds_in_timed_region": rebuilds, "section_timers": False,
                 "rank0_slab": sizes, "exchanged_bytes_rank0": xbytes})
     line = {
         "metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg, "roofline": None, "cpu_baseline": None,
         "e2e": {"value": n * args.steps / t_e2e, "unit": UNIT,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
@@ -487,6 +512,10 @@ def main():
                     help="lj: FCC LJ fluid (configs[0,1,4] by --cells 20/64/160); kg: "
                          "Kremer-Grest melt (configs[2]); slab: liquid-vapour slab "
                          "(configs[3])")
+    ap.add_argument("--weak", action="store_true",
+                    help="lj only: weak scaling at 2.048M particles per GPU (FCC 80^3 x 4 "
+                         "per GPU; the box doubles along x, y, z with N; 8 GPUs = the "
+                         "configs[4] 160^3 box)")
     ap.add_argument("--force-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)

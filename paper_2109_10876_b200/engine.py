@@ -480,6 +480,30 @@ def gen_fcc(cells: int, rho: float, temperature: float, seed: int,
     return FlatConfig(box, ids, pos, vel)
 
 
+def gen_fcc_box(nx: int, ny: int, nz: int, rho: float, temperature: float, seed: int,
+                offset: float = 0.25) -> FlatConfig:
+    """FCC nx x ny x nz x 4 lattice (the weak-scaling boxes of BASELINE.json
+    configs[4]: 2.048M particles per GPU, the 160^3 box at 8 GPUs). A cube is
+    exactly gen_fcc; otherwise lattice constant a = cbrt(4 / rho), box =
+    (nx, ny, nz) * a, ids in z, y, x, basis order, positions (i + b + offset) a,
+    the same velocity draw."""
+    if min(nx, ny, nz) < 1 or not rho > 0.0:
+        raise ConfigError("fcc generator: cells >= 1 and rho > 0 required")
+    if nx == ny == nz:
+        return gen_fcc(nx, rho, temperature, seed, offset)
+    a = float(np.cbrt(4.0 / rho))
+    basis = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0], [0.5, 0.0, 0.5], [0.0, 0.5, 0.5]])
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    cell = np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1).astype(np.float64)
+    pos = ((cell[:, None, :] + basis[None, :, :] + offset) * a).reshape(-1, 3)
+    n = pos.shape[0]
+    ids = np.arange(n, dtype=np.int64)
+    vel = np.empty((n, 3))
+    _abi.lib().tmd_thermal_velocities(n, _ptr(ids), None, float(temperature), int(seed),
+                                      _ptr(vel))
+    return FlatConfig(np.array([nx * a, ny * a, nz * a]), ids, np.ascontiguousarray(pos), vel)
+
+
 def gen_lattice(n: int, rho: float, temperature: float, seed: int) -> FlatConfig:
     """gen_lattice (generators.hpp:47-81): simple cubic, x-fastest, tail empty."""
     if n < 1:

@@ -178,3 +178,20 @@ def test_struct_layouts_match_the_header(tmp_path):
         cls = structs[cname]
         want = ctypes.sizeof(cls) if field == "size" else getattr(cls, field).offset
         assert int(val) == want, (cname, field, int(val), want)
+
+
+def test_fcc_box_generator():
+    """gen_fcc_box: a cube is gen_fcc bit for bit; an elongated box continues
+    the same lattice (its first half is the cube's) at 4 particles per cell."""
+    cube = E.gen_fcc(5, 0.8442, 1.0, 7)
+    same = E.gen_fcc_box(5, 5, 5, 0.8442, 1.0, 7)
+    np.testing.assert_array_equal(cube.pos, same.pos)
+    np.testing.assert_array_equal(cube.vel, same.vel)
+    long = E.gen_fcc_box(5, 5, 10, 0.8442, 1.0, 7)
+    assert long.size() == 2 * cube.size()
+    np.testing.assert_allclose(long.pos[: cube.size()], cube.pos, rtol=1e-15, atol=1e-14)
+    np.testing.assert_allclose(long.box, [cube.box[0], cube.box[1], 2 * cube.box[2]],
+                               rtol=1e-15)
+    rho = long.size() / np.prod(long.box)
+    assert abs(rho - 0.8442) < 1e-12
+    assert abs(long.vel.sum(axis=0)).max() < 1e-9  # zero net momentum

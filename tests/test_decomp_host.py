@@ -238,3 +238,22 @@ def test_native_balanced_cuts_match_the_python_rule():
                                           out.ctypes.data_as(ctypes.c_void_p))
         assert rc == 0
         assert out.tolist() == balanced_cuts(c, R)
+
+
+def test_run_observed_rows_match_observe_in_process():
+    """DecomposedEngine.run_observed (Python protocol): one row per stride-th
+    step, each equal to observe() after running to that step, across calls."""
+    flat = _system()
+    a = _make(flat, InProcessComm(2))
+    b = _make(flat, InProcessComm(2))
+    rows = np.vstack([a.run_observed(11, stride=4), a.run_observed(6, stride=4)])
+    assert rows[:, 0].tolist() == [4, 8, 12, 16]
+    done = 0
+    for r in rows:
+        b.run(int(r[0]) - done)
+        done = int(r[0])
+        o = b.observe()
+        assert o.step == done
+        assert np.allclose(r[1:], [o.kinetic, o.potential, o.temperature, o.virial],
+                           rtol=1e-13, atol=0.0)
+    assert a.step_count() == 17

@@ -544,10 +544,15 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
 // its bonds' partner slots and closest images.
 void launch_bond_resolve(tmd_gpu_ctx* c) {
   if (!c->bt.on) return;
-  c->launches += 3;
+  c->launches += 2;
   const int span = static_cast<int>(c->id_span);
   const int slots = static_cast<int>(c->n + c->n_ghost);
-  k_fill_int<<<blocks_for(span, kBlock), kBlock, 0, c->ls>>>(span, c->slot_of_id, -1, c->ctrl);
+  if (c->g.zslab) {  // absent ids (other slabs' particles) must read -1; a whole-box
+                     // context holds every id, each slot entry rewritten below
+    c->launches += 1;
+    k_fill_int<<<blocks_for(span, kBlock), kBlock, 0, c->ls>>>(span, c->slot_of_id, -1,
+                                                                c->ctrl);
+  }
   k_slot_of_id<<<std::max(1, blocks_for(slots, kBlock)), kBlock, 0, c->ls>>>(
       slots, c->id, c->id_min, c->slot_of_id, c->ctrl);
   k_bond_resolve<<<c->nblk, kBlock, 0, c->ls>>>(

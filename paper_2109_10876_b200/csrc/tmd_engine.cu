@@ -14,6 +14,7 @@
 // chunk to read the status word; a neighbour-list overflow rolls the chunk
 // back to its checkpoint, grows the list and replays it.
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <array>
@@ -1574,47 +1575,73 @@ void setup_bonds(tmd_gpu_ctx* c, const tmd_system* sys, const tmd_fene_params* f
     throw StatusError{TMD_ERR_CONFIG,
                       "bonded systems need particle ids in a dense range (max - min < 4 n)"};
   }
-  std::vector<int> deg(static_cast<size_t>(span) + 1, 0);
-  for (int64_t k = 0; k < sys->n_bonds; ++k) {
-    ++deg[static_cast<size_t>(sys->bonds[2 * k] - id_min)];
-    ++deg[static_cast<size_t>(sys->bonds[2 * k + 1] - id_min)];
-  }
-  std::vector<int> off(static_cast<size_t>(span) + 1, 0);
-  for (int64_t o = 0; o < span; ++o) {
-    if (deg[static_cast<size_t>(o)] > kMaxBonds) {
-      throw StatusError{TMD_ERR_CONFIG, "particle id " + std::to_string(id_min + o) + " has " +
-                                            std::to_string(deg[static_cast<size_t>(o)]) +
+  // CSR over id - id_min, built on the device (sizes only cross to the host)
+  const int64_t nb = sys->n_bonds;
+  const size_t ns = static_cast<size_t>(span);
+  long long* d_bonds = dalloc<long long>(static_cast<size_t>(2 * nb));
+  int* deg = dalloc<int>(ns + 1);
+  int* cur = dalloc<int>(ns + 1);
+  int* bidx = dalloc<int>(static_cast<size_t>(2 * nb));
+  int* bad = dalloc<int>(1);
+  c->id_min = id_min;
+  c->id_span = span;
+  c->slot_of_id = dalloc<int>(ns);
+  c->bond_off = dalloc<int>(ns + 1);
+  c->bond_nbr = dalloc<int>(static_cast<size_t>(2 * nb));
+  c->bond_anchor = dalloc<unsigned char>(static_cast<size_t>(2 * nb));
+  c->bnd_cnt = dalloc<int>(static_cast<size_t>(c->n_cap));
+  c->bnd_ent = dalloc<uint32_t>(static_cast<size_t>(c->n_cap) * kMaxBonds);
+  auto release = [&] {
+    cudaFree(d_bonds);
+    cudaFree(deg);
+    cudaFree(cur);
+    cudaFree(bidx);
+    cudaFree(bad);
+  };
+  try {
+    cudaStream_t st = c->stream;
+    ck(cudaMemcpyAsync(d_bonds, sys->bonds, sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice,
+                       st), "H2D bonds");
+    ck(cudaMemsetAsync(deg, 0, sizeof(int) * (ns + 1), st), "memset");
+    ck(cudaMemsetAsync(cur, 0, sizeof(int) * (ns + 1), st), "memset");
+    const int big = 0x7fffffff;
+    ck(cudaMemcpyAsync(bad, &big, sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+    const int gb = std::max(1, blocks_for(nb, kBlock));
+    const int gs = std::max(1, blocks_for(span, kBlock));
+    k_bond_degree<<<gb, kBlock, 0, st>>>(nb, d_bonds, id_min, deg);
+    k_bond_maxdeg<<<gs, kBlock, 0, st>>>(static_cast<int>(span), deg, bad);
+    size_t tmp_bytes = 0;
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg, c->bond_off,
+                                     static_cast<int>(span + 1), st), "cub scan (size)");
+    void* tmp = nullptr;
+    ck(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)), "cudaMalloc(scan)");
+    const cudaError_t se = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, c->bond_off,
+                                                         static_cast<int>(span + 1), st);
+    k_bond_fill<<<gb, kBlock, 0, st>>>(nb, d_bonds, id_min, c->bond_off, cur, bidx, c->bond_nbr,
+                                       c->bond_anchor);
+    k_bond_order<<<gs, kBlock, 0, st>>>(static_cast<int>(span), c->bond_off, bidx, c->bond_nbr,
+                                        c->bond_anchor);
+    ck(cudaMemsetAsync(c->bnd_cnt, 0, sizeof(int) * static_cast<size_t>(c->n_cap), st),
+       "memset");
+    int h_bad = big;
+    ck(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    cudaFree(tmp);
+    ck(se, "cub scan");
+    ck(cudaGetLastError(), "bond table kernels");
+    if (h_bad != big) {
+      int d = 0;
+      ck(cudaMemcpy(&d, deg + h_bad, sizeof(int), cudaMemcpyDeviceToHost), "D2H degree");
+      throw StatusError{TMD_ERR_CONFIG, "particle id " + std::to_string(id_min + h_bad) +
+                                            " has " + std::to_string(d) +
                                             " bonds; the GPU path allows " +
                                             std::to_string(kMaxBonds)};
     }
-    off[static_cast<size_t>(o) + 1] = off[static_cast<size_t>(o)] + deg[static_cast<size_t>(o)];
+  } catch (...) {
+    release();
+    throw;
   }
-  std::vector<int> nbr(static_cast<size_t>(2 * sys->n_bonds));
-  std::vector<unsigned char> anchor(static_cast<size_t>(2 * sys->n_bonds));
-  std::vector<int> fill(off.begin(), off.end() - 1);
-  for (int64_t k = 0; k < sys->n_bonds; ++k) {  // bond order kept at each end
-    const int64_t a = sys->bonds[2 * k] - id_min, b = sys->bonds[2 * k + 1] - id_min;
-    const int pa = fill[static_cast<size_t>(a)]++, pb = fill[static_cast<size_t>(b)]++;
-    nbr[static_cast<size_t>(pa)] = static_cast<int>(b);
-    anchor[static_cast<size_t>(pa)] = 1;
-    nbr[static_cast<size_t>(pb)] = static_cast<int>(a);
-    anchor[static_cast<size_t>(pb)] = 0;
-  }
-  c->id_min = id_min;
-  c->id_span = span;
-  c->slot_of_id = dalloc<int>(static_cast<size_t>(span));
-  c->bond_off = dalloc<int>(off.size());
-  c->bond_nbr = dalloc<int>(nbr.size());
-  c->bond_anchor = dalloc<unsigned char>(anchor.size());
-  c->bnd_cnt = dalloc<int>(static_cast<size_t>(c->n_cap));
-  c->bnd_ent = dalloc<uint32_t>(static_cast<size_t>(c->n_cap) * kMaxBonds);
-  ck(cudaMemcpy(c->bond_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice),
-     "H2D bond offsets");
-  ck(cudaMemcpy(c->bond_nbr, nbr.data(), nbr.size() * sizeof(int), cudaMemcpyHostToDevice),
-     "H2D bond partners");
-  ck(cudaMemcpy(c->bond_anchor, anchor.data(), anchor.size(), cudaMemcpyHostToDevice),
-     "H2D bond anchors");
-  ck(cudaMemset(c->bnd_cnt, 0, sizeof(int) * static_cast<size_t>(c->n_cap)), "memset");
+  release();
   c->bt.on = 1;
   c->bt.k = fene->k;
   c->bt.rmax2 = fene->r_max * fene->r_max;  // fene_eval (potentials.hpp:98)

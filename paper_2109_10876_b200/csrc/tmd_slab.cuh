@@ -243,4 +243,67 @@ __global__ void k_slab_row(int* __restrict__ row, const int* __restrict__ nb0,
   row[4] = gen;
 }
 
+// ---------------------------------------------------------------------------
+// Bond table (CSR over id - id_min) built on the device at create
+// (setup_bonds): degrees, an exclusive scan (CUB), then each bond appended to
+// both ends and every particle's few entries put back in bond order — the
+// order the host build keeps ("bond order kept at each end").
+__global__ void __launch_bounds__(kBlock)
+    k_bond_degree(int64_t nb, const long long* __restrict__ bonds, long long id_min,
+                  int* __restrict__ deg) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+  if (k >= nb) return;
+  atomicAdd(&deg[bonds[2 * k] - id_min], 1);
+  atomicAdd(&deg[bonds[2 * k + 1] - id_min], 1);
+}
+
+// Smallest id offset holding more than kMaxBonds bonds (the host's error).
+__global__ void __launch_bounds__(kBlock)
+    k_bond_maxdeg(int span, const int* __restrict__ deg, int* __restrict__ bad) {
+  const int o = blockIdx.x * kBlock + threadIdx.x;
+  if (o < span && deg[o] > kMaxBonds) atomicMin(bad, o);
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_bond_fill(int64_t nb, const long long* __restrict__ bonds, long long id_min,
+                const int* __restrict__ off, int* __restrict__ cur, int* __restrict__ bidx,
+                int* __restrict__ nbr, unsigned char* __restrict__ anchor) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+  if (k >= nb) return;
+  const int a = static_cast<int>(bonds[2 * k] - id_min);
+  const int b = static_cast<int>(bonds[2 * k + 1] - id_min);
+  const int pa = off[a] + atomicAdd(&cur[a], 1);
+  const int pb = off[b] + atomicAdd(&cur[b], 1);
+  bidx[pa] = static_cast<int>(k);
+  nbr[pa] = b;
+  anchor[pa] = 1;
+  bidx[pb] = static_cast<int>(k);
+  nbr[pb] = a;
+  anchor[pb] = 0;
+}
+
+// Each particle's entries by bond index (<= kMaxBonds of them; a bond to the
+// same partner twice keeps its two entries apart by index).
+__global__ void __launch_bounds__(kBlock)
+    k_bond_order(int span, const int* __restrict__ off, int* __restrict__ bidx,
+                 int* __restrict__ nbr, unsigned char* __restrict__ anchor) {
+  const int o = blockIdx.x * kBlock + threadIdx.x;
+  if (o >= span) return;
+  const int b0 = off[o], m = off[o + 1] - b0;
+  for (int x = 1; x < m; ++x) {
+    const int kx = bidx[b0 + x], nx = nbr[b0 + x];
+    const unsigned char ax = anchor[b0 + x];
+    int y = x - 1;
+    while (y >= 0 && bidx[b0 + y] > kx) {
+      bidx[b0 + y + 1] = bidx[b0 + y];
+      nbr[b0 + y + 1] = nbr[b0 + y];
+      anchor[b0 + y + 1] = anchor[b0 + y];
+      --y;
+    }
+    bidx[b0 + y + 1] = kx;
+    nbr[b0 + y + 1] = nx;
+    anchor[b0 + y + 1] = ax;
+  }
+}
+
 }  // namespace tmd

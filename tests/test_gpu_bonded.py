@@ -171,3 +171,19 @@ def test_kg_melt_warmup_then_nve():
     o = eng.observe()
     assert abs(o.kinetic + o.potential - e0) / abs(e0) < 5e-3
     assert 0.3 < o.temperature < 3.0
+
+
+def test_bond_table_degree_limit_and_order():
+    """The device-built bond table: a particle with more than kMaxBonds (8)
+    bonds is a ConfigError naming the smallest such id; duplicate bonds keep
+    both entries (forces and energies count the bond twice, as the reference's
+    bond list does)."""
+    box = np.full(3, 12.0)
+    rng = np.random.default_rng(5)
+    pos = rng.random((40, 3)) * 12.0
+    ids = np.arange(100, 140, dtype=np.int64)
+    star = np.array([[105, 110 + k] for k in range(9)], dtype=np.int64)
+    flat = E.FlatConfig(box, ids, pos, None, bonds=star)
+    inter = E.Interactions(fene=E.FeneParams(30.0, 1.5))
+    with pytest.raises(E.ConfigError, match="particle id 105 has 9 bonds"):
+        E.Engine(flat, inter, 0.4, E.EngineConfig(dt=0.001))

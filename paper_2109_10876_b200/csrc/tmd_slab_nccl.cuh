@@ -271,15 +271,13 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
         c->id2);
   }
   const size_t keep = static_cast<size_t>(n - off[uR]);
-  auto cp = [&](void* d, const void* src, size_t bytes) {
-    if (bytes) ck(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDeviceToDevice, c->stream), "copy");
-  };
-  cp(c->pos, c->pos2, keep * sizeof(double4));
-  cp(c->vx, c->vx2, keep * sizeof(double));
-  cp(c->vy, c->vy2, keep * sizeof(double));
-  cp(c->vz, c->vz2, keep * sizeof(double));
-  cp(c->mass, c->mass2, keep * sizeof(double));
-  cp(c->id, c->id2, keep * sizeof(long long));
+  if (keep > 0) {  // stayers back in place: one launch (the resort's copy-back; the
+                   // cell column it also copies is recomputed by the resort)
+    c->launches += 1;
+    k_copy_back<<<blocks_for(static_cast<int64_t>(keep), kBlock), kBlock, 0, c->ls>>>(
+        static_cast<int>(keep), c->pos2, c->vx2, c->vy2, c->vz2, c->mass2, c->id2, c->cell2,
+        c->pos, c->vx, c->vy, c->vz, c->mass, c->id, c->cell, c->ctrl);
+  }
   c->n = static_cast<int64_t>(keep);
   c->n_ghost = c->n_ghost_lo = c->n_ghost_hi = 0;
   int64_t nrecv = 0;

@@ -45,10 +45,11 @@ HBM_FALLBACK_GBS = 6650.0
 
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
+    try:
         d = json.loads(p.read_text())
         return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
-    return {"hbm_gbs": HBM_FALLBACK_GBS, "source": "fallback (B200_PROFILING.md)"}
+    except (OSError, ValueError, KeyError, TypeError):  # absent or another schema
+        return {"hbm_gbs": HBM_FALLBACK_GBS, "source": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:

@@ -1,31 +1,49 @@
 #!/usr/bin/env python3
-"""Throughput bench for the B200 LJ short-range engine (BASELINE.json configs[1]).
+"""Throughput bench for the B200 LJ short-range engine.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config lj|kg|slab] [--cells C] [--weak]
 
-Workload (BASELINE.json configs[1]): LJ fluid, 1,048,576 particles on an FCC
-64^3 x 4 lattice, rho 0.8442, eps = sigma = m = 1, r_cut 2.5 shifted, skin
-0.3, Gaussian velocities at T = 1.0 (seed 12345, zero net momentum),
-dt 0.005, FP64, NVE. A "step" is one velocity-Verlet step of the whole system
-(kick, drift, on-device rebuild decision, resort + list build when triggered,
-forces, kick). Synthetic input generated on the host (no dataset exists).
+Default workload (BASELINE.json configs[4], the configuration the north-star's
+scaling target is stated on, and one that fits one GPU): LJ fluid, 16,384,000
+particles on an FCC 160^3 x 4 lattice, rho 0.8442, eps = sigma = m = 1, r_cut
+2.5 shifted, skin 0.3, Gaussian velocities at T = 1.0 (seed 12345, zero net
+momentum), dt 0.005, FP64, NVE; the same system at every N (strong scaling).
+`--cells 64` is configs[1] (1M), `--cells 20` configs[0] (32K), `--config kg`
+configs[2], `--config slab` configs[3], `--weak` configs[4]'s weak series
+(2.048M particles per GPU). A "step" is one velocity-Verlet step of the whole
+system (kick, drift, on-device rebuild decision, resort + list build when
+triggered, forces, kick). Synthetic inputs (no dataset exists).
 
-One JSON line on rank 0 (see DESIGN.md §Measurement for every field):
-  value      device-timed particle-steps/s, inputs resident in HBM
+`--gpus N` with N > 1 and no torchrun environment re-launches this script
+under `python -m torch.distributed.run --nproc-per-node N`; under torchrun the
+world size must equal N. Each rank drives one GPU's slab of the z-slab
+decomposition (the native C++ step loop over NCCL).
+
+One JSON line on rank 0:
+  value      device-timed particle-steps/s (CUDA events on the engine's
+             stream, inputs resident in HBM, max over ranks)
   e2e        the same metric through the public API from host buffers:
-             create (H2D) + K x (step + observe D2H) + final download
-  roofline   the LJ force kernel against max(B/HBM, F/FP64)
-  cpu_baseline  the reference engine (oracle/_ref) on this box's host cores
+             create (H2D) + K x (step + observables D2H) + final download
+  roofline   the production step kernel (forces + fused integrator) against
+             max(B/HBM, F/FP64) (BASELINE.md §4 / SURVEY §8d), plus the
+             L1-wavefront model and ncu's DRAM / L1TEX figures
+  cpu_baseline  the reference engine (oracle/_ref) on this box's host cores:
+             all-core rate, its five SectionTimers, and a 1-thread rate
 
 --impl reference times the reference's own CPU engine (oracle/_ref: the
-unmodified taskmd headers compiled by oracle/Makefile) on the same config,
-rank 0 only.
+unmodified taskmd headers compiled by oracle/Makefile) on the same config
+with every host core, rank 0 only. Its inputs are generated without this
+repo's library (numpy + the reference's own velocity draw), so that arm
+never maps libtmd_gpu.so.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,6 +59,8 @@ sys.path.insert(0, str(ROOT))
 METRIC = "LJ particle-steps/sec at 1/2/4/8 B200; force-kernel % of HBM/FP64 roofline"
 UNIT = "particle-steps/s"
 HBM_FALLBACK_GBS = 6650.0
+L2_BYTES = 126 * 2 ** 20
+RHO, SEED = 0.8442, 12345
 
 
 def measured_peaks() -> dict:
@@ -114,6 +134,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------------
+# launch: one process per GPU
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -121,144 +144,353 @@ def dist_env():
     return ws, rank, local
 
 
-def workload(cells: int) -> dict:
-    n = 4 * cells ** 3
-    idx = {20: 0, 64: 1, 160: 4}.get(cells)
-    return {"workload": f"LJ fluid FCC {cells}^3x4" +
-            (f" (BASELINE.json configs[{idx}])" if idx is not None else ""),
-            "n_particles": n, "rho": 0.8442, "r_cut": 2.5, "energy_shifted": True,
-            "r_skin": 0.3, "temperature": 1.0, "seed": 12345, "dt": 0.005,
-            "ensemble": "NVE"}
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return int(s.getsockname()[1])
 
 
-class Workload:
-    """One BASELINE.json configuration: the synthetic system, its interactions
-    and integrator settings, and the reference-engine kwargs for the CPU arm."""
-
-    def __init__(self, kind: str, cells: int, weak_ranks: int = 0):
-        from paper_2109_10876_b200 import engine as E
-        self.kind = kind
-        self.setup_s = 0.0
-        t0 = time.perf_counter()
-        if kind == "lj" and weak_ranks > 0:
-            # configs[4] weak scaling: FCC 80^3 x 4 = 2.048M particles per GPU, the
-            # box doubled along x, then y, then z (8 GPUs: the 160^3 configs[4] box)
-            dims = [80, 80, 80]
-            k = 0
-            r = weak_ranks
-            while r > 1:
-                if r % 2:
-                    raise SystemExit("--weak needs a power-of-two GPU count")
-                dims[k % 3] *= 2
-                k += 1
-                r //= 2
-            self.flat = E.gen_fcc_box(*dims, 0.8442, 1.0, 12345)
-            self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
-            self.cfg = {"workload": "LJ fluid, weak scaling at 2.048M particles per GPU "
-                                    "(BASELINE.json configs[4])",
-                        "fcc_cells": dims, "n_particles": self.flat.size(),
-                        "n_per_gpu": self.flat.size() // weak_ranks, "rho": 0.8442,
-                        "r_cut": 2.5, "energy_shifted": True, "r_skin": 0.3,
-                        "temperature": 1.0, "seed": 12345, "dt": 0.005, "ensemble": "NVE"}
-            self.ref_kw = {}
-        elif kind == "lj":
-            self.cfg = workload(cells)
-            self.flat = E.gen_fcc(cells, 0.8442, 1.0, 12345)
-            self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
-            self.ref_kw = {}
-        elif kind == "kg":
-            # configs[2]: 20,000 x 200-bead KG melt (cells scales it: chains = 20000 *
-            # (cells/64)^3), random-walk chains + force-capped Langevin warm-up
-            chains = max(1, round(20000 * (cells / 64) ** 3))
-            raw = E.gen_chains(chains, 200, 0.85, 0.97, seed=12345)
-            self.flat = E.kg_warmup(raw)
-            self.inter, self.r_skin, self.dt = E.kg_interactions(), 0.4, 0.01
-            self.cfg = {"workload": "Kremer-Grest melt (BASELINE.json configs[2])"
-                        if chains == 20000 else "Kremer-Grest melt",
-                        "chains": chains, "beads_per_chain": 200,
-                        "n_particles": self.flat.size(), "rho": 0.85, "bond": 0.97,
-                        "lj": "WCA r_cut 2^(1/6) shifted", "fene": [30.0, 1.5],
-                        "r_skin": 0.4, "dt": 0.01, "ensemble": "NVE",
-                        "warmup": "force-capped Langevin (kg_warmup), untimed"}
-            self.ref_kw = dict(r_cut=2.0 ** (1.0 / 6.0), bonds=self.flat.bonds,
-                               fene=(30.0, 1.5))
-        elif kind == "slab":
-            # configs[3]: 2,097,152 particles, liquid FCC slab in the middle third of
-            # Lz = 3 Lx (81^3-cell block filled in id order, SURVEY §8d)
-            n = 2097152 if cells == 64 else 4 * cells ** 3
-            c = 81 if cells == 64 else cells
-            self.flat = E.gen_fcc_slab(c, 0.8442, 0.7, 12345, n=n)
-            self.inter, self.r_skin, self.dt = E.Interactions(), 0.3, 0.005
-            self.cfg = {"workload": "LJ liquid-vapour slab (BASELINE.json configs[3])"
-                        if n == 2097152 else "LJ liquid-vapour slab",
-                        "n_particles": n, "rho_liquid": 0.8442, "box": list(self.flat.box),
-                        "temperature": 0.7, "r_cut": 2.5, "r_skin": 0.3, "dt": 0.005,
-                        "ensemble": "NVE"}
-            self.ref_kw = {}
-        else:
-            raise SystemExit(f"unknown config {kind!r}")
-        self.setup_s = time.perf_counter() - t0
-        self.n = self.flat.size()
+def relaunch_if_needed(args, argv) -> None:
+    """`--gpus N` means N ranks: without a torchrun environment, N > 1 re-runs
+    this script under torch.distributed.run (one process per GPU); under
+    torchrun the world size must be N."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                   f"--master-port={_free_port()}", str(Path(__file__).resolve()), *argv]
+            sys.stdout.flush()
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(ws_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started "
+                         f"WORLD_SIZE={ws_env} ranks; pass --gpus {ws_env}")
 
 
 # ----------------------------------------------------------------------------------
-def cpu_reference_run(w: "Workload", steps_wanted: int, warmup: int, budget_s: float):
-    """The reference engine (oracle/_ref) on all host cores. Returns
-    (particle-steps/s, cores, sample description, steps timed)."""
+# workload description (identical in both arms) and synthetic inputs
+
+def config_index(kind: str, cells: int, weak: bool):
+    if kind == "lj":
+        if weak:
+            return 4
+        return {20: 0, 64: 1, 160: 4}.get(cells)
+    if kind == "kg":
+        return 2 if cells == 64 else None
+    if kind == "slab":
+        return 3 if cells == 64 else None
+    return None
+
+
+def weak_dims(ranks: int):
+    """configs[4] weak scaling: FCC 80^3 x 4 = 2.048M particles per GPU, the box
+    doubled along x, then y, then z (8 GPUs: the 160^3 configs[4] box)."""
+    dims = [80, 80, 80]
+    k, r = 0, ranks
+    while r > 1:
+        if r % 2:
+            raise SystemExit("--weak needs a power-of-two GPU count")
+        dims[k % 3] *= 2
+        k += 1
+        r //= 2
+    return dims
+
+
+def workload_config(kind: str, cells: int, weak: bool, ranks: int) -> dict:
+    """The `config` object of the JSON line — a pure function of the command
+    line, so both arms print the same dict."""
+    idx = config_index(kind, cells, weak)
+    tag = f" (BASELINE.json configs[{idx}])" if idx is not None else ""
+    if kind == "lj" and weak:
+        dims = weak_dims(ranks)
+        n = 4 * dims[0] * dims[1] * dims[2]
+        return {"workload": "LJ fluid, weak scaling at 2.048M particles per GPU" + tag,
+                "fcc_cells": dims, "n_particles": n, "n_per_gpu": n // ranks, "rho": RHO,
+                "r_cut": 2.5, "energy_shifted": True, "r_skin": 0.3, "temperature": 1.0,
+                "seed": SEED, "dt": 0.005, "ensemble": "NVE"}
+    if kind == "lj":
+        return {"workload": f"LJ fluid FCC {cells}^3x4" + tag, "n_particles": 4 * cells ** 3,
+                "rho": RHO, "r_cut": 2.5, "energy_shifted": True, "r_skin": 0.3,
+                "temperature": 1.0, "seed": SEED, "dt": 0.005, "ensemble": "NVE"}
+    if kind == "kg":
+        chains = max(1, round(20000 * (cells / 64) ** 3))
+        return {"workload": "Kremer-Grest melt" + tag, "chains": chains,
+                "beads_per_chain": 200, "n_particles": chains * 200, "rho": 0.85,
+                "bond": 0.97, "lj": "WCA r_cut 2^(1/6) shifted", "fene": [30.0, 1.5],
+                "r_skin": 0.4, "dt": 0.01, "ensemble": "NVE",
+                "warmup": "force-capped Langevin (kg_warmup), untimed"}
+    if kind == "slab":
+        n = 2097152 if cells == 64 else 4 * cells ** 3
+        return {"workload": "LJ liquid-vapour slab" + tag, "n_particles": n,
+                "rho_liquid": RHO, "box_lz_over_lx": 3, "temperature": 0.7, "r_cut": 2.5,
+                "r_skin": 0.3, "dt": 0.005, "ensemble": "NVE"}
+    raise SystemExit(f"unknown config {kind!r}")
+
+
+def fcc_numpy(nx: int, ny: int, nz: int, offset: float = 0.25):
+    """The FCC lattice of SURVEY §8(d) in numpy (no repo library): ids in z, y,
+    x, basis order, positions (i + b + offset) a; a cube uses a = L / cells
+    with L = cbrt(n / rho) (tmd_gen_fcc's rounding), other boxes a =
+    cbrt(4 / rho). Bit-identical to the engine's generators
+    (tests/test_bench_host.py)."""
+    n = 4 * nx * ny * nz
+    if nx == ny == nz:
+        L = math.cbrt(float(n) / RHO)  # libm cbrt, as tmd_gen_fcc (np.cbrt differs by an ulp)
+        a = L / nx
+        box = np.array([L, L, L])
+    else:
+        a = float(np.cbrt(4.0 / RHO))  # gen_fcc_box's rule
+        box = np.array([nx * a, ny * a, nz * a])
+    basis = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0], [0.5, 0.0, 0.5], [0.0, 0.5, 0.5]])
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    cell = np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1).astype(np.float64)
+    pos = np.ascontiguousarray(((cell[:, None, :] + basis[None, :, :] + offset) * a)
+                               .reshape(-1, 3))
+    return box, np.arange(n, dtype=np.int64), pos
+
+
+class Inputs:
+    """One system: box, ids, positions, velocities (+ bonds), the interaction
+    settings, and the reference-engine kwargs."""
+
+    def __init__(self, box, ids, pos, vel, *, r_skin, dt, bonds=None, ref_kw=None):
+        self.box, self.id, self.pos, self.vel = box, ids, pos, vel
+        self.bonds = bonds
+        self.r_skin, self.dt = r_skin, dt
+        self.ref_kw = ref_kw or {}
+        self.n = int(ids.shape[0])
+
+
+def kg_ref_kw(bonds):
+    return dict(r_cut=2.0 ** (1.0 / 6.0), bonds=bonds, fene=(30.0, 1.5))
+
+
+def make_inputs_ours(kind: str, cells: int, weak_ranks: int):
+    """Inputs through the engine's own generators (our arm)."""
+    from paper_2109_10876_b200 import engine as E
+    if kind == "lj":
+        if weak_ranks > 0:
+            f = E.gen_fcc_box(*weak_dims(weak_ranks), RHO, 1.0, SEED)
+        else:
+            f = E.gen_fcc(cells, RHO, 1.0, SEED)
+        return f, E.Interactions(), Inputs(f.box, f.id, f.pos, f.vel, r_skin=0.3, dt=0.005)
+    if kind == "kg":
+        chains = max(1, round(20000 * (cells / 64) ** 3))
+        f = E.kg_warmup(E.gen_chains(chains, 200, 0.85, 0.97, seed=SEED))
+        return f, E.kg_interactions(), Inputs(f.box, f.id, f.pos, f.vel, r_skin=0.4,
+                                              dt=0.01, bonds=f.bonds,
+                                              ref_kw=kg_ref_kw(f.bonds))
+    if kind == "slab":
+        n = 2097152 if cells == 64 else 4 * cells ** 3
+        c = 81 if cells == 64 else cells
+        f = E.gen_fcc_slab(c, RHO, 0.7, SEED, n=n)
+        return f, E.Interactions(), Inputs(f.box, f.id, f.pos, f.vel, r_skin=0.3, dt=0.005)
+    raise SystemExit(f"unknown config {kind!r}")
+
+
+def make_inputs_reference(kind: str, cells: int, weak_ranks: int) -> Inputs:
+    """Inputs for the reference arm without this repo's library: numpy FCC
+    positions + the reference's own velocity draw (gen_detail::
+    thermal_velocities + zero_net_momentum, generators.hpp:19-39, through
+    oracle/_ref). The KG melt needs the force-capped warm-up (absent from the
+    reference), so it is generated by a separate process of this script and
+    handed over as a file."""
     from oracle import ref
     if not ref.available():
         ref.build()
-    f = w.flat
+    if kind == "lj":
+        dims = weak_dims(weak_ranks) if weak_ranks > 0 else [cells] * 3
+        box, ids, pos = fcc_numpy(*dims)
+        vel = ref.thermal_velocities(ids, 1.0, SEED)
+        return Inputs(box, ids, pos, vel, r_skin=0.3, dt=0.005)
+    if kind == "slab":
+        n = 2097152 if cells == 64 else 4 * cells ** 3
+        c = 81 if cells == 64 else cells
+        box, ids, pos = fcc_numpy(c, c, c)
+        pos = pos.copy()
+        pos[:, 2] += box[2]
+        box = box.copy()
+        box[2] *= 3.0
+        ids, pos = ids[:n], np.ascontiguousarray(pos[:n])
+        vel = ref.thermal_velocities(ids, 0.7, SEED)
+        return Inputs(box, ids, pos, vel, r_skin=0.3, dt=0.005)
+    if kind == "kg":
+        path = Path(os.environ.get("TMPDIR", "/tmp")) / f"tmd_bench_kg_{cells}.npz"
+        if not path.exists():
+            subprocess.run([sys.executable, str(Path(__file__).resolve()), "--make-kg-input",
+                            str(path), "--cells", str(cells)], check=True,
+                           env={k: v for k, v in os.environ.items()
+                                if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+        d = np.load(path)
+        return Inputs(d["box"], d["id"], d["pos"], d["vel"], r_skin=0.4, dt=0.01,
+                      bonds=d["bonds"], ref_kw=kg_ref_kw(d["bonds"]))
+    raise SystemExit(f"unknown config {kind!r}")
+
+
+# ----------------------------------------------------------------------------------
+# the reference engine on the host cores
+
+def cpu_reference_run(w: Inputs, steps_wanted: int, warmup: int, budget_s: float,
+                      one_thread_budget_s: float = 0.0) -> dict:
+    """The reference engine (oracle/_ref) with every host core: particle-steps/s
+    over a bounded sample, its five SectionTimers over the timed steps, and
+    (one_thread_budget_s > 0) a 1-thread rate from a second Engine over a copy
+    of the same Domain (ref_clone)."""
+    from oracle import ref
+    if not ref.available():
+        ref.build()
     cores = os.cpu_count() or 1
-    n_sub = 2 * cores
+    rv = w.ref_kw.get("r_cut", 2.5) + w.r_skin
+    cells = int(np.prod([max(1, int(math.floor(float(L) / rv))) for L in w.box]))
+    n_sub = max(1, min(2 * cores, cells))
     t0 = time.perf_counter()
-    r = ref.RefEngine(f.box, f.id, f.pos, f.vel, r_skin=w.r_skin, n_sub=n_sub, workers=cores,
+    r = ref.RefEngine(w.box, w.id, w.pos, w.vel, r_skin=w.r_skin, n_sub=n_sub, workers=cores,
                       dt=w.dt, **w.ref_kw)
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
     r.run(max(1, warmup))
     est = (time.perf_counter() - t0) / max(1, warmup)
     steps = int(max(1, min(steps_wanted, budget_s / max(est, 1e-9))))
+    sec0, el0 = r.timers()
     t0 = time.perf_counter()
     r.run(steps)
     t = time.perf_counter() - t0
-    n = f.size()
-    sample = (f"{n}-particle {w.kind} config, {steps} NVE steps (of {steps_wanted} requested) after "
-              f"build_domain ({t_build:.1f} s, untimed) and {max(1, warmup)} warm-up steps; "
-              f"reference taskmd Engine, worker_threads={cores}, n_sub={n_sub} (fixed 2x "
-              f"workers), g++ -O3 -DNDEBUG")
+    sec1, el1 = r.timers()
+    n = w.n
+    out = {"value": n * steps / t, "cores": cores, "steps": steps, "n_sub": n_sub,
+           "build_s": t_build,
+           "sections_s": dict(zip(("Forces", "Comm", "Integrate", "Neigh", "Resort"),
+                                  (float(x) for x in sec1 - sec0))),
+           "elapsed_s": float(el1 - el0)}
+    out["sample"] = (f"{n}-particle system, {steps} NVE steps (of {steps_wanted} requested) "
+                     f"after build_domain + Engine ctor ({t_build:.1f} s, untimed) and "
+                     f"{max(1, warmup)} warm-up steps; reference taskmd Engine, "
+                     f"worker_threads={cores}, n_sub={n_sub} (fixed 2x workers, at most the cell count), "
+                     f"g++ -O3 -DNDEBUG")
+    if one_thread_budget_s > 0.0:
+        t0 = time.perf_counter()
+        r1 = r.clone(1)
+        t_clone = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r1.run(1)
+        est1 = time.perf_counter() - t0
+        s1 = int(max(1, min(steps_wanted, one_thread_budget_s / max(est1, 1e-9))))
+        t0 = time.perf_counter()
+        r1.run(s1)
+        t1 = time.perf_counter() - t0
+        sec_1, _ = r1.timers()
+        r1.close()
+        out["one_thread"] = {
+            "value": n * s1 / t1, "steps": s1,
+            "sample": f"same Domain (n_sub={n_sub}), worker_threads=1, {s1} steps after 1 "
+                      f"warm-up step (Engine ctor {t_clone:.1f} s, untimed)"}
     r.close()
-    return n * steps / t, cores, sample, steps
+    return out
 
 
 def run_reference_arm(args) -> None:
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    cfg = workload_config(args.config, args.cells, args.weak, ws)
     try:
-        w = Workload(args.config, args.cells, ws if args.weak else 0)
-        v, cores, sample, steps = cpu_reference_run(w, args.steps, args.warmup,
-                                                    args.ref_budget_s)
+        w = make_inputs_reference(args.config, args.cells, ws if args.weak else 0)
+        c = cpu_reference_run(w, args.steps, args.warmup, args.ref_budget_s)
     except Exception as e:  # pragma: no cover
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
         return
-    cfg = dict(w.cfg)
-    cfg["parallelism"] = "host threads (reference CPU engine)"
-    n = w.n
+    v = c["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
-        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
+        "steps": c["steps"], "warmup": args.warmup, "ms_per_step": 1e3 * w.n / v,
         "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
-        "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": cfg,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": sample},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": c["cores"], "kind": "reference",
+                         "sample": c["sample"], "sections_s": c["sections_s"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "details": {"parallelism": "host threads (reference CPU engine), rank 0 only",
+                    "inputs": "numpy FCC + the reference's thermal_velocities "
+                              "(no repo library in this process)"},
     }
     print(json.dumps(line))
 
 
 # ----------------------------------------------------------------------------------
+# our arm
+
+def ncu_capture(n: int, kernel: str):
+    """Per-launch DRAM bytes and the L1TEX / DRAM throughput fractions of the
+    step kernel from the committed ncu capture of this workload
+    (profiles/force_kernel_ncu.json, written by scripts/ncu_summary.py), or
+    None when the capture is of another size or kernel."""
+    prof = ROOT / "profiles" / "force_kernel_ncu.json"
+    try:
+        pj = json.loads(prof.read_text())
+    except (OSError, ValueError):
+        return None
+    for rec in pj if isinstance(pj, list) else [pj]:
+        if rec.get("n_particles") == n and rec.get("kernel", kernel) == kernel:
+            return rec
+    return None
+
+
+def roofline(eng, n: int, step_ms: float, sm_mhz: float, reps: int) -> dict:
+    """The production step kernel (forces + fused velocity-Verlet epilogue)
+    against the frozen roofline of SURVEY §8(d) / BASELINE.md §4:
+    B = N*52 + E*28 bytes, F = 8E + 20P, T_roof = max(B/HBM, F/FP64)."""
+    from paper_2109_10876_b200 import engine as E
+    st = eng.list_stats()
+    kc = eng.kernel_config()
+    E_ent, P_cut = st["entries"], st["in_cut"]
+    t_ms = eng.time_step_kernel(reps)
+    B = n * 52 + E_ent * 28
+    F = 8 * E_ent + 20 * P_cut
+    peaks = measured_peaks()
+    fp64 = E.fp64_peak_tflops(eng.config().device)
+    t_hbm = B / (peaks["hbm_gbs"] * 1e9)
+    t_flop = F / (fp64 * 1e12)
+    kernel = ("k_forces_l1<kFused>" if kc["lanes"] == 1
+              else f"k_forces_lanes<{kc['lanes']}, kFused>")
+    cap = ncu_capture(n, kernel)
+    if t_hbm >= t_flop:
+        achieved = B / (t_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"]}
+    else:
+        achieved = F / (t_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64}
+    roof["traffic"] = None if cap is None else cap.get("dram_bytes_per_launch")
+    # what binds it: every gathered neighbour of a warp's 32 lanes lies in its
+    # own 128-B line, one L1 wavefront each, one wavefront per clock per SM
+    t_l1 = E_ent / (148 * sm_mhz * 1e6)
+    roof.update({
+        "kernel": kernel, "algorithmic_bytes": B, "algorithmic_flops": F,
+        "entries": E_ent, "in_cut_entries": P_cut, "kernel_ms": t_ms,
+        "t_roof_ms": 1e3 * max(t_hbm, t_flop), "fp64_peak_tflops_measured": fp64,
+        "peak_source": peaks["source"], "share_of_step": t_ms / step_ms,
+        "l1": {"model": "one L1 wavefront per gathered list entry, 1 wavefront/clk/SM",
+               "t_ms": 1e3 * t_l1, "frac": 1e3 * t_l1 / t_ms, "sm_mhz": sm_mhz},
+        "definition": "B = N*52 + E*28 bytes (gathered x_j counted at HBM), F = 8E + 20P "
+                      "(E full-list entries, P in-cut entries); frac = achieved / peak = "
+                      "T_roof / T_kernel. frac > 1: the gathers are served by L1/L2; the "
+                      "binding resource is the L1 (see l1, ncu)",
+    })
+    if cap is not None:
+        roof["ncu"] = {k: cap.get(k) for k in ("dram_bytes_per_launch", "dram_frac_of_peak",
+                                               "l1tex_frac_of_peak", "fp64_pipe_frac",
+                                               "duration_ms", "source")}
+        if cap.get("dram_bytes_per_launch"):
+            roof["ncu"]["dram_gbs_live"] = cap["dram_bytes_per_launch"] / (t_ms * 1e-3) / 1e9
+    return roof
+
+
+def pinned_like(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+
 def run_ours(args) -> None:
     import torch
     from paper_2109_10876_b200 import engine as E
@@ -270,12 +502,14 @@ def run_ours(args) -> None:
     torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
 
-    w = Workload(args.config, args.cells, 1 if args.weak else 0)
-    cfg_w, n, flat = w.cfg, w.n, w.flat
+    cfg = workload_config(args.config, args.cells, args.weak, 1)
+    flat, inter, w = make_inputs_ours(args.config, args.cells, 1 if args.weak else 0)
+    n = w.n
     ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
-    eng = E.Engine(flat, w.inter, w.r_skin, ecfg)
+    eng = E.Engine(flat, inter, w.r_skin, ecfg)
 
     eng.run(args.warmup)
+    eng.prepare_graphs()  # every graph shape the timed run launches, captured now
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -293,62 +527,20 @@ def run_ours(args) -> None:
     rebuilds = eng.rebuild_count() - rebuilds0
     ms_per_step = ms / args.steps
     value = n * args.steps / (ms * 1e-3)
+    clk = clocks.summary()
 
-    # -- roofline of the force kernel -----------------------------
     st = eng.list_stats()
-    kc = eng.kernel_config()
-    E_ent, P_cut = st["entries"], st["in_cut"]
-    t_force_ms = eng.time_force_kernel(args.force_reps)
-    B = n * 52 + E_ent * 28
-    F = 8 * E_ent + 20 * P_cut
-    peaks = measured_peaks()
-    fp64 = E.fp64_peak_tflops(dev)
-    t_hbm = B / (peaks["hbm_gbs"] * 1e9)
-    t_flop = F / (fp64 * 1e12)
-    traffic = None
-    prof = ROOT / "profiles" / "force_kernel_ncu.json"
-    if prof.exists():
-        try:
-            pj = json.loads(prof.read_text())
-            if pj.get("n_particles") == n:
-                traffic = pj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    if t_hbm >= t_flop:
-        achieved = B / (t_force_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic}
-    else:
-        achieved = F / (t_force_ms * 1e-3) / 1e12
-        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
-                "frac": achieved / fp64, "traffic": traffic}
-    # The bound the kernel actually sits on: every gathered neighbour of a
-    # warp's 32 lanes lies in its own 128-B line, one L1 wavefront each, and
-    # an SM's L1 processes one wavefront per clock.
-    sm_count, clk_ghz = 148, (clocks_mhz := (clocks.summary().get("sm_mhz") or 1965.0)) / 1e3
-    t_l1 = E_ent / (sm_count * clk_ghz * 1e9)
-    roof["l1"] = {"model": "one L1 wavefront per gathered list entry, 1 wavefront/clk/SM",
-                  "t_ms": 1e3 * t_l1, "frac": 1e3 * t_l1 / t_force_ms, "sm_mhz": clocks_mhz}
-    roof.update({
-        "kernel": "k_forces_l1" if kc["lanes"] == 1 else f"k_forces_lanes<{kc['lanes']}>",
-        "algorithmic_bytes": B, "algorithmic_flops": F,
-        "entries": E_ent, "in_cut_entries": P_cut, "kernel_ms": t_force_ms,
-        "t_roof_ms": 1e3 * max(t_hbm, t_flop), "fp64_peak_tflops_measured": fp64,
-        "peak_source": peaks["source"], "share_of_step": t_force_ms / ms_per_step,
-        "definition": "B = N*52 + E*28 bytes, F = 8E + 20P (E full-list entries, P in-cut "
-                      "entries); frac = T_roof / T_kernel",
-    })
+    roof = roofline(eng, n, ms_per_step, clk.get("sm_mhz") or 1965.0, args.force_reps)
+    work_set = int(st["capacity"]) * 4 * ((n + 31) // 32 * 32) + n * 180
     eng.close()
 
     # -- e2e through the public API from host buffers ----------------------------------
     # The caller's arrays live in pinned host memory (allocated and filled
     # before the timed region, as a serving process keeps its staging
     # buffers); the upload and the final download are inside it.
-    def pinned(a):
-        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
-
-    flat_in = E.FlatConfig(flat.box, pinned(flat.id), pinned(flat.pos), pinned(flat.vel),
-                           mass=None if flat.mass is None else pinned(flat.mass),
+    flat_in = E.FlatConfig(flat.box, pinned_like(flat.id), pinned_like(flat.pos),
+                           pinned_like(flat.vel),
+                           mass=None if flat.mass is None else pinned_like(flat.mass),
                            type=flat.type, bonds=flat.bonds)
     out = E.FlatConfig(flat.box, torch.empty(n, dtype=torch.int64, pin_memory=True).numpy(),
                        torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy(),
@@ -357,7 +549,7 @@ def run_ours(args) -> None:
     h2d = flat_in.pos.nbytes + flat_in.vel.nbytes + flat_in.id.nbytes + (
         0 if flat_in.mass is None else flat_in.mass.nbytes)
     t0 = time.perf_counter()
-    e2 = E.Engine(flat_in, w.inter, w.r_skin, ecfg)
+    e2 = E.Engine(flat_in, inter, w.r_skin, ecfg)
     rows = e2.run_observed(args.steps, stride=1)  # each step's observables land in host memory
     e2.flatten(out=out)
     t_e2e = time.perf_counter() - t0
@@ -368,42 +560,46 @@ def run_ours(args) -> None:
     e2e = {"value": n * args.steps / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "seconds": t_e2e,
-           "what": "Engine(create from the caller's arrays in pinned host memory: upload, "
-                   "bin, build, first forces) + run_observed(K, stride 1): every step's "
-                   "(step, KE, PE, W) written by the device into mapped pinned host memory + "
-                   "flatten(out=pinned buffers) download"}
+           "what": "Engine(create from the caller's arrays in pinned host memory: validate, "
+                   "upload, bin, build, first forces) + run_observed(K, stride 1): every "
+                   "step's (step, KE, PE, W) written by the device into mapped pinned host "
+                   "memory + flatten(out=pinned buffers) download"}
 
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            v, cores, sample, _ = cpu_reference_run(w, args.steps, 2, args.cpu_budget_s)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": sample}
+            c = cpu_reference_run(w, args.steps, 2, args.cpu_budget_s, args.cpu1_budget_s)
+            cpu = {"value": c["value"], "unit": UNIT, "cores": c["cores"], "kind": "reference",
+                   "sample": c["sample"], "sections_s": c["sections_s"]}
+            if "one_thread" in c:
+                cpu["one_thread"] = c["one_thread"]
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
-    cfg = dict(cfg_w)
-    cfg.update({"parallelism": "single GPU",
-                "l2": "working set > 126 MB L2 (neighbour list alone ~0.4 GB); no flush",
-                "rebuilds_in_timed_region": rebuilds, "section_timers": False,
-                "nbr_capacity": st["capacity"], "cell_grid": list(st["dims"])})
+    l2 = (f"working set ~{work_set / 2 ** 30:.2f} GiB > 126 MB L2: no flush needed"
+          if work_set > 2 * L2_BYTES else
+          f"working set ~{work_set / 2 ** 20:.0f} MiB fits the 126 MB L2: steps run "
+          f"L2-warm (a production step re-reads the same state every step); no flush")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
-        "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+        "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "details": {"parallelism": "single GPU", "l2": l2,
+                    "rebuilds_in_timed_region": rebuilds, "section_timers": False,
+                    "nbr_capacity": st["capacity"], "cell_grid": list(st["dims"]),
+                    "graphs": "captured before the timed region (prepare_graphs)"},
     }
     print(json.dumps(line))
 
 
 def run_decomposed(args) -> None:
-    """N > 1: the BASELINE config on an N-slab z decomposition (decomp.py), one
-    process per GPU, NCCL point-to-point halo/migration + all-reduces
-    (strong scaling: the same 1M-particle system at every N; --weak: 2.048M
-    particles per GPU)."""
+    """N > 1: the workload on an N-slab z decomposition (decomp.py), one
+    process per GPU, the native C++ step loop: fused peer-store halo, NCCL
+    migration + all-reduces (strong scaling: the same system at every N;
+    --weak: 2.048M particles per GPU)."""
     import torch
     import torch.distributed as dist
     from paper_2109_10876_b200 import engine as E
@@ -421,8 +617,9 @@ def run_decomposed(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
     torch.cuda.set_device(dev)
-    w = Workload(args.config, args.cells, ws if args.weak else 0)  # identical on every rank
-    cfg_w, n, flat = w.cfg, w.n, w.flat
+    cfg = workload_config(args.config, args.cells, args.weak, ws)
+    flat, inter, w = make_inputs_ours(args.config, args.cells, ws if args.weak else 0)
+    n = w.n
     ecfg = E.EngineConfig(dt=w.dt, section_timers=False, device=dev)
     balance = "count" if args.config == "slab" else "static"
 
@@ -431,7 +628,7 @@ def run_decomposed(args) -> None:
     native = args.dist_backend == "nccl"
 
     def make():
-        return DecomposedEngine(flat, w.inter, w.r_skin, ecfg, comm=TorchDistComm(),
+        return DecomposedEngine(flat, inter, w.r_skin, ecfg, comm=TorchDistComm(),
                                 device_of=lambda r: local, balance=balance, native=native)
 
     def max_over_ranks(x: float) -> float:
@@ -480,13 +677,6 @@ def run_decomposed(args) -> None:
     dist.destroy_process_group()
     if rank != 0:
         return
-    cfg = dict(cfg_w)
-    cfg.update({"parallelism": f"{ws} z-slabs (spatial decomposition, {args.dist_backend} "
-                               f"halo + migration, {balance} cuts, "
-                               f"{'native C++' if native else 'python'} step loop)",
-                "l2": "working set > 126 MB L2 on every rank; no flush",
-                "rebuilds_in_timed_region": rebuilds, "section_timers": False,
-                "rank0_slab": sizes, "exchanged_bytes_rank0": xbytes})
     line = {
         "metric": METRIC, "value": n * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -496,23 +686,62 @@ def run_decomposed(args) -> None:
         "e2e": {"value": n * args.steps / t_e2e, "unit": UNIT,
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "seconds": t_e2e,
-                "what": "DecomposedEngine(create, NCCL init) + run_observed(K, stride 1): every step's rank-local (step, KE, PE, W) written by the device into mapped host memory, the table summed over ranks at the end + local_state()"},
+                "what": "DecomposedEngine(create, NCCL init) + run_observed(K, stride 1): every "
+                        "step's rank-local (step, KE, PE, W) written by the device into mapped "
+                        "host memory, the table summed over ranks at the end + local_state()"},
         "gpu_launches": launches * ws, "clocks": clocks.summary(),
+        "details": {"parallelism": f"{ws} z-slabs (spatial decomposition, {args.dist_backend} "
+                                   f"halo + migration, {balance} cuts, "
+                                   f"{'native C++' if native else 'python'} step loop)",
+                    "l2": "working set > 126 MB L2 on every rank; no flush",
+                    "rebuilds_in_timed_region": rebuilds, "section_timers": False,
+                    "rank0_slab": sizes, "exchanged_bytes_rank0": xbytes},
     }
     print(json.dumps(line))
 
 
-def main():
+def launch_check(args) -> None:
+    """CPU check of the launch path (tests/test_bench_host.py): every rank joins
+    a gloo group and all-reduces its rank; rank 0 prints the world it saw."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank + 1], dtype=torch.int64)
+        dist.all_reduce(t)
+        total = int(t.item())
+        dist.destroy_process_group()
+    else:
+        total = 1
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": ws, "gpus_flag": args.gpus,
+                          "rank_sum": total,
+                          "config": workload_config(args.config, args.cells, args.weak, ws)}))
+
+
+def make_kg_input(args) -> None:
+    """Writes the warmed-up KG melt (our engine's force-capped warm-up) for the
+    reference arm, which must not load this repo's library itself."""
+    flat, _inter, w = make_inputs_ours("kg", args.cells, 0)
+    np.savez(args.make_kg_input, box=flat.box, id=flat.id, pos=flat.pos, vel=flat.vel,
+             bonds=flat.bonds)
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cells", type=int, default=64, help="FCC cells per edge (64 = 1M)")
+    ap.add_argument("--cells", type=int, default=160,
+                    help="FCC cells per edge (160 = 16.4M configs[4], 64 = 1M configs[1], "
+                         "20 = 32K configs[0])")
     ap.add_argument("--config", choices=["lj", "kg", "slab"], default="lj",
                     help="lj: FCC LJ fluid (configs[0,1,4] by --cells 20/64/160); kg: "
-                         "Kremer-Grest melt (configs[2]); slab: liquid-vapour slab "
-                         "(configs[3])")
+                         "Kremer-Grest melt (configs[2], --cells 64); slab: liquid-vapour "
+                         "slab (configs[3], --cells 64)")
     ap.add_argument("--weak", action="store_true",
                     help="lj only: weak scaling at 2.048M particles per GPU (FCC 80^3 x 4 "
                          "per GPU; the box doubles along x, y, z with N; 8 GPUs = the "
@@ -520,16 +749,26 @@ def main():
     ap.add_argument("--force-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--cpu1-budget-s", type=float, default=10.0,
+                    help="bounded 1-thread sample of the reference (0 = skip)")
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     ap.add_argument("--decomposed", action="store_true",
                     help="run the slab decomposition even at N = 1 (under torchrun): the "
                          "single slab exchanges its halo with itself over NCCL")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="N > 1 only; gloo = pipeline check with every rank on GPU 0")
-    args = ap.parse_args()
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--make-kg-input", default=None, help=argparse.SUPPRESS)
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.make_kg_input:
+        make_kg_input(args)
+        return
+    relaunch_if_needed(args, argv)
+    if args.launch_check:
+        launch_check(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_ours(args)

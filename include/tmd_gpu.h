@@ -207,6 +207,21 @@ int tmd_gpu_list_stats(tmd_gpu_ctx* ctx, tmd_list_stats* out);
  * returns the mean milliseconds per launch. Results are left in place. */
 int tmd_gpu_time_force_kernel(tmd_gpu_ctx* ctx, int reps, double* ms_per_launch);
 
+/* Benchmark hook: the kernel a production step runs (forces + the fused
+ * velocity-Verlet epilogue: closing half-kick, next opening half-kick + drift,
+ * displacement max), `reps` launches back to back between CUDA events on the
+ * context's stream; mean milliseconds per launch. The launches advance the
+ * state, so positions and velocities are checkpointed before and restored
+ * after (list rebuilt, forces recomputed). Whole-box NVE contexts only. */
+int tmd_gpu_time_step_kernel(tmd_gpu_ctx* ctx, int reps, double* ms_per_launch);
+
+/* Captures the CUDA graphs the next run will launch (15-step blocks and
+ * single steps at the current buffer parity; obs_stride > 0: also the family
+ * tmd_gpu_run_observed(stride) launches) without running them, so that no
+ * capture falls inside a timed run. No-op with section timers or in slab
+ * mode. */
+int tmd_gpu_prepare_graphs(tmd_gpu_ctx* ctx, int64_t obs_stride);
+
 /* Benchmark hook: rebuilds the neighbour list `reps` times at the current
  * positions (no resort) between CUDA events; mean milliseconds per build. */
 int tmd_gpu_time_list_build(tmd_gpu_ctx* ctx, int reps, double* ms_per_build);

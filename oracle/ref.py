@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
         L.ref_create_ex.argtypes = [C.c_int64, P, P, P, P, P, D, D, D, C.c_int, D,
                                     C.c_int, C.c_int, D, C.POINTER(RefOpts),
                                     C.POINTER(P), C.c_char_p, C.c_int]
+        L.ref_clone.argtypes = [P, C.c_int, C.POINTER(P), C.c_char_p, C.c_int]
         L.ref_destroy.argtypes = [P]
         L.ref_destroy.restype = None
         L.ref_step.argtypes = [P, C.c_int64, C.c_char_p, C.c_int]
@@ -161,6 +162,17 @@ class RefEngine:
                              dt, C.byref(o), C.byref(h), err, 512)
         _raise(rc, err)
         self._h = h
+
+    def clone(self, workers: int) -> "RefEngine":
+        """A second reference Engine over a copy of this one's Domain with
+        `workers` worker threads (ref_clone: Engine(Domain, EngineConfig),
+        engine.hpp:68-77; the same subnode layout)."""
+        err = C.create_string_buffer(512)
+        h = C.c_void_p()
+        _raise(lib().ref_clone(self._h, int(workers), C.byref(h), err, 512), err)
+        c = RefEngine.__new__(RefEngine)
+        c._ids, c._n, c._bonds, c._h = self._ids, self._n, getattr(self, "_bonds", None), h
+        return c
 
     def close(self):
         if getattr(self, "_h", None):

@@ -176,6 +176,20 @@ int ref_create_ex(std::int64_t n, const std::int64_t* id, const double* mass,
 
 void ref_destroy(ref_engine* h) { delete h; }
 
+// Engine::Engine(Domain, EngineConfig) (engine.hpp:68-77) over a copy of h's
+// Domain with another worker count (the same subnode layout): the CPU
+// baseline's 1-thread rate without a second build_domain.
+int ref_clone(ref_engine* h, int workers, ref_engine** out, char* err, int errlen) {
+  *out = nullptr;
+  return guarded(err, errlen, [&] {
+    EngineConfig cfg = h->eng->config();
+    cfg.worker_threads = workers;
+    auto c = std::make_unique<ref_engine>();
+    c->eng = std::make_unique<Engine>(Domain(h->eng->domain()), cfg);
+    *out = c.release();
+  });
+}
+
 // Engine::run (engine.hpp:128).
 int ref_step(ref_engine* h, std::int64_t nsteps, char* err, int errlen) {
   return guarded(err, errlen, [&] { h->eng->run(nsteps); });

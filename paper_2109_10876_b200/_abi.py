@@ -39,6 +39,7 @@ EXPORTS = [
     "tmd_gen_spherical", "tmd_gen_random", "tmd_gpu_run_observed", "tmd_nccl_unique_id",
     "tmd_gpu_slab_attach_nccl", "tmd_gpu_slab_setup", "tmd_gpu_slab_run",
     "tmd_gpu_slab_observe", "tmd_balanced_cuts", "tmd_gpu_release_cache",
+    "tmd_gpu_time_step_kernel", "tmd_gpu_prepare_graphs",
 ]
 
 
@@ -152,6 +153,8 @@ def lib() -> C.CDLL:
     L.tmd_gpu_size.restype = C.c_int64
     L.tmd_gpu_list_stats.argtypes = [P, C.POINTER(TmdListStats)]
     L.tmd_gpu_time_force_kernel.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
+    L.tmd_gpu_time_step_kernel.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
+    L.tmd_gpu_prepare_graphs.argtypes = [P, C.c_int64]
     L.tmd_gpu_time_list_build.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_stream.argtypes = [P]
     L.tmd_gpu_stream.restype = P

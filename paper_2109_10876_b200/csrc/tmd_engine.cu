@@ -2345,6 +2345,83 @@ int tmd_gpu_time_force_kernel(tmd_gpu_ctx* c, int reps, double* ms) {
   });
 }
 
+// The kernel a production step runs: forces + the fused velocity-Verlet
+// epilogue (kFused: closing half-kick, next opening half-kick + drift into
+// the other position buffer, displacement max). Each launch advances the
+// state by one step without rebuild checks, so the state is checkpointed
+// first and restored afterwards (positions, velocities; the list is rebuilt
+// and the forces recomputed at the restored positions, as after a rollback).
+int tmd_gpu_time_step_kernel(tmd_gpu_ctx* c, int reps, double* ms) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (reps < 1) throw StatusError{TMD_ERR_CONFIG, "reps must be >= 1"};
+    if (c->nranks > 1 || c->g.zslab) {
+      throw StatusError{TMD_ERR_STATE, "step-kernel timing needs a whole-box context"};
+    }
+    if (c->th.on) {  // the restored forces would need the checkpoint's Langevin kick
+      throw StatusError{TMD_ERR_CONFIG, "step-kernel timing needs an NVE context"};
+    }
+    sync_ctrl(c);
+    const Ctrl before = *c->h_ctrl;
+    checkpoint(c);
+    launch_forces(c, kForcesOnly);  // warm (same list, same positions)
+    ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    for (int r = 0; r < reps; ++r) launch_forces(c, kFused);
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+    float t = 0.f;
+    ck(cudaEventElapsedTime(&t, c->t0, c->t1), "cudaEventElapsedTime");
+    ck(cudaGetLastError(), "kernel launch");
+    *ms = static_cast<double>(t) / reps;
+    restore(c, before);
+    c->ck_valid = false;
+    setup_pass(c);
+    enqueue_observables(c);
+    sync_ctrl(c);
+  });
+}
+
+// Captures the CUDA graphs a run will launch (blocks of kGraphSteps and
+// single steps at the current buffer parity; with obs_stride > 0 the
+// observed family as run_observed(stride) launches it), so that no capture
+// falls inside a later timed run.
+int tmd_gpu_prepare_graphs(tmd_gpu_ctx* c, int64_t obs_stride) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (!c->use_graphs || c->timers_on || c->nranks > 1 || c->g.zslab) return;
+    if (c->graph_dirty) drop_graphs(c);
+    for (int kind = 0; kind < 2; ++kind) {
+      auto& sgr = c->sg[kind][c->cur];
+      if (!sgr.exec) capture_graph(c, kind == 0 ? kGraphSteps : 1, sgr);
+    }
+    if (obs_stride > 0) {
+      const int stride = static_cast<int>(std::min<int64_t>(obs_stride, 1 << 30));
+      if (c->sgo_stride != stride) {
+        for (auto& row : c->sgo) {
+          for (auto& sg : row) {
+            if (sg.exec) cudaGraphExecDestroy(sg.exec);
+            if (sg.graph) cudaGraphDestroy(sg.graph);
+            sg = tmd_gpu_ctx::StepGraph{};
+          }
+        }
+        c->sgo_stride = stride;
+      }
+      const int keep = c->obs_stride;
+      c->obs_stride = stride;
+      try {
+        for (int kind = 0; kind < 2; ++kind) {
+          auto& sgr = c->sgo[kind][c->cur];
+          if (!sgr.exec) capture_graph(c, kind == 0 ? kGraphSteps : 1, sgr);
+        }
+      } catch (...) {
+        c->obs_stride = keep;
+        throw;
+      }
+      c->obs_stride = keep;
+    }
+  });
+}
+
 int tmd_gpu_time_list_build(tmd_gpu_ctx* c, int reps, double* ms) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");

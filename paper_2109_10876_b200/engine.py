@@ -450,6 +450,18 @@ class Engine:
         _check(_abi.lib().tmd_gpu_time_list_build(self._h, int(reps), C.byref(ms)), self._h)
         return ms.value
 
+    def time_step_kernel(self, reps: int) -> float:
+        """Mean ms per launch of the production step kernel (forces + fused
+        velocity-Verlet epilogue); the state is restored afterwards."""
+        ms = C.c_double()
+        _check(_abi.lib().tmd_gpu_time_step_kernel(self._h, int(reps), C.byref(ms)),
+               self._h)
+        return ms.value
+
+    def prepare_graphs(self, obs_stride: int = 0) -> None:
+        """Capture the CUDA graphs the next run(s) will launch (no steps run)."""
+        _check(_abi.lib().tmd_gpu_prepare_graphs(self._h, int(obs_stride)), self._h)
+
     def time_force_kernel(self, reps: int) -> float:
         ms = C.c_double()
         _check(_abi.lib().tmd_gpu_time_force_kernel(self._h, int(reps), C.byref(ms)),

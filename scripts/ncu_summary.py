@@ -83,6 +83,51 @@ def launches(path):
               f"{sum(v)/tot:6.1%}{extra}")
 
 
+def record(rep, n_particles, kernel, out_json):
+    """The step-kernel record bench.py reads (profiles/force_kernel_ncu.json):
+    per-launch DRAM bytes and the DRAM / L1TEX / FP64-pipe fractions of the
+    first captured launch in `rep`."""
+    import json
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    h, units, row = r[0], r[1], r[2]
+    d = dict(zip(h, row))
+    u = dict(zip(h, units))
+
+    def num(k, scale_units=None):
+        v = float(d[k].replace(",", ""))
+        if scale_units:
+            v *= scale_units.get(u.get(k, ""), 1.0)
+        return v
+    b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    t = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
+    rec = {"kernel": kernel, "n_particles": int(n_particles),
+           "ncu_kernel_name": d.get("Kernel Name", "")[:120],
+           "dram_bytes_per_launch": num("dram__bytes_read.sum", b) + num("dram__bytes_write.sum", b),
+           "dram_read_bytes": num("dram__bytes_read.sum", b),
+           "dram_write_bytes": num("dram__bytes_write.sum", b),
+           "duration_ms": num("gpu__time_duration.sum", t),
+           "dram_frac_of_peak": num("dram__throughput.avg.pct_of_peak_sustained_elapsed") / 100,
+           "l1tex_frac_of_peak": num("l1tex__throughput.avg.pct_of_peak_sustained_active") / 100,
+           "fp64_pipe_frac": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") / 100,
+           "issue_active_frac": num("smsp__issue_active.avg.pct_of_peak_sustained_active") / 100,
+           "registers": int(num("launch__registers_per_thread")),
+           "source": f"ncu --set full --clock-control none ({rep.split('/')[-1]})"}
+    try:
+        old = json.load(open(out_json))
+        old = old if isinstance(old, list) else [old]
+    except (OSError, ValueError):
+        old = []
+    old = [o for o in old if not (o.get("n_particles") == rec["n_particles"]
+                                  and o.get("kernel") == kernel)]
+    json.dump(old + [rec], open(out_json, "w"), indent=1)
+    print(json.dumps(rec, indent=1))
+
+
 if __name__ == "__main__":
     mode, arg = sys.argv[1], sys.argv[2]
-    {"raw": raw, "stalls": stalls, "launches": launches}[mode](arg)
+    if mode == "record":
+        record(arg, *sys.argv[3:6])
+    else:
+        {"raw": raw, "stalls": stalls, "launches": launches}[mode](arg)

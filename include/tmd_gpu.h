@@ -301,6 +301,21 @@ int tmd_gpu_slab_info(tmd_gpu_ctx* ctx, int64_t info[11]);
  * NCCL point-to-point. tmd_gpu_slab_observe all-reduces PE, W, KE. */
 int tmd_nccl_unique_id(void* id);
 int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id, int flags);
+/* The same loop with every rank's context in ONE process, one host thread per
+ * rank (R slabs on one GPU, or several GPUs of one process): a collective is a
+ * rendezvous of the rank threads exchanging stream events and device
+ * pointers, after which each rank's stream copies / reduces its peers'
+ * buffers — stream-ordered like NCCL, no kernel waits on another rank's
+ * kernel. Create one group per decomposition, attach each rank's context
+ * (flags as above), then call tmd_gpu_slab_setup / _run / _run_observed /
+ * _observe on every rank concurrently from its own thread. A rank that fails
+ * releases the others (they fail with "a peer rank failed"). The group may be
+ * destroyed once every context is attached (contexts hold a reference).
+ * Replaces the reference's in-process subnode decomposition driven by its
+ * TaskPool (decomp.hpp:47-224, task_pool.hpp:15-106). */
+int tmd_local_group_create(int nranks, void** group);
+void tmd_local_group_destroy(void* group);
+int tmd_gpu_slab_attach_local(tmd_gpu_ctx* ctx, void* group, int flags);
 int tmd_gpu_slab_setup(tmd_gpu_ctx* ctx);
 int tmd_gpu_slab_run(tmd_gpu_ctx* ctx, int64_t nsteps);
 /* tmd_gpu_slab_run recording every `stride`-th step's observables as the
@@ -363,7 +378,8 @@ int tmd_gpu_slab_ghost_in(tmd_gpu_ctx* ctx, int64_t n_lo, int64_t n_hi, void* lo
  * overflow). */
 int tmd_gpu_slab_ghosts_ready(tmd_gpu_ctx* ctx);
 
-/* Opening half-kick + drift of the owned particles (integrate.hpp:14-37). */
+/* Opening half-kick + drift of the owned particles (Engine::half_kick_and_drift,
+ * engine.hpp:174-189). */
 int tmd_gpu_slab_kick_drift(tmd_gpu_ctx* ctx);
 
 /* Forces on the owned particles; mode 0 forces only, 1 + closing half-kick,

@@ -40,6 +40,7 @@ EXPORTS = [
     "tmd_gpu_slab_attach_nccl", "tmd_gpu_slab_setup", "tmd_gpu_slab_run",
     "tmd_gpu_slab_observe", "tmd_balanced_cuts", "tmd_gpu_release_cache",
     "tmd_gpu_time_step_kernel", "tmd_gpu_prepare_graphs",
+    "tmd_local_group_create", "tmd_local_group_destroy", "tmd_gpu_slab_attach_local",
 ]
 
 
@@ -126,6 +127,10 @@ def lib() -> C.CDLL:
     L.tmd_nccl_unique_id.argtypes = [P]
     L.tmd_balanced_cuts.argtypes = [P, C.c_int, C.c_int, P]
     L.tmd_gpu_slab_attach_nccl.argtypes = [P, P, C.c_int]
+    L.tmd_local_group_create.argtypes = [C.c_int, PP]
+    L.tmd_local_group_destroy.argtypes = [P]
+    L.tmd_local_group_destroy.restype = None
+    L.tmd_gpu_slab_attach_local.argtypes = [P, P, C.c_int]
     L.tmd_gpu_slab_setup.argtypes = [P]
     L.tmd_gpu_slab_run.argtypes = [P, C.c_int64]
     L.tmd_gpu_slab_observe.argtypes = [P, C.c_int64, C.POINTER(TmdObservables)]

@@ -1,0 +1,298 @@
+// Transport of the native slab loop (tmd_slab_nccl.cuh): the collectives and
+// point-to-point messages of the z-slab decomposition behind one small
+// interface, stream-ordered like NCCL (nothing in a step waits for the host).
+//
+//   NcclComm   one process (or thread) per GPU, NCCL on the context stream.
+//   LocalComm  every rank's context in one process, one host thread per rank
+//              (R slabs on one GPU, or several GPUs of one process): a
+//              collective is a host rendezvous of the rank threads that
+//              publishes stream events and device pointers; each rank's stream
+//              then waits on its peers' events and copies / reduces their
+//              buffers on its own stream, and every rank's later work waits
+//              until all copies out of its buffers ran. No kernel ever waits
+//              on another rank's kernel — only on events of finished work.
+//
+// Point-to-point messages of a group between a pair of ranks match in
+// posting order (NCCL's rule); LocalComm also checks sizes and that every
+// message was matched, which turns a protocol bug into an error instead of a
+// hang.
+#pragma once
+
+#include <condition_variable>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#ifndef TMD_NO_NCCL
+#include <nccl.h>
+#endif
+
+namespace {
+
+enum class CType { kI32, kI64, kU64, kF64 };
+enum class COp { kSum, kMax };
+
+inline size_t ctype_bytes(CType t) { return t == CType::kI32 ? 4 : 8; }
+
+struct SlabComm {
+  virtual ~SlabComm() = default;
+  // in place over `count` elements of every rank's buf
+  virtual void allreduce(void* buf, size_t count, CType t, COp op, cudaStream_t s) = 0;
+  // recv[q * bytes, (q + 1) * bytes) = rank q's send (send and recv disjoint)
+  virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  virtual void group_start() = 0;
+  virtual void send(const void* buf, size_t bytes, int peer, cudaStream_t s) = 0;
+  virtual void recv(void* buf, size_t bytes, int peer, cudaStream_t s) = 0;
+  virtual void group_end(cudaStream_t s) = 0;
+  virtual void abort() {}  // a rank failed: release peers blocked in a collective
+  virtual bool in_process() const = 0;  // every rank's buffers are this process's pointers
+};
+
+#ifndef TMD_NO_NCCL
+inline void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    throw CudaFail{std::string(what) + ": " + ncclGetErrorString(r)};
+  }
+}
+
+struct NcclComm final : SlabComm {
+  ncclComm_t nc = nullptr;
+  ~NcclComm() override {
+    if (nc) ncclCommDestroy(nc);
+  }
+  static ncclDataType_t dt(CType t) {
+    switch (t) {
+      case CType::kI32: return ncclInt32;
+      case CType::kI64: return ncclInt64;
+      case CType::kU64: return ncclUint64;
+      default: return ncclFloat64;
+    }
+  }
+  void allreduce(void* buf, size_t count, CType t, COp op, cudaStream_t s) override {
+    nck(ncclAllReduce(buf, buf, count, dt(t), op == COp::kSum ? ncclSum : ncclMax, nc, s),
+        "ncclAllReduce");
+  }
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    nck(ncclAllGather(send, recv, bytes, ncclUint8, nc, s), "ncclAllGather");
+  }
+  void group_start() override { nck(ncclGroupStart(), "ncclGroupStart"); }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t s) override {
+    nck(ncclSend(buf, bytes, ncclUint8, peer, nc, s), "ncclSend");
+  }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t s) override {
+    nck(ncclRecv(buf, bytes, ncclUint8, peer, nc, s), "ncclRecv");
+  }
+  void group_end(cudaStream_t) override { nck(ncclGroupEnd(), "ncclGroupEnd"); }
+  bool in_process() const override { return false; }
+};
+#endif
+
+// ---- in-process transport -----------------------------------------------------
+
+// Shared by the R rank threads of one decomposition (reference-counted: the
+// creator's handle plus one per attached context).
+struct LocalGroup {
+  explicit LocalGroup(int nranks) : R(nranks), slot(static_cast<size_t>(nranks)) {}
+  const int R;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool aborted = false;
+  std::vector<char> taken = std::vector<char>(static_cast<size_t>(R), 0);
+  struct Msg {
+    int peer;
+    const void* p;
+    size_t bytes;
+  };
+  struct Slot {
+    cudaEvent_t ready = nullptr, done = nullptr;  // created by the owning rank
+    const void* src = nullptr;                     // all-gather / all-reduce source
+    std::vector<Msg> sends;                        // this group's sends, in posting order
+  };
+  std::vector<Slot> slot;
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) throw CudaFail{"slab loop: a peer rank failed"};
+    const uint64_t g = gen;
+    if (++arrived == R) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    cv.wait(lk, [&] { return gen != g || aborted; });
+    if (gen == g) throw CudaFail{"slab loop: a peer rank failed"};
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+template <class T>
+__global__ void k_local_reduce(const T* __restrict__ g, int R, size_t count, int op,
+                               T* __restrict__ out) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= count) return;
+  T acc = g[i];
+  for (int q = 1; q < R; ++q) {  // fixed rank order: deterministic sums
+    const T v = g[static_cast<size_t>(q) * count + i];
+    acc = op == 0 ? acc + v : (v > acc ? v : acc);
+  }
+  out[i] = acc;
+}
+
+struct LocalComm final : SlabComm {
+  std::shared_ptr<LocalGroup> grp;
+  int r = 0;
+  char* stage = nullptr;   // this rank's copy of an all-reduce input
+  char* gather = nullptr;  // every rank's copy, rank-major
+  size_t cap = 0;          // bytes per rank of stage / gather
+  std::vector<LocalGroup::Msg> recvs;
+
+  LocalComm(std::shared_ptr<LocalGroup> g, int rank) : grp(std::move(g)), r(rank) {
+    auto& me = grp->slot[static_cast<size_t>(r)];
+    ck(cudaEventCreateWithFlags(&me.ready, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&me.done, cudaEventDisableTiming), "cudaEventCreate");
+    reserve(4096);
+  }
+  ~LocalComm() override {
+    auto& me = grp->slot[static_cast<size_t>(r)];
+    if (me.ready) cudaEventDestroy(me.ready);
+    if (me.done) cudaEventDestroy(me.done);
+    me.ready = me.done = nullptr;
+    std::lock_guard<std::mutex> lk(grp->mu);
+    grp->taken[static_cast<size_t>(r)] = 0;
+    cudaFree(stage);
+    cudaFree(gather);
+  }
+  void reserve(size_t bytes) {
+    if (bytes <= cap) return;
+    ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");  // no peer still reads the old stage
+    cudaFree(stage);
+    cudaFree(gather);
+    cap = std::max<size_t>(bytes, 2 * cap);
+    void* a = nullptr;
+    void* b = nullptr;
+    ck(cudaMalloc(&a, cap), "cudaMalloc(stage)");
+    ck(cudaMalloc(&b, cap * static_cast<size_t>(grp->R)), "cudaMalloc(gather)");
+    stage = static_cast<char*>(a);
+    gather = static_cast<char*>(b);
+  }
+  LocalGroup::Slot& slot(int q) { return grp->slot[static_cast<size_t>(q)]; }
+  void wait_all(cudaStream_t s, bool ready) {
+    for (int q = 0; q < grp->R; ++q) {
+      ck(cudaStreamWaitEvent(s, ready ? slot(q).ready : slot(q).done, 0), "cudaStreamWaitEvent");
+    }
+  }
+  // publish (sources ready) -> rendezvous -> copy in -> rendezvous -> later
+  // work on this stream waits until every rank's copies out of this rank's
+  // buffers ran
+  template <class F>
+  void exchange(cudaStream_t s, F&& copy_in) {
+    ck(cudaEventRecord(slot(r).ready, s), "cudaEventRecord");
+    grp->barrier();
+    wait_all(s, true);
+    copy_in();
+    ck(cudaEventRecord(slot(r).done, s), "cudaEventRecord");
+    grp->barrier();
+    wait_all(s, false);
+  }
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    slot(r).src = send;
+    exchange(s, [&] {
+      for (int q = 0; q < grp->R; ++q) {
+        ck(cudaMemcpyAsync(static_cast<char*>(recv) + static_cast<size_t>(q) * bytes, slot(q).src,
+                           bytes, cudaMemcpyDefault, s), "allgather copy");
+      }
+    });
+  }
+  void allreduce(void* buf, size_t count, CType t, COp op, cudaStream_t s) override {
+    const size_t bytes = count * ctype_bytes(t);
+    reserve(bytes);
+    ck(cudaMemcpyAsync(stage, buf, bytes, cudaMemcpyDeviceToDevice, s), "allreduce stage");
+    slot(r).src = stage;
+    exchange(s, [&] {
+      for (int q = 0; q < grp->R; ++q) {
+        ck(cudaMemcpyAsync(gather + static_cast<size_t>(q) * bytes, slot(q).src, bytes,
+                           cudaMemcpyDefault, s), "allreduce gather");
+      }
+      const int blocks = static_cast<int>((count + 255) / 256);
+      const int o = op == COp::kSum ? 0 : 1;
+      if (blocks == 0) return;
+      switch (t) {
+        case CType::kI32:
+          k_local_reduce<int><<<blocks, 256, 0, s>>>(reinterpret_cast<const int*>(gather), grp->R,
+                                                     count, o, static_cast<int*>(buf));
+          break;
+        case CType::kI64:
+          k_local_reduce<long long><<<blocks, 256, 0, s>>>(
+              reinterpret_cast<const long long*>(gather), grp->R, count, o,
+              static_cast<long long*>(buf));
+          break;
+        case CType::kU64:
+          k_local_reduce<unsigned long long><<<blocks, 256, 0, s>>>(
+              reinterpret_cast<const unsigned long long*>(gather), grp->R, count, o,
+              static_cast<unsigned long long*>(buf));
+          break;
+        default:
+          k_local_reduce<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(gather),
+                                                        grp->R, count, o, static_cast<double*>(buf));
+      }
+      ck(cudaGetLastError(), "k_local_reduce");
+    });
+  }
+  void group_start() override {
+    slot(r).sends.clear();
+    recvs.clear();
+  }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t) override {
+    slot(r).sends.push_back({peer, buf, bytes});
+  }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t) override {
+    recvs.push_back({peer, buf, bytes});
+  }
+  void group_end(cudaStream_t s) override {
+    std::string err;
+    exchange(s, [&] {
+      // the k-th receive from q takes q's k-th send to this rank
+      std::vector<size_t> next(static_cast<size_t>(grp->R), 0);
+      for (const auto& m : recvs) {
+        const auto& theirs = slot(m.peer).sends;
+        size_t& k = next[static_cast<size_t>(m.peer)];
+        while (k < theirs.size() && theirs[k].peer != r) ++k;
+        if (k == theirs.size()) {
+          err = "receive from rank " + std::to_string(m.peer) + " has no matching send";
+          return;
+        }
+        if (theirs[k].bytes != m.bytes) {
+          err = "message size mismatch from rank " + std::to_string(m.peer) + ": " +
+                std::to_string(theirs[k].bytes) + " vs " + std::to_string(m.bytes) + " bytes";
+          return;
+        }
+        ck(cudaMemcpyAsync(const_cast<void*>(m.p), theirs[k].p, m.bytes, cudaMemcpyDefault, s),
+           "p2p copy");
+        ++k;
+      }
+      for (int q = 0; q < grp->R; ++q) {  // every send to this rank was received
+        const auto& theirs = slot(q).sends;
+        for (size_t k = next[static_cast<size_t>(q)]; k < theirs.size(); ++k) {
+          if (theirs[k].peer == r) {
+            err = "unmatched send from rank " + std::to_string(q);
+            return;
+          }
+        }
+      }
+    });
+    // (raised after the second rendezvous, so no peer is left waiting in it)
+    if (!err.empty()) throw CudaFail{"slab loop: " + err};
+  }
+  void abort() override { grp->abort(); }
+  bool in_process() const override { return true; }
+};
+
+}  // namespace

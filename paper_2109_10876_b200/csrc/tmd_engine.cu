@@ -264,7 +264,7 @@ struct tmd_gpu_ctx {
   int* boff[2] = {nullptr, nullptr};
   int64_t nb[2] = {0, 0};
   int* gcnt[2] = {nullptr, nullptr};            // received ghost-layer counts (lo, hi)
-  void* nccl = nullptr;          // ncclComm_t of the native slab loop (tmd_slab_nccl.cuh)
+  void* comm = nullptr;          // SlabComm* of the native slab loop (tmd_comm.cuh): NCCL or in-process
   bool balance_count = false;    // native loop: load-aware cut planes at rebuilds
   bool fused_halo = false;       // native loop: positions to the neighbours from the epilogue
   bool fused_ready = false;      // remote ghost addresses valid for the current layout
@@ -356,11 +356,11 @@ void drop_graphs(tmd_gpu_ctx* c) {
   c->graph_dirty = false;
 }
 
-void free_nccl(tmd_gpu_ctx* c);
+void free_comm(tmd_gpu_ctx* c);
 
 void free_all(tmd_gpu_ctx* c) {
   drop_graphs(c);
-  free_nccl(c);
+  free_comm(c);
   if (c->side) cudaStreamDestroy(c->side);
   void* ptrs[] = {c->posb[0], c->posb[1], c->pos2, c->snap, c->vx, c->vy, c->vz,
                   c->vx2,  c->vy2,   c->vz2,  c->fx,    c->fy,      c->fz,
@@ -2943,12 +2943,10 @@ void tmd_gpu_destroy(tmd_gpu_ctx* c) {
 #include "tmd_slab_nccl.cuh"
 
 namespace {
-void free_nccl(tmd_gpu_ctx* c) {
+void free_comm(tmd_gpu_ctx* c) {
   for (auto& e : c->ipc_open) cudaIpcCloseMemHandle(e.second);
   c->ipc_open.clear();
-#ifndef TMD_NO_NCCL
-  if (c->nccl) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl));
-#endif
-  c->nccl = nullptr;
+  delete comm(c);
+  c->comm = nullptr;
 }
 }  // namespace

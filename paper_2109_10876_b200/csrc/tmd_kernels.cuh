@@ -606,8 +606,11 @@ __global__ void __launch_bounds__(kBlock)
                 double4* __restrict__ pos, double* __restrict__ vx,
                 double* __restrict__ vy, double* __restrict__ vz,
                 double* __restrict__ mass, long long* __restrict__ id,
-                int* __restrict__ cell, Ctrl* ctrl) {
-  if (!ctrl->rebuild) return;
+                int* __restrict__ cell, const Ctrl* ctrl) {
+  // ctrl: gated on this step's rebuild decision (the resort); nullptr:
+  // unconditional (the native slab rebuild's stayer copy). cell: nullptr
+  // skips the cell column (recomputed by the resort that follows).
+  if (ctrl && !ctrl->rebuild) return;
   const int k = blockIdx.x * kBlock + threadIdx.x;
   if (k >= n) return;
   pos[k] = pos2[k];
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(kBlock)
   vz[k] = vz2[k];
   mass[k] = mass2[k];
   id[k] = id2[k];
-  cell[k] = cell2[k];
+  if (cell) cell[k] = cell2[k];
 }
 
 // ---------------------------------------------------------------------------

@@ -1,31 +1,44 @@
 // Native multi-GPU step loop of the z-slab decomposition: the
-// protocol of paper_2109_10876_b200/decomp.py, driven from C++ with NCCL on
-// the context's stream, one process (or thread) per GPU. Included at the end
-// of tmd_engine.cu (it drives the tmd_gpu_slab_* entry points and the
+// protocol of paper_2109_10876_b200/decomp.py, driven from C++ with its
+// collectives on the context's stream, one host thread per slab. Included at
+// the end of tmd_engine.cu (it drives the tmd_gpu_slab_* entry points and the
 // context internals).
 //
-// Per step (no rebuild): fused force + integrator kernel, boundary-layer pack,
-// one NCCL group of point-to-point sends/receives of 32-B positions into the
-// neighbours' ghost slots, an in-place MAX all-reduce of the displacement
-// word, one 8-byte device-to-host read for the host's rebuild decision. The
-// rebuild (every ~8 steps) runs the migration / border / ghost protocol with
-// its few host round trips.
+// Transport (`SlabComm`): every collective and point-to-point message of the
+// loop goes through one small interface with two implementations:
+//   * NcclComm — one process (or thread) per GPU, NCCL on the context stream;
+//   * LocalComm — every rank's context in one process, one host thread per
+//     rank: a collective is a host rendezvous of the rank threads that
+//     exchanges stream events and device pointers, after which each rank's
+//     stream waits on its peers' events and copies / reduces their buffers.
+//     Stream-ordered like NCCL (nothing waits for the host), so the same C++
+//     loop — fused peer-store halo, speculative batches, the rebuild
+//     protocol — runs with R slabs on one GPU, and no kernel ever waits on
+//     another rank's kernel (only on events of finished work).
 //
-// Message order. NCCL matches the point-to-point operations of a group
-// between a pair of ranks in posting order, so both ends post, per peer: the
-// message for the receiver's LOWER ghost layer first (the sender's highest
-// layer), then the one for its UPPER ghost layer (the sender's lowest layer),
-// each as counts, ids, positions. With one or two slabs the lower and upper
-// neighbour are the same rank and the order still agrees.
+// Per step (no rebuild): fused force + integrator kernel (whose epilogue
+// stores boundary particles' new positions into the neighbours' ghost slots,
+// or a pack + one group of point-to-point messages), an in-place MAX
+// all-reduce of the displacement word, the on-device decision. The rebuild
+// (every ~8 steps) runs the migration / border / ghost protocol with its few
+// host round trips.
+//
+// Message order. Point-to-point operations of a group between a pair of
+// ranks match in posting order (NCCL's rule; LocalComm checks it and the
+// sizes), so both ends post, per peer: the message for the receiver's LOWER
+// ghost layer first (the sender's highest layer), then the one for its UPPER
+// ghost layer (the sender's lowest layer), each as counts, ids, positions.
+// With one or two slabs the lower and upper neighbour are the same rank and
+// the order still agrees.
 #pragma once
 
 #include <unistd.h>
 
-#ifndef TMD_NO_NCCL
-#include <nccl.h>
-#endif
+#include "tmd_comm.cuh"
 
 namespace {
+
+SlabComm* comm(const tmd_gpu_ctx* c) { return static_cast<SlabComm*>(c->comm); }
 
 // Contiguous cut planes over the z layers minimising the largest slab
 // population, every slab >= 1 layer (decomp.py balanced_cuts: binary search
@@ -80,14 +93,6 @@ int64_t max_load(const std::vector<int64_t>& cnt, const std::vector<int>& cuts) 
   return m;
 }
 
-#ifndef TMD_NO_NCCL
-void nck(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) {
-    throw CudaFail{std::string(what) + ": " + ncclGetErrorString(r)};
-  }
-}
-
-ncclComm_t cm(const tmd_gpu_ctx* c) { return static_cast<ncclComm_t>(c->nccl); }
 
 void rck(tmd_gpu_ctx* c, int rc) {  // a tmd_gpu_slab_* call inside the native loop
   if (rc != TMD_OK) throw StatusError{rc, c->err};
@@ -107,27 +112,22 @@ void nccl_ghost_exchange(tmd_gpu_ctx* c, bool positions_only) {
   long long* gh_id = c->id + c->n + c->n_ghost_lo;
   double4* gl_pos = pos + c->n;
   double4* gh_pos = pos + c->n + c->n_ghost_lo;
+  SlabComm* cm = comm(c);
   auto send3 = [&](int side, int peer) {
     if (!positions_only) {
-      nck(ncclSend(c->bcnt[side], dxy, ncclInt32, peer, cm(c), c->stream), "ncclSend");
-      if (c->nb[side]) {
-        nck(ncclSend(c->bids[side], c->nb[side], ncclInt64, peer, cm(c), c->stream),
-            "ncclSend");
-      }
+      cm->send(c->bcnt[side], dxy * sizeof(int), peer, c->stream);
+      if (c->nb[side]) cm->send(c->bids[side], c->nb[side] * sizeof(long long), peer, c->stream);
     }
-    if (c->nb[side]) {
-      nck(ncclSend(c->bpos[side], 4 * c->nb[side], ncclFloat64, peer, cm(c), c->stream),
-          "ncclSend");
-    }
+    if (c->nb[side]) cm->send(c->bpos[side], c->nb[side] * sizeof(double4), peer, c->stream);
   };
   auto recv3 = [&](int* cnt, long long* ids, double4* p, int64_t n, int peer) {
     if (!positions_only) {
-      nck(ncclRecv(cnt, dxy, ncclInt32, peer, cm(c), c->stream), "ncclRecv");
-      if (n) nck(ncclRecv(ids, n, ncclInt64, peer, cm(c), c->stream), "ncclRecv");
+      cm->recv(cnt, dxy * sizeof(int), peer, c->stream);
+      if (n) cm->recv(ids, n * sizeof(long long), peer, c->stream);
     }
-    if (n) nck(ncclRecv(p, 4 * n, ncclFloat64, peer, cm(c), c->stream), "ncclRecv");
+    if (n) cm->recv(p, n * sizeof(double4), peer, c->stream);
   };
-  nck(ncclGroupStart(), "ncclGroupStart");
+  cm->group_start();
   // to hi: its lower ghost (my side 1); to lo: its upper ghost (my side 0) —
   // when hi == lo the lower-ghost message goes first, as the receiver expects
   send3(1, hi);
@@ -135,7 +135,7 @@ void nccl_ghost_exchange(tmd_gpu_ctx* c, bool positions_only) {
   // from lo: my lower ghost; from hi: my upper ghost (lower first per peer)
   recv3(gl_cnt, gl_id, gl_pos, c->n_ghost_lo, lo);
   recv3(gh_cnt, gh_id, gh_pos, c->n_ghost_hi, hi);
-  nck(ncclGroupEnd(), "ncclGroupEnd");
+  cm->group_end(c->stream);
 }
 
 // Load-aware cut planes (row f3) before a migration: per-layer counts summed
@@ -148,7 +148,7 @@ void nccl_rebalance(tmd_gpu_ctx* c) {
   int64_t* d = dalloc<int64_t>(static_cast<size_t>(dz));
   ck(cudaMemcpyAsync(d, cnt.data(), sizeof(int64_t) * dz, cudaMemcpyHostToDevice, c->stream),
      "H2D layer counts");
-  nck(ncclAllReduce(d, d, dz, ncclInt64, ncclSum, cm(c), c->stream), "ncclAllReduce(sum)");
+  comm(c)->allreduce(d, static_cast<size_t>(dz), CType::kI64, COp::kSum, c->stream);
   ck(cudaMemcpyAsync(cnt.data(), d, sizeof(int64_t) * dz, cudaMemcpyDeviceToHost, c->stream),
      "D2H layer counts");
   ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
@@ -175,11 +175,20 @@ struct PeerInfo {
   long long pid;
   long long ghost_lo_off, ghost_hi_off;
   long long gen;  // the rank's ipc_gen (buffer reallocations so far)
+  long long device;
 };
 
 double4* peer_buffer(tmd_gpu_ctx* c, const PeerInfo& p, int peer, int b) {
   if (peer == c->my_rank) return c->posb[b];
-  if (p.pid == static_cast<long long>(getpid())) {
+  if (p.pid == static_cast<long long>(getpid())) {  // in-process group: plain pointers
+    if (p.device != c->device) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(static_cast<int>(p.device), 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else {
+        ck(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
     return reinterpret_cast<double4*>(p.base[b]);
   }
   std::array<char, 64> key;
@@ -205,15 +214,21 @@ void nccl_publish_ghosts(tmd_gpu_ctx* c) {
   me.ghost_lo_off = c->n;
   me.ghost_hi_off = c->n + c->n_ghost_lo;
   me.gen = c->ipc_gen;
+  me.device = c->device;
   const size_t sz = sizeof(PeerInfo);
   char* d = dalloc<char>(sz * (static_cast<size_t>(R) + 1));
   ck(cudaMemcpyAsync(d, &me, sz, cudaMemcpyHostToDevice, c->stream), "H2D peer info");
-  nck(ncclAllGather(d, d + sz, sz, ncclUint8, cm(c), c->stream), "ncclAllGather(peer info)");
+  comm(c)->allgather(d, d + sz, sz, c->stream);
   std::vector<PeerInfo> all(static_cast<size_t>(R));
   ck(cudaMemcpyAsync(all.data(), d + sz, sz * R, cudaMemcpyDeviceToHost, c->stream),
      "D2H peer info");
   ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   cudaFree(d);
+  // some rank's buffers moved (the only reason for a new exchange): close
+  // every mapping and open what the new layout needs — a reallocated buffer
+  // may even come back under the old handle's bytes, so none is reused
+  for (auto& e : c->ipc_open) cudaIpcCloseMemHandle(e.second);
+  c->ipc_open.clear();
   const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
   for (int b = 0; b < 2; ++b) {
     // my lowest layer -> lo's upper ghost; my highest layer -> hi's lower ghost
@@ -252,7 +267,7 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
                                                   c->g, c->mig_dest, c->mig_count, c->ctrl);
   }
   int* Md = reinterpret_cast<int*>(c->nccl_i64);  // R*R ints (the buffer holds 2R^2 + 2R + 16)
-  nck(ncclAllGather(c->mig_count, Md, uR, ncclInt32, cm(c), c->stream), "ncclAllGather(M)");
+  comm(c)->allgather(c->mig_count, Md, uR * sizeof(int), c->stream);
   std::vector<int> M(uR * uR);
   ck(cudaMemcpyAsync(M.data(), Md, sizeof(int) * uR * uR, cudaMemcpyDeviceToHost, c->stream),
      "D2H counts");
@@ -271,12 +286,12 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
         c->id2);
   }
   const size_t keep = static_cast<size_t>(n - off[uR]);
-  if (keep > 0) {  // stayers back in place: one launch (the resort's copy-back; the
-                   // cell column it also copies is recomputed by the resort)
+  if (keep > 0) {  // stayers back in place: one unconditional launch (no cell
+                   // column: the resort that follows recomputes it)
     c->launches += 1;
     k_copy_back<<<blocks_for(static_cast<int64_t>(keep), kBlock), kBlock, 0, c->ls>>>(
-        static_cast<int>(keep), c->pos2, c->vx2, c->vy2, c->vz2, c->mass2, c->id2, c->cell2,
-        c->pos, c->vx, c->vy, c->vz, c->mass, c->id, c->cell, c->ctrl);
+        static_cast<int>(keep), c->pos2, c->vx2, c->vy2, c->vz2, c->mass2, c->id2, nullptr,
+        c->pos, c->vx, c->vy, c->vz, c->mass, c->id, nullptr, nullptr);
   }
   c->n = static_cast<int64_t>(keep);
   c->n_ghost = c->n_ghost_lo = c->n_ghost_hi = 0;
@@ -285,24 +300,25 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   grow_capacity(c, c->n + nrecv);  // (synchronises and bumps ipc_gen only when it grows)
   c->mig_nrecv = nrecv;
   const size_t rec = sizeof(MigRec);
-  nck(ncclGroupStart(), "ncclGroupStart");
+  SlabComm* cm = comm(c);
+  cm->group_start();
   for (int d = 0; d < R; ++d) {
     const int m = M[static_cast<size_t>(r) * uR + d];
     if (m) {
-      nck(ncclSend(reinterpret_cast<char*>(c->mig_send) + static_cast<size_t>(off[static_cast<size_t>(d)]) * rec,
-                   static_cast<size_t>(m) * rec, ncclUint8, d, cm(c), c->stream), "ncclSend");
+      cm->send(reinterpret_cast<char*>(c->mig_send) + static_cast<size_t>(off[static_cast<size_t>(d)]) * rec,
+               static_cast<size_t>(m) * rec, d, c->stream);
     }
   }
   int64_t roff = 0;
   for (int q = 0; q < R; ++q) {
     const int m = M[static_cast<size_t>(q) * uR + r];
     if (m) {
-      nck(ncclRecv(reinterpret_cast<char*>(c->mig_recv) + roff * rec, static_cast<size_t>(m) * rec,
-                   ncclUint8, q, cm(c), c->stream), "ncclRecv");
+      cm->recv(reinterpret_cast<char*>(c->mig_recv) + roff * rec, static_cast<size_t>(m) * rec, q,
+               c->stream);
     }
     roff += m;
   }
-  nck(ncclGroupEnd(), "ncclGroupEnd");
+  cm->group_end(c->stream);
   // 3. commit on the device; one row per rank all-gathered
   slab_commit_launch(c);
   const int dxy = c->g.dims[0] * c->g.dims[1];
@@ -311,7 +327,7 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   c->launches += 1;
   k_slab_row<<<1, 1, 0, c->ls>>>(row, c->boff[0] + dxy, c->boff[1] + dxy, static_cast<int>(c->n),
                                  static_cast<int>(c->n_cap), c->ipc_gen);
-  nck(ncclAllGather(row, table, kRowInts, ncclInt32, cm(c), c->stream), "ncclAllGather(rows)");
+  cm->allgather(row, table, kRowInts * sizeof(int), c->stream);
   std::vector<int> T(uR * kRowInts);
   ck(cudaMemcpyAsync(T.data(), table, sizeof(int) * T.size(), cudaMemcpyDeviceToHost, c->stream),
      "D2H rows");
@@ -378,27 +394,22 @@ int64_t spec_batch(const tmd_gpu_ctx* c, int64_t done_step) {
   return std::max<int64_t>(1, std::min<int64_t>(kSpecSteps, static_cast<int64_t>(k)));
 }
 
-// Global max displacement^2 of this step (in place on the device word that
-// k_decide reads), brought to the host for the rebuild decision.
-double nccl_global_max_d2(tmd_gpu_ctx* c) {
-  nck(ncclAllReduce(&c->ctrl->max_d2, &c->ctrl->max_d2, 1, ncclUint64, ncclMax, cm(c),
-                    c->stream), "ncclAllReduce(max)");
-  sync_ctrl(c);
-  raise_physics(c, true);
-  if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
-  double m = 0.0;
-  std::memcpy(&m, &c->h_ctrl->max_d2, sizeof m);
-  return m;
+void need_comm(const tmd_gpu_ctx* c) {
+  if (!c->comm) throw StatusError{TMD_ERR_STATE, "slab context has no transport (attach one first)"};
 }
-#endif  // TMD_NO_NCCL
 
-void need_nccl(const tmd_gpu_ctx* c) {
-#ifdef TMD_NO_NCCL
-  (void)c;
-  throw StatusError{TMD_ERR_CONFIG, "this build of libtmd_gpu.so has no NCCL"};
-#else
-  if (!c->nccl) throw StatusError{TMD_ERR_STATE, "slab context has no NCCL communicator"};
-#endif
+// A failure on one rank of an in-process group releases the others from the
+// collective they wait in (they fail with "a peer rank failed").
+template <class F>
+int native_guard(tmd_gpu_ctx* c, F&& fn) {
+  return guard(c, [&] {
+    try {
+      fn();
+    } catch (...) {
+      if (c->comm) comm(c)->abort();
+      throw;
+    }
+  });
 }
 
 }  // namespace
@@ -429,38 +440,88 @@ int tmd_nccl_unique_id(void* id) {
 #endif
 }
 
+namespace {
+void attach_common(tmd_gpu_ctx* c, int flags) {
+  need_slab(c);
+  if (c->comm) throw StatusError{TMD_ERR_STATE, "slab context already has a transport"};
+  c->balance_count = (flags & 1) != 0;
+  c->fused_halo = (flags & 2) != 0;
+  ck(cudaSetDevice(c->device), "cudaSetDevice");
+}
+void alloc_comm_staging(tmd_gpu_ctx* c) {
+  c->nccl_i64 = dalloc<int64_t>(static_cast<size_t>(c->nranks) * (c->nranks + 1) + 8);
+}
+}  // namespace
+
 int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id, int flags) {
   return guard(c, [&] {
-    c->balance_count = (flags & 1) != 0;
-    c->fused_halo = (flags & 2) != 0;
-    need_slab(c);
+    attach_common(c, flags);
 #ifdef TMD_NO_NCCL
     (void)unique_id;
-    need_nccl(c);
+    throw StatusError{TMD_ERR_CONFIG, "this build of libtmd_gpu.so has no NCCL"};
 #else
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     ncclUniqueId u;
     std::memcpy(&u, unique_id, sizeof u);
-    ncclComm_t comm = nullptr;
-    nck(ncclCommInitRank(&comm, c->nranks, u, c->my_rank), "ncclCommInitRank");
-    c->nccl = comm;
-    c->nccl_i64 = dalloc<int64_t>(static_cast<size_t>(c->nranks) * (c->nranks + 1) + 8);
+    auto nc = std::make_unique<NcclComm>();
+    nck(ncclCommInitRank(&nc->nc, c->nranks, u, c->my_rank), "ncclCommInitRank");
+    alloc_comm_staging(c);
+    c->comm = nc.release();
 #endif
   });
 }
 
-int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
+int tmd_local_group_create(int nranks, void** group) {
+  if (!group || nranks < 1) {
+    g_create_error = "local group: nranks >= 1 and an output pointer required";
+    return TMD_ERR_CONFIG;
+  }
+  *group = new std::shared_ptr<LocalGroup>(std::make_shared<LocalGroup>(nranks));
+  return TMD_OK;
+}
+
+void tmd_local_group_destroy(void* group) {
+  delete static_cast<std::shared_ptr<LocalGroup>*>(group);
+}
+
+int tmd_gpu_slab_attach_local(tmd_gpu_ctx* c, void* group, int flags) {
   return guard(c, [&] {
+    if (!group) throw StatusError{TMD_ERR_CONFIG, "local group missing"};
+    const auto& g = *static_cast<std::shared_ptr<LocalGroup>*>(group);
+    if (g->R != c->nranks) {
+      throw StatusError{TMD_ERR_CONFIG, "local group of " + std::to_string(g->R) +
+                                            " ranks for a slab of " + std::to_string(c->nranks)};
+    }
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      if (g->taken[static_cast<size_t>(c->my_rank)]) {
+        throw StatusError{TMD_ERR_CONFIG, "rank " + std::to_string(c->my_rank) +
+                                              " of the local group is already attached"};
+      }
+      g->taken[static_cast<size_t>(c->my_rank)] = 1;
+    }
+    try {
+      attach_common(c, flags);
+      auto lc = std::make_unique<LocalComm>(g, c->my_rank);
+      alloc_comm_staging(c);
+      c->comm = lc.release();
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->taken[static_cast<size_t>(c->my_rank)] = 0;
+      throw;
+    }
+  });
+}
+
+int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
+  return native_guard(c, [&] {
     need_slab(c);
-    need_nccl(c);
-#ifndef TMD_NO_NCCL
+    need_comm(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     nccl_rebuild(c, false);
     c->last_rebuild_step = c->step;
     rck(c, tmd_gpu_slab_forces(c, 0));
     sync_ctrl(c);
     raise_physics(c, false);
-#endif
   });
 }
 
@@ -475,7 +536,6 @@ int tmd_gpu_slab_setup(tmd_gpu_ctx* c) {
 // same step.
 namespace {
 
-#ifndef TMD_NO_NCCL
 // Rows the device recorded since the last collection (run_observed), then
 // the device counter is reset on the stream. Call right after a sync_ctrl.
 void collect_slab_obs(tmd_gpu_ctx* c) {
@@ -487,13 +547,11 @@ void collect_slab_obs(tmd_gpu_ctx* c) {
   }
   ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
 }
-#endif
 
 void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
     need_slab(c);
-    need_nccl(c);
+    need_comm(c);
     if (nsteps < 0) throw StatusError{TMD_ERR_CONFIG, "step count must be non-negative"};
-#ifndef TMD_NO_NCCL
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (nsteps == 0) return;
     if (c->obs_stride > 0) {
@@ -509,8 +567,7 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
       const int64_t K = std::min<int64_t>(K_next, target - done_step);
       int64_t fused_launches = 0;
       for (int64_t s = 0; s < K; ++s) {
-        nck(ncclAllReduce(&c->ctrl->max_d2, &c->ctrl->max_d2, 1, ncclUint64, ncclMax, cm(c),
-                          c->stream), "ncclAllReduce(max)");
+        comm(c)->allreduce(&c->ctrl->max_d2, 1, CType::kU64, COp::kMax, c->stream);
         c->launches += 1;
         k_decide_spec<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr);
         const bool last = done_step + s + 1 == target;
@@ -564,18 +621,17 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
     c->elapsed += 1e-3 * ms;
     c->step = c->h_ctrl->step;
     c->rebuilds = static_cast<uint64_t>(c->h_ctrl->rebuilds);
-#endif
 }
 
 }  // namespace
 
 int tmd_gpu_slab_run(tmd_gpu_ctx* c, int64_t nsteps) {
-  return guard(c, [&] { slab_run_impl(c, nsteps); });
+  return native_guard(c, [&] { slab_run_impl(c, nsteps); });
 }
 
 int tmd_gpu_slab_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride,
                               tmd_observables* out, int64_t cap, int64_t* n_out) {
-  return guard(c, [&] {
+  return native_guard(c, [&] {
     if (stride < 1) throw StatusError{TMD_ERR_CONFIG, "observable stride must be at least 1"};
     if (!n_out || (cap > 0 && !out)) throw StatusError{TMD_ERR_CONFIG, "row buffer missing"};
     ck(cudaSetDevice(c->device), "cudaSetDevice");
@@ -614,18 +670,16 @@ int tmd_gpu_slab_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride,
 }
 
 int tmd_gpu_slab_observe(tmd_gpu_ctx* c, int64_t n_total, tmd_observables* out) {
-  return guard(c, [&] {
+  return native_guard(c, [&] {
     need_slab(c);
-    need_nccl(c);
-#ifndef TMD_NO_NCCL
+    need_comm(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->launches += 1;
     k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
                                             c->mass, c->part_ke);
     launch_reduce_ke(c);
     launch_reduce_pe(c);
-    nck(ncclAllReduce(c->scalars, c->scalars, 3, ncclFloat64, ncclSum, cm(c), c->stream),
-        "ncclAllReduce(sum)");
+    comm(c)->allreduce(c->scalars, 3, CType::kF64, COp::kSum, c->stream);
     ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream), "D2H scalars");
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
@@ -634,7 +688,6 @@ int tmd_gpu_slab_observe(tmd_gpu_ctx* c, int64_t n_total, tmd_observables* out) 
     out->virial = c->h_scalars[1];
     out->kinetic = c->h_scalars[2];
     out->temperature = 2.0 * out->kinetic / (3.0 * static_cast<double>(n_total));
-#endif
   });
 }
 

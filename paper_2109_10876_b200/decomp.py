@@ -40,6 +40,7 @@ exported it.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -294,6 +295,12 @@ class SlabContext:
         flags = (1 if balance_count else 0) | (2 if fused_halo else 0)
         self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf, flags))
 
+    def attach_local(self, group, balance_count: bool = False, fused_halo: bool = True) -> None:
+        """Attach to an in-process group (tmd_local_group_create): the same C++
+        loop with every rank's context in this process, one thread per rank."""
+        flags = (1 if balance_count else 0) | (2 if fused_halo else 0)
+        self._c(_abi.lib().tmd_gpu_slab_attach_local(self._h, group, flags))
+
     def setup_native(self) -> None:
         self._c(_abi.lib().tmd_gpu_slab_setup(self._h))
 
@@ -535,17 +542,29 @@ class DecomposedEngine:
         self.exchanged_bytes = 0
         self.native = bool(native)
         if self.native:
-            # the whole protocol in C++ with NCCL on each context's stream
-            # (tmd_slab_nccl.cuh): one slab per process, static cuts
-            if len(self.ctx) != 1:
-                raise ConfigError("the native NCCL loop runs one slab per process")
-            (c,) = self.ctx.values()
+            # the whole protocol in C++ (tmd_slab_nccl.cuh) with its collectives
+            # on each context's stream: NCCL with one slab per process, or the
+            # in-process transport with every rank's context here, driven by
+            # one thread per rank
             if halo not in ("fused", "nccl"):
                 raise ConfigError(f"unknown halo mode {halo!r} (fused | nccl)")
-            c.attach_nccl(comm.broadcast_bytes(SlabContext.nccl_unique_id),
-                          balance_count=balance == "count", fused_halo=halo == "fused")
-            c.setup_native()
-            self.recuts = c.info()["recuts"]
+            kw = dict(balance_count=balance == "count", fused_halo=halo == "fused")
+            if isinstance(comm, InProcessComm):
+                L = _abi.lib()
+                g = C.c_void_p()
+                _check(L.tmd_local_group_create(int(R), C.byref(g)), None)
+                try:
+                    for c in self.ctx.values():
+                        c.attach_local(g, **kw)
+                finally:
+                    L.tmd_local_group_destroy(g)
+            else:
+                if len(self.ctx) != 1:
+                    raise ConfigError("the native NCCL loop runs one slab per process")
+                (c,) = self.ctx.values()
+                c.attach_nccl(comm.broadcast_bytes(SlabContext.nccl_unique_id), **kw)
+            self._par(lambda c: c.setup_native())
+            self.recuts = next(iter(self.ctx.values())).info()["recuts"]
             return
         self._rebuild(advance=False)
         for c in self.ctx.values():
@@ -554,6 +573,32 @@ class DecomposedEngine:
     def close(self) -> None:
         for c in self.ctx.values():
             c.close()
+
+    def _par(self, fn) -> Dict[int, object]:
+        """fn(ctx) for every local rank, concurrently (one thread per rank: the
+        native loop's collectives rendezvous across them). The first error
+        that is not a peer's "a peer rank failed" is raised."""
+        items = list(self.ctx.items())
+        if len(items) == 1:
+            r, c = items[0]
+            return {r: fn(c)}
+        out: Dict[int, object] = {}
+        errs: Dict[int, BaseException] = {}
+
+        def work(r, c):
+            try:
+                out[r] = fn(c)
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                errs[r] = e
+        ts = [threading.Thread(target=work, args=rc, daemon=True) for rc in items]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            own = [e for e in errs.values() if "a peer rank failed" not in str(e)]
+            raise (own or list(errs.values()))[0]
+        return out
 
     # -- protocol phases ---------------------------------------------------------
     def _rebuild(self, advance: bool) -> None:
@@ -640,9 +685,9 @@ class DecomposedEngine:
         if steps == 0:
             return
         if self.native:
-            (c,) = self.ctx.values()
-            c.run_native(steps)
+            self._par(lambda c: c.run_native(steps))
             self.steps += steps
+            c = next(iter(self.ctx.values()))
             self.rebuilds = c.rebuild_count()
             self.recuts = c.info()["recuts"]
             return
@@ -679,16 +724,18 @@ class DecomposedEngine:
         if stride < 1:
             raise ConfigError("observable stride must be at least 1")
         if self.native:
-            (r, c), = self.ctx.items()
             s0 = self.steps
-            local = c.run_observed_native(steps, stride)
+            local = self._par(lambda c: c.run_observed_native(steps, stride))
             self.steps += steps
+            c = next(iter(self.ctx.values()))
             self.rebuilds = c.rebuild_count()
             self.recuts = c.info()["recuts"]
             want = np.arange(s0 + stride - s0 % stride, s0 + steps + 1, stride)
-            if local.shape[0] != want.size or not np.array_equal(local[:, 0], want):
-                raise StateError("native loop recorded an unexpected set of steps")
-            tot = self.comm.allreduce_sum({r: local[:, 1:4].ravel()}).reshape(-1, 3)
+            for rows in local.values():
+                if rows.shape[0] != want.size or not np.array_equal(rows[:, 0], want):
+                    raise StateError("native loop recorded an unexpected set of steps")
+            tot = self.comm.allreduce_sum(
+                {r: rows[:, 1:4].ravel() for r, rows in local.items()}).reshape(-1, 3)
             ke, pe, w = tot[:, 0], tot[:, 1], tot[:, 2]
             return np.column_stack([want.astype(np.float64), ke, pe,
                                     2.0 * ke / (3.0 * self.n_total), w])
@@ -706,8 +753,8 @@ class DecomposedEngine:
 
     def observe(self) -> StepObservables:
         if self.native:
-            (c,) = self.ctx.values()
-            o = c.observe_native(self.n_total)
+            obs = self._par(lambda c: c.observe_native(self.n_total))
+            o = obs[min(obs)]
             return StepObservables(self.steps, o.kinetic, o.potential, o.temperature, o.virial)
         tot = self.comm.allreduce_sum({r: c.sums() for r, c in self.ctx.items()})
         pe, w, ke = (float(v) for v in tot)

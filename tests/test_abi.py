@@ -195,3 +195,14 @@ def test_fcc_box_generator():
     rho = long.size() / np.prod(long.box)
     assert abs(rho - 0.8442) < 1e-12
     assert abs(long.vel.sum(axis=0)).max() < 1e-9  # zero net momentum
+
+
+def test_local_group_handle_lifecycle():
+    """tmd_local_group_create / _destroy (the in-process transport of the
+    native slab loop) need no device."""
+    import ctypes as C
+    L = _abi.lib()
+    g = C.c_void_p()
+    assert L.tmd_local_group_create(0, C.byref(g)) == _abi.TMD_ERR_CONFIG
+    assert L.tmd_local_group_create(4, C.byref(g)) == _abi.TMD_OK and g.value
+    L.tmd_local_group_destroy(g)

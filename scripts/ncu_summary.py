@@ -108,7 +108,7 @@ def record(rep, n_particles, kernel, out_json):
            "dram_read_bytes": num("dram__bytes_read.sum", b),
            "dram_write_bytes": num("dram__bytes_write.sum", b),
            "duration_ms": num("gpu__time_duration.sum", t),
-           "dram_frac_of_peak": num("dram__throughput.avg.pct_of_peak_sustained_elapsed") / 100,
+           "dram_frac_of_peak": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed") / 100,
            "l1tex_frac_of_peak": num("l1tex__throughput.avg.pct_of_peak_sustained_active") / 100,
            "fp64_pipe_frac": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") / 100,
            "issue_active_frac": num("smsp__issue_active.avg.pct_of_peak_sustained_active") / 100,

@@ -2,12 +2,12 @@
 // (/root/reference/proj/include/taskmd/engine.hpp:66-290) backed by the B200
 // engine through the C ABI in include/tmd_gpu.h (libtmd_gpu.so).
 //
-// Reference users switch by replacing
-//     taskmd::Engine eng(taskmd::build_domain(flat, inter, r_skin, n_sub), cfg);
-// with
-//     taskmd_gpu::Engine eng(flat, inter, r_skin, cfg);
-// and keep calling step() / run() / observe() / potential_energy() / timers()
-// / step_count() / rebuild_count() / steal_count(). Errors come back as the
+// Reference users switch by replacing the class name only:
+//     taskmd::Engine     eng(taskmd::build_domain(flat, inter, r_skin, n_sub), cfg);
+//     taskmd_gpu::Engine eng(taskmd::build_domain(flat, inter, r_skin, n_sub), cfg);
+// (or skip the CPU build_domain: taskmd_gpu::Engine eng(flat, inter, r_skin,
+// cfg)) and keep calling step() / run() / observe() / potential_energy() /
+// timers() / step_count() / rebuild_count() / steal_count() / domain(). Errors come back as the
 // reference's own exception types (taskmd::ConfigError / PhysicsError /
 // StateError, errors.hpp:19-43), so the CLI's exit-code mapping
 // (md_cli.cpp:333-352) holds unchanged.
@@ -20,8 +20,10 @@
 #ifndef TASKMD_GPU_ENGINE_HPP_
 #define TASKMD_GPU_ENGINE_HPP_
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -173,7 +175,7 @@ class Engine {
   // FENE bonds and a thermostat run on the device.
   Engine(const taskmd::FlatConfig& flat, const taskmd::Interactions& inter, double r_skin,
          const taskmd::EngineConfig& cfg, const GpuOptions& opt = {})
-      : cfg_(cfg) {
+      : cfg_(cfg), inter_(inter), r_skin_(r_skin) {
     CSystem cs(flat, inter, r_skin, cfg, opt);
     const int rc = tmd_gpu_create(&cs.sys, &cs.lj, cs.fene_ptr(), &cs.p, &ctx_);
     if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
@@ -181,11 +183,53 @@ class Engine {
     topo_ = flat.topo;
   }
 
+#ifndef TASKMD_GPU_STANDALONE
+  // Engine(Domain, EngineConfig) (engine.hpp:68-77): the domain a caller
+  // assembled with build_domain is flattened (flatten_domain, domain.hpp:
+  // 193-207: ids, types, masses, wrapped positions, velocities, topology) and
+  // rebuilt on the device with its own interactions and skin.
+  Engine(taskmd::Domain domain, const taskmd::EngineConfig& cfg, const GpuOptions& opt = {})
+      : Engine(taskmd::flatten_domain(domain), domain.inter, domain.r_skin, cfg, opt) {}
+
+  // Engine::domain() (engine.hpp:142-143) for callers that read the stores
+  // (md_cli.cpp:226-250, acceptance.cpp:53-64): a reference Domain rebuilt on
+  // the host from the current device state (build_domain over flatten(), with
+  // EngineConfig::n_sub subnodes), every owned slot's force set to the
+  // device's last evaluation. Its neighbour lists are the reference's at the
+  // current positions. Cached until the next step.
+  const taskmd::Domain& domain() const {
+    if (!dom_ || dom_step_ != step_count()) {
+      const taskmd::FlatConfig f = flatten();
+      auto d = std::make_unique<taskmd::Domain>(
+          taskmd::build_domain(f, inter_, r_skin_, std::max(1, cfg_.n_sub)));
+      const auto fr = forces();  // sorted by id
+      for (taskmd::Subnode& sn : d->subs) {
+        for (std::int32_t cidx : sn.interior) {
+          const taskmd::CellSpan& span = sn.store.cells[static_cast<std::size_t>(cidx)];
+          for (std::size_t k = span.begin; k < span.begin + span.real; ++k) {
+            const auto it = std::lower_bound(
+                fr.begin(), fr.end(), sn.store.id[k],
+                [](const std::pair<std::int64_t, taskmd::Vec3>& a, std::int64_t v) {
+                  return a.first < v;
+                });
+            sn.store.fx[k] = it->second.x;
+            sn.store.fy[k] = it->second.y;
+            sn.store.fz[k] = it->second.z;
+          }
+        }
+      }
+      dom_ = std::move(d);
+      dom_step_ = step_count();
+    }
+    return *dom_;
+  }
+#endif
+
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
   Engine(Engine&& o) noexcept
-      : ctx_(std::exchange(o.ctx_, nullptr)), cfg_(o.cfg_), box_(o.box_),
-        topo_(std::move(o.topo_)) {}
+      : ctx_(std::exchange(o.ctx_, nullptr)), cfg_(o.cfg_), inter_(o.inter_),
+        r_skin_(o.r_skin_), box_(o.box_), topo_(std::move(o.topo_)) {}
   ~Engine() { tmd_gpu_destroy(ctx_); }
 
   void step() { run(1); }
@@ -221,18 +265,20 @@ class Engine {
   std::uint64_t rebuild_count() const { return tmd_gpu_rebuild_count(ctx_); }
   std::uint64_t steal_count() const { return 0; }  // no work-stealing pool on the GPU
 
-  // flatten_domain (domain.hpp:193-207): sorted by id, positions wrapped.
+  // flatten_domain (domain.hpp:193-207): sorted by id, positions wrapped,
+  // each particle's type and mass as created.
   taskmd::FlatConfig flatten() const {
     const std::size_t n = static_cast<std::size_t>(tmd_gpu_size(ctx_));
     std::vector<std::int64_t> id(n);
     std::vector<double> pos(3 * n), vel(3 * n);
-    check(tmd_gpu_download(ctx_, id.data(), pos.data(), vel.data(), nullptr));
     taskmd::FlatConfig f;
+    f.type.resize(n);
+    f.mass.resize(n);
+    check(tmd_gpu_download(ctx_, id.data(), pos.data(), vel.data(), nullptr, f.type.data(),
+                           f.mass.data()));
     f.box = box_;
     f.topo = topo_;
-    f.id = id;
-    f.type.assign(n, 0);
-    f.mass.assign(n, 1.0);
+    f.id.assign(id.begin(), id.end());
     f.pos.resize(n);
     f.vel.resize(n);
     for (std::size_t k = 0; k < n; ++k) {
@@ -248,7 +294,7 @@ class Engine {
     const std::size_t n = static_cast<std::size_t>(tmd_gpu_size(ctx_));
     std::vector<std::int64_t> id(n);
     std::vector<double> f(3 * n);
-    check(tmd_gpu_download(ctx_, id.data(), nullptr, nullptr, f.data()));
+    check(tmd_gpu_download(ctx_, id.data(), nullptr, nullptr, f.data(), nullptr, nullptr));
     std::vector<std::pair<std::int64_t, taskmd::Vec3>> out(n);
     for (std::size_t k = 0; k < n; ++k) out[k] = {id[k], {f[3 * k], f[3 * k + 1], f[3 * k + 2]}};
     return out;
@@ -274,8 +320,14 @@ class Engine {
 
   tmd_gpu_ctx* ctx_ = nullptr;
   taskmd::EngineConfig cfg_;
+  taskmd::Interactions inter_;
+  double r_skin_ = 0.0;
   taskmd::BoxSpec box_;
   taskmd::Topology topo_;
+#ifndef TASKMD_GPU_STANDALONE
+  mutable std::unique_ptr<taskmd::Domain> dom_;
+  mutable std::int64_t dom_step_ = -1;
+#endif
 };
 
 using NcclId = std::array<unsigned char, 128>;
@@ -327,17 +379,19 @@ class SlabEngine {
   std::int64_t step_count() const { return tmd_gpu_step_count(ctx_); }
   std::uint64_t rebuild_count() const { return tmd_gpu_rebuild_count(ctx_); }
 
-  // The particles this slab owns, sorted by id, positions wrapped.
+  // The particles this slab owns, sorted by id, positions wrapped, types and
+  // masses as created.
   taskmd::FlatConfig local() const {
     const std::size_t n = static_cast<std::size_t>(tmd_gpu_size(ctx_));
     std::vector<std::int64_t> id(n);
     std::vector<double> pos(3 * n), vel(3 * n);
-    check(tmd_gpu_download(ctx_, id.data(), pos.data(), vel.data(), nullptr));
     taskmd::FlatConfig f;
+    f.type.resize(n);
+    f.mass.resize(n);
+    check(tmd_gpu_download(ctx_, id.data(), pos.data(), vel.data(), nullptr, f.type.data(),
+                           f.mass.data()));
     f.box = box_;
-    f.id = id;
-    f.type.assign(n, 0);
-    f.mass.assign(n, 1.0);
+    f.id.assign(id.begin(), id.end());
     f.pos.resize(n);
     f.vel.resize(n);
     for (std::size_t k = 0; k < n; ++k) {

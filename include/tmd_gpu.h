@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TMD_GPU_ABI_VERSION 3
+#define TMD_GPU_ABI_VERSION 4
 
 /* Status codes. */
 #define TMD_OK 0
@@ -173,10 +173,11 @@ int tmd_gpu_run_observed(tmd_gpu_ctx* ctx, int64_t nsteps, int64_t stride, tmd_o
 int tmd_gpu_observe(tmd_gpu_ctx* ctx, tmd_observables* out);
 
 /* flatten_domain (domain.hpp:193-207): arrays of n entries sorted by id,
- * positions wrapped into the box; forces are the last evaluation's. Any
- * output pointer may be NULL. */
+ * positions wrapped into the box, each particle's type and mass as created
+ * (ParticleRec, flat_config.hpp:18-40); forces are the last evaluation's.
+ * Any output pointer may be NULL. */
 int tmd_gpu_download(tmd_gpu_ctx* ctx, int64_t* id, double* pos, double* vel,
-                     double* force);
+                     double* force, int32_t* type, double* mass);
 
 /* Overwrite velocities by id (ids sorted or not; every owned id exactly once).
  * The analog of tests poking Domain stores (test_engine.cpp:174-184). */

@@ -145,7 +145,7 @@ def lib() -> C.CDLL:
     L.tmd_gpu_observe.argtypes = [P, C.POINTER(TmdObservables)]
     L.tmd_gpu_run_observed.argtypes = [P, C.c_int64, C.c_int64, C.POINTER(TmdObservables),
                                        C.c_int64, C.POINTER(C.c_int64)]
-    L.tmd_gpu_download.argtypes = [P, P, P, P, P]
+    L.tmd_gpu_download.argtypes = [P, P, P, P, P, P, P]
     L.tmd_gpu_set_velocities.argtypes = [P, P, P]
     L.tmd_gpu_cell_of.argtypes = [P, P, P]
     L.tmd_gpu_pairs.argtypes = [P, P, C.c_size_t, C.POINTER(C.c_size_t)]

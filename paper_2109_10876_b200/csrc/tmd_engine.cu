@@ -196,6 +196,13 @@ struct tmd_gpu_ctx {
   bool ids_dense = false;
   long long dl_lo = 0;
   double* dl = nullptr;
+  // ParticleRec::type (flat_config.hpp:18-40): static per particle and never
+  // read by the LJ path, so it stays on the host as a table by id, returned
+  // by tmd_gpu_download like flatten_domain does (domain.hpp:193-207).
+  // Empty: every type is 0. type_id empty: dense, type_val[id - type_lo].
+  std::vector<long long> type_id;
+  std::vector<int32_t> type_val;
+  long long type_lo = 0;
   char* arena = nullptr;  // the per-slot arrays of a non-slab context, one allocation
   size_t arena_bytes = 0;
   size_t nbr_bytes = 0;   // size of the list block (big_alloc)
@@ -1647,6 +1654,38 @@ void setup_bonds(tmd_gpu_ctx* c, const tmd_system* sys, const tmd_fene_params* f
   c->bt.rmax2 = fene->r_max * fene->r_max;  // fene_eval (potentials.hpp:98)
 }
 
+// The type column of the caller's FlatConfig, kept by id (see tmd_gpu_ctx).
+void set_type_table(tmd_gpu_ctx* c, const tmd_system* sys) {
+  c->type_id.clear();
+  c->type_val.clear();
+  const size_t n = static_cast<size_t>(sys->n);
+  if (!sys->type || n == 0) return;
+  if (std::all_of(sys->type, sys->type + n, [](int32_t t) { return t == 0; })) return;
+  const auto mm = std::minmax_element(sys->id, sys->id + n);
+  if (static_cast<unsigned long long>(*mm.second - *mm.first) == n - 1) {
+    c->type_lo = *mm.first;
+    c->type_val.assign(n, 0);
+    for (size_t k = 0; k < n; ++k) c->type_val[static_cast<size_t>(sys->id[k] - c->type_lo)] = sys->type[k];
+    return;
+  }
+  std::vector<size_t> o(n);
+  std::iota(o.begin(), o.end(), size_t{0});
+  std::sort(o.begin(), o.end(), [&](size_t a, size_t b) { return sys->id[a] < sys->id[b]; });
+  c->type_id.resize(n);
+  c->type_val.resize(n);
+  for (size_t k = 0; k < n; ++k) {
+    c->type_id[k] = sys->id[o[k]];
+    c->type_val[k] = sys->type[o[k]];
+  }
+}
+
+int32_t type_of(const tmd_gpu_ctx* c, long long id) {
+  if (c->type_val.empty()) return 0;
+  if (c->type_id.empty()) return c->type_val[static_cast<size_t>(id - c->type_lo)];
+  const auto it = std::lower_bound(c->type_id.begin(), c->type_id.end(), id);
+  return c->type_val[static_cast<size_t>(it - c->type_id.begin())];
+}
+
 int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_params* fene,
                 const tmd_engine_params* params, int rank, int nranks, bool slab,
                 tmd_gpu_ctx** out) {
@@ -1665,6 +1704,8 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
   const int rc = guard(c, [&] {
     validate(sys, lj, fene, params);
     mark("validate");
+    set_type_table(c, sys);
+    mark("type table");
     build_geom(c, sys->box, lj->r_cut, params->r_skin);  // ConfigError before any CUDA call
     mark("geometry");
     int ndev = 0;
@@ -1807,7 +1848,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       want(c->ck_fy, n);
       want(c->ck_fz, n);
     }
-    if (!slab) want(c->dl, 10 * n);  // download / upload scratch
+    if (!slab) want(c->dl, 11 * n);  // download / upload scratch
     if (!slab) {
       size_t tot = 0;
       for (const auto& e : plan) tot += (e.second + 255) / 256 * 256;
@@ -1972,7 +2013,7 @@ namespace {
 struct HostState {
   std::vector<long long> id;
   std::vector<double4> pos;
-  std::vector<double> v[3], f[3];
+  std::vector<double> v[3], f[3], mass;
   std::vector<int> cell;
   std::vector<size_t> order;  // slots sorted by id
 };
@@ -1999,7 +2040,7 @@ const uint32_t* decoded_list(tmd_gpu_ctx* c) {
   return c->decoded;
 }
 
-HostState fetch(tmd_gpu_ctx* c, bool pos, bool vel, bool frc, bool cell) {
+HostState fetch(tmd_gpu_ctx* c, bool pos, bool vel, bool frc, bool cell, bool mass = false) {
   HostState h;
   const size_t n = static_cast<size_t>(c->n);
   h.id.resize(n);
@@ -2028,6 +2069,11 @@ HostState fetch(tmd_gpu_ctx* c, bool pos, bool vel, bool frc, bool cell) {
     h.cell.resize(n);
     ck(cudaMemcpyAsync(h.cell.data(), c->cell, n * sizeof(int),
                        cudaMemcpyDeviceToHost, c->stream), "D2H cell");
+  }
+  if (mass) {
+    h.mass.resize(n);
+    ck(cudaMemcpyAsync(h.mass.data(), c->mass, n * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H mass");
   }
   ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   h.order.resize(n);
@@ -2161,10 +2207,16 @@ int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
 }
 
 int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
-                     double* force) {
+                     double* force, int32_t* type, double* mass) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     const size_t nn = static_cast<size_t>(c->n);
+    std::vector<long long> ids_tmp;
+    long long* ids_out = reinterpret_cast<long long*>(id);
+    if (!ids_out && type && !c->type_val.empty()) {  // ids needed for the type lookup
+      ids_tmp.resize(nn);
+      ids_out = ids_tmp.data();
+    }
     if (c->ids_dense && !c->g.zslab && nn > 0) {
       // id order by direct placement on the device, positions wrapped there
       // (the same rounding as host_wrap1), one copy per array into the
@@ -2173,14 +2225,15 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
       double* dvel = c->dl + 3 * nn;
       double* dfrc = c->dl + 6 * nn;
       long long* did = reinterpret_cast<long long*>(c->dl + 9 * nn);
+      double* dmass = c->dl + 10 * nn;
       k_download<<<blocks_for(c->n, kBlock), kBlock, 0, c->stream>>>(
-          static_cast<int>(nn), c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->id,
+          static_cast<int>(nn), c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->id,
           c->dl_lo, c->g, pos ? dpos : nullptr, vel ? dvel : nullptr, force ? dfrc : nullptr,
-          did);
+          mass ? dmass : nullptr, did);
       ck(cudaGetLastError(), "k_download");
-      if (id) {
-        ck(cudaMemcpyAsync(id, did, nn * sizeof(long long), cudaMemcpyDeviceToHost, c->stream),
-           "D2H id");
+      if (ids_out) {
+        ck(cudaMemcpyAsync(ids_out, did, nn * sizeof(long long), cudaMemcpyDeviceToHost,
+                           c->stream), "D2H id");
       }
       if (pos) {
         ck(cudaMemcpyAsync(pos, dpos, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
@@ -2194,22 +2247,35 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
         ck(cudaMemcpyAsync(force, dfrc, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream), "D2H force");
       }
-      ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-      return;
-    }
-    HostState h = fetch(c, pos != nullptr, vel != nullptr, force != nullptr, false);
-    const size_t n = h.order.size();
-    for (size_t r = 0; r < n; ++r) {
-      const size_t s = h.order[r];
-      if (id) id[r] = h.id[s];
-      if (pos) {
-        pos[3 * r] = host_wrap1(h.pos[s].x, c->g.L[0]);
-        pos[3 * r + 1] = host_wrap1(h.pos[s].y, c->g.L[1]);
-        pos[3 * r + 2] = host_wrap1(h.pos[s].z, c->g.L[2]);
+      if (mass) {
+        ck(cudaMemcpyAsync(mass, dmass, nn * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+           "D2H mass");
       }
-      for (int k = 0; k < 3; ++k) {
-        if (vel) vel[3 * r + k] = h.v[k][s];
-        if (force) force[3 * r + k] = h.f[k][s];
+      ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    } else {
+      HostState h = fetch(c, pos != nullptr, vel != nullptr, force != nullptr, false,
+                          mass != nullptr);
+      const size_t n = h.order.size();
+      for (size_t r = 0; r < n; ++r) {
+        const size_t s = h.order[r];
+        if (ids_out) ids_out[r] = h.id[s];
+        if (pos) {
+          pos[3 * r] = host_wrap1(h.pos[s].x, c->g.L[0]);
+          pos[3 * r + 1] = host_wrap1(h.pos[s].y, c->g.L[1]);
+          pos[3 * r + 2] = host_wrap1(h.pos[s].z, c->g.L[2]);
+        }
+        for (int k = 0; k < 3; ++k) {
+          if (vel) vel[3 * r + k] = h.v[k][s];
+          if (force) force[3 * r + k] = h.f[k][s];
+        }
+        if (mass) mass[r] = h.mass[s];
+      }
+    }
+    if (type) {
+      if (c->type_val.empty()) {
+        std::fill(type, type + nn, 0);
+      } else {
+        for (size_t r = 0; r < nn; ++r) type[r] = type_of(c, ids_out[r]);
       }
     }
   });

@@ -803,9 +803,10 @@ __global__ void __launch_bounds__(kBlock)
     k_download(int n, const double4* __restrict__ pos, const double* __restrict__ vx,
                const double* __restrict__ vy, const double* __restrict__ vz,
                const double* __restrict__ fx, const double* __restrict__ fy,
-               const double* __restrict__ fz, const long long* __restrict__ id, long long lo,
-               Geom g, double* __restrict__ opos, double* __restrict__ ovel,
-               double* __restrict__ ofrc, long long* __restrict__ oid) {
+               const double* __restrict__ fz, const double* __restrict__ mass,
+               const long long* __restrict__ id, long long lo, Geom g,
+               double* __restrict__ opos, double* __restrict__ ovel, double* __restrict__ ofrc,
+               double* __restrict__ omass, long long* __restrict__ oid) {
   const int s = blockIdx.x * kBlock + threadIdx.x;
   if (s >= n) return;
   const long long ident = id[s];
@@ -827,6 +828,7 @@ __global__ void __launch_bounds__(kBlock)
     ofrc[3 * r + 1] = fy[s];
     ofrc[3 * r + 2] = fz[s];
   }
+  if (omass) omass[r] = mass[s];
 }
 
 // Per-step observable row (run_observed): PE and virial of this step's force

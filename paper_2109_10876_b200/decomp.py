@@ -265,7 +265,8 @@ class SlabContext:
         pos = np.empty((n, 3))
         vel = np.empty((n, 3))
         f = np.empty((n, 3))
-        self._c(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), _ptr(f)))
+        self._c(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), _ptr(f),
+                                               None, None))
         return ids, pos, vel, f
 
     def pairs(self) -> np.ndarray:

@@ -364,38 +364,46 @@ class Engine:
 
     # -- state access ----------------------------------------------------------
     def flatten(self, out: Optional[FlatConfig] = None) -> FlatConfig:
-        """flatten_domain (domain.hpp:193-207): sorted by id, wrapped.
+        """flatten_domain (domain.hpp:193-207): sorted by id, wrapped, with each
+        particle's type and mass as created.
 
         out: a FlatConfig whose id/pos/vel arrays (C-contiguous int64 (n,),
-        float64 (n, 3)) receive the state in place, e.g. buffers in pinned
-        host memory reused across downloads; it is returned."""
+        float64 (n, 3)) — and type (int32 (n,)) / mass (float64 (n,)) when not
+        None — receive the state in place, e.g. buffers in pinned host memory
+        reused across downloads; it is returned."""
         n = self._n
         if out is None:
             ids = np.empty(n, np.int64)
             pos = np.empty((n, 3))
             vel = np.empty((n, 3))
+            typ = np.empty(n, np.int32)
+            mass = np.empty(n)
         else:
-            ids, pos, vel = out.id, out.pos, out.vel
+            ids, pos, vel, typ, mass = out.id, out.pos, out.vel, out.type, out.mass
             for a, dt, shape in ((ids, np.int64, (n,)), (pos, np.float64, (n, 3)),
-                                 (vel, np.float64, (n, 3))):
+                                 (vel, np.float64, (n, 3)), (typ, np.int32, (n,)),
+                                 (mass, np.float64, (n,))):
+                if a is None:
+                    continue
                 if a.dtype != dt or a.shape != shape or not a.flags.c_contiguous \
                         or not a.flags.writeable:
                     raise ConfigError("flatten(out=...): id (n,) int64, pos/vel (n, 3) "
-                                      "float64, C-contiguous and writeable")
-        _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), None),
-               self._h)
+                                      "float64, type (n,) int32, mass (n,) float64, "
+                                      "C-contiguous and writeable")
+        _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), None,
+                                           _ptr(typ), _ptr(mass)), self._h)
         if out is not None:
             out.box = self.box.copy()
             return out
         bonds = None if self._keep.bonds is None else self._keep.bonds.copy()
-        return FlatConfig(self.box.copy(), ids, pos, vel, bonds=bonds)
+        return FlatConfig(self.box.copy(), ids, pos, vel, mass=mass, type=typ, bonds=bonds)
 
     def forces(self):
         """(ids, forces) of the last evaluation, sorted by id."""
         n = self._n
         ids = np.empty(n, np.int64)
         f = np.empty((n, 3))
-        _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), None, None, _ptr(f)),
+        _check(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), None, None, _ptr(f), None, None),
                self._h)
         return ids, f
 

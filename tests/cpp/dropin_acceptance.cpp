@@ -197,6 +197,56 @@ int main() {
             "max position spread " + std::to_string(worst) + ", rebuilds " +
                 std::to_string(g.rebuild_count()) + " / " + std::to_string(ref.rebuild_count()));
   }
+  // Engine(Domain, EngineConfig) + domain() + flatten() with mixed types and
+  // masses: the class-name-only switch of a reference caller
+  {
+    FlatConfig flat = gen_lattice(4096, 0.8442, 0.72, 11);
+    for (std::size_t k = 0; k < flat.size(); ++k) {
+      flat.type[k] = static_cast<std::int32_t>(k % 4);
+      flat.mass[k] = 1.0 + 0.5 * static_cast<double>(k % 3);
+    }
+    EngineConfig cfg;
+    cfg.dt = 0.005;
+    cfg.n_sub = 8;
+    Engine ref(build_domain(flat, lj_only(), 0.3, 8), cfg);
+    taskmd_gpu::Engine g(build_domain(flat, lj_only(), 0.3, 8), cfg);
+    ref.run(25);
+    g.run(25);
+    const FlatConfig a = flatten_domain(ref.domain());
+    const FlatConfig b = g.flatten();
+    const FlatConfig c = flatten_domain(g.domain());
+    bool same = a.id == b.id && a.type == b.type && a.mass == b.mass && c.id == a.id &&
+                c.type == a.type && c.mass == a.mass;
+    double worst = 0.0;
+    for (std::size_t k = 0; k < a.size() && same; ++k) {
+      worst = std::max({worst, std::abs(a.pos[k].x - b.pos[k].x), std::abs(a.vel[k].y - b.vel[k].y),
+                        std::abs(c.pos[k].z - b.pos[k].z)});
+    }
+    // forces read from the stores, as md_cli.cpp:230-240 does
+    std::map<std::int64_t, Vec3> fr, fg;
+    const Domain* doms[2] = {&ref.domain(), &g.domain()};
+    for (const Domain* d : doms) {
+      auto& dst = d == doms[0] ? fr : fg;
+      for (const Subnode& sn : d->subs) {
+        for (std::int32_t cidx : sn.interior) {
+          const CellSpan& span = sn.store.cells[cidx];
+          for (std::size_t k = span.begin; k < span.begin + span.real; ++k) {
+            dst[sn.store.id[k]] = sn.store.force(k);
+          }
+        }
+      }
+    }
+    double fworst = 0.0, fscale = 0.0;
+    for (const auto& [id, f] : fr) {
+      const Vec3& h = fg.at(id);
+      fscale = std::max({fscale, std::abs(f.x), std::abs(f.y), std::abs(f.z)});
+      fworst = std::max({fworst, std::abs(f.x - h.x), std::abs(f.y - h.y), std::abs(f.z - h.z)});
+    }
+    verdict("Engine(Domain) + domain() + flatten (types, masses)",
+            same && worst <= 1e-9 && fr.size() == flat.size() && fworst <= 1e-8 * fscale,
+            "ids/types/masses equal " + std::to_string(same) + ", max |dx| " +
+                std::to_string(worst) + ", max |dF| " + std::to_string(fworst));
+  }
   // criterion 3: NVE drift, N=4000 SC lattice, seed 3, T=0.6
   {
     const FlatConfig flat = gen_lattice(4000, 0.8442, 0.6, 3);

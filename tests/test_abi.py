@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
     assert sorted(_abi.EXPORTS) == names
-    assert L.tmd_gpu_abi_version() == 3
+    assert L.tmd_gpu_abi_version() == 4
 
 
 def test_library_is_sm100a_only():

@@ -81,7 +81,7 @@ def test_flatten_into_pinned_buffers_with_types_and_masses():
         np.testing.assert_array_equal(out.mass, flat.mass)
         with pytest.raises(E.ConfigError):
             eng.flatten(out=E.FlatConfig(flat.box, out.id, out.pos, out.vel,
-                                         type=np.empty(n, np.int64)))
+                                         type=np.empty(n + 1, np.int32)))
     finally:
         eng.close()
 

@@ -352,7 +352,6 @@ class SlabEngine {
              const GpuOptions& opt = {}, bool load_balance = false)
       : n_total_(static_cast<int64_t>(flat.size())), box_(flat.box) {
     CSystem cs(flat, inter, r_skin, cfg, opt);
-    cs.p.section_timers = 0;
     int rc = tmd_gpu_create_slab(&cs.sys, &cs.lj, cs.fene_ptr(), &cs.p, rank, nranks, &ctx_);
     if (rc != TMD_OK) throw_status(rc, tmd_gpu_last_error(nullptr));
     check(tmd_gpu_slab_attach_nccl(ctx_, id.data(), (load_balance ? 1 : 0) | 2));
@@ -378,6 +377,16 @@ class SlabEngine {
   }
   std::int64_t step_count() const { return tmd_gpu_step_count(ctx_); }
   std::uint64_t rebuild_count() const { return tmd_gpu_rebuild_count(ctx_); }
+  // Engine::timers (engine.hpp:145) of this rank's stream (CUDA-event phases
+  // of the native loop; GpuOptions::section_timers = false leaves only elapsed).
+  taskmd::SectionTimers timers() const {
+    taskmd::SectionTimers t;
+    double sec[5], el = 0.0;
+    check(tmd_gpu_timers(ctx_, sec, &el));
+    for (int k = 0; k < 5; ++k) t.seconds[k] = sec[k];
+    t.elapsed = el;
+    return t;
+  }
 
   // The particles this slab owns, sorted by id, positions wrapped, types and
   // masses as created.

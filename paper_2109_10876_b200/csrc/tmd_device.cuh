@@ -100,7 +100,29 @@ struct Ctrl {
   int halt;                   // native slab loop: a rebuild is due, later steps are no-ops
   double seen_d2;             // native slab loop: the global max |x - x_snap|^2 the last
                               // decision saw (the host sizes its next batch from it)
+  long long tick_base;        // section timers in graph mode: step count at the chunk
+                              // start (phase ticks are indexed by step - tick_base)
 };
+
+// Section timers without host round trips (graph mode, the native slab loop):
+// single-thread kernels of the step stamp %globaltimer into per-step phase
+// slots; the host turns consecutive stamps into the five SectionTimers.
+constexpr int kTickSteps = 256;      // steps a tick buffer holds (== a chunk)
+constexpr int kTickPhases = 4;       // per step: block start, decide, list build, forces
+enum : int { kTickBlock = 0, kTickDecide = 1, kTickBuild = 2, kTickForces = 3 };
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Stamps phase `ph` of the chunk-relative step ctrl->step - tick_base + off.
+__device__ __forceinline__ void stamp(const Ctrl* ctrl, long long* ticks, int ph, int off) {
+  if (!ticks) return;
+  const long long s = ctrl->step - ctrl->tick_base + off;
+  if (s >= 0 && s < kTickSteps) ticks[s * kTickPhases + ph] = global_ns();
+}
 
 // ---------------------------------------------------------------------------
 // Exact (non-contracted) FP64 helpers. nvcc contracts a*b+c into DFMA by

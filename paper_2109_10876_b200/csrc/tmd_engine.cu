@@ -320,6 +320,8 @@ struct tmd_gpu_ctx {
   std::vector<Span> ev_spans;
   int* rebuild_log = nullptr;     // device: rebuild decision per chunk step
   std::vector<int> h_rebuild_log;
+  long long* ticks = nullptr;     // device phase stamps (graph mode with section timers)
+  std::vector<long long> h_ticks;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   uint64_t launches = 0;  // kernels enqueued by this context (bench accounting)
 
@@ -376,7 +378,7 @@ void free_all(tmd_gpu_ctx* c) {
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
                   c->ck_fx, c->ck_fy, c->ck_fz,
-                  c->rebuild_log, c->cell_rank, c->brick_rank_off, c->ngroups,
+                  c->rebuild_log, c->ticks, c->cell_rank, c->brick_rank_off, c->ngroups,
                   c->group_off, c->decoded, c->scan_tmp, c->owner_of_z, c->mig_dest,
                   c->mig_count, c->mig_off, c->mig_keep, c->mig_send, c->mig_recv,
                   c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
@@ -449,12 +451,50 @@ void harvest_timers(tmd_gpu_ctx* c) {
   c->ev_used = 0;
 }
 
+// Graph mode: consecutive phase stamps of a chunk -> SectionTimers. The time
+// from a stamp to the next one is booked to the stamp's phase: block start
+// (the block's opening kick + drift) -> Integrate; decision -> Resort on
+// rebuild steps (decision + resort), else Neigh (the rebuild check); list
+// build -> Neigh; forces (+ fused integrator epilogue, observables) -> Forces.
+void harvest_ticks(tmd_gpu_ctx* c, int64_t steps) {
+  const auto& t = c->h_ticks;
+  const int64_t ns = std::min<int64_t>(steps, kTickSteps);
+  std::vector<std::pair<long long, int>> seq;  // (time, section)
+  for (int64_t s = 0; s < ns; ++s) {
+    const long long* p = t.data() + s * kTickPhases;
+    const bool rebuilt = p[kTickBuild] != 0;
+    if (p[kTickBlock]) seq.push_back({p[kTickBlock], TMD_SECTION_INTEGRATE});
+    if (p[kTickDecide]) {
+      seq.push_back({p[kTickDecide], rebuilt ? TMD_SECTION_RESORT : TMD_SECTION_NEIGH});
+    }
+    if (rebuilt) seq.push_back({p[kTickBuild], TMD_SECTION_NEIGH});
+    if (p[kTickForces]) seq.push_back({p[kTickForces], TMD_SECTION_FORCES});
+  }
+  const long long end = t[static_cast<size_t>(kTickSteps * kTickPhases)];
+  for (size_t k = 0; k < seq.size(); ++k) {
+    const long long next = k + 1 < seq.size() ? seq[k + 1].first : end;
+    if (next > seq[k].first) c->sec[seq[k].second] += 1e-9 * static_cast<double>(next - seq[k].first);
+  }
+}
+
 // --- kernel launch wrappers -------------------------------------------------
+// Phase stamps are taken in graph mode with section timers on (the eager
+// path times phases with CUDA events instead).
+long long* tick_ptr(const tmd_gpu_ctx* c) {
+  return c->timers_on && c->use_graphs ? c->ticks : nullptr;
+}
+
+void launch_tick(tmd_gpu_ctx* c, int phase, int off) {
+  if (!tick_ptr(c)) return;
+  c->launches += 1;
+  k_tick<<<1, 1, 0, c->ls>>>(c->ctrl, c->ticks, phase, off, -1);
+}
+
 void launch_decide(tmd_gpu_ctx* c, bool advance, int log_idx = -1) {
   c->launches += 1;
   k_decide<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr, advance ? 1 : 0,
                                log_idx >= 0 ? c->rebuild_log : nullptr, log_idx,
-                               c->cond_handle);
+                               c->cond_handle, advance ? tick_ptr(c) : nullptr);
 }
 
 // Exclusive scan of counts[0..n) into out[0..n] (3 tiled kernels).
@@ -571,7 +611,7 @@ void launch_bond_resolve(tmd_gpu_ctx* c) {
 void launch_build(tmd_gpu_ctx* c) {
   launch_bond_resolve(c);
   c->launches += 2;
-  k_build_prologue<<<1, 1, 0, c->ls>>>(c->ctrl);
+  k_build_prologue<<<1, 1, 0, c->ls>>>(c->ctrl, tick_ptr(c));
   if (c->variant == 1) {
     k_build_list<<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
@@ -977,6 +1017,7 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
                                    cudaStreamCaptureModeThreadLocal),
      "begin capture");
   c->ls = c->stream;
+  launch_tick(c, kTickBlock, 0);
   launch_kick_drift(c);
   uint64_t body = 0;
   for (int s = 0; s < nsteps; ++s) {
@@ -1012,6 +1053,7 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
     ck(cudaStreamUpdateCaptureDependencies(c->stream, &cnode, 1,
                                            cudaStreamSetCaptureDependencies),
        "cudaStreamUpdateCaptureDependencies");
+    launch_tick(c, kTickForces, -1);
     launch_forces(c, s + 1 < nsteps ? kFused : kKick2);
     launch_obs_record(c);
   }
@@ -1060,12 +1102,19 @@ void enqueue_segment(tmd_gpu_ctx* c, int64_t steps) {
 }
 
 bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
-  const bool graphs = c->use_graphs && !c->timers_on;
+  const bool graphs = c->use_graphs;
   if (c->obs_stride > 0) {
     ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
   }
   if (graphs) {
     if (c->graph_dirty) drop_graphs(c);
+    if (tick_ptr(c)) {
+      const long long base = c->step;
+      ck(cudaMemsetAsync(c->ticks, 0, sizeof(long long) * (kTickSteps * kTickPhases + 1),
+                         c->stream), "memset ticks");
+      ck(cudaMemcpyAsync(&c->ctrl->tick_base, &base, sizeof base, cudaMemcpyHostToDevice,
+                         c->stream), "H2D tick base");
+    }
     const long long rebuilds0 = c->h_ctrl->rebuilds;
     int64_t left = steps;
     while (left > 0) {
@@ -1087,11 +1136,20 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
       c->launches += sgr.fixed;
       left -= kind == 0 ? kGraphSteps : 1;
     }
+    if (tick_ptr(c)) {
+      c->launches += 1;
+      k_tick<<<1, 1, 0, c->stream>>>(c->ctrl, c->ticks, 0, 0, kTickSteps * kTickPhases);
+      c->h_ticks.resize(kTickSteps * kTickPhases + 1);
+      ck(cudaMemcpyAsync(c->h_ticks.data(), c->ticks, sizeof(long long) * c->h_ticks.size(),
+                         cudaMemcpyDeviceToHost, c->stream), "D2H ticks");
+    }
     ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
     sync_ctrl(c);
     c->launches += static_cast<uint64_t>(c->h_ctrl->rebuilds - rebuilds0) *
                    c->graph_body_kernels;
-    return (c->h_ctrl->status & kOverflowBits) == 0;
+    const bool ok = (c->h_ctrl->status & kOverflowBits) == 0;
+    if (ok && tick_ptr(c)) harvest_ticks(c, steps);
+    return ok;
   }
   enqueue_segment(c, steps);
   if (c->timers_on) {
@@ -1875,6 +1933,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     c->scalars = dalloc<double>(4);
     c->ctrl = dalloc<Ctrl>(1);
     c->rebuild_log = dalloc<int>(static_cast<size_t>(kChunk));
+    if (c->timers_on) c->ticks = dalloc<long long>(kTickSteps * kTickPhases + 1);
     mark("checkpoint arrays");
     ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost");
     ck(cudaMallocHost(&c->h_scalars, 4 * sizeof(double)), "cudaMallocHost");
@@ -2454,7 +2513,7 @@ int tmd_gpu_time_step_kernel(tmd_gpu_ctx* c, int reps, double* ms) {
 int tmd_gpu_prepare_graphs(tmd_gpu_ctx* c, int64_t obs_stride) {
   return guard(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    if (!c->use_graphs || c->timers_on || c->nranks > 1 || c->g.zslab) return;
+    if (!c->use_graphs || c->nranks > 1 || c->g.zslab) return;
     if (c->graph_dirty) drop_graphs(c);
     for (int kind = 0; kind < 2; ++kind) {
       auto& sgr = c->sg[kind][c->cur];

@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(kBlock)
 // Rebuild decision (Engine::step, engine.hpp:88-100): global OR of
 // needs_rebuild == max |dx|^2 > 0.25 skin^2 (strict), plus a host override.
 __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
-                         int log_idx, cudaGraphConditionalHandle cond) {
+                         int log_idx, cudaGraphConditionalHandle cond, long long* ticks) {
+  stamp(ctrl, ticks, kTickDecide, 0);
   const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
   // force_rebuild: 1 = host-forced (setup), 2 = forced after a rollback and
   // not counted (the reference would not have rebuilt here)
@@ -380,6 +381,16 @@ __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
   ctrl->max_d2 = 0ull;
   if (advance_step) ctrl->step += 1;
   if (advance_step && (force == 1 || m > thr)) ctrl->rebuilds += 1;
+}
+
+// A phase stamp on its own (block start: off 0; forces start: off -1, after
+// the step's decision advanced the counter; the chunk end: slot `end`).
+__global__ void k_tick(const Ctrl* ctrl, long long* ticks, int ph, int off, int end) {
+  if (end >= 0) {
+    ticks[end] = global_ns();
+    return;
+  }
+  stamp(ctrl, ticks, ph, off);
 }
 
 // ---------------------------------------------------------------------------
@@ -696,8 +707,9 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // Resets the per-build statistics before a build (only when rebuilding).
-__global__ void k_build_prologue(Ctrl* ctrl) {
+__global__ void k_build_prologue(Ctrl* ctrl, long long* ticks) {
   if (!ctrl->rebuild) return;
+  stamp(ctrl, ticks, kTickBuild, -1);
   ctrl->max_count = 0;
   ctrl->entries = 0;
 }

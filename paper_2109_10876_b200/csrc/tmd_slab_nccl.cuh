@@ -34,6 +34,8 @@
 
 #include <unistd.h>
 
+#include <optional>
+
 #include "tmd_comm.cuh"
 
 namespace {
@@ -255,6 +257,8 @@ constexpr int kRowInts = 5;  // nb0, nb1, n_own, n_cap, ipc_gen
 void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   const int R = c->nranks, r = c->my_rank;
   const size_t uR = static_cast<size_t>(R);
+  std::optional<Phase> ph;
+  ph.emplace(c, TMD_SECTION_RESORT);
   rck(c, tmd_gpu_slab_decide(c, 1, advance ? 1 : 0));
   if (c->balance_count) nccl_rebalance(c);
   // 1. classify; the leaver-count matrix M[s][d] all-gathered from the device
@@ -301,6 +305,7 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   c->mig_nrecv = nrecv;
   const size_t rec = sizeof(MigRec);
   SlabComm* cm = comm(c);
+  ph.emplace(c, TMD_SECTION_COMM);
   cm->group_start();
   for (int d = 0; d < R; ++d) {
     const int m = M[static_cast<size_t>(r) * uR + d];
@@ -320,6 +325,7 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   }
   cm->group_end(c->stream);
   // 3. commit on the device; one row per rank all-gathered
+  ph.emplace(c, TMD_SECTION_RESORT);
   slab_commit_launch(c);
   const int dxy = c->g.dims[0] * c->g.dims[1];
   int* row = Md;                 // this rank's row
@@ -341,9 +347,12 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   void* gl[3];
   void* gh[3];
   rck(c, tmd_gpu_slab_ghost_in(c, at(lo, 1), at(hi, 0), gl, gh));
+  ph.emplace(c, TMD_SECTION_COMM);
   nccl_ghost_exchange(c, false);
+  ph.emplace(c, TMD_SECTION_NEIGH);
   rck(c, tmd_gpu_slab_ghosts_ready(c));
   if (!c->fused_halo) return;
+  ph.emplace(c, TMD_SECTION_COMM);
   // 5. peer addresses of the fused halo: q's lower ghost layer starts at its
   // owned count, its upper one after the lower (= its lower neighbour's top
   // border)
@@ -559,28 +568,46 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
     }
     ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
     const int64_t start = c->step, target = c->step + nsteps;
-    if (c->n > 0) launch_kick_drift(c);
-    nccl_halo(c);
+    {
+      Phase p(c, TMD_SECTION_INTEGRATE);
+      if (c->n > 0) launch_kick_drift(c);
+    }
+    {
+      Phase p(c, TMD_SECTION_COMM);
+      nccl_halo(c);
+    }
     int64_t done_step = start;  // steps completed (host view)
     int64_t K_next = kSpecSteps;
     while (done_step < target) {
       const int64_t K = std::min<int64_t>(K_next, target - done_step);
       int64_t fused_launches = 0;
       for (int64_t s = 0; s < K; ++s) {
-        comm(c)->allreduce(&c->ctrl->max_d2, 1, CType::kU64, COp::kMax, c->stream);
-        c->launches += 1;
-        k_decide_spec<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr);
+        {
+          Phase p(c, TMD_SECTION_COMM);  // the global rebuild test's all-reduce
+          comm(c)->allreduce(&c->ctrl->max_d2, 1, CType::kU64, COp::kMax, c->stream);
+        }
+        {
+          Phase p(c, TMD_SECTION_NEIGH);
+          c->launches += 1;
+          k_decide_spec<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr);
+        }
         const bool last = done_step + s + 1 == target;
-        c->launches += 1;
         const bool fh = fused(c);  // the force epilogue delivers the halo itself
-        launch_forces(c, last ? kKick2 : kFused);
-        launch_obs_record(c);
+        {
+          Phase p(c, TMD_SECTION_FORCES);
+          launch_forces(c, last ? kKick2 : kFused);
+          launch_obs_record(c);
+        }
         if (!last) {
           ++fused_launches;
-          if (!fh) nccl_halo(c);
+          if (!fh) {
+            Phase p(c, TMD_SECTION_COMM);
+            nccl_halo(c);
+          }
         }
       }
       sync_ctrl(c);
+      harvest_timers(c);
       raise_physics(c, true);
       collect_slab_obs(c);
       if (c->h_ctrl->status & kStatStray) throw CudaFail{"slab: particle outside its slab"};
@@ -604,9 +631,15 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
       nccl_rebuild(c, true);  // counts the step and the rebuild
       const bool last = done_step + 1 == target;
       const bool fh = fused(c);
-      launch_forces(c, last ? kKick2 : kFused);
-      launch_obs_record(c);
-      if (!last && !fh) nccl_halo(c);
+      {
+        Phase p(c, TMD_SECTION_FORCES);
+        launch_forces(c, last ? kKick2 : kFused);
+        launch_obs_record(c);
+      }
+      if (!last && !fh) {
+        Phase p(c, TMD_SECTION_COMM);
+        nccl_halo(c);
+      }
       done_step += 1;
       if (c->last_rebuild_step >= 0) c->rebuild_gap = done_step - c->last_rebuild_step;
       c->last_rebuild_step = done_step;
@@ -614,6 +647,7 @@ void slab_run_impl(tmd_gpu_ctx* c, int64_t nsteps) {
     }
     ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
     sync_ctrl(c);
+    harvest_timers(c);
     raise_physics(c, true);
     collect_slab_obs(c);
     float ms = 0.f;

@@ -141,7 +141,7 @@ class SlabContext:
         sys = _system(flat)
         lj, fene = _interactions(inter)
         p = _engine_params(cfg, r_skin, device)
-        p.section_timers = 0
+        p.section_timers = 1 if cfg.section_timers else 0  # native loop: CUDA-event phases
         p.reserved[0] = 0
         h = C.c_void_p()
         _check(L.tmd_gpu_create_slab(C.byref(sys), C.byref(lj),
@@ -760,6 +760,20 @@ class DecomposedEngine:
         tot = self.comm.allreduce_sum({r: c.sums() for r, c in self.ctx.items()})
         pe, w, ke = (float(v) for v in tot)
         return StepObservables(self.steps, ke, pe, 2.0 * ke / (3.0 * self.n_total), w)
+
+    def timers(self):
+        """SectionTimers of the native loop (engine.hpp:145): per section the
+        largest of this process's ranks (each rank times its own stream with
+        CUDA events; the Python protocol fills none)."""
+        from .engine import SectionTimers
+        secs, el = np.zeros(5), 0.0
+        for c in self.ctx.values():
+            s5 = np.zeros(5)
+            e = C.c_double()
+            _check(_abi.lib().tmd_gpu_timers(c._h, _ptr(s5), C.byref(e)), c._h)
+            secs = np.maximum(secs, s5)
+            el = max(el, e.value)
+        return SectionTimers(secs, el)
 
     def step_count(self) -> int:
         return self.steps

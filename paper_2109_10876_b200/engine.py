@@ -149,6 +149,10 @@ class EngineConfig:
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off
     force_cap: float = 0.0
+    # step blocks run as CUDA graphs (section timers, when on, from device
+    # phase stamps); False: every kernel launched eagerly (timers from CUDA
+    # events) — bitwise the same results
+    graphs: bool = True
 
 
 @dataclass
@@ -256,6 +260,7 @@ def _engine_params(cfg: EngineConfig, r_skin: float, device: int) -> "_abi.TmdEn
     p.reserved[3] = int(cfg.build)
     p.reserved[4] = int(cfg.lanes)
     p.reserved[1] = int(cfg.unroll)
+    p.reserved[2] = 0 if cfg.graphs else 1
     p.force_cap = float(cfg.force_cap)
     if cfg.thermostat is not None:
         p.thermostat = 1

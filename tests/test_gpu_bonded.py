@@ -59,7 +59,7 @@ def test_initial_state_vs_golden(name, variant):
 @pytest.mark.parametrize("graphs,build", [(True, 0), (False, 0), (True, 3), (True, 5)])
 def test_trajectory_vs_golden(name, graphs, build):
     g = load(name)
-    eng = engine(g, section_timers=not graphs, build=build)
+    eng = engine(g, graphs=graphs, build=build)
     steps = int(g["steps"])
     every = max(1, steps // len(g["trace"]))
     for row in g["trace"]:

@@ -192,3 +192,23 @@ def test_a_failing_rank_releases_its_peers():
     with pytest.raises(E.PhysicsError, match="overlapping particles"):
         DecomposedEngine(flat, E.Interactions(), float(g["r_skin"]),
                          E.EngineConfig(dt=float(g["dt"])), comm=InProcessComm(3), native=True)
+
+
+def test_native_loop_section_timers():
+    """SectionTimers of the native loop (CUDA-event phases on each rank's
+    stream): Forces, Comm (rebuild-test all-reduce, migration, ghosts),
+    Integrate, Neigh (decision, list build) and Resort are filled and add up
+    to about the elapsed time."""
+    flat = E.gen_fcc(10, 0.8442, 1.0, 3)
+    dec = DecomposedEngine(flat, E.Interactions(), 0.3,
+                           E.EngineConfig(dt=0.005, section_timers=True),
+                           comm=InProcessComm(3), native=True)
+    try:
+        dec.run(120)
+        t = dec.timers()
+        assert dec.rebuild_count() > 5
+        for sec in E.Section:
+            assert t[sec] > 0.0, sec
+        assert 0.5 * t.elapsed <= t.section_sum() <= 1.05 * t.elapsed, t
+    finally:
+        dec.close()

@@ -433,7 +433,7 @@ def test_graph_mode_is_bitwise_identical_to_eager(variant):
     branch is a device-evaluated conditional node; the result must equal the
     eagerly launched run bit for bit (same kernels, same order)."""
     f = E.gen_fcc(8, 0.8442, 1.0, 777)
-    eager = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(variant=variant))
+    eager = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(variant=variant, graphs=False))
     graph = E.Engine(f, E.Interactions(), 0.3,
                      E.EngineConfig(variant=variant, section_timers=False))
     for chunk in (40, 15, 3, 97):
@@ -605,3 +605,30 @@ def test_rounding_band_pairs_match_the_reference(ref, seed):
                        E.EngineConfig(build=build))
         np.testing.assert_array_equal(eng.pairs(), want)
         eng.close()
+
+
+def test_section_timers_in_graph_mode():
+    """SectionTimers on the production path (CUDA graphs): the device stamps
+    each phase of each step (%globaltimer), so the five sections are filled
+    without eager launches — they add up to the elapsed time, Resort is
+    booked only on rebuild steps, and the split agrees with the eager
+    (CUDA-event) timers."""
+    f = E.gen_fcc(12, 0.8442, 1.0, 4)
+    res = {}
+    for graphs in (True, False):
+        eng = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(section_timers=True,
+                                                                graphs=graphs))
+        eng.run(300)
+        t = eng.timers()
+        assert eng.rebuild_count() > 10
+        for sec in E.Section:
+            if sec != E.Section.kComm:
+                assert t[sec] > 0.0, (graphs, sec)
+        assert t[E.Section.kComm] == 0.0
+        assert 0.7 * t.elapsed <= t.section_sum() <= 1.02 * t.elapsed, (graphs, t)
+        res[graphs] = t
+        eng.close()
+    g, e = res[True], res[False]
+    # the graph run is the faster one, and its Forces share is the larger
+    assert g.elapsed < e.elapsed
+    assert g[E.Section.kForces] / g.section_sum() > 0.5 * e[E.Section.kForces] / e.section_sum()

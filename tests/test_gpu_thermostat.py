@@ -45,7 +45,7 @@ def test_initial_forces_include_step0_noise(name):
 @pytest.mark.parametrize("graphs", [True, False])
 def test_trajectory_vs_golden(name, graphs):
     g = load(name)
-    eng = engine(g, section_timers=not graphs)
+    eng = engine(g, graphs=graphs)
     steps = int(g["steps"])
     every = max(1, steps // len(g["trace"]))
     for row in g["trace"]:
@@ -64,7 +64,7 @@ def test_graph_and_eager_are_bitwise_identical():
     g = load("langevin_fcc8")
     outs = []
     for timers in (True, False):
-        eng = engine(g, section_timers=timers)
+        eng = engine(g, graphs=not timers)
         eng.run(37)
         outs.append(eng.flatten())
     np.testing.assert_array_equal(outs[0].pos, outs[1].pos)

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -27,7 +28,9 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <type_traits>
+#include <unordered_set>
 #include <utility>
 #include <vector>
 
@@ -862,14 +865,30 @@ void choose_build_kind(tmd_gpu_ctx* c) {
   c->graph_dirty = true;
 }
 
+// TMD_DEBUG_TIMING: synchronise and print the time since the last mark (the
+// create() breakdown; no effect otherwise).
+void debug_mark(tmd_gpu_ctx* c, const char* what) {
+  if (!std::getenv("TMD_DEBUG_TIMING")) return;
+  static thread_local auto prev = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(c->stream);
+  const auto t = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[tmd setup ] %-24s %8.2f ms\n", what,
+               std::chrono::duration<double, std::milli>(t - prev).count());
+  prev = t;
+}
+
 void setup_pass(tmd_gpu_ctx* c) {
+  debug_mark(c, "setup start");
   for (;;) {
     set_force_rebuild(c);
     launch_decide(c, false);
     launch_resort(c);
+    debug_mark(c, "resort");
     if (c->build_auto) choose_build_kind(c);
+    debug_mark(c, "build kind");
     launch_build(c);
     sync_ctrl(c);
+    debug_mark(c, "build");
     raise_physics(c, false);
     if (c->h_ctrl->status & kOverflowBits) {
       const Ctrl h = *c->h_ctrl;
@@ -889,10 +908,12 @@ void setup_pass(tmd_gpu_ctx* c) {
       launch_build(c);
     }
   }
+  debug_mark(c, "cap");
   launch_forces(c);
   launch_thermo_init(c);
   launch_reduce_pe(c);
   sync_ctrl(c);
+  debug_mark(c, "forces");
   raise_physics(c, false);
 }
 
@@ -1238,107 +1259,199 @@ int guard(tmd_gpu_ctx* c, F&& fn) {
   }
 }
 
-void validate(const tmd_system* s, const tmd_lj_params* lj,
-              const tmd_fene_params* fene, const tmd_engine_params* p) {
-  auto cfg = [](const std::string& m) { throw StatusError{TMD_ERR_CONFIG, m}; };
-  if (!s || !lj || !p) cfg("null argument");
-  if (fene) {  // validate_fene (potentials.hpp:84-91)
-    if (!(fene->k > 0.0) || !std::isfinite(fene->k)) cfg("fene k must be finite and positive");
-    if (!(fene->r_max > 0.0) || !std::isfinite(fene->r_max))
-      cfg("fene r_max must be finite and positive");
+// ---- validation (build_domain's checks, domain.hpp:134-168, in its order:
+// validate_flat = box, then per particle in input order a duplicate id or a
+// non-positive mass, then the topology's ids (flat_config.hpp:42-61,
+// topology.hpp:33-52); then the interaction / skin / bond-reach / sentinel
+// checks, the cell grid, and the Engine ctor's validate_engine_config).
+
+[[noreturn]] void cfg_error(const std::string& m) { throw StatusError{TMD_ERR_CONFIG, m}; }
+
+// Arguments the reference cannot get wrong (null arrays, sizes).
+void validate_args(const tmd_system* s, const tmd_lj_params* lj, const tmd_engine_params* p) {
+  if (!s || !lj || !p) cfg_error("null argument");
+  if (s->n < 0) cfg_error("negative particle count");
+  if (s->n > kMaxSlots) {
+    cfg_error("system too large for one GPU context: " + std::to_string(s->n) +
+              " particles > " + std::to_string(kMaxSlots));
   }
+  if (s->n > 0 && (!s->id || !s->pos)) cfg_error("id and pos arrays are required");
+  if (s->n_bonds < 0 || (s->n_bonds > 0 && !s->bonds)) cfg_error("bond array missing");
+}
+
+// validate_box (box.hpp:21-29)
+void validate_box3(const double box[3]) {
   for (int k = 0; k < 3; ++k) {
-    // validate_box (box.hpp:21-29)
-    if (!std::isfinite(s->box[k]) || s->box[k] <= 0.0) {
-      cfg("box lengths must be finite and positive, got " + fmt_g(s->box[k]));
+    if (!std::isfinite(box[k]) || box[k] <= 0.0) {
+      cfg_error("box lengths must be finite and positive, got " + fmt_g(box[k]));
     }
   }
+}
+
+// Everything after validate_flat that needs no per-particle pass.
+void validate_params(const tmd_system* s, const tmd_lj_params* lj,
+                     const tmd_fene_params* fene, const tmd_engine_params* p) {
   // validate_lj (potentials.hpp:28-38)
   if (!(lj->epsilon > 0.0) || !std::isfinite(lj->epsilon))
-    cfg("lj epsilon must be finite and positive");
+    cfg_error("lj epsilon must be finite and positive");
   if (!(lj->sigma > 0.0) || !std::isfinite(lj->sigma))
-    cfg("lj sigma must be finite and positive");
+    cfg_error("lj sigma must be finite and positive");
   if (!(lj->r_cut > 0.0) || !std::isfinite(lj->r_cut))
-    cfg("lj r_cut must be finite and positive");
+    cfg_error("lj r_cut must be finite and positive");
+  if (fene) {  // validate_fene (potentials.hpp:84-91)
+    if (!(fene->k > 0.0) || !std::isfinite(fene->k)) cfg_error("fene k must be finite and positive");
+    if (!(fene->r_max > 0.0) || !std::isfinite(fene->r_max))
+      cfg_error("fene r_max must be finite and positive");
+  }
   if (!std::isfinite(p->r_skin) || p->r_skin < 0.0)
-    cfg("skin radius must be finite and non-negative");
-  // validate_engine_config (engine.hpp:28-41)
-  if (!std::isfinite(p->dt) || p->dt == 0.0)
-    cfg("time step must be finite and nonzero");
-  if (p->thermostat) {  // validate_langevin (potentials.hpp:180-189)
-    if (!(p->gamma >= 0.0) || !std::isfinite(p->gamma))
-      cfg("langevin gamma must be finite and >= 0");
-    if (!(p->temperature >= 0.0) || !std::isfinite(p->temperature))
-      cfg("langevin temperature must be finite and >= 0");
-  }
-  if (s->n < 0) cfg("negative particle count");
-  if (s->n > kMaxSlots) {
-    cfg("system too large for one GPU context: " + std::to_string(s->n) +
-        " particles > " + std::to_string(kMaxSlots));
-  }
-  if (s->n > 0 && (!s->id || !s->pos)) cfg("id and pos arrays are required");
-  // validate_flat (flat_config.hpp:42-61): unique ids, positive masses
-  // unique ids: O(n) with a bitmap when they fill a dense range (the usual
-  // 0..n-1), else by sorting
-  int64_t id_lo = 0, id_hi = -1;
-  if (s->n > 0) {
-    const auto mm = std::minmax_element(s->id, s->id + s->n);
-    id_lo = *mm.first;
-    id_hi = *mm.second;
-  }
-  const bool dense = static_cast<uint64_t>(id_hi - id_lo) < static_cast<uint64_t>(s->n);
-  std::vector<int64_t> ids;
-  if (dense) {
-    std::vector<unsigned char> seen(static_cast<size_t>(s->n), 0);
-    for (int64_t k = 0; k < s->n; ++k) {
-      unsigned char& b = seen[static_cast<size_t>(s->id[k] - id_lo)];
-      if (b) cfg("duplicate particle id " + std::to_string(s->id[k]));
-      b = 1;
-    }
-  } else {
-    ids.assign(s->id, s->id + s->n);
-    std::sort(ids.begin(), ids.end());
-    for (size_t k = 1; k < ids.size(); ++k) {
-      if (ids[k] == ids[k - 1]) cfg("duplicate particle id " + std::to_string(ids[k]));
-    }
-  }
-  auto known = [&](int64_t v) {
-    return dense ? (v >= id_lo && v <= id_hi) : std::binary_search(ids.begin(), ids.end(), v);
-  };
-  if (s->mass) {
-    for (int64_t k = 0; k < s->n; ++k) {
-      if (!(s->mass[k] > 0.0)) {
-        cfg("particle id " + std::to_string(s->id[k]) + " has non-positive mass");
-      }
-    }
-  }
-  if (!std::isfinite(p->force_cap) || p->force_cap < 0.0) {
-    cfg("force cap must be finite and non-negative");
-  }
-  // topology (validate_topology, topology.hpp:33-52; build_domain,
-  // domain.hpp:145-159)
-  if (s->n_bonds < 0 || (s->n_bonds > 0 && !s->bonds)) cfg("bond array missing");
-  if (s->n_bonds > 0) {
-    for (int64_t k = 0; k < s->n_bonds; ++k) {
-      const int64_t a = s->bonds[2 * k], b = s->bonds[2 * k + 1];
-      const bool ha = known(a);
-      const bool hb = known(b);
-      if (!ha || !hb) {
-        cfg("bond references unknown particle id " + std::to_string(ha ? b : a));
-      }
-      if (a == b) cfg("bond connects particle id " + std::to_string(a) + " to itself");
-    }
-    if (!fene) cfg("topology has bonds but no bond parameters configured");
-    if (fene->r_max > lj->r_cut + p->r_skin) {
-      cfg("bond r_max exceeds r_cut + r_skin; bonded partners could leave the ghost shell");
-    }
+    cfg_error("skin radius must be finite and non-negative");
+  if (s->n_bonds > 0 && !fene) cfg_error("topology has bonds but no bond parameters configured");
+  if (s->n_bonds > 0 && fene->r_max > lj->r_cut + p->r_skin) {
+    cfg_error("bond r_max exceeds r_cut + r_skin; bonded partners could leave the ghost shell");
   }
   // build_domain's sentinel guard (domain.hpp:162-168), kept for parity of
   // accepted inputs
   const double max_len = std::max({s->box[0], s->box[1], s->box[2]});
   if (max_len > 0.1 * 1.0e9) {
-    cfg("box too large: positions could alias the padding sentinel coordinate");
+    cfg_error("box too large: positions could alias the padding sentinel coordinate");
   }
+}
+
+// validate_engine_config (engine.hpp:28-41) + the GPU path's own knob.
+void validate_engine(const tmd_engine_params* p) {
+  if (!std::isfinite(p->dt) || p->dt == 0.0) cfg_error("time step must be finite and nonzero");
+  if (p->thermostat) {  // validate_langevin (potentials.hpp:180-189)
+    if (!(p->gamma >= 0.0) || !std::isfinite(p->gamma))
+      cfg_error("langevin gamma must be finite and >= 0");
+    if (!(p->temperature >= 0.0) || !std::isfinite(p->temperature))
+      cfg_error("langevin temperature must be finite and >= 0");
+  }
+  if (!std::isfinite(p->force_cap) || p->force_cap < 0.0) {
+    cfg_error("force cap must be finite and non-negative");
+  }
+}
+
+// Splits [0, n) over up to 16 host threads (chunks of >= 1M particles).
+template <class F>
+void parallel_chunks(int64_t n, F&& fn) {
+  const int64_t hw = std::max<int64_t>(1, std::thread::hardware_concurrency());
+  const int64_t T = std::min<int64_t>(std::min<int64_t>(hw, 16), std::max<int64_t>(1, n >> 20));
+  if (T <= 1) {
+    fn(0, int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  for (int64_t t = 0; t < T; ++t) {
+    ts.emplace_back([&, t] { fn(static_cast<int>(t), n * t / T, n * (t + 1) / T); });
+  }
+  for (auto& t : ts) t.join();
+}
+
+struct IdRange {
+  int64_t lo = 0, hi = -1;
+  bool dense = false;  // hi - lo < n: a bitmap over [lo, hi] decides uniqueness
+};
+
+IdRange id_range(const tmd_system* s) {
+  IdRange r;
+  if (s->n <= 0) return r;
+  std::vector<std::pair<int64_t, int64_t>> part(16, {INT64_MAX, INT64_MIN});
+  parallel_chunks(s->n, [&](int t, int64_t b, int64_t e) {
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    for (int64_t k = b; k < e; ++k) {
+      lo = std::min(lo, static_cast<int64_t>(s->id[k]));
+      hi = std::max(hi, static_cast<int64_t>(s->id[k]));
+    }
+    part[static_cast<size_t>(t)] = {lo, hi};
+  });
+  r.lo = INT64_MAX;
+  r.hi = INT64_MIN;
+  for (const auto& p : part) {
+    r.lo = std::min(r.lo, p.first);
+    r.hi = std::max(r.hi, p.second);
+  }
+  r.dense = static_cast<uint64_t>(r.hi - r.lo) < static_cast<uint64_t>(s->n);
+  return r;
+}
+
+// validate_flat's per-particle checks + validate_topology, serially in the
+// reference's order (the first failing particle in input order; then the
+// first failing bond). Throws the reference's message.
+void validate_particles_exact(const tmd_system* s, const IdRange& r) {
+  std::vector<unsigned char> seen;
+  std::unordered_set<int64_t> set;
+  if (r.dense) {
+    seen.assign(static_cast<size_t>(s->n), 0);
+  } else {
+    set.reserve(static_cast<size_t>(s->n));
+  }
+  for (int64_t k = 0; k < s->n; ++k) {
+    const int64_t id = s->id[k];
+    bool dup;
+    if (r.dense) {
+      unsigned char& b = seen[static_cast<size_t>(id - r.lo)];
+      dup = b != 0;
+      b = 1;
+    } else {
+      dup = !set.insert(id).second;
+    }
+    if (dup) cfg_error("duplicate particle id " + std::to_string(id));
+    if (s->mass && !(s->mass[k] > 0.0)) {
+      cfg_error("particle id " + std::to_string(id) + " has non-positive mass");
+    }
+  }
+  auto known = [&](int64_t v) {
+    if (r.dense) return v >= r.lo && v <= r.hi && seen[static_cast<size_t>(v - r.lo)] != 0;
+    return set.count(v) != 0;
+  };
+  for (int64_t k = 0; k < s->n_bonds; ++k) {
+    const int64_t a = s->bonds[2 * k], b = s->bonds[2 * k + 1];
+    const bool ha = known(a), hb = known(b);
+    if (!ha || !hb) cfg_error("bond references unknown particle id " + std::to_string(ha ? b : a));
+    if (a == b) cfg_error("bond connects particle id " + std::to_string(a) + " to itself");
+  }
+}
+
+// The same checks as a parallel pass that only answers "all good?" (a
+// failure re-runs validate_particles_exact for the reference's message).
+bool particles_ok_fast(const tmd_system* s, const IdRange& r) {
+  if (s->n <= 0) return s->n_bonds == 0;
+  std::atomic<bool> bad{false};
+  std::vector<uint64_t> bits;
+  std::vector<int64_t> sorted;
+  if (r.dense) {
+    bits.assign(static_cast<size_t>((s->n + 63) / 64), 0ull);
+  } else {
+    sorted.assign(s->id, s->id + s->n);
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) return false;
+  }
+  parallel_chunks(s->n, [&](int, int64_t b, int64_t e) {
+    bool my_bad = false;
+    for (int64_t k = b; k < e; ++k) {
+      if (r.dense) {
+        const uint64_t idx = static_cast<uint64_t>(s->id[k] - r.lo);
+        const uint64_t bit = 1ull << (idx & 63);
+        const uint64_t old = __atomic_fetch_or(&bits[idx >> 6], bit, __ATOMIC_RELAXED);
+        my_bad |= (old & bit) != 0;
+      }
+      if (s->mass) my_bad |= !(s->mass[k] > 0.0);
+    }
+    if (my_bad) bad.store(true, std::memory_order_relaxed);
+  });
+  if (bad.load()) return false;
+  for (int64_t k = 0; k < s->n_bonds; ++k) {
+    const int64_t a = s->bonds[2 * k], b = s->bonds[2 * k + 1];
+    for (int64_t v : {a, b}) {
+      const bool ok = r.dense ? (v >= r.lo && v <= r.hi &&
+                                 ((bits[static_cast<size_t>(v - r.lo) >> 6] >>
+                                   (static_cast<uint64_t>(v - r.lo) & 63)) & 1ull))
+                              : std::binary_search(sorted.begin(), sorted.end(), v);
+      if (!ok) return false;
+    }
+    if (a == b) return false;
+  }
+  return true;
 }
 
 // Brick decomposition of the cell grid (bricks of up to 2x2x2 cells), the
@@ -1713,15 +1826,14 @@ void setup_bonds(tmd_gpu_ctx* c, const tmd_system* sys, const tmd_fene_params* f
 }
 
 // The type column of the caller's FlatConfig, kept by id (see tmd_gpu_ctx).
-void set_type_table(tmd_gpu_ctx* c, const tmd_system* sys) {
+void set_type_table(tmd_gpu_ctx* c, const tmd_system* sys, const IdRange& r) {
   c->type_id.clear();
   c->type_val.clear();
   const size_t n = static_cast<size_t>(sys->n);
   if (!sys->type || n == 0) return;
   if (std::all_of(sys->type, sys->type + n, [](int32_t t) { return t == 0; })) return;
-  const auto mm = std::minmax_element(sys->id, sys->id + n);
-  if (static_cast<unsigned long long>(*mm.second - *mm.first) == n - 1) {
-    c->type_lo = *mm.first;
+  if (static_cast<unsigned long long>(r.hi - r.lo) == n - 1) {
+    c->type_lo = r.lo;
     c->type_val.assign(n, 0);
     for (size_t k = 0; k < n; ++k) c->type_val[static_cast<size_t>(sys->id[k] - c->type_lo)] = sys->type[k];
     return;
@@ -1760,12 +1872,26 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     t_prev = t;
   };
   const int rc = guard(c, [&] {
-    validate(sys, lj, fene, params);
-    mark("validate");
-    set_type_table(c, sys);
+    validate_args(sys, lj, params);
+    validate_box3(sys->box);
+    try {  // (ConfigErrors before any CUDA call)
+      validate_params(sys, lj, fene, params);
+      build_geom(c, sys->box, lj->r_cut, params->r_skin);
+      validate_engine(params);
+    } catch (const StatusError&) {
+      // build_domain checks the particles (validate_flat) before these
+      validate_particles_exact(sys, id_range(sys));
+      throw;
+    }
+    mark("validate params");
+    const IdRange idr = id_range(sys);
+    mark("id range");
+    // per-particle checks on the host threads (the exact serial pass only
+    // to name the reference's first error); still before any CUDA call
+    if (!particles_ok_fast(sys, idr)) validate_particles_exact(sys, idr);
+    mark("validate particles");
+    set_type_table(c, sys, idr);
     mark("type table");
-    build_geom(c, sys->box, lj->r_cut, params->r_skin);  // ConfigError before any CUDA call
-    mark("geometry");
     int ndev = 0;
     ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     mark("device count");
@@ -1907,10 +2033,12 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       want(c->ck_fz, n);
     }
     if (!slab) want(c->dl, 11 * n);  // download / upload scratch
+    mark("plan");
     if (!slab) {
       size_t tot = 0;
       for (const auto& e : plan) tot += (e.second + 255) / 256 * 256;
       c->arena = static_cast<char*>(big_alloc(tot, &c->arena_bytes));
+      mark("arena");
       size_t off = 0;
       for (const auto& e : plan) {
         *e.first = c->arena + off;
@@ -1954,10 +2082,9 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       // the caller's arrays as they are, unpacked on the device (double4
       // positions, SoA velocities); ids a dense range -> device download
       if (m > 0) {
-        const auto mm = std::minmax_element(sys->id, sys->id + m);
-        c->ids_dense = static_cast<unsigned long long>(*mm.second - *mm.first) ==
+        c->ids_dense = static_cast<unsigned long long>(idr.hi - idr.lo) ==
                        static_cast<unsigned long long>(m - 1);
-        c->dl_lo = *mm.first;
+        c->dl_lo = idr.lo;
         ck(cudaMemcpyAsync(c->dl, sys->pos, 3 * m * sizeof(double), cudaMemcpyHostToDevice,
                            c->stream), "H2D pos");
         if (sys->vel) {
@@ -1975,7 +2102,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
             sys->mass ? c->dl + 6 * m : nullptr, c->posb[0], c->vx, c->vy, c->vz, c->mass);
         ck(cudaGetLastError(), "k_upload");
       }
-      mark("upload");
+      mark("upload enqueued");
     } else {
       std::vector<double4> hp(m);
       std::vector<double> hv(3 * m, 0.0), hm(m, 1.0);

@@ -206,3 +206,41 @@ def test_local_group_handle_lifecycle():
     assert L.tmd_local_group_create(0, C.byref(g)) == _abi.TMD_ERR_CONFIG
     assert L.tmd_local_group_create(4, C.byref(g)) == _abi.TMD_OK and g.value
     L.tmd_local_group_destroy(g)
+
+
+@pytest.mark.parametrize("mutate,match", [
+    # build_domain runs validate_flat before validate_lj (domain.hpp:137-141)
+    (lambda f, i: (setattr(f, "id", np.array([0, 1, 2, 3, 4, 5, 6, 6])),
+                   setattr(i.lj, "epsilon", 0.0)), "duplicate particle id 6"),
+    # the first failing particle in input order: a mass at index 3 before a
+    # duplicate at index 7 (flat_config.hpp:50-58)
+    (lambda f, i: (setattr(f, "id", np.array([0, 1, 2, 3, 4, 5, 6, 6])),
+                   setattr(f, "mass", np.array([1, 1, 1, 0.0, 1, 1, 1, 1.0]))),
+     "id 3 has non-positive mass"),
+    (lambda f, i: (setattr(f, "id", np.array([0, 1, 2, 2, 4, 5, 6, 7])),
+                   setattr(f, "mass", np.array([1, 1, 1, 1, 1, 1, 1, 0.0]))),
+     "duplicate particle id 2"),
+    # sparse ids take the hash-set path
+    (lambda f, i: setattr(f, "id", np.array([10, 900, 7, 55, 3, 900, 1, 2])),
+     "duplicate particle id 900"),
+    # the box comes first of all (validate_box inside validate_flat)
+    (lambda f, i: (setattr(f, "box", np.array([-1.0, 10.0, 10.0])),
+                   setattr(f, "id", np.array([0, 1, 2, 3, 4, 5, 6, 6]))), "finite and positive"),
+])
+def test_config_error_order_follows_build_domain(mutate, match):
+    f, inter = _flat(), E.Interactions()
+    mutate(f, inter)
+    with pytest.raises(E.ConfigError, match=match):
+        E.Engine(f, inter, 0.3, E.EngineConfig())
+
+
+def test_parallel_validation_names_the_first_duplicate():
+    """Large systems validate on host threads; the reported id is still the
+    reference's (the first repeated id in input order)."""
+    n = 3 << 20
+    ids = np.arange(n, dtype=np.int64)
+    ids[2_000_000] = 1_500_000
+    ids[2_500_000] = 700
+    f = E.FlatConfig(np.full(3, 200.0), ids, np.zeros((n, 3)), None)
+    with pytest.raises(E.ConfigError, match="duplicate particle id 1500000"):
+        E.Engine(f, E.Interactions(), 0.3, E.EngineConfig())

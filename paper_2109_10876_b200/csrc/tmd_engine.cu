@@ -162,6 +162,38 @@ void big_free(void* p, size_t bytes) {
   g_cache.push_back({dev, bytes, p});
 }
 
+constexpr int kObsRowsAlloc = 256;  // observable rows a context's mapped buffer holds
+
+// Process-wide pool of small mapped pinned blocks (the per-context status
+// mirror, scalars, observable rows): cudaHostAlloc costs milliseconds per
+// call whatever the size, which an engine construction should not pay.
+std::mutex g_pin_mu;
+std::vector<std::pair<size_t, void*>> g_pin_free;  // (bytes, block)
+
+void* pinned_small(size_t bytes) {
+  bytes = (bytes + 255) / 256 * 256;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t k = 0; k < g_pin_free.size(); ++k) {
+      if (g_pin_free[k].first == bytes) {
+        void* p = g_pin_free[k].second;
+        g_pin_free[k] = g_pin_free.back();
+        g_pin_free.pop_back();
+        return p;
+      }
+    }
+  }
+  void* p = nullptr;
+  ck(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+  return p;
+}
+
+void pinned_small_free(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back({(bytes + 255) / 256 * 256, p});
+}
+
 std::string fmt_g(double v) {
   char b[64];
   std::snprintf(b, sizeof b, "%g", v);
@@ -396,9 +428,9 @@ void free_all(tmd_gpu_ctx* c) {
   }
   big_free(c->arena, c->arena_bytes);  // back to the process cache
   big_free(c->nbr, c->nbr_bytes);
-  if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
-  if (c->obs_host) cudaFreeHost(c->obs_host);
-  if (c->h_scalars) cudaFreeHost(c->h_scalars);
+  pinned_small_free(c->h_ctrl, sizeof(Ctrl));
+  pinned_small_free(c->obs_host, sizeof(double) * 4 * kObsRowsAlloc);
+  pinned_small_free(c->h_scalars, 4 * sizeof(double));
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
@@ -969,7 +1001,7 @@ constexpr int64_t kChunk = 256;
 // list overflowed (state is then garbage; the caller rolls back).
 constexpr int kGraphSteps = 15;  // odd: the ping-pong parity is unchanged per graph
 
-constexpr int kObsRows = 256;  // == kChunk: rows a chunk can record
+constexpr int kObsRows = kObsRowsAlloc;  // == kChunk: rows a chunk can record
 
 void launch_obs_record(tmd_gpu_ctx* c) {
   if (c->obs_stride <= 0) return;
@@ -1426,20 +1458,34 @@ bool particles_ok_fast(const tmd_system* s, const IdRange& r) {
     std::sort(sorted.begin(), sorted.end());
     if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) return false;
   }
+  // dense ids: a bitmap over [lo, lo + n) with plain (racy) ORs — a bit lost
+  // to a race between threads, like a duplicate, leaves fewer than n bits
+  // set, and either sends the caller to the exact serial pass
   parallel_chunks(s->n, [&](int, int64_t b, int64_t e) {
     bool my_bad = false;
     for (int64_t k = b; k < e; ++k) {
       if (r.dense) {
         const uint64_t idx = static_cast<uint64_t>(s->id[k] - r.lo);
         const uint64_t bit = 1ull << (idx & 63);
-        const uint64_t old = __atomic_fetch_or(&bits[idx >> 6], bit, __ATOMIC_RELAXED);
-        my_bad |= (old & bit) != 0;
+        uint64_t& w = bits[idx >> 6];
+        my_bad |= (w & bit) != 0;
+        w |= bit;
       }
       if (s->mass) my_bad |= !(s->mass[k] > 0.0);
     }
     if (my_bad) bad.store(true, std::memory_order_relaxed);
   });
   if (bad.load()) return false;
+  if (r.dense) {
+    std::atomic<int64_t> set{0};
+    const int64_t nw = static_cast<int64_t>(bits.size());
+    parallel_chunks(nw << 6, [&](int, int64_t b, int64_t e) {
+      int64_t cnt = 0;
+      for (int64_t w = b >> 6; w < (e >> 6); ++w) cnt += __builtin_popcountll(bits[static_cast<size_t>(w)]);
+      set.fetch_add(cnt, std::memory_order_relaxed);
+    });
+    if (set.load() != s->n) return false;
+  }
   for (int64_t k = 0; k < s->n_bonds; ++k) {
     const int64_t a = s->bonds[2 * k], b = s->bonds[2 * k + 1];
     for (int64_t v : {a, b}) {
@@ -1515,19 +1561,25 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   bg.hi2 = std::nextafter(static_cast<float>(rv2 + delta), 1e30f);
 }
 
+// Brick tables to the device (allocated here unless the context's arena
+// already holds them). The copies are stream-ordered on the context stream
+// (pageable sources: staged before the call returns).
 void upload_bricks(tmd_gpu_ctx* c) {
-  c->cell_rank = dalloc<int>(c->h_rank.size());
-  c->brick_rank_off = dalloc<int>(c->h_brick_off.size());
-  c->ngroups = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
-  c->group_off = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
-  c->scan_tmp = dalloc<int>(static_cast<size_t>(
-      blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1));
-  ck(cudaMemcpy(c->cell_rank, c->h_rank.data(), c->h_rank.size() * sizeof(int),
-                cudaMemcpyHostToDevice), "H2D cell_rank");
-  ck(cudaMemcpy(c->brick_rank_off, c->h_brick_off.data(), c->h_brick_off.size() * sizeof(int),
-                cudaMemcpyHostToDevice), "H2D brick offsets");
-  ck(cudaMemset(c->ngroups, 0, sizeof(int) * (static_cast<size_t>(c->bg.nbricks) + 1)),
-     "memset");
+  if (!c->cell_rank) {
+    c->cell_rank = dalloc<int>(c->h_rank.size());
+    c->brick_rank_off = dalloc<int>(c->h_brick_off.size());
+    c->ngroups = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
+    c->group_off = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
+    c->scan_tmp = dalloc<int>(static_cast<size_t>(
+        blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1));
+  }
+  ck(cudaMemcpyAsync(c->cell_rank, c->h_rank.data(), c->h_rank.size() * sizeof(int),
+                     cudaMemcpyHostToDevice, c->stream), "H2D cell_rank");
+  ck(cudaMemcpyAsync(c->brick_rank_off, c->h_brick_off.data(),
+                     c->h_brick_off.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream),
+     "H2D brick offsets");
+  ck(cudaMemsetAsync(c->ngroups, 0, sizeof(int) * (static_cast<size_t>(c->bg.nbricks) + 1),
+                     c->stream), "memset");
   set_smem_attrs(c);
   c->h_rank.clear();
   c->h_brick_off.clear();
@@ -1723,6 +1775,8 @@ void recut(tmd_gpu_ctx* c, const std::vector<int>& cuts) {
   for (void* p : old) {
     if (p) cudaFree(p);
   }
+  c->cell_rank = c->brick_rank_off = c->ngroups = c->group_off = c->scan_tmp = nullptr;
+  c->count = c->start = nullptr;
   setup_bricks(c, static_cast<double>(c->n_total), c->r_cut + c->r_skin);
   const int64_t want = c->n + c->n / 4 + 1024;
   c->ngroups_max = static_cast<int>(want / 32) + c->bg.nbricks + 1;
@@ -2033,6 +2087,27 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       want(c->ck_fz, n);
     }
     if (!slab) want(c->dl, 11 * n);  // download / upload scratch
+    // the context's small arrays: in the arena too for a whole-box context
+    // (slab contexts re-cut and regrow them, so they keep their own)
+    c->nparts = std::max(blocks_for(c->n_cap, kBlock), c->bg.nbricks);
+    const size_t nbk1 = static_cast<size_t>(c->bg.nbricks) + 1;
+    const size_t nscan = static_cast<size_t>(blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1);
+    if (!slab) {
+      want(c->count, static_cast<size_t>(c->g.ncells));
+      want(c->start, static_cast<size_t>(c->g.ncells) + 1);
+      want(c->part_e, static_cast<size_t>(c->nparts));
+      want(c->part_w, static_cast<size_t>(c->nparts));
+      want(c->part_ke, static_cast<size_t>(c->nparts));
+      want(c->scalars, 4);
+      want(c->ctrl, 1);
+      want(c->rebuild_log, static_cast<size_t>(kChunk));
+      if (c->timers_on) want(c->ticks, static_cast<size_t>(kTickSteps * kTickPhases + 1));
+      want(c->cell_rank, c->h_rank.size());
+      want(c->brick_rank_off, c->h_brick_off.size());
+      want(c->ngroups, nbk1);
+      want(c->group_off, nbk1);
+      want(c->scan_tmp, nscan);
+    }
     mark("plan");
     if (!slab) {
       size_t tot = 0;
@@ -2049,22 +2124,22 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     }
     c->cur = 0;
     c->pos = c->posb[0];
-    c->count = dalloc<int>(c->g.ncells);
-    c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
-    c->nparts = std::max(blocks_for(c->n_cap, kBlock), c->bg.nbricks);
-    c->part_e = dalloc<double>(c->nparts);
-    c->part_w = dalloc<double>(c->nparts);
-    c->part_ke = dalloc<double>(c->nparts);
+    if (slab) {
+      c->count = dalloc<int>(c->g.ncells);
+      c->start = dalloc<int>(static_cast<size_t>(c->g.ncells) + 1);
+      c->part_e = dalloc<double>(c->nparts);
+      c->part_w = dalloc<double>(c->nparts);
+      c->part_ke = dalloc<double>(c->nparts);
+      c->scalars = dalloc<double>(4);
+      c->ctrl = dalloc<Ctrl>(1);
+      c->rebuild_log = dalloc<int>(static_cast<size_t>(kChunk));
+      if (c->timers_on) c->ticks = dalloc<long long>(kTickSteps * kTickPhases + 1);
+    }
     mark("device arrays");
-    upload_bricks(c);
+    upload_bricks(c);  // (small, pageable: before the particle upload takes the copy engine)
     mark("upload bricks");
-    c->scalars = dalloc<double>(4);
-    c->ctrl = dalloc<Ctrl>(1);
-    c->rebuild_log = dalloc<int>(static_cast<size_t>(kChunk));
-    if (c->timers_on) c->ticks = dalloc<long long>(kTickSteps * kTickPhases + 1);
-    mark("checkpoint arrays");
-    ck(cudaMallocHost(&c->h_ctrl, sizeof(Ctrl)), "cudaMallocHost");
-    ck(cudaMallocHost(&c->h_scalars, 4 * sizeof(double)), "cudaMallocHost");
+    c->h_ctrl = static_cast<Ctrl*>(pinned_small(sizeof(Ctrl)));
+    c->h_scalars = static_cast<double*>(pinned_small(4 * sizeof(double)));
     mark("pinned");
     std::memset(c->h_ctrl, 0, sizeof(Ctrl));
     ck(cudaMemsetAsync(c->ctrl, 0, sizeof(Ctrl), c->stream), "memset ctrl");
@@ -2134,8 +2209,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       }
       mark("upload");
     }
-    ck(cudaMemcpy(c->posb[0] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
-    ck(cudaMemcpy(c->posb[1] + n, &far, sizeof(double4), cudaMemcpyHostToDevice), "H2D sentinel");
+    k_set_far<<<1, 1, 0, c->stream>>>(c->posb[0] + n, c->posb[1] + n, far);  // list padding slot
     if (slab) alloc_slab(c);
     if (sys->n_bonds > 0) setup_bonds(c, sys, fene);
 
@@ -2324,9 +2398,7 @@ int tmd_gpu_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride, tmd_obs
       throw StatusError{TMD_ERR_STATE, "engine is in an error state from an earlier step"};
     }
     if (!c->obs_host) {
-      ck(cudaHostAlloc(reinterpret_cast<void**>(&c->obs_host), sizeof(double) * 4 * kObsRows,
-                       cudaHostAllocMapped),
-         "cudaHostAlloc(mapped)");
+      c->obs_host = static_cast<double*>(pinned_small(sizeof(double) * 4 * kObsRows));
       ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->obs_dev), c->obs_host, 0),
          "cudaHostGetDevicePointer");
     }

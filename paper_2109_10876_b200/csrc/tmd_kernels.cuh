@@ -383,6 +383,13 @@ __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
   if (advance_step && (force == 1 || m > thr)) ctrl->rebuilds += 1;
 }
 
+// The far-away sentinel slot after the last particle of both position
+// buffers (the list's padding entries point at it).
+__global__ void k_set_far(double4* a, double4* b, double4 far) {
+  *a = far;
+  *b = far;
+}
+
 // A phase stamp on its own (block start: off 0; forces start: off -1, after
 // the step's decision advanced the counter; the chunk end: slot `end`).
 __global__ void k_tick(const Ctrl* ctrl, long long* ticks, int ph, int off, int end) {

@@ -670,9 +670,7 @@ int tmd_gpu_slab_run_observed(tmd_gpu_ctx* c, int64_t nsteps, int64_t stride,
     if (!n_out || (cap > 0 && !out)) throw StatusError{TMD_ERR_CONFIG, "row buffer missing"};
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (!c->obs_host) {
-      ck(cudaHostAlloc(reinterpret_cast<void**>(&c->obs_host), sizeof(double) * 4 * kObsRows,
-                       cudaHostAllocMapped),
-         "cudaHostAlloc(mapped)");
+      c->obs_host = static_cast<double*>(pinned_small(sizeof(double) * 4 * kObsRows));
       ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->obs_dev), c->obs_host, 0),
          "cudaHostGetDevicePointer");
     }

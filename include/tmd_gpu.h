@@ -193,6 +193,25 @@ int tmd_gpu_cell_of(tmd_gpu_ctx* ctx, int64_t* id, int32_t* cell);
  * most cap pairs to pairs[2*cap]; *n receives the total. */
 int tmd_gpu_pairs(tmd_gpu_ctx* ctx, int64_t* pairs, size_t cap, size_t* n);
 
+/* PairIndexList (neighbor_list.hpp:193-268): the reference's classical
+ * Verlet list of explicit (i, j) pairs and its Newton-3 traversal, the
+ * baseline of its traversal microbenchmark (bench_traversal.cpp).
+ * tmd_gpu_build_pair_index_list = build_pair_index_list (196-247): from the
+ * current neighbour list, each unordered pair (and periodic image) once;
+ * *n_pairs = its length. It holds until the particles are next re-sorted
+ * (a rebuild): later calls fail with TMD_ERR_STATE. */
+int tmd_gpu_build_pair_index_list(tmd_gpu_ctx* ctx, int64_t* n_pairs);
+/* Parity tap: the pair list as (id_i, id_j), list order; at most cap pairs,
+ * *n = the total. */
+int tmd_gpu_pair_index_list(tmd_gpu_ctx* ctx, int64_t* pairs, size_t cap, size_t* n);
+/* compute_pair_forces(const PairIndexList&, ...) (250-268): one force
+ * evaluation at the current positions over the pair list (per-pair forces,
+ * then per-particle sums in a fixed order: no floating-point atomics);
+ * forces stored as by tmd_gpu_compute_forces. */
+int tmd_gpu_compute_forces_pairs(tmd_gpu_ctx* ctx, double* pe, double* virial);
+/* Benchmark hook: mean ms per pair-list traversal (bench_traversal.cpp). */
+int tmd_gpu_time_pair_traversal(tmd_gpu_ctx* ctx, int reps, double* ms_per_traversal);
+
 /* Engine::timers (engine.hpp:145): seconds per section + elapsed. */
 int tmd_gpu_timers(tmd_gpu_ctx* ctx, double sec[5], double* elapsed);
 

@@ -41,6 +41,8 @@ EXPORTS = [
     "tmd_gpu_slab_observe", "tmd_balanced_cuts", "tmd_gpu_release_cache",
     "tmd_gpu_time_step_kernel", "tmd_gpu_prepare_graphs",
     "tmd_local_group_create", "tmd_local_group_destroy", "tmd_gpu_slab_attach_local",
+    "tmd_gpu_build_pair_index_list", "tmd_gpu_pair_index_list", "tmd_gpu_compute_forces_pairs",
+    "tmd_gpu_time_pair_traversal",
 ]
 
 
@@ -158,6 +160,10 @@ def lib() -> C.CDLL:
     L.tmd_gpu_size.restype = C.c_int64
     L.tmd_gpu_list_stats.argtypes = [P, C.POINTER(TmdListStats)]
     L.tmd_gpu_time_force_kernel.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
+    L.tmd_gpu_build_pair_index_list.argtypes = [P, C.POINTER(C.c_int64)]
+    L.tmd_gpu_pair_index_list.argtypes = [P, P, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.tmd_gpu_compute_forces_pairs.argtypes = [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.tmd_gpu_time_pair_traversal.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_time_step_kernel.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     L.tmd_gpu_prepare_graphs.argtypes = [P, C.c_int64]
     L.tmd_gpu_time_list_build.argtypes = [P, C.c_int, C.POINTER(C.c_double)]

@@ -38,6 +38,7 @@
 #include "tmd_kernels.cuh"
 #include "tmd_brick.cuh"
 #include "tmd_slab.cuh"
+#include "tmd_pairlist.cuh"
 
 using namespace tmd;
 
@@ -286,6 +287,17 @@ struct tmd_gpu_ctx {
   std::vector<int> h_rank, h_brick_off;  // host staging for upload_bricks
   int* scan_tmp = nullptr;               // tile sums of the tiled scan
 
+  // PairIndexList (tmd_pairlist.cuh): explicit pairs of the current list
+  uint2* pl_pairs = nullptr;      // {i, entry of j} per pair
+  int64_t pl_m = 0;
+  int* pl_off = nullptr;          // [n + 1] pairs of particle i start at pl_off[i]
+  long long* pl_jstart = nullptr; // [n + 1] transposed index rows
+  uint32_t* pl_jpairs = nullptr;  // pair numbers by j (stable)
+  double* pl_fp = nullptr;        // [3 m] per-pair force
+  double* pl_part = nullptr;      // [2 * blocks] energy / virial partials
+  uint64_t pl_layout = 0;         // layout generation the pair list was built at
+  uint64_t setups = 0;            // forced re-sorts (setup passes): slots move
+
   // z-slab decomposition (one context per GPU of a multi-GPU job)
   int64_t n_cap = 0;        // slot capacity (owned + ghosts in slab mode)
   int64_t n_total = 0;      // particles in the whole system
@@ -419,7 +431,8 @@ void free_all(tmd_gpu_ctx* c) {
                   c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
                   c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1],
                   c->slot_of_id, c->bond_off, c->bond_nbr, c->bond_anchor, c->bnd_cnt,
-                  c->bnd_ent, c->nccl_i64, c->exp, c->dl};
+                  c->bnd_ent, c->nccl_i64, c->exp, c->dl, c->pl_pairs, c->pl_off,
+                  c->pl_jstart, c->pl_jpairs, c->pl_fp, c->pl_part};
   const char* a0 = c->arena;
   const char* a1 = c->arena + c->arena_bytes;
   for (void* p : ptrs) {
@@ -910,6 +923,7 @@ void debug_mark(tmd_gpu_ctx* c, const char* what) {
 }
 
 void setup_pass(tmd_gpu_ctx* c) {
+  c->setups += 1;
   debug_mark(c, "setup start");
   for (;;) {
     set_force_rebuild(c);
@@ -1970,6 +1984,11 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     mark("streams");
     c->ls = c->stream;
     c->use_graphs = params->reserved[2] == 0;  // reserved[2] = 1 disables CUDA graphs
+    // TMD_GRAPHS=0: eager launches for profilers (ncu cannot profile the kernel
+    // nodes of graphs holding conditional nodes); results are bitwise the same
+    if (const char* e = std::getenv("TMD_GRAPHS")) {
+      if (e[0] == '0') c->use_graphs = false;
+    }
     ck(cudaEventCreate(&c->t0), "cudaEventCreate");
     ck(cudaEventCreate(&c->t1), "cudaEventCreate");
     mark("device + streams");
@@ -2373,6 +2392,173 @@ int tmd_gpu_compute_forces(tmd_gpu_ctx* c, double* pe, double* virial) {
     raise_physics(c, false);
     if (pe) *pe = c->h_scalars[0];
     if (virial) *virial = c->h_scalars[1];
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void free_pair_list(tmd_gpu_ctx* c) {
+  for (void* p : {static_cast<void*>(c->pl_pairs), static_cast<void*>(c->pl_off),
+                  static_cast<void*>(c->pl_jstart), static_cast<void*>(c->pl_jpairs),
+                  static_cast<void*>(c->pl_fp), static_cast<void*>(c->pl_part)}) {
+    if (p) cudaFree(p);
+  }
+  c->pl_pairs = nullptr;
+  c->pl_off = nullptr;
+  c->pl_jstart = nullptr;
+  c->pl_jpairs = nullptr;
+  c->pl_fp = nullptr;
+  c->pl_part = nullptr;
+  c->pl_m = 0;
+}
+
+// Slots move at every resort: a pair list holds for one layout generation.
+uint64_t layout_gen(const tmd_gpu_ctx* c) { return c->rebuilds * 1000003ull + c->setups; }
+
+void need_pair_list(const tmd_gpu_ctx* c) {
+  if (!c->pl_pairs) throw StatusError{TMD_ERR_STATE, "no pair index list built"};
+  if (c->pl_layout != layout_gen(c)) {
+    throw StatusError{TMD_ERR_STATE, "pair index list is stale: the particles were re-sorted "
+                                     "since it was built"};
+  }
+}
+
+// build_pair_index_list (neighbor_list.hpp:196-247) from the current list.
+void build_pair_list(tmd_gpu_ctx* c) {
+  free_pair_list(c);
+  const int n = static_cast<int>(c->n);
+  const uint32_t* gl = decoded_list(c);
+  c->pl_off = dalloc<int>(static_cast<size_t>(n) + 1);
+  int* cnt = dalloc<int>(static_cast<size_t>(n) + 1);
+  ck(cudaMemsetAsync(cnt, 0, sizeof(int) * (static_cast<size_t>(n) + 1), c->stream), "memset");
+  c->launches += 1;
+  if (n > 0) k_pl_count<<<blocks_for(n, kBlock), kBlock, 0, c->stream>>>(n, gl, c->nnbr, c->stride, cnt);
+  size_t tb = 0;
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, c->pl_off, n + 1, c->stream), "cub scan");
+  void* tmp = dalloc<char>(tb);
+  ck(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, c->pl_off, n + 1, c->stream), "cub scan");
+  int m = 0;
+  ck(cudaMemcpyAsync(&m, c->pl_off + n, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  cudaFree(tmp);
+  cudaFree(cnt);
+  c->pl_m = m;
+  const size_t um = std::max<size_t>(static_cast<size_t>(m), 1);
+  c->pl_pairs = dalloc<uint2>(um);
+  c->pl_jpairs = dalloc<uint32_t>(um);
+  c->pl_fp = dalloc<double>(3 * um);
+  c->pl_jstart = dalloc<long long>(static_cast<size_t>(n) + 1);
+  c->pl_part = dalloc<double>(2 * static_cast<size_t>(std::max(1, blocks_for(m, kBlock))));
+  uint32_t* jkey = dalloc<uint32_t>(um);
+  uint32_t* jsorted = dalloc<uint32_t>(um);
+  uint32_t* vals = dalloc<uint32_t>(um);
+  c->launches += 3;
+  if (n > 0) {
+    k_pl_fill<<<blocks_for(n, kBlock), kBlock, 0, c->stream>>>(n, gl, c->nnbr, c->stride,
+                                                               c->pl_off, c->pl_pairs, jkey);
+  }
+  if (m > 0) k_pl_iota<<<blocks_for(m, kBlock), kBlock, 0, c->stream>>>(m, vals);
+  int bits = 1;
+  while ((int64_t{1} << bits) <= c->n_cap) ++bits;
+  tb = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, jkey, jsorted, vals, c->pl_jpairs, m, 0, bits,
+                                     c->stream), "cub sort");
+  tmp = dalloc<char>(tb);
+  // stable: each j's pair numbers stay ascending (a fixed summation order)
+  ck(cub::DeviceRadixSort::SortPairs(tmp, tb, jkey, jsorted, vals, c->pl_jpairs, m, 0, bits,
+                                     c->stream), "cub sort");
+  k_pl_jstart<<<blocks_for(n + 1, kBlock), kBlock, 0, c->stream>>>(n, m, jsorted, c->pl_jstart);
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  cudaFree(tmp);
+  cudaFree(jkey);
+  cudaFree(jsorted);
+  cudaFree(vals);
+}
+
+// compute_pair_forces(const PairIndexList&, ...) (neighbor_list.hpp:250-268)
+void launch_pair_forces(tmd_gpu_ctx* c) {
+  const int n = static_cast<int>(c->n);
+  const int nb = std::max(1, blocks_for(c->pl_m, kBlock));
+  c->launches += 4;
+  k_pl_forces<<<nb, kBlock, 0, c->stream>>>(c->pl_m, c->pl_pairs, c->pos, c->g, c->lj, c->pl_fp,
+                                           c->pl_part, c->pl_part + nb, c->id, c->ctrl);
+  if (n > 0) {
+    k_pl_gather<<<blocks_for(n, kBlock), kBlock, 0, c->stream>>>(
+        n, c->pl_off, c->pl_jstart, c->pl_jpairs, c->pl_fp, c->fx, c->fy, c->fz);
+  }
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->pl_part, nb, 1.0, c->scalars + 0);
+  k_reduce<<<1, kRedThreads, 0, c->stream>>>(c->pl_part + nb, nb, 1.0, c->scalars + 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmd_gpu_build_pair_index_list(tmd_gpu_ctx* c, int64_t* n_pairs) {
+  return guard(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    build_pair_list(c);
+    c->pl_layout = layout_gen(c);
+    if (n_pairs) *n_pairs = c->pl_m;
+  });
+}
+
+int tmd_gpu_pair_index_list(tmd_gpu_ctx* c, int64_t* pairs, size_t cap, size_t* n_out) {
+  return guard(c, [&] {
+    if (!n_out) throw StatusError{TMD_ERR_CONFIG, "n_out is required"};
+    need_pair_list(c);
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    *n_out = static_cast<size_t>(c->pl_m);
+    if (!pairs || cap == 0) return;
+    const size_t m = std::min(cap, static_cast<size_t>(c->pl_m));
+    std::vector<uint2> pr(m);
+    std::vector<long long> ids(static_cast<size_t>(c->n_cap));
+    ck(cudaMemcpyAsync(pr.data(), c->pl_pairs, m * sizeof(uint2), cudaMemcpyDeviceToHost,
+                       c->stream), "D2H pairs");
+    ck(cudaMemcpyAsync(ids.data(), c->id, ids.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                       c->stream), "D2H ids");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    for (size_t k = 0; k < m; ++k) {
+      pairs[2 * k] = ids[pr[k].x];
+      pairs[2 * k + 1] = ids[pr[k].y & kIdxMask];
+    }
+  });
+}
+
+int tmd_gpu_compute_forces_pairs(tmd_gpu_ctx* c, double* pe, double* virial) {
+  return guard(c, [&] {
+    need_pair_list(c);
+    c->ck_valid = false;
+    c->obs_fresh = false;
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    launch_pair_forces(c);
+    ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream), "D2H scalars");
+    sync_ctrl(c);
+    raise_physics(c, false);
+    if (pe) *pe = c->h_scalars[0];
+    if (virial) *virial = c->h_scalars[1];
+  });
+}
+
+int tmd_gpu_time_pair_traversal(tmd_gpu_ctx* c, int reps, double* ms) {
+  return guard(c, [&] {
+    need_pair_list(c);
+    if (reps < 1) throw StatusError{TMD_ERR_CONFIG, "reps must be >= 1"};
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->ck_valid = false;
+    c->obs_fresh = false;
+    launch_pair_forces(c);  // warm
+    ck(cudaEventRecord(c->t0, c->stream), "cudaEventRecord");
+    for (int r = 0; r < reps; ++r) launch_pair_forces(c);
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    ck(cudaEventSynchronize(c->t1), "cudaEventSynchronize");
+    float t = 0.f;
+    ck(cudaEventElapsedTime(&t, c->t0, c->t1), "cudaEventElapsedTime");
+    ck(cudaGetLastError(), "kernel launch");
+    *ms = static_cast<double>(t) / reps;
   });
 }
 

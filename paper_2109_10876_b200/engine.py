@@ -423,6 +423,38 @@ class Engine:
         _check(_abi.lib().tmd_gpu_compute_forces(self._h, C.byref(pe), C.byref(w)), self._h)
         return pe.value, w.value
 
+    # -- PairIndexList (neighbor_list.hpp:193-268) ----------------------------------
+    def build_pair_index_list(self) -> int:
+        """build_pair_index_list (neighbor_list.hpp:196-247) from the current
+        neighbour list: each unordered pair once. Valid until the next
+        re-sort. Returns the number of pairs."""
+        m = C.c_int64()
+        _check(_abi.lib().tmd_gpu_build_pair_index_list(self._h, C.byref(m)), self._h)
+        return m.value
+
+    def pair_index_list(self) -> np.ndarray:
+        """The built pair list as (id_i, id_j) rows, list order."""
+        L = _abi.lib()
+        n = C.c_size_t()
+        _check(L.tmd_gpu_pair_index_list(self._h, None, 0, C.byref(n)), self._h)
+        out = np.empty((max(n.value, 1), 2), np.int64)
+        _check(L.tmd_gpu_pair_index_list(self._h, _ptr(out), n.value, C.byref(n)), self._h)
+        return out[: n.value]
+
+    def compute_forces_pairs(self):
+        """compute_pair_forces(const PairIndexList&, ...) (neighbor_list.hpp:
+        250-268): forces over the explicit pair list; returns (pe, virial)."""
+        pe, w = C.c_double(), C.c_double()
+        _check(_abi.lib().tmd_gpu_compute_forces_pairs(self._h, C.byref(pe), C.byref(w)),
+               self._h)
+        return pe.value, w.value
+
+    def time_pair_traversal(self, reps: int) -> float:
+        ms = C.c_double()
+        _check(_abi.lib().tmd_gpu_time_pair_traversal(self._h, int(reps), C.byref(ms)),
+               self._h)
+        return ms.value
+
     # -- parity taps -------------------------------------------------------------
     def cell_of(self):
         n = self._n

@@ -1517,19 +1517,25 @@ __global__ void __launch_bounds__(128)
 // differs (a rounding-level difference, within the parity tolerances).
 // Resident blocks per SM the register budget must allow (a grid of 128-
 // particle blocks fits one wave down to ~32K particles).
-constexpr int lanes_min_blocks(int lanes) { return lanes == 2 ? 3 : (lanes == 4 ? 2 : 1); }
+// Particles per block of k_forces_lanes: 32, so that a small system's grid
+// (1,000 blocks at 32K) spreads evenly over the 148 SMs instead of 250
+// blocks of 128 (102 SMs running two, 46 one).
+constexpr int kLanesPPB = 32;
+// resident blocks per SM: 768 / 1024 / 1024 threads per SM for 2 / 4 / 8 lanes
+constexpr int lanes_min_blocks(int lanes) { return lanes == 2 ? 12 : (lanes == 4 ? 8 : 4); }
 
 template <int kUnroll, int kMode, int kLanes>
-__global__ void __launch_bounds__(128 * kLanes, lanes_min_blocks(kLanes))
+__global__ void __launch_bounds__(kLanesPPB * kLanes, lanes_min_blocks(kLanes))
     k_forces_lanes(int n, const double4* __restrict__ pos, const uint32_t* __restrict__ list,
                    const int* __restrict__ nnbr, int cap, Geom g, LjConst lj,
                    double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                    double* __restrict__ part_e, double* __restrict__ part_w,
                    const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
   if (ctrl->halt) return;
-  __shared__ double red[4 * kLanes];
+  constexpr int kThreads = kLanesPPB * kLanes;
+  __shared__ double red[kThreads / 32];
   const int sub = threadIdx.x % kLanes;
-  const int i = blockIdx.x * 128 + threadIdx.x / kLanes;
+  const int i = blockIdx.x * kLanesPPB + threadIdx.x / kLanes;
   double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
   double ax = 0.0, ay = 0.0, az = 0.0;
   bool zero = false;
@@ -1588,13 +1594,13 @@ __global__ void __launch_bounds__(128 * kLanes, lanes_min_blocks(kLanes))
       fz[i] = az;
     }
   }
-  const double te = block_sum<128 * kLanes>(e, red);
-  const double tw = block_sum<128 * kLanes>(w, red);
+  const double te = block_sum<kThreads>(e, red);
+  const double tw = block_sum<kThreads>(w, red);
   if (threadIdx.x == 0) {
     part_e[blockIdx.x] = te;
     part_w[blockIdx.x] = tw;
   }
-  integrate_block<kMode, 128 * kLanes>(ke, d2, red, it, ctrl);
+  integrate_block<kMode, kThreads>(ke, d2, red, it, ctrl);
 }
 
 // Tap for variant 3: chunked global-slot list -> ELL-transposed copy.

@@ -354,6 +354,7 @@ struct tmd_gpu_ctx {
   int64_t step = 0;
   uint64_t rebuilds = 0;
   bool ke_fresh = false;  // part_ke holds the current velocities' partials
+  int ke_parts = 1;       // valid part_ke slots (see force_parts)
   bool obs_fresh = false; // h_scalars holds PE, W, KE of the current state
   bool ck_valid = false;  // a rollback checkpoint exists (invalidated by state edits)
   int64_t ck_step = 0;
@@ -726,7 +727,7 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
     auto kern = c->lanes == 2 ? k_forces_lanes<4, kMode, 2>
                               : (c->lanes == 4 ? k_forces_lanes<2, kMode, 4>
                                                : k_forces_lanes<2, kMode, 8>);
-    kern<<<c->nblk, 128 * c->lanes, 0, c->ls>>>(
+    kern<<<blocks_for(c->n, kLanesPPB), kLanesPPB * c->lanes, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
         c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else if (c->variant == 3) {
@@ -749,8 +750,18 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
 // epilogue (kKick2: closing half-kick; kFused: closing half-kick + next
 // step's opening half-kick and drift into the other position buffer, after
 // which the buffers swap).
+int force_parts(const tmd_gpu_ctx* c);
+
+// Kinetic partials of the current velocities, 128 particles per slot.
+void launch_kinetic(tmd_gpu_ctx* c) {
+  c->ke_parts = c->nblk;
+  k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz, c->mass,
+                                          c->part_ke);
+}
+
 void launch_forces(tmd_gpu_ctx* c, int mode = kForcesOnly) {
   c->launches += 1;
+  if (mode != kForcesOnly) c->ke_parts = force_parts(c);  // its kinetic partials
   if (mode == kFused) {
     launch_forces_mode<kFused>(c);
     c->cur ^= 1;
@@ -762,7 +773,15 @@ void launch_forces(tmd_gpu_ctx* c, int mode = kForcesOnly) {
   }
 }
 
-int force_parts(const tmd_gpu_ctx* c) { return c->variant == 2 ? c->bg.nbricks : c->nblk; }
+// Partial-sum slots the force kernel writes (its grid), and the kinetic
+// partials' count: the force grid after a kicking force launch, the
+// 128-particle grid after k_kinetic (recorded when the reducer is enqueued
+// or captured).
+int force_parts(const tmd_gpu_ctx* c) {
+  if (c->variant == 2) return c->bg.nbricks;
+  if (c->variant == 3 && c->lanes > 1) return std::max(1, blocks_for(c->n, kLanesPPB));
+  return c->nblk;
+}
 
 void launch_kick_drift(tmd_gpu_ctx* c) {
   c->launches += 1;
@@ -789,7 +808,7 @@ void launch_reduce_pe(tmd_gpu_ctx* c) {
 
 void launch_reduce_ke(tmd_gpu_ctx* c) {
   c->launches += 1;
-  k_reduce<<<1, kRedThreads, 0, c->ls>>>(c->part_ke, c->nblk, 1.0,
+  k_reduce<<<1, kRedThreads, 0, c->ls>>>(c->part_ke, c->ke_parts, 1.0,
                                              c->scalars + 2);
 }
 
@@ -1035,7 +1054,7 @@ void launch_obs_record(tmd_gpu_ctx* c, int step_off = 0) {
   if (c->obs_stride <= 0) return;
   c->launches += 1;
   k_obs_record<<<1, kRedThreads, 0, c->ls>>>(c->part_e, c->part_w, force_parts(c), c->part_ke,
-                                             c->nblk, c->ctrl, c->obs_stride, c->obs_dev,
+                                             c->ke_parts, c->ctrl, c->obs_stride, c->obs_dev,
                                              kObsRows, step_off);
 }
 
@@ -1045,8 +1064,7 @@ void enqueue_observables(tmd_gpu_ctx* c) {
   launch_reduce_pe(c);
   if (c->variant == 2) {  // brick variant: its kinetic partials are per brick
     c->launches += 1;
-    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
-                                            c->mass, c->part_ke);
+    launch_kinetic(c);
   }
   launch_reduce_ke(c);
   ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1791,7 +1809,7 @@ void grow_capacity(tmd_gpu_ctx* c, int64_t need) {
     ck(cudaMemcpy(c->posb[b] + nn, &far, sizeof(double4), cudaMemcpyHostToDevice),
        "H2D sentinel");
   }
-  const int parts = std::max(blocks_for(cap, kBlock), c->bg.nbricks);
+  const int parts = std::max({blocks_for(cap, kBlock), blocks_for(cap, kLanesPPB), c->bg.nbricks});
   if (parts > c->nparts) {
     cudaFree(c->part_e); cudaFree(c->part_w); cudaFree(c->part_ke);
     c->nparts = parts;
@@ -2141,7 +2159,8 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     if (!slab) want(c->dl, 11 * n);  // download / upload scratch
     // the context's small arrays: in the arena too for a whole-box context
     // (slab contexts re-cut and regrow them, so they keep their own)
-    c->nparts = std::max(blocks_for(c->n_cap, kBlock), c->bg.nbricks);
+    c->nparts = std::max({blocks_for(c->n_cap, kBlock), blocks_for(c->n_cap, kLanesPPB),
+                          c->bg.nbricks});
     const size_t nbk1 = static_cast<size_t>(c->bg.nbricks) + 1;
     const size_t nscan = static_cast<size_t>(blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1);
     if (!slab) {
@@ -2662,12 +2681,13 @@ int tmd_gpu_observe(tmd_gpu_ctx* c, tmd_observables* out) {
       return;
     }
     // after a run the closing half-kick already left the kinetic partials of
-    // the current velocities (same 128-particle blocks as k_kinetic, so the
-    // same sum bit for bit); the brick variant's partials are per brick
+    // the current velocities (the force kernel's blocks: 128 particles, or 32
+    // for the small-system lanes kernel — the same sum to rounding as
+    // k_kinetic's, and what run_observed recorded); the brick variant's
+    // partials are per brick
     if (!(c->ke_fresh && c->variant != 2)) {
       c->launches += 1;
-      k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
-                                              c->mass, c->part_ke);
+      launch_kinetic(c);
     }
     launch_reduce_ke(c);
     ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double),
@@ -3376,8 +3396,7 @@ int tmd_gpu_slab_sums(tmd_gpu_ctx* c, double out[3]) {
     need_slab(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->launches += 1;
-    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
-                                            c->mass, c->part_ke);
+    launch_kinetic(c);
     launch_reduce_ke(c);
     launch_reduce_pe(c);
     ck(cudaMemcpyAsync(c->h_scalars, c->scalars, 3 * sizeof(double), cudaMemcpyDeviceToHost,

@@ -707,8 +707,7 @@ int tmd_gpu_slab_observe(tmd_gpu_ctx* c, int64_t n_total, tmd_observables* out) 
     need_comm(c);
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->launches += 1;
-    k_kinetic<<<c->nblk, kBlock, 0, c->ls>>>(static_cast<int>(c->n), c->vx, c->vy, c->vz,
-                                            c->mass, c->part_ke);
+    launch_kinetic(c);
     launch_reduce_ke(c);
     launch_reduce_pe(c);
     comm(c)->allreduce(c->scalars, 3, CType::kF64, COp::kSum, c->stream);

@@ -695,6 +695,8 @@ void launch_build(tmd_gpu_ctx* c) {
   }
 }
 
+int force_parts(const tmd_gpu_ctx* c);
+
 template <int kMode>
 void launch_forces_mode(tmd_gpu_ctx* c) {
   Integ it;
@@ -727,7 +729,7 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
     auto kern = c->lanes == 2 ? k_forces_lanes<4, kMode, 2>
                               : (c->lanes == 4 ? k_forces_lanes<2, kMode, 4>
                                                : k_forces_lanes<2, kMode, 8>);
-    kern<<<blocks_for(c->n, kLanesPPB), kLanesPPB * c->lanes, 0, c->ls>>>(
+    kern<<<force_parts(c), kLanesPPB * c->lanes, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
         c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else if (c->variant == 3) {
@@ -750,8 +752,6 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
 // epilogue (kKick2: closing half-kick; kFused: closing half-kick + next
 // step's opening half-kick and drift into the other position buffer, after
 // which the buffers swap).
-int force_parts(const tmd_gpu_ctx* c);
-
 // Kinetic partials of the current velocities, 128 particles per slot.
 void launch_kinetic(tmd_gpu_ctx* c) {
   c->ke_parts = c->nblk;

@@ -62,6 +62,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         lib = nd / "lib"
         extra = [f"-I{nd / 'include'}", f"-L{lib}", "-l:libnccl.so.2",
                  "-Xlinker", f"-rpath,{lib}"]
+    if os.environ.get("TMD_RDC") == "1":  # (experiment: relocatable device code)
+        extra = ["-rdc=true", *extra, "-lcudadevrt"]
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(LIB), *map(str, SOURCES)]
     res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
     log = res.stdout + res.stderr

@@ -100,7 +100,6 @@ struct Ctrl {
   int halt;                   // native slab loop: a rebuild is due, later steps are no-ops
   double seen_d2;             // native slab loop: the global max |x - x_snap|^2 the last
                               // decision saw (the host sizes its next batch from it)
-  unsigned int done_blocks;   // folded decision: force blocks finished this launch
   long long tick_base;        // section timers in graph mode: step count at the chunk
                               // start (phase ticks are indexed by step - tick_base)
 };

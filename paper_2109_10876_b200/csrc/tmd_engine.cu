@@ -58,11 +58,9 @@ constexpr int kDefaultVariant = 3;
 // blocks, one per SM) never won by more than 1 %.
 constexpr int64_t kLanesTargetThreads = 148 * 768;
 constexpr int kLanesAutoMax = 4;
-// Up to this many particles the fused force kernel also takes the next
-// step's rebuild decision (its last block; no decide node per step): a small
-// system's step is launch latency, a large one's the force kernel, where the
-// per-block completion counter measured +3 % at 1M.
-constexpr int64_t kFoldMaxParticles = 262144;
+// Up to this many particles graph steps keep the rebuild kernels as
+// early-returning nodes instead of a conditional IF node (see if_nodes).
+constexpr int64_t kChainMaxParticles = 262144;
 
 struct CudaFail {
   std::string what;
@@ -401,12 +399,10 @@ struct tmd_gpu_ctx {
   bool use_graphs = true;
   uint64_t graph_body_kernels = 0;   // kernels per executed IF body
   unsigned long long cond_handle = 0;  // handle the next decide sets (0: none)
-  // Small systems: the next step's rebuild decision is taken by the last block
-  // of the fused force kernel (no decide node per step; launch latency is
-  // what a small system's step is made of). Chosen at create.
-  bool fold_decide = false;
-  int fold_next = 0;                          // set while capturing such a force launch
-  cudaGraphConditionalHandle fold_cond = 0;   // ... and the IF handle it sets
+  // Graph steps gate the rebuild kernels with a conditional IF node (large
+  // systems), or keep them as early-returning kernel nodes (small systems,
+  // where the IF node's ~9 us per step is a third of the step). At create.
+  bool if_nodes = true;
 };
 
 namespace {
@@ -716,9 +712,6 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
   it.bt.ent = c->bnd_ent;
   const bool fh = kMode == kFused && c->fused_halo && c->fused_ready;
   it.exp = fh ? c->exp : nullptr;
-  it.fold = kMode == kFused ? c->fold_next : 0;
-  it.thr = c->g.rebuild_thr;
-  it.next_cond = c->fold_cond;
   it.rg[0] = fh ? c->rg[0][c->cur ^ 1] : nullptr;
   it.rg[1] = fh ? c->rg[1][c->cur ^ 1] : nullptr;
   if (c->variant == 1) {
@@ -1050,12 +1043,12 @@ constexpr int kGraphSteps = 15;  // odd: the ping-pong parity is unchanged per g
 
 constexpr int kObsRows = kObsRowsAlloc;  // == kChunk: rows a chunk can record
 
-void launch_obs_record(tmd_gpu_ctx* c, int step_off = 0) {
+void launch_obs_record(tmd_gpu_ctx* c) {
   if (c->obs_stride <= 0) return;
   c->launches += 1;
   k_obs_record<<<1, kRedThreads, 0, c->ls>>>(c->part_e, c->part_w, force_parts(c), c->part_ke,
                                              c->ke_parts, c->ctrl, c->obs_stride, c->obs_dev,
-                                             kObsRows, step_off);
+                                             kObsRows);
 }
 
 // End of a run segment: PE / virial / KE reduced and copied into the pinned
@@ -1119,19 +1112,25 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
   launch_tick(c, kTickBlock, 0);
   launch_kick_drift(c);
   uint64_t body = 0;
-  const bool fold = c->fold_decide;
-  cudaGraphConditionalHandle h_next = 0;
-  for (int s = 0; s < nsteps; ++s) {
+  // Small systems: no conditional nodes (an IF node costs ~9 us per step on
+  // B200, a kernel node that returns at once well under 1 us): the rebuild
+  // kernels stay in the graph and return unless the step's decision is set
+  // (the eager sequence).
+  for (int s = 0; s < nsteps && !c->if_nodes; ++s) {
+    launch_decide(c, true);
+    launch_resort(c);
+    launch_build(c);
+    launch_tick(c, kTickForces, -1);
+    launch_forces(c, s + 1 < nsteps ? kFused : kKick2);
+    launch_obs_record(c);
+  }
+  for (int s = 0; s < nsteps && c->if_nodes; ++s) {
     cudaGraphConditionalHandle h;
-    if (s == 0 || !fold) {
-      ck(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault),
-         "cudaGraphConditionalHandleCreate");
-      c->cond_handle = h;
-      launch_decide(c, true);
-      c->cond_handle = 0;
-    } else {
-      h = h_next;  // set by the last block of the previous step's force kernel
-    }
+    ck(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault),
+       "cudaGraphConditionalHandleCreate");
+    c->cond_handle = h;
+    launch_decide(c, true);
+    c->cond_handle = 0;
     cudaStreamCaptureStatus st;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
@@ -1149,7 +1148,6 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
                                      0, cudaStreamCaptureModeThreadLocal),
        "begin body capture");
     c->ls = c->side;
-    if (fold && s > 0) launch_tick(c, kTickDecide, -1);  // (the folded decision has no stamp)
     launch_resort(c);
     launch_build(c);
     c->ls = c->stream;
@@ -1160,17 +1158,8 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
                                            cudaStreamSetCaptureDependencies),
        "cudaStreamUpdateCaptureDependencies");
     launch_tick(c, kTickForces, -1);
-    const bool fused = s + 1 < nsteps;
-    if (fold && fused) {
-      ck(cudaGraphConditionalHandleCreate(&h_next, g, 0, cudaGraphCondAssignDefault),
-         "cudaGraphConditionalHandleCreate");
-      c->fold_next = 1;
-      c->fold_cond = h_next;
-    }
-    launch_forces(c, fused ? kFused : kKick2);
-    c->fold_next = 0;
-    c->fold_cond = 0;
-    launch_obs_record(c, fold && fused ? -1 : 0);
+    launch_forces(c, s + 1 < nsteps ? kFused : kKick2);
+    launch_obs_record(c);
   }
   enqueue_observables(c);
   ck(cudaStreamEndCapture(c->stream, &g), "end capture");
@@ -2102,9 +2091,8 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     if (c->lanes_auto) {
       while (c->lanes < kLanesAutoMax && c->n * c->lanes < kLanesTargetThreads) c->lanes *= 2;
     }
-    // (a completion counter per block costs more than a graph node above this)
-    c->fold_decide = !slab && c->n <= kFoldMaxParticles && params->reserved[2] == 0;
-    if (const char* e = std::getenv("TMD_FOLD_DECIDE")) c->fold_decide = !slab && e[0] == '1';
+    c->if_nodes = c->n > kChainMaxParticles;
+    if (const char* e = std::getenv("TMD_IF_NODES")) c->if_nodes = e[0] == '1';
     c->build_kind = params->reserved[3];
     c->build_auto = c->build_kind != 3 && c->build_kind != 5 && c->build_kind != 6;
     if (c->build_auto) c->build_kind = 6;  // decided at the first binning (setup_pass)

@@ -66,11 +66,6 @@ struct Integ {
   // (peer memory over NVLink, or this GPU's own ghost slots with one slab).
   const int2* exp;
   double4* rg[2];
-  // Folded rebuild decision (small systems, graph mode): the last block of a
-  // kFused launch takes the next step's k_decide and sets its IF node.
-  int fold;
-  double thr;
-  cudaGraphConditionalHandle next_cond;
 };
 
 // FENE forces of slot i (compute_bonded_forces, bonded.hpp:167-199): the bond
@@ -168,22 +163,6 @@ __device__ __forceinline__ void integrate_one(int i, const double4& pi, double& 
 }
 
 // Block-level reductions of the epilogue (all threads of the block call it).
-// k_decide (below) for the next step, taken by the last block of a kFused
-// launch once every block's displacement maximum is in (the same rule and
-// counters; the step counter advances here instead of in a decide node).
-__device__ __forceinline__ void fold_decide(Ctrl* ctrl, double thr,
-                                            cudaGraphConditionalHandle cond) {
-  const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
-  const int force = ctrl->force_rebuild;
-  const int r = (force != 0) || (m > thr);
-  ctrl->rebuild = r;
-  cudaGraphSetConditional(cond, r ? 1u : 0u);
-  ctrl->force_rebuild = 0;
-  ctrl->max_d2 = 0ull;
-  ctrl->step += 1;
-  if (force == 1 || m > thr) ctrl->rebuilds += 1;
-}
-
 template <int kMode, int kThreads>
 __device__ __forceinline__ void integrate_block(double ke, double d2, double* red,
                                                 const Integ& it, Ctrl* ctrl) {
@@ -194,18 +173,6 @@ __device__ __forceinline__ void integrate_block(double ke, double d2, double* re
     for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
     if ((threadIdx.x & 31) == 0 && d2 > 0.0) {
       atomicMax(&ctrl->max_d2, static_cast<unsigned long long>(__double_as_longlong(d2)));
-    }
-    if (it.fold) {
-      __syncthreads();  // this block's maxima are in
-      if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned prev = atomicAdd(&ctrl->done_blocks, 1u);
-        if (prev == gridDim.x - 1) {  // every block finished: decide the next step
-          __threadfence();
-          ctrl->done_blocks = 0u;
-          fold_decide(ctrl, it.thr, it.next_cond);
-        }
-      }
     }
   }
 }
@@ -890,7 +857,7 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void __launch_bounds__(kRedThreads)
     k_obs_record(const double* __restrict__ part_e, const double* __restrict__ part_w,
                  int npe, const double* __restrict__ part_ke, int nke, Ctrl* ctrl, int stride,
-                 double* __restrict__ rows, int max_rows, int step_off) {
+                 double* __restrict__ rows, int max_rows) {
   if (ctrl->halt) return;  // native slab loop: a halted (replayed) step records nothing
   __shared__ double red[kRedThreads / 32];
   double se = 0.0, sw = 0.0, sk = 0.0;
@@ -903,7 +870,7 @@ __global__ void __launch_bounds__(kRedThreads)
   const double tw = block_sum<kRedThreads>(sw, red);
   const double tk = block_sum<kRedThreads>(sk, red);
   if (threadIdx.x == 0) {
-    const long long st = ctrl->step + step_off;  // -1 after a folded decision advanced it
+    const long long st = ctrl->step;
     if (st % stride == 0) {
       const int r = ctrl->obs_rows;
       if (r < max_rows) {

@@ -7,9 +7,12 @@ product path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libtmd_gpu.so"
+if os.environ.get("TMD_LIB"):  # A/B experiments against another build of the library
+    LIB_PATH = Path(os.environ["TMD_LIB"]).resolve()
 
 TMD_OK = 0
 TMD_ERR_CONFIG = 1

@@ -25,7 +25,10 @@
 
 namespace tmd {
 
-constexpr int kMaxHalo = 64;  // (2+2)^3
+// Bricks of 2 x 2 x kBrickZ cells: the list build stages a brick's
+// (2+2) x (2+2) x (kBrickZ+2) halo once for its 2 x 2 x kBrickZ own cells.
+constexpr int kBrickZ = 4;
+constexpr int kMaxHalo = 4 * 4 * (kBrickZ + 2);  // 96
 constexpr float kFarF = 1.0e30f;
 constexpr double kFarD = 1.0e30;
 
@@ -104,19 +107,27 @@ __device__ __forceinline__ void load_halo(int b, const Geom& g, const BrickGeom&
     s_code[t] = code;
   }
   __syncthreads();
-  if (t < 32) {  // warp-level exclusive scan of the padded counts (<= 64 cells)
-    const int a = t < ht.n ? pad4(s_cnt[t]) : 0;
-    const int c = t + 32 < ht.n ? pad4(s_cnt[t + 32]) : 0;
-    int sa = a, sc = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int ua = __shfl_up_sync(0xffffffffu, sa, o);
-      const int uc = __shfl_up_sync(0xffffffffu, sc, o);
-      if (t >= o) { sa += ua; sc += uc; }
+  if (t < 32) {  // warp-level exclusive scan of the padded counts (<= 96 cells)
+    int v[kMaxHalo / 32], sv[kMaxHalo / 32];
+#pragma unroll
+    for (int q = 0; q < kMaxHalo / 32; ++q) {
+      v[q] = t + 32 * q < ht.n ? pad4(s_cnt[t + 32 * q]) : 0;
+      sv[q] = v[q];
     }
-    const int tot_a = __shfl_sync(0xffffffffu, sa, 31);
-    if (t < ht.n) s_off[t] = sa - a;
-    if (t + 32 < ht.n) s_off[t + 32] = tot_a + sc - c;
-    if (t == 31) s_off[ht.n] = tot_a + sc;
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int q = 0; q < kMaxHalo / 32; ++q) {
+        const int u = __shfl_up_sync(0xffffffffu, sv[q], o);
+        if (t >= o) sv[q] += u;
+      }
+    }
+    int base = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxHalo / 32; ++q) {
+      if (t + 32 * q < ht.n) s_off[t + 32 * q] = base + sv[q] - v[q];
+      base += __shfl_sync(0xffffffffu, sv[q], 31);
+    }
+    if (t == 31) s_off[ht.n] = base;
   }
   __syncthreads();
   ht.total = s_off[ht.n];
@@ -943,11 +954,11 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
   __shared__ __align__(16) uint32_t s_ring[kBuildThreads / 32][kRingSlots][32];
   __shared__ __align__(16) float s_strm[kBuildThreads / 32][kCullCap * 4];
   __shared__ __align__(16) int4 s_rng[kBuildThreads / 32][11][3];  // per-warp range table
-  __shared__ int s_maxc;
+  __shared__ int s_maxc, s_next;
   __shared__ unsigned long long s_ent;
   const int b = blockIdx.x;
   HaloTable ht;
-  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
+  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; s_next = kBuildThreads / 32; }
   load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
             s_gcell);
   if (ht.total > bg.stage_cap) {
@@ -1000,7 +1011,9 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
   const float cull2 = bg.hi2 * 1.001f;
   int my_max = 0;
   unsigned long long my_ent = 0;
-  for (int oc = warp; oc < ncell_own; oc += kBuildThreads / 32) {
+  // own cells handed out one at a time (cells hold 10-32 particles: a static
+  // split leaves warps idle at the block's end)
+  for (int oc = warp; oc < ncell_own;) {
     const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
     const int hc = (ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1));
     const int ncl = s_cnt[hc];
@@ -1169,6 +1182,9 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
       }
       __syncwarp();
     }
+    int nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&s_next, 1);
+    oc = __shfl_sync(0xffffffffu, nxt, 0);
   }
   for (int o = 16; o > 0; o >>= 1) {
     my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));

@@ -40,3 +40,28 @@ for T in (0.0, 1.0):
     dec.close()
     print(f"T={T} n={f.size()} single {t_one:.4f} ms/step, native slab (1 rank) "
           f"{t_dec:.4f} ms/step, rebuilds in 400 steps: {r_dec}", flush=True)
+
+# where the native loop's time goes (CUDA-event section timers, liquid)
+f = E.gen_fcc(cells, 0.8442, 1.0, 12345)
+cfg = E.EngineConfig(dt=0.005, section_timers=True)
+dec = DecomposedEngine(f, E.Interactions(), 0.3, cfg, comm=InProcessComm(1), native=True)
+dec.run(50)
+t0 = dec.timers()
+r0 = dec.rebuild_count()
+dec.run(400)
+t1 = dec.timers()
+nreb = dec.rebuild_count() - r0
+d = t1.seconds - t0.seconds
+print("native loop sections (ms/step): " + ", ".join(
+    f"{n} {1e3 * v / 400:.4f}" for n, v in zip(E.SECTION_NAMES, d)) +
+    f"; elapsed {1e3 * (t1.elapsed - t0.elapsed) / 400:.4f}; {nreb} rebuilds", flush=True)
+dec.close()
+one = E.Engine(f, E.Interactions(), 0.3, cfg)
+one.run(50)
+t0 = one.timers()
+one.run(400)
+t1 = one.timers()
+d = t1.seconds - t0.seconds
+print("single context sections (ms/step): " + ", ".join(
+    f"{n} {1e3 * v / 400:.4f}" for n, v in zip(E.SECTION_NAMES, d)) +
+    f"; elapsed {1e3 * (t1.elapsed - t0.elapsed) / 400:.4f}", flush=True)

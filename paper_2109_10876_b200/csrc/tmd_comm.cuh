@@ -19,6 +19,7 @@
 #pragma once
 
 #include <condition_variable>
+#include <cstdlib>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -56,10 +57,60 @@ inline void nck(ncclResult_t r, const char* what) {
   }
 }
 
+// Communicators outlive their engines: a closed context hands its
+// communicator to a process-wide cache keyed by (device, ranks, rank), and
+// the next context of the process with the same key takes it instead of
+// paying ncclCommInitRank again (hundreds of ms). Every rank of an SPMD job
+// creates and closes its engines in the same sequence, so all hit or all
+// miss together. TMD_NCCL_CACHE=0 turns it off; tmd_gpu_release_cache
+// destroys the cached ones.
+struct NcclCached {
+  int device, nranks, rank;
+  ncclComm_t comm;
+};
+inline std::mutex& nccl_cache_mu() {
+  static std::mutex m;
+  return m;
+}
+inline std::vector<NcclCached>& nccl_cache() {
+  static std::vector<NcclCached> v;
+  return v;
+}
+inline bool nccl_cache_on() {
+  const char* e = std::getenv("TMD_NCCL_CACHE");
+  return !(e && e[0] == '0');
+}
+inline ncclComm_t nccl_cache_take(int device, int nranks, int rank) {
+  if (!nccl_cache_on()) return nullptr;
+  std::lock_guard<std::mutex> lk(nccl_cache_mu());
+  auto& v = nccl_cache();
+  for (size_t k = 0; k < v.size(); ++k) {
+    if (v[k].device == device && v[k].nranks == nranks && v[k].rank == rank) {
+      ncclComm_t c = v[k].comm;
+      v[k] = v.back();
+      v.pop_back();
+      return c;
+    }
+  }
+  return nullptr;
+}
+inline void nccl_cache_release_all() {
+  std::lock_guard<std::mutex> lk(nccl_cache_mu());
+  for (auto& e : nccl_cache()) ncclCommDestroy(e.comm);
+  nccl_cache().clear();
+}
+
 struct NcclComm final : SlabComm {
   ncclComm_t nc = nullptr;
+  int device = 0, nranks = 1, rank = 0;
   ~NcclComm() override {
-    if (nc) ncclCommDestroy(nc);
+    if (!nc) return;
+    if (nccl_cache_on()) {
+      std::lock_guard<std::mutex> lk(nccl_cache_mu());
+      nccl_cache().push_back({device, nranks, rank, nc});
+    } else {
+      ncclCommDestroy(nc);
+    }
   }
   static ncclDataType_t dt(CType t) {
     switch (t) {

@@ -15,6 +15,8 @@
 // back to its checkpoint, grows the list and replays it.
 #include <cuda_runtime.h>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <array>
@@ -167,6 +169,42 @@ void big_free(void* p, size_t bytes) {
 }
 
 constexpr int kObsRowsAlloc = 256;  // observable rows a context's mapped buffer holds
+
+// Device arrays that go through the block cache one by one (slab contexts'
+// per-slot arrays, which regrow): their sizes are remembered so that the
+// generic free path can hand them back to the cache.
+std::mutex g_sized_mu;
+std::vector<std::pair<void*, size_t>> g_sized;
+
+void* sized_alloc(size_t bytes) {
+  size_t got = 0;
+  void* p = big_alloc(bytes, &got);
+  std::lock_guard<std::mutex> lk(g_sized_mu);
+  g_sized.push_back({p, got});
+  return p;
+}
+
+// cudaFree, or back to the cache for a sized_alloc block.
+void dev_free(void* p) {
+  if (!p) return;
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_sized_mu);
+    for (size_t k = 0; k < g_sized.size(); ++k) {
+      if (g_sized[k].first == p) {
+        bytes = g_sized[k].second;
+        g_sized[k] = g_sized.back();
+        g_sized.pop_back();
+        break;
+      }
+    }
+  }
+  if (bytes) {
+    big_free(p, bytes);
+  } else {
+    cudaFree(p);
+  }
+}
 
 // Process-wide pool of small mapped pinned blocks (the per-context status
 // mirror, scalars, observable rows): cudaHostAlloc costs milliseconds per
@@ -445,7 +483,7 @@ void free_all(tmd_gpu_ctx* c) {
   const char* a1 = c->arena + c->arena_bytes;
   for (void* p : ptrs) {
     const char* q = static_cast<const char*>(p);
-    if (p && !(a0 && q >= a0 && q < a1)) cudaFree(p);
+    if (p && !(a0 && q >= a0 && q < a1)) dev_free(p);
   }
   big_free(c->arena, c->arena_bytes);  // back to the process cache
   big_free(c->nbr, c->nbr_bytes);
@@ -1765,9 +1803,9 @@ void grow_capacity(tmd_gpu_ctx* c, int64_t need) {
   auto regrow = [&](auto*& p, size_t extra) {
     using T = std::remove_reference_t<decltype(*p)>;
     if (!p) return;
-    T* q = dalloc<T>(nn + extra);
+    T* q = static_cast<T*>(sized_alloc((nn + extra) * sizeof(T)));
     ck(cudaMemcpy(q, p, o * sizeof(T), cudaMemcpyDeviceToDevice), "regrow copy");
-    cudaFree(p);
+    dev_free(p);
     p = q;
   };
   for (int b = 0; b < 2; ++b) regrow(c->posb[b], 1);
@@ -1935,6 +1973,81 @@ void setup_bonds(tmd_gpu_ctx* c, const tmd_system* sys, const tmd_fene_params* f
   c->bt.rmax2 = fene->r_max * fene->r_max;  // fene_eval (potentials.hpp:98)
 }
 
+// Slab mode's view of the whole system on the device (a cached block):
+// positions, velocities, masses, ids as the caller passed them, and the
+// input-order indices of this rank's particles.
+struct SlabStage {
+  char* block = nullptr;
+  size_t bytes = 0;
+  const double* pos = nullptr;
+  const double* vel = nullptr;   // nullptr: zero
+  const double* mass = nullptr;  // nullptr: 1
+  const long long* id = nullptr;
+  const int* sel = nullptr;
+  int64_t n_keep = 0;
+  void release() {
+    big_free(block, bytes);
+    block = nullptr;
+  }
+  ~SlabStage() { release(); }
+};
+
+void stage_slab_selection(tmd_gpu_ctx* c, const tmd_system* sys, SlabStage& st) {
+  const size_t n = static_cast<size_t>(sys->n);
+  const int ni = static_cast<int>(n);
+  size_t tb = 0;
+  ck(cub::DeviceSelect::Flagged(nullptr, tb, static_cast<const int*>(nullptr),
+                                static_cast<const unsigned char*>(nullptr),
+                                static_cast<int*>(nullptr), static_cast<int*>(nullptr), ni,
+                                c->stream), "cub select size");
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t b_pos = al(3 * n * sizeof(double)), b_vel = sys->vel ? b_pos : 0;
+  const size_t b_mass = sys->mass ? al(n * sizeof(double)) : 0, b_id = al(n * sizeof(long long));
+  const size_t b_idx = al(n * sizeof(int)), b_flag = al(n), b_cnt = 256;
+  st.block = static_cast<char*>(
+      big_alloc(b_pos + b_vel + b_mass + b_id + 2 * b_idx + b_flag + b_cnt + al(tb), &st.bytes));
+  char* q = st.block;
+  auto take = [&](size_t b) { char* r = q; q += b; return r; };
+  double* pos = reinterpret_cast<double*>(take(b_pos));
+  double* vel = sys->vel ? reinterpret_cast<double*>(take(b_vel)) : nullptr;
+  double* mass = sys->mass ? reinterpret_cast<double*>(take(b_mass)) : nullptr;
+  long long* id = reinterpret_cast<long long*>(take(b_id));
+  int* idx = reinterpret_cast<int*>(take(b_idx));
+  int* sel = reinterpret_cast<int*>(take(b_idx));
+  unsigned char* flag = reinterpret_cast<unsigned char*>(take(b_flag));
+  int* d_cnt = reinterpret_cast<int*>(take(b_cnt));
+  void* tmp = take(al(tb));
+  if (n > 0) {
+    ck(cudaMemcpyAsync(pos, sys->pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+       "H2D pos");
+    if (vel) {
+      ck(cudaMemcpyAsync(vel, sys->vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream), "H2D vel");
+    }
+    if (mass) {
+      ck(cudaMemcpyAsync(mass, sys->mass, n * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+         "H2D mass");
+    }
+    ck(cudaMemcpyAsync(id, sys->id, n * sizeof(long long), cudaMemcpyHostToDevice, c->stream),
+       "H2D id");
+    k_iota_int<<<blocks_for(sys->n, kBlock), kBlock, 0, c->stream>>>(ni, idx);
+    k_slab_flags<<<blocks_for(sys->n, kBlock), kBlock, 0, c->stream>>>(ni, pos, c->g, flag);
+    ck(cub::DeviceSelect::Flagged(tmp, tb, idx, flag, sel, d_cnt, ni, c->stream),
+       "cub select");
+  }
+  int cnt = 0;
+  if (n > 0) {
+    ck(cudaMemcpyAsync(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  }
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  st.pos = pos;
+  st.vel = vel;
+  st.mass = mass;
+  st.id = id;
+  st.sel = sel;
+  st.n_keep = cnt;
+}
+
 // The type column of the caller's FlatConfig, kept by id (see tmd_gpu_ctx).
 void set_type_table(tmd_gpu_ctx* c, const tmd_system* sys, const IdRange& r) {
   c->type_id.clear();
@@ -2037,17 +2150,18 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
 
     // Slab mode: keep the particles whose wrapped position lies in this
     // rank's z layers (exact host wrap + cell, bit-identical to the device's).
-    std::vector<int64_t> sel;  // slab mode: the kept particles (input order)
+    // Slab mode: the whole system goes to a device scratch block, where the
+    // particles whose wrapped position lies in this rank's z layers are
+    // selected (exact wrap + cell, bit-identical to the host's rule) and
+    // compacted in input order; they are unpacked into the slot arrays once
+    // those exist (below).
     int64_t n_keep = sys->n;
+    SlabStage stage;
     if (slab) {
       make_slab(c, rank, nranks);
-      for (int64_t k = 0; k < sys->n; ++k) {
-        const double z = host_wrap1(sys->pos[3 * k + 2], c->g.L[2]);
-        int cz = static_cast<int>(std::floor(z / c->g.cell_len[2]));
-        cz = std::min(std::max(cz, 0), c->g.dims[2] - 1);
-        if (cz >= c->g.z0 && cz < c->g.z0 + c->g.zown) sel.push_back(k);
-      }
-      n_keep = static_cast<int64_t>(sel.size());
+      stage_slab_selection(c, sys, stage);
+      n_keep = stage.n_keep;
+      mark("slab selection");
     }
     c->my_rank = rank;
     c->nranks = nranks;
@@ -2184,7 +2298,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
         off += (e.second + 255) / 256 * 256;
       }
     } else {
-      for (const auto& e : plan) *e.first = dalloc<char>(e.second);
+      for (const auto& e : plan) *e.first = sized_alloc(e.second);  // (cached: a slab regrows them)
     }
     c->cur = 0;
     c->pos = c->posb[0];
@@ -2243,34 +2357,14 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       }
       mark("upload enqueued");
     } else {
-      std::vector<double4> hp(m);
-      std::vector<double> hv(3 * m, 0.0), hm(m, 1.0);
-      std::vector<long long> hid(m);
-      for (size_t r = 0; r < m; ++r) {
-        const size_t k = static_cast<size_t>(sel[r]);
-        hp[r] = make_double4(sys->pos[3 * k], sys->pos[3 * k + 1], sys->pos[3 * k + 2], 0.0);
-        if (sys->vel) {
-          hv[r] = sys->vel[3 * k];
-          hv[m + r] = sys->vel[3 * k + 1];
-          hv[2 * m + r] = sys->vel[3 * k + 2];
-        }
-        if (sys->mass) hm[r] = sys->mass[k];
-        hid[r] = sys->id[k];
-      }
-      mark("host pack");
       if (m > 0) {
-        ck(cudaMemcpy(c->posb[0], hp.data(), m * sizeof(double4), cudaMemcpyHostToDevice),
-           "H2D pos");
-        ck(cudaMemcpy(c->vx, hv.data(), m * sizeof(double), cudaMemcpyHostToDevice), "H2D vx");
-        ck(cudaMemcpy(c->vy, hv.data() + m, m * sizeof(double), cudaMemcpyHostToDevice),
-           "H2D vy");
-        ck(cudaMemcpy(c->vz, hv.data() + 2 * m, m * sizeof(double), cudaMemcpyHostToDevice),
-           "H2D vz");
-        ck(cudaMemcpy(c->mass, hm.data(), m * sizeof(double), cudaMemcpyHostToDevice),
-           "H2D mass");
-        ck(cudaMemcpy(c->id, hid.data(), m * sizeof(long long), cudaMemcpyHostToDevice),
-           "H2D id");
+        k_slab_unpack<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
+            static_cast<int>(m), stage.sel, stage.pos, stage.vel, stage.mass, stage.id,
+            c->posb[0], c->vx, c->vy, c->vz, c->mass, c->id);
+        ck(cudaGetLastError(), "k_slab_unpack");
       }
+      ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+      stage.release();
       mark("upload");
     }
     k_set_far<<<1, 1, 0, c->stream>>>(c->posb[0] + n, c->posb[1] + n, far);  // list padding slot
@@ -2742,24 +2836,64 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
            "D2H mass");
       }
       ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-    } else {
-      HostState h = fetch(c, pos != nullptr, vel != nullptr, force != nullptr, false,
-                          mass != nullptr);
-      const size_t n = h.order.size();
-      for (size_t r = 0; r < n; ++r) {
-        const size_t s = h.order[r];
-        if (ids_out) ids_out[r] = h.id[s];
+    } else if (nn > 0) {
+      // ids of any shape (slab contexts, sparse ids): a device sort of the
+      // ids gives the slot order, one gather kernel writes id-ordered arrays
+      const int n = static_cast<int>(nn);
+      size_t tb = 0;
+      ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, static_cast<const long long*>(nullptr),
+                                         static_cast<long long*>(nullptr),
+                                         static_cast<const int*>(nullptr),
+                                         static_cast<int*>(nullptr), n, 0, 64, c->stream),
+         "cub sort size");
+      const size_t words = 11 * nn;  // pos 3, vel 3, force 3, mass 1 doubles + sorted ids
+      const size_t bytes = words * sizeof(double) + 2 * nn * sizeof(int) + tb + 256;
+      size_t got = 0;
+      char* scratch = static_cast<char*>(big_alloc(bytes, &got));
+      double* dpos = reinterpret_cast<double*>(scratch);
+      double* dvel = dpos + 3 * nn;
+      double* dfrc = dpos + 6 * nn;
+      double* dmass = dpos + 9 * nn;
+      long long* did = reinterpret_cast<long long*>(dpos + 10 * nn);
+      int* vin = reinterpret_cast<int*>(dpos + 11 * nn);
+      int* vout = vin + nn;
+      void* tmp = reinterpret_cast<char*>(vout + nn);
+      try {
+        k_iota_int<<<blocks_for(n, kBlock), kBlock, 0, c->stream>>>(n, vin);
+        ck(cub::DeviceRadixSort::SortPairs(tmp, tb, c->id, did, vin, vout, n, 0, 64, c->stream),
+           "cub sort ids");
+        k_download_gather<<<blocks_for(n, kBlock), kBlock, 0, c->stream>>>(
+            n, vout, c->pos, c->vx, c->vy, c->vz, c->fx, c->fy, c->fz, c->mass, c->g,
+            pos ? dpos : nullptr, vel ? dvel : nullptr, force ? dfrc : nullptr,
+            mass ? dmass : nullptr);
+        ck(cudaGetLastError(), "k_download_gather");
+        if (ids_out) {
+          ck(cudaMemcpyAsync(ids_out, did, nn * sizeof(long long), cudaMemcpyDeviceToHost,
+                             c->stream), "D2H id");
+        }
         if (pos) {
-          pos[3 * r] = host_wrap1(h.pos[s].x, c->g.L[0]);
-          pos[3 * r + 1] = host_wrap1(h.pos[s].y, c->g.L[1]);
-          pos[3 * r + 2] = host_wrap1(h.pos[s].z, c->g.L[2]);
+          ck(cudaMemcpyAsync(pos, dpos, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream), "D2H pos");
         }
-        for (int k = 0; k < 3; ++k) {
-          if (vel) vel[3 * r + k] = h.v[k][s];
-          if (force) force[3 * r + k] = h.f[k][s];
+        if (vel) {
+          ck(cudaMemcpyAsync(vel, dvel, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream), "D2H vel");
         }
-        if (mass) mass[r] = h.mass[s];
+        if (force) {
+          ck(cudaMemcpyAsync(force, dfrc, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream), "D2H force");
+        }
+        if (mass) {
+          ck(cudaMemcpyAsync(mass, dmass, nn * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream), "D2H mass");
+        }
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+      } catch (...) {
+        cudaStreamSynchronize(c->stream);
+        big_free(scratch, got);
+        throw;
       }
+      big_free(scratch, got);
     }
     if (type) {
       if (c->type_val.empty()) {
@@ -3473,7 +3607,10 @@ int tmd_gpu_brute_force(const tmd_system* sys, const tmd_lj_params* lj, double r
   return rc;
 }
 
+void release_nccl_cache();
+
 void tmd_gpu_release_cache(void) {
+  release_nccl_cache();
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (const CachedBlock& b : g_cache) {
     int cur = 0;
@@ -3496,6 +3633,12 @@ void tmd_gpu_destroy(tmd_gpu_ctx* c) {
 }  // extern "C"
 
 #include "tmd_slab_nccl.cuh"
+
+void release_nccl_cache() {
+#ifndef TMD_NO_NCCL
+  nccl_cache_release_all();
+#endif
+}
 
 namespace {
 void free_comm(tmd_gpu_ctx* c) {

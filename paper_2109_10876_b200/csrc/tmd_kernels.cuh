@@ -850,6 +850,74 @@ __global__ void __launch_bounds__(kBlock)
   if (omass) omass[r] = mass[s];
 }
 
+// The same, gathered in a given slot order (row r <- slot order[r]): the
+// download of contexts whose ids are not one dense range (slab contexts,
+// arbitrary ids), the order coming from a device sort of the ids.
+__global__ void __launch_bounds__(kBlock)
+    k_download_gather(int n, const int* __restrict__ order, const double4* __restrict__ pos,
+                      const double* __restrict__ vx, const double* __restrict__ vy,
+                      const double* __restrict__ vz, const double* __restrict__ fx,
+                      const double* __restrict__ fy, const double* __restrict__ fz,
+                      const double* __restrict__ mass, Geom g, double* __restrict__ opos,
+                      double* __restrict__ ovel, double* __restrict__ ofrc,
+                      double* __restrict__ omass) {
+  const int r = blockIdx.x * kBlock + threadIdx.x;
+  if (r >= n) return;
+  const int s = order[r];
+  if (opos) {
+    const double4 p = pos[s];
+    opos[3 * r] = wrap1(p.x, g.L[0]);
+    opos[3 * r + 1] = wrap1(p.y, g.L[1]);
+    opos[3 * r + 2] = wrap1(p.z, g.L[2]);
+  }
+  if (ovel) {
+    ovel[3 * r] = vx[s];
+    ovel[3 * r + 1] = vy[s];
+    ovel[3 * r + 2] = vz[s];
+  }
+  if (ofrc) {
+    ofrc[3 * r] = fx[s];
+    ofrc[3 * r + 1] = fy[s];
+    ofrc[3 * r + 2] = fz[s];
+  }
+  if (omass) omass[r] = mass[s];
+}
+
+// Slab create: particles whose wrapped position lies in this slab's z layers
+// (wrap1 + cell_coord: the rounding of distribute_records, domain.hpp:56-65).
+__global__ void __launch_bounds__(kBlock)
+    k_slab_flags(int n, const double* __restrict__ pos, Geom g, unsigned char* __restrict__ flag) {
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  if (k >= n) return;
+  const double z = wrap1(pos[3 * k + 2], g.L[2]);
+  const int cz = cell_coord(z, g.cell_len[2], g.dims[2]);
+  flag[k] = (cz >= g.z0 && cz < g.z0 + g.zown) ? 1 : 0;
+}
+
+// Slab create: this rank's particles (input order) from the staged system
+// into the slot arrays (double4 positions, SoA velocities).
+__global__ void __launch_bounds__(kBlock)
+    k_slab_unpack(int m, const int* __restrict__ sel, const double* __restrict__ pos,
+                  const double* __restrict__ vel, const double* __restrict__ mass,
+                  const long long* __restrict__ id, double4* __restrict__ opos,
+                  double* __restrict__ vx, double* __restrict__ vy, double* __restrict__ vz,
+                  double* __restrict__ omass, long long* __restrict__ oid) {
+  const int r = blockIdx.x * kBlock + threadIdx.x;
+  if (r >= m) return;
+  const size_t k = static_cast<size_t>(sel[r]);
+  opos[r] = make_double4(pos[3 * k], pos[3 * k + 1], pos[3 * k + 2], 0.0);
+  vx[r] = vel ? vel[3 * k] : 0.0;
+  vy[r] = vel ? vel[3 * k + 1] : 0.0;
+  vz[r] = vel ? vel[3 * k + 2] : 0.0;
+  omass[r] = mass ? mass[k] : 1.0;
+  oid[r] = id[k];
+}
+
+__global__ void k_iota_int(int n, int* __restrict__ v) {
+  const int r = blockIdx.x * kBlock + threadIdx.x;
+  if (r < n) v[r] = r;
+}
+
 // Per-step observable row (run_observed): PE and virial of this step's force
 // evaluation (halved full-list sums), KE of the post-kick velocities, written
 // straight into mapped pinned host memory — each recorded step's result

@@ -472,7 +472,11 @@ int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* c, const void* unique_id, int flags) {
     ncclUniqueId u;
     std::memcpy(&u, unique_id, sizeof u);
     auto nc = std::make_unique<NcclComm>();
-    nck(ncclCommInitRank(&nc->nc, c->nranks, u, c->my_rank), "ncclCommInitRank");
+    nc->device = c->device;
+    nc->nranks = c->nranks;
+    nc->rank = c->my_rank;
+    nc->nc = nccl_cache_take(c->device, c->nranks, c->my_rank);
+    if (!nc->nc) nck(ncclCommInitRank(&nc->nc, c->nranks, u, c->my_rank), "ncclCommInitRank");
     alloc_comm_staging(c);
     c->comm = nc.release();
 #endif

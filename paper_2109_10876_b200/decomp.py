@@ -259,8 +259,24 @@ class SlabContext:
     def size(self) -> int:
         return int(_abi.lib().tmd_gpu_size(self._h))
 
-    def download(self):
+    def download(self, out=None):
+        """(ids, pos, vel, forces) of the owned particles, sorted by id. out:
+        caller buffers (ids int64, pos / vel float64 (rows, 3), C-contiguous,
+        rows >= the owned count — e.g. pinned staging kept across calls) that
+        receive ids / positions / velocities in their first rows (forces are
+        not downloaded then); views of those rows are returned."""
         n = self.size()
+        if out is not None:
+            ids, pos, vel = out
+            for a, dt, cols in ((ids, np.int64, None), (pos, np.float64, 3),
+                                (vel, np.float64, 3)):
+                if a.dtype != dt or a.shape[0] < n or not a.flags.c_contiguous or \
+                        (cols and a.shape[1:] != (cols,)):
+                    raise ConfigError("download(out=...): ids (>=n,) int64, pos/vel (>=n, 3) "
+                                      "float64, C-contiguous")
+            self._c(_abi.lib().tmd_gpu_download(self._h, _ptr(ids), _ptr(pos), _ptr(vel), None,
+                                                   None, None))
+            return ids[:n], pos[:n], vel[:n], None
         ids = np.empty(n, np.int64)
         pos = np.empty((n, 3))
         vel = np.empty((n, 3))
@@ -785,9 +801,12 @@ class DecomposedEngine:
         return self.n_total
 
     # -- local state (this process's ranks) ---------------------------------------
-    def local_state(self):
+    def local_state(self, out=None):
         """(ids, pos, vel, forces) of the particles this process's ranks own,
-        sorted by id."""
+        sorted by id. out (one rank per process): caller buffers as in
+        SlabContext.download, filled in place (forces None)."""
+        if out is not None and len(self.ctx) == 1:
+            return next(iter(self.ctx.values())).download(out)
         parts = [c.download() for c in self.ctx.values()]
         ids = np.concatenate([p[0] for p in parts])
         o = np.argsort(ids, kind="stable")

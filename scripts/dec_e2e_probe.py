@@ -16,7 +16,10 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-f = E.gen_fcc(cells, 0.8442, 1.0, 12345)
+f0 = E.gen_fcc(cells, 0.8442, 1.0, 12345)
+pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+f = E.FlatConfig(f0.box, pin(f0.id), pin(f0.pos), pin(f0.vel))
+out = (pin(f0.id.copy()), pin(f0.pos.copy()), pin(f0.vel.copy()))
 cfg = E.EngineConfig(dt=0.005, section_timers=False, device=local)
 for rep in range(2):
     dist.barrier()
@@ -32,7 +35,7 @@ for rep in range(2):
     t3 = time.perf_counter()
     rows = ctx.run_observed_native(steps, 1)
     t4 = time.perf_counter()
-    st = ctx.download()
+    st = ctx.download(out)
     t5 = time.perf_counter()
     ms = lambda a, b: f"{1e3 * (b - a):.1f}"  # noqa: E731
     if r == 0:

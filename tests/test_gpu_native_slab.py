@@ -212,3 +212,22 @@ def test_native_loop_section_timers():
         assert 0.5 * t.elapsed <= t.section_sum() <= 1.05 * t.elapsed, t
     finally:
         dec.close()
+
+
+def test_local_state_into_caller_buffers():
+    """local_state(out=...) (one rank per process: the bench's pinned
+    download buffers, sized for the whole system) equals local_state()."""
+    g = load("fcc8_jit")
+    eng = native(g, 1)
+    try:
+        eng.run(30)
+        ids, pos, vel, _ = eng.local_state()
+        n = len(g["ids"])
+        out = (np.empty(n + 5, np.int64), np.empty((n + 5, 3)), np.empty((n + 5, 3)))
+        i2, p2, v2, f2 = eng.local_state(out=out)
+        assert f2 is None
+        np.testing.assert_array_equal(i2, ids)
+        np.testing.assert_array_equal(p2, pos)
+        np.testing.assert_array_equal(v2, vel)
+    finally:
+        eng.close()

@@ -778,18 +778,19 @@ class DecomposedEngine:
         return StepObservables(self.steps, ke, pe, 2.0 * ke / (3.0 * self.n_total), w)
 
     def timers(self):
-        """SectionTimers of the native loop (engine.hpp:145): per section the
-        largest of this process's ranks (each rank times its own stream with
-        CUDA events; the Python protocol fills none)."""
+        """SectionTimers of the native loop (engine.hpp:145): those of this
+        process's slowest rank (largest elapsed; each rank times its own
+        stream with CUDA events, a collective's wait for its peers included
+        in Comm). The Python protocol fills none."""
         from .engine import SectionTimers
-        secs, el = np.zeros(5), 0.0
+        best = SectionTimers(np.zeros(5), 0.0)
         for c in self.ctx.values():
             s5 = np.zeros(5)
             e = C.c_double()
             _check(_abi.lib().tmd_gpu_timers(c._h, _ptr(s5), C.byref(e)), c._h)
-            secs = np.maximum(secs, s5)
-            el = max(el, e.value)
-        return SectionTimers(secs, el)
+            if e.value >= best.elapsed:
+                best = SectionTimers(s5, e.value)
+        return best
 
     def step_count(self) -> int:
         return self.steps

@@ -1465,7 +1465,12 @@ __global__ void __launch_bounds__(128)
                 double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                 double* __restrict__ part_e, double* __restrict__ part_w,
                 const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
-  if (ctrl->halt) return;  // native slab loop: steps after a due rebuild are no-ops
+  if (ctrl->halt) {  // steps after a due rebuild are no-ops (speculative blocks: positions
+                     // carried to the other buffer)
+    const int i = blockIdx.x * 128 + threadIdx.x;
+    if (kMode == kFused && it.halt_copy && i < n) it.pos_out[i] = pos[i];
+    return;
+  }
   __shared__ double red[4];
   const int i = blockIdx.x * 128 + threadIdx.x;
   double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
@@ -1547,7 +1552,13 @@ __global__ void __launch_bounds__(kLanesPPB * kLanes, lanes_min_blocks(kLanes))
                    double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
                    double* __restrict__ part_e, double* __restrict__ part_w,
                    const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
-  if (ctrl->halt) return;
+  if (ctrl->halt) {  // (see k_forces_l1)
+    const int i = blockIdx.x * kLanesPPB + threadIdx.x;
+    if (kMode == kFused && it.halt_copy && threadIdx.x < kLanesPPB && i < n) {
+      it.pos_out[i] = pos[i];
+    }
+    return;
+  }
   constexpr int kThreads = kLanesPPB * kLanes;
   __shared__ double red[kThreads / 32];
   const int sub = threadIdx.x % kLanes;

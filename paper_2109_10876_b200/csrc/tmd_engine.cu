@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -63,6 +64,9 @@ constexpr int kLanesAutoMax = 4;
 // Up to this many particles graph steps keep the rebuild kernels as
 // early-returning nodes instead of a conditional IF node (see if_nodes).
 constexpr int64_t kChainMaxParticles = 262144;
+// Up to this many particles graph runs use speculative blocks (see
+// run_chunk); above, a conditional IF node per step (~7 us) is noise.
+constexpr int64_t kSpecMaxParticles = 4194304;
 
 struct CudaFail {
   std::string what;
@@ -427,6 +431,14 @@ struct tmd_gpu_ctx {
     uint64_t fixed = 0;  // kernels per launch outside the IF bodies
   };
   StepGraph sg[2][2];  // [block of kGraphSteps | single step][starting buffer parity]
+  // Speculative graph mode (spec_mode, chosen at create): blocks of K steps
+  // with no conditional node (k_decide_spec1 halts a block at a due rebuild)
+  // each followed by one closing step that holds the rebuild kernels; keyed
+  // K << 3 | open << 2 | parity << 1 | observed (K = 0: the closing step,
+  // open: it starts with the opening kick + drift).
+  bool spec_mode = false;
+  int halt_copy = 0;  // set while capturing a speculative block's force launches
+  std::map<int, StepGraph> spec;
   StepGraph sgo[2][2]; // the same with a per-step observable row (run_observed)
   int obs_stride = 0;           // > 0 while run_observed records rows
   int sgo_stride = 0;           // stride the observed graphs were captured with
@@ -445,16 +457,30 @@ struct tmd_gpu_ctx {
 
 namespace {
 
+void destroy_graph(tmd_gpu_ctx::StepGraph& s) {
+  if (s.exec) cudaGraphExecDestroy(s.exec);
+  if (s.graph) cudaGraphDestroy(s.graph);
+  s = tmd_gpu_ctx::StepGraph{};
+}
+
+void drop_spec_graphs(tmd_gpu_ctx* c, bool observed_only) {
+  for (auto it = c->spec.begin(); it != c->spec.end();) {
+    if (!observed_only || (it->first & 1)) {
+      destroy_graph(it->second);
+      it = c->spec.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
 void drop_graphs(tmd_gpu_ctx* c) {
   for (auto* fam : {&c->sg, &c->sgo}) {
     for (auto& row : *fam) {
-      for (auto& s : row) {
-        if (s.exec) cudaGraphExecDestroy(s.exec);
-        if (s.graph) cudaGraphDestroy(s.graph);
-        s = tmd_gpu_ctx::StepGraph{};
-      }
+      for (auto& s : row) destroy_graph(s);
     }
   }
+  drop_spec_graphs(c, false);
   c->graph_dirty = false;
 }
 
@@ -750,6 +776,7 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
   it.bt.ent = c->bnd_ent;
   const bool fh = kMode == kFused && c->fused_halo && c->fused_ready;
   it.exp = fh ? c->exp : nullptr;
+  it.halt_copy = kMode == kFused ? c->halt_copy : 0;
   it.rg[0] = fh ? c->rg[0][c->cur ^ 1] : nullptr;
   it.rg[1] = fh ? c->rg[1][c->cur ^ 1] : nullptr;
   if (c->variant == 1) {
@@ -1211,6 +1238,125 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
   if (c->cur != p) throw CudaFail{"graph capture changed the buffer parity"};
 }
 
+// ---- speculative graph mode ------------------------------------------------
+// A run is a sequence of cycles: a block of K steps (kick1 + drift, then per
+// step k_decide_spec1 + fused force kernel; no conditional node) and one
+// closing step (k_decide + resort + list build, gated on the decision, +
+// forces with the closing kick). A rebuild due inside the block halts it at
+// that step: the block's remaining force launches only carry the positions
+// to the other buffer (so the buffer parity after a block is known at
+// capture), and the closing step performs the halted step. K is predicted
+// so that the closing step lands on the next rebuild; a wrong guess costs
+// only time, never results. One host sync per cycle (~9 steps) replaces a
+// conditional IF node per step (~7 us each on B200, scripts/exp/if_cost.cu).
+constexpr int kSpecMax = 24;
+
+int spec_key(int K, bool open, int parity, bool observed) {
+  return (K << 3) | ((open ? 1 : 0) << 2) | (parity << 1) | (observed ? 1 : 0);
+}
+
+void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out) {
+  cudaGraph_t g = nullptr;
+  ck(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+  const int p = c->cur;
+  const uint64_t l0 = c->launches;
+  auto restore_host = [&] {
+    c->ls = c->stream;
+    c->halt_copy = 0;
+    c->cur = p;
+    c->pos = c->posb[p];
+    c->launches = l0;
+  };
+  try {
+    ck(cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal), "begin capture");
+    c->ls = c->stream;
+    if (K > 0) {  // block
+      launch_tick(c, kTickBlock, 0);
+      launch_kick_drift(c);
+      for (int s = 0; s < K; ++s) {
+        c->launches += 1;
+        k_decide_spec1<<<1, 1, 0, c->ls>>>(c->ctrl, c->g.rebuild_thr, tick_ptr(c));
+        launch_tick(c, kTickForces, -1);
+        c->halt_copy = 1;
+        launch_forces(c, kFused);
+        c->halt_copy = 0;
+        launch_obs_record(c);
+      }
+    } else {  // closing step
+      c->launches += 1;
+      k_clear_halt<<<1, 1, 0, c->ls>>>(c->ctrl);
+      if (open) {
+        launch_tick(c, kTickBlock, 0);
+        launch_kick_drift(c);
+      }
+      launch_decide(c, true);
+      launch_resort(c);
+      launch_build(c);
+      launch_tick(c, kTickForces, -1);
+      launch_forces(c, kKick2);
+      launch_obs_record(c);
+    }
+    enqueue_observables(c);
+    ck(cudaStreamEndCapture(c->stream, &g), "end capture");
+    cudaGraphExec_t exec = nullptr;
+    ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");
+    out.exec = exec;
+    out.graph = g;
+    out.fixed = c->launches - l0;
+  } catch (...) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t junk = nullptr;
+    if (cudaStreamIsCapturing(c->stream, &st) == cudaSuccess &&
+        st != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(c->stream, &junk);
+    }
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    out = tmd_gpu_ctx::StepGraph{};
+    restore_host();
+    throw;
+  }
+  restore_host();  // capture ran nothing: host state as before
+}
+
+tmd_gpu_ctx::StepGraph& spec_graph(tmd_gpu_ctx* c, int K, bool open, int parity) {
+  const bool observed = c->obs_stride > 0;
+  tmd_gpu_ctx::StepGraph& g = c->spec[spec_key(K, open, parity, observed)];
+  if (!g.exec) {
+    const int keep = c->cur;
+    c->cur = parity;
+    c->pos = c->posb[parity];
+    try {
+      capture_spec(c, K, open, g);
+    } catch (...) {
+      c->cur = keep;
+      c->pos = c->posb[keep];
+      throw;
+    }
+    c->cur = keep;
+    c->pos = c->posb[keep];
+  }
+  return g;
+}
+
+// Steps of the next block: the closing step aimed at the step whose decision
+// is predicted to rebuild (right after a rebuild: the last interval; later:
+// the displacement the last decision saw, extrapolated ballistically).
+int64_t spec_block(const tmd_gpu_ctx* c, int64_t done_step, int64_t left) {
+  int64_t k = 7;
+  if (c->last_rebuild_step >= 0) {
+    const int64_t t = done_step - c->last_rebuild_step;
+    const double m = c->h_ctrl->seen_d2, thr = c->g.rebuild_thr;
+    if (t <= 0 || !(m > 0.0)) {
+      if (c->rebuild_gap > 0) k = c->rebuild_gap - 1 - std::max<int64_t>(t, 0);
+    } else {
+      k = static_cast<int64_t>(std::ceil(static_cast<double>(t) * std::sqrt(thr / m))) - t - 1;
+    }
+  }
+  return std::max<int64_t>(0, std::min<int64_t>({k, kSpecMax, left - 1}));
+}
+
 // Enqueues `steps` steps without graphs: kick1+drift, then per step decide,
 // (gated) resort + list build, forces + fused integrator; PE reduction.
 void enqueue_segment(tmd_gpu_ctx* c, int64_t steps) {
@@ -1247,6 +1393,60 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
   const bool graphs = c->use_graphs;
   if (c->obs_stride > 0) {
     ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
+  }
+  if (graphs && c->spec_mode && c->variant == 3) {  // (variant 3's force kernels honour halt)
+    if (c->graph_dirty) drop_graphs(c);
+    if (c->obs_stride > 0 && c->sgo_stride != c->obs_stride) {
+      drop_spec_graphs(c, true);  // the stride is a kernel argument of the observed graphs
+      c->sgo_stride = c->obs_stride;
+    }
+    if (tick_ptr(c)) {
+      const long long base = c->step;
+      ck(cudaMemsetAsync(c->ticks, 0, sizeof(long long) * (kTickSteps * kTickPhases + 1),
+                         c->stream), "memset ticks");
+      ck(cudaMemcpyAsync(&c->ctrl->tick_base, &base, sizeof base, cudaMemcpyHostToDevice,
+                         c->stream), "H2D tick base");
+    }
+    int64_t done = c->step, left = steps;
+    if (c->last_rebuild_step < 0) c->last_rebuild_step = done;
+    long long rebuilds = c->h_ctrl->rebuilds;
+    while (left > 0) {
+      const int K = static_cast<int>(spec_block(c, done, left));
+      const int par_after = c->cur ^ (K & 1);
+      if (K > 0) {
+        tmd_gpu_ctx::StepGraph& b = spec_graph(c, K, false, c->cur);
+        ck(cudaGraphLaunch(b.exec, c->stream), "cudaGraphLaunch");
+        c->launches += b.fixed;
+      }
+      tmd_gpu_ctx::StepGraph& r = spec_graph(c, 0, K == 0, par_after);
+      ck(cudaGraphLaunch(r.exec, c->stream), "cudaGraphLaunch");
+      c->launches += r.fixed;
+      c->cur = par_after;
+      c->pos = c->posb[c->cur];
+      sync_ctrl(c);
+      if (c->h_ctrl->status & kOverflowBits) break;  // rolled back by the caller
+      const int64_t now = c->h_ctrl->step;
+      if (now <= done || now - done > K + 1) throw CudaFail{"speculative block: step count"};
+      left -= now - done;
+      done = now;
+      if (c->h_ctrl->rebuilds != rebuilds) {  // (only the closing step rebuilds)
+        rebuilds = c->h_ctrl->rebuilds;
+        c->rebuild_gap = now - c->last_rebuild_step;
+        c->last_rebuild_step = now;
+      }
+    }
+    if (tick_ptr(c)) {
+      c->launches += 1;
+      k_tick<<<1, 1, 0, c->stream>>>(c->ctrl, c->ticks, 0, 0, kTickSteps * kTickPhases);
+      c->h_ticks.resize(kTickSteps * kTickPhases + 1);
+      ck(cudaMemcpyAsync(c->h_ticks.data(), c->ticks, sizeof(long long) * c->h_ticks.size(),
+                         cudaMemcpyDeviceToHost, c->stream), "D2H ticks");
+    }
+    ck(cudaEventRecord(c->t1, c->stream), "cudaEventRecord");
+    sync_ctrl(c);
+    const bool ok = (c->h_ctrl->status & kOverflowBits) == 0;
+    if (ok && tick_ptr(c)) harvest_ticks(c, steps);
+    return ok;
   }
   if (graphs) {
     if (c->graph_dirty) drop_graphs(c);
@@ -2211,6 +2411,10 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       while (c->lanes < kLanesAutoMax && c->n * c->lanes < kLanesTargetThreads) c->lanes *= 2;
     }
     c->if_nodes = c->n > kChainMaxParticles;
+    // speculative blocks (no IF node per step) for systems up to 4M particles
+    // in the kernels that honour the halt word; the IF-node graphs above
+    c->spec_mode = !slab && c->n <= kSpecMaxParticles;
+    if (const char* e = std::getenv("TMD_SPEC")) c->spec_mode = !slab && e[0] == '1';
     if (const char* e = std::getenv("TMD_IF_NODES")) c->if_nodes = e[0] == '1';
     c->build_kind = params->reserved[3];
     c->build_auto = c->build_kind != 3 && c->build_kind != 5 && c->build_kind != 6;
@@ -3080,6 +3284,28 @@ int tmd_gpu_prepare_graphs(tmd_gpu_ctx* c, int64_t obs_stride) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (!c->use_graphs || c->nranks > 1 || c->g.zslab) return;
     if (c->graph_dirty) drop_graphs(c);
+    if (c->spec_mode && c->variant == 3) {  // the blocks a run of this system will launch
+      const int keep = c->obs_stride;
+      for (int pass = 0; pass < (obs_stride > 0 ? 2 : 1); ++pass) {
+        c->obs_stride = pass == 0 ? 0 : static_cast<int>(std::min<int64_t>(obs_stride, 1 << 30));
+        if (pass == 1 && c->sgo_stride != c->obs_stride) {
+          drop_spec_graphs(c, true);
+          c->sgo_stride = c->obs_stride;
+        }
+        try {
+          for (int par = 0; par < 2; ++par) {
+            for (int K = 1; K <= 12; ++K) spec_graph(c, K, false, par);
+            spec_graph(c, 0, false, par);
+            spec_graph(c, 0, true, par);
+          }
+        } catch (...) {
+          c->obs_stride = keep;
+          throw;
+        }
+      }
+      c->obs_stride = keep;
+      return;
+    }
     for (int kind = 0; kind < 2; ++kind) {
       auto& sgr = c->sg[kind][c->cur];
       if (!sgr.exec) capture_graph(c, kind == 0 ? kGraphSteps : 1, sgr);

@@ -66,6 +66,10 @@ struct Integ {
   // (peer memory over NVLink, or this GPU's own ghost slots with one slab).
   const int2* exp;
   double4* rg[2];
+  // Speculative graph blocks (single context): a launch after the block's
+  // rebuild decision halted it still advances the position buffers (copies
+  // pos -> pos_out), so the buffer parity after a block is fixed at capture.
+  int halt_copy;
 };
 
 // FENE forces of slot i (compute_bonded_forces, bonded.hpp:167-199): the bond
@@ -375,6 +379,7 @@ __global__ void k_decide(Ctrl* ctrl, double thr, int advance_step, int* log,
   const int force = ctrl->force_rebuild;
   const int r = (force != 0) || (m > thr);
   ctrl->rebuild = r;
+  ctrl->seen_d2 = m;
   if (cond != 0) cudaGraphSetConditional(cond, r ? 1u : 0u);  // graph mode: gate the IF node
   if (log) log[log_idx] = r;
   ctrl->force_rebuild = 0;
@@ -390,6 +395,26 @@ __global__ void k_set_far(double4* a, double4* b, double4 far) {
   *b = far;
 }
 
+// Rebuild decision of a speculative graph block (single context): a step
+// that needs a rebuild (or a host-forced one) halts the block — its force
+// launch and every later one only carry the positions forward — and the
+// block's closing rebuild step (k_decide + resort + build + forces) takes it.
+__global__ void k_decide_spec1(Ctrl* ctrl, double thr, long long* ticks) {
+  if (ctrl->halt) return;
+  stamp(ctrl, ticks, kTickDecide, 0);
+  const double m = __longlong_as_double(static_cast<long long>(ctrl->max_d2));
+  ctrl->seen_d2 = m;
+  if (ctrl->force_rebuild != 0 || m > thr) {
+    ctrl->halt = 1;
+    return;
+  }
+  ctrl->rebuild = 0;
+  ctrl->max_d2 = 0ull;
+  ctrl->step += 1;
+}
+
+__global__ void k_clear_halt(Ctrl* ctrl) { ctrl->halt = 0; }
+
 // A phase stamp on its own (block start: off 0; forces start: off -1, after
 // the step's decision advanced the counter; the chunk end: slot `end`).
 __global__ void k_tick(const Ctrl* ctrl, long long* ticks, int ph, int off, int end) {
@@ -397,6 +422,7 @@ __global__ void k_tick(const Ctrl* ctrl, long long* ticks, int ph, int off, int 
     ticks[end] = global_ns();
     return;
   }
+  if (ctrl->halt) return;  // a halted speculative block's remaining steps
   stamp(ctrl, ticks, ph, off);
 }
 

@@ -382,6 +382,8 @@ struct tmd_gpu_ctx {
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
   Ctrl* ctrl = nullptr;
   Ctrl* h_ctrl = nullptr;      // pinned mirror
+  Ctrl* h_ctrl_cyc = nullptr;  // pinned mirrors of in-flight speculative cycles [2]
+  cudaEvent_t ev_cyc[2] = {nullptr, nullptr};
   double* h_scalars = nullptr; // pinned
 
   // chunk checkpoint (rollback on list overflow)
@@ -514,6 +516,10 @@ void free_all(tmd_gpu_ctx* c) {
   big_free(c->arena, c->arena_bytes);  // back to the process cache
   big_free(c->nbr, c->nbr_bytes);
   pinned_small_free(c->h_ctrl, sizeof(Ctrl));
+  pinned_small_free(c->h_ctrl_cyc, 2 * sizeof(Ctrl));
+  for (cudaEvent_t e : c->ev_cyc) {
+    if (e) cudaEventDestroy(e);
+  }
   pinned_small_free(c->obs_host, sizeof(double) * 4 * kObsRowsAlloc);
   pinned_small_free(c->h_scalars, 4 * sizeof(double));
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
@@ -1407,34 +1413,84 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
       ck(cudaMemcpyAsync(&c->ctrl->tick_base, &base, sizeof base, cudaMemcpyHostToDevice,
                          c->stream), "H2D tick base");
     }
-    int64_t done = c->step, left = steps;
+    // Cycles are pipelined two deep: cycle i+1 is enqueued before the host
+    // waits for cycle i (its status word copied into a pinned mirror behind
+    // it), so the GPU never idles on the host. Cycle i+1 is planned as if
+    // cycle i ran in full and rebuilt at its closing step; a cycle that
+    // halted early advanced fewer steps, which only leaves more to plan
+    // (never an overshoot), and a wrong guess costs time, never results.
+    if (!c->h_ctrl_cyc) {
+      c->h_ctrl_cyc = static_cast<Ctrl*>(pinned_small(2 * sizeof(Ctrl)));
+      for (auto& e : c->ev_cyc) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ev");
+    }
+    struct Cycle {
+      int K, slot;
+      int64_t planned_end;  // step count if the cycle runs in full
+    };
+    Cycle q[2];
+    int nq = 0, next_slot = 0;
+    int64_t done = c->step;            // steps known complete (from synced cycles)
+    int64_t planned = c->step;         // steps enqueued (assuming full cycles)
+    const int64_t target = c->step + steps;
     if (c->last_rebuild_step < 0) c->last_rebuild_step = done;
     long long rebuilds = c->h_ctrl->rebuilds;
-    while (left > 0) {
-      const int K = static_cast<int>(spec_block(c, done, left));
-      const int par_after = c->cur ^ (K & 1);
-      if (K > 0) {
-        tmd_gpu_ctx::StepGraph& b = spec_graph(c, K, false, c->cur);
-        ck(cudaGraphLaunch(b.exec, c->stream), "cudaGraphLaunch");
-        c->launches += b.fixed;
+    bool overflow = false;
+    while (!overflow && (done < target || nq > 0)) {
+      while (nq < 2 && planned < target) {
+        // plan from the last synced state, or, with a cycle in flight, as if
+        // it rebuilt at its closing step
+        int K;
+        if (nq == 0) {
+          K = static_cast<int>(spec_block(c, planned, target - planned));
+        } else {
+          const int64_t gap = c->rebuild_gap > 0 ? c->rebuild_gap : 8;
+          K = static_cast<int>(std::max<int64_t>(
+              0, std::min<int64_t>({gap - 1, kSpecMax, target - planned - 1})));
+        }
+        const int par_after = c->cur ^ (K & 1);
+        if (K > 0) {
+          tmd_gpu_ctx::StepGraph& b = spec_graph(c, K, false, c->cur);
+          ck(cudaGraphLaunch(b.exec, c->stream), "cudaGraphLaunch");
+          c->launches += b.fixed;
+        }
+        tmd_gpu_ctx::StepGraph& r = spec_graph(c, 0, K == 0, par_after);
+        ck(cudaGraphLaunch(r.exec, c->stream), "cudaGraphLaunch");
+        c->launches += r.fixed;
+        c->cur = par_after;
+        c->pos = c->posb[c->cur];
+        const int slot = next_slot;
+        next_slot ^= 1;
+        ck(cudaMemcpyAsync(&c->h_ctrl_cyc[slot], c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
+                           c->stream), "D2H ctrl");
+        ck(cudaEventRecord(c->ev_cyc[slot], c->stream), "cudaEventRecord");
+        planned += K + 1;
+        q[nq++] = {K, slot, planned};
       }
-      tmd_gpu_ctx::StepGraph& r = spec_graph(c, 0, K == 0, par_after);
-      ck(cudaGraphLaunch(r.exec, c->stream), "cudaGraphLaunch");
-      c->launches += r.fixed;
-      c->cur = par_after;
-      c->pos = c->posb[c->cur];
-      sync_ctrl(c);
-      if (c->h_ctrl->status & kOverflowBits) break;  // rolled back by the caller
-      const int64_t now = c->h_ctrl->step;
-      if (now <= done || now - done > K + 1) throw CudaFail{"speculative block: step count"};
-      left -= now - done;
+      if (nq == 0) break;
+      const Cycle cy = q[0];
+      q[0] = q[1];
+      --nq;
+      ck(cudaEventSynchronize(c->ev_cyc[cy.slot]), "cudaEventSynchronize");
+      const Ctrl& h = c->h_ctrl_cyc[cy.slot];
+      *c->h_ctrl = h;
+      if (h.status & kOverflowBits) {
+        overflow = true;  // rolled back by the caller
+        break;
+      }
+      const int64_t now = h.step;
+      if (now <= done || now - done > cy.K + 1) throw CudaFail{"speculative block: step count"};
+      // a cycle that halted early ran fewer steps than planned: the rest is
+      // planned again
+      planned -= cy.planned_end - now;
+      if (nq > 0) q[0].planned_end -= cy.planned_end - now;
       done = now;
-      if (c->h_ctrl->rebuilds != rebuilds) {  // (only the closing step rebuilds)
-        rebuilds = c->h_ctrl->rebuilds;
+      if (h.rebuilds != rebuilds) {  // (only the closing step rebuilds)
+        rebuilds = h.rebuilds;
         c->rebuild_gap = now - c->last_rebuild_step;
         c->last_rebuild_step = now;
       }
     }
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");  // (overflow: drain)
     if (tick_ptr(c)) {
       c->launches += 1;
       k_tick<<<1, 1, 0, c->stream>>>(c->ctrl, c->ticks, 0, 0, kTickSteps * kTickPhases);

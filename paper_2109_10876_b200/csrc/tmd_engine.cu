@@ -1289,21 +1289,51 @@ void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out)
         c->halt_copy = 0;
         launch_obs_record(c);
       }
-    } else {  // closing step
+    } else {  // closing step: the rebuild kernels behind one IF node per cycle
       c->launches += 1;
       k_clear_halt<<<1, 1, 0, c->ls>>>(c->ctrl);
       if (open) {
         launch_tick(c, kTickBlock, 0);
         launch_kick_drift(c);
       }
+      cudaGraphConditionalHandle h;
+      ck(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault),
+         "cudaGraphConditionalHandleCreate");
+      c->cond_handle = h;
       launch_decide(c, true);
+      c->cond_handle = 0;
+      cudaStreamCaptureStatus st;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      ck(cudaStreamGetCaptureInfo(c->stream, &st, nullptr, nullptr, &deps, &ndeps),
+         "cudaStreamGetCaptureInfo");
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeIf;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cnode;
+      ck(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp), "cudaGraphAddNode(conditional)");
+      const uint64_t b0 = c->launches;
+      ck(cudaStreamBeginCaptureToGraph(c->side, cp.conditional.phGraph_out[0], nullptr, nullptr,
+                                       0, cudaStreamCaptureModeThreadLocal),
+         "begin body capture");
+      c->ls = c->side;
       launch_resort(c);
       launch_build(c);
+      c->ls = c->stream;
+      cudaGraph_t bodyg;
+      ck(cudaStreamEndCapture(c->side, &bodyg), "end body capture");
+      c->graph_body_kernels = c->launches - b0;
+      c->launches = b0;  // (counted when the body runs)
+      ck(cudaStreamUpdateCaptureDependencies(c->stream, &cnode, 1,
+                                             cudaStreamSetCaptureDependencies),
+         "cudaStreamUpdateCaptureDependencies");
       launch_tick(c, kTickForces, -1);
       launch_forces(c, kKick2);
       launch_obs_record(c);
+      enqueue_observables(c);  // (blocks skip it: a closing step always follows)
     }
-    enqueue_observables(c);
     ck(cudaStreamEndCapture(c->stream, &g), "end capture");
     cudaGraphExec_t exec = nullptr;
     ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");
@@ -1313,6 +1343,9 @@ void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out)
   } catch (...) {
     cudaStreamCaptureStatus st;
     cudaGraph_t junk = nullptr;
+    if (cudaStreamIsCapturing(c->side, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(c->side, &junk);
+    }
     if (cudaStreamIsCapturing(c->stream, &st) == cudaSuccess &&
         st != cudaStreamCaptureStatusNone) {
       cudaStreamEndCapture(c->stream, &junk);
@@ -1320,6 +1353,7 @@ void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out)
     cudaGetLastError();
     cudaGraphDestroy(g);
     out = tmd_gpu_ctx::StepGraph{};
+    c->cond_handle = 0;
     restore_host();
     throw;
   }
@@ -1350,7 +1384,7 @@ tmd_gpu_ctx::StepGraph& spec_graph(tmd_gpu_ctx* c, int K, bool open, int parity)
 // is predicted to rebuild (right after a rebuild: the last interval; later:
 // the displacement the last decision saw, extrapolated ballistically).
 int64_t spec_block(const tmd_gpu_ctx* c, int64_t done_step, int64_t left) {
-  int64_t k = 7;
+  int64_t k = kSpecMax;
   if (c->last_rebuild_step >= 0) {
     const int64_t t = done_step - c->last_rebuild_step;
     const double m = c->h_ctrl->seen_d2, thr = c->g.rebuild_thr;
@@ -1443,7 +1477,7 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
         if (nq == 0) {
           K = static_cast<int>(spec_block(c, planned, target - planned));
         } else {
-          const int64_t gap = c->rebuild_gap > 0 ? c->rebuild_gap : 8;
+          const int64_t gap = c->rebuild_gap > 0 ? c->rebuild_gap : kSpecMax + 1;
           K = static_cast<int>(std::max<int64_t>(
               0, std::min<int64_t>({gap - 1, kSpecMax, target - planned - 1})));
         }
@@ -1485,6 +1519,7 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
       if (nq > 0) q[0].planned_end -= cy.planned_end - now;
       done = now;
       if (h.rebuilds != rebuilds) {  // (only the closing step rebuilds)
+        c->launches += static_cast<uint64_t>(h.rebuilds - rebuilds) * c->graph_body_kernels;
         rebuilds = h.rebuilds;
         c->rebuild_gap = now - c->last_rebuild_step;
         c->last_rebuild_step = now;

@@ -382,8 +382,8 @@ struct tmd_gpu_ctx {
   double* scalars = nullptr;  // [0] pe, [1] virial, [2] ke
   Ctrl* ctrl = nullptr;
   Ctrl* h_ctrl = nullptr;      // pinned mirror
-  Ctrl* h_ctrl_cyc = nullptr;  // pinned mirrors of in-flight speculative cycles [2]
-  cudaEvent_t ev_cyc[2] = {nullptr, nullptr};
+  Ctrl* h_ctrl_cyc = nullptr;  // pinned status snapshots of speculative cycles [4]
+  cudaEvent_t ev_cyc[4] = {nullptr, nullptr, nullptr, nullptr};
   double* h_scalars = nullptr; // pinned
 
   // chunk checkpoint (rollback on list overflow)
@@ -516,7 +516,7 @@ void free_all(tmd_gpu_ctx* c) {
   big_free(c->arena, c->arena_bytes);  // back to the process cache
   big_free(c->nbr, c->nbr_bytes);
   pinned_small_free(c->h_ctrl, sizeof(Ctrl));
-  pinned_small_free(c->h_ctrl_cyc, 2 * sizeof(Ctrl));
+  pinned_small_free(c->h_ctrl_cyc, 4 * sizeof(Ctrl));
   for (cudaEvent_t e : c->ev_cyc) {
     if (e) cudaEventDestroy(e);
   }
@@ -1383,11 +1383,11 @@ tmd_gpu_ctx::StepGraph& spec_graph(tmd_gpu_ctx* c, int K, bool open, int parity)
 // Steps of the next block: the closing step aimed at the step whose decision
 // is predicted to rebuild (right after a rebuild: the last interval; later:
 // the displacement the last decision saw, extrapolated ballistically).
-int64_t spec_block(const tmd_gpu_ctx* c, int64_t done_step, int64_t left) {
+int64_t spec_block(const tmd_gpu_ctx* c, int64_t done_step, int64_t left, double m) {
   int64_t k = kSpecMax;
   if (c->last_rebuild_step >= 0) {
     const int64_t t = done_step - c->last_rebuild_step;
-    const double m = c->h_ctrl->seen_d2, thr = c->g.rebuild_thr;
+    const double thr = c->g.rebuild_thr;
     if (t <= 0 || !(m > 0.0)) {
       if (c->rebuild_gap > 0) k = c->rebuild_gap - 1 - std::max<int64_t>(t, 0);
     } else {
@@ -1447,83 +1447,87 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
       ck(cudaMemcpyAsync(&c->ctrl->tick_base, &base, sizeof base, cudaMemcpyHostToDevice,
                          c->stream), "H2D tick base");
     }
-    // Cycles are pipelined two deep: cycle i+1 is enqueued before the host
-    // waits for cycle i (its status word copied into a pinned mirror behind
-    // it), so the GPU never idles on the host. Cycle i+1 is planned as if
-    // cycle i ran in full and rebuilt at its closing step; a cycle that
-    // halted early advanced fewer steps, which only leaves more to plan
-    // (never an overshoot), and a wrong guess costs time, never results.
+    // Each cycle leaves two status snapshots in pinned memory: A after the
+    // block, B after the closing step. A tells the host exactly what the
+    // closing step will do (the block halted, or the displacement it left
+    // exceeds the threshold: a rebuild), so the next cycle is planned and
+    // enqueued while the closing step still runs — the GPU does not wait for
+    // the host — and B, read after that, carries the closing step's status
+    // (list overflow).
     if (!c->h_ctrl_cyc) {
-      c->h_ctrl_cyc = static_cast<Ctrl*>(pinned_small(2 * sizeof(Ctrl)));
+      c->h_ctrl_cyc = static_cast<Ctrl*>(pinned_small(4 * sizeof(Ctrl)));
       for (auto& e : c->ev_cyc) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ev");
     }
-    struct Cycle {
-      int K, slot;
-      int64_t planned_end;  // step count if the cycle runs in full
-    };
-    Cycle q[2];
-    int nq = 0, next_slot = 0;
-    int64_t done = c->step;            // steps known complete (from synced cycles)
-    int64_t planned = c->step;         // steps enqueued (assuming full cycles)
+    int64_t done = c->step;
     const int64_t target = c->step + steps;
     if (c->last_rebuild_step < 0) c->last_rebuild_step = done;
+    double seen = c->h_ctrl->seen_d2;
     long long rebuilds = c->h_ctrl->rebuilds;
     bool overflow = false;
-    while (!overflow && (done < target || nq > 0)) {
-      while (nq < 2 && planned < target) {
-        // plan from the last synced state, or, with a cycle in flight, as if
-        // it rebuilt at its closing step
-        int K;
-        if (nq == 0) {
-          K = static_cast<int>(spec_block(c, planned, target - planned));
-        } else {
-          const int64_t gap = c->rebuild_gap > 0 ? c->rebuild_gap : kSpecMax + 1;
-          K = static_cast<int>(std::max<int64_t>(
-              0, std::min<int64_t>({gap - 1, kSpecMax, target - planned - 1})));
-        }
-        const int par_after = c->cur ^ (K & 1);
-        if (K > 0) {
-          tmd_gpu_ctx::StepGraph& b = spec_graph(c, K, false, c->cur);
-          ck(cudaGraphLaunch(b.exec, c->stream), "cudaGraphLaunch");
-          c->launches += b.fixed;
-        }
-        tmd_gpu_ctx::StepGraph& r = spec_graph(c, 0, K == 0, par_after);
-        ck(cudaGraphLaunch(r.exec, c->stream), "cudaGraphLaunch");
-        c->launches += r.fixed;
-        c->cur = par_after;
-        c->pos = c->posb[c->cur];
-        const int slot = next_slot;
-        next_slot ^= 1;
-        ck(cudaMemcpyAsync(&c->h_ctrl_cyc[slot], c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
-                           c->stream), "D2H ctrl");
-        ck(cudaEventRecord(c->ev_cyc[slot], c->stream), "cudaEventRecord");
-        planned += K + 1;
-        q[nq++] = {K, slot, planned};
+    // cycle i uses snapshots / events [2 (i % 2)] (A) and [2 (i % 2) + 1] (B)
+    auto launch_cycle = [&](int K, int slot) {
+      const int par_after = c->cur ^ (K & 1);
+      if (K > 0) {
+        tmd_gpu_ctx::StepGraph& b = spec_graph(c, K, false, c->cur);
+        ck(cudaGraphLaunch(b.exec, c->stream), "cudaGraphLaunch");
+        c->launches += b.fixed;
       }
-      if (nq == 0) break;
-      const Cycle cy = q[0];
-      q[0] = q[1];
-      --nq;
-      ck(cudaEventSynchronize(c->ev_cyc[cy.slot]), "cudaEventSynchronize");
-      const Ctrl& h = c->h_ctrl_cyc[cy.slot];
-      *c->h_ctrl = h;
-      if (h.status & kOverflowBits) {
-        overflow = true;  // rolled back by the caller
+      ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot], c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
+                         c->stream), "D2H ctrl");
+      ck(cudaEventRecord(c->ev_cyc[2 * slot], c->stream), "cudaEventRecord");
+      tmd_gpu_ctx::StepGraph& r = spec_graph(c, 0, K == 0, par_after);
+      ck(cudaGraphLaunch(r.exec, c->stream), "cudaGraphLaunch");
+      c->launches += r.fixed;
+      ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot + 1], c->ctrl, sizeof(Ctrl),
+                         cudaMemcpyDeviceToHost, c->stream), "D2H ctrl");
+      ck(cudaEventRecord(c->ev_cyc[2 * slot + 1], c->stream), "cudaEventRecord");
+      c->cur = par_after;
+      c->pos = c->posb[c->cur];
+    };
+    int K = static_cast<int>(spec_block(c, done, target - done, seen));
+    int slot = 0;
+    launch_cycle(K, slot);
+    for (;;) {
+      // A: the block's outcome, hence the closing step's
+      ck(cudaEventSynchronize(c->ev_cyc[2 * slot]), "cudaEventSynchronize");
+      const Ctrl a = c->h_ctrl_cyc[2 * slot];
+      if (a.status & kOverflowBits) {
+        overflow = true;
         break;
       }
-      const int64_t now = h.step;
-      if (now <= done || now - done > cy.K + 1) throw CudaFail{"speculative block: step count"};
-      // a cycle that halted early ran fewer steps than planned: the rest is
-      // planned again
-      planned -= cy.planned_end - now;
-      if (nq > 0) q[0].planned_end -= cy.planned_end - now;
-      done = now;
-      if (h.rebuilds != rebuilds) {  // (only the closing step rebuilds)
-        c->launches += static_cast<uint64_t>(h.rebuilds - rebuilds) * c->graph_body_kernels;
-        rebuilds = h.rebuilds;
-        c->rebuild_gap = now - c->last_rebuild_step;
-        c->last_rebuild_step = now;
+      if (a.step < done || a.step - done > K) throw CudaFail{"speculative block: step count"};
+      const double m = __builtin_bit_cast(double, a.max_d2);
+      const bool rebuild = a.halt != 0 || a.force_rebuild != 0 || m > c->g.rebuild_thr;
+      done = a.step + 1;  // the closing step's
+      if (rebuild) {
+        c->rebuild_gap = done - c->last_rebuild_step;
+        c->last_rebuild_step = done;
+        seen = 0.0;
+      } else {
+        seen = m;
       }
+      // the next cycle goes in while this closing step still runs; its B is
+      // read after that
+      int K_next = -1;
+      if (done < target) {
+        K_next = static_cast<int>(spec_block(c, done, target - done, seen));
+        launch_cycle(K_next, slot ^ 1);
+      }
+      ck(cudaEventSynchronize(c->ev_cyc[2 * slot + 1]), "cudaEventSynchronize");
+      const Ctrl b = c->h_ctrl_cyc[2 * slot + 1];
+      *c->h_ctrl = b;
+      if (b.status & kOverflowBits) {
+        overflow = true;
+        break;
+      }
+      if (b.step != done) throw CudaFail{"speculative block: closing step count"};
+      if (b.rebuilds != rebuilds) {  // (only the closing step rebuilds)
+        c->launches += static_cast<uint64_t>(b.rebuilds - rebuilds) * c->graph_body_kernels;
+        rebuilds = b.rebuilds;
+      }
+      if (K_next < 0) break;
+      K = K_next;
+      slot ^= 1;
     }
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");  // (overflow: drain)
     if (tick_ptr(c)) {

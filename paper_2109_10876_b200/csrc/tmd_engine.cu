@@ -1257,11 +1257,15 @@ void capture_graph_body(tmd_gpu_ctx* c, int nsteps, cudaGraph_t g,
 // conditional IF node per step (~7 us each on B200, scripts/exp/if_cost.cu).
 constexpr int kSpecMax = 24;
 
-int spec_key(int K, bool open, int parity, bool observed) {
-  return (K << 3) | ((open ? 1 : 0) << 2) | (parity << 1) | (observed ? 1 : 0);
+int spec_key(int K, int slot, int parity, bool observed) {
+  return (K << 3) | (slot << 2) | (parity << 1) | (observed ? 1 : 0);
 }
 
-void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out) {
+// One cycle as one graph: the block (K >= 1 steps), the status snapshot A
+// (a copy of the status word into pinned memory + an event), the closing
+// step (opening kick + drift too when K = 0), snapshot B.
+void capture_spec(tmd_gpu_ctx* c, int K, int slot, tmd_gpu_ctx::StepGraph& out) {
+  const bool open = K == 0;
   cudaGraph_t g = nullptr;
   ck(cudaGraphCreate(&g, 0), "cudaGraphCreate");
   const int p = c->cur;
@@ -1289,7 +1293,11 @@ void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out)
         c->halt_copy = 0;
         launch_obs_record(c);
       }
-    } else {  // closing step: the rebuild kernels behind one IF node per cycle
+    }
+    ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot], c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
+                       c->stream), "D2H ctrl");
+    ck(cudaEventRecord(c->ev_cyc[2 * slot], c->stream), "cudaEventRecord");
+    {  // closing step: the rebuild kernels behind one IF node per cycle
       c->launches += 1;
       k_clear_halt<<<1, 1, 0, c->ls>>>(c->ctrl);
       if (open) {
@@ -1332,8 +1340,11 @@ void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out)
       launch_tick(c, kTickForces, -1);
       launch_forces(c, kKick2);
       launch_obs_record(c);
-      enqueue_observables(c);  // (blocks skip it: a closing step always follows)
+      enqueue_observables(c);
     }
+    ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot + 1], c->ctrl, sizeof(Ctrl),
+                       cudaMemcpyDeviceToHost, c->stream), "D2H ctrl");
+    ck(cudaEventRecord(c->ev_cyc[2 * slot + 1], c->stream), "cudaEventRecord");
     ck(cudaStreamEndCapture(c->stream, &g), "end capture");
     cudaGraphExec_t exec = nullptr;
     ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");
@@ -1360,15 +1371,19 @@ void capture_spec(tmd_gpu_ctx* c, int K, bool open, tmd_gpu_ctx::StepGraph& out)
   restore_host();  // capture ran nothing: host state as before
 }
 
-tmd_gpu_ctx::StepGraph& spec_graph(tmd_gpu_ctx* c, int K, bool open, int parity) {
+tmd_gpu_ctx::StepGraph& spec_graph(tmd_gpu_ctx* c, int K, int slot, int parity) {
   const bool observed = c->obs_stride > 0;
-  tmd_gpu_ctx::StepGraph& g = c->spec[spec_key(K, open, parity, observed)];
+  if (!c->h_ctrl_cyc) {
+    c->h_ctrl_cyc = static_cast<Ctrl*>(pinned_small(4 * sizeof(Ctrl)));
+    for (auto& e : c->ev_cyc) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ev");
+  }
+  tmd_gpu_ctx::StepGraph& g = c->spec[spec_key(K, slot, parity, observed)];
   if (!g.exec) {
     const int keep = c->cur;
     c->cur = parity;
     c->pos = c->posb[parity];
     try {
-      capture_spec(c, K, open, g);
+      capture_spec(c, K, slot, g);
     } catch (...) {
       c->cur = keep;
       c->pos = c->posb[keep];
@@ -1454,10 +1469,6 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
     // enqueued while the closing step still runs — the GPU does not wait for
     // the host — and B, read after that, carries the closing step's status
     // (list overflow).
-    if (!c->h_ctrl_cyc) {
-      c->h_ctrl_cyc = static_cast<Ctrl*>(pinned_small(4 * sizeof(Ctrl)));
-      for (auto& e : c->ev_cyc) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ev");
-    }
     int64_t done = c->step;
     const int64_t target = c->step + steps;
     if (c->last_rebuild_step < 0) c->last_rebuild_step = done;
@@ -1466,59 +1477,60 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
     bool overflow = false;
     // cycle i uses snapshots / events [2 (i % 2)] (A) and [2 (i % 2) + 1] (B)
     auto launch_cycle = [&](int K, int slot) {
-      const int par_after = c->cur ^ (K & 1);
-      if (K > 0) {
-        tmd_gpu_ctx::StepGraph& b = spec_graph(c, K, false, c->cur);
-        ck(cudaGraphLaunch(b.exec, c->stream), "cudaGraphLaunch");
-        c->launches += b.fixed;
-      }
-      ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot], c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
-                         c->stream), "D2H ctrl");
-      ck(cudaEventRecord(c->ev_cyc[2 * slot], c->stream), "cudaEventRecord");
-      tmd_gpu_ctx::StepGraph& r = spec_graph(c, 0, K == 0, par_after);
-      ck(cudaGraphLaunch(r.exec, c->stream), "cudaGraphLaunch");
-      c->launches += r.fixed;
-      ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot + 1], c->ctrl, sizeof(Ctrl),
-                         cudaMemcpyDeviceToHost, c->stream), "D2H ctrl");
-      ck(cudaEventRecord(c->ev_cyc[2 * slot + 1], c->stream), "cudaEventRecord");
-      c->cur = par_after;
+      tmd_gpu_ctx::StepGraph& g = spec_graph(c, K, slot, c->cur);
+      ck(cudaGraphLaunch(g.exec, c->stream), "cudaGraphLaunch");
+      c->launches += g.fixed;
+      c->cur ^= K & 1;
       c->pos = c->posb[c->cur];
     };
     int K = static_cast<int>(spec_block(c, done, target - done, seen));
     int slot = 0;
     launch_cycle(K, slot);
-    for (;;) {
-      // A: the block's outcome, hence the closing step's
-      ck(cudaEventSynchronize(c->ev_cyc[2 * slot]), "cudaEventSynchronize");
-      const Ctrl a = c->h_ctrl_cyc[2 * slot];
-      if (a.status & kOverflowBits) {
-        overflow = true;
-        break;
+    static const bool spec_log = std::getenv("TMD_SPEC_LOG") != nullptr;  // (diagnostics)
+    auto note_step = [&](int64_t now, bool rebuilt, double m) {
+      if (spec_log) {
+        std::fprintf(stderr, "[spec] K=%d steps %lld..%lld rebuilt=%d m=%.4g\n", K,
+                     static_cast<long long>(done), static_cast<long long>(now), rebuilt ? 1 : 0, m);
       }
-      if (a.step < done || a.step - done > K) throw CudaFail{"speculative block: step count"};
-      const double m = __builtin_bit_cast(double, a.max_d2);
-      const bool rebuild = a.halt != 0 || a.force_rebuild != 0 || m > c->g.rebuild_thr;
-      done = a.step + 1;  // the closing step's
-      if (rebuild) {
+      done = now;
+      if (rebuilt) {
         c->rebuild_gap = done - c->last_rebuild_step;
         c->last_rebuild_step = done;
         seen = 0.0;
       } else {
         seen = m;
       }
-      // the next cycle goes in while this closing step still runs; its B is
-      // read after that
+    };
+    for (;;) {
+      // A (after the block): with K > 0 it fixes what the closing step does
+      // (halted, or the displacement the block left exceeds the threshold:
+      // a rebuild), so the next cycle goes in while the closing step runs.
+      // With K = 0 the closing step's own kick and drift come after A: its
+      // outcome is read from B before the next cycle is planned.
+      ck(cudaEventSynchronize(c->ev_cyc[2 * slot]), "cudaEventSynchronize");
+      const Ctrl a = c->h_ctrl_cyc[2 * slot];
+      if (a.status & kOverflowBits) break;  // (rolled back by the caller)
+      if (a.step < done || a.step - done > K) throw CudaFail{"speculative block: step count"};
       int K_next = -1;
-      if (done < target) {
-        K_next = static_cast<int>(spec_block(c, done, target - done, seen));
-        launch_cycle(K_next, slot ^ 1);
+      const bool known = K > 0;
+      if (known) {
+        const double m = __builtin_bit_cast(double, a.max_d2);
+        note_step(a.step + 1, a.halt != 0 || a.force_rebuild != 0 || m > c->g.rebuild_thr, m);
+        if (done < target) {
+          K_next = static_cast<int>(spec_block(c, done, target - done, seen));
+          launch_cycle(K_next, slot ^ 1);
+        }
       }
       ck(cudaEventSynchronize(c->ev_cyc[2 * slot + 1]), "cudaEventSynchronize");
       const Ctrl b = c->h_ctrl_cyc[2 * slot + 1];
       *c->h_ctrl = b;
-      if (b.status & kOverflowBits) {
-        overflow = true;
-        break;
+      if (b.status & kOverflowBits) break;
+      if (!known) {
+        note_step(b.step, b.rebuilds != rebuilds, b.seen_d2);
+        if (done < target) {
+          K_next = static_cast<int>(spec_block(c, done, target - done, seen));
+          launch_cycle(K_next, slot ^ 1);
+        }
       }
       if (b.step != done) throw CudaFail{"speculative block: closing step count"};
       if (b.rebuilds != rebuilds) {  // (only the closing step rebuilds)
@@ -3389,9 +3401,9 @@ int tmd_gpu_prepare_graphs(tmd_gpu_ctx* c, int64_t obs_stride) {
         }
         try {
           for (int par = 0; par < 2; ++par) {
-            for (int K = 1; K <= 12; ++K) spec_graph(c, K, false, par);
-            spec_graph(c, 0, false, par);
-            spec_graph(c, 0, true, par);
+            for (int slot = 0; slot < 2; ++slot) {
+              for (int K = 0; K <= 12; ++K) spec_graph(c, K, slot, par);
+            }
           }
         } catch (...) {
           c->obs_stride = keep;

@@ -1296,7 +1296,10 @@ void capture_spec(tmd_gpu_ctx* c, int K, int slot, tmd_gpu_ctx::StepGraph& out) 
     }
     ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot], c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost,
                        c->stream), "D2H ctrl");
-    ck(cudaEventRecord(c->ev_cyc[2 * slot], c->stream), "cudaEventRecord");
+    // (external: an event record node the host can wait on, not a capture
+    // dependency marker)
+    ck(cudaEventRecordWithFlags(c->ev_cyc[2 * slot], c->stream, cudaEventRecordExternal),
+       "cudaEventRecord");
     {  // closing step: the rebuild kernels behind one IF node per cycle
       c->launches += 1;
       k_clear_halt<<<1, 1, 0, c->ls>>>(c->ctrl);
@@ -1344,7 +1347,8 @@ void capture_spec(tmd_gpu_ctx* c, int K, int slot, tmd_gpu_ctx::StepGraph& out) 
     }
     ck(cudaMemcpyAsync(&c->h_ctrl_cyc[2 * slot + 1], c->ctrl, sizeof(Ctrl),
                        cudaMemcpyDeviceToHost, c->stream), "D2H ctrl");
-    ck(cudaEventRecord(c->ev_cyc[2 * slot + 1], c->stream), "cudaEventRecord");
+    ck(cudaEventRecordWithFlags(c->ev_cyc[2 * slot + 1], c->stream, cudaEventRecordExternal),
+       "cudaEventRecord");
     ck(cudaStreamEndCapture(c->stream, &g), "end capture");
     cudaGraphExec_t exec = nullptr;
     ck(cudaGraphInstantiate(&exec, g, 0), "cudaGraphInstantiate");

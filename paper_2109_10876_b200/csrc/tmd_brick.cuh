@@ -1,23 +1,21 @@
-// Brick-staged kernels (variant 2, the default): one CTA per brick of up to
-// 2x2x2 cells. Particles are stored brick-major (brick, then cell x-fastest
-// inside the brick, then id), so a brick's own particles are one contiguous
-// range and its 27-cell neighbourhood is the (Bx+2)(By+2)(Bz+2) halo block.
+// Brick-staged kernels: particles are stored brick-major (bricks of 2x2x2 or
+// 2x2x4 cells, x-fastest; cells x-fastest inside a brick; particles by id
+// inside a cell), so a brick's own particles are one contiguous range and its
+// 27-cell neighbourhood is the (Bx+2)(By+2)(Bz+2) halo block. The list builds
+// stage that halo block in shared memory once per brick (load_halo defines the
+// staging layout: halo cells x-fastest, each padded to a multiple of 4 slots).
 //
-// The CTA stages the halo block into shared memory once and every list entry
-// is a halo-local index into that staging layout, so the gathers of the hot
-// loop are LDS (bank-conflict bound) instead of L1 line fetches. Each halo
-// cell's staged block is padded to a multiple of 4 slots with far-away
-// coordinates so the build can read candidates with aligned 16-B loads.
-//
-// List layout (sector-chunked ELL): particles of a brick form groups of 32
-// (lane = brick offset % 32). Entry k of lane l of group g lives at
+// List layout (sector-chunked ELL): groups of 32 consecutive particles. Entry
+// k of lane l of group g lives at
 //   list[g*cap*32 + (k/8)*256 + l*8 + k%8]
 // so each lane owns whole 32-byte sectors: the build flushes 8 entries with
 // two 16-B stores, the force kernel reads 8 entries with two 16-B loads, and
 // a warp touches 1 KB of contiguous memory per chunk. A lane's last chunk is
-// padded with the sentinel slot (index = staging capacity, coordinates far
-// away), like the reference's sentinel-padded runs (neighbor_list.hpp:14-18,
-// soa_store.hpp:47-79), so the force loop has no tail branch.
+// padded with the sentinel (coordinates far away), like the reference's
+// sentinel-padded runs (neighbor_list.hpp:14-18, soa_store.hpp:47-79), so the
+// force loop has no tail branch. Entries are global slots (variant 3, sentinel
+// slot N) or the brick's staging indices (variant 2, sentinel = staging slot
+// stage_cap), the latter gathered from shared memory by k_forces_staged.
 #pragma once
 
 #include "tmd_device.cuh"
@@ -149,32 +147,18 @@ __device__ __forceinline__ double code_shift(uint32_t code, int axis, double L) 
   return image_shift((code >> (25 + 2 * axis)) & 3u, L);
 }
 
-// ---------------------------------------------------------------------------
-// Groups per brick (for the list layout): n_groups[b] = ceil(n_b / 32).
-__global__ void __launch_bounds__(128)
-    k_brick_groups(int nbricks, const int* __restrict__ brick_rank_off,
-                   const int* __restrict__ start, int* __restrict__ ngroups, Ctrl* ctrl) {
-  if (!ctrl->rebuild) return;
-  const int b = blockIdx.x * 128 + threadIdx.x;
-  if (b >= nbricks) return;
-  const int n = start[brick_rank_off[b + 1]] - start[brick_rank_off[b]];
-  ngroups[b] = (n + 31) >> 5;
-}
-
 __device__ __forceinline__ size_t list_slot(int group, int cap, int lane, int k) {
   return static_cast<size_t>(group) * cap * 32 + static_cast<size_t>(k >> 3) * 256 +
          lane * 8 + (k & 7);
 }
 
 // ---------------------------------------------------------------------------
-// Full-list build, brick-staged (the full-list form of build_sorted_list,
-// neighbor_list.hpp:51-111). One warp per owned cell of the brick, lanes =
-// that cell's particles. Candidates are the 9 stencil rows of 3 x-adjacent
-// halo cells (contiguous in the staging), scanned 32 at a time with packed
-// FP32 arithmetic (FADD2/FFMA2) on negated brick-relative coordinates into a
-// per-lane hit mask. Only hits are then processed: those inside the band
-// |r2 - rv2| <= delta take the exact FP64 test with the reference's rounding,
-// so membership is bit-identical to the reference.
+// Brick-staged list builds (the full-list form of build_sorted_list,
+// neighbor_list.hpp:51-111): a CTA per brick stages the brick's halo block in
+// shared memory as negated brick-relative FP32 coordinates; candidates are
+// tested with packed FP32 arithmetic (FADD2/FFMA2) and only those inside the
+// band |r2 - rv2| <= delta take the exact FP64 test with the reference's
+// rounding, so membership is bit-identical to the reference.
 constexpr int kBuildThreads = 256;
 #ifndef TMD_BUILD_MIN_BLOCKS
 #define TMD_BUILD_MIN_BLOCKS 4
@@ -182,398 +166,6 @@ constexpr int kBuildThreads = 256;
 constexpr int kBuildMinBlocks = TMD_BUILD_MIN_BLOCKS;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-
-// kGlobal = false: entries are brick-local staging indices, groups are per
-// brick (variant 2). kGlobal = true: entries are global slots, groups are 32
-// consecutive global particles (variant 3); the sentinel is slot N, whose
-// position is parked far away.
-template <bool kGlobal>
-__global__ void __launch_bounds__(kBuildThreads)
-    k_build_brick(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
-                  const int* __restrict__ brick_rank_off, const int* __restrict__ start,
-                  const int* __restrict__ group_off, Geom g, BrickGeom bg,
-                  uint32_t* __restrict__ list, int* __restrict__ nnbr,
-                  double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
-  if (!ctrl->rebuild) return;
-  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z, each stage_cap + 32
-  __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
-  __shared__ uint32_t s_code[kMaxHalo];
-  __shared__ __align__(16) uint32_t s_buf[kBuildThreads / 32][32][8];
-  __shared__ int s_maxc;
-  __shared__ unsigned long long s_ent;
-  const int b = blockIdx.x;
-  HaloTable ht;
-  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
-  load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
-            s_gcell);
-  if (ht.total > bg.stage_cap) {
-    // Overfull halo (never at the BASELINE densities): flag it; the host
-    // grows the staging and replays (same path as a list overflow).
-    if (threadIdx.x == 0) {
-      atomicOr(&ctrl->status, kStatStageOverflow);
-      atomicMax(&ctrl->max_halo, ht.total);
-    }
-    return;
-  }
-  const int sc = bg.stage_cap + 32;
-  float* nx = s_f;
-  float* ny = s_f + sc;
-  float* nz = s_f + 2 * sc;
-  const double ox = ht.lo[0] * bg.origin_scale[0];
-  const double oy = ht.lo[1] * bg.origin_scale[1];
-  const double oz = ht.lo[2] * bg.origin_scale[2];
-  for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
-    float x = kFarF, y = kFarF, z = kFarF;
-    if (k < ht.total) {
-      const int h = halo_of(k, s_off, ht.n);
-      const int q = k - s_off[h];
-      if (q < s_cnt[h]) {
-        const double4 p = pos[s_gstart[h] + q];
-        const uint32_t c = s_code[h];
-        x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
-        y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
-        z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
-      }
-    }
-    nx[k] = -x;
-    ny[k] = -y;
-    nz[k] = -z;
-  }
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
-  const int gbase = kGlobal ? 0 : group_off[b];
-  const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
-  int my_max = 0;
-  unsigned long long my_ent = 0;
-  for (int oc = warp; oc < ncell_own; oc += kBuildThreads / 32) {
-    const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
-    const int hc = (ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1));
-    const int ncl = s_cnt[hc];
-    for (int p0 = 0; p0 < ncl; p0 += 32) {
-      const int q = p0 + lane;
-      const bool active = q < ncl;
-      const int qi = active ? q : 0;
-      const int i = s_gstart[hc] + qi;
-      const int ki = s_off[hc] + qi;
-      const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
-      const float2 xi2 = f2(xf, xf), yi2 = f2(yf, yf), zi2 = f2(zf, zf);
-      const int ib = kGlobal ? i : i - ht.bs;
-      const int grp = gbase + (ib >> 5), gl = ib & 31;
-      int n = 0;
-      double4 pi = make_double4(0.0, 0.0, 0.0, 0.0);
-      bool have_pi = false;
-      for (int oz2 = -1; oz2 <= 1; ++oz2) {
-        for (int oy2 = -1; oy2 <= 1; ++oy2) {
-          const int h0 = hc - 1 + ht.H[0] * (oy2 + ht.H[1] * oz2);  // ox = -1 of the row
-          const int kb = s_off[h0], ke = s_off[h0 + 3];
-          const int k1 = s_off[h0 + 1], k2 = s_off[h0 + 2];
-          // Per-row constants of the 3 halo cells, kept in registers: the
-          // value added to a staged index to get the entry's index field, the
-          // entry tag (image code + rounding orientation), own-cell flag.
-          const int first_yz = oy2 != 0 ? oy2 : oz2;
-          uint32_t tag3[3];
-          int add3[3];
-          bool self_row = false;
-#pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const int hh = h0 + t;
-            const uint32_t code = s_code[hh];
-            const int first = (t - 1) != 0 ? (t - 1) : first_yz;
-            tag3[t] = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
-            add3[t] = kGlobal ? s_gstart[hh] - s_off[hh] : 0;
-            self_row |= s_gcell[hh] == s_gcell[hc];
-          }
-          for (int k0 = kb; k0 < ke; k0 += 32) {
-            uint32_t m = 0, msure = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int kq = k0 + 4 * u;
-              const float4 X = *reinterpret_cast<const float4*>(nx + kq);
-              const float4 Y = *reinterpret_cast<const float4*>(ny + kq);
-              const float4 Z = *reinterpret_cast<const float4*>(nz + kq);
-              const float2 dxa = __fadd2_rn(xi2, f2(X.x, X.y));
-              const float2 dxb = __fadd2_rn(xi2, f2(X.z, X.w));
-              const float2 dya = __fadd2_rn(yi2, f2(Y.x, Y.y));
-              const float2 dyb = __fadd2_rn(yi2, f2(Y.z, Y.w));
-              const float2 dza = __fadd2_rn(zi2, f2(Z.x, Z.y));
-              const float2 dzb = __fadd2_rn(zi2, f2(Z.z, Z.w));
-              const float2 ra = __ffma2_rn(dza, dza, __ffma2_rn(dya, dya, __fmul2_rn(dxa, dxa)));
-              const float2 rb = __ffma2_rn(dzb, dzb, __ffma2_rn(dyb, dyb, __fmul2_rn(dxb, dxb)));
-              m |= (ra.x <= bg.hi2 ? 1u : 0u) << (4 * u);
-              m |= (ra.y <= bg.hi2 ? 1u : 0u) << (4 * u + 1);
-              m |= (rb.x <= bg.hi2 ? 1u : 0u) << (4 * u + 2);
-              m |= (rb.y <= bg.hi2 ? 1u : 0u) << (4 * u + 3);
-              msure |= (ra.x < bg.lo2 ? 1u : 0u) << (4 * u);
-              msure |= (ra.y < bg.lo2 ? 1u : 0u) << (4 * u + 1);
-              msure |= (rb.x < bg.lo2 ? 1u : 0u) << (4 * u + 2);
-              msure |= (rb.y < bg.lo2 ? 1u : 0u) << (4 * u + 3);
-            }
-            // (padding slots hold far coordinates: r2 = inf, never a hit)
-            const int rem = ke - k0;
-            if (rem < 32) m &= (1u << rem) - 1u;
-            if (!active) m = 0;
-            while (m != 0u) {
-              const int c = __ffs(m) - 1;
-              const uint32_t bit = 1u << c;
-              m ^= bit;
-              const int k = k0 + c;
-              const int t = (k >= k1 ? 1 : 0) + (k >= k2 ? 1 : 0);
-              const uint32_t tag = t == 0 ? tag3[0] : (t == 1 ? tag3[1] : tag3[2]);
-              const int idx = k + (t == 0 ? add3[0] : (t == 1 ? add3[1] : add3[2]));
-              if (self_row) {  // self / own periodic image (neighbor_list.hpp:91-93)
-                const int hh = h0 + t;
-                const int j = s_gstart[hh] + (k - s_off[hh]);
-                if (j == i && s_gcell[hh] == s_gcell[hc]) continue;
-              }
-              bool in = (msure & bit) != 0u;
-              if (!in) {  // inside the rounding band: decide exactly in FP64
-                const int hh = h0 + t;
-                const int j = s_gstart[hh] + (k - s_off[hh]);
-                if (!have_pi) { pi = pos[i]; have_pi = true; }
-                const double4 pj = pos[j];
-                double ex, ey, ez;
-                pair_delta(pi, pj, static_cast<uint32_t>(j & kIdxMask) | tag, g, ex, ey, ez);
-                in = exact_r2(ex, ey, ez) <= g.rv2;
-              }
-              if (in) {
-                s_buf[warp][lane][n & 7] = static_cast<uint32_t>(idx) | tag;
-                ++n;
-                if ((n & 7) == 0 && n <= bg.cap) {
-                  const uint4* src = reinterpret_cast<const uint4*>(&s_buf[warp][lane][0]);
-                  uint4* dst = reinterpret_cast<uint4*>(list + list_slot(grp, bg.cap, gl, n - 8));
-                  dst[0] = src[0];
-                  dst[1] = src[1];
-                }
-              }
-            }
-          }
-        }
-      }
-      if (active) {
-        if ((n & 7) != 0 && n <= bg.cap) {  // sentinel-pad the last chunk
-          for (int r = n & 7; r < 8; ++r) s_buf[warp][lane][r] = sentinel;
-          const uint4* src = reinterpret_cast<const uint4*>(&s_buf[warp][lane][0]);
-          uint4* dst = reinterpret_cast<uint4*>(list + list_slot(grp, bg.cap, gl, n & ~7));
-          dst[0] = src[0];
-          dst[1] = src[1];
-        }
-        nnbr[i] = n < bg.cap ? n : bg.cap;
-        snap[i] = have_pi ? pi : pos[i];
-        if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
-        my_max = max(my_max, n);
-        my_ent += static_cast<unsigned long long>(n);
-      }
-      __syncwarp();
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
-    my_ent += __shfl_xor_sync(0xffffffffu, my_ent, o);
-  }
-  if (lane == 0) {
-    atomicMax(&s_maxc, my_max);
-    atomicAdd(&s_ent, my_ent);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicMax(&ctrl->max_count, s_maxc);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries), s_ent);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Full-list build, lanes = candidates (the production build). Same staging and
-// membership rule as k_build_brick, but the roles are swapped: a warp owns one
-// cell of the brick, takes the 9 stencil rows 32 candidates at a time (one
-// candidate per lane, its tag/index/self-id resolved once per batch), and
-// loops over the cell's particles i with warp-uniform i: the FP32 test is
-// fully SIMD, hits are compacted with a ballot and each hit lane stores its
-// entry straight into i's chunked list at n_i + rank (consecutive slots of
-// one 32-B sector). No per-lane serial hit loop.
-template <bool kGlobal>
-__global__ void __launch_bounds__(kBuildThreads)
-    k_build_brick2(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
-                   const int* __restrict__ brick_rank_off, const int* __restrict__ start,
-                   const int* __restrict__ group_off, Geom g, BrickGeom bg,
-                   uint32_t* __restrict__ list, int* __restrict__ nnbr,
-                   double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
-  if (!ctrl->rebuild) return;
-  extern __shared__ __align__(16) float s_f[];  // -x | -y | -z, each stage_cap + 32
-  __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
-  __shared__ uint32_t s_code[kMaxHalo];
-  __shared__ int s_maxc;
-  __shared__ unsigned long long s_ent;
-  const int b = blockIdx.x;
-  HaloTable ht;
-  if (threadIdx.x == 0) { s_maxc = 0; s_ent = 0ull; }
-  load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
-            s_gcell);
-  if (ht.total > bg.stage_cap) {
-    if (threadIdx.x == 0) {
-      atomicOr(&ctrl->status, kStatStageOverflow);
-      atomicMax(&ctrl->max_halo, ht.total);
-    }
-    return;
-  }
-  const int sc = bg.stage_cap + 32;
-  float* nx = s_f;
-  float* ny = s_f + sc;
-  float* nz = s_f + 2 * sc;
-  const double ox = ht.lo[0] * bg.origin_scale[0];
-  const double oy = ht.lo[1] * bg.origin_scale[1];
-  const double oz = ht.lo[2] * bg.origin_scale[2];
-  for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
-    float x = kFarF, y = kFarF, z = kFarF;
-    if (k < ht.total) {
-      const int h = halo_of(k, s_off, ht.n);
-      const int q = k - s_off[h];
-      if (q < s_cnt[h]) {
-        const double4 p = pos[s_gstart[h] + q];
-        const uint32_t c = s_code[h];
-        x = static_cast<float>((p.x + code_shift(c, 0, g.L[0])) - ox);
-        y = static_cast<float>((p.y + code_shift(c, 1, g.L[1])) - oy);
-        z = static_cast<float>((p.z + code_shift(c, 2, g.L[2])) - oz);
-      }
-    }
-    nx[k] = -x;
-    ny[k] = -y;
-    nz[k] = -z;
-  }
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
-  const int gbase = kGlobal ? 0 : group_off[b];
-  const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
-  int my_max = 0;
-  unsigned long long my_ent = 0;
-  // Work items = (owned cell, 8 consecutive particles of it), dealt round-robin
-  // to the warps: finer than one cell per warp, so the CTA tail is short.
-  __shared__ int s_item_off[9];
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int oc = 0; oc < ncell_own; ++oc) {
-      const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
-      s_item_off[oc] = run;
-      run += (s_cnt[(ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1))] + 7) >> 3;
-    }
-    s_item_off[ncell_own] = run;
-  }
-  __syncthreads();
-  const int nitems = s_item_off[ncell_own];
-  constexpr int kItem = 8;
-  for (int it = warp; it < nitems; it += kBuildThreads / 32) {
-    int oc = 0;
-    while (s_item_off[oc + 1] <= it) ++oc;
-    const int ax = oc % ht.e[0], ay = (oc / ht.e[0]) % ht.e[1], az = oc / (ht.e[0] * ht.e[1]);
-    const int hc = (ax + 1) + ht.H[0] * ((ay + 1) + ht.H[1] * (az + 1));
-    const int ncl = s_cnt[hc];
-    {
-      const int p0 = (it - s_item_off[oc]) * kItem;
-      const int nq = min(kItem, ncl - p0);
-      // lanes 0..nq-1 hold particle i_q: global slot, list row base, counter
-      const int kq0 = s_off[hc] + p0;  // staged index of i_0 (multiple of 4)
-      const int my_i = s_gstart[hc] + p0 + (lane < nq ? lane : 0);
-      const int my_ib = kGlobal ? my_i : my_i - ht.bs;
-      const unsigned long long my_row = list_slot(gbase + (my_ib >> 5), bg.cap, my_ib & 31, 0);
-      int my_n = 0;
-      for (int oz2 = -1; oz2 <= 1; ++oz2) {
-        for (int oy2 = -1; oy2 <= 1; ++oy2) {
-          const int h0 = hc - 1 + ht.H[0] * (oy2 + ht.H[1] * oz2);  // ox = -1 of the row
-          const int kb = s_off[h0], ke = s_off[h0 + 3];
-          const int k1 = s_off[h0 + 1], k2 = s_off[h0 + 2];
-          const int first_yz = oy2 != 0 ? oy2 : oz2;
-          for (int k0 = kb; k0 < ke; k0 += 32) {
-            // this lane's candidate: staged slot k, its halo cell, entry, slot j
-            const int k = k0 + lane;
-            const int t = (k >= k1 ? 1 : 0) + (k >= k2 ? 1 : 0);
-            const int hh = h0 + t;
-            const uint32_t code = s_code[hh];
-            const int first = (t - 1) != 0 ? (t - 1) : first_yz;
-            const uint32_t tag = code | ((code != 0u && first < 0) ? kFlagIUpper : 0u);
-            const int j = s_gstart[hh] + (k - s_off[hh]);
-            const bool valid = k < ke && (k - s_off[hh]) < s_cnt[hh];
-            const uint32_t ent = static_cast<uint32_t>(kGlobal ? j : k) | tag;
-            const float2 cx2 = f2(nx[k], nx[k]), cy2 = f2(ny[k], ny[k]), cz2 = f2(nz[k], nz[k]);
-            const int i0 = s_gstart[hc] + p0;
-            for (int q = 0; q < nq; q += 2) {
-              // two particles per iteration: packed FP32 on (i_q, i_q+1)
-              const float2 xi = *reinterpret_cast<const float2*>(nx + kq0 + q);
-              const float2 yi = *reinterpret_cast<const float2*>(ny + kq0 + q);
-              const float2 zi = *reinterpret_cast<const float2*>(nz + kq0 + q);
-              const float2 dx = __fadd2_rn(xi, f2(-cx2.x, -cx2.y));
-              const float2 dy = __fadd2_rn(yi, f2(-cy2.x, -cy2.y));
-              const float2 dz = __fadd2_rn(zi, f2(-cz2.x, -cz2.y));
-              const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-              bool hit0 = valid && r2.x <= bg.hi2 && j != i0 + q;
-              bool hit1 = valid && r2.y <= bg.hi2 && j != i0 + q + 1 && q + 1 < nq;
-              if (__ballot_sync(0xffffffffu, hit0 || hit1) == 0u) continue;
-              if ((hit0 && !(r2.x < bg.lo2)) || (hit1 && !(r2.y < bg.lo2))) {
-                // rounding band: exact FP64 decision with the reference's rounding
-                const double4 pj = pos[j];
-                const uint32_t ej = static_cast<uint32_t>(j & kIdxMask) | tag;
-                double ex, ey, ez;
-                if (hit0 && !(r2.x < bg.lo2)) {
-                  pair_delta(pos[i0 + q], pj, ej, g, ex, ey, ez);
-                  hit0 = exact_r2(ex, ey, ez) <= g.rv2;
-                }
-                if (hit1 && !(r2.y < bg.lo2)) {
-                  pair_delta(pos[i0 + q + 1], pj, ej, g, ex, ey, ez);
-                  hit1 = exact_r2(ex, ey, ez) <= g.rv2;
-                }
-              }
-              const uint32_t bal0 = __ballot_sync(0xffffffffu, hit0);
-              const uint32_t bal1 = __ballot_sync(0xffffffffu, hit1);
-              const int n0 = __shfl_sync(0xffffffffu, my_n, q);
-              const int n1 = __shfl_sync(0xffffffffu, my_n, q + 1);
-              const unsigned long long row0 = __shfl_sync(0xffffffffu, my_row, q);
-              const unsigned long long row1 = __shfl_sync(0xffffffffu, my_row, q + 1);
-              if (hit0) {
-                const int pk = n0 + __popc(bal0 & lt_mask);
-                if (pk < bg.cap) list[row0 + (pk >> 3) * 256 + (pk & 7)] = ent;
-              }
-              if (hit1) {
-                const int pk = n1 + __popc(bal1 & lt_mask);
-                if (pk < bg.cap) list[row1 + (pk >> 3) * 256 + (pk & 7)] = ent;
-              }
-              if (lane == q) my_n += __popc(bal0);
-              if (lane == q + 1) my_n += __popc(bal1);
-            }
-          }
-        }
-      }
-      if (lane < nq) {
-        const int n = my_n;
-        if (n <= bg.cap) {
-          for (int r = n; r < ((n + 7) & ~7); ++r) {  // sentinel-pad the last chunk
-            list[my_row + (r >> 3) * 256 + (r & 7)] = sentinel;
-          }
-        }
-        nnbr[my_i] = n < bg.cap ? n : bg.cap;
-        snap[my_i] = pos[my_i];
-        if (n > bg.cap) atomicOr(&ctrl->status, kStatOverflow);
-        my_max = max(my_max, n);
-        my_ent += static_cast<unsigned long long>(n);
-      }
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, o));
-    my_ent += __shfl_xor_sync(0xffffffffu, my_ent, o);
-  }
-  if (lane == 0) {
-    atomicMax(&s_maxc, my_max);
-    atomicAdd(&s_ent, my_ent);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicMax(&ctrl->max_count, s_maxc);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl->entries), s_ent);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Full-list build, lanes = particles, branch-free appends (k_build_brick3).
@@ -610,8 +202,7 @@ template <bool kGlobal>
 __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
     k_build_brick3(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
                    const int* __restrict__ brick_rank_off, const int* __restrict__ start,
-                   const int* __restrict__ group_off, Geom g, BrickGeom bg,
-                   uint32_t* __restrict__ list, int* __restrict__ nnbr,
+                   Geom g, BrickGeom bg, uint32_t* __restrict__ list, int* __restrict__ nnbr,
                    double4* __restrict__ snap, uint32_t global_sentinel, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
   extern __shared__ __align__(16) float s_f[];  // -x | -y | -z | base, each stage_cap + 32
@@ -665,7 +256,6 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
-  const int gbase = kGlobal ? 0 : group_off[b];
   const uint32_t sentinel = kGlobal ? global_sentinel : static_cast<uint32_t>(bg.stage_cap);
   int my_max = 0;
   unsigned long long my_ent = 0;
@@ -681,8 +271,7 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
       const int ki = s_off[hc] + qi;
       const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
       const float2 xi2 = f2(xf, xf), yi2 = f2(yf, yf), zi2 = f2(zf, zf);
-      const int ib = kGlobal ? i : i - ht.bs;
-      const unsigned long long row = list_slot(gbase + (ib >> 5), bg.cap, ib & 31, 0);
+      const unsigned long long row = list_slot(i >> 5, bg.cap, i & 31, 0);
       const float hi2 = active ? bg.hi2 : -1.0f;  // inactive lanes never hit
       const uint32_t lo2m1 = __float_as_uint(bg.lo2) - 1u;
       const uint32_t rbase =
@@ -814,7 +403,8 @@ struct CullLane {
   uint32_t wb;     // bit pattern of the band width bound (r2 - lo2 <= width)
   uint32_t a;      // shared address of the next ring slot
   uint32_t rbase;  // shared address of ring slot 0
-  int i;
+  int i;           // global slot
+  uint32_t self;   // the lane's own entry index (global slot, or its staging index)
   int nflush;      // chunks flushed (or counted past the capacity)
   uint32_t* dst;   // list address of chunk nflush
 };
@@ -839,12 +429,28 @@ __device__ __forceinline__ void cull_flush(CullLane& L, int cap8, uint32_t* ring
   }
 }
 
-__device__ __forceinline__ bool cull_exact(const double4& pi, int i, uint32_t e,
+// The exact FP64 membership test of a band candidate (global slot j).
+__device__ __forceinline__ bool cull_exact(const double4& pi, int i, int j, uint32_t e,
                                            const double4* __restrict__ pos, const Geom& g) {
-  const int j = static_cast<int>(e & kIdxMask);
   double ex, ey, ez;
   pair_delta(pi, pos[j], e, g, ex, ey, ez);
   return j != i && exact_r2(ex, ey, ez) <= g.rv2;
+}
+
+// Global slot of a candidate entry: the entry itself, or (kLocal: brick-local
+// staging index) the halo cell's first global slot + the offset in the cell.
+struct StageMap {
+  const int* off;     // s_off: staging offset per halo cell (n + 1)
+  const int* gstart;  // s_gstart: first global slot per halo cell
+  int n;
+};
+
+template <bool kLocal>
+__device__ __forceinline__ int entry_slot(uint32_t e, const StageMap& sm) {
+  const int k = static_cast<int>(e & kIdxMask);
+  if (!kLocal) return k;
+  const int h = halo_of(k, sm.off, sm.n);
+  return sm.gstart[h] + (k - sm.off[h]);
 }
 
 // Four ring appends: unconditional stores, advances predicated on the FP32
@@ -894,21 +500,25 @@ __device__ __forceinline__ void cull_append1(uint32_t& a, uint32_t e, bool hit) 
 }
 
 // One candidate of a chunk that holds a rounding-band candidate.
+template <bool kLocal>
 __device__ __forceinline__ void cull_band1(uint32_t& a, uint32_t e, float r2, float d,
                                            const CullLane& L, const double4& pi,
-                                           const double4* __restrict__ pos, const Geom& g) {
-  const uint32_t me = static_cast<uint32_t>(L.i);
-  const bool hit = __float_as_uint(d) <= L.wb ? cull_exact(pi, L.i, e, pos, g)
-                                              : (r2 <= L.hi2 && e != me);
+                                           const double4* __restrict__ pos, const Geom& g,
+                                           const StageMap& sm) {
+  const bool hit = __float_as_uint(d) <= L.wb
+                       ? (e & kIdxMask) != L.self &&
+                             cull_exact(pi, L.i, entry_slot<kLocal>(e, sm), e, pos, g)
+                       : (r2 <= L.hi2 && e != L.self);
   cull_append1(a, e, hit);
 }
 
 // Tests a stream segment (a multiple of 4 candidates), 4 per iteration.
-template <bool kSelf>
+template <bool kSelf, bool kLocal>
 __device__ __forceinline__ void cull_segment(const float* __restrict__ strm, int fill,
                                              CullLane& L, const double4* __restrict__ pos,
-                                             const Geom& g, int cap8, uint32_t* ring_lane) {
-  const uint32_t me = static_cast<uint32_t>(L.i);
+                                             const Geom& g, int cap8, uint32_t* ring_lane,
+                                             const StageMap& sm) {
+  const uint32_t me = L.self;
   const uint32_t trig = L.rbase + 16u * 128u;
 #pragma unroll 1
   for (int c = 0; c < fill; c += 4) {
@@ -930,10 +540,10 @@ __device__ __forceinline__ void cull_segment(const float* __restrict__ strm, int
       cull_append4_fp32<kSelf>(a, E, ra, rb, L.hi2, me);
     } else {  // rounding band: the exact FP64 decision there
       const double4 pi = pos[L.i];
-      cull_band1(a, E.x, ra.x, da.x, L, pi, pos, g);
-      cull_band1(a, E.y, ra.y, da.y, L, pi, pos, g);
-      cull_band1(a, E.z, rb.x, db.x, L, pi, pos, g);
-      cull_band1(a, E.w, rb.y, db.y, L, pi, pos, g);
+      cull_band1<kLocal>(a, E.x, ra.x, da.x, L, pi, pos, g, sm);
+      cull_band1<kLocal>(a, E.y, ra.y, da.y, L, pi, pos, g, sm);
+      cull_band1<kLocal>(a, E.z, rb.x, db.x, L, pi, pos, g, sm);
+      cull_band1<kLocal>(a, E.w, rb.y, db.y, L, pi, pos, g, sm);
     }
     L.a = a;
     if (__any_sync(0xffffffffu, a >= trig)) cull_flush(L, cap8, ring_lane);
@@ -942,6 +552,12 @@ __device__ __forceinline__ void cull_segment(const float* __restrict__ strm, int
 
 // 3 CTAs per SM (76 registers): at 4 the register cap forces spills and
 // rematerialisation into the candidate loop (measured 5 % slower).
+// kLocal = false: entries are global slots (variant 3; the sentinel is slot
+// N, parked far away). kLocal = true: entries are the brick's staging indices
+// (the layout load_halo defines; the sentinel is staging slot stage_cap),
+// which the staged force kernel (k_forces_staged, variant 2) gathers from
+// shared memory. Groups are 32 consecutive global particles either way.
+template <bool kLocal>
 __global__ void __launch_bounds__(kBuildThreads, 3)
     k_build_cull(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
                  const int* __restrict__ brick_rank_off, const int* __restrict__ start, Geom g,
@@ -1003,6 +619,7 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
   __syncthreads();
 
   const uint32_t lt_mask = (1u << lane) - 1u;
+  const StageMap sm{s_off, s_gstart, ht.n};
   const int ncell_own = ht.e[0] * ht.e[1] * ht.e[2];
   const int cap8 = bg.cap >> 3;
   float* strm = s_strm[warp];
@@ -1036,9 +653,11 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
       const uint32_t u0 = tag_of(ca);
       const uint32_t u1 = ca + 1 < cb ? tag_of(ca + 1) : u0;
       const uint32_t u2 = ca + 2 < cb ? tag_of(ca + 2) : u1;
-      const int b0 = s_gstart[h0 + ca] - s_off[h0 + ca];
-      const int b1 = ca + 1 < cb ? s_gstart[h0 + ca + 1] - s_off[h0 + ca + 1] : b0;
-      const int b2 = ca + 2 < cb ? s_gstart[h0 + ca + 2] - s_off[h0 + ca + 2] : b1;
+      // staging index -> entry index: + (first global slot - staging offset)
+      // of the cell for global entries, + 0 for staging-index entries
+      const int b0 = kLocal ? 0 : s_gstart[h0 + ca] - s_off[h0 + ca];
+      const int b1 = kLocal ? 0 : (ca + 1 < cb ? s_gstart[h0 + ca + 1] - s_off[h0 + ca + 1] : b0);
+      const int b2 = kLocal ? 0 : (ca + 2 < cb ? s_gstart[h0 + ca + 2] - s_off[h0 + ca + 2] : b1);
       s_rng[warp][rr][0] = make_int4(s_off[h0 + ca], e1, e2, e3);
       s_rng[warp][rr][1] = make_int4(static_cast<int>(u0), static_cast<int>(u1),
                                      static_cast<int>(u2), 0);
@@ -1052,6 +671,7 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
       CullLane L;
       L.i = s_gstart[hc] + qi;
       const int ki = s_off[hc] + qi;
+      L.self = static_cast<uint32_t>(kLocal ? ki : L.i);
       const float xf = -nx[ki], yf = -ny[ki], zf = -nz[ki];
       L.xi2 = f2(xf, xf);
       L.yi2 = f2(yf, yf);
@@ -1148,9 +768,9 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
           }
           __syncwarp();
           if (cur_seg == 1) {
-            cull_segment<true>(strm, fill, L, pos, g, cap8, ring_lane);
+            cull_segment<true, kLocal>(strm, fill, L, pos, g, cap8, ring_lane, sm);
           } else {
-            cull_segment<false>(strm, fill, L, pos, g, cap8, ring_lane);
+            cull_segment<false, kLocal>(strm, fill, L, pos, g, cap8, ring_lane, sm);
           }
           __syncwarp();
           fill = 0;
@@ -1319,15 +939,10 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // ---------------------------------------------------------------------------
-// LJ forces over the brick-staged list (compute_pair_forces,
-// neighbor_list.hpp:150-187, full-list form). The halo block is staged as
-// unshifted SoA doubles; image shifts and the reference's rounding
-// orientation come from the entry tag (pair_delta), so the cutoff test sees
-// the reference's r2 bit for bit. Chunks of 8 entries are processed without
-// a tail branch (sentinel padding), letting the compiler overlap the 8
-// independent gathers.
-constexpr int kForceThreads = 192;
-
+// LJ pair term of one list entry (compute_pair_forces, neighbor_list.hpp:
+// 150-187, full-list form): image shift and the reference's rounding
+// orientation from the entry tag (pair_delta), so the cutoff test sees the
+// reference's r2 bit for bit.
 __device__ __forceinline__ void lj_accumulate(const double4& pi, double xj, double yj,
                                               double zj, uint32_t ent, const Geom& g,
                                               const LjConst& lj, double& ax, double& ay,
@@ -1349,75 +964,144 @@ __device__ __forceinline__ void lj_accumulate(const double4& pi, double xj, doub
   }
 }
 
-template <int kMode>
-__global__ void __launch_bounds__(kForceThreads)
-    k_forces_brick(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
-                   const int* __restrict__ brick_rank_off, const int* __restrict__ start,
-                   const int* __restrict__ group_off, Geom g, BrickGeom bg, LjConst lj,
-                   const uint32_t* __restrict__ list, const int* __restrict__ nnbr,
-                   double* __restrict__ fx, double* __restrict__ fy, double* __restrict__ fz,
-                   double* __restrict__ part_e, double* __restrict__ part_w,
-                   const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
-  extern __shared__ double s_d[];
+// ---------------------------------------------------------------------------
+// Variant 2: LJ forces with the neighbour positions gathered from SHARED
+// memory. One CTA per brick stages the brick's halo block — the staging
+// layout of load_halo, which the list build used, so list entries are staging
+// indices (k_build_cull<true>, k_build_brick3<false>) — as x|y pairs (double2)
+// and z (double) with 16-B and 8-B cp.async copies straight from the position
+// buffer. Each gather is then one LDS.128 + one LDS.64 instead of a 32-B L1
+// line request per entry (the bound of k_forces_l1, one L1 wavefront per
+// entry): ncu measures ~0.6 shared wavefronts per gather (half
+// of them bank conflicts of the random indices). Threads = the brick's
+// particles (a brick fuller than the CTA loops). Same pair arithmetic and
+// per-particle entry order as k_forces_l1: forces bitwise equal.
+//
+// Measured on B200 at 1M (scripts/force_variants.py): 0.287 ms
+// against 0.273 ms for k_forces_l1 — the L1 relief is real (L1TEX 66 %), but
+// the CTA-per-brick structure pays a staging phase and a tail per brick
+// (barrier stalls 27 %: on the FCC lattice a fifth of the 2x2x4 bricks hold
+// more than 320 particles), and a persistent warp-specialised version (cp.async
+// producer warps, mbarrier-handed stage buffers) measured 0.345 ms: too few
+// groups per staged brick to keep its consumers fed. So it is not the default.
+#ifndef TMD_STAGED_MINB_SMALL
+#define TMD_STAGED_MINB_SMALL 5
+#endif
+#ifndef TMD_STAGED_MINB_LARGE
+#define TMD_STAGED_MINB_LARGE 3
+#endif
+template <int kThreads>
+constexpr int staged_min_blocks() {
+  return kThreads <= 192 ? TMD_STAGED_MINB_SMALL : TMD_STAGED_MINB_LARGE;
+}
+#ifndef TMD_STAGED_UNROLL
+#define TMD_STAGED_UNROLL 1
+#endif
+constexpr int kStagedUnroll = TMD_STAGED_UNROLL;  // gathers in flight per thread
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <int kThreads, int kMode>
+__global__ void __launch_bounds__(kThreads, staged_min_blocks<kThreads>())
+    k_forces_staged(const double4* __restrict__ pos, const int* __restrict__ cell_rank,
+                    const int* __restrict__ brick_rank_off, const int* __restrict__ start,
+                    Geom g, BrickGeom bg, LjConst lj, const uint32_t* __restrict__ list,
+                    const int* __restrict__ nnbr, double* __restrict__ fx,
+                    double* __restrict__ fy, double* __restrict__ fz,
+                    double* __restrict__ part_e, double* __restrict__ part_w,
+                    const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
+  const int b = blockIdx.x;
+  if (ctrl->halt) {  // speculative blocks: positions carried to the other buffer
+    if (kMode == kFused && it.halt_copy) {
+      const int bs = start[brick_rank_off[b]], be = start[brick_rank_off[b + 1]];
+      for (int i = bs + threadIdx.x; i < be; i += kThreads) it.pos_out[i] = pos[i];
+    }
+    return;
+  }
+  extern __shared__ __align__(16) double2 s_xy[];  // [stage_cap + 1], then z [stage_cap + 1]
   __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
   __shared__ uint32_t s_code[kMaxHalo];
-  __shared__ double red[kForceThreads / 32];
-  const int b = blockIdx.x;
+  __shared__ double red[kThreads / 32];
+  double* s_z = reinterpret_cast<double*>(s_xy + bg.stage_cap + 1);
   HaloTable ht;
   load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
             s_gcell);
-  const int sc = bg.stage_cap + 4;
-  double* sx = s_d;
-  double* sy = s_d + sc;
-  double* sz = s_d + 2 * sc;
-  double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
-  if (ht.total <= bg.stage_cap) {  // (the build flags an overfull halo)
-    for (int k = threadIdx.x; k < sc; k += kForceThreads) {
-      double x = kFarD, y = kFarD, z = kFarD;
-      if (k < ht.total) {
-        const int h = halo_of(k, s_off, ht.n);
+  const bool fits = ht.total <= bg.stage_cap;  // (the build flags an overfull halo)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (fits) {
+    // a warp per x-row of the halo (H0 cells, contiguous in the staging),
+    // lanes over the row's slots; padding slots are never listed
+    const int H0 = ht.H[0];
+    const int rows = ht.H[1] * ht.H[2];
+    for (int r = warp; r < rows; r += kThreads / 32) {
+      const int h0 = r * H0;
+      const int k0 = s_off[h0], k1 = s_off[h0 + H0];
+      for (int k = k0 + lane; k < k1; k += 32) {
+        int h = h0;
+#pragma unroll
+        for (int t = 1; t < 4; ++t) h += (t < H0 && k >= s_off[h0 + t]) ? 1 : 0;
         const int q = k - s_off[h];
         if (q < s_cnt[h]) {
-          const double4 p = pos[s_gstart[h] + q];
-          x = p.x;
-          y = p.y;
-          z = p.z;
+          const double4* src = pos + s_gstart[h] + q;
+          cp_async16(s_xy + k, src);
+          cp_async8(s_z + k, reinterpret_cast<const double*>(src) + 2);
         }
       }
-      sx[k] = x;
-      sy[k] = y;
-      sz[k] = z;
     }
+    if (threadIdx.x == 0) {  // the sentinel slot
+      s_xy[bg.stage_cap] = make_double2(kFarD, kFarD);
+      s_z[bg.stage_cap] = kFarD;
+    }
+    cp_async_wait_all();
   }
   __syncthreads();
-  if (ht.total <= bg.stage_cap) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nb_i = ht.be - ht.bs;
-    const int ngr = (nb_i + 31) >> 5;
-    for (int gl = warp; gl < ngr; gl += kForceThreads / 32) {
-      const int ib = gl * 32 + lane;
-      const bool active = ib < nb_i;
-      const int i = ht.bs + (active ? ib : 0);
+  double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
+  if (fits) {
+    for (int i = ht.bs + threadIdx.x; i < ht.be; i += kThreads) {
       const double4 pi = pos[i];
-      const int cnt = active ? nnbr[i] : 0;
-      const uint32_t* row = list + list_slot(group_off[b] + gl, bg.cap, lane, 0);
+      const int cnt = nnbr[i];
+      const uint32_t* row = list + list_slot(i >> 5, bg.cap, i & 31, 0);
       double ax = 0.0, ay = 0.0, az = 0.0;
       bool zero = false;
+      // the next chunk's entries are loaded while this one is evaluated (the
+      // list streams from DRAM; shared-memory gathers leave little latency
+      // for the warp schedulers to hide it behind)
+      uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+      if (cnt > 0) {
+        n0 = __ldg(reinterpret_cast<const uint4*>(row));
+        n1 = __ldg(reinterpret_cast<const uint4*>(row + 4));
+      }
       for (int c0 = 0; c0 < cnt; c0 += 8) {
-        const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32));
-        const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32 + 4));
-        const uint32_t ents[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        double xj[8], yj[8], zj[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int k = static_cast<int>(ents[u] & kIdxMask);
-          xj[u] = sx[k];
-          yj[u] = sy[k];
-          zj[u] = sz[k];
+        const uint32_t ents[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+        if (c0 + 8 < cnt) {
+          n0 = __ldg(reinterpret_cast<const uint4*>(row + (c0 + 8) * 32));
+          n1 = __ldg(reinterpret_cast<const uint4*>(row + (c0 + 8) * 32 + 4));
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          lj_accumulate(pi, xj[u], yj[u], zj[u], ents[u], g, lj, ax, ay, az, e, w, zero);
+        for (int u0 = 0; u0 < 8; u0 += kStagedUnroll) {
+          double2 xy[kStagedUnroll];
+          double zj[kStagedUnroll];
+#pragma unroll
+          for (int u = 0; u < kStagedUnroll; ++u) {
+            const int k = static_cast<int>(ents[u0 + u] & kIdxMask);
+            xy[u] = s_xy[k];
+            zj[u] = s_z[k];
+          }
+#pragma unroll
+          for (int u = 0; u < kStagedUnroll; ++u) {
+            lj_accumulate(pi, xy[u].x, xy[u].y, zj[u], ents[u0 + u], g, lj, ax, ay, az, e, w,
+                          zero);
+          }
         }
       }
       if (zero) {  // r2 == 0: coincident particles (neighbor_list.hpp:166-170)
@@ -1425,7 +1109,8 @@ __global__ void __launch_bounds__(kForceThreads)
           const uint32_t ent = row[(k >> 3) * 256 + (k & 7)];
           const int kk = static_cast<int>(ent & kIdxMask);
           double dx, dy, dz;
-          pair_delta(pi, make_double4(sx[kk], sy[kk], sz[kk], 0.0), ent, g, dx, dy, dz);
+          pair_delta(pi, make_double4(s_xy[kk].x, s_xy[kk].y, s_z[kk], 0.0), ent, g, dx, dy,
+                     dz);
           if (exact_r2(dx, dy, dz) == 0.0) {
             const int h = halo_of(kk, s_off, ht.n);
             record_error(ctrl, kStatOverlap, id[i], id[s_gstart[h] + (kk - s_off[h])]);
@@ -1433,24 +1118,34 @@ __global__ void __launch_bounds__(kForceThreads)
           }
         }
       }
-      if (active) {
-        integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
-        if (kMode != kFused) {  // a fused step's force only feeds its own kicks
-          fx[i] = ax;
-          fy[i] = ay;
-          fz[i] = az;
-        }
+      integrate_one<kMode>(i, pi, ax, ay, az, it, ctrl, ke, d2);
+      if (kMode != kFused) {  // a fused step's force only feeds its own kicks
+        fx[i] = ax;
+        fy[i] = ay;
+        fz[i] = az;
       }
     }
   }
-  const double te = block_sum<kForceThreads>(e, red);
-  const double tw = block_sum<kForceThreads>(w, red);
+  const double te = block_sum<kThreads>(e, red);
+  const double tw = block_sum<kThreads>(w, red);
   if (threadIdx.x == 0) {
     part_e[b] = te;
     part_w[b] = tw;
   }
-  integrate_block<kMode, kForceThreads>(ke, d2, red, it, ctrl);
+  integrate_block<kMode, kThreads>(ke, d2, red, it, ctrl);
 }
+
+// Threads of a staged force CTA: one per particle of a brick (2x2x2 cells
+// hold ~150 particles at the BASELINE density, 2x2x4 ~300).
+constexpr int kStagedThreadsSmall = 192;
+constexpr int kStagedThreadsLarge = 320;
+
+// Dynamic shared memory of k_forces_staged: x|y (double2) and z (double) per
+// staging slot + the sentinel.
+inline size_t staged_smem_bytes(int stage_cap) {
+  return static_cast<size_t>(stage_cap + 1) * 3 * sizeof(double);
+}
+constexpr size_t kStagedSmemMax = 200 * 1024;
 
 // ---------------------------------------------------------------------------
 // Variant 3: thread per particle over the sector-chunked list with GLOBAL
@@ -1642,26 +1337,23 @@ __global__ void __launch_bounds__(128)
 }
 
 // ---------------------------------------------------------------------------
-// Parity/accounting tap: rewrite the brick-local list into the global-index
-// ELL-transposed form (entry k of particle i at out[k*stride + i], same tag
-// bits) consumed by the host-side pair dump and the in-cut counter.
+// Parity/accounting tap: rewrite the staging-index list of variant 2 into the
+// global-index ELL-transposed form (entry k of particle i at out[k*stride + i],
+// same tag bits) consumed by the host-side pair dump and the in-cut counter.
 __global__ void __launch_bounds__(128)
     k_decode_list(const int* __restrict__ cell_rank, const int* __restrict__ brick_rank_off,
-                  const int* __restrict__ start, const int* __restrict__ group_off, Geom g,
-                  BrickGeom bg, const uint32_t* __restrict__ list,
-                  const int* __restrict__ nnbr, uint32_t* __restrict__ out, int stride) {
+                  const int* __restrict__ start, Geom g, BrickGeom bg,
+                  const uint32_t* __restrict__ list, const int* __restrict__ nnbr,
+                  uint32_t* __restrict__ out, int stride) {
   __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
   __shared__ uint32_t s_code[kMaxHalo];
   const int b = blockIdx.x;
   HaloTable ht;
   load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
             s_gcell);
-  const int nb_i = ht.be - ht.bs;
-  for (int ib = threadIdx.x; ib < nb_i; ib += 128) {
-    const int i = ht.bs + ib;
-    const int grp = group_off[b] + (ib >> 5), gl = ib & 31;
+  for (int i = ht.bs + threadIdx.x; i < ht.be; i += 128) {
     for (int k = 0; k < nnbr[i]; ++k) {
-      const uint32_t ent = list[list_slot(grp, bg.cap, gl, k)];
+      const uint32_t ent = list[list_slot(i >> 5, bg.cap, i & 31, k)];
       const int loc = static_cast<int>(ent & kIdxMask);
       const int h = halo_of(loc, s_off, ht.n);
       const uint32_t j = static_cast<uint32_t>(s_gstart[h] + (loc - s_off[h]));

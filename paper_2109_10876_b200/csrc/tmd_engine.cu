@@ -5,11 +5,12 @@
 //   Integrate  k_kick_drift         opening half-kick + drift of the first step
 //   per step:
 //   Neigh      k_decide             global max-displacement test, on device
-//   Resort     k_wrap_bin, scan, k_scatter, k_sort_cells, k_permute, k_copy_back,
-//              k_brick_groups + scan          (no-ops unless the device decided rebuild)
+//   Resort     k_wrap_bin, scan, k_scatter, k_sort_cells, k_permute, k_copy_back
+//                                             (no-ops unless the device decided rebuild)
 //   Neigh      k_build_prologue, k_build_cull / k_build_thread (no-op unless rebuild)
-//   Forces     k_forces_l1<kFused>  forces + closing half-kick (+ Langevin) of this
-//              step + opening half-kick + drift of the next (kKick2 on the last)
+//   Forces     k_forces_staged / k_forces_l1 <kFused>  forces + closing half-kick
+//              (+ Langevin) of this step + opening half-kick + drift of the next
+//              (kKick2 on the last)
 // Nothing in a chunk waits for the host. The host synchronises once per
 // chunk to read the status word; a neighbour-list overflow rolls the chunk
 // back to its checkpoint, grows the list and replays it.
@@ -246,13 +247,6 @@ std::string fmt_g(double v) {
   return b;
 }
 
-// Host wrap1 (box.hpp:47-51); no FMA contraction on the x86-64 host path.
-double host_wrap1(double p, double L) {
-  double r = p - L * std::floor(p / L);
-  if (r >= L) r -= L;
-  return r;
-}
-
 }  // namespace
 
 struct tmd_gpu_ctx {
@@ -323,8 +317,6 @@ struct tmd_gpu_ctx {
   BrickGeom bg{};
   int* cell_rank = nullptr;       // global cell -> brick-major rank
   int* brick_rank_off = nullptr;  // brick -> first rank (nbricks + 1)
-  int* ngroups = nullptr;         // per brick, scanned into group_off
-  int* group_off = nullptr;       // nbricks + 1
   int ngroups_max = 0;
   int nparts = 0;                 // partial-sum slots of the force kernel
   uint32_t* decoded = nullptr;    // global-index ELL copy for the taps
@@ -499,8 +491,8 @@ void free_all(tmd_gpu_ctx* c) {
                   c->part_e, c->part_w, c->part_ke, c->scalars, c->ctrl,
                   c->ck_pos, c->ck_vx, c->ck_vy, c->ck_vz, c->ck_mass, c->ck_id,
                   c->ck_fx, c->ck_fy, c->ck_fz,
-                  c->rebuild_log, c->ticks, c->cell_rank, c->brick_rank_off, c->ngroups,
-                  c->group_off, c->decoded, c->scan_tmp, c->owner_of_z, c->mig_dest,
+                  c->rebuild_log, c->ticks, c->cell_rank, c->brick_rank_off,
+                  c->decoded, c->scan_tmp, c->owner_of_z, c->mig_dest,
                   c->mig_count, c->mig_off, c->mig_keep, c->mig_send, c->mig_recv,
                   c->bidx[0], c->bidx[1], c->bids[0], c->bids[1], c->bpos[0], c->bpos[1],
                   c->bcnt[0], c->bcnt[1], c->boff[0], c->boff[1], c->gcnt[0], c->gcnt[1],
@@ -662,22 +654,13 @@ void launch_resort(tmd_gpu_ctx* c) {
                                             c->vz2, c->mass2, c->id2, c->cell2,
                                             c->pos, c->vx, c->vy, c->vz,
                                             c->mass, c->id, c->cell, c->ctrl);
-  // list groups per brick (32 particles each), scanned into group offsets:
-  // only the brick-local list of variant 2 has per-brick groups
-  if (c->variant == 2) {
-    c->launches += 1;
-    k_brick_groups<<<blocks_for(c->bg.nbricks, 128), 128, 0, c->ls>>>(
-        c->bg.nbricks, c->brick_rank_off, c->start, c->ngroups, c->ctrl);
-    launch_scan(c, c->bg.nbricks, c->ngroups, c->group_off);
-  }
 }
 
 size_t build_smem(const tmd_gpu_ctx* c) {
   return static_cast<size_t>(c->bg.stage_cap + 32) * 4 * sizeof(float);
 }
-size_t force_smem(const tmd_gpu_ctx* c) {
-  return static_cast<size_t>(c->bg.stage_cap + 4) * 3 * sizeof(double);
-}
+size_t force_smem(const tmd_gpu_ctx* c) { return staged_smem_bytes(c->bg.stage_cap); }
+bool staged_large(const tmd_gpu_ctx* c) { return c->bg.B[0] * c->bg.B[1] * c->bg.B[2] > 8; }
 
 // Max dynamic shared memory is a per-kernel, per-device attribute shared by
 // every context of the process, while the staging capacity is per context:
@@ -697,18 +680,24 @@ void set_smem_attrs(tmd_gpu_ctx* c) {
                             static_cast<int>(b)), "smem attr build");
     ck(cudaFuncSetAttribute(k_build_brick3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(b)), "smem attr build");
-    ck(cudaFuncSetAttribute(k_build_cull, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(k_build_cull<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(b)), "smem attr build");
+    ck(cudaFuncSetAttribute(k_build_cull<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(b)), "smem attr build");
     g_build = b;
   }
-  if (f > g_force) {
-    ck(cudaFuncSetAttribute(k_forces_brick<kForcesOnly>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(f)),
-       "smem attr forces");
-    ck(cudaFuncSetAttribute(k_forces_brick<kKick2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(f)), "smem attr forces");
-    ck(cudaFuncSetAttribute(k_forces_brick<kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(f)), "smem attr forces");
+  if (f > g_force && f <= kStagedSmemMax) {  // (larger: the context runs variant 3)
+    const void* ks[] = {
+        reinterpret_cast<const void*>(k_forces_staged<kStagedThreadsSmall, kForcesOnly>),
+        reinterpret_cast<const void*>(k_forces_staged<kStagedThreadsSmall, kKick2>),
+        reinterpret_cast<const void*>(k_forces_staged<kStagedThreadsSmall, kFused>),
+        reinterpret_cast<const void*>(k_forces_staged<kStagedThreadsLarge, kForcesOnly>),
+        reinterpret_cast<const void*>(k_forces_staged<kStagedThreadsLarge, kKick2>),
+        reinterpret_cast<const void*>(k_forces_staged<kStagedThreadsLarge, kFused>)};
+    for (const void* k : ks) {
+      ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(f)), "smem attr forces");
+    }
     g_force = f;
   }
 }
@@ -746,18 +735,17 @@ void launch_build(tmd_gpu_ctx* c) {
     k_build_thread<<<c->nblk, kBlock, 0, c->ls>>>(
         static_cast<int>(c->n), c->pos, c->cell, c->start, c->cell_rank, c->g, c->nbr,
         c->nnbr, c->cap, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
-  } else if (c->variant == 3 && c->build_kind == 6) {
-    k_build_cull<<<c->bg.nbricks, kBuildThreads, build_smem(c) / 4 * 3, c->ls>>>(
+  } else if (c->build_kind == 6) {  // variant 2: staging-index entries
+    auto kern = c->variant == 2 ? k_build_cull<true> : k_build_cull<false>;
+    kern<<<c->bg.nbricks, kBuildThreads, build_smem(c) / 4 * 3, c->ls>>>(
+        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->g, c->bg, c->nbr, c->nnbr,
+        c->snap,
+        static_cast<uint32_t>(c->variant == 2 ? c->bg.stage_cap : c->n_cap), c->ctrl);
+  } else {
+    auto kern = c->variant == 2 ? k_build_brick3<false> : k_build_brick3<true>;
+    kern<<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
         c->pos, c->cell_rank, c->brick_rank_off, c->start, c->g, c->bg, c->nbr, c->nnbr,
         c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
-  } else if (c->variant == 3) {
-    k_build_brick3<true><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
-        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
-        c->nbr, c->nnbr, c->snap, static_cast<uint32_t>(c->n_cap), c->ctrl);
-  } else {
-    k_build_brick3<false><<<c->bg.nbricks, kBuildThreads, build_smem(c), c->ls>>>(
-        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
-        c->nbr, c->nnbr, c->snap, 0u, c->ctrl);
   }
 }
 
@@ -805,10 +793,12 @@ void launch_forces_mode(tmd_gpu_ctx* c) {
         static_cast<int>(c->n), c->pos, c->nbr, c->nnbr, c->cap, c->g, c->lj, c->fx, c->fy,
         c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   } else {
-    k_forces_brick<kMode><<<c->bg.nbricks, kForceThreads, force_smem(c), c->ls>>>(
-        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg,
-        c->lj, c->nbr, c->nnbr, c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it,
-        c->ctrl);
+    auto kern = staged_large(c) ? k_forces_staged<kStagedThreadsLarge, kMode>
+                                : k_forces_staged<kStagedThreadsSmall, kMode>;
+    kern<<<c->bg.nbricks, staged_large(c) ? kStagedThreadsLarge : kStagedThreadsSmall,
+           force_smem(c), c->ls>>>(
+        c->pos, c->cell_rank, c->brick_rank_off, c->start, c->g, c->bg, c->lj, c->nbr,
+        c->nnbr, c->fx, c->fy, c->fz, c->part_e, c->part_w, c->id, it, c->ctrl);
   }
 }
 
@@ -963,6 +953,10 @@ void alloc_list(tmd_gpu_ctx* c, int cap) {
 void grow_after_overflow(tmd_gpu_ctx* c, const Ctrl& h) {
   if (h.status & kStatStageOverflow) {
     const int want = (static_cast<int>(h.max_halo * 1.15) + 64 + 31) / 32 * 32;
+    if (c->variant == 2 && staged_smem_bytes(want) > kStagedSmemMax) {
+      c->variant = 3;  // staged forces: the buffers no longer fit shared memory
+      c->graph_dirty = true;
+    }
     if (static_cast<size_t>(want + 4) * 3 * sizeof(double) > 200 * 1024) {
       c->variant = 1;
     } else {
@@ -1007,6 +1001,15 @@ void choose_build_kind(tmd_gpu_ctx* c) {
   c->graph_dirty = true;
 }
 
+// The staged force kernel (variant 2, on request) needs the brick build's
+// staging-index list (build kinds 3 and 6) and its staging in shared memory.
+void choose_variant(tmd_gpu_ctx* c) {
+  if (c->variant == 2 && (c->build_kind == 5 || force_smem(c) > kStagedSmemMax)) {
+    c->variant = 3;
+    c->graph_dirty = true;
+  }
+}
+
 // TMD_DEBUG_TIMING: synchronise and print the time since the last mark (the
 // create() breakdown; no effect otherwise).
 void debug_mark(tmd_gpu_ctx* c, const char* what) {
@@ -1028,6 +1031,7 @@ void setup_pass(tmd_gpu_ctx* c) {
     launch_resort(c);
     debug_mark(c, "resort");
     if (c->build_auto) choose_build_kind(c);
+    choose_variant(c);
     debug_mark(c, "build kind");
     launch_build(c);
     sync_ctrl(c);
@@ -1453,7 +1457,7 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
   if (c->obs_stride > 0) {
     ck(cudaMemsetAsync(&c->ctrl->obs_rows, 0, sizeof(int), c->stream), "memset obs rows");
   }
-  if (graphs && c->spec_mode && c->variant == 3) {  // (variant 3's force kernels honour halt)
+  if (graphs && c->spec_mode && c->variant >= 2) {  // (these force kernels honour halt)
     if (c->graph_dirty) drop_graphs(c);
     if (c->obs_stride > 0 && c->sgo_stride != c->obs_stride) {
       drop_spec_graphs(c, true);  // the stride is a kernel argument of the observed graphs
@@ -1478,7 +1482,6 @@ bool run_chunk(tmd_gpu_ctx* c, int64_t steps) {
     if (c->last_rebuild_step < 0) c->last_rebuild_step = done;
     double seen = c->h_ctrl->seen_d2;
     long long rebuilds = c->h_ctrl->rebuilds;
-    bool overflow = false;
     // cycle i uses snapshots / events [2 (i % 2)] (A) and [2 (i % 2) + 1] (B)
     auto launch_cycle = [&](int K, int slot) {
       tmd_gpu_ctx::StepGraph& g = spec_graph(c, K, slot, c->cur);
@@ -1913,7 +1916,8 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   // build at once (staging amortised over 16 own cells: -7 % per build at
   // 16.4M); 2 x 2 x 2 for small systems, whose builds are latency-bound
   const int nb4 = ((ext[0] + 1) / 2) * ((ext[1] + 1) / 2) * ((ext[2] + kBrickZ - 1) / kBrickZ);
-  const int bz = nb4 >= 148 * 3 ? kBrickZ : 2;
+  int bz = nb4 >= 148 * 3 ? kBrickZ : 2;
+  if (const char* e = std::getenv("TMD_BRICK_Z")) bz = std::atoi(e) == 2 ? 2 : kBrickZ;  // (probes)
   for (int k = 0; k < 3; ++k) {
     bg.B[k] = std::min(k == 2 ? bz : 2, ext[k]);
     bg.nb[k] = (ext[k] + bg.B[k] - 1) / bg.B[k];
@@ -1973,8 +1977,6 @@ void upload_bricks(tmd_gpu_ctx* c) {
   if (!c->cell_rank) {
     c->cell_rank = dalloc<int>(c->h_rank.size());
     c->brick_rank_off = dalloc<int>(c->h_brick_off.size());
-    c->ngroups = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
-    c->group_off = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
     c->scan_tmp = dalloc<int>(static_cast<size_t>(
         blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1));
   }
@@ -1983,8 +1985,6 @@ void upload_bricks(tmd_gpu_ctx* c) {
   ck(cudaMemcpyAsync(c->brick_rank_off, c->h_brick_off.data(),
                      c->h_brick_off.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream),
      "H2D brick offsets");
-  ck(cudaMemsetAsync(c->ngroups, 0, sizeof(int) * (static_cast<size_t>(c->bg.nbricks) + 1),
-                     c->stream), "memset");
   set_smem_attrs(c);
   c->h_rank.clear();
   c->h_brick_off.clear();
@@ -2175,12 +2175,11 @@ void recut(tmd_gpu_ctx* c, const std::vector<int>& cuts) {
   if (z0 == c->g.z0 && z1 - z0 == c->g.zown) return;
   ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   set_slab_range(c, z0, z1);
-  void* old[] = {c->cell_rank, c->brick_rank_off, c->ngroups, c->group_off, c->scan_tmp,
-                 c->count, c->start};
+  void* old[] = {c->cell_rank, c->brick_rank_off, c->scan_tmp, c->count, c->start};
   for (void* p : old) {
     if (p) cudaFree(p);
   }
-  c->cell_rank = c->brick_rank_off = c->ngroups = c->group_off = c->scan_tmp = nullptr;
+  c->cell_rank = c->brick_rank_off = c->scan_tmp = nullptr;
   c->count = c->start = nullptr;
   setup_bricks(c, static_cast<double>(c->n_total), c->r_cut + c->r_skin);
   const int64_t want = c->n + c->n / 4 + 1024;
@@ -2583,7 +2582,6 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // (slab contexts re-cut and regrow them, so they keep their own)
     c->nparts = std::max({blocks_for(c->n_cap, kBlock), blocks_for(c->n_cap, kLanesPPB),
                           c->bg.nbricks});
-    const size_t nbk1 = static_cast<size_t>(c->bg.nbricks) + 1;
     const size_t nscan = static_cast<size_t>(blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1);
     if (!slab) {
       want(c->count, static_cast<size_t>(c->g.ncells));
@@ -2597,8 +2595,6 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       if (c->timers_on) want(c->ticks, static_cast<size_t>(kTickSteps * kTickPhases + 1));
       want(c->cell_rank, c->h_rank.size());
       want(c->brick_rank_off, c->h_brick_off.size());
-      want(c->ngroups, nbk1);
-      want(c->group_off, nbk1);
       want(c->scan_tmp, nscan);
     }
     mark("plan");
@@ -2768,8 +2764,8 @@ const uint32_t* decoded_list(tmd_gpu_ctx* c) {
     return c->decoded;
   }
   k_decode_list<<<c->bg.nbricks, 128, 0, c->ls>>>(
-      c->cell_rank, c->brick_rank_off, c->start, c->group_off, c->g, c->bg, c->nbr,
-      c->nnbr, c->decoded, c->stride);
+      c->cell_rank, c->brick_rank_off, c->start, c->g, c->bg, c->nbr, c->nnbr, c->decoded,
+      c->stride);
   return c->decoded;
 }
 
@@ -3118,7 +3114,7 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
     }
     if (c->ids_dense && !c->g.zslab && nn > 0) {
       // id order by direct placement on the device, positions wrapped there
-      // (the same rounding as host_wrap1), one copy per array into the
+      // (wrap1, box.hpp:47-51), one copy per array into the
       // caller's buffers
       double* dpos = c->dl;
       double* dvel = c->dl + 3 * nn;
@@ -3395,7 +3391,7 @@ int tmd_gpu_prepare_graphs(tmd_gpu_ctx* c, int64_t obs_stride) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (!c->use_graphs || c->nranks > 1 || c->g.zslab) return;
     if (c->graph_dirty) drop_graphs(c);
-    if (c->spec_mode && c->variant == 3) {  // the blocks a run of this system will launch
+    if (c->spec_mode && c->variant >= 2) {  // the blocks a run of this system will launch
       const int keep = c->obs_stride;
       for (int pass = 0; pass < (obs_stride > 0 ? 2 : 1); ++pass) {
         c->obs_stride = pass == 0 ? 0 : static_cast<int>(std::min<int64_t>(obs_stride, 1 << 30));
@@ -3473,7 +3469,7 @@ uint64_t tmd_gpu_launch_count(const tmd_gpu_ctx* c) { return c->launches; }
 void tmd_gpu_kernel_config(const tmd_gpu_ctx* c, int* variant, int* lanes, int* build_kind) {
   if (variant) *variant = c->variant;
   if (lanes) *lanes = c->variant == 3 ? c->lanes : 1;
-  if (build_kind) *build_kind = c->variant == 3 ? c->build_kind : 0;
+  if (build_kind) *build_kind = c->variant >= 2 ? c->build_kind : 0;
 }
 
 int tmd_gpu_fp64_peak(int device, double* tflops) {

@@ -133,12 +133,13 @@ class EngineConfig:
     device: int = -1
     nbr_capacity: int = 0
     # kernel variant: 0 = library default (3); 1 = thread-per-particle ELL list +
-    # 2x LDG.128 gathers; 2 = brick-staged shared memory; 3 = sector-chunked
-    # list + 256-bit LDG gathers
+    # 2x LDG.128 gathers; 2 = sector-chunked list of brick staging indices,
+    # neighbour positions gathered from shared memory; 3 = sector-chunked list
+    # of global slots + 256-bit LDG gathers
     variant: int = 0
-    # list build of variant 3: 0 = by cell occupancy, 3 = warp per cell
-    # (brick-staged), 5 = thread per particle (sparse cells), 6 = warp per
-    # cell over a culled candidate stream
+    # list build of variants 2/3: 0 = by cell occupancy, 3 = warp per cell
+    # (brick-staged), 5 = thread per particle (sparse cells; variant 3 only),
+    # 6 = warp per cell over a culled candidate stream
     build: int = 0
     # variant-3 force kernel: threads per particle (1, 2, 4, 8; 0 = by
     # particle count, more lanes for small systems)

@@ -427,6 +427,44 @@ def test_variants_bitwise_same_list_membership_1m_scale():
     assert_rel(ob.virial, oa.virial, 1e-12, "virial v1 vs v2")
 
 
+@pytest.mark.parametrize("cells,steps", [(8, 120), (24, 40)])
+def test_staged_forces_bitwise_equal_to_global_gathers(cells, steps):
+    """Variant 2 (neighbour positions gathered from shared memory, list
+    entries = brick staging indices) and variant 3 (gathers from global
+    memory, entries = global slots) list the same entries in the same order
+    and evaluate them with the same arithmetic: forces, energies and whole
+    trajectories are bitwise equal (k_forces_staged vs k_forces_l1)."""
+    f = E.gen_fcc(cells, 0.8442, 1.0, 4242)
+    a = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(variant=3, lanes=1))
+    b = E.Engine(f, E.Interactions(), 0.3, E.EngineConfig(variant=2))
+    assert b.kernel_config()["variant"] == 2
+    np.testing.assert_array_equal(a.pairs(), b.pairs())
+    np.testing.assert_array_equal(a.forces()[1], b.forces()[1])
+    a.run(steps)
+    b.run(steps)
+    fa, fb = a.flatten(), b.flatten()
+    np.testing.assert_array_equal(fa.pos, fb.pos)
+    np.testing.assert_array_equal(fa.vel, fb.vel)
+    oa, ob = a.observe(), b.observe()  # (partial sums per brick vs per 128 particles)
+    assert_rel(ob.potential, oa.potential, 1e-13, "PE staged vs global")
+    assert_rel(ob.virial, oa.virial, 1e-13, "virial staged vs global")
+    assert a.rebuild_count() == b.rebuild_count() > 0
+    a.close()
+    b.close()
+
+
+def test_default_kernel_choice():
+    """Dense systems run the global-gather kernel with one thread per particle
+    (measured fastest, DESIGN.md §5), small ones several threads per particle;
+    a staged-kernel request for a sparse system falls back to it."""
+    big = E.Engine(E.gen_fcc(32, 0.8442, 1.0, 1), E.Interactions(), 0.3, E.EngineConfig())
+    assert big.kernel_config() == dict(variant=3, lanes=1, build_kind=6)
+    big.close()
+    small = E.Engine(E.gen_fcc(8, 0.8442, 1.0, 1), E.Interactions(), 0.3, E.EngineConfig())
+    assert small.kernel_config()["variant"] == 3 and small.kernel_config()["lanes"] > 1
+    small.close()
+
+
 @pytest.mark.parametrize("variant", [1, 2, 3])
 def test_graph_mode_is_bitwise_identical_to_eager(variant):
     """With section timers off a run executes as CUDA graphs whose rebuild

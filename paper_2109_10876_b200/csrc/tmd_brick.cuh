@@ -147,6 +147,13 @@ __device__ __forceinline__ double code_shift(uint32_t code, int axis, double L) 
   return image_shift((code >> (25 + 2 * axis)) & 3u, L);
 }
 
+// Global z coordinate of a brick's origin layer (local layer lz; slab mode:
+// global layer z0 + lz - 1), so that the FP32 brick-relative coordinates stay
+// within a few cells of 0 on every slab (the prefilter band assumes it).
+__device__ __forceinline__ double origin_z(const Geom& g, int lz, double cell_len) {
+  return (g.zslab ? g.z0 + lz - 1 : lz) * cell_len;
+}
+
 __device__ __forceinline__ size_t list_slot(int group, int cap, int lane, int k) {
   return static_cast<size_t>(group) * cap * 32 + static_cast<size_t>(k >> 3) * 256 +
          lane * 8 + (k & 7);
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
   int* sbase = reinterpret_cast<int*>(s_f + 3 * sc);  // entry index field per slot
   const double ox = ht.lo[0] * bg.origin_scale[0];
   const double oy = ht.lo[1] * bg.origin_scale[1];
-  const double oz = ht.lo[2] * bg.origin_scale[2];
+  const double oz = origin_z(g, ht.lo[2], bg.origin_scale[2]);
   for (int k = threadIdx.x; k < ht.total + 32; k += kBuildThreads) {
     float x = kFarF, y = kFarF, z = kFarF;
     int base = 0;
@@ -592,7 +599,7 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
   {  // staging: a warp per halo cell, lanes over its (padded) slots
     const double ox = ht.lo[0] * bg.origin_scale[0];
     const double oy = ht.lo[1] * bg.origin_scale[1];
-    const double oz = ht.lo[2] * bg.origin_scale[2];
+    const double oz = origin_z(g, ht.lo[2], bg.origin_scale[2]);
     for (int h = warp; h < ht.n; h += kBuildThreads / 32) {
       const int kb = s_off[h], cnt = s_cnt[h], gs = s_gstart[h];
       const uint32_t c = s_code[h];

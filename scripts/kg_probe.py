@@ -12,9 +12,9 @@ cells = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 lanes_list = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,2,4").split(",")]
 builds = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "5").split(",")]
 unrolls = [int(x) for x in (sys.argv[4] if len(sys.argv) > 4 else "4").split(",")]
-w = bench.Workload("kg", cells)
+flat, inter, w = bench.make_inputs_ours("kg", cells, 0)
 for build, unroll, lanes in itertools.product(builds, unrolls, lanes_list):
-    eng = E.Engine(w.flat, w.inter, w.r_skin,
+    eng = E.Engine(flat, inter, w.r_skin,
                    E.EngineConfig(dt=w.dt, build=build, lanes=lanes, unroll=unroll,
                                   section_timers=False))
     eng.run(50)

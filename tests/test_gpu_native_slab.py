@@ -231,3 +231,34 @@ def test_local_state_into_caller_buffers():
         np.testing.assert_array_equal(v2, vel)
     finally:
         eng.close()
+
+
+def _planted_far_slab(seed, n_pairs=400, L=200.0, rv=2.8):
+    """Pairs planted at |r - r_v| of a few ulps in a large box, all in its
+    upper half (the slabs of the high ranks) and many along z: the FP32
+    prefilter must use coordinates relative to the brick's GLOBAL origin on
+    every slab, or its rounding error (~1e-5 at |z| ~ 150) outgrows the exact
+    band and membership goes wrong."""
+    rng = np.random.default_rng(seed)
+    deltas = np.array([0.0, 1e-16, -1e-16, 2e-16, -2e-16, 1e-13, -1e-13, 1e-9, -1e-9])
+    p = rng.uniform(0.0, L, (n_pairs, 3))
+    p[:, 2] = rng.uniform(0.55 * L, 0.98 * L, n_pairs)
+    u = rng.normal(size=(n_pairs, 3)) * np.array([0.3, 0.3, 1.0])
+    u /= np.linalg.norm(u, axis=1)[:, None]
+    d = rv * (1.0 + deltas[rng.integers(0, len(deltas), n_pairs)])
+    q = p + d[:, None] * u
+    pos = np.concatenate([p, q]).reshape(-1, 3) % L
+    ids = np.arange(1, 2 * n_pairs + 1, dtype=np.int64)
+    return np.array([L, L, L]), ids, pos, np.zeros_like(pos)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_native_slab_rounding_band_far_from_origin(ref, seed):
+    box, ids, pos, vel = _planted_far_slab(seed)
+    want = ref.RefEngine(box, ids, pos, vel, r_skin=0.3).pairs()
+    eng = DecomposedEngine(E.FlatConfig(box, ids, pos, vel), E.Interactions(), 0.3,
+                           E.EngineConfig(dt=0.005), comm=InProcessComm(4), native=True)
+    try:
+        np.testing.assert_array_equal(eng.local_pairs(), want)
+    finally:
+        eng.close()

@@ -282,7 +282,8 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
   for (int d = 0; d < R; ++d) off[static_cast<size_t>(d) + 1] = off[static_cast<size_t>(d)] + M[static_cast<size_t>(r) * uR + d];
   c->launches += 1;
   k_mig_offsets<<<1, 1, 0, c->ls>>>(Md, r, R, c->mig_off);
-  if (n > 0) {
+  const bool leavers = off[uR] > 0;  // none: the stayers are already in place
+  if (n > 0 && leavers) {
     c->launches += 1;
     k_mig_pack<<<c->nblk, kBlock, 0, c->ls>>>(
         n, c->pos, c->vx, c->vy, c->vz, c->mass, c->id, c->mig_dest, c->my_rank, c->mig_off,
@@ -290,8 +291,8 @@ void nccl_rebuild(tmd_gpu_ctx* c, bool advance) {
         c->id2);
   }
   const size_t keep = static_cast<size_t>(n - off[uR]);
-  if (keep > 0) {  // stayers back in place: one unconditional launch (no cell
-                   // column: the resort that follows recomputes it)
+  if (keep > 0 && leavers) {  // stayers back in place: one launch (no cell column:
+                              // the resort that follows recomputes it)
     c->launches += 1;
     k_copy_back<<<blocks_for(static_cast<int64_t>(keep), kBlock), kBlock, 0, c->ls>>>(
         static_cast<int>(keep), c->pos2, c->vx2, c->vy2, c->vz2, c->mass2, c->id2, nullptr,

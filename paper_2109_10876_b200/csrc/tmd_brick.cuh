@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(kThreads, staged_min_blocks<kThreads>())
   extern __shared__ __align__(16) double2 s_xy[];  // [stage_cap + 1], then z [stage_cap + 1]
   __shared__ int s_gstart[kMaxHalo], s_cnt[kMaxHalo], s_off[kMaxHalo + 1], s_gcell[kMaxHalo];
   __shared__ uint32_t s_code[kMaxHalo];
-  __shared__ double red[kThreads / 32];
+  __shared__ double red[3 * (kThreads / 32)];
   double* s_z = reinterpret_cast<double*>(s_xy + bg.stage_cap + 1);
   HaloTable ht;
   load_halo(b, g, bg, cell_rank, brick_rank_off, start, ht, s_gstart, s_cnt, s_off, s_code,
@@ -1133,13 +1133,7 @@ __global__ void __launch_bounds__(kThreads, staged_min_blocks<kThreads>())
       }
     }
   }
-  const double te = block_sum<kThreads>(e, red);
-  const double tw = block_sum<kThreads>(w, red);
-  if (threadIdx.x == 0) {
-    part_e[b] = te;
-    part_w[b] = tw;
-  }
-  integrate_block<kMode, kThreads>(ke, d2, red, it, ctrl);
+  block_partials<kMode, kThreads>(e, w, ke, d2, red, part_e, part_w, it, ctrl);  // (b = blockIdx.x)
 }
 
 // Threads of a staged force CTA: one per particle of a brick (2x2x2 cells
@@ -1173,7 +1167,7 @@ __global__ void __launch_bounds__(128)
     if (kMode == kFused && it.halt_copy && i < n) it.pos_out[i] = pos[i];
     return;
   }
-  __shared__ double red[4];
+  __shared__ double red[3 * 4];
   const int i = blockIdx.x * 128 + threadIdx.x;
   double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
   if (i < n) {
@@ -1218,13 +1212,7 @@ __global__ void __launch_bounds__(128)
       fz[i] = az;
     }
   }
-  const double te = block_sum<128>(e, red);
-  const double tw = block_sum<128>(w, red);
-  if (threadIdx.x == 0) {
-    part_e[blockIdx.x] = te;
-    part_w[blockIdx.x] = tw;
-  }
-  integrate_block<kMode, 128>(ke, d2, red, it, ctrl);
+  block_partials<kMode, 128>(e, w, ke, d2, red, part_e, part_w, it, ctrl);
 }
 
 // ---------------------------------------------------------------------------
@@ -1262,7 +1250,7 @@ __global__ void __launch_bounds__(kLanesPPB * kLanes, lanes_min_blocks(kLanes))
     return;
   }
   constexpr int kThreads = kLanesPPB * kLanes;
-  __shared__ double red[kThreads / 32];
+  __shared__ double red[3 * (kThreads / 32)];
   const int sub = threadIdx.x % kLanes;
   const int i = blockIdx.x * kLanesPPB + threadIdx.x / kLanes;
   double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
@@ -1323,13 +1311,7 @@ __global__ void __launch_bounds__(kLanesPPB * kLanes, lanes_min_blocks(kLanes))
       fz[i] = az;
     }
   }
-  const double te = block_sum<kThreads>(e, red);
-  const double tw = block_sum<kThreads>(w, red);
-  if (threadIdx.x == 0) {
-    part_e[blockIdx.x] = te;
-    part_w[blockIdx.x] = tw;
-  }
-  integrate_block<kMode, kThreads>(ke, d2, red, it, ctrl);
+  block_partials<kMode, kThreads>(e, w, ke, d2, red, part_e, part_w, it, ctrl);
 }
 
 // Tap for variant 3: chunked global-slot list -> ELL-transposed copy.

@@ -166,18 +166,42 @@ __device__ __forceinline__ void integrate_one(int i, const double4& pi, double& 
   it.vz[i] = uz;
 }
 
-// Block-level reductions of the epilogue (all threads of the block call it).
+// The block's energy, virial and (kicking modes) kinetic partial sums in one
+// pass: per-warp xor trees, then the warps' sums in warp order by thread 0 —
+// the same fixed order as three block_sum calls, with one barrier instead of
+// six. d2: the step's largest displacement, one atomicMax per warp.
 template <int kMode, int kThreads>
-__device__ __forceinline__ void integrate_block(double ke, double d2, double* red,
-                                                const Integ& it, Ctrl* ctrl) {
-  if (kMode == kForcesOnly) return;
-  const double t = block_sum<kThreads>(ke, red);
-  if (threadIdx.x == 0) it.part_ke[blockIdx.x] = t;
-  if (kMode == kFused) {
-    for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
-    if ((threadIdx.x & 31) == 0 && d2 > 0.0) {
+__device__ __forceinline__ void block_partials(double e, double w, double ke, double d2,
+                                               double* red3, double* part_e, double* part_w,
+                                               const Integ& it, Ctrl* ctrl) {
+  constexpr int kW = kThreads / 32;
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+    w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (kMode != kForcesOnly) ke += __shfl_xor_sync(0xffffffffu, ke, o);
+    if (kMode == kFused) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red3[warp] = e;
+    red3[kW + warp] = w;
+    red3[2 * kW + warp] = ke;
+    if (kMode == kFused && d2 > 0.0) {
       atomicMax(&ctrl->max_d2, static_cast<unsigned long long>(__double_as_longlong(d2)));
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double te = 0.0, tw = 0.0, tk = 0.0;
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      te += red3[q];
+      tw += red3[kW + q];
+      tk += red3[2 * kW + q];
+    }
+    part_e[blockIdx.x] = te;
+    part_w[blockIdx.x] = tw;
+    if (kMode != kForcesOnly) it.part_ke[blockIdx.x] = tk;
   }
 }
 
@@ -762,7 +786,7 @@ __global__ void __launch_bounds__(kBlock)
                 double* __restrict__ fy, double* __restrict__ fz,
                 double* __restrict__ part_e, double* __restrict__ part_w,
                 const long long* __restrict__ id, Integ it, Ctrl* ctrl) {
-  __shared__ double red[kBlock / 32];
+  __shared__ double red[3 * (kBlock / 32)];
   const int i = blockIdx.x * kBlock + threadIdx.x;
   double e = 0.0, w = 0.0, ke = 0.0, d2 = 0.0;
   if (i < n) {
@@ -804,13 +828,7 @@ __global__ void __launch_bounds__(kBlock)
       fz[i] = az;
     }
   }
-  const double te = block_sum<kBlock>(e, red);
-  const double tw = block_sum<kBlock>(w, red);
-  if (threadIdx.x == 0) {
-    part_e[blockIdx.x] = te;
-    part_w[blockIdx.x] = tw;
-  }
-  integrate_block<kMode, kBlock>(ke, d2, red, it, ctrl);
+  block_partials<kMode, kBlock>(e, w, ke, d2, red, part_e, part_w, it, ctrl);
 }
 
 // Deterministic final reduction of per-block partials (fixed order tree).

@@ -4,7 +4,7 @@
 # at 16.4M and 32K, and full ncu captures of the fused step kernel and the
 # list build at 16.4M (each ncu pass after its command ran clean without ncu).
 set -u
-TAG=${TAG:-r02m}
+TAG=${TAG:-r02q}
 mkdir -p gpurun_out
 run() { local name=$1; shift; timeout 1200 "$@" > gpurun_out/${TAG}_${name}.json 2> gpurun_out/${TAG}_${name}.err || echo "$name failed"; tail -c 400 gpurun_out/${TAG}_${name}.json; echo; }
 run bench python bench.py --steps 20 --warmup 5
@@ -31,4 +31,7 @@ fi
 timeout 300 python scripts/small_probe.py 20 > gpurun_out/${TAG}_small_probe.log 2>&1
 timeout 300 python scripts/build_probe.py 20 64 160 > gpurun_out/${TAG}_build_probe.log 2>&1
 timeout 300 python scripts/slab_overhead_probe.py 64 > gpurun_out/${TAG}_slab_overhead64.log 2>&1
+timeout 300 python scripts/slab_overhead_probe.py 20 > gpurun_out/${TAG}_slab_overhead20.log 2>&1
+timeout 300 python scripts/small_probe2.py 20 > gpurun_out/${TAG}_small_probe2.log 2>&1
+timeout 300 python scripts/force_variants.py --cells 64 --steps 50 --variants 2,3:4 > gpurun_out/${TAG}_force_variants64.log 2>&1
 echo done

@@ -336,6 +336,14 @@ int tmd_gpu_slab_attach_nccl(tmd_gpu_ctx* ctx, const void* unique_id, int flags)
 int tmd_local_group_create(int nranks, void** group);
 void tmd_local_group_destroy(void* group);
 int tmd_gpu_slab_attach_local(tmd_gpu_ctx* ctx, void* group, int flags);
+/* One process per rank whose collectives and messages are staged through host
+ * memory shared by mapping the file `path` (every rank passes the same path;
+ * the file is created and sized on first use and should start empty). Each
+ * operation synchronises the context stream first, so no kernel ever waits on
+ * another rank: several ranks can share ONE GPU. The fused halo's peer
+ * buffers are CUDA IPC mappings as with NCCL. The multi-process test path of
+ * the native loop (NCCL needs a GPU per rank); not a production transport. */
+int tmd_gpu_slab_attach_host(tmd_gpu_ctx* ctx, const char* path, int flags);
 int tmd_gpu_slab_setup(tmd_gpu_ctx* ctx);
 int tmd_gpu_slab_run(tmd_gpu_ctx* ctx, int64_t nsteps);
 /* tmd_gpu_slab_run recording every `stride`-th step's observables as the

@@ -44,6 +44,7 @@ EXPORTS = [
     "tmd_gpu_slab_observe", "tmd_balanced_cuts", "tmd_gpu_release_cache",
     "tmd_gpu_time_step_kernel", "tmd_gpu_prepare_graphs",
     "tmd_local_group_create", "tmd_local_group_destroy", "tmd_gpu_slab_attach_local",
+    "tmd_gpu_slab_attach_host",
     "tmd_gpu_build_pair_index_list", "tmd_gpu_pair_index_list", "tmd_gpu_compute_forces_pairs",
     "tmd_gpu_time_pair_traversal",
 ]
@@ -136,6 +137,7 @@ def lib() -> C.CDLL:
     L.tmd_local_group_destroy.argtypes = [P]
     L.tmd_local_group_destroy.restype = None
     L.tmd_gpu_slab_attach_local.argtypes = [P, P, C.c_int]
+    L.tmd_gpu_slab_attach_host.argtypes = [P, C.c_char_p, C.c_int]
     L.tmd_gpu_slab_setup.argtypes = [P]
     L.tmd_gpu_slab_run.argtypes = [P, C.c_int64]
     L.tmd_gpu_slab_observe.argtypes = [P, C.c_int64, C.POINTER(TmdObservables)]

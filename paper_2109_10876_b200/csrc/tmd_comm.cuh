@@ -3,6 +3,13 @@
 // interface, stream-ordered like NCCL (nothing in a step waits for the host).
 //
 //   NcclComm   one process (or thread) per GPU, NCCL on the context stream.
+//   HostFileComm  one process per rank, collectives and messages staged through
+//              host memory shared by a file mapping (every op synchronises the
+//              stream first): slow, but it runs the multi-process path — CUDA
+//              IPC peer buffers of the fused halo included — with several
+//              ranks on ONE GPU without any kernel waiting on another rank
+//              (the test of the cross-process protocol; NCCL needs one GPU per
+//              rank).
 //   LocalComm  every rank's context in one process, one host thread per rank
 //              (R slabs on one GPU, or several GPUs of one process): a
 //              collective is a host rendezvous of the rank threads that
@@ -20,6 +27,13 @@
 
 #include <condition_variable>
 #include <cstdlib>
+#include <cstring>
+#include <cstdio>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -344,6 +358,190 @@ struct LocalComm final : SlabComm {
   }
   void abort() override { grp->abort(); }
   bool in_process() const override { return true; }
+};
+
+// Cross-process transport over a shared file mapping (test path, see the
+// header). Layout: a 4 KB header {arrivals, generation, abort}, one 1 MB slot
+// per rank for collectives, one mailbox per ordered rank pair for point-to-
+// point messages (a message table, then the payloads in posting order).
+struct HostFileComm final : SlabComm {
+  static constexpr size_t kHeader = 4096;
+  static constexpr size_t kSlot = size_t{1} << 20;
+  static constexpr size_t kBox = size_t{32} << 20;
+  static constexpr int kMaxMsgs = 64;
+  struct Pending {
+    void* p;
+    size_t bytes;
+    int peer;
+  };
+  int rank = 0, nranks = 1;
+  char* base = nullptr;
+  size_t mapped = 0;
+  std::vector<Pending> sends, recvs;
+
+  HostFileComm(const char* path, int r, int R) : rank(r), nranks(R) {
+    mapped = kHeader + static_cast<size_t>(R) * kSlot + static_cast<size_t>(R) * R * kBox;
+    const int fd = ::open(path, O_RDWR | O_CREAT, 0600);
+    if (fd < 0) throw CudaFail{std::string("host transport: cannot open ") + path};
+    struct stat st {};
+    if (::fstat(fd, &st) != 0 ||
+        (static_cast<size_t>(st.st_size) < mapped && ::ftruncate(fd, static_cast<off_t>(mapped)) != 0)) {
+      ::close(fd);
+      throw CudaFail{"host transport: cannot size the mapping"};
+    }
+    void* m = ::mmap(nullptr, mapped, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    ::close(fd);
+    if (m == MAP_FAILED) throw CudaFail{"host transport: mmap failed"};
+    base = static_cast<char*>(m);
+  }
+  ~HostFileComm() override {
+    if (base) ::munmap(base, mapped);
+  }
+  int* word(int k) { return reinterpret_cast<int*>(base) + k; }  // 0 arrivals, 1 gen, 2 abort
+  char* slot(int q) { return base + kHeader + static_cast<size_t>(q) * kSlot; }
+  char* box(int src, int dst) {
+    return base + kHeader + static_cast<size_t>(nranks) * kSlot +
+           (static_cast<size_t>(src) * nranks + dst) * kBox;
+  }
+  void barrier() {
+    const int g = __atomic_load_n(word(1), __ATOMIC_ACQUIRE);
+    if (__atomic_add_fetch(word(0), 1, __ATOMIC_ACQ_REL) == nranks) {
+      __atomic_store_n(word(0), 0, __ATOMIC_RELAXED);
+      __atomic_add_fetch(word(1), 1, __ATOMIC_RELEASE);
+      return;
+    }
+    while (__atomic_load_n(word(1), __ATOMIC_ACQUIRE) == g) {
+      if (__atomic_load_n(word(2), __ATOMIC_ACQUIRE)) throw CudaFail{"a peer rank failed"};
+      sched_yield();
+    }
+  }
+  static void sync(cudaStream_t s) { ck(cudaStreamSynchronize(s), "cudaStreamSynchronize"); }
+  // Copies on the context stream, completed before returning (the shared
+  // pages are pageable host memory: a plain cudaMemcpy H2D may return before
+  // its DMA lands, and the context stream does not order after it).
+  static void copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind k, cudaStream_t s,
+                   const char* what) {
+    ck(cudaMemcpyAsync(dst, src, bytes, k, s), what);
+    sync(s);
+  }
+  void allreduce(void* buf, size_t count, CType t, COp op, cudaStream_t s) override {
+    const size_t bytes = count * ctype_bytes(t);
+    if (bytes > kSlot) throw CudaFail{"host transport: all-reduce too large"};
+    sync(s);
+    copy(slot(rank), buf, bytes, cudaMemcpyDeviceToHost, s, "D2H all-reduce");
+    barrier();
+    std::vector<char> acc(slot(0), slot(0) + bytes);
+    for (int q = 1; q < nranks; ++q) {  // fixed rank order
+      const char* v = slot(q);
+      for (size_t k = 0; k < count; ++k) {
+        switch (t) {
+          case CType::kI32: {
+            auto* a = reinterpret_cast<int32_t*>(acc.data()) + k;
+            const int32_t b = reinterpret_cast<const int32_t*>(v)[k];
+            *a = op == COp::kSum ? *a + b : std::max(*a, b);
+            break;
+          }
+          case CType::kI64: {
+            auto* a = reinterpret_cast<int64_t*>(acc.data()) + k;
+            const int64_t b = reinterpret_cast<const int64_t*>(v)[k];
+            *a = op == COp::kSum ? *a + b : std::max(*a, b);
+            break;
+          }
+          case CType::kU64: {
+            auto* a = reinterpret_cast<uint64_t*>(acc.data()) + k;
+            const uint64_t b = reinterpret_cast<const uint64_t*>(v)[k];
+            *a = op == COp::kSum ? *a + b : std::max(*a, b);
+            break;
+          }
+          default: {
+            auto* a = reinterpret_cast<double*>(acc.data()) + k;
+            const double b = reinterpret_cast<const double*>(v)[k];
+            *a = op == COp::kSum ? *a + b : std::max(*a, b);
+          }
+        }
+      }
+    }
+    copy(buf, acc.data(), bytes, cudaMemcpyHostToDevice, s, "H2D all-reduce");
+    barrier();  // the slots are free again
+  }
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    if (bytes > kSlot) throw CudaFail{"host transport: all-gather too large"};
+    sync(s);
+    copy(slot(rank), send, bytes, cudaMemcpyDeviceToHost, s, "D2H all-gather");
+    barrier();
+    for (int q = 0; q < nranks; ++q) {
+      ck(cudaMemcpyAsync(static_cast<char*>(recv) + static_cast<size_t>(q) * bytes, slot(q),
+                         bytes, cudaMemcpyHostToDevice, s), "H2D all-gather");
+    }
+    sync(s);
+    barrier();
+  }
+  void group_start() override {
+    sends.clear();
+    recvs.clear();
+  }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t) override {
+    sends.push_back({const_cast<void*>(buf), bytes, peer});
+  }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t) override {
+    recvs.push_back({buf, bytes, peer});
+  }
+  // mailbox (src -> dst): int count, size_t sizes[kMaxMsgs], payloads in order
+  static size_t* sizes_of(char* b) { return reinterpret_cast<size_t*>(b + 64); }
+  static char* data_of(char* b) { return b + 64 + kMaxMsgs * sizeof(size_t); }
+  void group_end(cudaStream_t s) override {
+    sync(s);
+    for (int d = 0; d < nranks; ++d) *reinterpret_cast<int*>(box(rank, d)) = 0;
+    std::vector<size_t> fill(static_cast<size_t>(nranks), 0);
+    for (const Pending& m : sends) {
+      char* b = box(rank, m.peer);
+      int& n = *reinterpret_cast<int*>(b);
+      size_t& f = fill[static_cast<size_t>(m.peer)];
+      if (n >= kMaxMsgs || 64 + kMaxMsgs * sizeof(size_t) + f + m.bytes > kBox) {
+        throw CudaFail{"host transport: mailbox full"};
+      }
+      sizes_of(b)[n++] = m.bytes;
+      if (m.bytes) {
+        ck(cudaMemcpyAsync(data_of(b) + f, m.p, m.bytes, cudaMemcpyDeviceToHost, s),
+           "D2H message");
+      }
+      f += m.bytes;
+    }
+    sync(s);
+    barrier();
+    std::string err;
+    std::vector<int> next(static_cast<size_t>(nranks), 0);
+    std::vector<size_t> off(static_cast<size_t>(nranks), 0);
+    for (const Pending& m : recvs) {
+      char* b = box(m.peer, rank);
+      const int n = *reinterpret_cast<int*>(b);
+      int& k = next[static_cast<size_t>(m.peer)];
+      if (k >= n) {
+        err = "receive from rank " + std::to_string(m.peer) + " has no matching send";
+        break;
+      }
+      if (sizes_of(b)[k] != m.bytes) {
+        err = "message size mismatch from rank " + std::to_string(m.peer);
+        break;
+      }
+      if (m.bytes) {
+        ck(cudaMemcpyAsync(m.p, data_of(b) + off[static_cast<size_t>(m.peer)], m.bytes,
+                           cudaMemcpyHostToDevice, s), "H2D message");
+      }
+      off[static_cast<size_t>(m.peer)] += m.bytes;
+      ++k;
+    }
+    sync(s);
+    for (int q = 0; q < nranks && err.empty(); ++q) {
+      if (next[static_cast<size_t>(q)] != *reinterpret_cast<int*>(box(q, rank))) {
+        err = "unmatched send from rank " + std::to_string(q);
+      }
+    }
+    barrier();  // (errors raised after it: no peer is left waiting)
+    if (!err.empty()) throw CudaFail{"slab loop: " + err};
+  }
+  void abort() override { __atomic_store_n(word(2), 1, __ATOMIC_RELEASE); }
+  bool in_process() const override { return false; }
 };
 
 }  // namespace

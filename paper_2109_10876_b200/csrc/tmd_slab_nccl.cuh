@@ -199,8 +199,16 @@ double4* peer_buffer(tmd_gpu_ctx* c, const PeerInfo& p, int peer, int b) {
     if (e.first == key) return static_cast<double4*>(e.second);
   }
   void* ptr = nullptr;
-  ck(cudaIpcOpenMemHandle(&ptr, p.h[b], cudaIpcMemLazyEnablePeerAccess),
-     "cudaIpcOpenMemHandle");
+  const cudaError_t e = cudaIpcOpenMemHandle(&ptr, p.h[b], cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CudaFail{std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e) + " (rank " +
+                   std::to_string(c->my_rank) + " pid " + std::to_string(getpid()) +
+                   ", peer " + std::to_string(peer) + " pid " + std::to_string(p.pid) +
+                   " device " + std::to_string(p.device) + " buffer " + std::to_string(b) +
+                   " base " + std::to_string(p.base[b]) + ", " +
+                   std::to_string(c->ipc_open.size()) + " mappings open)"};
+  }
   c->ipc_open.emplace_back(key, ptr);
   return static_cast<double4*>(ptr);
 }
@@ -523,6 +531,16 @@ int tmd_gpu_slab_attach_local(tmd_gpu_ctx* c, void* group, int flags) {
       g->taken[static_cast<size_t>(c->my_rank)] = 0;
       throw;
     }
+  });
+}
+
+int tmd_gpu_slab_attach_host(tmd_gpu_ctx* c, const char* path, int flags) {
+  return guard(c, [&] {
+    if (!path || !*path) throw StatusError{TMD_ERR_CONFIG, "host transport: a file path"};
+    attach_common(c, flags);
+    auto hc = std::make_unique<HostFileComm>(path, c->my_rank, c->nranks);
+    alloc_comm_staging(c);
+    c->comm = hc.release();
   });
 }
 

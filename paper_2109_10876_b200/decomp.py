@@ -312,6 +312,11 @@ class SlabContext:
         flags = (1 if balance_count else 0) | (2 if fused_halo else 0)
         self._c(_abi.lib().tmd_gpu_slab_attach_nccl(self._h, buf, flags))
 
+    def attach_host(self, path: str, balance_count: bool = False,
+                    fused_halo: bool = True) -> None:
+        flags = (1 if balance_count else 0) | (2 if fused_halo else 0)
+        self._c(_abi.lib().tmd_gpu_slab_attach_host(self._h, str(path).encode(), flags))
+
     def attach_local(self, group, balance_count: bool = False, fused_halo: bool = True) -> None:
         """Attach to an in-process group (tmd_local_group_create): the same C++
         loop with every rank's context in this process, one thread per rank."""
@@ -382,6 +387,21 @@ class Comm:
     def broadcast_bytes(self, make) -> bytes:
         """make() on rank 0, its bytes on every rank."""
         raise NotImplementedError
+
+
+class HostFileComm(Comm):
+    """One rank per process; the native loop's collectives and messages go
+    through host memory shared by mapping one file (tmd_gpu_slab_attach_host).
+    Every operation synchronises the stream first, so the ranks may share one
+    GPU: the multi-process path of the native loop — CUDA IPC peer buffers of
+    the fused halo included — tested on a single-GPU box. Native loop only
+    (the Python protocol needs a torch.distributed or in-process Comm)."""
+
+    def __init__(self, path: str, rank: int, nranks: int):
+        self.path = str(path)
+        self.me = int(rank)
+        self.nranks = int(nranks)
+        self.local_ranks = [self.me]
 
 
 class InProcessComm(Comm):
@@ -531,6 +551,8 @@ class DecomposedEngine:
         validate_engine_config(cfg)
         if comm is None:
             raise ConfigError("DecomposedEngine needs a Comm (InProcessComm / TorchDistComm)")
+        if isinstance(comm, HostFileComm) and not native:
+            raise ConfigError("HostFileComm drives the native loop only (native=True)")
         self.comm = comm
         self.cfg = cfg
         self.n_total = flat.size()
@@ -575,6 +597,9 @@ class DecomposedEngine:
                         c.attach_local(g, **kw)
                 finally:
                     L.tmd_local_group_destroy(g)
+            elif isinstance(comm, HostFileComm):
+                (c,) = self.ctx.values()
+                c.attach_host(comm.path, **kw)
             else:
                 if len(self.ctx) != 1:
                     raise ConfigError("the native NCCL loop runs one slab per process")

@@ -401,7 +401,22 @@ __global__ void __launch_bounds__(kBuildThreads, kBuildMinBlocks)
 //     unsigned min.
 // The own cell (self exclusion) is a stream segment of its own.
 constexpr int kCullCap = 96;    // stream candidates per warp (multiple of 32)
-constexpr int kRingSlots = 20;  // flush trigger at 16 + up to 3 appends in flight
+#ifndef TMD_RING_SLOTS
+#define TMD_RING_SLOTS 28
+#endif
+#ifndef TMD_RING_TRIGGER
+#define TMD_RING_TRIGGER 16
+#endif
+#ifndef TMD_FLUSH_EVERY
+#define TMD_FLUSH_EVERY 3
+#endif
+// per-lane ring: flushed when any lane holds kRingTrigger entries, checked
+// every kFlushEvery chunks of 4 (so up to kRingTrigger - 1 + 4 kFlushEvery
+// entries in flight)
+constexpr int kRingSlots = TMD_RING_SLOTS;
+constexpr int kRingTrigger = TMD_RING_TRIGGER;
+constexpr int kFlushEvery = TMD_FLUSH_EVERY;
+static_assert(kRingTrigger - 1 + 4 * kFlushEvery <= kRingSlots, "ring too small");
 
 struct CullLane {
   float2 xi2, yi2, zi2;
@@ -526,9 +541,12 @@ __device__ __forceinline__ void cull_segment(const float* __restrict__ strm, int
                                              const Geom& g, int cap8, uint32_t* ring_lane,
                                              const StageMap& sm) {
   const uint32_t me = L.self;
-  const uint32_t trig = L.rbase + 16u * 128u;
+  const uint32_t trig = L.rbase + static_cast<uint32_t>(kRingTrigger) * 128u;
 #pragma unroll 1
-  for (int c = 0; c < fill; c += 4) {
+  for (int c0 = 0; c0 < fill; c0 += 4 * kFlushEvery) {
+#pragma unroll
+  for (int c = c0; c < c0 + 4 * kFlushEvery; c += 4) {
+    if (kFlushEvery > 1 && c >= fill) break;
     const float* ch = strm + c * 4;  // chunk of 4: x4 | y4 | z4 | entry4
     const float4 X = *reinterpret_cast<const float4*>(ch);
     const float4 Y = *reinterpret_cast<const float4*>(ch + 4);
@@ -553,7 +571,8 @@ __device__ __forceinline__ void cull_segment(const float* __restrict__ strm, int
       cull_band1<kLocal>(a, E.w, rb.y, db.y, L, pi, pos, g, sm);
     }
     L.a = a;
-    if (__any_sync(0xffffffffu, a >= trig)) cull_flush(L, cap8, ring_lane);
+  }
+    if (__any_sync(0xffffffffu, L.a >= trig)) cull_flush(L, cap8, ring_lane);
   }
 }
 

@@ -4,7 +4,7 @@
 # at 16.4M and 32K, and full ncu captures of the fused step kernel and the
 # list build at 16.4M (each ncu pass after its command ran clean without ncu).
 set -u
-TAG=${TAG:-r02q}
+TAG=${TAG:-r02t}
 mkdir -p gpurun_out
 run() { local name=$1; shift; timeout 1200 "$@" > gpurun_out/${TAG}_${name}.json 2> gpurun_out/${TAG}_${name}.err || echo "$name failed"; tail -c 400 gpurun_out/${TAG}_${name}.json; echo; }
 run bench python bench.py --steps 20 --warmup 5

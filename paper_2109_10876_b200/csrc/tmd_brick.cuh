@@ -154,6 +154,50 @@ __device__ __forceinline__ double origin_z(const Geom& g, int lz, double cell_le
   return (g.zslab ? g.z0 + lz - 1 : lz) * cell_len;
 }
 
+// Brick-major cell ranks (setup_bricks' order: bricks x-fastest, cells
+// x-fastest inside a brick; slab mode: the two ghost layers ranked after every
+// owned cell, x-fastest) and each brick's first rank, in closed form: the
+// cells of the bricks before brick (bx, by, bz) are the full brick layers
+// below it, the full brick rows before it in its layer and the bricks before
+// it in its row.
+__global__ void __launch_bounds__(kBlock)
+    k_brick_tables(Geom g, BrickGeom bg, int* __restrict__ cell_rank,
+                   int* __restrict__ brick_rank_off) {
+  const int t = blockIdx.x * kBlock + threadIdx.x;
+  const int d0 = g.dims[0], d1 = g.dims[1];
+  const int zoff = g.zslab ? 1 : 0;
+  const int ext2 = g.zslab ? g.zown : g.dims[2];
+  const int owned = d0 * d1 * ext2;
+  auto before = [&](int bx, int by, int bz) {
+    const int ey = min(bg.B[1], d1 - by * bg.B[1]);
+    const int ez = min(bg.B[2], ext2 - bz * bg.B[2]);
+    return min(bz * bg.B[2], ext2) * d0 * d1 + min(by * bg.B[1], d1) * d0 * ez +
+           min(bx * bg.B[0], d0) * ey * ez;
+  };
+  if (t <= bg.nbricks) {
+    if (t == bg.nbricks) {
+      brick_rank_off[t] = owned;
+    } else {
+      const int bx = t % bg.nb[0], by = (t / bg.nb[0]) % bg.nb[1], bz = t / (bg.nb[0] * bg.nb[1]);
+      brick_rank_off[t] = before(bx, by, bz);
+    }
+  }
+  if (t < g.ncells) {
+    const int x = t % d0, y = (t / d0) % d1, zl = t / (d0 * d1);
+    int r;
+    if (g.zslab && (zl == 0 || zl == g.ldz - 1)) {
+      r = owned + (zl == 0 ? 0 : d0 * d1) + x + d0 * y;
+    } else {
+      const int z = zl - zoff;
+      const int bx = x / bg.B[0], by = y / bg.B[1], bz = z / bg.B[2];
+      const int ex = min(bg.B[0], d0 - bx * bg.B[0]);
+      const int ey = min(bg.B[1], d1 - by * bg.B[1]);
+      r = before(bx, by, bz) + (x - bx * bg.B[0]) + ex * ((y - by * bg.B[1]) + ey * (z - bz * bg.B[2]));
+    }
+    cell_rank[t] = r;
+  }
+}
+
 __device__ __forceinline__ size_t list_slot(int group, int cap, int lane, int k) {
   return static_cast<size_t>(group) * cap * 32 + static_cast<size_t>(k >> 3) * 256 +
          lane * 8 + (k & 7);

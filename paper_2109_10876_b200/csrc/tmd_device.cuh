@@ -102,6 +102,7 @@ struct Ctrl {
                               // decision saw (the host sizes its next batch from it)
   long long tick_base;        // section timers in graph mode: step count at the chunk
                               // start (phase ticks are indexed by step - tick_base)
+  unsigned long long occ_s2;  // sum over owned cells of (particles in the cell)^2 (k_occupancy)
 };
 
 // Section timers without host round trips (graph mode, the native slab loop):

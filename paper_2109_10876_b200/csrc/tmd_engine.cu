@@ -321,7 +321,6 @@ struct tmd_gpu_ctx {
   int nparts = 0;                 // partial-sum slots of the force kernel
   uint32_t* decoded = nullptr;    // global-index ELL copy for the taps
   size_t decoded_words = 0;
-  std::vector<int> h_rank, h_brick_off;  // host staging for upload_bricks
   int* scan_tmp = nullptr;               // tile sums of the tiled scan
 
   // PairIndexList (tmd_pairlist.cuh): explicit pairs of the current list
@@ -981,16 +980,17 @@ constexpr double kBuildCellWarpMin = 12.0;  // mean particles per cell (measured
 // thread per particle (sparse cells, e.g. the KG melt).
 void choose_build_kind(tmd_gpu_ctx* c) {
   const int nc = c->g.owned_cells;
-  std::vector<int> st(static_cast<size_t>(nc) + 1);
-  ck(cudaMemcpyAsync(st.data(), c->start, st.size() * sizeof(int), cudaMemcpyDeviceToHost,
-                     c->stream), "D2H start");
-  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-  double s1 = 0.0, s2 = 0.0;
-  for (int k = 0; k < nc; ++k) {
-    const double m = static_cast<double>(st[k + 1] - st[k]);
-    s1 += m;
-    s2 += m * m;
-  }
+  // sum of n_c^2 on the device (sum of n_c = the owned particles)
+  ck(cudaMemsetAsync(&c->ctrl->occ_s2, 0, sizeof(unsigned long long), c->stream), "memset");
+  c->launches += 1;
+  k_occupancy<<<std::max(1, blocks_for(nc, kBlock)), kBlock, 0, c->stream>>>(nc, c->start,
+                                                                              c->ctrl);
+  int s1i = 0;
+  ck(cudaMemcpyAsync(&s1i, c->start + nc, sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+     "D2H count");
+  sync_ctrl(c);
+  const double s1 = static_cast<double>(s1i);
+  const double s2 = static_cast<double>(c->h_ctrl->occ_s2);
   c->occupancy = s1 > 0.0 ? s2 / s1 : 0.0;
   c->build_kind = c->occupancy >= kBuildCellWarpMin ? 6 : 5;
   // sparse cells (short lists, ~12 entries in the KG melt): two gathers in
@@ -1924,26 +1924,7 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
     bg.origin_scale[k] = c->g.cell_len[k];
   }
   bg.nbricks = bg.nb[0] * bg.nb[1] * bg.nb[2];
-  const int d0 = c->g.dims[0], d1 = c->g.dims[1];
-  c->h_rank.assign(static_cast<size_t>(c->g.ncells), 0);
-  c->h_brick_off.assign(static_cast<size_t>(bg.nbricks) + 1, 0);
-  int r = 0;
-  for (int b = 0; b < bg.nbricks; ++b) {
-    const int bx = b % bg.nb[0], by = (b / bg.nb[0]) % bg.nb[1], bz = b / (bg.nb[0] * bg.nb[1]);
-    c->h_brick_off[b] = r;
-    for (int z = bz * bg.B[2]; z < std::min((bz + 1) * bg.B[2], ext[2]); ++z)
-      for (int y = by * bg.B[1]; y < std::min((by + 1) * bg.B[1], ext[1]); ++y)
-        for (int x = bx * bg.B[0]; x < std::min((bx + 1) * bg.B[0], ext[0]); ++x)
-          c->h_rank[static_cast<size_t>(x + d0 * (y + d1 * (z + zoff)))] = r++;
-  }
-  c->h_brick_off[bg.nbricks] = r;
-  if (c->g.zslab) {  // ghost layers ranked after every owned cell, x-fastest
-    const int dxy = d0 * d1;
-    for (int q = 0; q < dxy; ++q) c->h_rank[static_cast<size_t>(q)] = r + q;
-    for (int q = 0; q < dxy; ++q) {
-      c->h_rank[static_cast<size_t>(q + dxy * (c->g.ldz - 1))] = r + dxy + q;
-    }
-  }
+  (void)zoff;  // (the brick-major ranks are filled on the device: k_brick_tables)
   c->ngroups_max = static_cast<int>(n / 32.0) + bg.nbricks + 1;
   // staging capacity: twice the expected halo population, 32-aligned
   const double vol = c->g.L[0] * c->g.L[1] * c->g.L[2];
@@ -1970,24 +1951,20 @@ void setup_bricks(tmd_gpu_ctx* c, double n, double r_verlet) {
   bg.hi2 = std::nextafter(static_cast<float>(rv2 + delta), 1e30f);
 }
 
-// Brick tables to the device (allocated here unless the context's arena
-// already holds them). The copies are stream-ordered on the context stream
-// (pageable sources: staged before the call returns).
+// Brick tables (cell -> brick-major rank, brick -> first rank), filled on the
+// device (allocated here unless the context's arena already holds them).
 void upload_bricks(tmd_gpu_ctx* c) {
   if (!c->cell_rank) {
-    c->cell_rank = dalloc<int>(c->h_rank.size());
-    c->brick_rank_off = dalloc<int>(c->h_brick_off.size());
+    c->cell_rank = dalloc<int>(static_cast<size_t>(c->g.ncells));
+    c->brick_rank_off = dalloc<int>(static_cast<size_t>(c->bg.nbricks) + 1);
     c->scan_tmp = dalloc<int>(static_cast<size_t>(
         blocks_for(std::max(c->g.ncells, c->bg.nbricks), kScanTile) + 1));
   }
-  ck(cudaMemcpyAsync(c->cell_rank, c->h_rank.data(), c->h_rank.size() * sizeof(int),
-                     cudaMemcpyHostToDevice, c->stream), "H2D cell_rank");
-  ck(cudaMemcpyAsync(c->brick_rank_off, c->h_brick_off.data(),
-                     c->h_brick_off.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream),
-     "H2D brick offsets");
+  c->launches += 1;
+  k_brick_tables<<<blocks_for(std::max(c->g.ncells, c->bg.nbricks + 1), kBlock), kBlock, 0,
+                   c->stream>>>(c->g, c->bg, c->cell_rank, c->brick_rank_off);
+  ck(cudaGetLastError(), "k_brick_tables");
   set_smem_attrs(c);
-  c->h_rank.clear();
-  c->h_brick_off.clear();
 }
 
 void build_geom(tmd_gpu_ctx* c, const double box[3], double r_cut,
@@ -2593,8 +2570,8 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       want(c->ctrl, 1);
       want(c->rebuild_log, static_cast<size_t>(kChunk));
       if (c->timers_on) want(c->ticks, static_cast<size_t>(kTickSteps * kTickPhases + 1));
-      want(c->cell_rank, c->h_rank.size());
-      want(c->brick_rank_off, c->h_brick_off.size());
+      want(c->cell_rank, static_cast<size_t>(c->g.ncells));
+      want(c->brick_rank_off, static_cast<size_t>(c->bg.nbricks) + 1);
       want(c->scan_tmp, nscan);
     }
     mark("plan");

@@ -831,6 +831,20 @@ __global__ void __launch_bounds__(kBlock)
   block_partials<kMode, kBlock>(e, w, ke, d2, red, part_e, part_w, it, ctrl);
 }
 
+// Sum of squared cell populations (the particle-weighted cell occupancy that
+// picks the list build): integer sums, so the atomics are exact.
+__global__ void __launch_bounds__(kBlock)
+    k_occupancy(int ncells, const int* __restrict__ start, Ctrl* ctrl) {
+  const int k = blockIdx.x * kBlock + threadIdx.x;
+  unsigned long long m2 = 0;
+  if (k < ncells) {
+    const unsigned long long m = static_cast<unsigned long long>(start[k + 1] - start[k]);
+    m2 = m * m;
+  }
+  for (int o = 16; o > 0; o >>= 1) m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+  if ((threadIdx.x & 31) == 0 && m2) atomicAdd(&ctrl->occ_s2, m2);
+}
+
 // Deterministic final reduction of per-block partials (fixed order tree).
 constexpr int kRedThreads = 1024;
 __global__ void __launch_bounds__(kRedThreads)

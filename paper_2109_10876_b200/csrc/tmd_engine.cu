@@ -2394,14 +2394,36 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       throw;
     }
     mark("validate params");
-    const IdRange idr = id_range(sys);
-    mark("id range");
-    // per-particle checks on the host threads (the exact serial pass only
-    // to name the reference's first error); still before any CUDA call
-    if (!particles_ok_fast(sys, idr)) validate_particles_exact(sys, idr);
-    mark("validate particles");
-    set_type_table(c, sys, idr);
-    mark("type table");
+    // The per-particle checks (id range, then validate_flat's checks on the
+    // host threads; the exact serial pass only to name the reference's first
+    // error) run on a helper thread while the device is set up and the
+    // particle upload is enqueued: joined before anything reads their result,
+    // and before any other error is reported, so a bad particle is still the
+    // ConfigError the reference raises (a failing device init included).
+    IdRange idr;
+    std::exception_ptr verr;
+    std::thread vthread([&] {
+      try {
+        idr = id_range(sys);
+        if (!particles_ok_fast(sys, idr)) validate_particles_exact(sys, idr);
+      } catch (...) {
+        verr = std::current_exception();
+      }
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{vthread};
+    auto join_validation = [&] {
+      if (vthread.joinable()) vthread.join();
+      if (verr) {
+        if (c->stream) cudaStreamSynchronize(c->stream);  // (the upload reads the caller's arrays)
+        std::rethrow_exception(verr);
+      }
+    };
+    try {  // device setup (a particle error found meanwhile takes precedence)
     int ndev = 0;
     ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     mark("device count");
@@ -2434,6 +2456,11 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     ck(cudaEventCreate(&c->t0), "cudaEventCreate");
     ck(cudaEventCreate(&c->t1), "cudaEventCreate");
     mark("device + streams");
+    } catch (...) {
+      join_validation();
+      throw;
+    }
+    if (slab) join_validation();  // (the slab selection reads the particles)
 
     // Slab mode: keep the particles whose wrapped position lies in this
     // rank's z layers (exact host wrap + cell, bit-identical to the device's).
@@ -2623,9 +2650,6 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       // the caller's arrays as they are, unpacked on the device (double4
       // positions, SoA velocities); ids a dense range -> device download
       if (m > 0) {
-        c->ids_dense = static_cast<unsigned long long>(idr.hi - idr.lo) ==
-                       static_cast<unsigned long long>(m - 1);
-        c->dl_lo = idr.lo;
         ck(cudaMemcpyAsync(c->dl, sys->pos, 3 * m * sizeof(double), cudaMemcpyHostToDevice,
                            c->stream), "H2D pos");
         if (sys->vel) {
@@ -2644,6 +2668,13 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
         ck(cudaGetLastError(), "k_upload");
       }
       mark("upload enqueued");
+      join_validation();  // (overlapped with the upload)
+      mark("validated");
+      if (m > 0) {
+        c->ids_dense = static_cast<unsigned long long>(idr.hi - idr.lo) ==
+                       static_cast<unsigned long long>(m - 1);
+        c->dl_lo = idr.lo;
+      }
     } else {
       if (m > 0) {
         k_slab_unpack<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
@@ -2655,6 +2686,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       stage.release();
       mark("upload");
     }
+    set_type_table(c, sys, idr);
     k_set_far<<<1, 1, 0, c->stream>>>(c->posb[0] + n, c->posb[1] + n, far);  // list padding slot
     if (slab) alloc_slab(c);
     if (sys->n_bonds > 0) setup_bonds(c, sys, fene);

@@ -3135,10 +3135,7 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
           c->dl_lo, c->g, pos ? dpos : nullptr, vel ? dvel : nullptr, force ? dfrc : nullptr,
           mass ? dmass : nullptr, did);
       ck(cudaGetLastError(), "k_download");
-      if (ids_out) {
-        ck(cudaMemcpyAsync(ids_out, did, nn * sizeof(long long), cudaMemcpyDeviceToHost,
-                           c->stream), "D2H id");
-      }
+      (void)did;  // (dense ids in id order are lo, lo + 1, ...: written by the host below)
       if (pos) {
         ck(cudaMemcpyAsync(pos, dpos, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream), "D2H pos");
@@ -3154,6 +3151,12 @@ int tmd_gpu_download(tmd_gpu_ctx* c, int64_t* id, double* pos, double* vel,
       if (mass) {
         ck(cudaMemcpyAsync(mass, dmass, nn * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
            "D2H mass");
+      }
+      if (ids_out) {  // while the copies run
+        const long long lo = c->dl_lo;
+        parallel_chunks(static_cast<int64_t>(nn), [&](int, int64_t b, int64_t e) {
+          for (int64_t k = b; k < e; ++k) ids_out[k] = lo + k;
+        });
       }
       ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     } else if (nn > 0) {

@@ -2402,10 +2402,23 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // ConfigError the reference raises (a failing device init included).
     IdRange idr;
     std::exception_ptr verr;
+    bool ids_iota = false;  // ids[k] == lo + k: generated on the device, not uploaded
     std::thread vthread([&] {
       try {
         idr = id_range(sys);
         if (!particles_ok_fast(sys, idr)) validate_particles_exact(sys, idr);
+        if (idr.dense && sys->n > 0) {
+          std::atomic<bool> iota{true};
+          parallel_chunks(sys->n, [&](int, int64_t b, int64_t e) {
+            for (int64_t k = b; k < e; ++k) {
+              if (sys->id[k] != idr.lo + k) {
+                iota = false;
+                return;
+              }
+            }
+          });
+          ids_iota = iota;
+        }
       } catch (...) {
         verr = std::current_exception();
       }
@@ -2660,17 +2673,23 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
           ck(cudaMemcpyAsync(c->dl + 6 * m, sys->mass, m * sizeof(double),
                              cudaMemcpyHostToDevice, c->stream), "H2D mass");
         }
-        ck(cudaMemcpyAsync(c->id, sys->id, m * sizeof(long long), cudaMemcpyHostToDevice,
-                           c->stream), "H2D id");
-        k_upload<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
-            static_cast<int>(m), c->dl, sys->vel ? c->dl + 3 * m : nullptr,
-            sys->mass ? c->dl + 6 * m : nullptr, c->posb[0], c->vx, c->vy, c->vz, c->mass);
-        ck(cudaGetLastError(), "k_upload");
       }
       mark("upload enqueued");
       join_validation();  // (overlapped with the upload)
       mark("validated");
       if (m > 0) {
+        if (ids_iota) {  // ids lo, lo + 1, ... in input order: no 8 B per particle over PCIe
+          c->launches += 1;
+          k_iota_i64<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
+              static_cast<int>(m), idr.lo, c->id);
+        } else {
+          ck(cudaMemcpyAsync(c->id, sys->id, m * sizeof(long long), cudaMemcpyHostToDevice,
+                             c->stream), "H2D id");
+        }
+        k_upload<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
+            static_cast<int>(m), c->dl, sys->vel ? c->dl + 3 * m : nullptr,
+            sys->mass ? c->dl + 6 * m : nullptr, c->posb[0], c->vx, c->vy, c->vz, c->mass);
+        ck(cudaGetLastError(), "k_upload");
         c->ids_dense = static_cast<unsigned long long>(idr.hi - idr.lo) ==
                        static_cast<unsigned long long>(m - 1);
         c->dl_lo = idr.lo;

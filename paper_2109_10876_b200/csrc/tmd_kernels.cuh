@@ -971,6 +971,11 @@ __global__ void __launch_bounds__(kBlock)
   oid[r] = id[k];
 }
 
+__global__ void k_iota_i64(int n, long long lo, long long* __restrict__ v) {
+  const int r = blockIdx.x * kBlock + threadIdx.x;
+  if (r < n) v[r] = lo + r;
+}
+
 __global__ void k_iota_int(int n, int* __restrict__ v) {
   const int r = blockIdx.x * kBlock + threadIdx.x;
   if (r < n) v[r] = r;

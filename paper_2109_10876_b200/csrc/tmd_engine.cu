@@ -375,6 +375,7 @@ struct tmd_gpu_ctx {
   Ctrl* h_ctrl = nullptr;      // pinned mirror
   Ctrl* h_ctrl_cyc = nullptr;  // pinned status snapshots of speculative cycles [4]
   cudaEvent_t ev_cyc[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_up[2] = {nullptr, nullptr};  // create(): positions copied / velocities copied
   double* h_scalars = nullptr; // pinned
 
   // chunk checkpoint (rollback on list overflow)
@@ -509,6 +510,9 @@ void free_all(tmd_gpu_ctx* c) {
   pinned_small_free(c->h_ctrl, sizeof(Ctrl));
   pinned_small_free(c->h_ctrl_cyc, 4 * sizeof(Ctrl));
   for (cudaEvent_t e : c->ev_cyc) {
+    if (e) cudaEventDestroy(e);
+  }
+  for (cudaEvent_t e : c->ev_up) {
     if (e) cudaEventDestroy(e);
   }
   pinned_small_free(c->obs_host, sizeof(double) * 4 * kObsRowsAlloc);
@@ -2403,6 +2407,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     IdRange idr;
     std::exception_ptr verr;
     bool ids_iota = false;  // ids[k] == lo + k: generated on the device, not uploaded
+    bool defer_vm = false;  // velocities / masses placed after the setup pass
     std::thread vthread([&] {
       try {
         idr = id_range(sys);
@@ -2432,7 +2437,9 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     auto join_validation = [&] {
       if (vthread.joinable()) vthread.join();
       if (verr) {
-        if (c->stream) cudaStreamSynchronize(c->stream);  // (the upload reads the caller's arrays)
+        // (the upload reads the caller's arrays)
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        if (c->side) cudaStreamSynchronize(c->side);
         std::rethrow_exception(verr);
       }
     };
@@ -2662,17 +2669,27 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     if (!slab) {
       // the caller's arrays as they are, unpacked on the device (double4
       // positions, SoA velocities); ids a dense range -> device download
+      // positions first on the context stream; velocities and masses behind
+      // them on the side stream (one copy at a time over PCIe), so that with
+      // ids lo, lo + 1, ... in input order they arrive while the setup pass
+      // (resort, list build, first forces — none of which reads them) runs
+      // and are placed by id afterwards
       if (m > 0) {
         ck(cudaMemcpyAsync(c->dl, sys->pos, 3 * m * sizeof(double), cudaMemcpyHostToDevice,
                            c->stream), "H2D pos");
+        ck(cudaEventCreateWithFlags(&c->ev_up[0], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&c->ev_up[1], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(c->ev_up[0], c->stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->side, c->ev_up[0], 0), "cudaStreamWaitEvent");
         if (sys->vel) {
           ck(cudaMemcpyAsync(c->dl + 3 * m, sys->vel, 3 * m * sizeof(double),
-                             cudaMemcpyHostToDevice, c->stream), "H2D vel");
+                             cudaMemcpyHostToDevice, c->side), "H2D vel");
         }
         if (sys->mass) {
           ck(cudaMemcpyAsync(c->dl + 6 * m, sys->mass, m * sizeof(double),
-                             cudaMemcpyHostToDevice, c->stream), "H2D mass");
+                             cudaMemcpyHostToDevice, c->side), "H2D mass");
         }
+        ck(cudaEventRecord(c->ev_up[1], c->side), "cudaEventRecord");
       }
       mark("upload enqueued");
       join_validation();  // (overlapped with the upload)
@@ -2686,9 +2703,14 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
           ck(cudaMemcpyAsync(c->id, sys->id, m * sizeof(long long), cudaMemcpyHostToDevice,
                              c->stream), "H2D id");
         }
+        // (the Langevin bath's first force reads velocities and masses)
+        defer_vm = ids_iota && !c->th.on && (sys->vel || sys->mass);
+        if (!defer_vm) ck(cudaStreamWaitEvent(c->stream, c->ev_up[1], 0), "cudaStreamWaitEvent");
         k_upload<<<blocks_for(static_cast<int64_t>(m), kBlock), kBlock, 0, c->stream>>>(
-            static_cast<int>(m), c->dl, sys->vel ? c->dl + 3 * m : nullptr,
-            sys->mass ? c->dl + 6 * m : nullptr, c->posb[0], c->vx, c->vy, c->vz, c->mass);
+            static_cast<int>(m), c->dl,
+            (sys->vel && !defer_vm) ? c->dl + 3 * m : nullptr,
+            (sys->mass && !defer_vm) ? c->dl + 6 * m : nullptr, c->posb[0], c->vx, c->vy, c->vz,
+            c->mass);
         ck(cudaGetLastError(), "k_upload");
         c->ids_dense = static_cast<unsigned long long>(idr.hi - idr.lo) ==
                        static_cast<unsigned long long>(m - 1);
@@ -2727,6 +2749,14 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
     // first migration/ghost exchange (tmd_gpu_slab_*); whole box: now
     mark("list alloc");
     if (!slab) setup_pass(c);
+    if (defer_vm) {  // velocities / masses placed by id into the slots the setup pass chose
+      ck(cudaStreamWaitEvent(c->stream, c->ev_up[1], 0), "cudaStreamWaitEvent");
+      c->launches += 1;
+      k_place_vm<<<blocks_for(c->n, kBlock), kBlock, 0, c->stream>>>(
+          static_cast<int>(c->n), c->id, c->dl_lo, sys->vel ? c->dl + 3 * c->n : nullptr,
+          sys->mass ? c->dl + 6 * c->n : nullptr, c->vx, c->vy, c->vz, c->mass);
+      ck(cudaGetLastError(), "k_place_vm");
+    }
     mark("setup pass");
     c->step = 0;
     c->rebuilds = 0;

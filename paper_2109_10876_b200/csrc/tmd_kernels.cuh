@@ -971,6 +971,24 @@ __global__ void __launch_bounds__(kBlock)
   oid[r] = id[k];
 }
 
+// Velocities and masses of a system uploaded in id order (ids lo, lo + 1, ...
+// in input order) placed into the slots the first resort chose.
+__global__ void __launch_bounds__(kBlock)
+    k_place_vm(int n, const long long* __restrict__ id, long long lo,
+               const double* __restrict__ v3, const double* __restrict__ m1,
+               double* __restrict__ vx, double* __restrict__ vy, double* __restrict__ vz,
+               double* __restrict__ mass) {
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  if (s >= n) return;
+  const long long r = id[s] - lo;
+  if (v3) {
+    vx[s] = v3[3 * r];
+    vy[s] = v3[3 * r + 1];
+    vz[s] = v3[3 * r + 2];
+  }
+  if (m1) mass[s] = m1[r];
+}
+
 __global__ void k_iota_i64(int n, long long lo, long long* __restrict__ v) {
   const int r = blockIdx.x * kBlock + threadIdx.x;
   if (r < n) v[r] = lo + r;

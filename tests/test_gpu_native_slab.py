@@ -262,3 +262,29 @@ def test_native_slab_rounding_band_far_from_origin(ref, seed):
         np.testing.assert_array_equal(eng.local_pairs(), want)
     finally:
         eng.close()
+
+
+def test_native_loop_matches_single_context_1m_r8():
+    """configs[1] (1,048,576 particles) as 8 slabs on one GPU against the
+    single context: the same pair set, the same rebuild steps, energies to
+    1e-10 and forces to 1e-8 after 60 steps of the melting lattice."""
+    flat = E.gen_fcc(64, 0.8442, 1.0, 12345)
+    cfg = E.EngineConfig(dt=0.005, section_timers=False)
+    one = E.Engine(flat, E.Interactions(), 0.3, cfg)
+    dec = DecomposedEngine(flat, E.Interactions(), 0.3, cfg, comm=InProcessComm(8), native=True)
+    try:
+        np.testing.assert_array_equal(dec.local_pairs(), one.pairs())
+        one.run(60)
+        dec.run(60)
+        o1, o2 = one.observe(), dec.observe()
+        assert_rel(o2.potential, o1.potential, 1e-10, "PE")
+        assert_rel(o2.kinetic, o1.kinetic, 1e-10, "KE")
+        assert dec.rebuild_count() == one.rebuild_count() > 0
+        ids, pos, vel, f = dec.local_state()
+        ids1, f1 = one.forces()
+        np.testing.assert_array_equal(ids, ids1)
+        assert_forces_close(f, f1, rtol=1e-8)
+        np.testing.assert_array_equal(dec.local_pairs(), one.pairs())
+    finally:
+        dec.close()
+        one.close()

@@ -213,11 +213,29 @@ double4* peer_buffer(tmd_gpu_ctx* c, const PeerInfo& p, int peer, int b) {
   return static_cast<double4*>(ptr);
 }
 
+// A rank that cannot export or map a position buffer (no peer access between
+// two GPUs, IPC disabled in a container, ...) must not leave the others in a
+// collective: every rank finishes the exchange, the failures are MAX-reduced,
+// and if any rank failed all of them drop to the message halo (pack + one
+// point-to-point group per step) for the rest of the run — same trajectories,
+// no peer stores. TMD_HALO_STRICT=1 turns the fallback into the error (the
+// tests set it, so a silently degraded path cannot pass them);
+// TMD_HALO_FAIL_INJECT=<rank> makes that rank's mapping fail (test hook).
+bool env_is(const char* name, const char* v) {
+  const char* e = std::getenv(name);
+  return e && std::strcmp(e, v) == 0;
+}
+
 void nccl_publish_ghosts(tmd_gpu_ctx* c) {
   const int R = c->nranks, r = c->my_rank;
   PeerInfo me{};
+  std::string fail_why;
   for (int b = 0; b < 2; ++b) {
-    ck(cudaIpcGetMemHandle(&me.h[b], c->posb[b]), "cudaIpcGetMemHandle");
+    const cudaError_t e = cudaIpcGetMemHandle(&me.h[b], c->posb[b]);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail_why = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+    }
     me.base[b] = reinterpret_cast<unsigned long long>(c->posb[b]);
   }
   me.pid = static_cast<long long>(getpid());
@@ -225,27 +243,63 @@ void nccl_publish_ghosts(tmd_gpu_ctx* c) {
   me.ghost_hi_off = c->n + c->n_ghost_lo;
   me.gen = c->ipc_gen;
   me.device = c->device;
+  static_assert(sizeof(PeerInfo) % 8 == 0, "the failure word follows the table, 8-aligned");
   const size_t sz = sizeof(PeerInfo);
-  char* d = dalloc<char>(sz * (static_cast<size_t>(R) + 1));
+  char* d = dalloc<char>(sz * (static_cast<size_t>(R) + 1) + sizeof(int64_t));
+  int64_t* d_fail = reinterpret_cast<int64_t*>(d + sz * (static_cast<size_t>(R) + 1));
   ck(cudaMemcpyAsync(d, &me, sz, cudaMemcpyHostToDevice, c->stream), "H2D peer info");
   comm(c)->allgather(d, d + sz, sz, c->stream);
   std::vector<PeerInfo> all(static_cast<size_t>(R));
   ck(cudaMemcpyAsync(all.data(), d + sz, sz * R, cudaMemcpyDeviceToHost, c->stream),
      "D2H peer info");
   ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-  cudaFree(d);
   // some rank's buffers moved (the only reason for a new exchange): close
   // every mapping and open what the new layout needs — a reallocated buffer
   // may even come back under the old handle's bytes, so none is reused
   for (auto& e : c->ipc_open) cudaIpcCloseMemHandle(e.second);
   c->ipc_open.clear();
   const int lo = (r - 1 + R) % R, hi = (r + 1) % R;
-  for (int b = 0; b < 2; ++b) {
-    // my lowest layer -> lo's upper ghost; my highest layer -> hi's lower ghost
-    c->peer_base[0][b] = peer_buffer(c, all[static_cast<size_t>(lo)], lo, b);
-    c->peer_base[1][b] = peer_buffer(c, all[static_cast<size_t>(hi)], hi, b);
-    c->rg[0][b] = c->peer_base[0][b] + all[static_cast<size_t>(lo)].ghost_hi_off;
-    c->rg[1][b] = c->peer_base[1][b] + all[static_cast<size_t>(hi)].ghost_lo_off;
+  if (fail_why.empty()) {
+    try {
+      if (R > 1 && env_is("TMD_HALO_FAIL_INJECT", std::to_string(r).c_str())) {
+        throw CudaFail{"mapping failure injected (TMD_HALO_FAIL_INJECT)"};
+      }
+      for (int b = 0; b < 2; ++b) {
+        // my lowest layer -> lo's upper ghost; my highest layer -> hi's lower ghost
+        c->peer_base[0][b] = peer_buffer(c, all[static_cast<size_t>(lo)], lo, b);
+        c->peer_base[1][b] = peer_buffer(c, all[static_cast<size_t>(hi)], hi, b);
+        c->rg[0][b] = c->peer_base[0][b] + all[static_cast<size_t>(lo)].ghost_hi_off;
+        c->rg[1][b] = c->peer_base[1][b] + all[static_cast<size_t>(hi)].ghost_lo_off;
+      }
+    } catch (const CudaFail& f) {
+      fail_why = f.what;
+    }
+  }
+  // agree on the outcome: any failure anywhere turns the fused halo off everywhere
+  const int64_t mine = fail_why.empty() ? 0 : 1;
+  int64_t any = 0;
+  ck(cudaMemcpyAsync(d_fail, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream), "H2D flag");
+  comm(c)->allreduce(d_fail, 1, CType::kI64, COp::kMax, c->stream);
+  ck(cudaMemcpyAsync(&any, d_fail, sizeof any, cudaMemcpyDeviceToHost, c->stream), "D2H flag");
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  cudaFree(d);
+  if (any) {
+    for (auto& e : c->ipc_open) cudaIpcCloseMemHandle(e.second);
+    c->ipc_open.clear();
+    c->peer_gen.clear();
+    if (env_is("TMD_HALO_STRICT", "1")) {
+      throw CudaFail{"fused halo unavailable" +
+                     (mine ? ": " + fail_why : std::string(" (a peer rank could not map a buffer)"))};
+    }
+    if (mine || r == 0) {
+      std::fprintf(stderr,
+                   "[tmd_gpu] rank %d: fused peer-store halo unavailable%s%s; every rank uses the "
+                   "message halo (pack + point-to-point) from here on\n",
+                   r, mine ? ": " : "", mine ? fail_why.c_str() : "");
+    }
+    c->fused_halo = false;
+    c->fused_ready = false;
+    return;
   }
   c->peer_gen.assign(static_cast<size_t>(R), 0);
   for (int q = 0; q < R; ++q) c->peer_gen[static_cast<size_t>(q)] = static_cast<int>(all[static_cast<size_t>(q)].gen);

@@ -2,10 +2,16 @@
 else runs on the CPU (the oracle, host logic, ABI symbol checks)."""
 from __future__ import annotations
 
+import os
 import sys
 from pathlib import Path
 
 import pytest
+
+# the native slab loop falls back to the message halo when a rank cannot map a
+# peer's buffers; under test that is an error, so the fused path cannot
+# silently degrade (tmd_slab_nccl.cuh, nccl_publish_ghosts)
+os.environ.setdefault("TMD_HALO_STRICT", "1")
 
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:

@@ -233,6 +233,34 @@ def test_local_state_into_caller_buffers():
         eng.close()
 
 
+@pytest.mark.parametrize("bad", [0, 2])
+def test_fused_halo_falls_back_when_a_rank_cannot_map_its_peers(bad, monkeypatch, capfd):
+    """One rank fails to map a neighbour's position buffers (injected): every
+    rank agrees to use the message halo, and the run is bitwise the
+    halo="nccl" run (same rebuild steps, same states). With
+    TMD_HALO_STRICT=1 (the test suite's default) the same failure raises."""
+    g = load("fcc8_jit")
+    monkeypatch.setenv("TMD_HALO_FAIL_INJECT", str(bad))
+    with pytest.raises(E.CudaError, match="fused halo unavailable"):
+        native(g, 3, "fused")
+    monkeypatch.setenv("TMD_HALO_STRICT", "0")
+    a = native(g, 3, "fused")
+    monkeypatch.delenv("TMD_HALO_FAIL_INJECT")
+    b = native(g, 3, "nccl")
+    try:
+        err = capfd.readouterr().err
+        assert "fused peer-store halo unavailable" in err and f"rank {bad}" in err
+        for k in (1, 9, 30):
+            a.run(k)
+            b.run(k)
+            for x, y in zip(a.local_state(), b.local_state()):
+                np.testing.assert_array_equal(x, y)
+            assert a.rebuild_count() == b.rebuild_count()
+    finally:
+        a.close()
+        b.close()
+
+
 def _planted_far_slab(seed, n_pairs=400, L=200.0, rv=2.8):
     """Pairs planted at |r - r_v| of a few ulps in a large box, all in its
     upper half (the slabs of the high ranks) and many along z: the FP32

@@ -47,6 +47,7 @@ import socket
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 from pathlib import Path
@@ -610,9 +611,12 @@ def run_decomposed(args) -> None:
     from paper_2109_10876_b200.decomp import DecomposedEngine, TorchDistComm
 
     ws, rank, local = dist_env()
-    if args.dist_backend == "gloo":
-        # pipeline check on a one-GPU box: every rank on GPU 0, buffers staged
-        # through host memory (the numbers are not a scaling measurement)
+    if args.dist_backend in ("gloo", "hostfile"):
+        # pipeline checks on a one-GPU box, every rank on GPU 0 (the numbers are
+        # not a scaling measurement). gloo: the Python protocol, buffers staged
+        # through host memory. hostfile: the production C++ loop, one process
+        # per rank, collectives through a shared file mapping, the fused halo
+        # through CUDA IPC mappings of the other processes' buffers.
         local = 0
         torch.cuda.set_device(0)
         dist.init_process_group("gloo")
@@ -629,10 +633,34 @@ def run_decomposed(args) -> None:
 
     # the C++ step loop with NCCL on the context stream (tmd_slab_nccl.cuh);
     # the Python protocol for the gloo pipeline check
-    native = args.dist_backend == "nccl"
+    native = args.dist_backend != "gloo"
+    made = [0]
+
+    def transport():
+        if args.dist_backend != "hostfile":
+            return TorchDistComm()
+        from paper_2109_10876_b200.decomp import HostFileComm
+
+        class HostFileBenchComm(HostFileComm):
+            """+ the host-side sum run_observed reduces its table with, over
+            the job's gloo group (the transport itself is device-stream only)."""
+
+            def allreduce_sum(self, vals):
+                t = torch.from_numpy(np.sum(list(vals.values()), axis=0).astype(np.float64))
+                dist.all_reduce(t)
+                return t.numpy()
+
+        # a fresh mapping per engine, named by the job's rendezvous port
+        made[0] += 1
+        path = os.path.join(tempfile.gettempdir(),
+                            f"tmd_bench_{os.environ.get('MASTER_PORT', '0')}_{made[0]}.bin")
+        if rank == 0 and os.path.exists(path):
+            os.unlink(path)
+        dist.barrier()
+        return HostFileBenchComm(path, rank, ws)
 
     def make():
-        return DecomposedEngine(flat, inter, w.r_skin, ecfg, comm=TorchDistComm(),
+        return DecomposedEngine(flat, inter, w.r_skin, ecfg, comm=transport(),
                                 device_of=lambda r: local, balance=balance, native=native)
 
     def max_over_ranks(x: float) -> float:
@@ -673,7 +701,8 @@ def run_decomposed(args) -> None:
     out = (torch.empty(n, dtype=torch.int64, pin_memory=True).numpy(),
            torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy(),
            torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy())
-    e2_make = lambda: DecomposedEngine(flat_in, inter, w.r_skin, ecfg, comm=TorchDistComm(),  # noqa: E731
+    e2_comm = transport()
+    e2_make = lambda: DecomposedEngine(flat_in, inter, w.r_skin, ecfg, comm=e2_comm,  # noqa: E731
                                        device_of=lambda r: local, balance=balance, native=native)
     torch.cuda.synchronize()
     dist.barrier()
@@ -772,8 +801,10 @@ def main(argv=None):
     ap.add_argument("--decomposed", action="store_true",
                     help="run the slab decomposition even at N = 1 (under torchrun): the "
                          "single slab exchanges its halo with itself over NCCL")
-    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
-                    help="N > 1 only; gloo = pipeline check with every rank on GPU 0")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo", "hostfile"], default="nccl",
+                    help="N > 1 only; gloo / hostfile = pipeline checks with every rank on "
+                         "GPU 0 (Python protocol / the native C++ loop over the host-staged "
+                         "transport with CUDA IPC halo)")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--make-kg-input", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args(argv)

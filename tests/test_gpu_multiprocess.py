@@ -114,3 +114,23 @@ def test_native_loop_one_process_per_rank(tmp_path, name, R, halo, balance):
         np.testing.assert_array_equal(vel1, vel)
     finally:
         one.close()
+
+
+def test_bench_launches_n_ranks_through_the_native_loop(tmp_path):
+    """`bench.py --gpus 2` re-launches itself under torchrun; with
+    --dist-backend hostfile both ranks share GPU 0 and run the production C++
+    loop as separate processes (fused halo over CUDA IPC), so the N > 1 arm of
+    the bench — launch, slab engines, device timing, the e2e leg — is
+    exercised on a one-GPU box. The line must carry the rank count."""
+    import json
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dist-backend",
+                        "hostfile", "--cells", "20", "--steps", "30", "--warmup", "5"],
+                       env=env, cwd=str(tmp_path), capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["steps"] == 30 and line["value"] > 0
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    assert "native C++ step loop" in line["details"]["parallelism"]
+    assert line["details"]["rank0_slab"]["nranks"] == 2
+    assert 0 < line["details"]["rank0_slab"]["n_own"] < 32000

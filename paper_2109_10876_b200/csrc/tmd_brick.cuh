@@ -907,21 +907,45 @@ __global__ void __launch_bounds__(kBuildThreads, 3)
 #define TMD_BUILD_THREAD_BATCH 2
 #endif
 constexpr int kBuildThreadBatch = TMD_BUILD_THREAD_BATCH;
+#ifndef TMD_BUILD_THREAD_SLOTS
+#define TMD_BUILD_THREAD_SLOTS 24
+#endif
+constexpr int kBuildThreadSlots = TMD_BUILD_THREAD_SLOTS;  // a multiple of 8
 __global__ void __launch_bounds__(kBlock)
     k_build_thread(int n, const double4* __restrict__ pos, const int* __restrict__ cell,
                    const int* __restrict__ start, const int* __restrict__ cell_rank, Geom g,
                    uint32_t* __restrict__ list, int* __restrict__ nnbr, int cap,
                    double4* __restrict__ snap, uint32_t sentinel, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
-  __shared__ __align__(16) uint32_t s_buf[8][kBlock];
+  // kBuildThreadSlots entries per thread wait in shared memory (one more row
+  // takes the store of a miss): a sparse system's ~12 entries per particle
+  // then leave together at the end, lanes side by side, instead of chunk by
+  // chunk from inside the divergent hit branch
+  __shared__ __align__(16) uint32_t s_buf[kBuildThreadSlots + 1][kBlock];
   __shared__ double red[kBlock / 32];
   const int i = blockIdx.x * kBlock + threadIdx.x;
   const int t = threadIdx.x;
   int cnt = 0;
+  int base = 0;  // entries already written to the list (a multiple of 8)
   if (i < n) {
     const double4 pi = pos[i];
     snap[i] = pi;
     const size_t row = list_slot(i >> 5, cap, i & 31, 0);
+    // chunks 0..nch-1 of the buffer become list chunks base/8 .. (capacity permitting)
+    auto flush_chunks = [&](int nch) {
+      for (int k = 0; k < nch; ++k) {
+        const int c8 = (base >> 3) + k;
+        if (c8 * 8 >= cap) break;
+        uint4 a, b;
+        a.x = s_buf[8 * k + 0][t]; a.y = s_buf[8 * k + 1][t];
+        a.z = s_buf[8 * k + 2][t]; a.w = s_buf[8 * k + 3][t];
+        b.x = s_buf[8 * k + 4][t]; b.y = s_buf[8 * k + 5][t];
+        b.z = s_buf[8 * k + 6][t]; b.w = s_buf[8 * k + 7][t];
+        uint4* dst = reinterpret_cast<uint4*>(list + row + static_cast<size_t>(c8) * 256);
+        dst[0] = a;
+        dst[1] = b;
+      }
+    };
     const int c = cell[i];  // global cell at the last resort
     const int dxy = g.dims[0] * g.dims[1];
     const int cx = c % g.dims[0];
@@ -1001,30 +1025,22 @@ __global__ void __launch_bounds__(kBlock)
             const uint32_t ent = en[u];
             double dx, dy, dz;
             pair_delta(pi, pj[u], ent, g, dx, dy, dz);
-            if (static_cast<int>(ent & kIdxMask) != i && exact_r2(dx, dy, dz) <= g.rv2) {
-              s_buf[cnt & 7][t] = ent;
-              if ((cnt & 7) == 7 && cnt < cap) {
-                uint4 a, b;
-                a.x = s_buf[0][t]; a.y = s_buf[1][t]; a.z = s_buf[2][t]; a.w = s_buf[3][t];
-                b.x = s_buf[4][t]; b.y = s_buf[5][t]; b.z = s_buf[6][t]; b.w = s_buf[7][t];
-                uint4* dst = reinterpret_cast<uint4*>(list + row + (cnt >> 3) * 256);
-                dst[0] = a;
-                dst[1] = b;
-              }
-              ++cnt;
+            const bool hit =
+                static_cast<int>(ent & kIdxMask) != i && exact_r2(dx, dy, dz) <= g.rv2;
+            s_buf[cnt - base][t] = ent;  // (a miss is overwritten by the next store)
+            cnt += hit ? 1 : 0;
+            if (cnt - base == kBuildThreadSlots) {  // buffer full (dense neighbourhoods only)
+              flush_chunks(kBuildThreadSlots / 8);
+              base = cnt;
             }
           }
         }
       }
     }
-    if ((cnt & 7) != 0 && cnt < cap) {  // sentinel-pad and flush the last chunk
-      for (int r = cnt & 7; r < 8; ++r) s_buf[r][t] = sentinel;
-      uint4 a, b;
-      a.x = s_buf[0][t]; a.y = s_buf[1][t]; a.z = s_buf[2][t]; a.w = s_buf[3][t];
-      b.x = s_buf[4][t]; b.y = s_buf[5][t]; b.z = s_buf[6][t]; b.w = s_buf[7][t];
-      uint4* dst = reinterpret_cast<uint4*>(list + row + (cnt >> 3) * 256);
-      dst[0] = a;
-      dst[1] = b;
+    {  // the waiting entries: whole chunks, then the sentinel-padded last one
+      const int rem = cnt - base;
+      for (int r = rem; r < ((rem + 7) & ~7); ++r) s_buf[r][t] = sentinel;
+      flush_chunks((rem + 7) >> 3);
     }
     nnbr[i] = cnt < cap ? cnt : cap;
     if (cnt > cap) atomicOr(&ctrl->status, kStatOverflow);

@@ -917,11 +917,11 @@ __global__ void __launch_bounds__(kBlock)
                    uint32_t* __restrict__ list, int* __restrict__ nnbr, int cap,
                    double4* __restrict__ snap, uint32_t sentinel, Ctrl* ctrl) {
   if (!ctrl->rebuild) return;
-  // kBuildThreadSlots entries per thread wait in shared memory (one more row
-  // takes the store of a miss): a sparse system's ~12 entries per particle
+  // kBuildThreadSlots entries per thread wait in shared memory (a batch more
+  // rows take the stores of a batch that fills it): a sparse system's ~12 entries per particle
   // then leave together at the end, lanes side by side, instead of chunk by
   // chunk from inside the divergent hit branch
-  __shared__ __align__(16) uint32_t s_buf[kBuildThreadSlots + 1][kBlock];
+  __shared__ __align__(16) uint32_t s_buf[kBuildThreadSlots + kBuildThreadBatch][kBlock];
   __shared__ double red[kBlock / 32];
   const int i = blockIdx.x * kBlock + threadIdx.x;
   const int t = threadIdx.x;
@@ -1019,20 +1019,28 @@ __global__ void __launch_bounds__(kBlock)
             en[u] = static_cast<uint32_t>(j) | (s2 ? tg[2] : (s1 ? tg[1] : tg[0]));
             pj[u] = ldg_pos256(pos + j);
           }
+          // every candidate of the batch is decided before any is appended:
+          // the FP64 chains are independent and interleave
+          bool hit[kBuildThreadBatch];
 #pragma unroll
           for (int u = 0; u < kBuildThreadBatch; ++u) {
-            if (q0 + u >= nt) break;
-            const uint32_t ent = en[u];
             double dx, dy, dz;
-            pair_delta(pi, pj[u], ent, g, dx, dy, dz);
-            const bool hit =
-                static_cast<int>(ent & kIdxMask) != i && exact_r2(dx, dy, dz) <= g.rv2;
-            s_buf[cnt - base][t] = ent;  // (a miss is overwritten by the next store)
-            cnt += hit ? 1 : 0;
-            if (cnt - base == kBuildThreadSlots) {  // buffer full (dense neighbourhoods only)
-              flush_chunks(kBuildThreadSlots / 8);
-              base = cnt;
+            pair_delta(pi, pj[u], en[u], g, dx, dy, dz);
+            const bool in = exact_r2(dx, dy, dz) <= g.rv2;
+            hit[u] = (q0 + u < nt) & (static_cast<int>(en[u] & kIdxMask) != i) & in;
+          }
+#pragma unroll
+          for (int u = 0; u < kBuildThreadBatch; ++u) {
+            s_buf[cnt - base][t] = en[u];  // (a miss is overwritten by the next store)
+            cnt += hit[u] ? 1 : 0;
+          }
+          if (cnt - base >= kBuildThreadSlots) {  // buffer full (dense neighbourhoods only)
+            flush_chunks(kBuildThreadSlots / 8);
+#pragma unroll
+            for (int u = 0; u + 1 < kBuildThreadBatch; ++u) {  // entries past the flushed chunks
+              if (cnt - base > kBuildThreadSlots + u) s_buf[u][t] = s_buf[kBuildThreadSlots + u][t];
             }
+            base += kBuildThreadSlots;
           }
         }
       }

@@ -1267,6 +1267,43 @@ inline size_t staged_smem_bytes(int stage_cap) {
 constexpr size_t kStagedSmemMax = 200 * 1024;
 
 // ---------------------------------------------------------------------------
+// The epilogue's per-particle operands (velocities, mass, snapshot, bond
+// table) stream from DRAM once per step and are first touched after the list
+// loop: requested into L2 at the top of the kernel their latency runs under
+// the gathers instead of after them. Matters where a thread's list is short
+// (the Kremer-Grest melt: ~12 entries, the kernel waits on loads half the
+// time); a long list hides it anyway. (The small-system kernel
+// k_forces_lanes works out of L2: the same prefetches measured no gain.)
+#ifndef TMD_FORCE_PREFETCH
+#define TMD_FORCE_PREFETCH 1
+#endif
+#ifndef TMD_LIST_PREFETCH
+#define TMD_LIST_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_line(const void* p) {
+#if TMD_FORCE_PREFETCH == 2
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#elif TMD_FORCE_PREFETCH == 1
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#else
+  (void)p;
+#endif
+}
+template <int kMode>
+__device__ __forceinline__ void prefetch_epilogue(int i, const Integ& it) {
+  if (kMode == kForcesOnly) return;
+  prefetch_line(it.vx + i);
+  prefetch_line(it.vy + i);
+  prefetch_line(it.vz + i);
+  prefetch_line(it.mass + i);
+  if (kMode == kFused) prefetch_line(it.snap + i);
+  if (it.bt.on) {
+    prefetch_line(it.bt.cnt + i);
+    prefetch_line(it.bt.ent + static_cast<size_t>(i) * kMaxBonds);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Variant 3: thread per particle over the sector-chunked list with GLOBAL
 // slots (groups = 32 consecutive particles of the brick-major order). Each
 // chunk of 8 entries is two 16-B loads; each gather is one 256-bit
@@ -1292,9 +1329,15 @@ __global__ void __launch_bounds__(128)
     const double4 pi = pos[i];
     const int cnt = nnbr[i];
     const uint32_t* row = list + list_slot(i >> 5, cap, i & 31, 0);
+    prefetch_epilogue<kMode>(i, it);
     double ax = 0.0, ay = 0.0, az = 0.0;
     bool zero = false;
     for (int c0 = 0; c0 < cnt; c0 += 8) {
+      // the next chunk of the list into L2 while this one is worked on: the
+      // list streams from DRAM, and a chunk's load would otherwise wait for
+      // it right before its gathers (16.4M: 4.02 -> 3.89 ms; two chunks
+      // ahead, or into L1, measured no better)
+      if (TMD_LIST_PREFETCH && c0 + 8 < cnt) prefetch_line(row + (c0 + 8) * 32);
       const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32));
       const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c0 * 32 + 4));
       const uint32_t ents[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};

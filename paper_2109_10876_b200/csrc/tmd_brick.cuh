@@ -1297,6 +1297,7 @@ __device__ __forceinline__ void prefetch_epilogue(int i, const Integ& it) {
   prefetch_line(it.vz + i);
   prefetch_line(it.mass + i);
   if (kMode == kFused) prefetch_line(it.snap + i);
+  if (kMode == kFused && it.exp) prefetch_line(it.exp + i);  // fused halo's export map
   if (it.bt.on) {
     prefetch_line(it.bt.cnt + i);
     prefetch_line(it.bt.ent + static_cast<size_t>(i) * kMaxBonds);

@@ -305,7 +305,7 @@ struct tmd_gpu_ctx {
 
   // brick-major ordering + variant selection
   int variant = 2;            // 1: thread-per-particle ELL + L1 gathers; 2: brick-staged
-  int unroll = 4;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
+  int unroll = 1;             // variant 3: gathers in flight per thread (1, 2, 4, 8)
   bool unroll_auto = true;    // unroll chosen with the build kind (sparse cells: 2)
   int lanes = 1;              // variant 3: threads per particle (1, 2, 4, 8)
   bool lanes_auto = true;     // lanes chosen from the particle count at create
@@ -1000,7 +1000,11 @@ void choose_build_kind(tmd_gpu_ctx* c) {
   // sparse cells (short lists, ~12 entries in the KG melt): two gathers in
   // flight per thread beat four (KG force kernel 0.281 vs 0.307 ms at 4M,
   // scripts/kg_probe.py; fewer registers, more resident warps)
-  if (c->unroll_auto) c->unroll = c->build_kind == 5 ? 2 : 4;
+  // dense cells: one gather at a time since the list's next chunk is
+  // prefetched into L2 (fewer registers, more resident warps; 16.4M: 3.82 ms
+  // against 3.83 / 3.88 with two / four in flight, 442K: 0.126 / 0.129 / 0.136;
+  // scripts/unroll_probe.py) — four were best before the prefetches
+  if (c->unroll_auto) c->unroll = c->build_kind == 5 ? 2 : 1;
   c->build_auto = false;
   c->graph_dirty = true;
 }
@@ -2531,7 +2535,7 @@ int create_impl(const tmd_system* sys, const tmd_lj_params* lj, const tmd_fene_p
       if (slab) throw StatusError{TMD_ERR_CONFIG, "force cap: single-GPU warm-up only"};
       c->variant = 1;  // the capped pair force lives in the thread-per-particle kernel
     }
-    c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 4;
+    c->unroll = params->reserved[1] > 0 ? params->reserved[1] : 1;
     c->unroll_auto = params->reserved[1] <= 0;
     {
       const int l = params->reserved[4];

@@ -145,7 +145,7 @@ class EngineConfig:
     # particle count, more lanes for small systems)
     lanes: int = 0
     # variant-3 force kernel: neighbour gathers in flight per thread (1, 2, 4,
-    # 8; 0 = 4)
+    # 8; 0 = by cell occupancy: 1 for dense cells, 2 for sparse ones)
     unroll: int = 0
     # > 0: cap each LJ pair force at this magnitude (overlap warm-up of a fresh
     # polymer melt, BASELINE configs[2]); 0 = off
